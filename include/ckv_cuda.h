@@ -1,0 +1,275 @@
+/*
+ * ckv_cuda.h — C-ABI of the B200-native ClusterKV hot path (libckv_b200.so).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Device pointers are raw CUDA device addresses on the context's device.
+ * Every entry point returns CKV_OK (0) or a CKV_E* status and never throws;
+ * ckv_last_error() returns the message for the calling thread.
+ *
+ * Each entry point replaces one reference function from
+ * /root/reference/proj/include/clusterkv/*.hpp, cited per declaration.
+ * The reference-signature C++ drop-in (include/clusterkv_b200/clusterkv.hpp)
+ * and the Python mirror (paper_2412_03213_b200/api.py) both sit on this ABI.
+ *
+ * Layout conventions:
+ *   "unit"     = one (batch, layer, kv-head) k-means / KV problem
+ *   "q head"   = one query; q head h reads kv unit h / group (GQA)
+ *   keys, values: bf16 (uint16 bit patterns), row-major [unit][p_cap][d]
+ *   centroids:   f32 [unit][c_cap][d]  (raw means, never renormalised)
+ *   labels:      i32 [unit][p_cap]     (-1 = sink / not yet clustered)
+ *   index:       sizes u32 [unit][c_cap], starts u32 [unit][c_cap+1],
+ *                sorted_ids u32 [unit][p_cap]
+ *   d must be 128 (Llama-3 head dim; the only shape the kernels specialise).
+ */
+#ifndef CKV_CUDA_H
+#define CKV_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKV_OK 0
+#define CKV_EINVAL 1   /* maps to ckv::ValidationError (same predicates)   */
+#define CKV_ECUDA 2    /* CUDA runtime / launch failure                    */
+#define CKV_ENOMEM 3   /* device allocation failure                        */
+#define CKV_ENCCL 4    /* collective failure (sequence-sharded paths)      */
+
+#define CKV_HEAD_DIM 128
+
+typedef struct ckv_ctx ckv_ctx;
+typedef struct ckv_cache ckv_cache;
+typedef struct ckv_session ckv_session;
+
+/* ------------------------------------------------------------------ */
+/* context                                                             */
+/* ------------------------------------------------------------------ */
+/* stream: a cudaStream_t to launch on, or NULL for a private stream.
+ * A context is single-threaded; use one context per host thread
+ * (the reference calls the hot path concurrently per head,
+ * harness.hpp:362-378). */
+int ckv_ctx_create(int device, void* stream, ckv_ctx** out);
+int ckv_ctx_destroy(ckv_ctx* ctx);
+int ckv_ctx_sync(ckv_ctx* ctx);
+void* ckv_ctx_stream(ckv_ctx* ctx);
+const char* ckv_last_error(void);
+/* number of hot-path kernels this context has launched (bench evidence) */
+uint64_t ckv_ctx_launch_count(ckv_ctx* ctx);
+
+/* device memory helpers (the C++ shim uses these; no torch) */
+int ckv_malloc(ckv_ctx* ctx, void** ptr, size_t bytes);
+int ckv_free(ckv_ctx* ctx, void* ptr);
+int ckv_memcpy_h2d(ckv_ctx* ctx, void* dst, const void* src, size_t bytes);
+int ckv_memcpy_d2h(ckv_ctx* ctx, void* dst, const void* src, size_t bytes);
+int ckv_memset(ckv_ctx* ctx, void* dst, int value, size_t bytes);
+/* f32 -> bf16 (RNE) on device; also reports whether every value was
+ * bf16-representable (exact) in *all_exact_host (may be NULL). */
+int ckv_f32_to_bf16(ckv_ctx* ctx, const float* src, uint16_t* dst, size_t n,
+                    int* all_exact_host);
+
+/* ------------------------------------------------------------------ */
+/* k-means (clustering.hpp:157-263, 265-332)                           */
+/* ------------------------------------------------------------------ */
+/* Host-side init sampling, bit-identical to kmeans_cosine's partial
+ * Fisher-Yates over std::mt19937_64(seed) (clustering.hpp:186-193). */
+int ckv_kmeans_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows_out);
+uint64_t ckv_mix_seed(uint64_t seed, uint64_t a, uint64_t b); /* common.hpp:108-113 */
+
+typedef struct {
+  uint32_t n_units;      /* independent problems                          */
+  uint32_t n;            /* keys per unit                                 */
+  uint32_t C;            /* clusters per unit (1 <= C <= n)               */
+  uint32_t max_iters;    /* ClusterConfig::max_iters                      */
+  uint64_t key_stride;   /* elements between consecutive units' keys      */
+  uint32_t c_stride;     /* centroid rows between units (>= C)            */
+  uint32_t label_stride; /* labels between units (>= n)                   */
+  uint32_t flags;        /* CKV_KM_* below                                */
+} ckv_kmeans_desc;
+
+#define CKV_KM_OBJECTIVE 1u   /* fill objective_history (diagnostic)        */
+#define CKV_KM_EXACT_ONLY 2u  /* force the CUDA-core exact assignment path  */
+#define CKV_KM_NO_VALIDATE 4u /* skip the finite / non-degenerate check     */
+
+typedef struct {
+  uint32_t iterations_used;  /* ClusterModel::iterations_used            */
+  int32_t converged;         /* ClusterModel::converged                  */
+  uint32_t n_repair;         /* entries in repair_iterations             */
+  uint32_t n_objective;      /* entries in objective_history             */
+} ckv_kmeans_info;
+
+/* Batched kmeans_cosine (clustering.hpp:160-263), cosine metric.
+ * keys: device bf16; init_rows: device u32 [n_units*C] (from
+ * ckv_kmeans_init_rows or the caller's init_rows); outputs on device.
+ * info_host: host array [n_units]; objective_host: host f64
+ * [n_units*(max_iters+1)] or NULL; repair_host: host u32
+ * [n_units*(max_iters+1)] or NULL.  Replaces kmeans_cosine. */
+int ckv_kmeans(ckv_ctx* ctx, const ckv_kmeans_desc* desc, const uint16_t* keys,
+               const uint32_t* init_rows, float* centroids, int32_t* labels,
+               ckv_kmeans_info* info_host, double* objective_host, uint32_t* repair_host);
+
+/* Batched cluster_prefill (clustering.hpp:278-305): units share L; rows
+ * [0,sink) get label -1, rows [sink,L) are clustered into C0 =
+ * prefill_cluster_count(L) clusters with seed seeds_host[u].
+ * keys [unit][p_cap][128], labels [unit][p_cap], centroids [unit][c_cap][128]. */
+typedef struct {
+  uint32_t n_units, L, p_cap, c_cap;
+  uint32_t c0_divisor, sink_tokens, max_iters, c0_override;
+  uint32_t flags;  /* CKV_KM_* */
+} ckv_prefill_desc;
+uint32_t ckv_prefill_cluster_count(uint32_t L, uint32_t c0_divisor, uint32_t sink_tokens,
+                                   uint32_t c0_override);   /* clustering.hpp:267-274 */
+int ckv_cluster_prefill(ckv_ctx* ctx, const ckv_prefill_desc* desc, const uint16_t* keys,
+                        const uint64_t* seeds_host, float* centroids, int32_t* labels,
+                        uint32_t* n_clusters /* device [n_units] */,
+                        ckv_kmeans_info* info_host, double* objective_host,
+                        uint32_t* repair_host);
+
+/* Batched cluster_decode_batch (clustering.hpp:310-332): each unit's rows
+ * [pos0, pos0+rows) of keys are clustered in isolation into
+ * C+ = min(c_plus, rows) clusters, seed mix_seed(seeds_host[u], 0xdecade,
+ * pos0); centroids appended at n_clusters[u], labels written with the
+ * fresh ids, n_clusters[u] += C+.  Device-resident, no host round trip
+ * except the init sampling. */
+typedef struct {
+  uint32_t n_units, pos0, rows, p_cap, c_cap, c_plus, max_iters;
+} ckv_decode_cluster_desc;
+int ckv_cluster_decode_batch(ckv_ctx* ctx, const ckv_decode_cluster_desc* desc,
+                             const uint16_t* keys, const uint64_t* seeds_host,
+                             float* centroids, int32_t* labels, uint32_t* n_clusters,
+                             uint32_t* iterations_host /* [n_units] or NULL */);
+
+/* ------------------------------------------------------------------ */
+/* index (selection.hpp:16-48)                                         */
+/* ------------------------------------------------------------------ */
+/* Stable counting sort of labels[unit][0:n_pos] into the ClusterIndex
+ * layout.  n_clusters: device [n_units].  Replaces build_index. */
+int ckv_build_index(ckv_ctx* ctx, uint32_t n_units, uint32_t n_pos, uint32_t p_cap,
+                    uint32_t c_cap, const int32_t* labels, const uint32_t* n_clusters,
+                    uint32_t* sizes, uint32_t* starts, uint32_t* sorted_ids);
+
+/* ------------------------------------------------------------------ */
+/* selection + cache (selection.hpp:50-111, cache.hpp:25-93)           */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  uint32_t n_q;        /* q heads                                        */
+  uint32_t group;      /* q heads per kv unit                            */
+  uint32_t budget;     /* B                                              */
+  uint32_t sink_count; /* ids 0..sink_count-1 appended after clusters    */
+  uint32_t p_cap, c_cap;
+  uint32_t sel_cap;    /* token-id slots per q head                      */
+  uint32_t rec_begin;  /* recency positions [rec_begin, rec_end)         */
+  uint32_t rec_end;    /*   appended after the sinks (harness.hpp:246)   */
+  uint32_t flags;      /* CKV_SEL_* below                                */
+} ckv_select_desc;
+
+#define CKV_SEL_FULL_RANK 1u  /* write ranked_clusters for every cluster   */
+#define CKV_SEL_SCORES 2u     /* write the f64 scores (score_clusters)     */
+
+/* score_clusters + select_tokens for n_q queries in one launch.
+ * q: device f32 [n_q][128]; outputs device:
+ *   token_ids [n_q][sel_cap], n_tokens [n_q], n_taken [n_q],
+ *   trimmed [n_q], ranked [n_q][c_cap] (FULL_RANK: all C; otherwise
+ *   at least the taken prefix), scores [n_q][c_cap] (SCORES) or NULL.
+ * cache: NULL, or a cache with n_q slots — then each q head's taken
+ * clusters (sorted) go through ClusterCache::lookup_and_update, fused. */
+int ckv_select(ckv_ctx* ctx, const ckv_select_desc* desc, const float* q,
+               const float* centroids, const uint32_t* n_clusters, const uint32_t* sizes,
+               const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
+               uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked,
+               double* scores, ckv_cache* cache);
+
+/* ClusterCache with n_slots independent caches of retention R over at
+ * most c_cap cluster ids (bitmap ring).  cache.hpp:25-36. */
+int ckv_cache_create(ckv_ctx* ctx, uint32_t n_slots, uint32_t c_cap, uint32_t retention,
+                     uint32_t d, ckv_cache** out);
+int ckv_cache_destroy(ckv_cache* cache);
+/* counters_host: [n_slots][4] = requested, hit, tokens, bytes (cache.hpp:12-17) */
+int ckv_cache_counters(ckv_cache* cache, uint64_t* counters_host);
+/* Standalone lookup_and_update for one slot (cache.hpp:38-57):
+ * selected/sizes device; hit_ids/miss_ids device [n_sel];
+ * counts_host[2] = n_hit, n_miss. */
+int ckv_cache_lookup(ckv_ctx* ctx, ckv_cache* cache, uint32_t slot, const uint32_t* selected,
+                     uint32_t n_sel, const uint32_t* sizes, uint32_t* hit_ids,
+                     uint32_t* miss_ids, uint32_t* counts_host);
+/* invalidate_on_recluster (cache.hpp:67-76); retired: host ids */
+int ckv_cache_invalidate(ckv_ctx* ctx, ckv_cache* cache, uint32_t slot,
+                         const uint32_t* retired_host, uint32_t n_retired);
+
+/* ------------------------------------------------------------------ */
+/* sparse decode attention (attention.hpp:16-69)                       */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  uint32_t n_q, group, p_cap, sel_cap;
+  uint32_t max_tokens;  /* upper bound of n_tokens[] (sizes the split grid) */
+} ckv_attend_desc;
+
+/* approx_attention for n_q queries: softmax(q K[I]^T / sqrt(d)) V[I]
+ * over I = token_ids[h][0:n_tokens[h]], split-K flash-decode with an
+ * LSE merge.  K, V: device bf16 [unit][p_cap][128].  out: device f32
+ * [n_q][128].  weights: device f32 [n_q][sel_cap] in I order, or NULL.
+ * An empty selection is CKV_EINVAL (attention.hpp:66-67) and is checked
+ * on the host copy of n_tokens only when weights != NULL (parity mode). */
+int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* desc, const float* q, const uint16_t* K,
+               const uint16_t* V, const uint32_t* token_ids, const uint32_t* n_tokens,
+               float* out, float* weights);
+
+/* ------------------------------------------------------------------ */
+/* session: the batched serving path (simulate_head's ClusterKV branch, */
+/* harness.hpp:155-346, minus the metric oracles), device-resident.     */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  uint32_t n_units;        /* batch * layers * kv heads                 */
+  uint32_t group;          /* q heads per kv unit                       */
+  uint32_t prompt_len;     /* L                                         */
+  uint32_t max_decode;     /* T capacity                                */
+  uint32_t budget;         /* B                                         */
+  uint32_t retention;      /* cache R (0 = no cache)                    */
+  uint32_t c0_divisor, c_plus, decode_batch, sink_tokens, max_iters;
+  uint64_t cluster_seed;   /* ClusterConfig::seed; per-unit seed =
+                              mix_seed(cluster_seed, layer, head) with
+                              unit = layer * kv_heads + head             */
+  uint32_t kv_heads;       /* for the per-unit seed derivation          */
+  uint32_t flags;          /* CKV_KM_* for the prefill k-means          */
+} ckv_session_desc;
+
+int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* desc, ckv_session** out);
+int ckv_session_destroy(ckv_session* s);
+/* Device pointers of the session's KV store (bf16 [unit][p_cap][128]),
+ * so callers can fill the prompt KV in place. */
+int ckv_session_kv(ckv_session* s, uint16_t** K, uint16_t** V, uint32_t* p_cap);
+/* Upload prompt KV from HOST bf16 [unit][L][128]. */
+int ckv_session_load_prompt(ckv_session* s, const uint16_t* K_host, const uint16_t* V_host);
+/* cluster_prefill + build_index for every unit (harness.hpp:209-210).
+ * info_host [n_units] or NULL. */
+int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info_host);
+/* One decode step for every q head (harness.hpp:218-339):
+ *   select (budget, sinks, recency window [labeled_end, n_ctx)) + cache,
+ *   approx attention, append (k_t, v_t), decode-batch clustering every m.
+ * q: f32 [n_q][128]; k_new, v_new: bf16 [n_units][128]; out: f32 [n_q][128].
+ * on_device != 0: all four are device pointers; otherwise host pointers
+ * (copied in/out on the session stream inside the call). */
+int ckv_session_step(ckv_session* s, const float* q, const uint16_t* k_new,
+                     const uint16_t* v_new, float* out, int on_device);
+/* Select + attend only (no append/cluster), device pointers, for timing
+ * the steady-state hot path.  Equivalent to the first half of step. */
+int ckv_session_attend_only(ckv_session* s, const float* q_dev, float* out_dev);
+/* Introspection for tests / bench. */
+typedef struct {
+  uint32_t n_ctx, labeled_end, steps;
+  uint32_t max_clusters;
+  uint64_t launches;
+} ckv_session_stats;
+int ckv_session_stats_get(ckv_session* s, ckv_session_stats* st);
+/* device pointers of the model/index/selection state */
+int ckv_session_state(ckv_session* s, float** centroids, int32_t** labels,
+                      uint32_t** n_clusters, uint32_t** sizes, uint32_t** starts,
+                      uint32_t** sorted_ids, uint32_t** token_ids, uint32_t** n_tokens,
+                      uint32_t* c_cap, uint32_t* sel_cap);
+ckv_cache* ckv_session_cache(ckv_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

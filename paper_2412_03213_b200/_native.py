@@ -1,0 +1,143 @@
+"""ctypes binding of libckv_b200.so (include/ckv_cuda.h).
+
+There is no fallback: if the CUDA library is missing or fails to load, this
+module raises, so no caller can silently run anything but the sm_100a path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libckv_b200.so")
+
+CKV_OK, CKV_EINVAL, CKV_ECUDA, CKV_ENOMEM, CKV_ENCCL = 0, 1, 2, 3, 4
+CKV_KM_OBJECTIVE, CKV_KM_EXACT_ONLY, CKV_KM_NO_VALIDATE = 1, 2, 4
+CKV_SEL_FULL_RANK, CKV_SEL_SCORES = 1, 2
+
+vp, u32, u64, i32, f32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32, C.c_float
+
+
+class KMeansDesc(C.Structure):
+    _fields_ = [("n_units", u32), ("n", u32), ("C", u32), ("max_iters", u32),
+                ("key_stride", u64), ("c_stride", u32), ("label_stride", u32), ("flags", u32)]
+
+
+class KMeansInfo(C.Structure):
+    _fields_ = [("iterations_used", u32), ("converged", i32), ("n_repair", u32),
+                ("n_objective", u32)]
+
+
+class PrefillDesc(C.Structure):
+    _fields_ = [("n_units", u32), ("L", u32), ("p_cap", u32), ("c_cap", u32),
+                ("c0_divisor", u32), ("sink_tokens", u32), ("max_iters", u32),
+                ("c0_override", u32), ("flags", u32)]
+
+
+class DecodeClusterDesc(C.Structure):
+    _fields_ = [("n_units", u32), ("pos0", u32), ("rows", u32), ("p_cap", u32),
+                ("c_cap", u32), ("c_plus", u32), ("max_iters", u32)]
+
+
+class SelectDesc(C.Structure):
+    _fields_ = [("n_q", u32), ("group", u32), ("budget", u32), ("sink_count", u32),
+                ("p_cap", u32), ("c_cap", u32), ("sel_cap", u32), ("rec_begin", u32),
+                ("rec_end", u32), ("flags", u32)]
+
+
+class AttendDesc(C.Structure):
+    _fields_ = [("n_q", u32), ("group", u32), ("p_cap", u32), ("sel_cap", u32),
+                ("max_tokens", u32)]
+
+
+class SessionDesc(C.Structure):
+    _fields_ = [("n_units", u32), ("group", u32), ("prompt_len", u32), ("max_decode", u32),
+                ("budget", u32), ("retention", u32), ("c0_divisor", u32), ("c_plus", u32),
+                ("decode_batch", u32), ("sink_tokens", u32), ("max_iters", u32),
+                ("cluster_seed", u64), ("kv_heads", u32), ("flags", u32)]
+
+
+class SessionStats(C.Structure):
+    _fields_ = [("n_ctx", u32), ("labeled_end", u32), ("steps", u32), ("max_clusters", u32),
+                ("launches", u64)]
+
+
+# every symbol declared in include/ckv_cuda.h, with its ctypes signature
+SIGNATURES = {
+    "ckv_ctx_create": (C.c_int, [C.c_int, vp, C.POINTER(vp)]),
+    "ckv_ctx_destroy": (C.c_int, [vp]),
+    "ckv_ctx_sync": (C.c_int, [vp]),
+    "ckv_ctx_stream": (vp, [vp]),
+    "ckv_last_error": (C.c_char_p, []),
+    "ckv_ctx_launch_count": (u64, [vp]),
+    "ckv_malloc": (C.c_int, [vp, C.POINTER(vp), C.c_size_t]),
+    "ckv_free": (C.c_int, [vp, vp]),
+    "ckv_memcpy_h2d": (C.c_int, [vp, vp, vp, C.c_size_t]),
+    "ckv_memcpy_d2h": (C.c_int, [vp, vp, vp, C.c_size_t]),
+    "ckv_memset": (C.c_int, [vp, vp, C.c_int, C.c_size_t]),
+    "ckv_f32_to_bf16": (C.c_int, [vp, vp, vp, C.c_size_t, C.POINTER(C.c_int)]),
+    "ckv_kmeans_init_rows": (C.c_int, [u32, u32, u64, vp]),
+    "ckv_mix_seed": (u64, [u64, u64, u64]),
+    "ckv_kmeans": (C.c_int, [vp, C.POINTER(KMeansDesc), vp, vp, vp, vp, vp, vp, vp]),
+    "ckv_prefill_cluster_count": (u32, [u32, u32, u32, u32]),
+    "ckv_cluster_prefill": (C.c_int, [vp, C.POINTER(PrefillDesc), vp, vp, vp, vp, vp, vp, vp, vp]),
+    "ckv_cluster_decode_batch": (C.c_int, [vp, C.POINTER(DecodeClusterDesc), vp, vp, vp, vp, vp,
+                                           vp]),
+    "ckv_build_index": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp]),
+    "ckv_select": (C.c_int, [vp, C.POINTER(SelectDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                             vp, vp, vp]),
+    "ckv_cache_create": (C.c_int, [vp, u32, u32, u32, u32, C.POINTER(vp)]),
+    "ckv_cache_destroy": (C.c_int, [vp]),
+    "ckv_cache_counters": (C.c_int, [vp, vp]),
+    "ckv_cache_lookup": (C.c_int, [vp, vp, u32, vp, u32, vp, vp, vp, vp]),
+    "ckv_cache_invalidate": (C.c_int, [vp, vp, u32, vp, u32]),
+    "ckv_attend": (C.c_int, [vp, C.POINTER(AttendDesc), vp, vp, vp, vp, vp, vp, vp]),
+    "ckv_session_create": (C.c_int, [vp, C.POINTER(SessionDesc), C.POINTER(vp)]),
+    "ckv_session_destroy": (C.c_int, [vp]),
+    "ckv_session_kv": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(u32)]),
+    "ckv_session_load_prompt": (C.c_int, [vp, vp, vp]),
+    "ckv_session_prefill": (C.c_int, [vp, vp]),
+    "ckv_session_step": (C.c_int, [vp, vp, vp, vp, vp, C.c_int]),
+    "ckv_session_attend_only": (C.c_int, [vp, vp, vp]),
+    "ckv_session_stats_get": (C.c_int, [vp, C.POINTER(SessionStats)]),
+    "ckv_session_state": (C.c_int, [vp] + [C.POINTER(vp)] * 8 + [C.POINTER(u32)] * 2),
+    "ckv_session_cache": (vp, [vp]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libckv_b200.so (raises if it is absent: no CPU fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is not built; run `python -m paper_2412_03213_b200.build` "
+                "(the ClusterKV hot path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class CkvError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[ckv {code}] {msg}")
+        self.code = code
+
+
+class ValidationError(CkvError, ValueError):
+    """Raised under the predicates that make the reference throw
+    ckv::ValidationError (common.hpp:27-30)."""
+
+
+def check(rc: int) -> None:
+    if rc != CKV_OK:
+        msg = lib().ckv_last_error().decode()
+        if rc == CKV_EINVAL:
+            raise ValidationError(rc, msg)
+        raise CkvError(rc, msg)

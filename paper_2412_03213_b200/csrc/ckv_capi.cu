@@ -1,0 +1,712 @@
+// ckv_capi.cu — the extern "C" boundary (include/ckv_cuda.h) and the
+// device-resident decode session.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "ckv_internal.cuh"
+
+namespace ckvb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int cuda_status(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? CKV_ENOMEM : CKV_ECUDA;
+}
+int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+// common.hpp:100-113
+static uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b) {
+  uint64_t h = splitmix64(seed);
+  h = splitmix64(h ^ (a + 0x9e3779b97f4a7c15ull));
+  return splitmix64(h ^ (b + 0xbf58476d1ce4e5b9ull));
+}
+// clustering.hpp:186-193 (std::mt19937_64 is bit-specified by the standard;
+// uniform_below is rng() % n, common.hpp:124-126)
+void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows) {
+  std::mt19937_64 rng(seed);
+  std::vector<uint32_t> pool(n);
+  for (uint32_t i = 0; i < n; ++i) pool[i] = i;
+  for (uint32_t c = 0; c < C; ++c) {
+    uint32_t j = c + uint32_t(rng() % uint64_t(n - c));
+    std::swap(pool[c], pool[j]);
+  }
+  std::copy(pool.begin(), pool.begin() + C, rows);
+}
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+__global__ void k_f32_to_bf16(const float* __restrict__ src, uint16_t* __restrict__ dst,
+                              size_t n, int* __restrict__ inexact) {
+  int bad = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    float x = src[i];
+    uint16_t b = f32_to_bf16_rn(x);
+    dst[i] = b;
+    if (__float_as_uint(x) != (uint32_t(b) << 16) && !isnan(x)) bad = 1;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(inexact, 1);
+}
+
+__global__ void k_fill_i32(int32_t* __restrict__ p, uint32_t n, uint32_t stride, int32_t v) {
+  const uint32_t u = blockIdx.y;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[size_t(u) * stride + i] = v;
+}
+
+__global__ void k_set_u32(uint32_t* __restrict__ p, uint32_t n, uint32_t v) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// append decode-batch clusters: centroids / labels at each unit's n_clusters
+__global__ void k_append_clusters(const float* __restrict__ tmp_c, const int32_t* __restrict__ tmp_l,
+                                  uint32_t cplus, uint32_t rows, uint32_t pos0, uint32_t c_cap,
+                                  uint32_t p_cap, float* __restrict__ cents,
+                                  int32_t* __restrict__ labels, uint32_t* __restrict__ n_clusters) {
+  const uint32_t u = blockIdx.x;
+  const uint32_t base = n_clusters[u];
+  for (uint32_t i = threadIdx.x; i < cplus * D; i += blockDim.x)
+    cents[(size_t(u) * c_cap + base) * D + i] = tmp_c[size_t(u) * cplus * D + i];
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x)
+    labels[size_t(u) * p_cap + pos0 + i] = tmp_l[size_t(u) * rows + i] + int32_t(base);
+  __syncthreads();
+  if (threadIdx.x == 0) n_clusters[u] = base + cplus;
+}
+
+// append one token's K/V row per unit at position pos
+__global__ void k_append_kv(const uint16_t* __restrict__ kn, const uint16_t* __restrict__ vn,
+                            uint16_t* __restrict__ K, uint16_t* __restrict__ V, uint32_t pos,
+                            uint32_t p_cap) {
+  const uint32_t u = blockIdx.x, j = threadIdx.x;  // 16 threads x 16 B
+  const uint4* ks = reinterpret_cast<const uint4*>(kn + size_t(u) * D);
+  const uint4* vs = reinterpret_cast<const uint4*>(vn + size_t(u) * D);
+  reinterpret_cast<uint4*>(K + (size_t(u) * p_cap + pos) * D)[j] = ks[j];
+  reinterpret_cast<uint4*>(V + (size_t(u) * p_cap + pos) * D)[j] = vs[j];
+}
+
+}  // namespace ckvb
+
+using namespace ckvb;
+
+// ===========================================================================
+// context + memory
+// ===========================================================================
+extern "C" {
+
+const char* ckv_last_error(void) { return g_err.c_str(); }
+
+int ckv_ctx_create(int device, void* stream, ckv_ctx** out) {
+  if (!out) { set_error("ckv_ctx_create: out is NULL"); return CKV_EINVAL; }
+  CKV_CUDA_TRY(cudaSetDevice(device));
+  ckv_ctx* c = new ckv_ctx();
+  c->device = device;
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete c; return cuda_status(e, "cudaStreamCreate"); }
+    c->own_stream = true;
+  }
+  *out = c;
+  return CKV_OK;
+}
+
+int ckv_ctx_destroy(ckv_ctx* ctx) {
+  if (!ctx) return CKV_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+  delete ctx;
+  return CKV_OK;
+}
+
+int ckv_ctx_sync(ckv_ctx* ctx) {
+  CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CKV_OK;
+}
+void* ckv_ctx_stream(ckv_ctx* ctx) { return ctx->stream; }
+uint64_t ckv_ctx_launch_count(ckv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ckv_malloc(ckv_ctx* ctx, void** ptr, size_t bytes) {
+  (void)ctx;
+  CKV_CUDA_TRY(cudaMalloc(ptr, bytes ? bytes : 16));
+  return CKV_OK;
+}
+int ckv_free(ckv_ctx* ctx, void* ptr) {
+  (void)ctx;
+  if (ptr) CKV_CUDA_TRY(cudaFree(ptr));
+  return CKV_OK;
+}
+int ckv_memcpy_h2d(ckv_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  CKV_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CKV_OK;
+}
+int ckv_memcpy_d2h(ckv_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  CKV_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CKV_OK;
+}
+int ckv_memset(ckv_ctx* ctx, void* dst, int value, size_t bytes) {
+  CKV_CUDA_TRY(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+  return CKV_OK;
+}
+
+int ckv_f32_to_bf16(ckv_ctx* ctx, const float* src, uint16_t* dst, size_t n, int* all_exact) {
+  int* flag = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), ctx->stream));
+  CKV_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  if (n) {
+    int blocks = int(std::min<size_t>((n + 255) / 256, size_t(num_sms()) * 8));
+    k_f32_to_bf16<<<blocks, 256, 0, ctx->stream>>>(src, dst, n, flag);
+    CKV_LAUNCH_CHECK("k_f32_to_bf16");
+    ctx->launches++;
+  }
+  int h = 0;
+  CKV_CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CKV_CUDA_TRY(cudaFreeAsync(flag, ctx->stream));
+  CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (all_exact) *all_exact = h ? 0 : 1;
+  return CKV_OK;
+}
+
+// ===========================================================================
+// k-means
+// ===========================================================================
+uint64_t ckv_mix_seed(uint64_t seed, uint64_t a, uint64_t b) { return host_mix_seed(seed, a, b); }
+
+int ckv_kmeans_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows_out) {
+  if (C < 1 || C > n) { set_error("kmeans: need 1 <= C <= N"); return CKV_EINVAL; }
+  host_init_rows(n, C, seed, rows_out);
+  return CKV_OK;
+}
+
+int ckv_kmeans(ckv_ctx* ctx, const ckv_kmeans_desc* d, const uint16_t* keys,
+               const uint32_t* init_rows, float* centroids, int32_t* labels,
+               ckv_kmeans_info* info_host, double* objective_host, uint32_t* repair_host) {
+  if (!ctx || !d) { set_error("ckv_kmeans: NULL argument"); return CKV_EINVAL; }
+  KMeansArgs a;
+  a.n_units = d->n_units;
+  a.n = d->n;
+  a.C = d->C;
+  a.max_iters = d->max_iters;
+  a.key_stride = d->key_stride;
+  a.c_stride = d->c_stride;
+  a.label_stride = d->label_stride;
+  a.flags = d->flags;
+  a.keys = keys;
+  a.init_rows = init_rows;
+  a.centroids = centroids;
+  a.labels = labels;
+  if (a.c_stride < a.C || a.label_stride < a.n) {
+    set_error("ckv_kmeans: strides smaller than C / n");
+    return CKV_EINVAL;
+  }
+  return kmeans_run(ctx, a, info_host, objective_host, repair_host);
+}
+
+uint32_t ckv_prefill_cluster_count(uint32_t L, uint32_t divisor, uint32_t sink, uint32_t ovr) {
+  if (L <= sink) return 0;
+  const uint32_t n = L - sink;
+  uint32_t c0 = ovr ? ovr : uint32_t(std::llround(double(n) / double(divisor ? divisor : 1)));
+  return std::clamp<uint32_t>(c0, 1, n);
+}
+
+int ckv_cluster_prefill(ckv_ctx* ctx, const ckv_prefill_desc* d, const uint16_t* keys,
+                        const uint64_t* seeds, float* centroids, int32_t* labels,
+                        uint32_t* n_clusters, ckv_kmeans_info* info_host, double* objective_host,
+                        uint32_t* repair_host) {
+  if (d->c0_divisor < 1) { set_error("ClusterConfig: c0_divisor must be >= 1"); return CKV_EINVAL; }
+  if (d->max_iters < 1) { set_error("ClusterConfig: max_iters must be >= 1"); return CKV_EINVAL; }
+  const uint32_t U = d->n_units, L = d->L, sink = d->sink_tokens;
+  const uint32_t C0 = ckv_prefill_cluster_count(L, d->c0_divisor, sink, d->c0_override);
+  cudaStream_t st = ctx->stream;
+  // labels: -1 everywhere first (sinks, and anything beyond L)
+  k_fill_i32<<<dim3(std::max<uint32_t>(1, std::min<uint32_t>((d->p_cap + 255) / 256, 64)), U),
+               256, 0, st>>>(labels, d->p_cap, d->p_cap, -1);
+  CKV_LAUNCH_CHECK("k_fill_i32");
+  k_set_u32<<<(U + 127) / 128, 128, 0, st>>>(n_clusters, U, C0);
+  CKV_LAUNCH_CHECK("k_set_u32");
+  ctx->launches += 2;
+  if (C0 == 0) {
+    for (uint32_t u = 0; info_host && u < U; ++u) info_host[u] = {0, 1, 0, 0};
+    return ckv_ctx_sync(ctx);
+  }
+  if (C0 > d->c_cap) { set_error("cluster_prefill: C0 exceeds c_cap"); return CKV_EINVAL; }
+  const uint32_t n = L - sink;
+  std::vector<uint32_t> rows(size_t(U) * C0);
+  for (uint32_t u = 0; u < U; ++u) host_init_rows(n, C0, seeds[u], rows.data() + size_t(u) * C0);
+  uint32_t* d_rows = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&d_rows, rows.size() * 4, st));
+  CKV_CUDA_TRY(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st));
+  KMeansArgs a;
+  a.n_units = U;
+  a.n = n;
+  a.C = C0;
+  a.max_iters = d->max_iters;
+  a.key_stride = uint64_t(d->p_cap) * D;
+  a.c_stride = d->c_cap;
+  a.label_stride = d->p_cap;
+  a.flags = d->flags;
+  a.keys = keys + size_t(sink) * D;
+  a.init_rows = d_rows;
+  a.centroids = centroids;
+  a.labels = labels + sink;
+  int rc = kmeans_run(ctx, a, info_host, objective_host, repair_host);
+  cudaFreeAsync(d_rows, st);
+  if (rc) return rc;
+  return ckv_ctx_sync(ctx);
+}
+
+int ckv_cluster_decode_batch(ckv_ctx* ctx, const ckv_decode_cluster_desc* d,
+                             const uint16_t* keys, const uint64_t* seeds, float* centroids,
+                             int32_t* labels, uint32_t* n_clusters, uint32_t* iterations_host) {
+  const uint32_t U = d->n_units, rows = d->rows;
+  if (rows == 0 || U == 0) return CKV_OK;  // clustering.hpp:311
+  if (d->c_plus < 1) { set_error("ClusterConfig: c_plus must be >= 1"); return CKV_EINVAL; }
+  if (d->max_iters < 1) { set_error("ClusterConfig: max_iters must be >= 1"); return CKV_EINVAL; }
+  cudaStream_t st = ctx->stream;
+  const uint32_t C = std::min(d->c_plus, rows);
+  std::vector<uint32_t> init(size_t(U) * C);
+  for (uint32_t u = 0; u < U; ++u)
+    host_init_rows(rows, C, host_mix_seed(seeds[u], 0xdecadeull, d->pos0),
+                   init.data() + size_t(u) * C);
+  uint32_t* d_init = nullptr;
+  float* tmp_c = nullptr;
+  int32_t* tmp_l = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&d_init, init.size() * 4, st));
+  CKV_CUDA_TRY(cudaMallocAsync(&tmp_c, size_t(U) * C * D * 4, st));
+  CKV_CUDA_TRY(cudaMallocAsync(&tmp_l, size_t(U) * rows * 4, st));
+  CKV_CUDA_TRY(cudaMemcpyAsync(d_init, init.data(), init.size() * 4, cudaMemcpyHostToDevice, st));
+  KMeansArgs a;
+  a.n_units = U;
+  a.n = rows;
+  a.C = C;
+  a.max_iters = d->max_iters;
+  a.key_stride = uint64_t(d->p_cap) * D;
+  a.c_stride = C;
+  a.label_stride = rows;
+  a.flags = CKV_KM_EXACT_ONLY;
+  a.keys = keys + size_t(d->pos0) * D;
+  a.init_rows = d_init;
+  a.centroids = tmp_c;
+  a.labels = tmp_l;
+  std::vector<ckv_kmeans_info> info(U);
+  int rc = kmeans_run(ctx, a, info.data(), nullptr, nullptr);
+  if (rc == CKV_OK) {
+    k_append_clusters<<<U, 256, 0, st>>>(tmp_c, tmp_l, C, rows, d->pos0, d->c_cap, d->p_cap,
+                                         centroids, labels, n_clusters);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_status(e, "k_append_clusters");
+    ctx->launches++;
+  }
+  cudaFreeAsync(d_init, st);
+  cudaFreeAsync(tmp_c, st);
+  cudaFreeAsync(tmp_l, st);
+  if (rc) return rc;
+  if (iterations_host)
+    for (uint32_t u = 0; u < U; ++u) iterations_host[u] = info[u].iterations_used;
+  return ckv_ctx_sync(ctx);
+}
+
+// ===========================================================================
+// index, select, cache, attend
+// ===========================================================================
+int ckv_build_index(ckv_ctx* ctx, uint32_t n_units, uint32_t n_pos, uint32_t p_cap,
+                    uint32_t c_cap, const int32_t* labels, const uint32_t* n_clusters,
+                    uint32_t* sizes, uint32_t* starts, uint32_t* sorted_ids) {
+  if (n_pos > p_cap) { set_error("build_index: n_pos > p_cap"); return CKV_EINVAL; }
+  CKV_TRY(launch_index(ctx->stream, n_units, labels, n_pos, p_cap, c_cap, n_clusters, 0, sizes,
+                       starts, sorted_ids, nullptr, nullptr, nullptr, nullptr));
+  ctx->launches++;
+  return CKV_OK;
+}
+
+static CacheDev null_cache() {
+  CacheDev c;
+  std::memset(&c, 0, sizeof c);
+  return c;
+}
+
+int ckv_select(ckv_ctx* ctx, const ckv_select_desc* d, const float* q, const float* centroids,
+               const uint32_t* n_clusters, const uint32_t* sizes, const uint32_t* starts,
+               const uint32_t* sorted_ids, uint32_t* token_ids, uint32_t* n_tokens,
+               uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
+               ckv_cache* cache) {
+  if (!ranked) { set_error("ckv_select: ranked buffer required"); return CKV_EINVAL; }
+  if (cache && cache->dev.n_slots < d->n_q) {
+    set_error("ckv_select: cache has fewer slots than q heads");
+    return CKV_EINVAL;
+  }
+  CKV_TRY(launch_select(ctx->stream, *d, q, centroids, n_clusters, sizes, starts, sorted_ids,
+                        token_ids, n_tokens, n_taken, trimmed, ranked, scores,
+                        cache ? cache->dev : null_cache()));
+  ctx->launches++;
+  return CKV_OK;
+}
+
+int ckv_cache_create(ckv_ctx* ctx, uint32_t n_slots, uint32_t c_cap, uint32_t retention,
+                     uint32_t d, ckv_cache** out) {
+  if (retention < 1) { set_error("ClusterCache: retention must be >= 1"); return CKV_EINVAL; }
+  ckv_cache* c = new ckv_cache();
+  c->ctx = ctx;
+  c->dev.n_slots = n_slots;
+  c->dev.c_cap = c_cap;
+  c->dev.retention = retention;
+  c->dev.d = d;
+  c->dev.words = (c_cap + 31) / 32;
+  size_t bits = size_t(n_slots) * retention * c->dev.words * 4;
+  cudaError_t e = cudaMalloc(&c->dev.bits, bits ? bits : 4);
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev.ring, size_t(n_slots) * 8 + 8);
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev.counters, size_t(n_slots) * 32 + 32);
+  if (e != cudaSuccess) { delete c; return cuda_status(e, "ckv_cache_create"); }
+  cudaMemsetAsync(c->dev.bits, 0, bits ? bits : 4, ctx->stream);
+  cudaMemsetAsync(c->dev.ring, 0, size_t(n_slots) * 8 + 8, ctx->stream);
+  cudaMemsetAsync(c->dev.counters, 0, size_t(n_slots) * 32 + 32, ctx->stream);
+  *out = c;
+  return CKV_OK;
+}
+
+int ckv_cache_destroy(ckv_cache* c) {
+  if (!c) return CKV_OK;
+  cudaStreamSynchronize(c->ctx->stream);
+  cudaFree(c->dev.bits);
+  cudaFree(c->dev.ring);
+  cudaFree(c->dev.counters);
+  delete c;
+  return CKV_OK;
+}
+
+int ckv_cache_counters(ckv_cache* c, uint64_t* out) {
+  CKV_CUDA_TRY(cudaMemcpyAsync(out, c->dev.counters, size_t(c->dev.n_slots) * 32,
+                               cudaMemcpyDeviceToHost, c->ctx->stream));
+  CKV_CUDA_TRY(cudaStreamSynchronize(c->ctx->stream));
+  return CKV_OK;
+}
+
+int ckv_cache_lookup(ckv_ctx* ctx, ckv_cache* c, uint32_t slot, const uint32_t* selected,
+                     uint32_t n_sel, const uint32_t* sizes, uint32_t* hit, uint32_t* miss,
+                     uint32_t* counts_host) {
+  if (slot >= c->dev.n_slots) { set_error("cache: slot out of range"); return CKV_EINVAL; }
+  uint32_t* dcounts = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&dcounts, 8, ctx->stream));
+  CKV_TRY(launch_cache_lookup(ctx->stream, c->dev, slot, selected, n_sel, sizes, hit, miss,
+                              dcounts));
+  ctx->launches++;
+  CKV_CUDA_TRY(cudaMemcpyAsync(counts_host, dcounts, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CKV_CUDA_TRY(cudaFreeAsync(dcounts, ctx->stream));
+  CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CKV_OK;
+}
+
+int ckv_cache_invalidate(ckv_ctx* ctx, ckv_cache* c, uint32_t slot, const uint32_t* retired,
+                         uint32_t n) {
+  if (n == 0) return CKV_OK;
+  uint32_t* d = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&d, size_t(n) * 4, ctx->stream));
+  CKV_CUDA_TRY(cudaMemcpyAsync(d, retired, size_t(n) * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CKV_TRY(launch_cache_invalidate(ctx->stream, c->dev, slot, d, n));
+  ctx->launches++;
+  CKV_CUDA_TRY(cudaFreeAsync(d, ctx->stream));
+  CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CKV_OK;
+}
+
+int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q, const uint16_t* K,
+               const uint16_t* V, const uint32_t* token_ids, const uint32_t* n_tokens, float* out,
+               float* weights) {
+  cudaStream_t st = ctx->stream;
+  if (weights) {  // parity mode: approx_attention's empty-selection check
+    std::vector<uint32_t> nt(d->n_q);
+    CKV_CUDA_TRY(cudaMemcpyAsync(nt.data(), n_tokens, 4 * size_t(d->n_q),
+                                 cudaMemcpyDeviceToHost, st));
+    CKV_CUDA_TRY(cudaStreamSynchronize(st));
+    for (uint32_t v : nt)
+      if (v == 0) { set_error("approx_attention: empty selection"); return CKV_EINVAL; }
+  }
+  const size_t pf = attend_part_floats(d->n_q, d->max_tokens);
+  float* part = nullptr;
+  float* lw = nullptr;
+  uint32_t* tickets = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&part, pf * 4 + 16, st));
+  CKV_CUDA_TRY(cudaMallocAsync(&tickets, size_t(d->n_q) * 4 + 4, st));
+  CKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(d->n_q) * 4 + 4, st));
+  if (weights) CKV_CUDA_TRY(cudaMallocAsync(&lw, size_t(d->n_q) * d->sel_cap * 4 + 16, st));
+  int rc = launch_attend(st, *d, q, K, V, token_ids, n_tokens, out, weights, lw, part, tickets);
+  ctx->launches++;
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(tickets, st);
+  if (lw) cudaFreeAsync(lw, st);
+  return rc;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// session
+// ===========================================================================
+struct ckv_session {
+  ckv_ctx* ctx = nullptr;
+  ckv_session_desc d{};
+  uint32_t U = 0, n_q = 0, p_cap = 0, c_cap = 0, sel_cap = 0;
+  uint16_t *K = nullptr, *V = nullptr;
+  float* cents = nullptr;
+  int32_t* labels = nullptr;
+  uint32_t *n_clusters = nullptr, *sizes = nullptr, *starts = nullptr, *sorted = nullptr;
+  uint32_t *token_ids = nullptr, *n_tokens = nullptr, *n_taken = nullptr, *trimmed = nullptr,
+           *ranked = nullptr;
+  float* part = nullptr;
+  uint32_t* tickets = nullptr;
+  float *q_dev = nullptr, *out_dev = nullptr;
+  uint16_t *kn_dev = nullptr, *vn_dev = nullptr;
+  ckv_cache* cache = nullptr;
+  std::vector<uint64_t> seeds;
+  uint32_t n_ctx = 0, labeled_end = 0, steps = 0, pending = 0, C_cur = 0;
+  bool prefilled = false;
+};
+
+namespace {
+template <typename T>
+int salloc(T** p, size_t count) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count * sizeof(T), 16));
+  if (e != cudaSuccess) return cuda_status(e, "ckv_session alloc");
+  return CKV_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** out) {
+  if (d->group < 1 || d->budget < 1 || d->decode_batch < 1 || d->c_plus < 1 ||
+      d->max_iters < 1 || d->c0_divisor < 1) {
+    set_error("ckv_session_create: invalid configuration");
+    return CKV_EINVAL;
+  }
+  ckv_session* s = new ckv_session();
+  s->ctx = ctx;
+  s->d = *d;
+  s->U = d->n_units;
+  s->n_q = d->n_units * d->group;
+  s->p_cap = d->prompt_len + d->max_decode;
+  const uint32_t C0 = ckv_prefill_cluster_count(d->prompt_len, d->c0_divisor, d->sink_tokens, 0);
+  s->c_cap = C0 + d->c_plus * (d->max_decode / d->decode_batch + 1);
+  s->sel_cap = d->budget + d->sink_tokens + d->decode_batch + 1;
+  const size_t kv = size_t(s->U) * s->p_cap * D;
+  int rc = CKV_OK;
+  rc |= salloc(&s->K, kv);
+  rc |= salloc(&s->V, kv);
+  rc |= salloc(&s->cents, size_t(s->U) * s->c_cap * D);
+  rc |= salloc(&s->labels, size_t(s->U) * s->p_cap);
+  rc |= salloc(&s->n_clusters, s->U);
+  rc |= salloc(&s->sizes, size_t(s->U) * s->c_cap);
+  rc |= salloc(&s->starts, size_t(s->U) * (s->c_cap + 1));
+  rc |= salloc(&s->sorted, size_t(s->U) * s->p_cap);
+  rc |= salloc(&s->token_ids, size_t(s->n_q) * s->sel_cap);
+  rc |= salloc(&s->n_tokens, s->n_q);
+  rc |= salloc(&s->n_taken, s->n_q);
+  rc |= salloc(&s->trimmed, s->n_q);
+  rc |= salloc(&s->ranked, size_t(s->n_q) * s->c_cap);
+  rc |= salloc(&s->part, attend_part_floats(s->n_q, s->sel_cap));
+  rc |= salloc(&s->tickets, s->n_q);
+  rc |= salloc(&s->q_dev, size_t(s->n_q) * D);
+  rc |= salloc(&s->out_dev, size_t(s->n_q) * D);
+  rc |= salloc(&s->kn_dev, size_t(s->U) * D);
+  rc |= salloc(&s->vn_dev, size_t(s->U) * D);
+  if (rc) { ckv_session_destroy(s); return CKV_ENOMEM; }
+  cudaMemsetAsync(s->tickets, 0, size_t(s->n_q) * 4, ctx->stream);
+  cudaMemsetAsync(s->n_clusters, 0, size_t(s->U) * 4, ctx->stream);
+  if (d->retention > 0) {
+    rc = ckv_cache_create(ctx, s->n_q, s->c_cap, d->retention, D, &s->cache);
+    if (rc) { ckv_session_destroy(s); return rc; }
+  }
+  s->seeds.resize(s->U);
+  const uint32_t kvh = std::max<uint32_t>(1, d->kv_heads);
+  // unit u = layer * kv_heads + head (batch folded into the layer index)
+  for (uint32_t u = 0; u < s->U; ++u)
+    s->seeds[u] = host_mix_seed(d->cluster_seed, u / kvh, u % kvh);  // harness.hpp:195
+  s->n_ctx = d->prompt_len;
+  s->labeled_end = d->prompt_len;
+  *out = s;
+  return CKV_OK;
+}
+
+int ckv_session_destroy(ckv_session* s) {
+  if (!s) return CKV_OK;
+  cudaStreamSynchronize(s->ctx->stream);
+  cudaFree(s->K); cudaFree(s->V); cudaFree(s->cents); cudaFree(s->labels);
+  cudaFree(s->n_clusters); cudaFree(s->sizes); cudaFree(s->starts); cudaFree(s->sorted);
+  cudaFree(s->token_ids); cudaFree(s->n_tokens); cudaFree(s->n_taken); cudaFree(s->trimmed);
+  cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
+  cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
+  ckv_cache_destroy(s->cache);
+  delete s;
+  return CKV_OK;
+}
+
+int ckv_session_kv(ckv_session* s, uint16_t** K, uint16_t** V, uint32_t* p_cap) {
+  *K = s->K;
+  *V = s->V;
+  *p_cap = s->p_cap;
+  return CKV_OK;
+}
+
+int ckv_session_load_prompt(ckv_session* s, const uint16_t* Kh, const uint16_t* Vh) {
+  const size_t row = size_t(s->d.prompt_len) * D * 2;
+  CKV_CUDA_TRY(cudaMemcpy2DAsync(s->K, size_t(s->p_cap) * D * 2, Kh, row, row, s->U,
+                                 cudaMemcpyHostToDevice, s->ctx->stream));
+  CKV_CUDA_TRY(cudaMemcpy2DAsync(s->V, size_t(s->p_cap) * D * 2, Vh, row, row, s->U,
+                                 cudaMemcpyHostToDevice, s->ctx->stream));
+  CKV_CUDA_TRY(cudaStreamSynchronize(s->ctx->stream));
+  return CKV_OK;
+}
+
+int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
+  ckv_prefill_desc pd{};
+  pd.n_units = s->U;
+  pd.L = s->d.prompt_len;
+  pd.p_cap = s->p_cap;
+  pd.c_cap = s->c_cap;
+  pd.c0_divisor = s->d.c0_divisor;
+  pd.sink_tokens = s->d.sink_tokens;
+  pd.max_iters = s->d.max_iters;
+  pd.c0_override = 0;
+  pd.flags = s->d.flags;
+  CKV_TRY(ckv_cluster_prefill(s->ctx, &pd, s->K, s->seeds.data(), s->cents, s->labels,
+                              s->n_clusters, info, nullptr, nullptr));
+  s->C_cur = ckv_prefill_cluster_count(pd.L, pd.c0_divisor, pd.sink_tokens, 0);
+  CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
+                          s->n_clusters, s->sizes, s->starts, s->sorted));
+  s->prefilled = true;
+  return ckv_ctx_sync(s->ctx);
+}
+
+static int session_select_attend(ckv_session* s, const float* q_dev, float* out_dev) {
+  ckv_select_desc sd{};
+  sd.n_q = s->n_q;
+  sd.group = s->d.group;
+  sd.budget = s->d.budget;
+  sd.sink_count = std::min(s->d.sink_tokens, s->d.prompt_len);
+  sd.p_cap = s->p_cap;
+  sd.c_cap = s->c_cap;
+  sd.sel_cap = s->sel_cap;
+  sd.rec_begin = s->labeled_end;
+  sd.rec_end = s->n_ctx;
+  sd.flags = 0;
+  CKV_TRY(launch_select(s->ctx->stream, sd, q_dev, s->cents, s->n_clusters, s->sizes, s->starts,
+                        s->sorted, s->token_ids, s->n_tokens, s->n_taken, s->trimmed, s->ranked,
+                        nullptr, s->cache ? s->cache->dev : null_cache()));
+  ckv_attend_desc ad{};
+  ad.n_q = s->n_q;
+  ad.group = s->d.group;
+  ad.p_cap = s->p_cap;
+  ad.sel_cap = s->sel_cap;
+  ad.max_tokens = std::min(s->d.budget, s->labeled_end) + sd.sink_count + (s->n_ctx - s->labeled_end);
+  CKV_TRY(launch_attend(s->ctx->stream, ad, q_dev, s->K, s->V, s->token_ids, s->n_tokens,
+                        out_dev, nullptr, nullptr, s->part, s->tickets));
+  s->ctx->launches += 2;
+  return CKV_OK;
+}
+
+int ckv_session_attend_only(ckv_session* s, const float* q_dev, float* out_dev) {
+  if (!s->prefilled) { set_error("session: prefill first"); return CKV_EINVAL; }
+  return session_select_attend(s, q_dev, out_dev);
+}
+
+int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const uint16_t* vn,
+                     float* out, int on_device) {
+  if (!s->prefilled) { set_error("session: prefill first"); return CKV_EINVAL; }
+  if (s->n_ctx >= s->p_cap) { set_error("session: decode capacity exhausted"); return CKV_EINVAL; }
+  cudaStream_t st = s->ctx->stream;
+  const float* qd = q;
+  const uint16_t *kd = kn, *vd = vn;
+  float* od = out;
+  if (!on_device) {
+    CKV_CUDA_TRY(cudaMemcpyAsync(s->q_dev, q, size_t(s->n_q) * D * 4, cudaMemcpyHostToDevice, st));
+    CKV_CUDA_TRY(cudaMemcpyAsync(s->kn_dev, kn, size_t(s->U) * D * 2, cudaMemcpyHostToDevice, st));
+    CKV_CUDA_TRY(cudaMemcpyAsync(s->vn_dev, vn, size_t(s->U) * D * 2, cudaMemcpyHostToDevice, st));
+    qd = s->q_dev;
+    kd = s->kn_dev;
+    vd = s->vn_dev;
+    od = s->out_dev;
+  }
+  CKV_TRY(session_select_attend(s, qd, od));
+  // append this step's token (harness.hpp:318-320)
+  k_append_kv<<<s->U, 16, 0, st>>>(kd, vd, s->K, s->V, s->n_ctx, s->p_cap);
+  CKV_LAUNCH_CHECK("k_append_kv");
+  s->ctx->launches++;
+  s->n_ctx++;
+  s->pending++;
+  s->steps++;
+  if (s->pending == s->d.decode_batch) {  // harness.hpp:325-337 (synchronous mode)
+    ckv_decode_cluster_desc dd{};
+    dd.n_units = s->U;
+    dd.pos0 = s->labeled_end;
+    dd.rows = s->pending;
+    dd.p_cap = s->p_cap;
+    dd.c_cap = s->c_cap;
+    dd.c_plus = s->d.c_plus;
+    dd.max_iters = s->d.max_iters;
+    CKV_TRY(ckv_cluster_decode_batch(s->ctx, &dd, s->K, s->seeds.data(), s->cents, s->labels,
+                                     s->n_clusters, nullptr));
+    s->labeled_end += s->pending;
+    s->C_cur += std::min(s->d.c_plus, s->pending);
+    s->pending = 0;
+    CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
+                            s->n_clusters, s->sizes, s->starts, s->sorted));
+  }
+  if (!on_device) {
+    CKV_CUDA_TRY(cudaMemcpyAsync(out, s->out_dev, size_t(s->n_q) * D * 4, cudaMemcpyDeviceToHost,
+                                 st));
+    CKV_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return CKV_OK;
+}
+
+int ckv_session_stats_get(ckv_session* s, ckv_session_stats* st) {
+  st->n_ctx = s->n_ctx;
+  st->labeled_end = s->labeled_end;
+  st->steps = s->steps;
+  st->max_clusters = s->C_cur;
+  st->launches = s->ctx->launches;
+  return CKV_OK;
+}
+
+int ckv_session_state(ckv_session* s, float** cents, int32_t** labels, uint32_t** n_clusters,
+                      uint32_t** sizes, uint32_t** starts, uint32_t** sorted,
+                      uint32_t** token_ids, uint32_t** n_tokens, uint32_t* c_cap,
+                      uint32_t* sel_cap) {
+  if (cents) *cents = s->cents;
+  if (labels) *labels = s->labels;
+  if (n_clusters) *n_clusters = s->n_clusters;
+  if (sizes) *sizes = s->sizes;
+  if (starts) *starts = s->starts;
+  if (sorted) *sorted = s->sorted;
+  if (token_ids) *token_ids = s->token_ids;
+  if (n_tokens) *n_tokens = s->n_tokens;
+  if (c_cap) *c_cap = s->c_cap;
+  if (sel_cap) *sel_cap = s->sel_cap;
+  return CKV_OK;
+}
+
+ckv_cache* ckv_session_cache(ckv_session* s) { return s->cache; }
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+// ckv_index.cu — K5: stable counting sort of cluster labels into the
+// ClusterIndex layout (selection.hpp:16-48 build_index).
+//
+// One CTA per unit.  W warps each own a contiguous segment of positions:
+//   1. per-warp histograms hist[w][c] (smem atomics);
+//   2. column scan: starts[c] = sum_{c'<c} size[c'], and per-warp write
+//      cursors off[w][c] = starts[c] + sum_{w'<w} hist[w'][c];
+//   3. each warp walks its segment in order, 32 positions at a time, ranks
+//      equal labels with __match_any_sync and scatters position ids.
+// Warp w's ids precede warp w+1's for every cluster and each warp scatters
+// in position order, so the sort is stable: identical to the reference's
+// sequential cursor loop (selection.hpp:41-46), bit for bit.
+//
+// The same kernel produces the member lists and counts the k-means update
+// needs (ckv_kmeans.cu) and, optionally, compares the labels against a
+// previous assignment (the convergence test, clustering.hpp:252).
+#include "ckv_internal.cuh"
+
+namespace ckvb {
+
+__global__ void __launch_bounds__(512)
+k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint32_t c_cap,
+        const uint32_t* __restrict__ n_clusters, uint32_t c_uniform,
+        uint32_t* __restrict__ sizes, uint32_t* __restrict__ starts,
+        uint32_t* __restrict__ sorted_ids, const int32_t* __restrict__ prev_labels,
+        int32_t* __restrict__ changed, const int32_t* __restrict__ active,
+        int32_t* __restrict__ any_empty) {
+  const uint32_t u = blockIdx.x;
+  if (active && !active[u]) return;
+  const uint32_t C = n_clusters ? n_clusters[u] : c_uniform;
+  const int W = blockDim.x >> 5;
+  const int w = warp_id(), lane = lane_id();
+  extern __shared__ uint32_t sm[];
+  uint32_t* hist = sm;                       // [W][C]
+  __shared__ uint32_t s_total;
+  __shared__ int s_changed, s_empty;
+
+  const int32_t* lab = labels + size_t(u) * p_cap;
+  for (uint32_t i = threadIdx.x; i < uint32_t(W) * C; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x == 0) { s_changed = 0; s_empty = 0; }
+  __syncthreads();
+
+  const uint32_t seg = (n_pos + W - 1) / W;
+  const uint32_t p0 = min(n_pos, seg * w), p1 = min(n_pos, p0 + seg);
+  int my_changed = 0;
+  const int32_t* prev = prev_labels ? prev_labels + size_t(u) * p_cap : nullptr;
+  for (uint32_t p = p0 + lane; p < p1; p += 32) {
+    int32_t l = lab[p];
+    if (l >= 0) atomicAdd(&hist[w * C + l], 1u);
+    if (prev && prev[p] != l) my_changed = 1;
+  }
+  if (prev && __any_sync(0xffffffffu, my_changed) && lane == 0) s_changed = 1;
+  __syncthreads();
+
+  // column totals -> exclusive scan over clusters (chunked, one warp per
+  // 32 clusters at a time, serial carry through the block)
+  uint32_t* sz = sizes + size_t(u) * c_cap;
+  uint32_t* st = starts + size_t(u) * (c_cap + 1);
+  if (w == 0) {
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+      uint32_t c = c0 + lane;
+      uint32_t tot = 0;
+      if (c < C) {
+        uint32_t run = 0;
+        for (int ww = 0; ww < W; ++ww) {
+          uint32_t h = hist[ww * C + c];
+          hist[ww * C + c] = run;  // becomes the intra-column offset
+          run += h;
+        }
+        tot = run;
+      }
+      uint32_t incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      uint32_t excl = carry + incl - tot;
+      if (c < C) {
+        sz[c] = tot;
+        st[c] = excl;
+        if (tot == 0) s_empty = 1;
+        for (int ww = 0; ww < W; ++ww) hist[ww * C + c] += excl;
+      }
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) { st[C] = carry; s_total = carry; }
+  }
+  __syncthreads();
+
+  // stable scatter: warp w walks its segment in order
+  uint32_t* out = sorted_ids + size_t(u) * p_cap;
+  uint32_t* cur = hist + w * C;
+  for (uint32_t b = p0; b < p1; b += 32) {
+    uint32_t p = b + lane;
+    int32_t l = p < p1 ? lab[p] : -1;
+    unsigned valid = __ballot_sync(0xffffffffu, l >= 0);
+    if (l >= 0) {
+      unsigned peers = __match_any_sync(valid, l);
+      unsigned rank = __popc(peers & ((1u << lane) - 1u));
+      out[cur[l] + rank] = p;
+      __syncwarp(valid);
+      if (rank == 0) cur[l] += __popc(peers);
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) {
+    if (changed && prev) changed[u] = s_changed;
+    if (any_empty && s_empty) any_empty[u] = 1;
+  }
+}
+
+int launch_index(cudaStream_t st, uint32_t n_units, const int32_t* labels, uint32_t n_pos,
+                 uint32_t p_cap, uint32_t c_cap, const uint32_t* n_clusters,
+                 uint32_t c_uniform, uint32_t* sizes, uint32_t* starts, uint32_t* sorted_ids,
+                 const int32_t* prev_labels, int32_t* changed, const int32_t* active,
+                 int32_t* any_empty) {
+  if (n_units == 0) return CKV_OK;
+  // warps per CTA limited by the smem histogram [W][c_cap]
+  const size_t budget = 200 * 1024;
+  int W = 16;
+  while (W > 1 && size_t(W) * c_cap * 4 > budget) W >>= 1;
+  if (size_t(W) * c_cap * 4 > budget) {
+    set_error("build_index: cluster capacity exceeds the 51200-cluster smem limit");
+    return CKV_EINVAL;
+  }
+  size_t smem = size_t(W) * c_cap * 4;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CKV_CUDA_TRY(cudaFuncSetAttribute(k_index, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(budget)));
+    attr_set = true;
+  }
+  k_index<<<n_units, W * 32, smem, st>>>(labels, n_pos, p_cap, c_cap, n_clusters, c_uniform,
+                                         sizes, starts, sorted_ids, prev_labels, changed, active,
+                                         any_empty);
+  CKV_LAUNCH_CHECK("k_index");
+  return CKV_OK;
+}
+
+}  // namespace ckvb

@@ -1,0 +1,70 @@
+// ckv_internal.cuh — launch wrappers shared between the kernel files and the
+// C-ABI (ckv_capi.cu).  Internal; not part of the installed interface.
+#pragma once
+#include "ckv_common.cuh"
+
+struct ckv_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint64_t launches = 0;
+  // pinned host scratch for small control read-backs
+  int32_t* h_flags = nullptr;
+  size_t h_flags_cap = 0;
+};
+
+namespace ckvb {
+
+int launch_index(cudaStream_t st, uint32_t n_units, const int32_t* labels, uint32_t n_pos,
+                 uint32_t p_cap, uint32_t c_cap, const uint32_t* n_clusters,
+                 uint32_t c_uniform, uint32_t* sizes, uint32_t* starts, uint32_t* sorted_ids,
+                 const int32_t* prev_labels, int32_t* changed, const int32_t* active,
+                 int32_t* any_empty);
+
+// k-means driver (ckv_kmeans.cu); keys may be strided per unit
+struct KMeansArgs {
+  uint32_t n_units, n, C, max_iters;
+  uint64_t key_stride;      // elements between units' keys
+  uint32_t c_stride;        // centroid rows between units
+  uint32_t label_stride;    // labels between units
+  uint32_t flags;
+  const uint16_t* keys;
+  const uint32_t* init_rows;  // device [n_units*C]
+  float* centroids;
+  int32_t* labels;
+};
+int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
+               double* objective_host, uint32_t* repair_host);
+
+}  // namespace ckvb
+
+namespace ckvb {
+struct CacheDev {
+  uint32_t n_slots, c_cap, retention, d, words;
+  uint32_t* bits;                // [n_slots][retention][words]
+  uint32_t* ring;                // [n_slots][2] = head, len
+  unsigned long long* counters;  // [n_slots][4]
+};
+int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
+                  const float* cents, const uint32_t* n_clusters, const uint32_t* sizes,
+                  const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
+                  uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked,
+                  double* scores, const CacheDev& cache);
+int launch_cache_lookup(cudaStream_t st, const CacheDev& cache, uint32_t slot,
+                        const uint32_t* sel, uint32_t n_sel, const uint32_t* sizes,
+                        uint32_t* hit, uint32_t* miss, uint32_t* counts);
+int launch_cache_invalidate(cudaStream_t st, const CacheDev& cache, uint32_t slot,
+                            const uint32_t* retired, uint32_t n);
+int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
+                  const uint16_t* K, const uint16_t* V, const uint32_t* token_ids,
+                  const uint32_t* n_tokens, float* out, float* weights, float* logits_ws,
+                  float* part, uint32_t* tickets);
+size_t attend_part_floats(uint32_t n_q, uint32_t max_tokens);
+uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
+void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows);
+}  // namespace ckvb
+
+struct ckv_cache {
+  ckv_ctx* ctx;
+  ckvb::CacheDev dev;
+};

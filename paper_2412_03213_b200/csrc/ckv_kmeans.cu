@@ -1,0 +1,570 @@
+// ckv_kmeans.cu — K1-K4: batched cosine k-means (clustering.hpp:157-263).
+//
+// All active units advance in lock step, one assignment pass per host loop
+// iteration; per-unit convergence masks the finished ones.  Per iteration:
+//   update   : centroid = float(f64 sum / count) over the members in the
+//              counting-sort order (position-ascending per cluster, exactly
+//              the reference's accumulation order, clustering.hpp:207-216),
+//              fused with normalize() of the next assignment's directions
+//   assign   : tensor-core candidate filter + exact f64 re-score
+//              (ckv_assign_tc.cu), or the exact CUDA-core pass below
+//   index    : counting sort -> counts, member lists, changed-vs-previous
+//   repair   : empty-cluster repair (clustering.hpp:128-153), rare
+//   control  : convergence / max_iters bookkeeping, one 4-byte read-back
+// Every integer result (labels, iterations, converged, repair iterations)
+// and every centroid bit equals the reference for identical inputs.
+#include <vector>
+
+#include "ckv_internal.cuh"
+
+namespace ckvb {
+
+// ---------------------------------------------------------------------------
+// validation: kmeans_cosine's input checks (clustering.hpp:166-172)
+// flags[u]: bit0 = some non-finite value, bit1 = some row with norm >= 1e-12
+// ---------------------------------------------------------------------------
+__global__ void k_validate(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
+                           int32_t* __restrict__ flags) {
+  const uint32_t u = blockIdx.y;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  int f = 0;
+  if (i < n) {
+    const uint16_t* row = keys + u * key_stride + size_t(i) * D;
+    double s = 0.0;
+    for (int j = 0; j < D; ++j) {
+      uint16_t b = row[j];
+      if ((b & 0x7f80u) == 0x7f80u) f |= 1;
+      float x = bf16_to_f32(b);
+      s = __fma_rn(double(x), double(x), s);
+    }
+    if (!(f & 1) && sqrt(s) >= 1e-12) f |= 2;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (lane_id() == 0 && f) atomicOr(&flags[u], f);
+}
+
+// centroids[u][c] = keys[u][init_rows[u][c]]  (clustering.hpp:195-198)
+__global__ void k_init_centroids(const uint16_t* __restrict__ keys, uint64_t key_stride,
+                                 const uint32_t* __restrict__ init_rows, uint32_t C,
+                                 uint32_t c_stride, float* __restrict__ cents) {
+  const uint32_t u = blockIdx.y, c = blockIdx.x;
+  const uint32_t r = init_rows[size_t(u) * C + c];
+  const uint16_t* src = keys + u * key_stride + size_t(r) * D;
+  float* dst = cents + (size_t(u) * c_stride + c) * D;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) dst[j] = bf16_to_f32(src[j]);
+}
+
+// normalize() (common.hpp:141-147) of every centroid -> f32 dirs (exact),
+// bf16 dirs (tensor-core B operand), f64 norms (for cosine_distance).
+// One thread per centroid: the norm is a sequential f64 chain by contract.
+__global__ void k_dirs(const float* __restrict__ cents, uint32_t C, uint32_t c_stride,
+                       uint32_t c_pad, float* __restrict__ dirs, uint16_t* __restrict__ dirs_bf,
+                       double* __restrict__ cnorm, const int32_t* __restrict__ active) {
+  const uint32_t u = blockIdx.y;
+  if (active && !active[u]) return;
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c_pad) return;
+  float* dr = dirs + (size_t(u) * c_pad + c) * D;
+  uint16_t* db = dirs_bf + (size_t(u) * c_pad + c) * D;
+  if (c >= C) {  // padding columns of the MMA operand
+    for (int j = 0; j < D; ++j) { dr[j] = 0.f; db[j] = 0; }
+    return;
+  }
+  const float* src = cents + (size_t(u) * c_stride + c) * D;
+  double nrm = sqrt(dot_seq_ff(src, src));
+  cnorm[size_t(u) * c_pad + c] = nrm;
+  for (int j = 0; j < D; ++j) {
+    float x = src[j];
+    float y = nrm > 0.0 ? float(double(x) / nrm) : x;
+    dr[j] = y;
+    db[j] = f32_to_bf16_rn(y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// exact assignment on CUDA cores (AssignScorer::assign, clustering.hpp:104-115)
+// 128 keys per CTA, keys transposed in smem, one sequential f64 chain per
+// (key, centroid).  Used for small problems (decode batches) and as the
+// reference path the tensor-core filter is tested against.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128)
+k_assign_exact(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n, uint32_t C,
+               uint32_t c_pad, const float* __restrict__ dirs, int32_t* __restrict__ labels,
+               uint32_t label_stride, const int32_t* __restrict__ active) {
+  const uint32_t u = blockIdx.y;
+  if (active && !active[u]) return;
+  __shared__ uint16_t ks[D][130];
+  const uint32_t i0 = blockIdx.x * 128;
+  const uint16_t* kb = keys + u * key_stride;
+  for (uint32_t e = threadIdx.x; e < 128u * D; e += 128) {
+    uint32_t r = e / D, j = e % D;
+    ks[j][r] = (i0 + r < n) ? kb[size_t(i0 + r) * D + j] : uint16_t(0);
+  }
+  __syncthreads();
+  const uint32_t i = i0 + threadIdx.x;
+  if (i >= n) return;
+  const float* dr = dirs + size_t(u) * c_pad * D;
+  uint32_t best = 0;
+  double best_s = -INFINITY;
+  for (uint32_t c = 0; c < C; ++c) {
+    const float* dc = dr + size_t(c) * D;
+    double s = 0.0;
+#pragma unroll 16
+    for (int j = 0; j < D; ++j) s = __fma_rn(double(bf16_to_f32(ks[j][threadIdx.x])), double(__ldg(dc + j)), s);
+    if (s > best_s) { best_s = s; best = c; }
+  }
+  labels[size_t(u) * label_stride + i] = int32_t(best);
+}
+
+// ---------------------------------------------------------------------------
+// update: per (unit, cluster) one warp; lane owns dims [4*lane, 4*lane+4).
+// f64 sums over the members in sorted (= position) order, then
+// float(sum / count), then the next pass's dirs (normalize, fused).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uint32_t c_stride,
+         uint32_t c_pad, uint32_t label_stride, const uint32_t* __restrict__ sizes,
+         const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
+         float* __restrict__ cents, float* __restrict__ dirs, uint16_t* __restrict__ dirs_bf,
+         double* __restrict__ cnorm, const int32_t* __restrict__ active) {
+  const uint32_t u = blockIdx.y;
+  if (active && !active[u]) return;
+  const uint32_t c = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  const int lane = lane_id();
+  if (c >= c_pad) return;
+  float* dr = dirs + (size_t(u) * c_pad + c) * D;
+  uint16_t* db = dirs_bf + (size_t(u) * c_pad + c) * D;
+  if (c >= C) {
+    for (int j = lane; j < D; j += 32) { dr[j] = 0.f; db[j] = 0; }
+    return;
+  }
+  const uint32_t cnt = sizes[size_t(u) * c_stride + c];
+  const uint32_t beg = starts[size_t(u) * (c_stride + 1) + c];
+  const uint32_t* ids = sorted_ids + size_t(u) * label_stride + beg;
+  const uint16_t* kb = keys + u * key_stride;
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  uint32_t m = 0;
+  // software-pipelined member walk: prefetch 4 rows ahead
+  for (; m + 4 <= cnt; m += 4) {
+    uint2 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t id = __ldg(ids + m + k);
+      v[k] = __ldg(reinterpret_cast<const uint2*>(kb + size_t(id) * D) + lane);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a0 += double(__uint_as_float(v[k].x << 16));
+      a1 += double(__uint_as_float(v[k].x & 0xffff0000u));
+      a2 += double(__uint_as_float(v[k].y << 16));
+      a3 += double(__uint_as_float(v[k].y & 0xffff0000u));
+    }
+  }
+  for (; m < cnt; ++m) {
+    uint32_t id = __ldg(ids + m);
+    uint2 v = __ldg(reinterpret_cast<const uint2*>(kb + size_t(id) * D) + lane);
+    a0 += double(__uint_as_float(v.x << 16));
+    a1 += double(__uint_as_float(v.x & 0xffff0000u));
+    a2 += double(__uint_as_float(v.y << 16));
+    a3 += double(__uint_as_float(v.y & 0xffff0000u));
+  }
+  const double dc = double(cnt);
+  float x0 = float(a0 / dc), x1 = float(a1 / dc), x2 = float(a2 / dc), x3 = float(a3 / dc);
+  float* ct = cents + (size_t(u) * c_stride + c) * D;
+  reinterpret_cast<float4*>(ct)[lane] = make_float4(x0, x1, x2, x3);
+  // sequential norm chain over j = 0..127: lane L holds j = 4L..4L+3
+  double s = 0.0;
+  for (int L = 0; L < 32; ++L) {
+    double y0 = __shfl_sync(0xffffffffu, double(x0), L);
+    double y1 = __shfl_sync(0xffffffffu, double(x1), L);
+    double y2 = __shfl_sync(0xffffffffu, double(x2), L);
+    double y3 = __shfl_sync(0xffffffffu, double(x3), L);
+    s = __fma_rn(y0, y0, s);
+    s = __fma_rn(y1, y1, s);
+    s = __fma_rn(y2, y2, s);
+    s = __fma_rn(y3, y3, s);
+  }
+  const double nrm = sqrt(s);
+  if (lane == 0) cnorm[size_t(u) * c_pad + c] = nrm;
+  float d0 = nrm > 0.0 ? float(double(x0) / nrm) : x0;
+  float d1 = nrm > 0.0 ? float(double(x1) / nrm) : x1;
+  float d2 = nrm > 0.0 ? float(double(x2) / nrm) : x2;
+  float d3 = nrm > 0.0 ? float(double(x3) / nrm) : x3;
+  reinterpret_cast<float4*>(dr)[lane] = make_float4(d0, d1, d2, d3);
+  uint2 pk;
+  pk.x = uint32_t(f32_to_bf16_rn(d0)) | (uint32_t(f32_to_bf16_rn(d1)) << 16);
+  pk.y = uint32_t(f32_to_bf16_rn(d2)) | (uint32_t(f32_to_bf16_rn(d3)) << 16);
+  reinterpret_cast<uint2*>(db)[lane] = pk;
+}
+
+// ---------------------------------------------------------------------------
+// empty-cluster repair (clustering.hpp:128-153) — one CTA per unit that has
+// an empty cluster; sequential over empty ids as the reference is.
+// ---------------------------------------------------------------------------
+__device__ double cosine_distance_dev(const uint16_t* k, const float* c, double nb) {
+  double na = sqrt(dot_seq_bb(k, k));
+  if (na < 1e-12 || nb < 1e-12) return 1.0;
+  double dd = 1.0 - dot_seq_bf(k, c) / (na * nb);
+  return dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
+}
+
+__global__ void __launch_bounds__(256)
+k_repair(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n, uint32_t C,
+         uint32_t c_stride, uint32_t c_pad, int32_t* __restrict__ labels, uint32_t label_stride,
+         uint32_t* __restrict__ sizes, const float* __restrict__ cents,
+         const double* __restrict__ cnorm, const int32_t* __restrict__ need,
+         uint32_t* __restrict__ repair_count) {
+  const uint32_t u = blockIdx.x;
+  if (!need[u]) return;
+  uint32_t* counts = sizes + size_t(u) * c_stride;
+  int32_t* lab = labels + size_t(u) * label_stride;
+  const uint16_t* kb = keys + u * key_stride;
+  __shared__ uint32_t s_cnt[8];
+  __shared__ uint32_t s_idx[8];
+  __shared__ double s_d[8];
+  __shared__ uint32_t s_largest;
+  uint32_t repairs = 0;
+  for (uint32_t c = 0; c < C; ++c) {
+    __syncthreads();
+    if (counts[c] > 0) continue;
+    // largest = first maximum of counts
+    uint32_t bc = 0, bi = 0xffffffffu;
+    for (uint32_t k = threadIdx.x; k < C; k += blockDim.x) {
+      uint32_t v = counts[k];
+      if (v > bc || (v == bc && k < bi)) { bc = v; bi = k; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      uint32_t oc = __shfl_xor_sync(0xffffffffu, bc, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oc > bc || (oc == bc && oi < bi)) { bc = oc; bi = oi; }
+    }
+    if (lane_id() == 0) { s_cnt[warp_id()] = bc; s_idx[warp_id()] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t b = s_cnt[0], ix = s_idx[0];
+      for (int w = 1; w < int(blockDim.x >> 5); ++w)
+        if (s_cnt[w] > b || (s_cnt[w] == b && s_idx[w] < ix)) { b = s_cnt[w]; ix = s_idx[w]; }
+      s_largest = ix;
+      s_cnt[0] = b;
+    }
+    __syncthreads();
+    const uint32_t largest = s_largest;
+    if (s_cnt[0] <= 1) continue;
+    // victim = first member of `largest` with the maximum cosine distance
+    const float* cl = cents + (size_t(u) * c_stride + largest) * D;
+    const double nb = cnorm[size_t(u) * c_pad + largest];
+    double bd = -1.0;
+    uint32_t bv = 0xffffffffu;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      if (uint32_t(lab[i]) != largest) continue;
+      double dd = cosine_distance_dev(kb + size_t(i) * D, cl, nb);
+      if (dd > bd) { bd = dd; bv = i; }  // i increases per thread: first max kept
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      uint32_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      if (od > bd || (od == bd && ov < bv)) { bd = od; bv = ov; }
+    }
+    __syncthreads();
+    if (lane_id() == 0) { s_d[warp_id()] = bd; s_idx[warp_id()] = bv; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = s_d[0];
+      uint32_t v = s_idx[0];
+      for (int w = 1; w < int(blockDim.x >> 5); ++w)
+        if (s_d[w] > b || (s_d[w] == b && s_idx[w] < v)) { b = s_d[w]; v = s_idx[w]; }
+      if (v == 0xffffffffu) v = 0;  // no member beat worst = -1 (NaN): reference keeps 0
+      lab[v] = int32_t(c);
+      counts[largest]--;
+      counts[c]++;
+    }
+    repairs++;
+  }
+  if (threadIdx.x == 0) repair_count[u] = repairs;
+}
+
+// objective (clustering.hpp:118-124) — diagnostic; f64 sum, any order
+__global__ void k_objective(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
+                            uint32_t c_stride, uint32_t c_pad, const int32_t* __restrict__ labels,
+                            uint32_t label_stride, const float* __restrict__ cents,
+                            const double* __restrict__ cnorm, double* __restrict__ obj,
+                            const int32_t* __restrict__ active) {
+  const uint32_t u = blockIdx.y;
+  if (active && !active[u]) return;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    uint32_t l = uint32_t(labels[size_t(u) * label_stride + i]);
+    v = cosine_distance_dev(keys + u * key_stride + size_t(i) * D,
+                            cents + (size_t(u) * c_stride + l) * D, cnorm[size_t(u) * c_pad + l]);
+  }
+  v = warp_sum(v);
+  if (lane_id() == 0) atomicAdd(&obj[u], v);
+}
+
+// convergence bookkeeping after pass t (t = 0 is the initial assignment)
+__global__ void k_control(uint32_t n_units, uint32_t t, uint32_t max_iters,
+                          int32_t* __restrict__ active, const int32_t* __restrict__ changed,
+                          int32_t* __restrict__ converged, uint32_t* __restrict__ iters,
+                          int32_t* __restrict__ any_empty, uint32_t* __restrict__ repair_count,
+                          uint32_t* __restrict__ repair_log, double* __restrict__ obj,
+                          double* __restrict__ obj_log, int32_t* __restrict__ n_active) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  int still = 0;
+  if (u < n_units && active[u]) {
+    repair_log[size_t(u) * (max_iters + 1) + t] = repair_count[u];
+    obj_log[size_t(u) * (max_iters + 1) + t] = obj[u];
+    repair_count[u] = 0;
+    obj[u] = 0.0;
+    any_empty[u] = 0;
+    if (t >= 1 && !changed[u]) {
+      converged[u] = 1;
+      iters[u] = t;
+      active[u] = 0;
+    } else if (t == max_iters) {
+      iters[u] = t;
+      active[u] = 0;
+    } else {
+      still = 1;
+    }
+  }
+  still = __reduce_add_sync(0xffffffffu, still);
+  if (lane_id() == 0 && still) atomicAdd(n_active, still);
+}
+
+__global__ void k_copy_labels(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+                              uint32_t n, uint32_t stride, const uint32_t* __restrict__ iters,
+                              int parity_wanted) {
+  const uint32_t u = blockIdx.y;
+  if (int(iters[u] & 1u) != parity_wanted) return;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[size_t(u) * stride + i] = src[size_t(u) * stride + i];
+}
+
+// tensor-core assignment (ckv_assign_tc.cu); returns CKV_EINVAL if the shape
+// is unsupported so the caller falls back to the exact path
+int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
+              uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs_bf,
+              const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
+              void* scratch, size_t scratch_bytes, uint64_t* launches);
+size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C);
+bool assign_tc_supported(uint32_t n, uint32_t C);
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  template <typename T> T* as() { return static_cast<T*>(p); }
+};
+int dalloc(DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string("kmeans: device allocation failed: ") + cudaGetErrorString(e));
+    return CKV_ENOMEM;
+  }
+  return CKV_OK;
+}
+}  // namespace
+
+int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
+               double* objective_host, uint32_t* repair_host) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t U = a.n_units, n = a.n, C = a.C, MI = a.max_iters;
+  if (U == 0) return CKV_OK;
+  if (C < 1 || C > n) { set_error("kmeans: need 1 <= C <= N"); return CKV_EINVAL; }
+  if (MI < 1) { set_error("ClusterConfig: max_iters must be >= 1"); return CKV_EINVAL; }
+  const uint32_t c_pad = (C + 31) / 32 * 32;
+  const bool want_obj = (a.flags & CKV_KM_OBJECTIVE) != 0;
+
+  // ---- scratch ----------------------------------------------------------
+  DevBuf b_flags, b_lab1, b_sizes, b_starts, b_sorted, b_dirs, b_dirsbf, b_cnorm, b_active,
+      b_changed, b_conv, b_iters, b_empty, b_rep, b_replog, b_obj, b_objlog, b_nact, b_tc;
+  const uint32_t LS = a.label_stride, CS = a.c_stride;
+  CKV_TRY(dalloc(b_flags, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(b_lab1, sizeof(int32_t) * size_t(U) * LS));
+  CKV_TRY(dalloc(b_sizes, sizeof(uint32_t) * size_t(U) * CS));
+  CKV_TRY(dalloc(b_starts, sizeof(uint32_t) * size_t(U) * (CS + 1)));
+  CKV_TRY(dalloc(b_sorted, sizeof(uint32_t) * size_t(U) * LS));
+  CKV_TRY(dalloc(b_dirs, sizeof(float) * size_t(U) * c_pad * D));
+  CKV_TRY(dalloc(b_dirsbf, sizeof(uint16_t) * size_t(U) * c_pad * D));
+  CKV_TRY(dalloc(b_cnorm, sizeof(double) * size_t(U) * c_pad));
+  CKV_TRY(dalloc(b_active, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(b_changed, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(b_conv, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(b_iters, sizeof(uint32_t) * U));
+  CKV_TRY(dalloc(b_empty, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(b_rep, sizeof(uint32_t) * U));
+  CKV_TRY(dalloc(b_replog, sizeof(uint32_t) * size_t(U) * (MI + 1)));
+  CKV_TRY(dalloc(b_obj, sizeof(double) * U));
+  CKV_TRY(dalloc(b_objlog, sizeof(double) * size_t(U) * (MI + 1)));
+  CKV_TRY(dalloc(b_nact, sizeof(int32_t)));
+
+  const bool use_tc = !(a.flags & CKV_KM_EXACT_ONLY) && assign_tc_supported(n, C);
+  size_t tc_bytes = use_tc ? assign_tc_scratch_bytes(U, n, C) : 0;
+  if (use_tc) CKV_TRY(dalloc(b_tc, tc_bytes));
+
+  if (!ctx->h_flags || ctx->h_flags_cap < U + 1) {
+    if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+    CKV_CUDA_TRY(cudaMallocHost(&ctx->h_flags, sizeof(int32_t) * (U + 1)));
+    ctx->h_flags_cap = U + 1;
+  }
+  int32_t* hf = ctx->h_flags;
+
+  // ---- validation (clustering.hpp:166-172) -------------------------------
+  if (!(a.flags & CKV_KM_NO_VALIDATE)) {
+    CKV_CUDA_TRY(cudaMemsetAsync(b_flags.p, 0, sizeof(int32_t) * U, st));
+    dim3 g((n + 255) / 256, U);
+    k_validate<<<g, 256, 0, st>>>(a.keys, a.key_stride, n, b_flags.as<int32_t>());
+    CKV_LAUNCH_CHECK("k_validate");
+    ctx->launches++;
+    CKV_CUDA_TRY(cudaMemcpyAsync(hf, b_flags.p, sizeof(int32_t) * U, cudaMemcpyDeviceToHost, st));
+    CKV_CUDA_TRY(cudaStreamSynchronize(st));
+    for (uint32_t u = 0; u < U; ++u)
+      if (hf[u] & 1) { set_error("kmeans: keys must be finite"); return CKV_EINVAL; }
+    for (uint32_t u = 0; u < U; ++u)
+      if (!(hf[u] & 2)) {
+        set_error("kmeans: degenerate input, all keys zero-norm");
+        return CKV_EINVAL;
+      }
+  }
+
+  int32_t* lab[2] = {a.labels, b_lab1.as<int32_t>()};
+  float* dirs = b_dirs.as<float>();
+  uint16_t* dirs_bf = b_dirsbf.as<uint16_t>();
+  double* cnorm = b_cnorm.as<double>();
+  int32_t* active = b_active.as<int32_t>();
+
+  // active = 1, others = 0
+  {
+    std::vector<int32_t> ones(U, 1);
+    CKV_CUDA_TRY(cudaMemcpyAsync(active, ones.data(), sizeof(int32_t) * U,
+                                 cudaMemcpyHostToDevice, st));
+    CKV_CUDA_TRY(cudaMemsetAsync(b_conv.p, 0, sizeof(int32_t) * U, st));
+    CKV_CUDA_TRY(cudaMemsetAsync(b_iters.p, 0, sizeof(uint32_t) * U, st));
+    CKV_CUDA_TRY(cudaMemsetAsync(b_empty.p, 0, sizeof(int32_t) * U, st));
+    CKV_CUDA_TRY(cudaMemsetAsync(b_rep.p, 0, sizeof(uint32_t) * U, st));
+    CKV_CUDA_TRY(cudaMemsetAsync(b_obj.p, 0, sizeof(double) * U, st));
+    CKV_CUDA_TRY(cudaMemsetAsync(b_changed.p, 0, sizeof(int32_t) * U, st));
+    CKV_CUDA_TRY(cudaStreamSynchronize(st));  // `ones` leaves scope
+  }
+
+  // ---- init (clustering.hpp:174-198) --------------------------------------
+  k_init_centroids<<<dim3(C, U), 128, 0, st>>>(a.keys, a.key_stride, a.init_rows, C, CS,
+                                                a.centroids);
+  CKV_LAUNCH_CHECK("k_init_centroids");
+  k_dirs<<<dim3((c_pad + 127) / 128, U), 128, 0, st>>>(a.centroids, C, CS, c_pad, dirs, dirs_bf,
+                                                       cnorm, active);
+  CKV_LAUNCH_CHECK("k_dirs");
+  ctx->launches += 2;
+
+  auto assign = [&](int32_t* out) -> int {
+    if (use_tc)
+      return assign_tc(st, a.keys, a.key_stride, n, C, c_pad, U, dirs_bf, dirs, out, LS, active,
+                       b_tc.p, tc_bytes, &ctx->launches);
+    k_assign_exact<<<dim3((n + 127) / 128, U), 128, 0, st>>>(a.keys, a.key_stride, n, C, c_pad,
+                                                            dirs, out, LS, active);
+    CKV_LAUNCH_CHECK("k_assign_exact");
+    ctx->launches++;
+    return CKV_OK;
+  };
+
+  auto count_repair = [&](int32_t* cur, const int32_t* prev) -> int {
+    CKV_TRY(launch_index(st, U, cur, n, LS, CS, nullptr, C, b_sizes.as<uint32_t>(),
+                         b_starts.as<uint32_t>(), b_sorted.as<uint32_t>(), prev,
+                         b_changed.as<int32_t>(), active, b_empty.as<int32_t>()));
+    k_repair<<<U, 256, 0, st>>>(a.keys, a.key_stride, n, C, CS, c_pad, cur, LS,
+                                b_sizes.as<uint32_t>(), a.centroids, cnorm,
+                                b_empty.as<int32_t>(), b_rep.as<uint32_t>());
+    CKV_LAUNCH_CHECK("k_repair");
+    // re-sort (and re-compare) the units that were repaired
+    CKV_TRY(launch_index(st, U, cur, n, LS, CS, nullptr, C, b_sizes.as<uint32_t>(),
+                         b_starts.as<uint32_t>(), b_sorted.as<uint32_t>(), prev,
+                         b_changed.as<int32_t>(), b_empty.as<int32_t>(), nullptr));
+    ctx->launches += 3;
+    if (want_obj) {
+      k_objective<<<dim3((n + 255) / 256, U), 256, 0, st>>>(a.keys, a.key_stride, n, CS, c_pad,
+                                                             cur, LS, a.centroids, cnorm,
+                                                             b_obj.as<double>(), active);
+      CKV_LAUNCH_CHECK("k_objective");
+      ctx->launches++;
+    }
+    return CKV_OK;
+  };
+
+  auto control = [&](uint32_t t, int32_t* n_active_host) -> int {
+    CKV_CUDA_TRY(cudaMemsetAsync(b_nact.p, 0, sizeof(int32_t), st));
+    k_control<<<(U + 127) / 128, 128, 0, st>>>(
+        U, t, MI, active, b_changed.as<int32_t>(), b_conv.as<int32_t>(), b_iters.as<uint32_t>(),
+        b_empty.as<int32_t>(), b_rep.as<uint32_t>(), b_replog.as<uint32_t>(), b_obj.as<double>(),
+        b_objlog.as<double>(), b_nact.as<int32_t>());
+    CKV_LAUNCH_CHECK("k_control");
+    ctx->launches++;
+    CKV_CUDA_TRY(cudaMemcpyAsync(n_active_host, b_nact.p, sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, st));
+    CKV_CUDA_TRY(cudaStreamSynchronize(st));
+    return CKV_OK;
+  };
+
+  // pass 0: initial assignment, count, repair, objective
+  CKV_TRY(assign(lab[0]));
+  CKV_TRY(count_repair(lab[0], nullptr));
+  CKV_TRY(control(0, &hf[U]));
+
+  for (uint32_t t = 1; t <= MI && hf[U] > 0; ++t) {
+    int32_t* prev = lab[(t - 1) & 1];
+    int32_t* cur = lab[t & 1];
+    // update from the previous labels (sizes/starts/sorted hold its sort)
+    k_update<<<dim3((c_pad + 7) / 8, U), 256, 0, st>>>(
+        a.keys, a.key_stride, C, CS, c_pad, LS, b_sizes.as<uint32_t>(), b_starts.as<uint32_t>(),
+        b_sorted.as<uint32_t>(), a.centroids, dirs, dirs_bf, cnorm, active);
+    CKV_LAUNCH_CHECK("k_update");
+    ctx->launches++;
+    CKV_TRY(assign(cur));
+    CKV_TRY(count_repair(cur, prev));
+    CKV_TRY(control(t, &hf[U]));
+  }
+
+  // final labels live in lab[iterations_used & 1]; lab[0] is the output
+  k_copy_labels<<<dim3(32, U), 256, 0, st>>>(lab[1], lab[0], n, LS, b_iters.as<uint32_t>(), 1);
+  CKV_LAUNCH_CHECK("k_copy_labels");
+  ctx->launches++;
+
+  // ---- results -----------------------------------------------------------
+  std::vector<uint32_t> iters(U), reps(size_t(U) * (MI + 1));
+  std::vector<int32_t> conv(U);
+  std::vector<double> objs(size_t(U) * (MI + 1));
+  CKV_CUDA_TRY(cudaMemcpyAsync(iters.data(), b_iters.p, sizeof(uint32_t) * U,
+                               cudaMemcpyDeviceToHost, st));
+  CKV_CUDA_TRY(cudaMemcpyAsync(conv.data(), b_conv.p, sizeof(int32_t) * U,
+                               cudaMemcpyDeviceToHost, st));
+  CKV_CUDA_TRY(cudaMemcpyAsync(reps.data(), b_replog.p, sizeof(uint32_t) * reps.size(),
+                               cudaMemcpyDeviceToHost, st));
+  if (want_obj)
+    CKV_CUDA_TRY(cudaMemcpyAsync(objs.data(), b_objlog.p, sizeof(double) * objs.size(),
+                                 cudaMemcpyDeviceToHost, st));
+  CKV_CUDA_TRY(cudaStreamSynchronize(st));
+  for (uint32_t u = 0; u < U; ++u) {
+    uint32_t it = iters[u];
+    uint32_t nrep = 0;
+    for (uint32_t t = 0; t <= it; ++t) {
+      if (reps[size_t(u) * (MI + 1) + t] > 0) {
+        if (repair_host) repair_host[size_t(u) * (MI + 1) + nrep] = t;
+        nrep++;
+      }
+      if (objective_host && want_obj)
+        objective_host[size_t(u) * (MI + 1) + t] = objs[size_t(u) * (MI + 1) + t];
+    }
+    if (info_host) {
+      info_host[u].iterations_used = it;
+      info_host[u].converged = conv[u];
+      info_host[u].n_repair = nrep;
+      info_host[u].n_objective = want_obj ? it + 1 : 0;
+    }
+  }
+  return CKV_OK;
+}
+
+}  // namespace ckvb

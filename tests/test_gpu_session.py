@@ -1,0 +1,87 @@
+"""End-to-end decode-loop parity: the device session (prefill clustering,
+per-step select + cache + attention, append, decode-batch clustering every m
+steps) against the oracle replaying simulate_head's ClusterKV branch
+(harness.hpp:193-339) for every (unit, q head)."""
+import numpy as np
+import pytest
+
+from oracle.oracle import ClusterConfig as OCfg
+from tests._inputs import bf16_bits, head, port
+
+pytestmark = pytest.mark.gpu
+
+
+def test_session_vs_oracle_decode_loop(gpu_ctx):
+    import torch
+    from paper_2412_03213_b200 import api
+    from paper_2412_03213_b200.session import Session
+
+    layers, kvh, G = 2, 2, 2
+    L, T, B, m, R = 700, 45, 96, 20, 2
+    U = layers * kvh
+    heads = [head(7, u // kvh, u % kvh, L, T) for u in range(U)]
+    cfg = api.ClusterConfig(decode_batch=m, c0_divisor=40)
+    s = Session(U, G, L, T, B, retention=R, cfg=cfg, kv_heads=kvh)
+    s.load_prompt_host(np.stack([bf16_bits(h["K"]) for h in heads]),
+                       np.stack([bf16_bits(h["V"]) for h in heads]))
+    s.prefill()
+
+    # oracle state per unit
+    P = port()
+    models = []
+    for u in range(U):
+        o = P.cluster_prefill(heads[u]["K"], OCfg(seed=P.mix_seed(0, u // kvh, u % kvh),
+                                                  decode_batch=m, c0_divisor=40))
+        models.append([o.centroids, o.labels])
+    caches = [P.cache(R) for _ in range(U * G)]
+    Kc = [h["K"].copy() for h in heads]
+    Vc = [h["V"].copy() for h in heads]
+    labeled_end, n_ctx = L, L
+    dev = gpu_ctx.device
+    for t in range(T):
+        # q head (u, r) queries row (t + r*T//G) % T of its unit's trace
+        q = np.stack([heads[u]["Q"][(t + r * (T // G)) % T] for u in range(U) for r in range(G)])
+        kn = np.stack([bf16_bits(heads[u]["dK"][t]) for u in range(U)])
+        vn = np.stack([bf16_bits(heads[u]["dV"][t]) for u in range(U)])
+        out = s.step(torch.from_numpy(q).to(dev), torch.from_numpy(kn.view(np.int16)).to(dev),
+                     torch.from_numpy(vn.view(np.int16)).to(dev))
+        st = s.state()
+        tok = st["token_ids"].cpu().numpy().view(np.uint32)
+        ntok = st["n_tokens"].cpu().numpy()
+        go = out.cpu().numpy()
+        rec = np.arange(labeled_end, n_ctx, dtype=np.uint32)
+        for u in range(U):
+            cents, labels = models[u]
+            for r in range(G):
+                hq = u * G + r
+                sel = P.select_tokens(q[hq], cents, labels, 16, B, rec)
+                assert np.array_equal(tok[hq, : ntok[hq]], sel.token_ids), (t, u, r)
+                sizes, _, _ = P.build_index(labels, cents.shape[0])
+                caches[hq].lookup_and_update(np.sort(sel.taken_clusters), sizes)
+                oo, _ = P.approx_attention(q[hq], Kc[u][:n_ctx], Vc[u][:n_ctx], sel.token_ids)
+                assert np.abs(go[hq] - oo).max() <= 2e-5 * np.abs(Vc[u][:n_ctx]).max()
+        # append + decode-batch clustering (harness.hpp:318-337)
+        for u in range(U):
+            Kc[u] = np.concatenate([Kc[u], heads[u]["dK"][t:t + 1]])
+            Vc[u] = np.concatenate([Vc[u], heads[u]["dV"][t:t + 1]])
+        n_ctx += 1
+        if n_ctx - labeled_end == m:
+            for u in range(U):
+                cents, labels = models[u]
+                seed = P.mix_seed(0, u // kvh, u % kvh)
+                c2, l2, _ = P.cluster_decode_batch(cents, labels, Kc[u][labeled_end:n_ctx],
+                                                   OCfg(seed=seed, decode_batch=m))
+                models[u] = [c2, l2]
+            labeled_end = n_ctx
+    # device model after the decode clustering events equals the oracle's
+    st = s.state()
+    for u in range(U):
+        cents, labels = models[u]
+        nc = int(st["n_clusters"][u].item())
+        assert nc == cents.shape[0]
+        assert np.array_equal(st["centroids"][u, :nc].cpu().numpy().view(np.uint32),
+                              cents.view(np.uint32))
+        assert np.array_equal(st["labels"][u, :labeled_end].cpu().numpy(), labels)
+    ctr = s.cache_counters()
+    for hq in range(U * G):
+        assert [int(x) for x in ctr[hq]] == [int(x) for x in caches[hq].counters()]
