@@ -127,25 +127,33 @@ def fill_kv(torch, dev, g, centers, K, V, L, chunk=16):
                            .to(torch.bfloat16).view(torch.int16))
 
 
-def gen_decode(torch, dev, g, centers, G, T, drift=0.15):
-    """queries [T, U*G, D] f32 (bf16-representable), new k/v [T, U, D] bf16 bits."""
+def gen_decode(torch, dev, g, centers, G, T, drift=0.15, T_gen=256):
+    """queries [T, U*G, D] f32 (bf16-representable), new k/v [T, U, D] bf16 bits.
+
+    One drifting query walk of T_gen = 256 steps per kv unit (the trace's
+    decode_len); q head r of a group reads walk row (t + r*T_gen/G) % T_gen,
+    the GQA mapping of SURVEY §8d."""
     U, NC, _ = centers.shape
     q_scale = 2.0 * math.sqrt(D)
-    u = centers[torch.arange(U, device=dev), torch.randint(0, NC, (U,), device=dev, generator=g)]
-    u = u[:, None, :].expand(U, G, D).clone()
-    retarget = max(1, T // (2 * NC))
-    qs = []
+    ar = torch.arange(U, device=dev)
+    u = centers[ar, torch.randint(0, NC, (U,), device=dev, generator=g)]
+    retarget = max(1, T_gen // (2 * NC))
+    walk = []
     tgt = None
-    for t in range(T):
+    for t in range(T_gen):
         if t % retarget == 0:
-            tgt = centers[torch.arange(U, device=dev)[:, None],
-                          torch.randint(0, NC, (U, G), device=dev, generator=g)]
-        u = u + drift * (tgt - u) + 0.25 * drift * torch.randn(U, G, D, device=dev, generator=g)
+            tgt = centers[ar, torch.randint(0, NC, (U,), device=dev, generator=g)]
+        u = u + drift * (tgt - u) + 0.25 * drift * torch.randn(U, D, device=dev, generator=g)
         u = u / u.norm(dim=-1, keepdim=True)
-        qs.append((q_scale * u).reshape(U * G, D))
-    q = torch.stack(qs).to(torch.bfloat16).float().contiguous()
+        walk.append(q_scale * u)
+    walk = torch.stack(walk)  # [T_gen, U, D]
+    rows = (torch.arange(T, device=dev)[:, None] + torch.arange(G, device=dev)[None, :] *
+            (T_gen // G)) % T_gen  # [T, G]
+    q = walk[rows]  # [T, G, U, D]
+    q = q.permute(0, 2, 1, 3).reshape(T, U * G, D)
+    q = q.to(torch.bfloat16).float().contiguous()
     idx = torch.randint(0, NC, (T, U), device=dev, generator=g)
-    c = centers[torch.arange(U, device=dev)[None, :].expand(T, U), idx]
+    c = centers[ar[None, :].expand(T, U), idx]
     kn = c + 0.15 * torch.randn(T, U, D, device=dev, generator=g)
     kn = (kn / kn.norm(dim=-1, keepdim=True)).to(torch.bfloat16).view(torch.int16).contiguous()
     vn = torch.randn(T, U, D, device=dev, generator=g).to(torch.bfloat16).view(torch.int16)
@@ -183,8 +191,13 @@ def layer_sample_from_device(torch, sess, U_layer, G, L, q0):
         cents.append(np.ascontiguousarray(st["centroids"][u, :n].cpu().numpy()))
         ncl.append(n)
         labels.append(np.ascontiguousarray(st["labels"][u, :L].cpu().numpy()))
-        K.append(np.ascontiguousarray(bf(sess.K[u, :L]).cpu().numpy()))
-        V.append(np.ascontiguousarray(bf(sess.V[u, :L]).cpu().numpy()))
+        # the store is cluster-major after prefill: scatter back to positions
+        srt = st["sorted_ids"][u, : L - 16].to(torch.int64)
+        for store, dst in ((sess.K, K), (sess.V, V)):
+            pos = torch.empty((L, D), dtype=torch.int16, device=store.device)
+            pos[:16] = store[u, :16]
+            pos[srt] = store[u, 16:L]
+            dst.append(np.ascontiguousarray(bf(pos).cpu().numpy()))
     qs = np.ascontiguousarray(q0[: U_layer * G].cpu().numpy())
     return cents, np.array(ncl, np.uint32), labels, K, V, qs
 
@@ -273,6 +286,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exact-kmeans", action="store_true")
+    ap.add_argument("--max-iters", type=int, default=50,
+                    help="k-means cap (profiling only; the bench default is the reference's 50)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -296,7 +311,8 @@ def main():
     G, L, B = args.group, args.L, args.budget
     T = args.warmup + args.steps + args.e2e_steps + 2
     ctx = Context(local)
-    sess = Session(U, G, L, T, B, retention=1, cfg=ClusterConfig(), kv_heads=args.kv_heads,
+    sess = Session(U, G, L, T, B, retention=1, cfg=ClusterConfig(max_iters=args.max_iters),
+                   kv_heads=args.kv_heads,
                    flags=N.CKV_KM_EXACT_ONLY if args.exact_kmeans else 0, ctx=ctx)
     g, centers = gen_inputs(torch, dev, U, G, L, T, seed=7 + rank)
     fill_kv(torch, dev, g, centers, sess.K, sess.V, L)
@@ -326,17 +342,28 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    l0 = ctx.launches
+    soak_out = torch.empty_like(out)
+
+    def soak(seconds):  # keeps the GPU busy so nvidia-smi samples loaded clocks
+        t_end = time.time() + seconds
+        while time.time() < t_end:
+            for _ in range(20):
+                sess.attend_only(q_all[0], soak_out)
+            torch.cuda.synchronize()
+
     with ClockSampler(local) as clk:
+        soak(0.4)
+        l0 = ctx.launches
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record()
         for _ in range(args.steps):
             sess.step(q_all[t], kn_all[t], vn_all[t], out)
             t += 1
         ev[1].record()
+        launches = ctx.launches - l0
         torch.cuda.synchronize()
+        soak(0.2)
     step_ms = ev[0].elapsed_time(ev[1]) / args.steps
-    launches = ctx.launches - l0
     if world > 1:
         tt = torch.tensor([step_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -365,7 +392,7 @@ def main():
     select_bytes = cent_bytes + n_taken_tok * 4 * 2 + n_q * D * 4
     step_bytes_unique = attend_bytes_unique + select_bytes
 
-    sd = N.SelectDesc(n_q, G, B, 16, sess.p_cap, c_cap, sel_cap, rec_begin, rec_end, 0)
+    sd = N.SelectDesc(n_q, G, B, 16, sess.p_cap, c_cap, sel_cap, rec_begin, rec_end, 0, 16)
     ad = N.AttendDesc(n_q, G, sess.p_cap, sel_cap, min(B, rec_begin) + 16 + (rec_end - rec_begin))
     st_ptrs = [C.c_void_p() for _ in range(8)]
     cc, scap = C.c_uint32(), C.c_uint32()
@@ -374,6 +401,7 @@ def main():
     ntk = torch.empty(n_q, dtype=torch.int32, device=dev)
     trm = torch.empty(n_q, dtype=torch.int32, device=dev)
     tok2 = torch.empty((n_q, sel_cap), dtype=torch.int32, device=dev)
+    rows2 = torch.empty((n_q, sel_cap), dtype=torch.int32, device=dev)
     nt2 = torch.empty(n_q, dtype=torch.int32, device=dev)
     qd = q_all[t - 1].contiguous()
     reps = 10
@@ -382,11 +410,11 @@ def main():
         evs[3 * i].record()
         N.check(N.lib().ckv_select(ctx.h, C.byref(sd), qd.data_ptr(), st_ptrs[0], st_ptrs[2],
                                    st_ptrs[3], st_ptrs[4], st_ptrs[5], tok2.data_ptr(),
-                                   nt2.data_ptr(), ntk.data_ptr(), trm.data_ptr(),
-                                   ranked.data_ptr(), None, None))
+                                   rows2.data_ptr(), nt2.data_ptr(), ntk.data_ptr(),
+                                   trm.data_ptr(), ranked.data_ptr(), None, None))
         evs[3 * i + 1].record()
         N.check(N.lib().ckv_attend(ctx.h, C.byref(ad), qd.data_ptr(), sess.K.data_ptr(),
-                                   sess.V.data_ptr(), tok2.data_ptr(), nt2.data_ptr(),
+                                   sess.V.data_ptr(), rows2.data_ptr(), nt2.data_ptr(),
                                    out.data_ptr(), None))
         evs[3 * i + 2].record()
     torch.cuda.synchronize()

@@ -46,7 +46,7 @@ typedef struct ckv_session ckv_session;
 /* ------------------------------------------------------------------ */
 /* context                                                             */
 /* ------------------------------------------------------------------ */
-/* stream: a cudaStream_t to launch on, or NULL for a private stream.
+/* stream: the cudaStream_t to launch on; NULL = the legacy default stream.
  * A context is single-threaded; use one context per host thread
  * (the reference calls the hot path concurrently per head,
  * harness.hpp:362-378). */
@@ -162,14 +162,19 @@ typedef struct {
   uint32_t rec_begin;  /* recency positions [rec_begin, rec_end)         */
   uint32_t rec_end;    /*   appended after the sinks (harness.hpp:246)   */
   uint32_t flags;      /* CKV_SEL_* below                                */
+  uint32_t row_base;   /* cluster-major store: sorted entry j is row
+                          row_base + j (= the sink count); see `rows`    */
 } ckv_select_desc;
 
 #define CKV_SEL_FULL_RANK 1u  /* write ranked_clusters for every cluster   */
 #define CKV_SEL_SCORES 2u     /* write the f64 scores (score_clusters)     */
 
-/* score_clusters + select_tokens for n_q queries in one launch.
+/* score_clusters + select_tokens for n_q queries (two launches).
  * q: device f32 [n_q][128]; outputs device:
- *   token_ids [n_q][sel_cap], n_tokens [n_q], n_taken [n_q],
+ *   token_ids [n_q][sel_cap]: I_T positions (selection.hpp:91-109), or NULL;
+ *   rows [n_q][sel_cap]: the same entries as rows of a cluster-major KV
+ *     store (row_base + index position for cluster tokens, the position for
+ *     sinks / recency), or NULL;  n_tokens [n_q], n_taken [n_q],
  *   trimmed [n_q], ranked [n_q][c_cap] (FULL_RANK: all C; otherwise
  *   at least the taken prefix), scores [n_q][c_cap] (SCORES) or NULL.
  * cache: NULL, or a cache with n_q slots — then each q head's taken
@@ -177,8 +182,8 @@ typedef struct {
 int ckv_select(ckv_ctx* ctx, const ckv_select_desc* desc, const float* q,
                const float* centroids, const uint32_t* n_clusters, const uint32_t* sizes,
                const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
-               uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked,
-               double* scores, ckv_cache* cache);
+               uint32_t* rows, uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed,
+               uint32_t* ranked, double* scores, ckv_cache* cache);
 
 /* ClusterCache with n_slots independent caches of retention R over at
  * most c_cap cluster ids (bitmap ring).  cache.hpp:25-36. */
@@ -206,13 +211,15 @@ typedef struct {
 } ckv_attend_desc;
 
 /* approx_attention for n_q queries: softmax(q K[I]^T / sqrt(d)) V[I]
- * over I = token_ids[h][0:n_tokens[h]], split-K flash-decode with an
+ * over I = rows[h][0:n_tokens[h]] — rows of K / V: positions for a
+ * position-ordered store, ckv_select's `rows` for a cluster-major one —
+ * split-K flash-decode with an
  * LSE merge.  K, V: device bf16 [unit][p_cap][128].  out: device f32
  * [n_q][128].  weights: device f32 [n_q][sel_cap] in I order, or NULL.
  * An empty selection is CKV_EINVAL (attention.hpp:66-67) and is checked
  * on the host copy of n_tokens only when weights != NULL (parity mode). */
 int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* desc, const float* q, const uint16_t* K,
-               const uint16_t* V, const uint32_t* token_ids, const uint32_t* n_tokens,
+               const uint16_t* V, const uint32_t* rows, const uint32_t* n_tokens,
                float* out, float* weights);
 
 /* ------------------------------------------------------------------ */
@@ -237,7 +244,11 @@ typedef struct {
 int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* desc, ckv_session** out);
 int ckv_session_destroy(ckv_session* s);
 /* Device pointers of the session's KV store (bf16 [unit][p_cap][128]),
- * so callers can fill the prompt KV in place. */
+ * so callers can fill the prompt KV in place.  The store is position-
+ * ordered until ckv_session_prefill, which relays it cluster-major (rows
+ * [0,sink) sinks, [sink, labeled_end) tokens in index order, then the
+ * unclustered recency positions) into NEW buffers: query the pointers
+ * again after prefill. */
 int ckv_session_kv(ckv_session* s, uint16_t** K, uint16_t** V, uint32_t* p_cap);
 /* Upload prompt KV from HOST bf16 [unit][L][128]. */
 int ckv_session_load_prompt(ckv_session* s, const uint16_t* K_host, const uint16_t* V_host);

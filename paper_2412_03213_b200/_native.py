@@ -42,7 +42,7 @@ class DecodeClusterDesc(C.Structure):
 class SelectDesc(C.Structure):
     _fields_ = [("n_q", u32), ("group", u32), ("budget", u32), ("sink_count", u32),
                 ("p_cap", u32), ("c_cap", u32), ("sel_cap", u32), ("rec_begin", u32),
-                ("rec_end", u32), ("flags", u32)]
+                ("rec_end", u32), ("flags", u32), ("row_base", u32)]
 
 
 class AttendDesc(C.Structure):
@@ -85,7 +85,7 @@ SIGNATURES = {
                                            vp]),
     "ckv_build_index": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp]),
     "ckv_select": (C.c_int, [vp, C.POINTER(SelectDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                             vp, vp, vp]),
+                             vp, vp, vp, vp]),
     "ckv_cache_create": (C.c_int, [vp, u32, u32, u32, u32, C.POINTER(vp)]),
     "ckv_cache_destroy": (C.c_int, [vp]),
     "ckv_cache_counters": (C.c_int, [vp, vp]),

@@ -317,11 +317,11 @@ def _select(ctx, q, model, index, budget, recency, want_scores=False):
     rnk = torch.zeros(dm.c_cap, dtype=torch.int32, device=dev)
     sc = torch.zeros(dm.c_cap, dtype=torch.float64, device=dev) if want_scores else None
     desc = N.SelectDesc(1, 1, budget, model.sink_count, dm.p_cap, dm.c_cap, sel_cap, 0, 0,
-                        N.CKV_SEL_FULL_RANK | (N.CKV_SEL_SCORES if want_scores else 0))
+                        N.CKV_SEL_FULL_RANK | (N.CKV_SEL_SCORES if want_scores else 0), 0)
     check(lib().ckv_select(ctx.h, C.byref(desc), qd.data_ptr(), dm.cents.data_ptr(),
                            dm.ncl.data_ptr(), dm.sizes.data_ptr(), dm.starts.data_ptr(),
-                           dm.sorted.data_ptr(), tok.data_ptr(), ntok.data_ptr(), ntk.data_ptr(),
-                           trm.data_ptr(), rnk.data_ptr(), _ptr(sc), None))
+                           dm.sorted.data_ptr(), tok.data_ptr(), None, ntok.data_ptr(),
+                           ntk.data_ptr(), trm.data_ptr(), rnk.data_ptr(), _ptr(sc), None))
     n = int(ntok.item())
     ids = np.concatenate([tok.cpu().numpy().view(np.uint32)[:n], rec]).astype(np.uint32)
     res = SelectionResult(rnk.cpu().numpy().view(np.uint32)[: model.n_clusters],

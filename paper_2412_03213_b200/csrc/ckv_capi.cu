@@ -102,6 +102,49 @@ __global__ void k_append_kv(const uint16_t* __restrict__ kn, const uint16_t* __r
   reinterpret_cast<uint4*>(V + (size_t(u) * p_cap + pos) * D)[j] = vs[j];
 }
 
+// cluster-major relayout of the prompt KV (after the prefill index):
+// dst row r = src position  r              for r < sink or r >= labeled_end
+//                           sorted[r-sink] for sink <= r < labeled_end
+__global__ void k_relayout(const uint16_t* __restrict__ K, const uint16_t* __restrict__ V,
+                           uint16_t* __restrict__ K2, uint16_t* __restrict__ V2,
+                           const uint32_t* __restrict__ sorted, uint32_t p_cap, uint32_t sink,
+                           uint32_t labeled_end, uint32_t n_ctx) {
+  const uint32_t u = blockIdx.y;
+  const uint32_t r = blockIdx.x * 8 + (threadIdx.x >> 4);  // 16 threads x 16 B per row
+  const uint32_t j = threadIdx.x & 15;
+  if (r >= n_ctx) return;
+  uint32_t src = r;
+  if (r >= sink && r < labeled_end) src = __ldg(sorted + size_t(u) * p_cap + (r - sink));
+  const size_t base = size_t(u) * p_cap;
+  reinterpret_cast<uint4*>(K2 + (base + r) * D)[j] =
+      __ldg(reinterpret_cast<const uint4*>(K + (base + src) * D) + j);
+  reinterpret_cast<uint4*>(V2 + (base + r) * D)[j] =
+      __ldg(reinterpret_cast<const uint4*>(V + (base + src) * D) + j);
+}
+
+// relayout of one clustered decode batch: rows [le0, le0+m) get the batch's
+// tokens in index order (sorted entries le0-sink .. le0-sink+m-1)
+__global__ void k_relayout_batch(uint16_t* __restrict__ K, uint16_t* __restrict__ V,
+                                 uint16_t* __restrict__ tK, uint16_t* __restrict__ tV,
+                                 const uint32_t* __restrict__ sorted, uint32_t p_cap,
+                                 uint32_t sink, uint32_t le0, uint32_t m) {
+  const uint32_t u = blockIdx.x;
+  const size_t base = size_t(u) * p_cap;
+  uint4* tk = reinterpret_cast<uint4*>(tK + size_t(u) * m * D);
+  uint4* tv = reinterpret_cast<uint4*>(tV + size_t(u) * m * D);
+  for (uint32_t e = threadIdx.x; e < m * 16; e += blockDim.x) {
+    tk[e] = reinterpret_cast<const uint4*>(K + (base + le0) * D)[e];
+    tv[e] = reinterpret_cast<const uint4*>(V + (base + le0) * D)[e];
+  }
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e < m * 16; e += blockDim.x) {
+    const uint32_t r = e >> 4, j = e & 15;
+    const uint32_t src = sorted[base + (le0 - sink) + r] - le0;
+    reinterpret_cast<uint4*>(K + (base + le0 + r) * D)[j] = tk[src * 16 + j];
+    reinterpret_cast<uint4*>(V + (base + le0 + r) * D)[j] = tv[src * 16 + j];
+  }
+}
+
 }  // namespace ckvb
 
 using namespace ckvb;
@@ -118,13 +161,9 @@ int ckv_ctx_create(int device, void* stream, ckv_ctx** out) {
   CKV_CUDA_TRY(cudaSetDevice(device));
   ckv_ctx* c = new ckv_ctx();
   c->device = device;
-  if (stream) {
-    c->stream = static_cast<cudaStream_t>(stream);
-  } else {
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) { delete c; return cuda_status(e, "cudaStreamCreate"); }
-    c->own_stream = true;
-  }
+  // NULL is the CUDA legacy default stream (torch's default stream too), so
+  // work launched here is ordered with the caller's default-stream work.
+  c->stream = static_cast<cudaStream_t>(stream);
   *out = c;
   return CKV_OK;
 }
@@ -349,19 +388,22 @@ static CacheDev null_cache() {
 
 int ckv_select(ckv_ctx* ctx, const ckv_select_desc* d, const float* q, const float* centroids,
                const uint32_t* n_clusters, const uint32_t* sizes, const uint32_t* starts,
-               const uint32_t* sorted_ids, uint32_t* token_ids, uint32_t* n_tokens,
-               uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
-               ckv_cache* cache) {
+               const uint32_t* sorted_ids, uint32_t* token_ids, uint32_t* rows,
+               uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked,
+               double* scores, ckv_cache* cache) {
   if (!ranked) { set_error("ckv_select: ranked buffer required"); return CKV_EINVAL; }
   if (cache && cache->dev.n_slots < d->n_q) {
     set_error("ckv_select: cache has fewer slots than q heads");
     return CKV_EINVAL;
   }
-  CKV_TRY(launch_select(ctx->stream, *d, q, centroids, n_clusters, sizes, starts, sorted_ids,
-                        token_ids, n_tokens, n_taken, trimmed, ranked, scores,
-                        cache ? cache->dev : null_cache()));
-  ctx->launches++;
-  return CKV_OK;
+  void* scratch = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&scratch, select_scratch_bytes(d->n_q, d->c_cap), ctx->stream));
+  int rc = launch_select(ctx->stream, *d, q, centroids, n_clusters, sizes, starts, sorted_ids,
+                         token_ids, rows, d->row_base, n_tokens, n_taken, trimmed, ranked, scores,
+                         cache ? cache->dev : null_cache(), scratch);
+  cudaFreeAsync(scratch, ctx->stream);
+  ctx->launches += 2;
+  return rc;
 }
 
 int ckv_cache_create(ckv_ctx* ctx, uint32_t n_slots, uint32_t c_cap, uint32_t retention,
@@ -472,8 +514,10 @@ struct ckv_session {
   float* cents = nullptr;
   int32_t* labels = nullptr;
   uint32_t *n_clusters = nullptr, *sizes = nullptr, *starts = nullptr, *sorted = nullptr;
-  uint32_t *token_ids = nullptr, *n_tokens = nullptr, *n_taken = nullptr, *trimmed = nullptr,
-           *ranked = nullptr;
+  uint32_t *token_ids = nullptr, *rows = nullptr, *n_tokens = nullptr, *n_taken = nullptr,
+           *trimmed = nullptr, *ranked = nullptr;
+  void* sel_scratch = nullptr;
+  uint16_t *tmpK = nullptr, *tmpV = nullptr;  // decode-batch relayout staging
   float* part = nullptr;
   uint32_t* tickets = nullptr;
   float *q_dev = nullptr, *out_dev = nullptr;
@@ -521,6 +565,11 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   rc |= salloc(&s->starts, size_t(s->U) * (s->c_cap + 1));
   rc |= salloc(&s->sorted, size_t(s->U) * s->p_cap);
   rc |= salloc(&s->token_ids, size_t(s->n_q) * s->sel_cap);
+  rc |= salloc(&s->rows, size_t(s->n_q) * s->sel_cap);
+  rc |= salloc(reinterpret_cast<unsigned char**>(&s->sel_scratch),
+               select_scratch_bytes(s->n_q, s->c_cap));
+  rc |= salloc(&s->tmpK, size_t(s->U) * d->decode_batch * D);
+  rc |= salloc(&s->tmpV, size_t(s->U) * d->decode_batch * D);
   rc |= salloc(&s->n_tokens, s->n_q);
   rc |= salloc(&s->n_taken, s->n_q);
   rc |= salloc(&s->trimmed, s->n_q);
@@ -554,7 +603,8 @@ int ckv_session_destroy(ckv_session* s) {
   cudaStreamSynchronize(s->ctx->stream);
   cudaFree(s->K); cudaFree(s->V); cudaFree(s->cents); cudaFree(s->labels);
   cudaFree(s->n_clusters); cudaFree(s->sizes); cudaFree(s->starts); cudaFree(s->sorted);
-  cudaFree(s->token_ids); cudaFree(s->n_tokens); cudaFree(s->n_taken); cudaFree(s->trimmed);
+  cudaFree(s->token_ids); cudaFree(s->rows); cudaFree(s->sel_scratch); cudaFree(s->tmpK);
+  cudaFree(s->tmpV); cudaFree(s->n_tokens); cudaFree(s->n_taken); cudaFree(s->trimmed);
   cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
   cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
   ckv_cache_destroy(s->cache);
@@ -595,6 +645,26 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
   s->C_cur = ckv_prefill_cluster_count(pd.L, pd.c0_divisor, pd.sink_tokens, 0);
   CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
                           s->n_clusters, s->sizes, s->starts, s->sorted));
+  // relay the KV store cluster-major: row sink + j <- position sorted[j]
+  const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
+  const uint32_t N = s->labeled_end - sink;
+  if (N > 0) {
+    uint16_t *K2 = nullptr, *V2 = nullptr;
+    const size_t kv = size_t(s->U) * s->p_cap * D;
+    CKV_TRY(salloc(&K2, kv));
+    int rc = salloc(&V2, kv);
+    if (rc) { cudaFree(K2); return rc; }
+    dim3 g((s->p_cap + 7) / 8, s->U);
+    k_relayout<<<g, 128, 0, s->ctx->stream>>>(s->K, s->V, K2, V2, s->sorted, s->p_cap, sink,
+                                              s->labeled_end, s->n_ctx);
+    CKV_LAUNCH_CHECK("k_relayout");
+    s->ctx->launches++;
+    CKV_CUDA_TRY(cudaStreamSynchronize(s->ctx->stream));
+    cudaFree(s->K);
+    cudaFree(s->V);
+    s->K = K2;
+    s->V = V2;
+  }
   s->prefilled = true;
   return ckv_ctx_sync(s->ctx);
 }
@@ -611,18 +681,20 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
   sd.rec_begin = s->labeled_end;
   sd.rec_end = s->n_ctx;
   sd.flags = 0;
+  sd.row_base = sd.sink_count;
   CKV_TRY(launch_select(s->ctx->stream, sd, q_dev, s->cents, s->n_clusters, s->sizes, s->starts,
-                        s->sorted, s->token_ids, s->n_tokens, s->n_taken, s->trimmed, s->ranked,
-                        nullptr, s->cache ? s->cache->dev : null_cache()));
+                        s->sorted, s->token_ids, s->rows, sd.row_base, s->n_tokens, s->n_taken,
+                        s->trimmed, s->ranked, nullptr,
+                        s->cache ? s->cache->dev : null_cache(), s->sel_scratch));
   ckv_attend_desc ad{};
   ad.n_q = s->n_q;
   ad.group = s->d.group;
   ad.p_cap = s->p_cap;
   ad.sel_cap = s->sel_cap;
   ad.max_tokens = std::min(s->d.budget, s->labeled_end) + sd.sink_count + (s->n_ctx - s->labeled_end);
-  CKV_TRY(launch_attend(s->ctx->stream, ad, q_dev, s->K, s->V, s->token_ids, s->n_tokens,
+  CKV_TRY(launch_attend(s->ctx->stream, ad, q_dev, s->K, s->V, s->rows, s->n_tokens,
                         out_dev, nullptr, nullptr, s->part, s->tickets));
-  s->ctx->launches += 2;
+  s->ctx->launches += 3;
   return CKV_OK;
 }
 
@@ -667,11 +739,18 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
     dd.max_iters = s->d.max_iters;
     CKV_TRY(ckv_cluster_decode_batch(s->ctx, &dd, s->K, s->seeds.data(), s->cents, s->labels,
                                      s->n_clusters, nullptr));
-    s->labeled_end += s->pending;
-    s->C_cur += std::min(s->d.c_plus, s->pending);
+    const uint32_t le0 = s->labeled_end, m = s->pending;
+    s->labeled_end += m;
+    s->C_cur += std::min(s->d.c_plus, m);
     s->pending = 0;
     CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
                             s->n_clusters, s->sizes, s->starts, s->sorted));
+    // relay the batch's rows [le0, le0+m) into index order (in place via staging)
+    const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
+    k_relayout_batch<<<s->U, 256, 0, st>>>(s->K, s->V, s->tmpK, s->tmpV, s->sorted, s->p_cap,
+                                           sink, le0, m);
+    CKV_LAUNCH_CHECK("k_relayout_batch");
+    s->ctx->launches++;
   }
   if (!on_device) {
     CKV_CUDA_TRY(cudaMemcpyAsync(out, s->out_dev, size_t(s->n_q) * D * 4, cudaMemcpyDeviceToHost,

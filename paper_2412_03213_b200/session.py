@@ -49,13 +49,18 @@ class Session:
         h = C.c_void_p()
         check(lib().ckv_session_create(self.ctx.h, C.byref(desc), C.byref(h)))
         self.h = h
+        self._refresh_kv()
+        self.prompt_len = prompt_len
+
+    def _refresh_kv(self):
+        """(Re)bind torch views of the KV store; prefill relays it
+        cluster-major into new buffers."""
         Kp, Vp, pc = C.c_void_p(), C.c_void_p(), C.c_uint32()
         check(lib().ckv_session_kv(self.h, C.byref(Kp), C.byref(Vp), C.byref(pc)))
         self.p_cap = pc.value
         dev = self.ctx.device
-        self.K = device_view(Kp.value, (n_units, self.p_cap, D), torch.int16, dev)
-        self.V = device_view(Vp.value, (n_units, self.p_cap, D), torch.int16, dev)
-        self.prompt_len = prompt_len
+        self.K = device_view(Kp.value, (self.n_units, self.p_cap, D), torch.int16, dev)
+        self.V = device_view(Vp.value, (self.n_units, self.p_cap, D), torch.int16, dev)
 
     def __del__(self):
         try:
@@ -73,6 +78,7 @@ class Session:
     def prefill(self):
         info = (N.KMeansInfo * self.n_units)()
         check(lib().ckv_session_prefill(self.h, info))
+        self._refresh_kv()
         return [(i.iterations_used, bool(i.converged)) for i in info]
 
     def step(self, q, k_new, v_new, out=None, on_device: bool = True):
