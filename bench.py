@@ -372,26 +372,10 @@ def main():
 
     # ---- per-kernel timing of one step's select and attend --------------
     st = sess.state()
-    ntok = st["n_tokens"].to(torch.int64)
-    tok = st["token_ids"]
     sel_cap, c_cap = st["sel_cap"], st["c_cap"]
     ncl = st["n_clusters"].to(torch.int64)
     stats = sess.stats()
     rec_begin, rec_end = stats.labeled_end, stats.n_ctx
-    nq_tok = int(ntok.sum().item())
-    # unique rows per kv unit (the q heads of a group share their unit's KV)
-    uniq = 0
-    for u in range(U):
-        rows = torch.cat([tok[u * G + r, : int(ntok[u * G + r].item())] for r in range(G)])
-        uniq += int(torch.unique(rows).numel())
-    n_taken_tok = nq_tok - n_q * 16 - n_q * (rec_end - rec_begin)
-    cent_bytes = int(ncl.sum().item()) * D * 4 + int(ncl.sum().item()) * 8
-    qo_bytes = n_q * D * 8
-    attend_bytes_unique = uniq * D * 2 * 2 + nq_tok * 4 + qo_bytes
-    attend_bytes_perq = nq_tok * D * 2 * 2 + nq_tok * 4 + qo_bytes
-    select_bytes = cent_bytes + n_taken_tok * 4 * 2 + n_q * D * 4
-    step_bytes_unique = attend_bytes_unique + select_bytes
-
     sd = N.SelectDesc(n_q, G, B, 16, sess.p_cap, c_cap, sel_cap, rec_begin, rec_end, 0, 16)
     ad = N.AttendDesc(n_q, G, sess.p_cap, sel_cap, min(B, rec_begin) + 16 + (rec_end - rec_begin))
     st_ptrs = [C.c_void_p() for _ in range(8)]
@@ -400,21 +384,44 @@ def main():
     ranked = torch.empty((n_q, c_cap), dtype=torch.int32, device=dev)
     ntk = torch.empty(n_q, dtype=torch.int32, device=dev)
     trm = torch.empty(n_q, dtype=torch.int32, device=dev)
-    tok2 = torch.empty((n_q, sel_cap), dtype=torch.int32, device=dev)
     rows2 = torch.empty((n_q, sel_cap), dtype=torch.int32, device=dev)
+    run_cap = c_cap + 2
+    run_row = torch.empty((n_q, run_cap), dtype=torch.int32, device=dev)
+    run_off = torch.empty((n_q, run_cap + 1), dtype=torch.int32, device=dev)
+    run_cnt = torch.empty(n_q, dtype=torch.int32, device=dev)
+    runs = N.Runs(run_row.data_ptr(), run_off.data_ptr(), run_cnt.data_ptr(), run_cap)
     nt2 = torch.empty(n_q, dtype=torch.int32, device=dev)
     qd = q_all[t - 1].contiguous()
+
+    def select(rows_ptr=None):
+        N.check(N.lib().ckv_select(ctx.h, C.byref(sd), qd.data_ptr(), st_ptrs[0], st_ptrs[2],
+                                   st_ptrs[3], st_ptrs[4], st_ptrs[5], None, rows_ptr,
+                                   C.byref(runs), nt2.data_ptr(), ntk.data_ptr(),
+                                   trm.data_ptr(), ranked.data_ptr(), None, None))
+
+    # byte accounting from one untimed selection with per-entry rows
+    select(rows2.data_ptr())
+    ntok = nt2.to(torch.int64)
+    nq_tok = int(ntok.sum().item())
+    uniq = 0  # unique (kv unit, row) pairs: the q heads of a group share their unit's KV
+    for u in range(U):
+        rr = torch.cat([rows2[u * G + r, : int(ntok[u * G + r].item())] for r in range(G)])
+        uniq += int(torch.unique(rr).numel())
+    n_runs = int(run_cnt.sum().item())
+    n_cl = int(ncl.sum().item())
+    qo_bytes = n_q * D * 8
+    attend_bytes_unique = uniq * D * 2 * 2 + n_runs * 8 + qo_bytes
+    attend_bytes_perq = nq_tok * D * 2 * 2 + n_runs * 8 + qo_bytes
+    select_bytes = n_cl * D * 4 + n_cl * 8 + n_runs * 8 + n_q * D * 4
+    step_bytes_unique = attend_bytes_unique + select_bytes
     reps = 10
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(3 * reps)]
     for i in range(reps):
         evs[3 * i].record()
-        N.check(N.lib().ckv_select(ctx.h, C.byref(sd), qd.data_ptr(), st_ptrs[0], st_ptrs[2],
-                                   st_ptrs[3], st_ptrs[4], st_ptrs[5], tok2.data_ptr(),
-                                   rows2.data_ptr(), nt2.data_ptr(), ntk.data_ptr(),
-                                   trm.data_ptr(), ranked.data_ptr(), None, None))
+        select()
         evs[3 * i + 1].record()
         N.check(N.lib().ckv_attend(ctx.h, C.byref(ad), qd.data_ptr(), sess.K.data_ptr(),
-                                   sess.V.data_ptr(), rows2.data_ptr(), nt2.data_ptr(),
+                                   sess.V.data_ptr(), None, C.byref(runs), nt2.data_ptr(),
                                    out.data_ptr(), None))
         evs[3 * i + 2].record()
     torch.cuda.synchronize()
@@ -494,7 +501,7 @@ def main():
                      "unit": "GB/s", "frac": att_gbs / hbm, "traffic": None,
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": attend_bytes_unique,
-                     "bytes_rule": "unique (kv unit, row) K+V bf16 rows + token ids + q/out",
+                     "bytes_rule": "unique (kv unit, row) K+V bf16 rows + I_T runs + q/out",
                      "launch_us": att_ms * 1e3},
         "step_roofline": {"achieved_gbs": step_bytes_unique / (step_ms * 1e-3) / 1e9,
                           "frac": step_bytes_unique / (step_ms * 1e-3) / 1e9 / hbm,

@@ -169,21 +169,36 @@ typedef struct {
 #define CKV_SEL_FULL_RANK 1u  /* write ranked_clusters for every cluster   */
 #define CKV_SEL_SCORES 2u     /* write the f64 scores (score_clusters)     */
 
-/* score_clusters + select_tokens for n_q queries (two launches).
- * q: device f32 [n_q][128]; outputs device:
- *   token_ids [n_q][sel_cap]: I_T positions (selection.hpp:91-109), or NULL;
- *   rows [n_q][sel_cap]: the same entries as rows of a cluster-major KV
- *     store (row_base + index position for cluster tokens, the position for
- *     sinks / recency), or NULL;  n_tokens [n_q], n_taken [n_q],
- *   trimmed [n_q], ranked [n_q][c_cap] (FULL_RANK: all C; otherwise
- *   at least the taken prefix), scores [n_q][c_cap] (SCORES) or NULL.
- * cache: NULL, or a cache with n_q slots — then each q head's taken
- * clusters (sorted) go through ClusterCache::lookup_and_update, fused. */
+/* I_T as runs of consecutive KV-store rows (the cluster-major store makes
+ * every taken cluster one run; sinks and the recency window are one run
+ * each): run r covers I_T entries [off[r], off[r+1]) at store rows
+ * row[r] + (e - off[r]).  Device arrays, per q head. */
+typedef struct {
+  uint32_t* row;     /* [n_q][run_cap]                                      */
+  uint32_t* off;     /* [n_q][run_cap + 1]                                  */
+  uint32_t* count;   /* [n_q] number of runs                                */
+  uint32_t run_cap;  /* >= c_cap + 2                                        */
+} ckv_runs;
+
+/* score_clusters + select_tokens (+ the fused cache) for n_q queries, two
+ * launches.  q: device f32 [n_q][128].  Outputs (device, each optional
+ * unless noted):
+ *   token_ids [n_q][sel_cap]: I_T positions (selection.hpp:91-109);
+ *   rows [n_q][sel_cap]: the same entries as cluster-major store rows
+ *     (row_base + index position for cluster tokens, the position for
+ *     sinks / recency);
+ *   runs: I_T as store-row runs (see ckv_runs) — what ckv_attend consumes;
+ *   n_tokens, n_taken, trimmed [n_q] (required);
+ *   ranked [n_q][c_cap] (required): every cluster for CKV_SEL_FULL_RANK,
+ *     otherwise the taken prefix;
+ *   scores [n_q][c_cap] f64 (score_clusters) when CKV_SEL_SCORES.
+ * cache: NULL, or a cache with n_q slots — each q head's taken clusters go
+ * through ClusterCache::lookup_and_update (cache.hpp:38-57), fused. */
 int ckv_select(ckv_ctx* ctx, const ckv_select_desc* desc, const float* q,
                const float* centroids, const uint32_t* n_clusters, const uint32_t* sizes,
                const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
-               uint32_t* rows, uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed,
-               uint32_t* ranked, double* scores, ckv_cache* cache);
+               uint32_t* rows, const ckv_runs* runs, uint32_t* n_tokens, uint32_t* n_taken,
+               uint32_t* trimmed, uint32_t* ranked, double* scores, ckv_cache* cache);
 
 /* ClusterCache with n_slots independent caches of retention R over at
  * most c_cap cluster ids (bitmap ring).  cache.hpp:25-36. */
@@ -210,17 +225,18 @@ typedef struct {
   uint32_t max_tokens;  /* upper bound of n_tokens[] (sizes the split grid) */
 } ckv_attend_desc;
 
-/* approx_attention for n_q queries: softmax(q K[I]^T / sqrt(d)) V[I]
- * over I = rows[h][0:n_tokens[h]] — rows of K / V: positions for a
- * position-ordered store, ckv_select's `rows` for a cluster-major one —
- * split-K flash-decode with an
- * LSE merge.  K, V: device bf16 [unit][p_cap][128].  out: device f32
- * [n_q][128].  weights: device f32 [n_q][sel_cap] in I order, or NULL.
- * An empty selection is CKV_EINVAL (attention.hpp:66-67) and is checked
- * on the host copy of n_tokens only when weights != NULL (parity mode). */
+/* approx_attention for n_q queries: softmax(q K[I]^T / sqrt(d)) V[I] over
+ * I_T given either as per-entry store rows (rows [n_q][sel_cap]: positions
+ * for a position-ordered store) or as runs (ckv_select's ckv_runs for the
+ * cluster-major store; pass rows = NULL), entries 0..n_tokens[h]-1.
+ * Split-K flash-decode with an LSE merge.  K, V: device bf16
+ * [unit][p_cap][128].  out: device f32 [n_q][128].  weights: device f32
+ * [n_q][sel_cap] in I order, or NULL.  An empty selection is CKV_EINVAL
+ * (attention.hpp:66-67), checked on a host copy of n_tokens only when
+ * weights != NULL (parity mode). */
 int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* desc, const float* q, const uint16_t* K,
-               const uint16_t* V, const uint32_t* rows, const uint32_t* n_tokens,
-               float* out, float* weights);
+               const uint16_t* V, const uint32_t* rows, const ckv_runs* runs,
+               const uint32_t* n_tokens, float* out, float* weights);
 
 /* ------------------------------------------------------------------ */
 /* session: the batched serving path (simulate_head's ClusterKV branch, */
@@ -238,8 +254,14 @@ typedef struct {
                               mix_seed(cluster_seed, layer, head) with
                               unit = layer * kv_heads + head             */
   uint32_t kv_heads;       /* for the per-unit seed derivation          */
-  uint32_t flags;          /* CKV_KM_* for the prefill k-means          */
+  uint32_t flags;          /* CKV_KM_* for the prefill k-means, plus    */
+                           /* CKV_SESSION_TOKEN_IDS                     */
 } ckv_session_desc;
+
+/* Also materialise each step's I_T as reference token positions
+ * (ckv_session_state's token_ids); the attention itself consumes the run
+ * list, so this is only needed for introspection / parity checks. */
+#define CKV_SESSION_TOKEN_IDS 0x100u
 
 int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* desc, ckv_session** out);
 int ckv_session_destroy(ckv_session* s);

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libckv_b200.so")
 CKV_OK, CKV_EINVAL, CKV_ECUDA, CKV_ENOMEM, CKV_ENCCL = 0, 1, 2, 3, 4
 CKV_KM_OBJECTIVE, CKV_KM_EXACT_ONLY, CKV_KM_NO_VALIDATE = 1, 2, 4
 CKV_SEL_FULL_RANK, CKV_SEL_SCORES = 1, 2
+CKV_SESSION_TOKEN_IDS = 0x100
 
 vp, u32, u64, i32, f32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32, C.c_float
 
@@ -43,6 +44,11 @@ class SelectDesc(C.Structure):
     _fields_ = [("n_q", u32), ("group", u32), ("budget", u32), ("sink_count", u32),
                 ("p_cap", u32), ("c_cap", u32), ("sel_cap", u32), ("rec_begin", u32),
                 ("rec_end", u32), ("flags", u32), ("row_base", u32)]
+
+
+class Runs(C.Structure):
+    _fields_ = [("row", C.c_void_p), ("off", C.c_void_p), ("count", C.c_void_p),
+                ("run_cap", u32)]
 
 
 class AttendDesc(C.Structure):
@@ -84,14 +90,15 @@ SIGNATURES = {
     "ckv_cluster_decode_batch": (C.c_int, [vp, C.POINTER(DecodeClusterDesc), vp, vp, vp, vp, vp,
                                            vp]),
     "ckv_build_index": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp]),
-    "ckv_select": (C.c_int, [vp, C.POINTER(SelectDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                             vp, vp, vp, vp]),
+    "ckv_select": (C.c_int, [vp, C.POINTER(SelectDesc), vp, vp, vp, vp, vp, vp, vp, vp,
+                             C.POINTER(Runs), vp, vp, vp, vp, vp, vp]),
     "ckv_cache_create": (C.c_int, [vp, u32, u32, u32, u32, C.POINTER(vp)]),
     "ckv_cache_destroy": (C.c_int, [vp]),
     "ckv_cache_counters": (C.c_int, [vp, vp]),
     "ckv_cache_lookup": (C.c_int, [vp, vp, u32, vp, u32, vp, vp, vp, vp]),
     "ckv_cache_invalidate": (C.c_int, [vp, vp, u32, vp, u32]),
-    "ckv_attend": (C.c_int, [vp, C.POINTER(AttendDesc), vp, vp, vp, vp, vp, vp, vp]),
+    "ckv_attend": (C.c_int, [vp, C.POINTER(AttendDesc), vp, vp, vp, vp, C.POINTER(Runs), vp, vp,
+                             vp]),
     "ckv_session_create": (C.c_int, [vp, C.POINTER(SessionDesc), C.POINTER(vp)]),
     "ckv_session_destroy": (C.c_int, [vp]),
     "ckv_session_kv": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(u32)]),

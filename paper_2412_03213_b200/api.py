@@ -320,7 +320,7 @@ def _select(ctx, q, model, index, budget, recency, want_scores=False):
                         N.CKV_SEL_FULL_RANK | (N.CKV_SEL_SCORES if want_scores else 0), 0)
     check(lib().ckv_select(ctx.h, C.byref(desc), qd.data_ptr(), dm.cents.data_ptr(),
                            dm.ncl.data_ptr(), dm.sizes.data_ptr(), dm.starts.data_ptr(),
-                           dm.sorted.data_ptr(), tok.data_ptr(), None, ntok.data_ptr(),
+                           dm.sorted.data_ptr(), tok.data_ptr(), None, None, ntok.data_ptr(),
                            ntk.data_ptr(), trm.data_ptr(), rnk.data_ptr(), _ptr(sc), None))
     n = int(ntok.item())
     ids = np.concatenate([tok.cpu().numpy().view(np.uint32)[:n], rec]).astype(np.uint32)
@@ -362,7 +362,7 @@ def approx_attention(q: np.ndarray, keys: np.ndarray, values: np.ndarray,
     w = torch.empty(len(sel), dtype=torch.float32, device=dev)
     desc = N.AttendDesc(1, 1, keys.shape[0], len(sel), len(sel))
     check(lib().ckv_attend(ctx.h, C.byref(desc), qd.data_ptr(), kb.data_ptr(), vb.data_ptr(),
-                           ids.data_ptr(), nt.data_ptr(), out.data_ptr(), w.data_ptr()))
+                           ids.data_ptr(), None, nt.data_ptr(), out.data_ptr(), w.data_ptr()))
     return AttentionOutput(out.cpu().numpy()[0], w.cpu().numpy())
 
 

@@ -2,40 +2,84 @@
 // (attention.hpp:20-69 attention_over / approx_attention), split-K
 // flash-decode with a log-sum-exp merge.
 //
-// Grid (q head, split).  Each CTA owns a contiguous slice of the q head's
-// row list (I_T mapped to KV-store rows) and streams it through a
-// STAGES-deep shared-memory ring of 32-row tiles with cp.async (16 B per
-// request, L1 bypass).  The whole slice's row ids are staged in smem first,
-// so every tile's K/V requests issue back to back without waiting on an id
-// load; with the cluster-major store (ckv_session_prefill) the rows of a
-// selected cluster are consecutive, so the requests are long contiguous runs.
-// Per tile, a half-warp owns one row (16 lanes x 8 bf16 dims): dot product
-// (fp32 FMA + 4 shuffles), then an online-softmax update of that half-warp's
-// running (m, l, acc[8]).  The eight half-warp states merge in smem, and the
-// last CTA of a q head (atomic ticket) merges the split partials in a fixed
-// order, so results do not depend on scheduling.
-//
-// Numerics: fp32 logits / exp2 / sums; the reference uses f64.  Tolerance-
+// Persistent, warp-specialised kernel (one CTA per SM slot):
+//   work item  = (q head h, slice s): I_T entries [nt*s/S, nt*(s+1)/S).
+//   producer   = warp 4, one elected lane.  For each item it stages the q
+//                head's run list (I_T as runs of consecutive KV-store rows,
+//                ckv_select) in smem, then for each 32-row tile waits for a
+//                free ring stage and issues one TMA bulk copy
+//                (cp.async.bulk ... mbarrier::complete_tx) per contiguous run
+//                segment for K and for V; the stage's mbarrier completes when
+//                the bytes land.  The query vector rides a 2-slot ring the
+//                same way.  Tiles stream back to back across item
+//                boundaries, so the HBM pipeline never drains.
+//   consumers  = warps 0-3.  A half-warp owns one row per step (16 lanes x 8
+//                bf16 dims): dot product (fp32 FMA + 4 shuffles), online
+//                softmax (m, l, acc[8]) per half-warp; each warp releases the
+//                stage to the producer.  At the end of an item the 8
+//                half-warp states merge in smem into the item partial; the
+//                last CTA to finish a q head (atomic ticket) merges its S
+//                partials in a fixed order, so results never depend on
+//                scheduling.
+// Numerics: fp32 logits / exp2 / sums; the reference uses f64 — tolerance-
 // checked against the oracle (tests/test_gpu_attend.py).
 #include "ckv_internal.cuh"
 
 namespace ckvb {
 
-constexpr int AT_THREADS = 128;  // 4 warps = 8 half-warps
-constexpr int AT_TILE = 32;      // rows per pipeline stage
+constexpr int AT_CWARPS = 4;                      // consumer warps
+constexpr int AT_THREADS = (AT_CWARPS + 1) * 32;  // + producer warp
+constexpr int AT_TILE = 32;                       // rows per stage
 constexpr int AT_STAGES = 4;
-constexpr int AT_MAX_ROWS = 2048;  // rows per CTA slice (ids staged in smem)
-constexpr int PART = 2 + D;        // partial: m (log2 domain), l, acc[128]
+constexpr int AT_RUNS = 256;                      // runs staged in smem
+constexpr int PART = 2 + D;                       // partial: m (log2 domain), l, acc[128]
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  const int n = valid ? 16 : 0;  // src-size 0 zero-fills
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {  // 2^x, ex2.approx (-inf -> +0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(AT_CWARPS * 32) : "memory");
 }
 
 __device__ __forceinline__ float dot8(const uint4 k, const float* qv) {
@@ -62,193 +106,303 @@ __device__ __forceinline__ void axpy8(float p, const uint4 v, float* acc) {
   acc[7] = fmaf(p, __uint_as_float(v.w & 0xffff0000u), acc[7]);
 }
 
-struct AttSmem {
-  uint4 k[AT_STAGES][AT_TILE][16];  // 16 KB
-  uint4 v[AT_STAGES][AT_TILE][16];  // 16 KB
-  uint32_t ids[AT_MAX_ROWS];        // 8 KB
+struct __align__(128) AttSmem {
+  uint4 k[AT_STAGES][AT_TILE][16];  // 8 KB per stage
+  uint4 v[AT_STAGES][AT_TILE][16];  // 8 KB per stage
+  float q[2][D];                    // query ring
+  uint64_t full[AT_STAGES], empty[AT_STAGES], qfull[2], qempty[2];
+  uint32_t roff[AT_RUNS + 1], rrow[AT_RUNS];  // producer: runs of the current item
   float hm[8], hl[8];
   float hacc[8][D];
   uint32_t last;
 };
 
-__global__ void __launch_bounds__(AT_THREADS, 4)
+struct ItemInfo {
+  uint32_t h, s, e0, e1;
+};
+__device__ __forceinline__ ItemInfo item_info(uint32_t i, uint32_t splits,
+                                              const uint32_t* n_tokens) {
+  ItemInfo it;
+  it.h = i / splits;
+  it.s = i % splits;
+  const uint32_t nt = n_tokens[it.h];
+  it.e0 = uint32_t((uint64_t(nt) * it.s) / splits);
+  it.e1 = uint32_t((uint64_t(nt) * (it.s + 1)) / splits);
+  return it;
+}
+
+template <bool WEIGHTS>
+__global__ void __launch_bounds__(AT_THREADS, 1)
 k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
          const uint16_t* __restrict__ K, const uint16_t* __restrict__ V,
-         const uint32_t* __restrict__ rows, const uint32_t* __restrict__ n_tokens,
+         const uint32_t* __restrict__ rows, ckv_runs runs, const uint32_t* __restrict__ n_tokens,
          float* __restrict__ out, float* __restrict__ logits_ws, float* __restrict__ part,
          uint32_t* __restrict__ tickets, float* __restrict__ weights) {
-  extern __shared__ __align__(16) unsigned char sm_raw[];
+  extern __shared__ __align__(128) unsigned char sm_raw[];
   AttSmem& sm = *reinterpret_cast<AttSmem*>(sm_raw);
-  const uint32_t h = blockIdx.x, split = blockIdx.y;
-  const uint32_t nt = n_tokens[h];
-  // balanced slices: split s covers [nt*s/S, nt*(s+1)/S)
-  const uint32_t r0 = uint32_t((uint64_t(nt) * split) / splits);
-  const uint32_t r1 = uint32_t((uint64_t(nt) * (split + 1)) / splits);
-  const uint32_t nr = r1 - r0;
-  const int t = threadIdx.x;
-  const uint32_t unit = h / desc.group;
-  const uint16_t* Ku = K + size_t(unit) * desc.p_cap * D;
-  const uint16_t* Vu = V + size_t(unit) * desc.p_cap * D;
-
-  const uint32_t* rl = rows + size_t(h) * desc.sel_cap + r0;
-  for (uint32_t i = t; i < nr; i += AT_THREADS) sm.ids[i] = __ldg(rl + i);
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
+  const uint32_t n_items = desc.n_q * splits;
+  if (t == 0) {
+    for (int s = 0; s < AT_STAGES; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], AT_CWARPS);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.qfull[s], 1);
+      mbar_init(&sm.qempty[s], AT_CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
-  const uint32_t n_tiles = (nr + AT_TILE - 1) / AT_TILE;
-  auto issue = [&](uint32_t tile) {
-    const int st = tile % AT_STAGES;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int e = t + AT_THREADS * k;  // 0..511: row e/16, 16-B column e%16
-      const int r = e >> 4, c = e & 15;
-      const uint32_t gr = tile * AT_TILE + r;
-      const bool ok = gr < nr;
-      const size_t row = ok ? sm.ids[gr] : 0;
-      cp_async16(&sm.k[st][r][c], reinterpret_cast<const uint4*>(Ku + row * D) + c, ok);
-      cp_async16(&sm.v[st][r][c], reinterpret_cast<const uint4*>(Vu + row * D) + c, ok);
+  if (wid == AT_CWARPS) {
+    // ======================= producer warp =====================================
+    uint32_t st = 0, ph = 0, qk = 0;  // ring stage / parity, query-ring counter
+    for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x, ++qk) {
+      const ItemInfo it = item_info(i, splits, n_tokens);
+      const uint32_t unit = it.h / desc.group;
+      const uint16_t* Ku = K + size_t(unit) * desc.p_cap * D;
+      const uint16_t* Vu = V + size_t(unit) * desc.p_cap * D;
+      // stage this q head's runs (rows mode: one entry per row, read in place)
+      uint32_t nrun = 0;
+      bool staged = false;
+      const uint32_t* gro = nullptr;
+      const uint32_t* grr = nullptr;
+      if (!rows) {
+        nrun = runs.count[it.h];
+        gro = runs.off + size_t(it.h) * (runs.run_cap + 1);
+        grr = runs.row + size_t(it.h) * runs.run_cap;
+        staged = nrun <= uint32_t(AT_RUNS);
+        __syncwarp();  // the previous item's runs are no longer read
+        if (staged) {
+          for (uint32_t r = lane; r <= nrun; r += 32) sm.roff[r] = __ldg(gro + r);
+          for (uint32_t r = lane; r < nrun; r += 32) sm.rrow[r] = __ldg(grr + r);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
+        mbar_wait(&sm.qempty[qs], qp ^ 1);
+        mbar_expect_tx(&sm.qfull[qs], D * 4);
+        bulk_g2s(sm.q[qs], q + size_t(it.h) * D, D * 4, &sm.qfull[qs]);
+        const uint32_t* rowlist = rows ? rows + size_t(it.h) * desc.sel_cap : nullptr;
+        uint32_t r = 0;
+        if (!rows) {  // last run with off <= e0
+          uint32_t lo = 0, hi = nrun;
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((staged ? sm.roff[mid] : __ldg(gro + mid)) <= it.e0) lo = mid; else hi = mid;
+          }
+          r = lo;
+        }
+        for (uint32_t e = it.e0; e < it.e1; e += AT_TILE) {
+          const uint32_t te = min(e + AT_TILE, it.e1);
+          mbar_wait(&sm.empty[st], ph ^ 1);
+          mbar_expect_tx(&sm.full[st], (te - e) * D * 2 * 2);
+          for (uint32_t x = e; x < te;) {
+            uint32_t row, n;
+            if (rows) {
+              row = __ldg(rowlist + x);
+              n = 1;
+            } else {
+              while ((staged ? sm.roff[r + 1] : __ldg(gro + r + 1)) <= x) ++r;
+              const uint32_t ro = staged ? sm.roff[r] : __ldg(gro + r);
+              const uint32_t rend = staged ? sm.roff[r + 1] : __ldg(gro + r + 1);
+              row = (staged ? sm.rrow[r] : __ldg(grr + r)) + (x - ro);
+              n = min(te, rend) - x;
+            }
+            bulk_g2s(&sm.k[st][x - e][0], Ku + size_t(row) * D, n * D * 2, &sm.full[st]);
+            bulk_g2s(&sm.v[st][x - e][0], Vu + size_t(row) * D, n * D * 2, &sm.full[st]);
+            x += n;
+          }
+          if (++st == AT_STAGES) { st = 0; ph ^= 1; }
+        }
+      }
+      st = __shfl_sync(0xffffffffu, st, 0);
+      ph = __shfl_sync(0xffffffffu, ph, 0);
     }
-  };
-#pragma unroll
-  for (int s = 0; s < AT_STAGES - 1; ++s) {
-    if (uint32_t(s) < n_tiles) issue(s);
-    cp_async_commit();
+    return;
   }
 
+  // ========================= consumer warps ====================================
   const int hw = t >> 4;  // half-warp 0..7
   const int hl = t & 15;  // dims [8*hl, 8*hl+8)
   const float qscale = 1.4426950408889634f * rsqrtf(float(D));  // exp -> exp2
-  float qv[8];
-  {
-    const float4* qp = reinterpret_cast<const float4*>(q + size_t(h) * D + 8 * hl);
-    const float4 a = __ldg(qp), b = __ldg(qp + 1);
-    qv[0] = a.x * qscale; qv[1] = a.y * qscale; qv[2] = a.z * qscale; qv[3] = a.w * qscale;
-    qv[4] = b.x * qscale; qv[5] = b.y * qscale; qv[6] = b.z * qscale; qv[7] = b.w * qscale;
-  }
-  float m = -INFINITY, l = 0.f;
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  float* lw = logits_ws ? logits_ws + size_t(h) * desc.sel_cap + r0 : nullptr;
-
-  for (uint32_t tile = 0; tile < n_tiles; ++tile) {
-    cp_async_wait<AT_STAGES - 2>();
-    __syncthreads();  // tile's bytes visible to all; the stage refilled below is free
-    if (tile + AT_STAGES - 1 < n_tiles) issue(tile + AT_STAGES - 1);
-    cp_async_commit();
-    const int st = tile % AT_STAGES;
-    // this half-warp's 4 rows of the tile: hw, hw+8, hw+16, hw+24
-    float s[4];
-    uint4 vv[4];
-    float tmax = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int r = hw + 8 * k;
-      const uint4 kk = sm.k[st][r][hl];
-      vv[k] = sm.v[st][r][hl];
-      float x = dot8(kk, qv);
-      x += __shfl_xor_sync(0xffffffffu, x, 8);
-      x += __shfl_xor_sync(0xffffffffu, x, 4);
-      x += __shfl_xor_sync(0xffffffffu, x, 2);
-      x += __shfl_xor_sync(0xffffffffu, x, 1);
-      const bool ok = tile * AT_TILE + r < nr;
-      s[k] = ok ? x : -INFINITY;
-      if (lw && ok && hl == 0) lw[tile * AT_TILE + r] = x;
-      tmax = fmaxf(tmax, s[k]);
+  uint32_t st = 0, ph = 0, qk = 0;
+  for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x, ++qk) {
+    const ItemInfo it = item_info(i, splits, n_tokens);
+    const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
+    mbar_wait(&sm.qfull[qs], qp);
+    float qv[8];
+    {
+      const float4 a = *reinterpret_cast<const float4*>(&sm.q[qs][8 * hl]);
+      const float4 b = *reinterpret_cast<const float4*>(&sm.q[qs][8 * hl + 4]);
+      qv[0] = a.x * qscale; qv[1] = a.y * qscale; qv[2] = a.z * qscale; qv[3] = a.w * qscale;
+      qv[4] = b.x * qscale; qv[5] = b.y * qscale; qv[6] = b.z * qscale; qv[7] = b.w * qscale;
     }
-    const float mn = fmaxf(m, tmax);
-    if (mn != -INFINITY) {
-      const float sc = exp2f(m - mn);  // m = -inf -> 0
-      l *= sc;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.qempty[qs]);
+    float m = -INFINITY, l = 0.f;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float* lw = WEIGHTS ? logits_ws + size_t(it.h) * desc.sel_cap : nullptr;
+    for (uint32_t e = it.e0; e < it.e1; e += AT_TILE) {
+      mbar_wait(&sm.full[st], ph);
+      const bool full_tile = e + AT_TILE <= it.e1;
+      float s[4];
+      uint4 vv[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] *= sc;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float p = exp2f(s[k] - mn);
-        l += p;
-        axpy8(p, vv[k], acc);
+      for (int kk = 0; kk < 4; ++kk) {
+        const int r = hw + 8 * kk;
+        const uint4 kr = sm.k[st][r][hl];
+        vv[kk] = sm.v[st][r][hl];
+        float x = dot8(kr, qv);
+        x += __shfl_xor_sync(0xffffffffu, x, 8);
+        x += __shfl_xor_sync(0xffffffffu, x, 4);
+        x += __shfl_xor_sync(0xffffffffu, x, 2);
+        x += __shfl_xor_sync(0xffffffffu, x, 1);
+        s[kk] = x;
       }
-      m = mn;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[st]);  // stage data is in registers now
+      if (++st == AT_STAGES) { st = 0; ph ^= 1; }
+      if (full_tile) {
+        if (WEIGHTS && hl == 0)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) lw[e + hw + 8 * kk] = s[kk];
+        const float mn = fmaxf(fmaxf(m, fmaxf(s[0], s[1])), fmaxf(s[2], s[3]));
+        const float sc = ex2(m - mn);  // m = -inf -> 0
+        l *= sc;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] *= sc;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float p = ex2(s[kk] - mn);
+          l += p;
+          axpy8(p, vv[kk], acc);
+        }
+        m = mn;
+      } else {  // the slice's last, partial tile: rows past its end hold stale data
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const bool ok = e + hw + 8 * kk < it.e1;
+          if (WEIGHTS && ok && hl == 0) lw[e + hw + 8 * kk] = s[kk];
+          s[kk] = ok ? s[kk] : -INFINITY;
+          tmax = fmaxf(tmax, s[kk]);
+        }
+        const float mn = fmaxf(m, tmax);
+        if (mn != -INFINITY) {
+          const float sc = ex2(m - mn);
+          l *= sc;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] *= sc;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            if (s[kk] != -INFINITY) {
+              const float p = ex2(s[kk] - mn);
+              l += p;
+              axpy8(p, vv[kk], acc);
+            }
+          }
+          m = mn;
+        }
+      }
+    }
+    // ---- merge the 8 half-warp states into the item partial -------------------
+    consumer_bar();  // the previous item's merge scratch is free
+    if (hl == 0) { sm.hm[hw] = m; sm.hl[hw] = l; }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sm.hacc[hw][8 * hl + j] = acc[j];
+    consumer_bar();
+    float M = sm.hm[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) M = fmaxf(M, sm.hm[j]);
+    float* pp = part + size_t(i) * PART;
+    {
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float w = sm.hm[j] == -INFINITY ? 0.f : exp2f(sm.hm[j] - M);
+        a += sm.hacc[j][t] * w;
+      }
+      pp[2 + t] = a;  // 128 consumer threads == D
+    }
+    if (t == 0) {
+      float ls = 0.f;
+      for (int j = 0; j < 8; ++j)
+        ls += sm.hm[j] == -INFINITY ? 0.f : sm.hl[j] * exp2f(sm.hm[j] - M);
+      pp[0] = M;
+      pp[1] = ls;
+    }
+    // ---- the last CTA to finish a q head merges its S partials -----------------
+    // bar.sync orders the CTA's partial stores before thread 0's release; the
+    // acq_rel RMW makes every other CTA's released partials visible to the
+    // last one (PTX release/acquire cumulativity), no per-thread fences.
+    consumer_bar();
+    if (t == 0) sm.last = (atom_add_acq_rel(&tickets[it.h], 1u) == splits - 1);
+    consumer_bar();
+    if (sm.last) {
+      const float* pb = part + size_t(it.h) * splits * PART;
+      float MM = -INFINITY;
+      for (uint32_t c = 0; c < splits; ++c) MM = fmaxf(MM, __ldcg(pb + c * PART));
+      float L = 0.f, o = 0.f;
+      for (uint32_t c = 0; c < splits; ++c) {
+        const float mc = __ldcg(pb + c * PART);
+        const float w = mc == -INFINITY ? 0.f : exp2f(mc - MM);
+        L += __ldcg(pb + c * PART + 1) * w;
+        o += __ldcg(pb + c * PART + 2 + t) * w;
+      }
+      const float invL = 1.f / L;
+      out[size_t(it.h) * D + t] = o * invL;
+      if (WEIGHTS) {
+        const uint32_t nt = n_tokens[it.h];
+        const float* lg = logits_ws + size_t(it.h) * desc.sel_cap;
+        float* wo = weights + size_t(it.h) * desc.sel_cap;
+        for (uint32_t j = t; j < nt; j += AT_CWARPS * 32)
+          wo[j] = exp2f(__ldcg(lg + j) - MM) * invL;
+      }
+      if (t == 0) tickets[it.h] = 0;  // re-arm for the next launch
     }
   }
-  cp_async_wait<0>();
-
-  // merge the 8 half-warp states of this CTA
-  if (hl == 0) { sm.hm[hw] = m; sm.hl[hw] = l; }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) sm.hacc[hw][8 * hl + i] = acc[i];
-  __syncthreads();
-  float M = sm.hm[0];
-#pragma unroll
-  for (int i = 1; i < 8; ++i) M = fmaxf(M, sm.hm[i]);
-  float* pp = part + (size_t(h) * splits + split) * PART;
-  {
-    float a = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float w = sm.hm[i] == -INFINITY ? 0.f : exp2f(sm.hm[i] - M);
-      a += sm.hacc[i][t] * w;
-    }
-    pp[2 + t] = a;  // AT_THREADS == D
-  }
-  if (t == 0) {
-    float ls = 0.f;
-    for (int i = 0; i < 8; ++i) ls += sm.hm[i] == -INFINITY ? 0.f : sm.hl[i] * exp2f(sm.hm[i] - M);
-    pp[0] = M;
-    pp[1] = ls;
-  }
-  // ---- the last CTA of this q head merges the split partials ----------------
-  __threadfence();
-  __syncthreads();
-  if (t == 0) sm.last = (atomicAdd(&tickets[h], 1u) == splits - 1);
-  __syncthreads();
-  if (!sm.last) return;
-  __threadfence();
-  const float* pb = part + size_t(h) * splits * PART;
-  float MM = -INFINITY;
-  for (uint32_t c = 0; c < splits; ++c) MM = fmaxf(MM, __ldcg(pb + c * PART));
-  float L = 0.f, o = 0.f;
-  for (uint32_t c = 0; c < splits; ++c) {
-    const float mc = __ldcg(pb + c * PART);
-    const float w = mc == -INFINITY ? 0.f : exp2f(mc - MM);
-    L += __ldcg(pb + c * PART + 1) * w;
-    o += __ldcg(pb + c * PART + 2 + t) * w;
-  }
-  const float invL = 1.f / L;
-  out[size_t(h) * D + t] = o * invL;
-  if (weights) {
-    const float* lg = logits_ws + size_t(h) * desc.sel_cap;
-    float* wo = weights + size_t(h) * desc.sel_cap;
-    for (uint32_t i = t; i < nt; i += AT_THREADS) wo[i] = exp2f(__ldcg(lg + i) - MM) * invL;
-  }
-  if (t == 0) tickets[h] = 0;  // re-arm for the next launch
 }
 
 uint32_t attend_splits(const ckv_attend_desc& d) {
-  // aim for >= ~4 CTAs per SM worth of work, slices of <= AT_MAX_ROWS rows
-  uint32_t s = 1;
-  const uint32_t want = uint32_t(num_sms()) * 8;
-  while (d.n_q * s < want && s < 16 && d.max_tokens / (2 * s) >= 256) s *= 2;
-  while ((d.max_tokens + s - 1) / s > AT_MAX_ROWS) ++s;
-  return s;
+  // ~16 tiles per work item: few per-item epilogues, enough items to balance
+  const uint32_t s = (d.max_tokens + 16 * AT_TILE - 1) / (16 * AT_TILE);
+  return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 
 int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
                   const uint16_t* K, const uint16_t* V, const uint32_t* rows,
-                  const uint32_t* n_tokens, float* out, float* weights, float* logits_ws,
-                  float* part, uint32_t* tickets) {
+                  const ckv_runs& runs, const uint32_t* n_tokens, float* out, float* weights,
+                  float* logits_ws, float* part, uint32_t* tickets) {
+  if (!rows && !runs.row) { set_error("attend: need rows or runs"); return CKV_EINVAL; }
   if (desc.n_q == 0 || desc.max_tokens == 0) return CKV_OK;
   const uint32_t splits = attend_splits(desc);
   const size_t smem = sizeof(AttSmem);
   static int attr_dev = -1;
+  static int per_sm = 1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_attend, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(smem)));
+    for (auto fn : {k_attend<false>, k_attend<true>}) {
+      CKV_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(smem)));
+      CKV_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        cudaSharedmemCarveoutMaxShared));
+    }
+    CKV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<false>,
+                                                               AT_THREADS, smem));
     attr_dev = dev;
   }
-  dim3 grid(desc.n_q, splits);
-  k_attend<<<grid, AT_THREADS, smem, st>>>(desc, splits, q, K, V, rows, n_tokens, out,
-                                           weights ? logits_ws : nullptr, part, tickets,
-                                           weights);
+  const uint32_t n_items = desc.n_q * splits;
+  const uint32_t grid = std::min<uint32_t>(n_items, uint32_t(std::max(1, per_sm)) * num_sms());
+  if (weights)
+    k_attend<true><<<grid, AT_THREADS, smem, st>>>(desc, splits, q, K, V, rows, runs, n_tokens,
+                                                   out, logits_ws, part, tickets, weights);
+  else
+    k_attend<false><<<grid, AT_THREADS, smem, st>>>(desc, splits, q, K, V, rows, runs, n_tokens,
+                                                    out, nullptr, part, tickets, nullptr);
   CKV_LAUNCH_CHECK("k_attend");
   return CKV_OK;
 }

@@ -386,21 +386,35 @@ static CacheDev null_cache() {
   return c;
 }
 
+static ckv_runs null_runs() {
+  ckv_runs r;
+  std::memset(&r, 0, sizeof r);
+  return r;
+}
+
 int ckv_select(ckv_ctx* ctx, const ckv_select_desc* d, const float* q, const float* centroids,
                const uint32_t* n_clusters, const uint32_t* sizes, const uint32_t* starts,
                const uint32_t* sorted_ids, uint32_t* token_ids, uint32_t* rows,
-               uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked,
-               double* scores, ckv_cache* cache) {
-  if (!ranked) { set_error("ckv_select: ranked buffer required"); return CKV_EINVAL; }
+               const ckv_runs* runs, uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed,
+               uint32_t* ranked, double* scores, ckv_cache* cache) {
+  if (!ranked || !n_tokens || !n_taken || !trimmed) {
+    set_error("ckv_select: ranked / n_tokens / n_taken / trimmed are required");
+    return CKV_EINVAL;
+  }
   if (cache && cache->dev.n_slots < d->n_q) {
     set_error("ckv_select: cache has fewer slots than q heads");
+    return CKV_EINVAL;
+  }
+  if (runs && runs->run_cap < d->c_cap + 2) {
+    set_error("ckv_select: runs.run_cap must be >= c_cap + 2");
     return CKV_EINVAL;
   }
   void* scratch = nullptr;
   CKV_CUDA_TRY(cudaMallocAsync(&scratch, select_scratch_bytes(d->n_q, d->c_cap), ctx->stream));
   int rc = launch_select(ctx->stream, *d, q, centroids, n_clusters, sizes, starts, sorted_ids,
-                         token_ids, rows, d->row_base, n_tokens, n_taken, trimmed, ranked, scores,
-                         cache ? cache->dev : null_cache(), scratch);
+                         token_ids, rows, runs ? *runs : null_runs(), d->row_base, n_tokens,
+                         n_taken, trimmed, ranked, scores, cache ? cache->dev : null_cache(),
+                         scratch);
   cudaFreeAsync(scratch, ctx->stream);
   ctx->launches += 2;
   return rc;
@@ -474,8 +488,8 @@ int ckv_cache_invalidate(ckv_ctx* ctx, ckv_cache* c, uint32_t slot, const uint32
 }
 
 int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q, const uint16_t* K,
-               const uint16_t* V, const uint32_t* token_ids, const uint32_t* n_tokens, float* out,
-               float* weights) {
+               const uint16_t* V, const uint32_t* rows, const ckv_runs* runs,
+               const uint32_t* n_tokens, float* out, float* weights) {
   cudaStream_t st = ctx->stream;
   if (weights) {  // parity mode: approx_attention's empty-selection check
     std::vector<uint32_t> nt(d->n_q);
@@ -493,7 +507,8 @@ int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q, const uin
   CKV_CUDA_TRY(cudaMallocAsync(&tickets, size_t(d->n_q) * 4 + 4, st));
   CKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(d->n_q) * 4 + 4, st));
   if (weights) CKV_CUDA_TRY(cudaMallocAsync(&lw, size_t(d->n_q) * d->sel_cap * 4 + 16, st));
-  int rc = launch_attend(st, *d, q, K, V, token_ids, n_tokens, out, weights, lw, part, tickets);
+  int rc = launch_attend(st, *d, q, K, V, rows, runs ? *runs : null_runs(), n_tokens, out,
+                         weights, lw, part, tickets);
   ctx->launches++;
   cudaFreeAsync(part, st);
   cudaFreeAsync(tickets, st);
@@ -517,6 +532,7 @@ struct ckv_session {
   uint32_t *token_ids = nullptr, *rows = nullptr, *n_tokens = nullptr, *n_taken = nullptr,
            *trimmed = nullptr, *ranked = nullptr;
   void* sel_scratch = nullptr;
+  ckv_runs runs{};
   uint16_t *tmpK = nullptr, *tmpV = nullptr;  // decode-batch relayout staging
   float* part = nullptr;
   uint32_t* tickets = nullptr;
@@ -568,6 +584,10 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   rc |= salloc(&s->rows, size_t(s->n_q) * s->sel_cap);
   rc |= salloc(reinterpret_cast<unsigned char**>(&s->sel_scratch),
                select_scratch_bytes(s->n_q, s->c_cap));
+  s->runs.run_cap = s->c_cap + 2;
+  rc |= salloc(&s->runs.row, size_t(s->n_q) * s->runs.run_cap);
+  rc |= salloc(&s->runs.off, size_t(s->n_q) * (s->runs.run_cap + 1));
+  rc |= salloc(&s->runs.count, s->n_q);
   rc |= salloc(&s->tmpK, size_t(s->U) * d->decode_batch * D);
   rc |= salloc(&s->tmpV, size_t(s->U) * d->decode_batch * D);
   rc |= salloc(&s->n_tokens, s->n_q);
@@ -604,6 +624,7 @@ int ckv_session_destroy(ckv_session* s) {
   cudaFree(s->K); cudaFree(s->V); cudaFree(s->cents); cudaFree(s->labels);
   cudaFree(s->n_clusters); cudaFree(s->sizes); cudaFree(s->starts); cudaFree(s->sorted);
   cudaFree(s->token_ids); cudaFree(s->rows); cudaFree(s->sel_scratch); cudaFree(s->tmpK);
+  cudaFree(s->runs.row); cudaFree(s->runs.off); cudaFree(s->runs.count);
   cudaFree(s->tmpV); cudaFree(s->n_tokens); cudaFree(s->n_taken); cudaFree(s->trimmed);
   cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
   cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
@@ -682,9 +703,10 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
   sd.rec_end = s->n_ctx;
   sd.flags = 0;
   sd.row_base = sd.sink_count;
+  const bool want_ids = (s->d.flags & CKV_SESSION_TOKEN_IDS) != 0;
   CKV_TRY(launch_select(s->ctx->stream, sd, q_dev, s->cents, s->n_clusters, s->sizes, s->starts,
-                        s->sorted, s->token_ids, s->rows, sd.row_base, s->n_tokens, s->n_taken,
-                        s->trimmed, s->ranked, nullptr,
+                        s->sorted, want_ids ? s->token_ids : nullptr, nullptr, s->runs,
+                        sd.row_base, s->n_tokens, s->n_taken, s->trimmed, s->ranked, nullptr,
                         s->cache ? s->cache->dev : null_cache(), s->sel_scratch));
   ckv_attend_desc ad{};
   ad.n_q = s->n_q;
@@ -692,7 +714,7 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
   ad.p_cap = s->p_cap;
   ad.sel_cap = s->sel_cap;
   ad.max_tokens = std::min(s->d.budget, s->labeled_end) + sd.sink_count + (s->n_ctx - s->labeled_end);
-  CKV_TRY(launch_attend(s->ctx->stream, ad, q_dev, s->K, s->V, s->rows, s->n_tokens,
+  CKV_TRY(launch_attend(s->ctx->stream, ad, q_dev, s->K, s->V, nullptr, s->runs, s->n_tokens,
                         out_dev, nullptr, nullptr, s->part, s->tickets));
   s->ctx->launches += 3;
   return CKV_OK;

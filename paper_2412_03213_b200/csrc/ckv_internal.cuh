@@ -48,9 +48,9 @@ struct CacheDev {
 int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const float* cents, const uint32_t* n_clusters, const uint32_t* sizes,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
-                  uint32_t* rows, uint32_t row_base, uint32_t* n_tokens, uint32_t* n_taken,
-                  uint32_t* trimmed, uint32_t* ranked, double* scores, const CacheDev& cache,
-                  void* scratch);
+                  uint32_t* rows, const ckv_runs& runs, uint32_t row_base, uint32_t* n_tokens,
+                  uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
+                  const CacheDev& cache, void* scratch);
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap);
 int launch_cache_lookup(cudaStream_t st, const CacheDev& cache, uint32_t slot,
                         const uint32_t* sel, uint32_t n_sel, const uint32_t* sizes,
@@ -58,9 +58,9 @@ int launch_cache_lookup(cudaStream_t st, const CacheDev& cache, uint32_t slot,
 int launch_cache_invalidate(cudaStream_t st, const CacheDev& cache, uint32_t slot,
                             const uint32_t* retired, uint32_t n);
 int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
-                  const uint16_t* K, const uint16_t* V, const uint32_t* token_ids,
-                  const uint32_t* n_tokens, float* out, float* weights, float* logits_ws,
-                  float* part, uint32_t* tickets);
+                  const uint16_t* K, const uint16_t* V, const uint32_t* rows,
+                  const ckv_runs& runs, const uint32_t* n_tokens, float* out, float* weights,
+                  float* logits_ws, float* part, uint32_t* tickets);
 size_t attend_part_floats(uint32_t n_q, uint32_t max_tokens);
 uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
 void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows);

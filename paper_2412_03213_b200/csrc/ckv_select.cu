@@ -1,223 +1,472 @@
 // ckv_select.cu — K6 + K8: score_clusters + select_tokens + ClusterCache
 // for every q head of a decode step (selection.hpp:50-111, cache.hpp:38-57).
 //
-// Two launches:
-//  k_score : one thread per (kv unit, cluster) runs the `group` q heads'
-//            sequential f64 FMA chains over d = 128 (bit-identical to
-//            dot_f64) and writes order-preserving u64 rank
-//            keys.  Each centroid row is read once per unit, every q head of
-//            the GQA group reuses it from registers.
-//  k_rank  : one warp per q head.  Each lane insertion-sorts its strided
-//            share of the keys by (score desc, id asc) — the reference's
-//            std::sort comparator (selection.hpp:83-87) — then a 32-way warp
-//            tournament pops clusters in global rank order until the running
-//            size reaches the budget (all C for CKV_SEL_FULL_RANK).  The taken
-//            slices (last one trimmed to its lowest positions), sinks and the
-//            recency window are then written in parallel:
-//              token_ids : reference I_T positions (selection.hpp:91-109)
-//              rows      : the same entries as rows of the cluster-major KV
-//                          store (row = row_base + starts[c] + i for cluster
-//                          tokens, the position for sinks / recency), i.e.
-//                          contiguous runs for the attention kernel.
-//            The cache step (bitmap ring of the last R taken-sets) is fused.
+// K1 k_score_approx — fp32 GEMV, one warp per 8 centroid rows of a kv unit
+//   (one coalesced 512-B row per warp load, 8 rows in flight), all G q heads
+//   of the unit per row, so every centroid is read from HBM once.  For each
+//   (q head, cluster) it writes the fp32 dot a and a rigorous bound
+//   E = 2^-14 |q| |mu| >= |a - s|, where s is the reference's sequential
+//   f64 dot_f64 (the fp32 error is <= gamma_9 sum|q_j mu_j|
+//   <= gamma_9 |q||mu| by Cauchy-Schwarz, ~60x below E).
+// K2 k_select_warp — one warp per q head:
+//   1. pop clusters in approximate (a desc, id asc) order until the running
+//      size reaches the budget: set U, L = min_{c in U}(a_c - E_c).
+//   2. Every cluster of the reference's exact prefix has s >= L (otherwise
+//      all of U, whose sizes sum to >= B, would rank before it and it would
+//      not be taken), and every cluster with a + E < L ranks strictly after
+//      all of them.  So S = {c : a_c + E_c >= L} contains the exact prefix
+//      and is exactly ordered against everything outside it.
+//   3. S (|U| + a few near-ties) is re-scored with the sequential f64 FMA
+//      chain — bit-identical to dot_f64 — ranked by (s desc, id asc), the
+//      reference's std::sort comparator (selection.hpp:83-87), and cut at
+//      the budget (selection.hpp:91-106).
+//   CKV_SEL_FULL_RANK / CKV_SEL_SCORES (the parity API), C > 512, > 64 pops
+//   or > 64 candidates take the exhaustive path: exact f64 scores for every
+//   cluster and a warp bitonic sort.
+//   Output: I_T as runs of the cluster-major KV store (one run per taken
+//   cluster, last one trimmed to its lowest positions, then the sink and
+//   recency runs), optionally the reference's position list and per-entry
+//   rows; the R-step cluster cache (bitmap ring, cache.hpp:38-57) is fused.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "ckv_internal.cuh"
 
 namespace ckvb {
 
+constexpr int SC_WARPS = 4;            // K1 warps per CTA
+constexpr int SC_ROWS = 8;             // K1 rows per warp
+constexpr int SW_WARPS = 4;            // K2 warps (q heads) per CTA
+constexpr int SW_KPL = 16;             // approx keys per lane in registers (C <= 512)
+constexpr int SW_MAXCAND = 64;         // exact candidates before the exhaustive path
+constexpr int SW_STAGE = 32;           // candidate rows staged per pass (16 KB)
+constexpr float SEL_ERR = 1.0f / 16384.0f;
+
 __device__ __forceinline__ unsigned long long rank_key(double s) {
-  // NaN scores (only from empty-cluster NaN centroids) rank last
-  return isnan(s) ? 0ull : dkey(s);
+  return isnan(s) ? 0ull : dkey(s);  // NaN (empty-cluster centroids) ranks last
 }
-
-constexpr int SC_ROWS = 64;       // clusters per k_score CTA (one per thread)
-constexpr int SC_STRIDE = D + 4;  // padded smem row: conflict-free 16-B reads
-
+__device__ __forceinline__ uint32_t fkey(float s) {  // order-preserving f32 -> u32
+  const uint32_t u = __float_as_uint(s);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ bool rank_before(unsigned long long ka, uint32_t ia,
+                                            unsigned long long kb, uint32_t ib) {
+  return ka > kb || (ka == kb && ia < ib);  // selection.hpp:83-87
+}
 __device__ __forceinline__ void cp_async16_sel(void* smem, const void* gmem, bool valid) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
                "r"(valid ? 16 : 0));
 }
 
+// ---------------------------------------------------------------------------
+// K1
+// ---------------------------------------------------------------------------
 template <int G>
-__global__ void __launch_bounds__(SC_ROWS)
-k_score(const float* __restrict__ q, const float* __restrict__ cents,
-        const uint32_t* __restrict__ n_clusters, uint32_t c_cap, uint32_t c_pad,
-        unsigned long long* __restrict__ keys, double* __restrict__ scores_out) {
+__global__ void __launch_bounds__(SC_WARPS * 32)
+k_score_approx(const float* __restrict__ q, const float* __restrict__ cents,
+               const uint32_t* __restrict__ n_clusters, uint32_t c_cap, uint32_t c_pad,
+               float* __restrict__ aval, float* __restrict__ aerr) {
   const uint32_t unit = blockIdx.x;
-  const uint32_t c0 = blockIdx.y * SC_ROWS;
+  const int lane = lane_id();
+  const uint32_t c0 = (blockIdx.y * SC_WARPS + warp_id()) * SC_ROWS;
   const uint32_t C = n_clusters[unit];
   if (c0 >= C) return;
-  __shared__ __align__(16) float cs[SC_ROWS][SC_STRIDE];
-  __shared__ double qs[G][D];
-  // stage this CTA's centroid rows: coalesced 16-B cp.async, one latency
-  const float* src = cents + (size_t(unit) * c_cap + c0) * D;
-  for (int e = threadIdx.x; e < SC_ROWS * (D / 4); e += SC_ROWS) {
-    const int r = e / (D / 4), c4 = e % (D / 4);
-    const bool ok = c0 + r < C;
-    cp_async16_sel(&cs[r][4 * c4], src + size_t(ok ? r : 0) * D + 4 * c4, ok);
-  }
-  asm volatile("cp.async.commit_group;\n");
-  for (int i = threadIdx.x; i < G * D; i += SC_ROWS)
-    qs[i / D][i % D] = double(q[(size_t(unit) * G + i / D) * D + i % D]);
-  asm volatile("cp.async.wait_group 0;\n");
-  __syncthreads();
-  const uint32_t c = c0 + threadIdx.x;
-  if (c >= C) return;
-  double acc[G];
+  const float* cu = cents + size_t(unit) * c_cap * D;
+  float4 m[SC_ROWS];
 #pragma unroll
-  for (int g = 0; g < G; ++g) acc[g] = 0.0;
-  const float4* row = reinterpret_cast<const float4*>(&cs[threadIdx.x][0]);
-#pragma unroll 8
-  for (int j4 = 0; j4 < D / 4; ++j4) {
-    const float4 m = row[j4];
-    const double m0 = m.x, m1 = m.y, m2 = m.z, m3 = m.w;
+  for (int r = 0; r < SC_ROWS; ++r)
+    m[r] = c0 + r < C ? __ldg(reinterpret_cast<const float4*>(cu + size_t(c0 + r) * D) + lane)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 qv[G];
+  float qn[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    qv[g] = __ldg(reinterpret_cast<const float4*>(q + (size_t(unit) * G + g) * D) + lane);
+    qn[g] = qv[g].x * qv[g].x + qv[g].y * qv[g].y + qv[g].z * qv[g].z + qv[g].w * qv[g].w;
+  }
+  float dg[SC_ROWS][G], mn[SC_ROWS];
+#pragma unroll
+  for (int r = 0; r < SC_ROWS; ++r) {
+    mn[r] = m[r].x * m[r].x + m[r].y * m[r].y + m[r].z * m[r].z + m[r].w * m[r].w;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      acc[g] = __fma_rn(qs[g][4 * j4 + 0], m0, acc[g]);
-      acc[g] = __fma_rn(qs[g][4 * j4 + 1], m1, acc[g]);
-      acc[g] = __fma_rn(qs[g][4 * j4 + 2], m2, acc[g]);
-      acc[g] = __fma_rn(qs[g][4 * j4 + 3], m3, acc[g]);
+      float d = qv[g].x * m[r].x;
+      d = fmaf(qv[g].y, m[r].y, d);
+      d = fmaf(qv[g].z, m[r].z, d);
+      dg[r][g] = fmaf(qv[g].w, m[r].w, d);
     }
   }
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const size_t h = size_t(unit) * G + g;
-    keys[h * c_pad + c] = rank_key(acc[g]);
-    if (scores_out) scores_out[h * c_cap + c] = acc[g];
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) qn[g] += __shfl_xor_sync(0xffffffffu, qn[g], o);
+#pragma unroll
+    for (int r = 0; r < SC_ROWS; ++r) {
+      mn[r] += __shfl_xor_sync(0xffffffffu, mn[r], o);
+#pragma unroll
+      for (int g = 0; g < G; ++g) dg[r][g] += __shfl_xor_sync(0xffffffffu, dg[r][g], o);
+    }
+  }
+  // every lane holds every sum; lane (r*G + g) stores (row r, head g)
+  float qs[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) qs[g] = SEL_ERR * sqrtf(qn[g]);
+#pragma unroll
+  for (int r = 0; r < SC_ROWS; ++r) {
+    const float ms = sqrtf(mn[r]);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (lane == ((r * G + g) & 31) && c0 + r < C) {
+        const size_t o = (size_t(unit) * G + g) * c_pad + c0 + r;
+        aval[o] = dg[r][g];
+        aerr[o] = fmaf(qs[g], ms, 1e-30f);
+      }
+    }
   }
 }
 
-__global__ void __launch_bounds__(128)
-k_rank(ckv_select_desc desc, uint32_t c_pad, uint32_t row_base,
-       const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ n_clusters,
-       const uint32_t* __restrict__ sizes, const uint32_t* __restrict__ starts,
-       const uint32_t* __restrict__ sorted_ids, uint32_t* __restrict__ token_ids,
-       uint32_t* __restrict__ rows_out, uint32_t* __restrict__ n_tokens,
-       uint32_t* __restrict__ n_taken_out, uint32_t* __restrict__ trimmed_out,
-       uint32_t* __restrict__ ranked_out, CacheDev cache) {
-  const int lane = lane_id();
-  const int wpb = blockDim.x >> 5;
-  const uint32_t h = blockIdx.x * wpb + warp_id();
+// ---------------------------------------------------------------------------
+// K2
+// ---------------------------------------------------------------------------
+struct WarpSel {  // per-warp static bookkeeping
+  uint32_t cand[SW_MAXCAND];
+  unsigned long long ckey[SW_MAXCAND];
+  uint32_t hist[256];
+};
+
+// per-warp phase timestamps, compiled in with -DCKV_SEL_DEBUG and enabled by
+// CKV_DEBUG_TIMING=1 (diagnostics only; absent from the product build)
+__device__ unsigned long long* g_sel_dbg = nullptr;
+__device__ __forceinline__ void dbg_stamp(uint32_t h, int slot) {
+#ifdef CKV_SEL_DEBUG
+  if (g_sel_dbg && lane_id() == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sel_dbg[size_t(h) * 8 + slot] = t;
+  }
+#else
+  (void)h;
+  (void)slot;
+#endif
+}
+
+__global__ void __launch_bounds__(SW_WARPS * 32)
+k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_base,
+              const float* __restrict__ q, const float* __restrict__ cents,
+              const float* __restrict__ aval, const float* __restrict__ aerr,
+              const uint32_t* __restrict__ n_clusters, const uint32_t* __restrict__ sizes,
+              const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
+              uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
+              uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
+              uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
+              double* __restrict__ scores_out, CacheDev cache, uint32_t warp_bytes) {
+  const int lane = lane_id(), wid = warp_id();
+  const uint32_t h = blockIdx.x * SW_WARPS + wid;
   if (h >= desc.n_q) return;
+  dbg_stamp(h, 0);
   const uint32_t unit = h / desc.group;
   const uint32_t C = n_clusters[unit];
+  const uint32_t B = desc.budget;
   extern __shared__ __align__(16) unsigned char smraw[];
-  // per warp: keys u64[c_pad] | order u32[c_pad] | taken u32[c_pad] | offsets u32[c_pad]
-  unsigned long long* kg = reinterpret_cast<unsigned long long*>(smraw) + size_t(warp_id()) * c_pad;
-  uint32_t* og = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned long long*>(smraw) +
-                                             size_t(wpb) * c_pad) + size_t(warp_id()) * 3 * c_pad;
-  uint32_t* taken_c = og + c_pad;
-  uint32_t* taken_off = og + 2 * c_pad;
+  unsigned char* wbase = smraw + size_t(wid) * warp_bytes;
+  unsigned long long* xkey = reinterpret_cast<unsigned long long*>(wbase);  // [p2]
+  uint32_t* ids = reinterpret_cast<uint32_t*>(xkey + p2);                    // [p2]
+  uint32_t* incl = ids + p2;                                                 // [p2]
+  float (*stage)[D] = reinterpret_cast<float (*)[D]>(wbase);                 // [SW_STAGE][D]
+  __shared__ WarpSel wsa[SW_WARPS];
+  WarpSel& ws = wsa[wid];
 
-  const unsigned long long* kin = keys + size_t(h) * c_pad;
-  for (uint32_t c = lane; c < C; c += 32) kg[c] = kin[c];
-  __syncwarp();
-  // per-lane insertion sort of clusters c = lane + 32k (k-major layout)
-  const uint32_t cnt = C > uint32_t(lane) ? (C - lane + 31) / 32 : 0;
-  for (uint32_t k = 0; k < cnt; ++k) {
-    const uint32_t c = lane + 32 * k;
-    const unsigned long long kc = kg[c];
-    uint32_t pos = k;
-    while (pos > 0) {
-      const uint32_t prev = og[(pos - 1) * 32 + lane];
-      const unsigned long long kp = kg[prev];
-      if (kp > kc || (kp == kc && prev < c)) break;
-      og[pos * 32 + lane] = prev;
-      --pos;
-    }
-    og[pos * 32 + lane] = c;
-  }
-  __syncwarp();
-
+  const float* cu = cents + size_t(unit) * desc.c_cap * D;
   const uint32_t* sz = sizes + size_t(unit) * desc.c_cap;
   const uint32_t* stt = starts + size_t(unit) * (desc.c_cap + 1);
-  uint32_t* rk = ranked_out + size_t(h) * desc.c_cap;
-  const bool full = (desc.flags & CKV_SEL_FULL_RANK) != 0;
-  uint32_t head = 0, cum = 0, taken = 0, trimmed = 0;
-  uint32_t my_c = cnt > 0 ? og[lane] : 0xffffffffu;
-  unsigned long long my_k = cnt > 0 ? kg[my_c] : 0ull;
-  uint32_t my_sz = cnt > 0 ? sz[my_c] : 0u;
-  bool my_valid = cnt > 0;
-  for (uint32_t r = 0; r < C; ++r) {
-    if (!full && cum >= desc.budget) break;
-    unsigned long long bk = my_valid ? my_k : 0ull;
-    uint32_t bc = my_valid ? my_c : 0xffffffffu;
+  const float4* qh4 = reinterpret_cast<const float4*>(q + size_t(h) * D);
+  const bool exhaustive_req = (desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) != 0;
+  bool fast = !exhaustive_req && C <= 32u * SW_KPL;
+  uint32_t taken = 0;
+
+  if (fast) {
+    // ---- 1. approximate pops ------------------------------------------------
+    const float* av = aval + size_t(h) * c_pad;
+    const float* ae = aerr + size_t(h) * c_pad;
+    unsigned long long kr[SW_KPL];
+    uint32_t szr[SW_KPL];
+    float er[SW_KPL];
+    bool bad = false;  // non-finite scores (NaN centroids): exhaustive path
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      const uint32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
-      if (ok > bk || (ok == bk && oc < bc)) { bk = ok; bc = oc; }
+    for (int k = 0; k < SW_KPL; ++k) {
+      const uint32_t c = lane + 32 * k;
+      const float a = c < C ? av[c] : 0.f;
+      er[k] = c < C ? ae[c] : 0.f;
+      kr[k] = c < C ? ((unsigned long long)fkey(a) << 32) | (0xffffffffu - c) : 0ull;
+      szr[k] = c < C ? __ldg(sz + c) : 0u;
+      bad |= c < C && !(isfinite(a) && isfinite(er[k]));
     }
-    const bool mine = my_valid && bc == my_c;
-    const uint32_t s = __shfl_sync(0xffffffffu, my_sz, __ffs(__ballot_sync(0xffffffffu, mine)) - 1);
-    if (mine) {
-      ++head;
-      my_valid = head < cnt;
-      if (my_valid) { my_c = og[head * 32 + lane]; my_k = kg[my_c]; my_sz = sz[my_c]; }
+    // size-weighted radix select on the fp32 keys: tau = the largest key with
+    // sum_{key >= tau} size >= B (U = {key >= tau}); all of C when the total
+    // labeled size is below B.  Four 8-bit passes over warp-private bins.
+    uint32_t* hist = ws.hist;
+    uint32_t prefix = 0, above = 0;
+    uint32_t total = 0;
+#pragma unroll
+    for (int k = 0; k < SW_KPL; ++k) total += szr[k];
+    total = __reduce_add_sync(0xffffffffu, total);
+    uint32_t tau = 0;
+    if (total > B) {
+      for (int pass = 0; pass < 4; ++pass) {
+        const int sh = 24 - 8 * pass;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < SW_KPL; ++k) {
+          const uint32_t key = uint32_t(kr[k] >> 32);
+          const bool match = pass == 0 || (key >> (sh + 8)) == (prefix >> (sh + 8));
+          if (szr[k] && match) atomicAdd(&hist[(key >> sh) & 255u], szr[k]);
+        }
+        __syncwarp();
+        uint32_t loc[8], lsum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { loc[i] = hist[lane * 8 + i]; lsum += loc[i]; }
+        // suffix sum over lanes above me
+        uint32_t suf = lsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_down_sync(0xffffffffu, suf, o);
+          if (lane + o < 32) suf += y;
+        }
+        uint32_t run = above + suf - lsum;  // weight of bins above my 8
+        int dsel = -1;
+        uint32_t above_sel = 0;
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+          if (dsel < 0 && run + loc[i] >= B) { dsel = lane * 8 + i; above_sel = run; }
+          run += loc[i];
+        }
+        // the highest digit reaching B: the highest lane that found one
+        const unsigned found = __ballot_sync(0xffffffffu, dsel >= 0);
+        const int src = 31 - __clz(found);
+        const int d = __shfl_sync(0xffffffffu, dsel, src);
+        above = __shfl_sync(0xffffffffu, above_sel, src);
+        prefix |= uint32_t(d) << sh;
+        __syncwarp();
+      }
+      tau = prefix;
     }
-    if (lane == 0) rk[r] = bc;
-    if (cum < desc.budget) {  // take cluster bc (selection.hpp:92-106)
-      const uint32_t rem = desc.budget - cum;
-      const uint32_t take = s <= rem ? s : rem;
-      if (lane == 0) { taken_c[taken] = bc; taken_off[taken] = cum; }
-      if (s > rem) trimmed = s - rem;
-      cum += take;
-      ++taken;
+    fast = !__any_sync(0xffffffffu, bad);
+    if (fast) {
+      // L = min over U = {key >= tau} of (a - E)
+      float lower = INFINITY;
+#pragma unroll
+      for (int k = 0; k < SW_KPL; ++k) {
+        const uint32_t c = lane + 32 * k;
+        if (c < C && uint32_t(kr[k] >> 32) >= tau) lower = fminf(lower, av[c] - er[k]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lower = fminf(lower, __shfl_xor_sync(0xffffffffu, lower, o));
+      // ---- 2. candidates S = {c : a + E >= L} -----------------------------------
+      uint32_t nc = 0;
+#pragma unroll
+      for (int k = 0; k < SW_KPL; ++k) {
+        const uint32_t c = lane + 32 * k;
+        bool in = false;
+        if (c < C) in = av[c] + er[k] >= lower;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        const uint32_t pos = nc + __popc(bal & ((1u << lane) - 1u));
+        if (in && pos < uint32_t(SW_MAXCAND)) ws.cand[pos] = c;
+        nc += __popc(bal);
+      }
+      fast = nc <= uint32_t(SW_MAXCAND);
+      __syncwarp();
+      if (fast) {
+        dbg_stamp(h, 1);
+        // ---- 3. exact f64 re-score of S (rows staged through smem) ---------------
+        for (uint32_t b = 0; b < nc; b += SW_STAGE) {
+          const uint32_t nb = min(uint32_t(SW_STAGE), nc - b);
+          for (uint32_t r = 0; r < nb; ++r)
+            cp_async16_sel(&stage[r][4 * lane], cu + size_t(ws.cand[b + r]) * D + 4 * lane, true);
+          asm volatile("cp.async.commit_group;\n");
+          asm volatile("cp.async.wait_group 0;\n");
+          __syncwarp();
+          if (uint32_t(lane) < nb) {
+            double acc = 0.0;
+            const float4* row = reinterpret_cast<const float4*>(&stage[lane][0]);
+#pragma unroll 8
+            for (int j4 = 0; j4 < D / 4; ++j4) {
+              const float4 m = row[j4], qq = __ldg(qh4 + j4);
+              acc = __fma_rn(double(qq.x), double(m.x), acc);
+              acc = __fma_rn(double(qq.y), double(m.y), acc);
+              acc = __fma_rn(double(qq.z), double(m.z), acc);
+              acc = __fma_rn(double(qq.w), double(m.w), acc);
+            }
+            ws.ckey[b + lane] = rank_key(acc);
+          }
+          __syncwarp();
+        }
+        // exact rank of every candidate within S -> ids[rank]
+        for (uint32_t i = lane; i < nc; i += 32) {
+          const unsigned long long ki = ws.ckey[i];
+          const uint32_t ci = ws.cand[i];
+          uint32_t r = 0;
+          for (uint32_t j = 0; j < nc; ++j) r += rank_before(ws.ckey[j], ws.cand[j], ki, ci);
+          ids[r] = ci;
+        }
+        __syncwarp();
+        // sizes in exact order -> inclusive prefix, cutoff at the budget
+        uint32_t carry = 0;
+        taken = nc;
+        for (uint32_t b = 0; b < nc; b += 32) {
+          const uint32_t i = b + lane;
+          uint32_t x = i < nc ? __ldg(sz + ids[i]) : 0u;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          x += carry;
+          if (i < nc) incl[i] = x;
+          const unsigned hit = __ballot_sync(0xffffffffu, i < nc && x >= B);
+          if (hit && taken == nc) taken = b + __ffs(hit);  // first r with incl >= B, plus one
+          carry = __shfl_sync(0xffffffffu, x, 31);
+        }
+        __syncwarp();
+      }
     }
   }
-  __syncwarp();
-  // flat parallel fill of the taken slices: entry e (< cum) belongs to the
-  // last taken cluster whose offset is <= e (binary search in smem)
+
+  if (!fast) {
+    // ---- exhaustive: exact f64 scores for all C + warp bitonic sort -----------
+    for (uint32_t c = lane; c < p2; c += 32) {
+      if (c < C) {
+        const float4* row = reinterpret_cast<const float4*>(cu + size_t(c) * D);
+        double acc = 0.0;
+#pragma unroll 4
+        for (int j4 = 0; j4 < D / 4; ++j4) {
+          const float4 m = __ldg(row + j4), qq = __ldg(qh4 + j4);
+          acc = __fma_rn(double(qq.x), double(m.x), acc);
+          acc = __fma_rn(double(qq.y), double(m.y), acc);
+          acc = __fma_rn(double(qq.z), double(m.z), acc);
+          acc = __fma_rn(double(qq.w), double(m.w), acc);
+        }
+        xkey[c] = rank_key(acc);
+        ids[c] = c;
+        if (scores_out) scores_out[size_t(h) * desc.c_cap + c] = acc;
+      } else {
+        xkey[c] = 0ull;
+        ids[c] = 0xffffffffu;  // padding sorts after every real cluster
+      }
+    }
+    __syncwarp();
+    for (uint32_t k = 2; k <= p2; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = lane; i < p2; i += 32) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const unsigned long long ka = xkey[i], kb = xkey[ixj];
+            const uint32_t ia = ids[i], ib = ids[ixj];
+            const bool asc = (i & k) == 0;
+            const bool swap = asc ? rank_before(kb, ib, ka, ia) : rank_before(ka, ia, kb, ib);
+            if (swap) { xkey[i] = kb; xkey[ixj] = ka; ids[i] = ib; ids[ixj] = ia; }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    uint32_t carry = 0;
+    taken = C;
+    for (uint32_t b = 0; b < C; b += 32) {
+      const uint32_t i = b + lane;
+      uint32_t x = i < C ? __ldg(sz + ids[i]) : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      x += carry;
+      if (i < C) incl[i] = x;
+      const unsigned hit = __ballot_sync(0xffffffffu, i < C && x >= B);
+      if (hit && taken == C) taken = b + __ffs(hit);
+      carry = __shfl_sync(0xffffffffu, x, 31);
+    }
+    __syncwarp();
+  }
+  dbg_stamp(h, 2);
+
+  // ---- outputs ---------------------------------------------------------------
+  const uint32_t full_cum = taken ? incl[taken - 1] : 0;
+  const uint32_t cum = full_cum < B ? full_cum : B;
+  const uint32_t trimmed = full_cum > B ? full_cum - B : 0;
+  uint32_t* rk = ranked_out + size_t(h) * desc.c_cap;
+  const uint32_t n_rank = (!fast && (desc.flags & CKV_SEL_FULL_RANK)) ? C : taken;
+  for (uint32_t i = lane; i < n_rank; i += 32) rk[i] = ids[i];
+  const uint32_t sinks = desc.sink_count;
+  const uint32_t nrec = desc.rec_end > desc.rec_begin ? desc.rec_end - desc.rec_begin : 0;
+  const uint32_t n = cum + sinks + nrec;
+  // runs: one per taken cluster, then sinks, then recency (selection.hpp:91-109)
+  if (runs.row) {
+    uint32_t* rr = runs.row + size_t(h) * runs.run_cap;
+    uint32_t* ro = runs.off + size_t(h) * (runs.run_cap + 1);
+    for (uint32_t i = lane; i < taken; i += 32) {
+      rr[i] = row_base + __ldg(stt + ids[i]);
+      ro[i] = i ? incl[i - 1] : 0u;
+    }
+    if (lane == 0) {
+      uint32_t nr = taken;
+      if (sinks) { rr[nr] = 0; ro[nr] = cum; ++nr; }
+      if (nrec) { rr[nr] = desc.rec_begin; ro[nr] = cum + sinks; ++nr; }
+      ro[nr] = n;
+      runs.count[h] = nr;
+    }
+  }
+  // per-entry outputs (parity / position-ordered stores): flat fill
   uint32_t* out = token_ids ? token_ids + size_t(h) * desc.sel_cap : nullptr;
   uint32_t* rows = rows_out ? rows_out + size_t(h) * desc.sel_cap : nullptr;
-  const uint32_t* sid = sorted_ids + size_t(unit) * desc.p_cap;
-  for (uint32_t t = lane; t < taken; t += 32) taken_c[t] = stt[taken_c[t]];  // -> slice start
-  __syncwarp();
-  for (uint32_t e0 = 0; e0 < cum; e0 += 128) {
-    uint32_t src[4];
+  if (out || rows) {
+    const uint32_t* sid = sorted_ids + size_t(unit) * desc.p_cap;
+    for (uint32_t e0 = 0; e0 < cum; e0 += 128) {
+      uint32_t src[4], pos[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t e = e0 + 32 * k + lane;
-      uint32_t lo = 0, hi = taken;  // largest t with taken_off[t] <= e
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (taken_off[mid] <= e) lo = mid; else hi = mid;
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t e = e0 + 32 * k + lane;
+        uint32_t lo = 0, hi = taken;  // first r with incl[r] > e
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (incl[mid] > e) hi = mid; else lo = mid + 1;
+        }
+        const uint32_t before = lo ? incl[lo - 1] : 0;
+        src[k] = (e < cum && lo < taken) ? __ldg(stt + ids[lo]) + (e - before) : 0u;
       }
-      src[k] = taken_c[lo] + (e - taken_off[lo]);
-    }
-    uint32_t pos[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t e = e0 + 32 * k + lane;
-      pos[k] = (out && e < cum) ? __ldg(sid + src[k]) : 0u;
-    }
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t e = e0 + 32 * k + lane;
+        pos[k] = (out && e < cum) ? __ldg(sid + src[k]) : 0u;
+      }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t e = e0 + 32 * k + lane;
-      if (e < cum) {
-        if (rows) rows[e] = row_base + src[k];
-        if (out) out[e] = pos[k];
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t e = e0 + 32 * k + lane;
+        if (e < cum) {
+          if (rows) rows[e] = row_base + src[k];
+          if (out) out[e] = pos[k];
+        }
       }
     }
+    for (uint32_t s2 = lane; s2 < sinks; s2 += 32) {
+      if (rows) rows[cum + s2] = s2;
+      if (out) out[cum + s2] = s2;
+    }
+    for (uint32_t i = lane; i < nrec; i += 32) {
+      if (rows) rows[cum + sinks + i] = desc.rec_begin + i;
+      if (out) out[cum + sinks + i] = desc.rec_begin + i;
+    }
   }
-  uint32_t n = cum;
-  for (uint32_t s = lane; s < desc.sink_count; s += 32) {
-    if (rows) rows[n + s] = s;
-    if (out) out[n + s] = s;
-  }
-  n += desc.sink_count;
-  const uint32_t nrec = desc.rec_end > desc.rec_begin ? desc.rec_end - desc.rec_begin : 0;
-  for (uint32_t i = lane; i < nrec; i += 32) {
-    if (rows) rows[n + i] = desc.rec_begin + i;
-    if (out) out[n + i] = desc.rec_begin + i;
-  }
-  n += nrec;
   if (lane == 0) {
     n_tokens[h] = n;
     n_taken_out[h] = taken;
     trimmed_out[h] = trimmed;
   }
-  // ---- cache (cache.hpp:38-57) ----------------------------------------------
+  // ---- cache (cache.hpp:38-57) -------------------------------------------------
   if (cache.bits) {
     const uint32_t W = cache.words, R = cache.retention;
     uint32_t* bits = cache.bits + size_t(h) * R * W;
@@ -225,8 +474,8 @@ k_rank(ckv_select_desc desc, uint32_t c_pad, uint32_t row_base,
     uint32_t rhead = ring[0], rlen = ring[1];
     uint32_t hits = 0;
     unsigned long long miss_tokens = 0;
-    for (uint32_t t = lane; t < taken; t += 32) {
-      const uint32_t c = rk[t];
+    for (uint32_t i = lane; i < taken; i += 32) {
+      const uint32_t c = ids[i];
       bool res = false;
       for (uint32_t k = 0; k < R; ++k) res |= (bits[size_t(k) * W + (c >> 5)] >> (c & 31)) & 1u;
       if (res) ++hits; else miss_tokens += sz[c];
@@ -240,7 +489,7 @@ k_rank(ckv_select_desc desc, uint32_t c_pad, uint32_t row_base,
     uint32_t* sb = bits + size_t(slot) * W;
     for (uint32_t i = lane; i < W; i += 32) sb[i] = 0u;
     __syncwarp();
-    for (uint32_t t = lane; t < taken; t += 32) atomicOr(&sb[rk[t] >> 5], 1u << (rk[t] & 31));
+    for (uint32_t i = lane; i < taken; i += 32) atomicOr(&sb[ids[i] >> 5], 1u << (ids[i] & 31));
     if (lane == 0) {
       ring[0] = rhead;
       ring[1] = rlen;
@@ -251,18 +500,35 @@ k_rank(ckv_select_desc desc, uint32_t c_pad, uint32_t row_base,
       ctr[3] = ctr[2] * 2ull * cache.d * 4ull;
     }
   }
+  dbg_stamp(h, 3);
 }
 
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap) {
-  return size_t(n_q) * ((c_cap + 31) / 32 * 32) * 8 + 16;
+  const uint32_t c_pad = (c_cap + 31) / 32 * 32;
+  return size_t(n_q) * c_pad * 8 + 64;  // aval + aerr
+}
+
+static void dbg_report(uint32_t n, const unsigned long long* dbuf, float k1_ms, float k2_ms) {
+  std::vector<unsigned long long> hb(size_t(n) * 8);
+  cudaMemcpy(hb.data(), dbuf, hb.size() * 8, cudaMemcpyDeviceToHost);
+  double ph[3] = {0, 0, 0};
+  uint32_t nfast = 0;
+  for (uint32_t b = 0; b < n; ++b) {
+    const unsigned long long* x = &hb[size_t(b) * 8];
+    if (x[1]) { ph[0] += double(x[1] - x[0]); ph[1] += double(x[2] - x[1]); ++nfast; }
+    ph[2] += double(x[3] - x[2]);
+  }
+  fprintf(stderr, "[k_select dbg] K1 %.1f us K2 %.1f us | K2 per-warp us: pop %.2f exact %.2f "
+          "out %.2f | fast %u/%u\n", k1_ms * 1e3, k2_ms * 1e3, nfast ? ph[0] / nfast * 1e-3 : 0,
+          nfast ? ph[1] / nfast * 1e-3 : 0, ph[2] / n * 1e-3, nfast, n);
 }
 
 int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const float* cents, const uint32_t* n_clusters, const uint32_t* sizes,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
-                  uint32_t* rows, uint32_t row_base, uint32_t* n_tokens, uint32_t* n_taken,
-                  uint32_t* trimmed, uint32_t* ranked, double* scores, const CacheDev& cache,
-                  void* scratch) {
+                  uint32_t* rows, const ckv_runs& runs, uint32_t row_base, uint32_t* n_tokens,
+                  uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
+                  const CacheDev& cache, void* scratch) {
   const uint32_t G = desc.group;
   if (G < 1 || desc.n_q % G || !(G == 1 || G == 2 || G == 4 || G == 8)) {
     set_error("select: group must be 1, 2, 4 or 8 and divide n_q");
@@ -271,30 +537,62 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   if (desc.budget < 1) { set_error("select: budget must be >= 1"); return CKV_EINVAL; }
   const uint32_t units = desc.n_q / G;
   const uint32_t c_pad = (desc.c_cap + 31) / 32 * 32;
-  auto* keys = static_cast<unsigned long long*>(scratch);
-  const dim3 gs(units, (c_pad + SC_ROWS - 1) / SC_ROWS);
-  switch (G) {
-    case 1: k_score<1><<<gs, SC_ROWS, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, keys, scores); break;
-    case 2: k_score<2><<<gs, SC_ROWS, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, keys, scores); break;
-    case 4: k_score<4><<<gs, SC_ROWS, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, keys, scores); break;
-    default: k_score<8><<<gs, SC_ROWS, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, keys, scores); break;
+  float* aval = static_cast<float*>(scratch);
+  float* aerr = aval + size_t(desc.n_q) * c_pad;
+  static const bool dbg = getenv("CKV_DEBUG_TIMING") != nullptr;
+  cudaEvent_t ev[3];
+  if (dbg) for (auto& e : ev) cudaEventCreate(&e);
+  if (dbg) cudaEventRecord(ev[0], st);
+  if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES))) {
+    const dim3 g1(units, (c_pad + SC_WARPS * SC_ROWS - 1) / (SC_WARPS * SC_ROWS));
+    switch (G) {
+      case 1: k_score_approx<1><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, aval, aerr); break;
+      case 2: k_score_approx<2><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, aval, aerr); break;
+      case 4: k_score_approx<4><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, aval, aerr); break;
+      default: k_score_approx<8><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, aval, aerr); break;
+    }
+    CKV_LAUNCH_CHECK("k_score_approx");
   }
-  CKV_LAUNCH_CHECK("k_score");
-  const size_t per_warp = size_t(c_pad) * (8 + 12);
-  int wpb = 4;
-  while (wpb > 1 && per_warp * wpb > 200 * 1024) wpb >>= 1;
-  if (per_warp * wpb > 200 * 1024) {
+  if (dbg) cudaEventRecord(ev[1], st);
+  uint32_t p2 = 64;
+  while (p2 < desc.c_cap) p2 <<= 1;
+  const uint32_t warp_bytes =
+      uint32_t(std::max<size_t>(size_t(p2) * 16, size_t(SW_STAGE) * D * 4));
+  const size_t smem = size_t(warp_bytes) * SW_WARPS;
+  if (smem > 200 * 1024) {
     set_error("select: cluster capacity too large for the smem ranking buffers");
     return CKV_EINVAL;
   }
-  const size_t smem = per_warp * wpb;
-  if (smem > 48 * 1024)
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_rank, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(smem)));
-  k_rank<<<(desc.n_q + wpb - 1) / wpb, wpb * 32, smem, st>>>(
-      desc, c_pad, row_base, keys, n_clusters, sizes, starts, sorted_ids, token_ids, rows,
-      n_tokens, n_taken, trimmed, ranked, cache);
-  CKV_LAUNCH_CHECK("k_rank");
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+    attr_dev = dev;
+  }
+  unsigned long long* dbuf = nullptr;
+  if (dbg) {
+    cudaMalloc(&dbuf, size_t(desc.n_q) * 64);
+    cudaMemset(dbuf, 0, size_t(desc.n_q) * 64);
+    cudaMemcpyToSymbol(g_sel_dbg, &dbuf, sizeof(dbuf));
+  }
+  k_select_warp<<<(desc.n_q + SW_WARPS - 1) / SW_WARPS, SW_WARPS * 32, smem, st>>>(
+      desc, p2, c_pad, row_base, q, cents, aval, aerr, n_clusters, sizes, starts, sorted_ids,
+      token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, scores, cache, warp_bytes);
+  CKV_LAUNCH_CHECK("k_select_warp");
+  if (dbg) {
+    cudaEventRecord(ev[2], st);
+    cudaEventSynchronize(ev[2]);
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    dbg_report(desc.n_q, dbuf, a, b);
+    unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_sel_dbg, &z, sizeof(z));
+    cudaFree(dbuf);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   return CKV_OK;
 }
 

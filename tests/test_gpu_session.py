@@ -21,7 +21,8 @@ def test_session_vs_oracle_decode_loop(gpu_ctx):
     U = layers * kvh
     heads = [head(7, u // kvh, u % kvh, L, T) for u in range(U)]
     cfg = api.ClusterConfig(decode_batch=m, c0_divisor=40)
-    s = Session(U, G, L, T, B, retention=R, cfg=cfg, kv_heads=kvh)
+    from paper_2412_03213_b200 import _native as N
+    s = Session(U, G, L, T, B, retention=R, cfg=cfg, kv_heads=kvh, flags=N.CKV_SESSION_TOKEN_IDS)
     s.load_prompt_host(np.stack([bf16_bits(h["K"]) for h in heads]),
                        np.stack([bf16_bits(h["V"]) for h in heads]))
     s.prefill()
