@@ -1,12 +1,491 @@
-// ckv_assign_tc.cu — K1: tensor-core (tcgen05) assignment filter.  (stub)
+// ckv_assign_tc.cu — K1: tensor-core (tcgen05 / TMEM / TMA) assignment pass
+// of cosine k-means (AssignScorer::assign, clustering.hpp:88-115), exact.
+//
+// The reference labels key i with argmax_c dot_f64(k_i, dir_c) (ties -> lowest
+// c), dir_c = normalize(mu_c) in f32.  On B200:
+//   1. a bf16 GEMM S = K . bf16(dir)^T on the 5th-gen tensor cores
+//      (tcgen05.mma kind::f16, fp32 accumulation in TMEM), 128 keys x all C
+//      columns per tile;
+//   2. the epilogue (tcgen05.ld) keeps each key's top-4 approximate scores.
+//      |S_c - s_c| <= E = 2^-9 |k| (bf16 rounding of dir, |dir| = 1) plus
+//      the fp32 accumulation error, so the exact argmax lies in
+//      {c : S_c >= S_max - 2E}.  The band used is 2^-7 |k| (2x margin).
+//      One candidate in band -> that is the label.  Otherwise the key goes to
+//      a fix-up list with its 2-4 candidates (or "all" when the 4th is in
+//      band too) and k_fixup re-scores them with the sequential f64 chain —
+//      bit-identical to dot_f64 — picking the first maximum.  Labels are
+//      therefore bit-exact for every key while the tensor FLOPs stay at 1x.
+//
+// Kernel anatomy (persistent, one CTA per SM, 6 warps):
+//   warp 0  TMA producer: key tiles (2 stages, 128B-swizzled boxes of
+//           128 rows x 64 cols) and, at each unit change, the unit's bf16
+//           directions (resident B operand, up to 512 rows).
+//   warp 1  TMEM allocator + MMA issuer (one elected thread): per tile and
+//           256-column chunk, 8 K=16 steps into TMEM buffer (chunk & 1).
+//   warps 2-5 epilogue: TMEM lane quarter = warp % 4, one key row per thread.
+#include <cuda.h>
+
+#include <vector>
+
 #include "ckv_internal.cuh"
+
 namespace ckvb {
-bool assign_tc_supported(uint32_t, uint32_t) { return false; }
-size_t assign_tc_scratch_bytes(uint32_t, uint32_t, uint32_t) { return 0; }
-int assign_tc(cudaStream_t, const uint16_t*, uint64_t, uint32_t, uint32_t, uint32_t, uint32_t,
-              const uint16_t*, const float*, int32_t*, uint32_t, const int32_t*, void*, size_t,
-              uint64_t*) {
-  set_error("assign_tc: not built");
-  return CKV_EINVAL;
+
+constexpr int TC_M = 128;              // keys per tile (UMMA_M)
+constexpr int TC_BK = 64;              // bf16 columns per 128-B swizzle atom
+constexpr int TC_STAGES = 2;           // key-tile stages
+constexpr int TC_MAXC = 512;           // C_pad limit: B resident, 2 x 256 TMEM cols
+constexpr int TC_CH = 256;             // columns per MMA chunk / TMEM buffer
+constexpr int TC_THREADS = 6 * 32;
+constexpr uint32_t TC_FULL = 0xffffffffu;
+
+struct TcSmem {
+  // 1024-B aligned operand regions (SWIZZLE_128B atoms)
+  uint8_t a[TC_STAGES][2][TC_M * 128];  // [stage][k-half][128 rows x 128 B]   64 KB
+  uint8_t b[2][TC_MAXC * 128];          // [k-half][C_pad rows x 128 B]      128 KB
+  uint64_t a_full[TC_STAGES], a_empty[TC_STAGES];
+  uint64_t b_full, b_empty;
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+// K-major, SWIZZLE_128B smem matrix descriptor (tcgen05 "version 1"):
+// start >> 4 | LBO (unused for swizzled K-major) = 1 | SBO = 1024 B (8 rows)
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3fff);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;  // version
+  d |= uint64_t(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: kind::f16, A/B bf16, D f32, K-major A and B
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; "
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
+                   "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcArgs {
+  const int32_t* unit_list;  // active units
+  const int32_t* n_list;     // device count of active units
+  uint32_t n, C, c_pad, tiles_per_unit;
+  uint32_t key_rows_per_unit;  // key_stride / 128
+  uint32_t label_stride;
+  const float* knorm;          // [unit][n] key norms (band scale)
+  int32_t* labels;
+  uint32_t* fix_count;         // device counter
+  uint4* fix_list;             // {unit, row, n_cand | FULL, packed ids}
+  uint32_t fix_cap;
+  uint32_t* fix_ids;           // [fix_cap][4] candidate ids
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap dmap,
+            TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  TcSmem& sm = *reinterpret_cast<TcSmem*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
+  const uint32_t n_units = uint32_t(*a.n_list);
+  const uint32_t total = n_units * a.tiles_per_unit;
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t w0 = min(total, blockIdx.x * per), w1 = min(total, w0 + per);
+  const uint32_t nchunks = (a.c_pad + TC_CH - 1) / TC_CH;
+
+  if (t == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) { mb_init(&sm.a_full[s], 1); mb_init(&sm.a_empty[s], 1); }
+    mb_init(&sm.b_full, 1);
+    mb_init(&sm.b_empty, 1);
+    for (int s = 0; s < 2; ++s) { mb_init(&sm.acc_full[s], 1); mb_init(&sm.acc_empty[s], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (wid == 1) {  // TMEM: 512 columns (two 256-column accumulator buffers)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     su32(&sm.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (wid == 0) {
+    // ============================ TMA producer =================================
+    if (lane == 0 && w0 < w1) {
+      uint32_t st = 0, ph = 0, bswitch = 0, cur_unit = TC_FULL;
+      // full TMA boxes are counted even past c_pad (rows read but unused)
+      const uint32_t box_rows = min(256u, a.c_pad);
+      const uint32_t bbytes = ((a.c_pad + box_rows - 1) / box_rows) * box_rows * 128 * 2;
+      for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t ui = w / a.tiles_per_unit, tile = w % a.tiles_per_unit;
+        const uint32_t unit = uint32_t(a.unit_list[ui]);
+        if (unit != cur_unit) {
+          // the previous unit's MMAs must be done reading B
+          if (cur_unit != TC_FULL) mb_wait(&sm.b_empty, (bswitch - 1) & 1);
+          mb_expect(&sm.b_full, bbytes);
+          for (uint32_t r0 = 0; r0 < a.c_pad; r0 += box_rows) {
+            for (int kh = 0; kh < 2; ++kh)
+              tma_2d(&sm.b[kh][r0 * 128], &dmap, kh * TC_BK, int(unit * a.c_pad + r0),
+                     &sm.b_full);
+          }
+          cur_unit = unit;
+          ++bswitch;
+        }
+        mb_wait(&sm.a_empty[st], ph ^ 1);
+        mb_expect(&sm.a_full[st], TC_M * 128 * 2);
+        const int row = int(unit * a.key_rows_per_unit + tile * TC_M);
+        tma_2d(&sm.a[st][0][0], &kmap, 0, row, &sm.a_full[st]);
+        tma_2d(&sm.a[st][1][0], &kmap, TC_BK, row, &sm.a_full[st]);
+        if (++st == TC_STAGES) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (wid == 1) {
+    // ============================ MMA issuer ===================================
+    if (lane == 0 && w0 < w1) {
+      uint32_t st = 0, ph = 0, g = 0, bswitch = 0, cur_unit = TC_FULL;
+      for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t ui = w / a.tiles_per_unit;
+        const uint32_t unit = uint32_t(a.unit_list[ui]);
+        const bool last_of_unit =
+            (w + 1 == w1) || (uint32_t(a.unit_list[(w + 1) / a.tiles_per_unit]) != unit);
+        if (unit != cur_unit) {
+          mb_wait(&sm.b_full, bswitch & 1);
+          cur_unit = unit;
+          ++bswitch;
+        }
+        mb_wait(&sm.a_full[st], ph);
+        tc_fence_after();
+        for (uint32_t ch = 0; ch < nchunks; ++ch, ++g) {
+          const uint32_t buf = g & 1, bph = (g >> 1) & 1;
+          const uint32_t c0 = ch * TC_CH;
+          const uint32_t nc = min(uint32_t(TC_CH), a.c_pad - c0);
+          mb_wait(&sm.acc_empty[buf], bph ^ 1);
+          tc_fence_after();
+          const uint32_t idesc = idesc_bf16_f32(TC_M, nc);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const int kh = kk >> 2, ko = (kk & 3) * 32;  // 16 bf16 = 32 B per K step
+            const uint64_t ad = kmajor_sw128_desc(su32(&sm.a[st][kh][0]) + ko);
+            const uint64_t bd = kmajor_sw128_desc(su32(&sm.b[kh][c0 * 128]) + ko);
+            umma_bf16(tmem + buf * TC_CH, ad, bd, idesc, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&sm.acc_full[buf]);
+        }
+        umma_commit(&sm.a_empty[st]);  // key tile consumed once these MMAs finish
+        if (last_of_unit) umma_commit(&sm.b_empty);
+        if (++st == TC_STAGES) { st = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // ============================ epilogue =====================================
+    const uint32_t quarter = wid & 3;  // TMEM lanes [32q, 32q+32)
+    const uint32_t lane_row = quarter * 32 + lane;
+    uint32_t g = 0;
+    for (uint32_t w = w0; w < w1; ++w) {
+      const uint32_t ui = w / a.tiles_per_unit, tile = w % a.tiles_per_unit;
+      const uint32_t unit = uint32_t(a.unit_list[ui]);
+      const uint32_t row = tile * TC_M + lane_row;
+      float s0 = -INFINITY, s1 = -INFINITY, s2 = -INFINITY, s3 = -INFINITY;
+      uint32_t i0 = 0, i1 = 0, i2 = 0, i3 = 0;
+      for (uint32_t ch = 0; ch < nchunks; ++ch, ++g) {
+        const uint32_t buf = g & 1, bph = (g >> 1) & 1;
+        const uint32_t c0 = ch * TC_CH;
+        const uint32_t nc = min(uint32_t(TC_CH), a.c_pad - c0);
+        mb_wait(&sm.acc_full[buf], bph);
+        tc_fence_after();
+        const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * TC_CH;
+        for (uint32_t cc = 0; cc < nc; cc += 16) {
+          float v[16];
+          tmem_ld16(taddr + cc, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t c = c0 + cc + j;
+            const float x = c < a.C ? v[j] : -INFINITY;
+            if (x > s3) {  // NaN never enters (clustering.hpp:109 strict >)
+              if (x > s0) { s3 = s2; i3 = i2; s2 = s1; i2 = i1; s1 = s0; i1 = i0; s0 = x; i0 = c; }
+              else if (x > s1) { s3 = s2; i3 = i2; s2 = s1; i2 = i1; s1 = x; i1 = c; }
+              else if (x > s2) { s3 = s2; i3 = i2; s2 = x; i2 = c; }
+              else { s3 = x; i3 = c; }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mb_arrive(&sm.acc_empty[buf]);
+      }
+      if (row < a.n) {
+        const float kn = a.knorm[size_t(unit) * a.n + row];
+        const float band = kn * (1.0f / 128.0f) * 1.01f + 1e-30f;  // 2 * 2^-8 |k|, margin
+        int32_t* lab = a.labels + size_t(unit) * a.label_stride + row;
+        const bool none = !(s0 > -INFINITY);
+        const float lo = s0 - band;
+        const uint32_t nin = none ? 0u : 1u + (s1 >= lo) + (s2 >= lo) + (s3 >= lo);
+        if (nin == 1) {
+          *lab = int32_t(i0);
+        } else {
+          *lab = -1;
+          const bool full = none || s3 >= lo;
+          const unsigned want = __ballot_sync(__activemask(), true);
+          const uint32_t leader = __ffs(want) - 1;
+          uint32_t base = 0;
+          if (uint32_t(lane) == leader) base = atomicAdd(a.fix_count, __popc(want));
+          base = __shfl_sync(want, base, leader);
+          const uint32_t slot = base + __popc(want & ((1u << lane) - 1u));
+          if (slot < a.fix_cap) {
+            a.fix_list[slot] = make_uint4(unit, row, full ? TC_FULL : nin, 0u);
+            uint32_t* ids = a.fix_ids + size_t(slot) * 4;
+            ids[0] = i0; ids[1] = i1; ids[2] = i2; ids[3] = i3;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (wid == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// exact re-score of the fix-up keys: one warp per key, one lane per
+// candidate, sequential f64 chain over d = 128 (dot_f64), first maximum wins
+__global__ void __launch_bounds__(256)
+k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
+        const uint32_t* __restrict__ count, const uint16_t* __restrict__ keys,
+        uint64_t key_stride, const float* __restrict__ dirs, uint32_t C, uint32_t c_pad,
+        int32_t* __restrict__ labels, uint32_t label_stride) {
+  const uint32_t nfix = *count;
+  const int lane = lane_id();
+  for (uint32_t e = blockIdx.x * (blockDim.x >> 5) + warp_id(); e < nfix;
+       e += gridDim.x * (blockDim.x >> 5)) {
+    const uint4 it = list[e];
+    const uint32_t unit = it.x, row = it.y;
+    const uint16_t* kr = keys + unit * key_stride + size_t(row) * D;
+    const float* du = dirs + size_t(unit) * c_pad * D;
+    double best = -INFINITY;
+    uint32_t bid = 0xffffffffu;
+    auto score = [&](uint32_t c) {
+      const float* dc = du + size_t(c) * D;
+      double s = 0.0;
+#pragma unroll 8
+      for (int j = 0; j < D; ++j) s = __fma_rn(double(bf16_to_f32(kr[j])), double(__ldg(dc + j)), s);
+      if (s > best || (s == best && c < bid)) { best = s; bid = c; }
+    };
+    if (it.z == TC_FULL) {
+      for (uint32_t c = lane; c < C; c += 32) score(c);
+    } else if (uint32_t(lane) < it.z) {
+      score(ids[size_t(e) * 4 + lane]);
+    }
+    // warp argmax: max score, ties -> lowest id; NaN never wins (strict >)
+    for (int o = 16; o > 0; o >>= 1) {
+      const double os = __shfl_xor_sync(0xffffffffu, best, o);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, bid, o);
+      if (os > best || (os == best && oi < bid)) { best = os; bid = oi; }
+    }
+    if (lane == 0) labels[size_t(unit) * label_stride + row] = int32_t(bid == 0xffffffffu ? 0 : bid);
+  }
+}
+
+__global__ void k_key_norms(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
+                            float* __restrict__ knorm) {
+  const uint32_t u = blockIdx.y;
+  const uint32_t i = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (i >= n) return;
+  const uint2 v = reinterpret_cast<const uint2*>(keys + u * key_stride + size_t(i) * D)[lane_id()];
+  const float a = __uint_as_float(v.x << 16), b = __uint_as_float(v.x & 0xffff0000u);
+  const float c = __uint_as_float(v.y << 16), d = __uint_as_float(v.y & 0xffff0000u);
+  const float s = warp_sum(a * a + b * b + c * c + d * d);
+  if (lane_id() == 0) knorm[size_t(u) * n + i] = sqrtf(s) * 1.0001f;  // rounding margin
+}
+
+__global__ void k_compact_active(const int32_t* __restrict__ active, uint32_t n_units,
+                                  int32_t* __restrict__ list, int32_t* __restrict__ count,
+                                  uint32_t* __restrict__ fix_count) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int32_t n = 0;
+    for (uint32_t u = 0; u < n_units; ++u)
+      if (!active || active[u]) list[n++] = int32_t(u);
+    *count = n;
+    *fix_count = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+bool assign_tc_supported(uint32_t n, uint32_t C) {
+  const uint32_t c_pad = (C + 31) / 32 * 32;
+  return C >= 32 && c_pad <= uint32_t(TC_MAXC) && n >= uint32_t(TC_M);
+}
+
+namespace {
+struct TcScratch {
+  int32_t* list;
+  int32_t* count;
+  uint32_t* fix_count;
+  uint4* fix_list;
+  uint32_t* fix_ids;
+  float* knorm;
+  uint32_t fix_cap;
+};
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+TcScratch carve(void* base, uint32_t n_units, uint32_t n) {
+  TcScratch s;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  s.list = reinterpret_cast<int32_t*>(p);
+  p += align256(size_t(n_units) * 4);
+  s.count = reinterpret_cast<int32_t*>(p);
+  p += 256;
+  s.fix_count = reinterpret_cast<uint32_t*>(p);
+  p += 256;
+  s.fix_cap = n_units * n;  // every key can need a fix-up
+  s.fix_list = reinterpret_cast<uint4*>(p);
+  p += align256(size_t(s.fix_cap) * 16);
+  s.fix_ids = reinterpret_cast<uint32_t*>(p);
+  p += align256(size_t(s.fix_cap) * 16);
+  s.knorm = reinterpret_cast<float*>(p);
+  return s;
+}
+int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
+  const cuuint64_t dims[2] = {cuuint64_t(D), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(D) * 2};
+  const cuuint32_t box[2] = {cuuint32_t(TC_BK), cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                      const_cast<void*>(base), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return CKV_ECUDA;
+  }
+  return CKV_OK;
+}
+}  // namespace
+
+// key norms (the band scale): once per k-means run, keys never change
+int assign_tc_prepare(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
+                      uint32_t n_units, void* scratch) {
+  TcScratch s = carve(scratch, n_units, n);
+  k_key_norms<<<dim3((n + 7) / 8, n_units), 256, 0, st>>>(keys, key_stride, n, s.knorm);
+  CKV_LAUNCH_CHECK("k_key_norms");
+  return CKV_OK;
+}
+
+size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
+  (void)C;
+  return align256(size_t(n_units) * 4) + 512 + 2 * align256(size_t(n_units) * n * 16) +
+         align256(size_t(n_units) * n * 4) + 256;
+}
+
+int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
+              uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs_bf,
+              const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
+              void* scratch, size_t scratch_bytes, uint64_t* launches) {
+  (void)scratch_bytes;
+  if (key_stride % D) {
+    set_error("assign_tc: key stride must be a whole number of rows");
+    return CKV_EINVAL;
+  }
+  TcScratch s = carve(scratch, n_units, n);
+  k_compact_active<<<1, 32, 0, st>>>(active, n_units, s.list, s.count, s.fix_count);
+  CKV_LAUNCH_CHECK("k_compact_active");
+  CUtensorMap kmap, dmap;
+  const uint32_t rows_per_unit = uint32_t(key_stride / D);
+  CKV_TRY(encode_2d(&kmap, keys, uint64_t(n_units - 1) * rows_per_unit + n, TC_M));
+  CKV_TRY(encode_2d(&dmap, dirs_bf, uint64_t(n_units) * c_pad, std::min<uint32_t>(256, c_pad)));
+  TcArgs ta;
+  ta.unit_list = s.list;
+  ta.n_list = s.count;
+  ta.n = n;
+  ta.C = C;
+  ta.c_pad = c_pad;
+  ta.tiles_per_unit = (n + TC_M - 1) / TC_M;
+  ta.key_rows_per_unit = rows_per_unit;
+  ta.label_stride = label_stride;
+  ta.knorm = s.knorm;
+  ta.labels = labels;
+  ta.fix_count = s.fix_count;
+  ta.fix_list = s.fix_list;
+  ta.fix_cap = s.fix_cap;
+  ta.fix_ids = s.fix_ids;
+  const size_t smem = sizeof(TcSmem) + 1024;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    CKV_CUDA_TRY(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(smem)));
+    attr_dev = dev;
+  }
+  k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
+  CKV_LAUNCH_CHECK("k_assign_tc");
+  k_fixup<<<num_sms() * 4, 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, keys, key_stride,
+                                          dirs, C, c_pad, labels, label_stride);
+  CKV_LAUNCH_CHECK("k_fixup");
+  *launches += 3;
+  return CKV_OK;
+}
+
 }  // namespace ckvb

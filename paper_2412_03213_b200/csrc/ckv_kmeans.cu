@@ -347,6 +347,8 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
               const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
               void* scratch, size_t scratch_bytes, uint64_t* launches);
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C);
+int assign_tc_prepare(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
+                      uint32_t n_units, void* scratch);
 bool assign_tc_supported(uint32_t n, uint32_t C);
 
 // ---------------------------------------------------------------------------
@@ -404,7 +406,11 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
 
   const bool use_tc = !(a.flags & CKV_KM_EXACT_ONLY) && assign_tc_supported(n, C);
   size_t tc_bytes = use_tc ? assign_tc_scratch_bytes(U, n, C) : 0;
-  if (use_tc) CKV_TRY(dalloc(b_tc, tc_bytes));
+  if (use_tc) {
+    CKV_TRY(dalloc(b_tc, tc_bytes));
+    CKV_TRY(assign_tc_prepare(st, a.keys, a.key_stride, n, U, b_tc.p));
+    ctx->launches++;
+  }
 
   if (!ctx->h_flags || ctx->h_flags_cap < U + 1) {
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
