@@ -33,21 +33,22 @@ namespace ckvb {
 
 constexpr int TC_M = 128;              // keys per tile (UMMA_M)
 constexpr int TC_BK = 64;              // bf16 columns per 128-B swizzle atom
-constexpr int TC_STAGES = 2;           // key-tile stages
 constexpr int TC_MAXC = 512;           // C_pad limit: B resident, 2 x 256 TMEM cols
 constexpr int TC_CH = 256;             // columns per MMA chunk / TMEM buffer
 constexpr int TC_THREADS = 6 * 32;
 constexpr uint32_t TC_FULL = 0xffffffffu;
 
-struct TcSmem {
-  // 1024-B aligned operand regions (SWIZZLE_128B atoms)
-  uint8_t a[TC_STAGES][2][TC_M * 128];  // [stage][k-half][128 rows x 128 B]   64 KB
-  uint8_t b[2][TC_MAXC * 128];          // [k-half][C_pad rows x 128 B]      128 KB
-  uint64_t a_full[TC_STAGES], a_empty[TC_STAGES];
+// dynamic smem (1024-B aligned base): A stages [stages][2 k-halves][128 x 128 B],
+// then B [2 k-halves][c_pad x 128 B], then the barriers.  B is the resident
+// operand for one unit; A (key tiles) streams.
+struct TcBars {
+  uint64_t a_full[4], a_empty[4];
   uint64_t b_full, b_empty;
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
 };
+constexpr uint32_t TC_ABYTES = TC_M * 128 * 2;  // one key-tile stage (both k-halves)
+constexpr uint32_t TC_BOXR = 32;                // rows per B TMA box (B sized to c_pad)
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -125,7 +126,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 32 bit, 32 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 struct TcArgs {
+  uint32_t stages;           // key-tile stages that fit next to B
   const int32_t* unit_list;  // active units
   const int32_t* n_list;     // device count of active units
   uint32_t n, C, c_pad, tiles_per_unit;
@@ -134,17 +154,23 @@ struct TcArgs {
   const float* knorm;          // [unit][n] key norms (band scale)
   int32_t* labels;
   uint32_t* fix_count;         // device counter
-  uint4* fix_list;             // {unit, row, n_cand | FULL, packed ids}
+  uint4* fix_list;             // {unit, row, n_cand | FULL, 0}
   uint32_t fix_cap;
-  uint32_t* fix_ids;           // [fix_cap][4] candidate ids
+  uint32_t* fix_ids;           // [fix_cap][8] candidate ids
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap dmap,
             TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smraw[];
-  TcSmem& sm = *reinterpret_cast<TcSmem*>(
+  uint8_t* sbase = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  const uint32_t S = a.stages;
+  uint8_t* sm_a = sbase;                         // [S][2][TC_M*128]
+  uint8_t* sm_b = sbase + S * TC_ABYTES;         // [2][c_pad*128]
+  TcBars& sm = *reinterpret_cast<TcBars*>(sm_b + 2 * a.c_pad * 128);
+  auto A = [&](uint32_t st, uint32_t kh) { return sm_a + st * TC_ABYTES + kh * (TC_M * 128); };
+  auto Bp = [&](uint32_t kh, uint32_t row) { return sm_b + kh * (a.c_pad * 128) + row * 128; };
   const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
   const uint32_t n_units = uint32_t(*a.n_list);
   const uint32_t total = n_units * a.tiles_per_unit;
@@ -153,7 +179,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   const uint32_t nchunks = (a.c_pad + TC_CH - 1) / TC_CH;
 
   if (t == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) { mb_init(&sm.a_full[s], 1); mb_init(&sm.a_empty[s], 1); }
+    for (uint32_t s = 0; s < S; ++s) { mb_init(&sm.a_full[s], 1); mb_init(&sm.a_empty[s], 1); }
     mb_init(&sm.b_full, 1);
     mb_init(&sm.b_empty, 1);
     for (int s = 0; s < 2; ++s) { mb_init(&sm.acc_full[s], 1); mb_init(&sm.acc_empty[s], 4); }
@@ -173,9 +199,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     // ============================ TMA producer =================================
     if (lane == 0 && w0 < w1) {
       uint32_t st = 0, ph = 0, bswitch = 0, cur_unit = TC_FULL;
-      // full TMA boxes are counted even past c_pad (rows read but unused)
-      const uint32_t box_rows = min(256u, a.c_pad);
-      const uint32_t bbytes = ((a.c_pad + box_rows - 1) / box_rows) * box_rows * 128 * 2;
+      const uint32_t bbytes = a.c_pad * 128 * 2;  // c_pad is a multiple of TC_BOXR
       for (uint32_t w = w0; w < w1; ++w) {
         const uint32_t ui = w / a.tiles_per_unit, tile = w % a.tiles_per_unit;
         const uint32_t unit = uint32_t(a.unit_list[ui]);
@@ -183,20 +207,19 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
           // the previous unit's MMAs must be done reading B
           if (cur_unit != TC_FULL) mb_wait(&sm.b_empty, (bswitch - 1) & 1);
           mb_expect(&sm.b_full, bbytes);
-          for (uint32_t r0 = 0; r0 < a.c_pad; r0 += box_rows) {
+          for (uint32_t r0 = 0; r0 < a.c_pad; r0 += TC_BOXR) {
             for (int kh = 0; kh < 2; ++kh)
-              tma_2d(&sm.b[kh][r0 * 128], &dmap, kh * TC_BK, int(unit * a.c_pad + r0),
-                     &sm.b_full);
+              tma_2d(Bp(kh, r0), &dmap, kh * TC_BK, int(unit * a.c_pad + r0), &sm.b_full);
           }
           cur_unit = unit;
           ++bswitch;
         }
         mb_wait(&sm.a_empty[st], ph ^ 1);
-        mb_expect(&sm.a_full[st], TC_M * 128 * 2);
+        mb_expect(&sm.a_full[st], TC_ABYTES);
         const int row = int(unit * a.key_rows_per_unit + tile * TC_M);
-        tma_2d(&sm.a[st][0][0], &kmap, 0, row, &sm.a_full[st]);
-        tma_2d(&sm.a[st][1][0], &kmap, TC_BK, row, &sm.a_full[st]);
-        if (++st == TC_STAGES) { st = 0; ph ^= 1; }
+        tma_2d(A(st, 0), &kmap, 0, row, &sm.a_full[st]);
+        tma_2d(A(st, 1), &kmap, TC_BK, row, &sm.a_full[st]);
+        if (++st == S) { st = 0; ph ^= 1; }
       }
     }
   } else if (wid == 1) {
@@ -225,66 +248,115 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const int kh = kk >> 2, ko = (kk & 3) * 32;  // 16 bf16 = 32 B per K step
-            const uint64_t ad = kmajor_sw128_desc(su32(&sm.a[st][kh][0]) + ko);
-            const uint64_t bd = kmajor_sw128_desc(su32(&sm.b[kh][c0 * 128]) + ko);
+            const uint64_t ad = kmajor_sw128_desc(su32(A(st, kh)) + ko);
+            const uint64_t bd = kmajor_sw128_desc(su32(Bp(kh, c0)) + ko);
             umma_bf16(tmem + buf * TC_CH, ad, bd, idesc, kk > 0 ? 1u : 0u);
           }
           umma_commit(&sm.acc_full[buf]);
         }
         umma_commit(&sm.a_empty[st]);  // key tile consumed once these MMAs finish
         if (last_of_unit) umma_commit(&sm.b_empty);
-        if (++st == TC_STAGES) { st = 0; ph ^= 1; }
+        if (++st == S) { st = 0; ph ^= 1; }
       }
     }
   } else {
     // ============================ epilogue =====================================
+    // Per 256-column chunk (still in TMEM): pass 1 = chunk max M_j; pass 2 =
+    // a 32-bit in-band mask per 32-column load (S >= M_j - band), from which
+    // the count and up to 4 column ids are extracted.  Any column in the
+    // global band (S >= M - band, M = max_j M_j) is in its chunk's band, so
+    // the union of the kept chunks' in-band columns is a superset of the
+    // global candidates.  The buffer is released after pass 2, so the next
+    // tile's MMA overlaps this epilogue.
     const uint32_t quarter = wid & 3;  // TMEM lanes [32q, 32q+32)
     const uint32_t lane_row = quarter * 32 + lane;
+    const uint32_t NONE = TC_FULL;
     uint32_t g = 0;
     for (uint32_t w = w0; w < w1; ++w) {
       const uint32_t ui = w / a.tiles_per_unit, tile = w % a.tiles_per_unit;
       const uint32_t unit = uint32_t(a.unit_list[ui]);
       const uint32_t row = tile * TC_M + lane_row;
-      float s0 = -INFINITY, s1 = -INFINITY, s2 = -INFINITY, s3 = -INFINITY;
-      uint32_t i0 = 0, i1 = 0, i2 = 0, i3 = 0;
-      for (uint32_t ch = 0; ch < nchunks; ++ch, ++g) {
+      const float kn = row < a.n ? a.knorm[size_t(unit) * a.n + row] : 0.f;
+      // 2E with E = u_bf16 |k| |dir| = 2^-8 |k|, plus 1% for the fp32 sums
+      const float band = kn * (1.0f / 128.0f) * 1.01f + 1e-30f;
+      float cm[2] = {-INFINITY, -INFINITY};
+      uint32_t ccnt[2] = {0, 0};
+      uint32_t cid[2][4] = {{NONE, NONE, NONE, NONE}, {NONE, NONE, NONE, NONE}};
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        if (uint32_t(ch) >= nchunks) break;
         const uint32_t buf = g & 1, bph = (g >> 1) & 1;
+        ++g;
         const uint32_t c0 = ch * TC_CH;
         const uint32_t nc = min(uint32_t(TC_CH), a.c_pad - c0);
         mb_wait(&sm.acc_full[buf], bph);
         tc_fence_after();
         const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * TC_CH;
-        for (uint32_t cc = 0; cc < nc; cc += 16) {
-          float v[16];
-          tmem_ld16(taddr + cc, v);
+        float m = -INFINITY;
+        for (uint32_t cc = 0; cc < nc; cc += 32) {
+          float v[32];
+          tmem_ld32(taddr + cc, v);
+          if (c0 + cc + 32 > a.C) {  // warp-uniform: only the group holding padding
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const uint32_t c = c0 + cc + j;
-            const float x = c < a.C ? v[j] : -INFINITY;
-            if (x > s3) {  // NaN never enters (clustering.hpp:109 strict >)
-              if (x > s0) { s3 = s2; i3 = i2; s2 = s1; i2 = i1; s1 = s0; i1 = i0; s0 = x; i0 = c; }
-              else if (x > s1) { s3 = s2; i3 = i2; s2 = s1; i2 = i1; s1 = x; i1 = c; }
-              else if (x > s2) { s3 = s2; i3 = i2; s2 = x; i2 = c; }
-              else { s3 = x; i3 = c; }
-            }
+            for (int j = 0; j < 32; ++j)
+              if (c0 + cc + j >= a.C) v[j] = -INFINITY;
+          }
+          // tree max: independent FMNMX, not a 32-deep dependency chain
+#pragma unroll
+          for (int w2 = 16; w2 > 0; w2 >>= 1)
+#pragma unroll
+            for (int j = 0; j < w2; ++j) v[j] = fmaxf(v[j], v[j + w2]);
+          m = fmaxf(m, v[0]);
+        }
+        const float lo = m - band;
+        uint32_t cnt = 0, n4 = 0;
+        uint32_t i0 = NONE, i1 = NONE, i2 = NONE, i3 = NONE;
+        for (uint32_t cc = 0; cc < nc; cc += 32) {
+          float v[32];
+          tmem_ld32(taddr + cc, v);
+          uint32_t mb[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) mb[j] = (v[j] >= lo) ? (1u << j) : 0u;  // NaN: no
+#pragma unroll
+          for (int w2 = 16; w2 > 0; w2 >>= 1)  // tree OR
+#pragma unroll
+            for (int j = 0; j < w2; ++j) mb[j] |= mb[j + w2];
+          uint32_t mask = mb[0];
+          if (c0 + cc + 32 > a.C) {
+            const uint32_t nvalid = a.C > c0 + cc ? a.C - (c0 + cc) : 0u;
+            mask &= nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+          }
+          cnt += __popc(mask);
+          while (mask && n4 < 4) {
+            const uint32_t c = c0 + cc + uint32_t(__ffs(mask) - 1);
+            mask &= mask - 1;
+            if (n4 == 0) i0 = c; else if (n4 == 1) i1 = c; else if (n4 == 2) i2 = c; else i3 = c;
+            ++n4;
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mb_arrive(&sm.acc_empty[buf]);
+        cm[ch] = m;
+        ccnt[ch] = cnt;
+        cid[ch][0] = i0; cid[ch][1] = i1; cid[ch][2] = i2; cid[ch][3] = i3;
       }
       if (row < a.n) {
-        const float kn = a.knorm[size_t(unit) * a.n + row];
-        const float band = kn * (1.0f / 128.0f) * 1.01f + 1e-30f;  // 2 * 2^-8 |k|, margin
+        const float M = fmaxf(cm[0], cm[1]);
         int32_t* lab = a.labels + size_t(unit) * a.label_stride + row;
-        const bool none = !(s0 > -INFINITY);
-        const float lo = s0 - band;
-        const uint32_t nin = none ? 0u : 1u + (s1 >= lo) + (s2 >= lo) + (s3 >= lo);
-        if (nin == 1) {
-          *lab = int32_t(i0);
+        bool full = !(M > -INFINITY);
+        uint32_t nin = 0, single = NONE;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch)
+          if (cm[ch] >= M - band && ccnt[ch] > 0) {
+            if (ccnt[ch] > 4) full = true;
+            nin += ccnt[ch];
+            single = cid[ch][0];
+          }
+        if (!full && nin == 1) {
+          *lab = int32_t(single);
         } else {
           *lab = -1;
-          const bool full = none || s3 >= lo;
           const unsigned want = __ballot_sync(__activemask(), true);
           const uint32_t leader = __ffs(want) - 1;
           uint32_t base = 0;
@@ -293,8 +365,14 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
           const uint32_t slot = base + __popc(want & ((1u << lane) - 1u));
           if (slot < a.fix_cap) {
             a.fix_list[slot] = make_uint4(unit, row, full ? TC_FULL : nin, 0u);
-            uint32_t* ids = a.fix_ids + size_t(slot) * 4;
-            ids[0] = i0; ids[1] = i1; ids[2] = i2; ids[3] = i3;
+            uint32_t* fi = a.fix_ids + size_t(slot) * 8;
+            uint32_t k = 0;
+#pragma unroll
+            for (int ch = 0; ch < 2; ++ch)
+              if (cm[ch] >= M - band && ccnt[ch] > 0)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  if (uint32_t(j) < ccnt[ch]) fi[k++] = cid[ch][j];
           }
         }
       }
@@ -307,42 +385,89 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   }
 }
 
-// exact re-score of the fix-up keys: one warp per key, one lane per
-// candidate, sequential f64 chain over d = 128 (dot_f64), first maximum wins
+// exact re-score of the fix-up keys (sequential f64 chain = dot_f64, first
+// maximum wins).  k_fixup: 4 lanes per key (one per candidate), 8 keys per
+// warp; a FULL key (more candidates than the epilogue kept) is left for
+// k_fixup_full: one warp per key, one lane per cluster.
+__device__ __forceinline__ double exact_dot(const uint16_t* __restrict__ kr,
+                                            const float* __restrict__ dc) {
+  double s = 0.0;
+  const uint4* k4 = reinterpret_cast<const uint4*>(kr);
+  const float4* d4 = reinterpret_cast<const float4*>(dc);
+#pragma unroll 2
+  for (int b = 0; b < D / 8; ++b) {
+    const uint4 kk = __ldg(k4 + b);
+    const float4 x = __ldg(d4 + 2 * b), y = __ldg(d4 + 2 * b + 1);
+    s = __fma_rn(double(__uint_as_float(kk.x << 16)), double(x.x), s);
+    s = __fma_rn(double(__uint_as_float(kk.x & 0xffff0000u)), double(x.y), s);
+    s = __fma_rn(double(__uint_as_float(kk.y << 16)), double(x.z), s);
+    s = __fma_rn(double(__uint_as_float(kk.y & 0xffff0000u)), double(x.w), s);
+    s = __fma_rn(double(__uint_as_float(kk.z << 16)), double(y.x), s);
+    s = __fma_rn(double(__uint_as_float(kk.z & 0xffff0000u)), double(y.y), s);
+    s = __fma_rn(double(__uint_as_float(kk.w << 16)), double(y.z), s);
+    s = __fma_rn(double(__uint_as_float(kk.w & 0xffff0000u)), double(y.w), s);
+  }
+  return s;
+}
+
 __global__ void __launch_bounds__(256)
 k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
         const uint32_t* __restrict__ count, const uint16_t* __restrict__ keys,
-        uint64_t key_stride, const float* __restrict__ dirs, uint32_t C, uint32_t c_pad,
+        uint64_t key_stride, const float* __restrict__ dirs, uint32_t c_pad,
         int32_t* __restrict__ labels, uint32_t label_stride) {
+  const uint32_t nfix = *count;
+  const int lane = lane_id(), sub = lane & 7;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  for (uint32_t base = gw * 4; base < nfix; base += gridDim.x * (blockDim.x >> 5) * 4) {
+    const uint32_t e = base + (lane >> 3);  // 4 keys per warp; the bound is warp-uniform
+    const bool valid = e < nfix;
+    uint4 it = make_uint4(0, 0, 0, 0);
+    if (valid) it = list[e];
+    const bool mine = valid && it.z != TC_FULL && uint32_t(sub) < it.z;
+    double best = -INFINITY;
+    uint32_t bid = 0xffffffffu;
+    if (mine) {
+      const uint32_t c = ids[size_t(e) * 8 + sub];
+      best = exact_dot(keys + it.x * key_stride + size_t(it.y) * D,
+                       dirs + (size_t(it.x) * c_pad + c) * D);
+      bid = c;
+      if (isnan(best)) { best = -INFINITY; bid = 0xffffffffu; }  // never wins (strict >)
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {  // argmax within the 8-lane group
+      const double os = __shfl_xor_sync(0xffffffffu, best, o);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, bid, o);
+      if (os > best || (os == best && oi < bid)) { best = os; bid = oi; }
+    }
+    if (valid && it.z != TC_FULL && sub == 0)
+      labels[size_t(it.x) * label_stride + it.y] = int32_t(bid == 0xffffffffu ? 0 : bid);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_fixup_full(const uint4* __restrict__ list, const uint32_t* __restrict__ count,
+             const uint16_t* __restrict__ keys, uint64_t key_stride,
+             const float* __restrict__ dirs, uint32_t C, uint32_t c_pad,
+             int32_t* __restrict__ labels, uint32_t label_stride) {
   const uint32_t nfix = *count;
   const int lane = lane_id();
   for (uint32_t e = blockIdx.x * (blockDim.x >> 5) + warp_id(); e < nfix;
        e += gridDim.x * (blockDim.x >> 5)) {
     const uint4 it = list[e];
-    const uint32_t unit = it.x, row = it.y;
-    const uint16_t* kr = keys + unit * key_stride + size_t(row) * D;
-    const float* du = dirs + size_t(unit) * c_pad * D;
+    if (it.z != TC_FULL) continue;
+    const uint16_t* kr = keys + it.x * key_stride + size_t(it.y) * D;
     double best = -INFINITY;
     uint32_t bid = 0xffffffffu;
-    auto score = [&](uint32_t c) {
-      const float* dc = du + size_t(c) * D;
-      double s = 0.0;
-#pragma unroll 8
-      for (int j = 0; j < D; ++j) s = __fma_rn(double(bf16_to_f32(kr[j])), double(__ldg(dc + j)), s);
-      if (s > best || (s == best && c < bid)) { best = s; bid = c; }
-    };
-    if (it.z == TC_FULL) {
-      for (uint32_t c = lane; c < C; c += 32) score(c);
-    } else if (uint32_t(lane) < it.z) {
-      score(ids[size_t(e) * 4 + lane]);
+    for (uint32_t c = lane; c < C; c += 32) {
+      const double s = exact_dot(kr, dirs + (size_t(it.x) * c_pad + c) * D);
+      if (s > best) { best = s; bid = c; }  // c increases per lane: first max kept
     }
-    // warp argmax: max score, ties -> lowest id; NaN never wins (strict >)
     for (int o = 16; o > 0; o >>= 1) {
       const double os = __shfl_xor_sync(0xffffffffu, best, o);
       const uint32_t oi = __shfl_xor_sync(0xffffffffu, bid, o);
       if (os > best || (os == best && oi < bid)) { best = os; bid = oi; }
     }
-    if (lane == 0) labels[size_t(unit) * label_stride + row] = int32_t(bid == 0xffffffffu ? 0 : bid);
+    if (lane == 0) labels[size_t(it.x) * label_stride + it.y] = int32_t(bid == 0xffffffffu ? 0 : bid);
   }
 }
 
@@ -402,7 +527,7 @@ TcScratch carve(void* base, uint32_t n_units, uint32_t n) {
   s.fix_list = reinterpret_cast<uint4*>(p);
   p += align256(size_t(s.fix_cap) * 16);
   s.fix_ids = reinterpret_cast<uint32_t*>(p);
-  p += align256(size_t(s.fix_cap) * 16);
+  p += align256(size_t(s.fix_cap) * 32);
   s.knorm = reinterpret_cast<float*>(p);
   return s;
 }
@@ -435,8 +560,8 @@ int assign_tc_prepare(cudaStream_t st, const uint16_t* keys, uint64_t key_stride
 
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
   (void)C;
-  return align256(size_t(n_units) * 4) + 512 + 2 * align256(size_t(n_units) * n * 16) +
-         align256(size_t(n_units) * n * 4) + 256;
+  return align256(size_t(n_units) * 4) + 512 + align256(size_t(n_units) * n * 16) +
+         align256(size_t(n_units) * n * 32) + align256(size_t(n_units) * n * 4) + 256;
 }
 
 int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
@@ -454,7 +579,7 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   CUtensorMap kmap, dmap;
   const uint32_t rows_per_unit = uint32_t(key_stride / D);
   CKV_TRY(encode_2d(&kmap, keys, uint64_t(n_units - 1) * rows_per_unit + n, TC_M));
-  CKV_TRY(encode_2d(&dmap, dirs_bf, uint64_t(n_units) * c_pad, std::min<uint32_t>(256, c_pad)));
+  CKV_TRY(encode_2d(&dmap, dirs_bf, uint64_t(n_units) * c_pad, TC_BOXR));
   TcArgs ta;
   ta.unit_list = s.list;
   ta.n_list = s.count;
@@ -470,21 +595,31 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   ta.fix_list = s.fix_list;
   ta.fix_cap = s.fix_cap;
   ta.fix_ids = s.fix_ids;
-  const size_t smem = sizeof(TcSmem) + 1024;
+  const size_t max_smem = 232448;  // 227 KB opt-in per CTA
+  const size_t fixed = 1024 + 2 * size_t(c_pad) * 128 + sizeof(TcBars);
+  ta.stages = uint32_t(std::min<size_t>(4, (max_smem - fixed) / TC_ABYTES));
+  if (ta.stages < 2) {
+    set_error("assign_tc: not enough shared memory for two key-tile stages");
+    return CKV_EINVAL;
+  }
+  const size_t smem = fixed + size_t(ta.stages) * TC_ABYTES;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
     CKV_CUDA_TRY(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(smem)));
+                                      int(max_smem)));
     attr_dev = dev;
   }
   k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
   CKV_LAUNCH_CHECK("k_assign_tc");
-  k_fixup<<<num_sms() * 4, 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, keys, key_stride,
-                                          dirs, C, c_pad, labels, label_stride);
+  k_fixup<<<num_sms() * 8, 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, keys, key_stride,
+                                          dirs, c_pad, labels, label_stride);
   CKV_LAUNCH_CHECK("k_fixup");
-  *launches += 3;
+  k_fixup_full<<<num_sms() * 2, 256, 0, st>>>(s.fix_list, s.fix_count, keys, key_stride, dirs, C,
+                                               c_pad, labels, label_stride);
+  CKV_LAUNCH_CHECK("k_fixup_full");
+  *launches += 4;
   return CKV_OK;
 }
 

@@ -13,6 +13,8 @@
 //   control  : convergence / max_iters bookkeeping, one 4-byte read-back
 // Every integer result (labels, iterations, converged, repair iterations)
 // and every centroid bit equals the reference for identical inputs.
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "ckv_internal.cuh"
@@ -519,19 +521,37 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   CKV_TRY(count_repair(lab[0], nullptr));
   CKV_TRY(control(0, &hf[U]));
 
+  // CKV_DEBUG_KMEANS=1: per-phase device times of each pass on stderr
+  static const bool dbg = getenv("CKV_DEBUG_KMEANS") != nullptr;
+  cudaEvent_t dev_[5];
+  if (dbg) for (auto& e : dev_) cudaEventCreate(&e);
   for (uint32_t t = 1; t <= MI && hf[U] > 0; ++t) {
     int32_t* prev = lab[(t - 1) & 1];
     int32_t* cur = lab[t & 1];
+    if (dbg) cudaEventRecord(dev_[0], st);
     // update from the previous labels (sizes/starts/sorted hold its sort)
     k_update<<<dim3((c_pad + 7) / 8, U), 256, 0, st>>>(
         a.keys, a.key_stride, C, CS, c_pad, LS, b_sizes.as<uint32_t>(), b_starts.as<uint32_t>(),
         b_sorted.as<uint32_t>(), a.centroids, dirs, dirs_bf, cnorm, active);
     CKV_LAUNCH_CHECK("k_update");
     ctx->launches++;
+    if (dbg) cudaEventRecord(dev_[1], st);
     CKV_TRY(assign(cur));
+    if (dbg) cudaEventRecord(dev_[2], st);
     CKV_TRY(count_repair(cur, prev));
+    if (dbg) cudaEventRecord(dev_[3], st);
+    const int32_t active_before = hf[U];
     CKV_TRY(control(t, &hf[U]));
+    if (dbg) {
+      cudaEventRecord(dev_[4], st);
+      cudaEventSynchronize(dev_[4]);
+      float x[4];
+      for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&x[k], dev_[k], dev_[k + 1]);
+      fprintf(stderr, "[kmeans dbg] pass %u active %d: update %.3f assign %.3f index+repair %.3f "
+              "control %.3f ms\n", t, active_before, x[0], x[1], x[2], x[3]);
+    }
   }
+  if (dbg) for (auto& e : dev_) cudaEventDestroy(e);
 
   // final labels live in lab[iterations_used & 1]; lab[0] is the output
   k_copy_labels<<<dim3(32, U), 256, 0, st>>>(lab[1], lab[0], n, LS, b_iters.as<uint32_t>(), 1);
