@@ -536,7 +536,26 @@ int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows
   const cuuint64_t strides[1] = {cuuint64_t(D) * 2};
   const cuuint32_t box[2] = {cuuint32_t(TC_BK), cuuint32_t(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  // Resolved through the runtime so libckv_b200.so has no link-time libcuda
+  // dependency (it must load on hosts without a driver, e.g. the CPU tests).
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<EncodeFn>(fn);
+  }();
+  if (!encode) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return CKV_ECUDA;
+  }
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                       const_cast<void*>(base), dims, strides, box, estr,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

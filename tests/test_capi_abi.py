@@ -48,3 +48,26 @@ def test_host_side_abi_without_gpu():
     assert L.ckv_mix_seed(0, 3, 5) == Oracle("port").mix_seed(0, 3, 5)
     assert L.ckv_prefill_cluster_count(32016, 80, 16, 0) == 400
     assert L.ckv_kmeans_init_rows(3, 4, 0, rows.ctypes.data) == 1
+
+
+def test_cpp_dropin_exports_and_links():
+    """The reference-signature C++ drop-in (include/clusterkv_b200/clusterkv.hpp)
+    has a definition in libckv_b200.so for every free function / ClusterCache
+    member it declares, and the parity program links against it."""
+    import subprocess
+    from paper_2412_03213_b200 import build as B
+    if not os.path.exists(B.LIB):
+        B.build()
+    out = subprocess.run(["nm", "-DC", "--defined-only", B.LIB], capture_output=True,
+                         text=True, check=True).stdout
+    for name in ("ckv::kmeans_cosine(", "ckv::prefill_cluster_count(", "ckv::cluster_prefill(",
+                 "ckv::cluster_decode_batch(", "ckv::build_index(", "ckv::score_clusters(",
+                 "ckv::select_tokens(", "ckv::approx_attention(", "ckv::ClusterCache::ClusterCache(",
+                 "ckv::ClusterCache::~ClusterCache(", "ckv::ClusterCache::lookup_and_update(",
+                 "ckv::ClusterCache::hit_rate(", "ckv::ClusterCache::invalidate_on_recluster(",
+                 "ckv::ClusterCache::counters("):
+        assert name in out, name
+    from oracle.oracle import build as obuild
+    obuild()
+    from tests.cpp.build import build as sbuild
+    assert os.path.exists(sbuild())
