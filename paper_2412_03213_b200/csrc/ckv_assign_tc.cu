@@ -6,15 +6,20 @@
 //   1. a bf16 GEMM S = K . bf16(dir)^T on the 5th-gen tensor cores
 //      (tcgen05.mma kind::f16, fp32 accumulation in TMEM), 128 keys x all C
 //      columns per tile;
-//   2. the epilogue (tcgen05.ld) keeps each key's top-4 approximate scores.
-//      |S_c - s_c| <= E = 2^-9 |k| (bf16 rounding of dir, |dir| = 1) plus
-//      the fp32 accumulation error, so the exact argmax lies in
-//      {c : S_c >= S_max - 2E}.  The band used is 2^-7 |k| (2x margin).
-//      One candidate in band -> that is the label.  Otherwise the key goes to
-//      a fix-up list with its 2-4 candidates (or "all" when the 4th is in
-//      band too) and k_fixup re-scores them with the sequential f64 chain —
-//      bit-identical to dot_f64 — picking the first maximum.  Labels are
-//      therefore bit-exact for every key while the tensor FLOPs stay at 1x.
+//   2. the epilogue (tcgen05.ld, ONE pass over the accumulator) keeps a
+//      running max M and the columns within a band of it.  The error of a
+//      tensor-core score is |S_c - s_c| <= |k| |dir_c - bf16(dir_c)| (the
+//      operand rounding, Cauchy-Schwarz) + |k| 2^-14 (fp32 accumulation of
+//      128 products, conservatively), so the exact argmax lies in
+//      {c : S_c >= M - band}, band = |k| (2 eps_u + 2^-13) * 1.01 with eps_u
+//      = max_c |dir_c - bf16(dir_c)| of the unit (computed exactly when the
+//      dirs are made).  One candidate in band -> that is the label.
+//      Otherwise the key goes to a fix-up list with its <= 8 candidates (or
+//      "all" when more were in band) and k_fixup decides with f64 dot
+//      products — the sequential dot_f64 chain itself whenever two
+//      candidates are closer than the f64 rounding could separate — taking
+//      the first maximum.  Labels are therefore bit-exact for every key
+//      while the tensor FLOPs stay at 1x.
 //
 // Kernel anatomy (persistent, one CTA per SM, 6 warps):
 //   warp 0  TMA producer: key tiles (2 stages, 128B-swizzled boxes of
@@ -22,8 +27,13 @@
 //           directions (resident B operand, up to 512 rows).
 //   warp 1  TMEM allocator + MMA issuer (one elected thread): per tile and
 //           256-column chunk, 8 K=16 steps into TMEM buffer (chunk & 1).
-//   warps 2-5 epilogue: TMEM lane quarter = warp % 4, one key row per thread.
+//   warps 2-17 epilogue: TMEM lane quarter = warp % 4 (one key row per
+//           thread); the 4 warps of a quarter split each chunk's 32-column
+//           blocks and meet at a named barrier per chunk (see below).
 #include <cuda.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include <vector>
 
@@ -35,8 +45,10 @@ constexpr int TC_M = 128;              // keys per tile (UMMA_M)
 constexpr int TC_BK = 64;              // bf16 columns per 128-B swizzle atom
 constexpr int TC_MAXC = 512;           // C_pad limit: B resident, 2 x 256 TMEM cols
 constexpr int TC_CH = 256;             // columns per MMA chunk / TMEM buffer
-constexpr int TC_THREADS = 6 * 32;
+constexpr int TC_EGROUPS = 4;          // epilogue warp groups (4 warps = 128 TMEM lanes each)
+constexpr int TC_THREADS = (2 + 4 * TC_EGROUPS) * 32;
 constexpr uint32_t TC_FULL = 0xffffffffu;
+constexpr int TC_NCAND = 8;            // candidates an epilogue row keeps
 
 // dynamic smem (1024-B aligned base): A stages [stages][2 k-halves][128 x 128 B],
 // then B [2 k-halves][c_pad x 128 B], then the barriers.  B is the resident
@@ -46,6 +58,12 @@ struct TcBars {
   uint64_t b_full, b_empty;
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
+  uint32_t pad_[3];
+  // epilogue exchange, [..][row] so a warp's accesses are conflict-free
+  float m_part[TC_EGROUPS][TC_M];         // per-group max of the current chunk
+  float m_ch[2][TC_M];                    // chunk maxima of the current tile
+  uint32_t n_ch[2][TC_M];                 // in-band columns per chunk
+  uint16_t id_ch[2][TC_NCAND][TC_M];      // their ids (first TC_NCAND)
 };
 constexpr uint32_t TC_ABYTES = TC_M * 128 * 2;  // one key-tile stage (both k-halves)
 constexpr uint32_t TC_BOXR = 32;                // rows per B TMA box (B sized to c_pad)
@@ -126,6 +144,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 32 bit, 32 consecutive columns per thread, no wait (pair with
+// tmem_wait so several loads are in flight)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // 32 lanes x 32 bit, 32 consecutive columns per thread
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
@@ -152,6 +191,7 @@ struct TcArgs {
   uint32_t key_rows_per_unit;  // key_stride / 128
   uint32_t label_stride;
   const float* knorm;          // [unit][n] key norms (band scale)
+  const float* eps_u;          // [unit] max_c |dir_c - bf16(dir_c)|
   int32_t* labels;
   uint32_t* fix_count;         // device counter
   uint4* fix_list;             // {unit, row, n_cand | FULL, 0}
@@ -182,7 +222,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     for (uint32_t s = 0; s < S; ++s) { mb_init(&sm.a_full[s], 1); mb_init(&sm.a_empty[s], 1); }
     mb_init(&sm.b_full, 1);
     mb_init(&sm.b_empty, 1);
-    for (int s = 0; s < 2; ++s) { mb_init(&sm.acc_full[s], 1); mb_init(&sm.acc_empty[s], 4); }
+    for (int s = 0; s < 2; ++s) { mb_init(&sm.acc_full[s], 1); mb_init(&sm.acc_empty[s], 4 * TC_EGROUPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (wid == 1) {  // TMEM: 512 columns (two 256-column accumulator buffers)
@@ -261,120 +301,155 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     }
   } else {
     // ============================ epilogue =====================================
-    // Per 256-column chunk (still in TMEM): pass 1 = chunk max M_j; pass 2 =
-    // a 32-bit in-band mask per 32-column load (S >= M_j - band), from which
-    // the count and up to 4 column ids are extracted.  Any column in the
-    // global band (S >= M - band, M = max_j M_j) is in its chunk's band, so
-    // the union of the kept chunks' in-band columns is a superset of the
-    // global candidates.  The buffer is released after pass 2, so the next
-    // tile's MMA overlaps this epilogue.
-    const uint32_t quarter = wid & 3;  // TMEM lanes [32q, 32q+32)
+    // 16 warps: 4 per TMEM lane quarter (one key row per thread), splitting
+    // each chunk's 32-column blocks round-robin, <= 2 blocks each, held in
+    // registers after ONE tcgen05.ld pass, so the buffer is released at once.
+    // Per chunk: (1) block maxima -> m_part; named barrier of the quarter;
+    // (2) chunk max M_ch = max of the 4 parts; in-band mask S >= M_ch - band
+    // per block; the (rare) in-band ids go to the row's chunk list; barrier.
+    // After the tile's last chunk the quarter's first warp decides each row:
+    // M = max_ch M_ch; the chunks with M_ch >= M - band contribute their
+    // in-band ids (a superset of {c : S_c >= M - band}; it only differs when
+    // two chunks are both in band, i.e. the row has >= 2 candidates anyway).
+    const uint32_t quarter = wid & 3;               // TMEM lanes [32q, 32q+32)
+    const uint32_t grp = uint32_t(wid - 2) >> 2;    // 0..3: column share
     const uint32_t lane_row = quarter * 32 + lane;
-    const uint32_t NONE = TC_FULL;
+    const uint32_t bar_id = 1 + quarter;            // named barrier per quarter
+    auto qbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(4 * 32) : "memory"); };
     uint32_t g = 0;
+    if (grp == 0)
+      for (int ch = 0; ch < 2; ++ch) sm.n_ch[ch][lane_row] = 0;
     for (uint32_t w = w0; w < w1; ++w) {
       const uint32_t ui = w / a.tiles_per_unit, tile = w % a.tiles_per_unit;
       const uint32_t unit = uint32_t(a.unit_list[ui]);
       const uint32_t row = tile * TC_M + lane_row;
       const float kn = row < a.n ? a.knorm[size_t(unit) * a.n + row] : 0.f;
-      // 2E with E = u_bf16 |k| |dir| = 2^-8 |k|, plus 1% for the fp32 sums
-      const float band = kn * (1.0f / 128.0f) * 1.01f + 1e-30f;
-      float cm[2] = {-INFINITY, -INFINITY};
-      uint32_t ccnt[2] = {0, 0};
-      uint32_t cid[2][4] = {{NONE, NONE, NONE, NONE}, {NONE, NONE, NONE, NONE}};
-#pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        if (uint32_t(ch) >= nchunks) break;
+      const float band = kn * (2.0f * a.eps_u[unit] + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
+#pragma unroll 1
+      for (uint32_t ch = 0; ch < nchunks; ++ch) {
         const uint32_t buf = g & 1, bph = (g >> 1) & 1;
         ++g;
         const uint32_t c0 = ch * TC_CH;
-        const uint32_t nc = min(uint32_t(TC_CH), a.c_pad - c0);
+        const uint32_t nb = min(uint32_t(TC_CH), a.c_pad - c0) / 32;  // blocks in chunk
+        const uint32_t b0 = grp, b1 = grp + TC_EGROUPS;               // my blocks
+        const bool h0 = b0 < nb, h1 = b1 < nb;                         // warp-uniform
+        float v[64];
         mb_wait(&sm.acc_full[buf], bph);
         tc_fence_after();
         const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * TC_CH;
-        float m = -INFINITY;
-        for (uint32_t cc = 0; cc < nc; cc += 32) {
-          float v[32];
-          tmem_ld32(taddr + cc, v);
-          if (c0 + cc + 32 > a.C) {  // warp-uniform: only the group holding padding
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c0 + cc + j >= a.C) v[j] = -INFINITY;
-          }
-          // tree max: independent FMNMX, not a 32-deep dependency chain
-#pragma unroll
-          for (int w2 = 16; w2 > 0; w2 >>= 1)
-#pragma unroll
-            for (int j = 0; j < w2; ++j) v[j] = fmaxf(v[j], v[j + w2]);
-          m = fmaxf(m, v[0]);
-        }
-        const float lo = m - band;
-        uint32_t cnt = 0, n4 = 0;
-        uint32_t i0 = NONE, i1 = NONE, i2 = NONE, i3 = NONE;
-        for (uint32_t cc = 0; cc < nc; cc += 32) {
-          float v[32];
-          tmem_ld32(taddr + cc, v);
-          uint32_t mb[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) mb[j] = (v[j] >= lo) ? (1u << j) : 0u;  // NaN: no
-#pragma unroll
-          for (int w2 = 16; w2 > 0; w2 >>= 1)  // tree OR
-#pragma unroll
-            for (int j = 0; j < w2; ++j) mb[j] |= mb[j + w2];
-          uint32_t mask = mb[0];
-          if (c0 + cc + 32 > a.C) {
-            const uint32_t nvalid = a.C > c0 + cc ? a.C - (c0 + cc) : 0u;
-            mask &= nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
-          }
-          cnt += __popc(mask);
-          while (mask && n4 < 4) {
-            const uint32_t c = c0 + cc + uint32_t(__ffs(mask) - 1);
-            mask &= mask - 1;
-            if (n4 == 0) i0 = c; else if (n4 == 1) i1 = c; else if (n4 == 2) i2 = c; else i3 = c;
-            ++n4;
-          }
-        }
+        if (h0) tmem_ld32_nw(taddr + b0 * 32, v);
+        if (h1) tmem_ld32_nw(taddr + b1 * 32, v + 32);
+        tmem_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mb_arrive(&sm.acc_empty[buf]);
-        cm[ch] = m;
-        ccnt[ch] = cnt;
-        cid[ch][0] = i0; cid[ch][1] = i1; cid[ch][2] = i2; cid[ch][3] = i3;
+        if (lane == 0) mb_arrive(&sm.acc_empty[buf]);  // scores now live in registers
+        const uint32_t cb0 = c0 + b0 * 32, cb1 = c0 + b1 * 32;
+        // padding columns (only in the unit's last block; warp-uniform branch)
+        if (h0 && cb0 + 32 > a.C) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) if (cb0 + j >= a.C) v[j] = -INFINITY;
+        }
+        if (h1 && cb1 + 32 > a.C) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) if (cb1 + j >= a.C) v[32 + j] = -INFINITY;
+        }
+        // (1) block maximum: FMNMX3 trees (ALU pipe, 0.5 op per score)
+        float mx = -INFINITY;
+        if (h1) {
+          float t[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            t[j] = fmaxf(fmaxf(v[j], v[j + 16]), fmaxf(v[j + 32], v[j + 48]));
+#pragma unroll
+          for (int w2 = 8; w2 > 0; w2 >>= 1)
+#pragma unroll
+            for (int j = 0; j < w2; ++j) t[j] = fmaxf(t[j], t[j + w2]);
+          mx = t[0];
+        } else if (h0) {
+          float t[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) t[j] = fmaxf(v[j], v[j + 16]);
+#pragma unroll
+          for (int w2 = 8; w2 > 0; w2 >>= 1)
+#pragma unroll
+            for (int j = 0; j < w2; ++j) t[j] = fmaxf(t[j], t[j + w2]);
+          mx = t[0];
+        }
+        sm.m_part[grp][lane_row] = mx;
+        qbar();
+        float mc = sm.m_part[0][lane_row];
+#pragma unroll
+        for (int q = 1; q < TC_EGROUPS; ++q) mc = fmaxf(mc, sm.m_part[q][lane_row]);
+        if (grp == 0) sm.m_ch[ch][lane_row] = mc;
+        const float lo = mc - band;
+        // (2) in-band mask: sign of S - lo (FADD, FMA pipe) funnel-shifted into
+        // a word (SHF, ALU pipe): bit 31-j set  <=>  S_j < lo
+        uint32_t in0 = 0u, in1 = 0u;
+        if (h0) {
+          uint32_t below = 0u;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) below = __funnelshift_l(__float_as_uint(v[j] - lo), below, 1);
+          in0 = ~below;
+        }
+        if (h1) {
+          uint32_t below = 0u;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            below = __funnelshift_l(__float_as_uint(v[32 + j] - lo), below, 1);
+          in1 = ~below;
+        }
+        // (3) the rare in-band columns -> the row's chunk list
+        while (in0 | in1) {
+          const bool first = in0 != 0u;
+          const uint32_t word = first ? in0 : in1;
+          const uint32_t jj = __clz(word);
+          const uint32_t c = (first ? cb0 : cb1) + jj;
+          if (first) in0 &= ~(0x80000000u >> jj); else in1 &= ~(0x80000000u >> jj);
+          const uint32_t slot = atomicAdd(&sm.n_ch[ch][lane_row], 1u);
+          if (slot < uint32_t(TC_NCAND)) sm.id_ch[ch][slot][lane_row] = uint16_t(c);
+        }
+        qbar();
       }
-      if (row < a.n) {
-        const float M = fmaxf(cm[0], cm[1]);
-        int32_t* lab = a.labels + size_t(unit) * a.label_stride + row;
-        bool full = !(M > -INFINITY);
-        uint32_t nin = 0, single = NONE;
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch)
-          if (cm[ch] >= M - band && ccnt[ch] > 0) {
-            if (ccnt[ch] > 4) full = true;
-            nin += ccnt[ch];
-            single = cid[ch][0];
+      if (grp == 0) {
+        if (row < a.n) {
+          float M = sm.m_ch[0][lane_row];
+          if (nchunks > 1) M = fmaxf(M, sm.m_ch[1][lane_row]);
+          bool full = !(M > -INFINITY);
+          uint32_t nin = 0, single = TC_FULL;
+          for (uint32_t ch = 0; ch < nchunks; ++ch) {
+            if (sm.m_ch[ch][lane_row] >= M - band) {
+              const uint32_t nn = sm.n_ch[ch][lane_row];
+              if (nn > uint32_t(TC_NCAND)) full = true;
+              if (nn > 0) single = sm.id_ch[ch][0][lane_row];
+              nin += nn;
+            }
           }
-        if (!full && nin == 1) {
-          *lab = int32_t(single);
-        } else {
-          *lab = -1;
-          const unsigned want = __ballot_sync(__activemask(), true);
-          const uint32_t leader = __ffs(want) - 1;
-          uint32_t base = 0;
-          if (uint32_t(lane) == leader) base = atomicAdd(a.fix_count, __popc(want));
-          base = __shfl_sync(want, base, leader);
-          const uint32_t slot = base + __popc(want & ((1u << lane) - 1u));
-          if (slot < a.fix_cap) {
-            a.fix_list[slot] = make_uint4(unit, row, full ? TC_FULL : nin, 0u);
-            uint32_t* fi = a.fix_ids + size_t(slot) * 8;
-            uint32_t k = 0;
-#pragma unroll
-            for (int ch = 0; ch < 2; ++ch)
-              if (cm[ch] >= M - band && ccnt[ch] > 0)
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                  if (uint32_t(j) < ccnt[ch]) fi[k++] = cid[ch][j];
+          if (nin > uint32_t(TC_NCAND)) full = true;
+          int32_t* lab = a.labels + size_t(unit) * a.label_stride + row;
+          if (!full && nin == 1) {
+            *lab = int32_t(single);
+          } else {
+            *lab = -1;
+            const unsigned want = __activemask();
+            const uint32_t leader = __ffs(want) - 1;
+            uint32_t base = 0;
+            if (uint32_t(lane) == leader) base = atomicAdd(a.fix_count, __popc(want));
+            base = __shfl_sync(want, base, leader);
+            const uint32_t slot = base + __popc(want & ((1u << lane) - 1u));
+            if (slot < a.fix_cap) {
+              a.fix_list[slot] = make_uint4(unit, row, full ? TC_FULL : nin, 0u);
+              uint32_t* fi = a.fix_ids + size_t(slot) * TC_NCAND;
+              uint32_t k2 = 0;
+              if (!full)
+                for (uint32_t ch = 0; ch < nchunks; ++ch)
+                  if (sm.m_ch[ch][lane_row] >= M - band)
+                    for (uint32_t k = 0; k < sm.n_ch[ch][lane_row]; ++k)
+                      fi[k2++] = sm.id_ch[ch][k][lane_row];
+            }
           }
         }
+        __syncwarp();
+        for (int ch = 0; ch < 2; ++ch) sm.n_ch[ch][lane_row] = 0;
       }
     }
   }
@@ -385,16 +460,20 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   }
 }
 
-// exact re-score of the fix-up keys (sequential f64 chain = dot_f64, first
-// maximum wins).  k_fixup: 4 lanes per key (one per candidate), 8 keys per
-// warp; a FULL key (more candidates than the epilogue kept) is left for
-// k_fixup_full: one warp per key, one lane per cluster.
+// exact re-score of the fix-up keys (clustering.hpp:104-115: argmax of
+// dot_f64(key, dir_c), strict >, so ties go to the lowest id).
+// One warp per key; lane L holds dims 4L..4L+3.  Every candidate's score is
+// computed in f64 with a lane-tree sum (all products are exact in f64; the
+// result differs from the sequential chain by < 2^-46 |k|).  If the best two
+// are closer than 2^-40 |k|, the order could depend on the chain's rounding,
+// so those candidates are re-scored with the sequential chain itself (lane 0).
+// A FULL key (more in-band columns than the epilogue kept) scans all C.
 __device__ __forceinline__ double exact_dot(const uint16_t* __restrict__ kr,
                                             const float* __restrict__ dc) {
   double s = 0.0;
   const uint4* k4 = reinterpret_cast<const uint4*>(kr);
   const float4* d4 = reinterpret_cast<const float4*>(dc);
-#pragma unroll 2
+#pragma unroll 4
   for (int b = 0; b < D / 8; ++b) {
     const uint4 kk = __ldg(k4 + b);
     const float4 x = __ldg(d4 + 2 * b), y = __ldg(d4 + 2 * b + 1);
@@ -410,65 +489,89 @@ __device__ __forceinline__ double exact_dot(const uint16_t* __restrict__ kr,
   return s;
 }
 
-__global__ void __launch_bounds__(256)
-k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
-        const uint32_t* __restrict__ count, const uint16_t* __restrict__ keys,
-        uint64_t key_stride, const float* __restrict__ dirs, uint32_t c_pad,
-        int32_t* __restrict__ labels, uint32_t label_stride) {
-  const uint32_t nfix = *count;
-  const int lane = lane_id(), sub = lane & 7;
-  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp_id();
-  for (uint32_t base = gw * 4; base < nfix; base += gridDim.x * (blockDim.x >> 5) * 4) {
-    const uint32_t e = base + (lane >> 3);  // 4 keys per warp; the bound is warp-uniform
-    const bool valid = e < nfix;
-    uint4 it = make_uint4(0, 0, 0, 0);
-    if (valid) it = list[e];
-    const bool mine = valid && it.z != TC_FULL && uint32_t(sub) < it.z;
-    double best = -INFINITY;
-    uint32_t bid = 0xffffffffu;
-    if (mine) {
-      const uint32_t c = ids[size_t(e) * 8 + sub];
-      best = exact_dot(keys + it.x * key_stride + size_t(it.y) * D,
-                       dirs + (size_t(it.x) * c_pad + c) * D);
-      bid = c;
-      if (isnan(best)) { best = -INFINITY; bid = 0xffffffffu; }  // never wins (strict >)
-    }
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {  // argmax within the 8-lane group
-      const double os = __shfl_xor_sync(0xffffffffu, best, o);
-      const uint32_t oi = __shfl_xor_sync(0xffffffffu, bid, o);
-      if (os > best || (os == best && oi < bid)) { best = os; bid = oi; }
-    }
-    if (valid && it.z != TC_FULL && sub == 0)
-      labels[size_t(it.x) * label_stride + it.y] = int32_t(bid == 0xffffffffu ? 0 : bid);
-  }
+__device__ __forceinline__ double lane_partial(const double k[4], const float4 d) {
+  return __fma_rn(k[3], double(d.w),
+                  __fma_rn(k[2], double(d.z), __fma_rn(k[1], double(d.y), k[0] * double(d.x))));
 }
 
 __global__ void __launch_bounds__(256)
-k_fixup_full(const uint4* __restrict__ list, const uint32_t* __restrict__ count,
-             const uint16_t* __restrict__ keys, uint64_t key_stride,
-             const float* __restrict__ dirs, uint32_t C, uint32_t c_pad,
-             int32_t* __restrict__ labels, uint32_t label_stride) {
+k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
+        const uint32_t* __restrict__ count, const uint16_t* __restrict__ keys,
+        uint64_t key_stride, const float* __restrict__ dirs, uint32_t C, uint32_t c_pad,
+        const float* __restrict__ knorm, uint32_t n, int32_t* __restrict__ labels,
+        uint32_t label_stride) {
   const uint32_t nfix = *count;
   const int lane = lane_id();
-  for (uint32_t e = blockIdx.x * (blockDim.x >> 5) + warp_id(); e < nfix;
-       e += gridDim.x * (blockDim.x >> 5)) {
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t e = blockIdx.x * (blockDim.x >> 5) + warp_id(); e < nfix; e += nw) {
     const uint4 it = list[e];
-    if (it.z != TC_FULL) continue;
-    const uint16_t* kr = keys + it.x * key_stride + size_t(it.y) * D;
-    double best = -INFINITY;
+    const uint32_t u = it.x, row = it.y;
+    const bool full = it.z == TC_FULL;
+    const uint32_t nc = full ? C : it.z;
+    const uint16_t* kr = keys + u * key_stride + size_t(row) * D;
+    const uint2 kv = __ldg(reinterpret_cast<const uint2*>(kr) + lane);
+    const double k[4] = {double(__uint_as_float(kv.x << 16)),
+                         double(__uint_as_float(kv.x & 0xffff0000u)),
+                         double(__uint_as_float(kv.y << 16)),
+                         double(__uint_as_float(kv.y & 0xffff0000u))};
+    const float* du = dirs + size_t(u) * c_pad * D;
+    const uint32_t* cid = ids + size_t(e) * TC_NCAND;
+    double best = -INFINITY, second = -INFINITY;
     uint32_t bid = 0xffffffffu;
-    for (uint32_t c = lane; c < C; c += 32) {
-      const double s = exact_dot(kr, dirs + (size_t(it.x) * c_pad + c) * D);
-      if (s > best) { best = s; bid = c; }  // c increases per lane: first max kept
+    for (uint32_t j0 = 0; j0 < nc; j0 += TC_NCAND) {
+      double p[TC_NCAND];
+      uint32_t c[TC_NCAND];
+#pragma unroll
+      for (int j = 0; j < TC_NCAND; ++j) {  // 8 independent loads + partials
+        c[j] = j0 + j < nc ? (full ? j0 + j : __ldg(cid + j0 + j)) : 0u;
+        const float4 d = __ldg(reinterpret_cast<const float4*>(du + size_t(c[j]) * D) + lane);
+        p[j] = lane_partial(k, d);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < TC_NCAND; ++j) p[j] += __shfl_xor_sync(0xffffffffu, p[j], o);
+#pragma unroll
+      for (int j = 0; j < TC_NCAND; ++j) {
+        if (j0 + j >= nc) break;
+        const double sj = isnan(p[j]) ? -INFINITY : p[j];
+        if (sj > best) { second = best; best = sj; bid = c[j]; }  // ids ascend: first max
+        else if (sj > second) second = sj;
+      }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double os = __shfl_xor_sync(0xffffffffu, best, o);
-      const uint32_t oi = __shfl_xor_sync(0xffffffffu, bid, o);
-      if (os > best || (os == best && oi < bid)) { best = os; bid = oi; }
+    const double kn = double(knorm[size_t(u) * n + row]);
+    const double tie = kn * 0x1p-40;
+    if (!(best - second > tie) && best > -INFINITY) {
+      // near-tie: the sequential chain (dot_f64's exact rounding) decides;
+      // lanes split the candidates, first maximum per lane, then lowest id
+      double b2 = -INFINITY;
+      uint32_t i2 = 0xffffffffu;
+      for (uint32_t j = lane; j < nc; j += 32) {
+        const uint32_t cj = full ? j : cid[j];
+        const double sj = exact_dot(kr, du + size_t(cj) * D);
+        if (sj > b2) { b2 = sj; i2 = cj; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, b2, o);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, i2, o);
+        if (os > b2 || (os == b2 && oi < i2)) { b2 = os; i2 = oi; }
+      }
+      bid = i2;
     }
-    if (lane == 0) labels[size_t(it.x) * label_stride + it.y] = int32_t(bid == 0xffffffffu ? 0 : bid);
+    if (lane == 0)
+      labels[size_t(u) * label_stride + row] = int32_t(bid == 0xffffffffu ? 0 : bid);
   }
+}
+
+__global__ void k_eps_max(const float* __restrict__ deps, uint32_t c_pad, uint32_t n_units,
+                          float* __restrict__ eps_u) {
+  const uint32_t u = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  if (u >= n_units) return;
+  float m = 0.f;
+  for (uint32_t c = lane_id(); c < c_pad; c += 32) m = fmaxf(m, deps[size_t(u) * c_pad + c]);
+  m = warp_max(m);
+  if (lane_id() == 0) eps_u[u] = m;
 }
 
 __global__ void k_key_norms(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
@@ -511,6 +614,7 @@ struct TcScratch {
   uint4* fix_list;
   uint32_t* fix_ids;
   float* knorm;
+  float* eps_u;
   uint32_t fix_cap;
 };
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -529,6 +633,8 @@ TcScratch carve(void* base, uint32_t n_units, uint32_t n) {
   s.fix_ids = reinterpret_cast<uint32_t*>(p);
   p += align256(size_t(s.fix_cap) * 32);
   s.knorm = reinterpret_cast<float*>(p);
+  p += align256(size_t(n_units) * n * 4);
+  s.eps_u = reinterpret_cast<float*>(p);
   return s;
 }
 int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
@@ -580,12 +686,13 @@ int assign_tc_prepare(cudaStream_t st, const uint16_t* keys, uint64_t key_stride
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
   (void)C;
   return align256(size_t(n_units) * 4) + 512 + align256(size_t(n_units) * n * 16) +
-         align256(size_t(n_units) * n * 32) + align256(size_t(n_units) * n * 4) + 256;
+         align256(size_t(n_units) * n * 32) + align256(size_t(n_units) * n * 4) +
+         align256(size_t(n_units) * 4) + 256;
 }
 
 int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
               uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs_bf,
-              const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
+              const float* deps, const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
               void* scratch, size_t scratch_bytes, uint64_t* launches) {
   (void)scratch_bytes;
   if (key_stride % D) {
@@ -595,6 +702,8 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   TcScratch s = carve(scratch, n_units, n);
   k_compact_active<<<1, 32, 0, st>>>(active, n_units, s.list, s.count, s.fix_count);
   CKV_LAUNCH_CHECK("k_compact_active");
+  k_eps_max<<<(n_units + 7) / 8, 256, 0, st>>>(deps, c_pad, n_units, s.eps_u);
+  CKV_LAUNCH_CHECK("k_eps_max");
   CUtensorMap kmap, dmap;
   const uint32_t rows_per_unit = uint32_t(key_stride / D);
   CKV_TRY(encode_2d(&kmap, keys, uint64_t(n_units - 1) * rows_per_unit + n, TC_M));
@@ -609,6 +718,7 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   ta.key_rows_per_unit = rows_per_unit;
   ta.label_stride = label_stride;
   ta.knorm = s.knorm;
+  ta.eps_u = s.eps_u;
   ta.labels = labels;
   ta.fix_count = s.fix_count;
   ta.fix_list = s.fix_list;
@@ -633,12 +743,17 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
   CKV_LAUNCH_CHECK("k_assign_tc");
   k_fixup<<<num_sms() * 8, 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, keys, key_stride,
-                                          dirs, c_pad, labels, label_stride);
+                                          dirs, C, c_pad, s.knorm, n, labels, label_stride);
   CKV_LAUNCH_CHECK("k_fixup");
-  k_fixup_full<<<num_sms() * 2, 256, 0, st>>>(s.fix_list, s.fix_count, keys, key_stride, dirs, C,
-                                               c_pad, labels, label_stride);
-  CKV_LAUNCH_CHECK("k_fixup_full");
   *launches += 4;
+  static const bool dbg = getenv("CKV_DEBUG_KMEANS") != nullptr;
+  if (dbg) {
+    uint32_t nfix = 0;
+    cudaMemcpyAsync(&nfix, s.fix_count, 4, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[kmeans dbg] assign_tc fix-ups %u of %u keys (%.2f%%)\n", nfix,
+            n * n_units, 100.0 * nfix / (double(n) * n_units));
+  }
   return CKV_OK;
 }
 

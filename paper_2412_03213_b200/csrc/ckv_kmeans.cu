@@ -61,7 +61,8 @@ __global__ void k_init_centroids(const uint16_t* __restrict__ keys, uint64_t key
 // One thread per centroid: the norm is a sequential f64 chain by contract.
 __global__ void k_dirs(const float* __restrict__ cents, uint32_t C, uint32_t c_stride,
                        uint32_t c_pad, float* __restrict__ dirs, uint16_t* __restrict__ dirs_bf,
-                       double* __restrict__ cnorm, const int32_t* __restrict__ active) {
+                       double* __restrict__ cnorm, float* __restrict__ deps,
+                       const int32_t* __restrict__ active) {
   const uint32_t u = blockIdx.y;
   if (active && !active[u]) return;
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -70,17 +71,23 @@ __global__ void k_dirs(const float* __restrict__ cents, uint32_t C, uint32_t c_s
   uint16_t* db = dirs_bf + (size_t(u) * c_pad + c) * D;
   if (c >= C) {  // padding columns of the MMA operand
     for (int j = 0; j < D; ++j) { dr[j] = 0.f; db[j] = 0; }
+    deps[size_t(u) * c_pad + c] = 0.f;
     return;
   }
   const float* src = cents + (size_t(u) * c_stride + c) * D;
   double nrm = sqrt(dot_seq_ff(src, src));
   cnorm[size_t(u) * c_pad + c] = nrm;
+  double e2 = 0.0;
   for (int j = 0; j < D; ++j) {
     float x = src[j];
     float y = nrm > 0.0 ? float(double(x) / nrm) : x;
     dr[j] = y;
-    db[j] = f32_to_bf16_rn(y);
+    const uint16_t b = f32_to_bf16_rn(y);
+    db[j] = b;
+    const double e = double(y) - double(bf16_to_f32(b));
+    e2 += e * e;
   }
+  deps[size_t(u) * c_pad + c] = float(sqrt(e2)) * 1.0001f;
 }
 
 // ---------------------------------------------------------------------------
@@ -128,7 +135,7 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
          uint32_t c_pad, uint32_t label_stride, const uint32_t* __restrict__ sizes,
          const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
          float* __restrict__ cents, float* __restrict__ dirs, uint16_t* __restrict__ dirs_bf,
-         double* __restrict__ cnorm, const int32_t* __restrict__ active) {
+         double* __restrict__ cnorm, float* __restrict__ deps, const int32_t* __restrict__ active) {
   const uint32_t u = blockIdx.y;
   if (active && !active[u]) return;
   const uint32_t c = blockIdx.x * (blockDim.x >> 5) + warp_id();
@@ -138,37 +145,36 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
   uint16_t* db = dirs_bf + (size_t(u) * c_pad + c) * D;
   if (c >= C) {
     for (int j = lane; j < D; j += 32) { dr[j] = 0.f; db[j] = 0; }
+    if (lane == 0) deps[size_t(u) * c_pad + c] = 0.f;
     return;
   }
   const uint32_t cnt = sizes[size_t(u) * c_stride + c];
   const uint32_t beg = starts[size_t(u) * (c_stride + 1) + c];
   const uint32_t* ids = sorted_ids + size_t(u) * label_stride + beg;
-  const uint16_t* kb = keys + u * key_stride;
+  const uint2* kb = reinterpret_cast<const uint2*>(keys + u * key_stride) + lane;
   double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-  uint32_t m = 0;
-  // software-pipelined member walk: prefetch 4 rows ahead
-  for (; m + 4 <= cnt; m += 4) {
-    uint2 v[4];
+  // member ids 32 at a time (one coalesced load), rows 16 in flight; the
+  // f64 adds stay in member (= position) order, as update_centroids sums.
+  for (uint32_t m0 = 0; m0 < cnt; m0 += 32) {
+    const uint32_t nb = min(32u, cnt - m0);
+    const uint32_t myid = uint32_t(lane) < nb ? __ldg(ids + m0 + lane) : 0u;
+    for (uint32_t k0 = 0; k0 < nb; k0 += 16) {
+      uint2 v[16];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t id = __ldg(ids + m + k);
-      v[k] = __ldg(reinterpret_cast<const uint2*>(kb + size_t(id) * D) + lane);
-    }
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t id = __shfl_sync(0xffffffffu, myid, (k0 + k) & 31);
+        v[k] = k0 + k < nb ? __ldg(kb + size_t(id) * (D / 4)) : make_uint2(0, 0);
+      }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      a0 += double(__uint_as_float(v[k].x << 16));
-      a1 += double(__uint_as_float(v[k].x & 0xffff0000u));
-      a2 += double(__uint_as_float(v[k].y << 16));
-      a3 += double(__uint_as_float(v[k].y & 0xffff0000u));
+      for (int k = 0; k < 16; ++k) {
+        if (k0 + k < nb) {
+          a0 += double(__uint_as_float(v[k].x << 16));
+          a1 += double(__uint_as_float(v[k].x & 0xffff0000u));
+          a2 += double(__uint_as_float(v[k].y << 16));
+          a3 += double(__uint_as_float(v[k].y & 0xffff0000u));
+        }
+      }
     }
-  }
-  for (; m < cnt; ++m) {
-    uint32_t id = __ldg(ids + m);
-    uint2 v = __ldg(reinterpret_cast<const uint2*>(kb + size_t(id) * D) + lane);
-    a0 += double(__uint_as_float(v.x << 16));
-    a1 += double(__uint_as_float(v.x & 0xffff0000u));
-    a2 += double(__uint_as_float(v.y << 16));
-    a3 += double(__uint_as_float(v.y & 0xffff0000u));
   }
   const double dc = double(cnt);
   float x0 = float(a0 / dc), x1 = float(a1 / dc), x2 = float(a2 / dc), x3 = float(a3 / dc);
@@ -197,6 +203,13 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
   pk.x = uint32_t(f32_to_bf16_rn(d0)) | (uint32_t(f32_to_bf16_rn(d1)) << 16);
   pk.y = uint32_t(f32_to_bf16_rn(d2)) | (uint32_t(f32_to_bf16_rn(d3)) << 16);
   reinterpret_cast<uint2*>(db)[lane] = pk;
+  // |dir - bf16(dir)|: the per-centroid error the tensor-core band uses
+  const double e0 = double(d0) - double(__uint_as_float(pk.x << 16));
+  const double e1 = double(d1) - double(__uint_as_float(pk.x & 0xffff0000u));
+  const double e2 = double(d2) - double(__uint_as_float(pk.y << 16));
+  const double e3 = double(d3) - double(__uint_as_float(pk.y & 0xffff0000u));
+  const double ee = warp_sum(e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
+  if (lane == 0) deps[size_t(u) * c_pad + c] = float(sqrt(ee)) * 1.0001f;
 }
 
 // ---------------------------------------------------------------------------
@@ -346,6 +359,7 @@ __global__ void k_copy_labels(const int32_t* __restrict__ src, int32_t* __restri
 // is unsupported so the caller falls back to the exact path
 int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
               uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs_bf,
+              const float* deps,
               const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
               void* scratch, size_t scratch_bytes, uint64_t* launches);
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C);
@@ -384,7 +398,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   const bool want_obj = (a.flags & CKV_KM_OBJECTIVE) != 0;
 
   // ---- scratch ----------------------------------------------------------
-  DevBuf b_flags, b_lab1, b_sizes, b_starts, b_sorted, b_dirs, b_dirsbf, b_cnorm, b_active,
+  DevBuf b_flags, b_lab1, b_sizes, b_starts, b_sorted, b_dirs, b_dirsbf, b_cnorm, b_deps, b_active,
       b_changed, b_conv, b_iters, b_empty, b_rep, b_replog, b_obj, b_objlog, b_nact, b_tc;
   const uint32_t LS = a.label_stride, CS = a.c_stride;
   CKV_TRY(dalloc(b_flags, sizeof(int32_t) * U));
@@ -395,6 +409,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   CKV_TRY(dalloc(b_dirs, sizeof(float) * size_t(U) * c_pad * D));
   CKV_TRY(dalloc(b_dirsbf, sizeof(uint16_t) * size_t(U) * c_pad * D));
   CKV_TRY(dalloc(b_cnorm, sizeof(double) * size_t(U) * c_pad));
+  CKV_TRY(dalloc(b_deps, sizeof(float) * size_t(U) * c_pad));
   CKV_TRY(dalloc(b_active, sizeof(int32_t) * U));
   CKV_TRY(dalloc(b_changed, sizeof(int32_t) * U));
   CKV_TRY(dalloc(b_conv, sizeof(int32_t) * U));
@@ -443,6 +458,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   float* dirs = b_dirs.as<float>();
   uint16_t* dirs_bf = b_dirsbf.as<uint16_t>();
   double* cnorm = b_cnorm.as<double>();
+  float* deps = b_deps.as<float>();
   int32_t* active = b_active.as<int32_t>();
 
   // active = 1, others = 0
@@ -464,13 +480,13 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
                                                 a.centroids);
   CKV_LAUNCH_CHECK("k_init_centroids");
   k_dirs<<<dim3((c_pad + 127) / 128, U), 128, 0, st>>>(a.centroids, C, CS, c_pad, dirs, dirs_bf,
-                                                       cnorm, active);
+                                                       cnorm, deps, active);
   CKV_LAUNCH_CHECK("k_dirs");
   ctx->launches += 2;
 
   auto assign = [&](int32_t* out) -> int {
     if (use_tc)
-      return assign_tc(st, a.keys, a.key_stride, n, C, c_pad, U, dirs_bf, dirs, out, LS, active,
+      return assign_tc(st, a.keys, a.key_stride, n, C, c_pad, U, dirs_bf, deps, dirs, out, LS, active,
                        b_tc.p, tc_bytes, &ctx->launches);
     k_assign_exact<<<dim3((n + 127) / 128, U), 128, 0, st>>>(a.keys, a.key_stride, n, C, c_pad,
                                                             dirs, out, LS, active);
@@ -532,7 +548,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     // update from the previous labels (sizes/starts/sorted hold its sort)
     k_update<<<dim3((c_pad + 7) / 8, U), 256, 0, st>>>(
         a.keys, a.key_stride, C, CS, c_pad, LS, b_sizes.as<uint32_t>(), b_starts.as<uint32_t>(),
-        b_sorted.as<uint32_t>(), a.centroids, dirs, dirs_bf, cnorm, active);
+        b_sorted.as<uint32_t>(), a.centroids, dirs, dirs_bf, cnorm, deps, active);
     CKV_LAUNCH_CHECK("k_update");
     ctx->launches++;
     if (dbg) cudaEventRecord(dev_[1], st);
