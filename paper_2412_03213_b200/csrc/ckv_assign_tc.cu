@@ -64,6 +64,7 @@ struct TcBars {
   float m_ch[2][TC_M];                    // chunk maxima of the current tile
   uint32_t n_ch[2][TC_M];                 // in-band columns per chunk
   uint16_t id_ch[2][TC_NCAND][TC_M];      // their ids (first TC_NCAND)
+  uint32_t fix_n;                         // this CTA's fix-up entries
 };
 constexpr uint32_t TC_ABYTES = TC_M * 128 * 2;  // one key-tile stage (both k-halves)
 constexpr uint32_t TC_BOXR = 32;                // rows per B TMA box (B sized to c_pad)
@@ -193,10 +194,11 @@ struct TcArgs {
   const float* knorm;          // [unit][n] key norms (band scale)
   const float* eps_u;          // [unit] max_c |dir_c - bf16(dir_c)|
   int32_t* labels;
-  uint32_t* fix_count;         // device counter
+  uint32_t* fix_count;         // [gridDim.x] per-CTA fix-up counts (region = w0 * 128)
   uint4* fix_list;             // {unit, row, n_cand | FULL, 0}
   uint32_t fix_cap;
   uint32_t* fix_ids;           // [fix_cap][8] candidate ids
+  uint32_t mode;               // experiment knob (CKV_TC_MODE): 1 = no epilogue math
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -208,7 +210,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   const uint32_t S = a.stages;
   uint8_t* sm_a = sbase;                         // [S][2][TC_M*128]
   uint8_t* sm_b = sbase + S * TC_ABYTES;         // [2][c_pad*128]
-  TcBars& sm = *reinterpret_cast<TcBars*>(sm_b + 2 * a.c_pad * 128);
+  __shared__ TcBars sm;  // static: the compiler keeps these accesses LDS/STS
   auto A = [&](uint32_t st, uint32_t kh) { return sm_a + st * TC_ABYTES + kh * (TC_M * 128); };
   auto Bp = [&](uint32_t kh, uint32_t row) { return sm_b + kh * (a.c_pad * 128) + row * 128; };
   const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
@@ -223,6 +225,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     mb_init(&sm.b_full, 1);
     mb_init(&sm.b_empty, 1);
     for (int s = 0; s < 2; ++s) { mb_init(&sm.acc_full[s], 1); mb_init(&sm.acc_empty[s], 4 * TC_EGROUPS); }
+    sm.fix_n = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (wid == 1) {  // TMEM: 512 columns (two 256-column accumulator buffers)
@@ -319,12 +322,32 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     uint32_t g = 0;
     if (grp == 0)
       for (int ch = 0; ch < 2; ++ch) sm.n_ch[ch][lane_row] = 0;
+    // (unit, tile) advance incrementally; the next tile's key norm is loaded
+    // one tile ahead so its latency hides behind this tile's work
+    uint32_t ui = w0 / a.tiles_per_unit, tile = w0 % a.tiles_per_unit;
+    uint32_t unit = w0 < w1 ? uint32_t(a.unit_list[ui]) : 0u;
+    float eps = w0 < w1 ? a.eps_u[unit] : 0.f;
+    float kn_next = 0.f;
+    if (w0 < w1 && tile * TC_M + lane_row < a.n)
+      kn_next = a.knorm[size_t(unit) * a.n + tile * TC_M + lane_row];
     for (uint32_t w = w0; w < w1; ++w) {
-      const uint32_t ui = w / a.tiles_per_unit, tile = w % a.tiles_per_unit;
-      const uint32_t unit = uint32_t(a.unit_list[ui]);
+      if (w > w0) {
+        if (++tile == a.tiles_per_unit) {
+          tile = 0;
+          ++ui;
+          unit = uint32_t(a.unit_list[ui]);
+          eps = a.eps_u[unit];
+        }
+      }
       const uint32_t row = tile * TC_M + lane_row;
-      const float kn = row < a.n ? a.knorm[size_t(unit) * a.n + row] : 0.f;
-      const float band = kn * (2.0f * a.eps_u[unit] + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
+      const float kn = kn_next;
+      if (w + 1 < w1) {
+        uint32_t t2 = tile + 1, u2 = unit;
+        if (t2 == a.tiles_per_unit) { t2 = 0; u2 = uint32_t(a.unit_list[ui + 1]); }
+        const uint32_t r2 = t2 * TC_M + lane_row;
+        kn_next = r2 < a.n ? a.knorm[size_t(u2) * a.n + r2] : 0.f;
+      }
+      const float band = kn * (2.0f * eps + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
 #pragma unroll 1
       for (uint32_t ch = 0; ch < nchunks; ++ch) {
         const uint32_t buf = g & 1, bph = (g >> 1) & 1;
@@ -344,6 +367,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
         __syncwarp();
         if (lane == 0) mb_arrive(&sm.acc_empty[buf]);  // scores now live in registers
         const uint32_t cb0 = c0 + b0 * 32, cb1 = c0 + b1 * 32;
+        if (a.mode == 1) {
+          if (grp == 0) sm.m_ch[ch][lane_row] = 0.f;
+          qbar();
+          qbar();
+          continue;
+        }
         // padding columns (only in the unit's last block; warp-uniform branch)
         if (h0 && cb0 + 32 > a.C) {
 #pragma unroll
@@ -411,7 +440,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
         qbar();
       }
       if (grp == 0) {
-        if (row < a.n) {
+        if (row < a.n && a.mode == 0) {
           float M = sm.m_ch[0][lane_row];
           if (nchunks > 1) M = fmaxf(M, sm.m_ch[1][lane_row]);
           bool full = !(M > -INFINITY);
@@ -430,12 +459,9 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
             *lab = int32_t(single);
           } else {
             *lab = -1;
-            const unsigned want = __activemask();
-            const uint32_t leader = __ffs(want) - 1;
-            uint32_t base = 0;
-            if (uint32_t(lane) == leader) base = atomicAdd(a.fix_count, __popc(want));
-            base = __shfl_sync(want, base, leader);
-            const uint32_t slot = base + __popc(want & ((1u << lane) - 1u));
+            // this CTA's region of the list: a shared-memory counter, no
+            // device-wide atomic (one hot address across all SMs serialises)
+            const uint32_t slot = w0 * TC_M + atomicAdd(&sm.fix_n, 1u);
             if (slot < a.fix_cap) {
               a.fix_list[slot] = make_uint4(unit, row, full ? TC_FULL : nin, 0u);
               uint32_t* fi = a.fix_ids + size_t(slot) * TC_NCAND;
@@ -454,6 +480,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     }
   }
   __syncthreads();
+  if (t == 0) a.fix_count[blockIdx.x] = sm.fix_n;
   if (wid == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -496,14 +523,22 @@ __device__ __forceinline__ double lane_partial(const double k[4], const float4 d
 
 __global__ void __launch_bounds__(256)
 k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
-        const uint32_t* __restrict__ count, const uint16_t* __restrict__ keys,
+        const uint32_t* __restrict__ count, const int32_t* __restrict__ n_active,
+        uint32_t tiles_per_unit, const uint16_t* __restrict__ keys,
         uint64_t key_stride, const float* __restrict__ dirs, uint32_t C, uint32_t c_pad,
         const float* __restrict__ knorm, uint32_t n, int32_t* __restrict__ labels,
         uint32_t label_stride) {
-  const uint32_t nfix = *count;
+  // region r = blockIdx.y holds count[r] entries from index r * per * 128
+  // (k_assign_tc's CTA r processed tiles [r * per, (r + 1) * per))
+  const uint32_t r = blockIdx.y;
+  const uint32_t total = uint32_t(*n_active) * tiles_per_unit;
+  const uint32_t per = (total + gridDim.y - 1) / gridDim.y;
+  const uint32_t nfix = count[r];
+  const uint32_t rbase = r * per * TC_M;
   const int lane = lane_id();
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t e = blockIdx.x * (blockDim.x >> 5) + warp_id(); e < nfix; e += nw) {
+  for (uint32_t e0 = blockIdx.x * (blockDim.x >> 5) + warp_id(); e0 < nfix; e0 += nw) {
+    const uint32_t e = rbase + e0;
     const uint4 it = list[e];
     const uint32_t u = it.x, row = it.y;
     const bool full = it.z == TC_FULL;
@@ -625,9 +660,9 @@ TcScratch carve(void* base, uint32_t n_units, uint32_t n) {
   p += align256(size_t(n_units) * 4);
   s.count = reinterpret_cast<int32_t*>(p);
   p += 256;
-  s.fix_count = reinterpret_cast<uint32_t*>(p);
-  p += 256;
-  s.fix_cap = n_units * n;  // every key can need a fix-up
+  s.fix_count = reinterpret_cast<uint32_t*>(p);  // [grid] per-CTA counts
+  p += 4096;
+  s.fix_cap = n_units * ((n + TC_M - 1) / TC_M) * TC_M;  // every key can need a fix-up
   s.fix_list = reinterpret_cast<uint4*>(p);
   p += align256(size_t(s.fix_cap) * 16);
   s.fix_ids = reinterpret_cast<uint32_t*>(p);
@@ -685,8 +720,8 @@ int assign_tc_prepare(cudaStream_t st, const uint16_t* keys, uint64_t key_stride
 
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
   (void)C;
-  return align256(size_t(n_units) * 4) + 512 + align256(size_t(n_units) * n * 16) +
-         align256(size_t(n_units) * n * 32) + align256(size_t(n_units) * n * 4) +
+  const size_t cap = size_t(n_units) * ((n + TC_M - 1) / TC_M) * TC_M;
+  return align256(size_t(n_units) * 4) + 256 + 4096 + align256(cap * 16) + align256(cap * 32) + align256(size_t(n_units) * n * 4) +
          align256(size_t(n_units) * 4) + 256;
 }
 
@@ -724,33 +759,43 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   ta.fix_list = s.fix_list;
   ta.fix_cap = s.fix_cap;
   ta.fix_ids = s.fix_ids;
-  const size_t max_smem = 232448;  // 227 KB opt-in per CTA
-  const size_t fixed = 1024 + 2 * size_t(c_pad) * 128 + sizeof(TcBars);
-  ta.stages = uint32_t(std::min<size_t>(4, (max_smem - fixed) / TC_ABYTES));
+  static size_t max_dyn = 0;  // opt-in per-CTA smem minus the kernel's static part
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    int optin = 0;
+    cudaFuncAttributes fa;
+    CKV_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CKV_CUDA_TRY(cudaFuncGetAttributes(&fa, k_assign_tc));
+    max_dyn = size_t(optin) - fa.sharedSizeBytes;
+    CKV_CUDA_TRY(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(max_dyn)));
+    attr_dev = dev;
+  }
+  static const uint32_t tc_mode = getenv("CKV_TC_MODE") ? uint32_t(atoi(getenv("CKV_TC_MODE"))) : 0u;
+  ta.mode = tc_mode;
+  const size_t fixed = 1024 + 2 * size_t(c_pad) * 128;
+  ta.stages = uint32_t(std::min<size_t>(4, (max_dyn - fixed) / TC_ABYTES));
   if (ta.stages < 2) {
     set_error("assign_tc: not enough shared memory for two key-tile stages");
     return CKV_EINVAL;
   }
   const size_t smem = fixed + size_t(ta.stages) * TC_ABYTES;
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(max_smem)));
-    attr_dev = dev;
-  }
   k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
   CKV_LAUNCH_CHECK("k_assign_tc");
-  k_fixup<<<num_sms() * 8, 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, keys, key_stride,
+  k_fixup<<<dim3(8, num_sms()), 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, s.count,
+                                               ta.tiles_per_unit, keys, key_stride,
                                           dirs, C, c_pad, s.knorm, n, labels, label_stride);
   CKV_LAUNCH_CHECK("k_fixup");
   *launches += 4;
   static const bool dbg = getenv("CKV_DEBUG_KMEANS") != nullptr;
   if (dbg) {
-    uint32_t nfix = 0;
-    cudaMemcpyAsync(&nfix, s.fix_count, 4, cudaMemcpyDeviceToHost, st);
+    std::vector<uint32_t> cnts(num_sms());
+    cudaMemcpyAsync(cnts.data(), s.fix_count, 4 * cnts.size(), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
+    uint32_t nfix = 0;
+    for (uint32_t c : cnts) nfix += c;
     fprintf(stderr, "[kmeans dbg] assign_tc fix-ups %u of %u keys (%.2f%%)\n", nfix,
             n * n_units, 100.0 * nfix / (double(n) * n_units));
   }
