@@ -19,7 +19,7 @@ BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libckv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
 
@@ -34,9 +34,11 @@ def _compile(src: str) -> tuple[str, str]:
     deps.append(os.path.join(ROOT, "include", "ckv_cuda.h"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj, ""
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]
+    # CUDA sources in C++17; the C++ drop-in shim needs C++20 (std::span, the
+    # reference headers' dialect)
+    cmd = [NVCC, *ARCH, *FLAGS, "-std=c++17", "-c", path, "-o", obj]
     if src.endswith(".cpp"):
-        cmd = [NVCC, *ARCH, *FLAGS, "-x", "cu", "-c", path, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, "-std=c++20", "-x", "cu", "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

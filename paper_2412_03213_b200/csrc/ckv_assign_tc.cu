@@ -609,18 +609,6 @@ __global__ void k_eps_max(const float* __restrict__ deps, uint32_t c_pad, uint32
   if (lane_id() == 0) eps_u[u] = m;
 }
 
-__global__ void k_key_norms(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
-                            float* __restrict__ knorm) {
-  const uint32_t u = blockIdx.y;
-  const uint32_t i = blockIdx.x * (blockDim.x >> 5) + warp_id();
-  if (i >= n) return;
-  const uint2 v = reinterpret_cast<const uint2*>(keys + u * key_stride + size_t(i) * D)[lane_id()];
-  const float a = __uint_as_float(v.x << 16), b = __uint_as_float(v.x & 0xffff0000u);
-  const float c = __uint_as_float(v.y << 16), d = __uint_as_float(v.y & 0xffff0000u);
-  const float s = warp_sum(a * a + b * b + c * c + d * d);
-  if (lane_id() == 0) knorm[size_t(u) * n + i] = sqrtf(s) * 1.0001f;  // rounding margin
-}
-
 __global__ void k_compact_active(const int32_t* __restrict__ active, uint32_t n_units,
                                   int32_t* __restrict__ list, int32_t* __restrict__ count,
                                   uint32_t* __restrict__ fix_count) {
@@ -709,13 +697,10 @@ int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows
 }
 }  // namespace
 
-// key norms (the band scale): once per k-means run, keys never change
-int assign_tc_prepare(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
-                      uint32_t n_units, void* scratch) {
-  TcScratch s = carve(scratch, n_units, n);
-  k_key_norms<<<dim3((n + 7) / 8, n_units), 256, 0, st>>>(keys, key_stride, n, s.knorm);
-  CKV_LAUNCH_CHECK("k_key_norms");
-  return CKV_OK;
+// key norms (the band scale) live in the scratch; k_scan_keys (ckv_kmeans.cu)
+// fills them once per k-means run, keys never change
+float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n) {
+  return carve(scratch, n_units, n).knorm;
 }
 
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <random>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -39,14 +40,22 @@ uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b) {
 // clustering.hpp:186-193 (std::mt19937_64 is bit-specified by the standard;
 // uniform_below is rng() % n, common.hpp:124-126)
 void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows) {
+  // the reference's partial Fisher-Yates over pool = 0..n-1, with the pool
+  // kept sparse (only the <= 2C touched slots), so a unit costs O(C) not O(n)
   std::mt19937_64 rng(seed);
-  std::vector<uint32_t> pool(n);
-  for (uint32_t i = 0; i < n; ++i) pool[i] = i;
+  std::unordered_map<uint32_t, uint32_t> pool;
+  pool.reserve(size_t(2) * C);
+  auto get = [&](uint32_t i) {
+    auto it = pool.find(i);
+    return it == pool.end() ? i : it->second;
+  };
   for (uint32_t c = 0; c < C; ++c) {
-    uint32_t j = c + uint32_t(rng() % uint64_t(n - c));
-    std::swap(pool[c], pool[j]);
+    const uint32_t j = c + uint32_t(rng() % uint64_t(n - c));
+    const uint32_t pc = get(c), pj = get(j);
+    pool[c] = pj;
+    pool[j] = pc;
+    rows[c] = pj;
   }
-  std::copy(pool.begin(), pool.begin() + C, rows);
 }
 
 // ---------------------------------------------------------------------------
@@ -160,6 +169,7 @@ int ckv_ctx_create(int device, void* stream, ckv_ctx** out) {
   if (!out) { set_error("ckv_ctx_create: out is NULL"); return CKV_EINVAL; }
   CKV_CUDA_TRY(cudaSetDevice(device));
   ckv_ctx* c = new ckv_ctx();
+  for (int i = 0; i < 32; ++i) { c->scratch[i] = nullptr; c->scratch_cap[i] = 0; }
   c->device = device;
   // NULL is the CUDA legacy default stream (torch's default stream too), so
   // work launched here is ordered with the caller's default-stream work.
@@ -174,6 +184,8 @@ int ckv_ctx_destroy(ckv_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+  for (int i = 0; i < 32; ++i)
+    if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
   delete ctx;
   return CKV_OK;
 }

@@ -11,6 +11,11 @@ struct ckv_ctx {
   // pinned host scratch for small control read-backs
   int32_t* h_flags = nullptr;
   size_t h_flags_cap = 0;
+  // grow-only device scratch slots reused across calls on this context
+  // (cudaMalloc / cudaFree of ~0.5 GB per k-means call cost milliseconds and
+  // device-wide synchronisation)
+  void* scratch[32];        // zeroed in ckv_ctx_create
+  size_t scratch_cap[32];
 };
 
 namespace ckvb {

@@ -23,23 +23,73 @@ namespace ckvb {
 
 // ---------------------------------------------------------------------------
 // validation: kmeans_cosine's input checks (clustering.hpp:166-172)
-// flags[u]: bit0 = some non-finite value, bit1 = some row with norm >= 1e-12
+// flags[u]: bit0 = some non-finite value, bit1 = some row with norm >= 1e-12,
+// bit2 = some non-zero element (k_validate_scan: a streaming pass; only a
+// unit whose non-zero elements are all tiny needs the per-row f64 norms of
+// k_validate_rows).
 // ---------------------------------------------------------------------------
-__global__ void k_validate(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
-                           int32_t* __restrict__ flags) {
+__global__ void __launch_bounds__(256)
+k_scan_keys(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
+            int32_t* __restrict__ flags, float* __restrict__ knorm) {
+  // one pass over the keys: validation flags (if flags) and the f32 key norms
+  // the tensor-core band scales with (if knorm).  A warp takes 16 rows, a
+  // half-warp one row per step (16 lanes x 16 B), all 8 loads in flight.
   const uint32_t u = blockIdx.y;
+  const int lane = lane_id(), half = lane >> 4, hl = lane & 15;
+  const uint32_t r0 = (blockIdx.x * (blockDim.x >> 5) + warp_id()) * 16;
+  const uint16_t* base = keys + u * key_stride;
+  // one element >= 1e-12 already gives its row norm >= 1e-12 (float threshold
+  // rounded up so the decision is never looser than the f64 comparison)
+  const float big = __uint_as_float(__float_as_uint(1e-12f) + 1u);
+  uint4 q[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t r = r0 + 2 * i + half;
+    q[i] = r < n ? __ldg(reinterpret_cast<const uint4*>(base + size_t(r) * D) + hl)
+                 : make_uint4(0, 0, 0, 0);
+  }
+  int f = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t w[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t b = h ? (w[k] >> 16) : (w[k] & 0xffffu);
+        const float x = __uint_as_float(b << 16);
+        ss = fmaf(x, x, ss);
+        if ((b & 0x7f80u) == 0x7f80u) f |= 1;
+        if (b & 0x7fffu) f |= 4;
+        if (fabsf(x) >= big) f |= 2;
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const uint32_t r = r0 + 2 * i + half;
+    if (knorm && hl == 0 && r < n) knorm[size_t(u) * n + r] = sqrtf(ss) * 1.0001f;  // rounding margin
+  }
+  if (flags) {
+    f = __reduce_or_sync(0xffffffffu, f);
+    if (lane == 0 && f) atomicOr(&flags[u], f);
+  }
+}
+
+__global__ void k_validate_rows(const uint16_t* __restrict__ keys, uint64_t key_stride,
+                                uint32_t n, int32_t* __restrict__ flags) {
+  const uint32_t u = blockIdx.y;
+  if ((flags[u] & 6) != 4) return;  // decided by the scan
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   int f = 0;
   if (i < n) {
     const uint16_t* row = keys + u * key_stride + size_t(i) * D;
     double s = 0.0;
     for (int j = 0; j < D; ++j) {
-      uint16_t b = row[j];
-      if ((b & 0x7f80u) == 0x7f80u) f |= 1;
-      float x = bf16_to_f32(b);
+      float x = bf16_to_f32(row[j]);
       s = __fma_rn(double(x), double(x), s);
     }
-    if (!(f & 1) && sqrt(s) >= 1e-12) f |= 2;
+    if (sqrt(s) >= 1e-12) f |= 2;
   }
   f = __reduce_or_sync(0xffffffffu, f);
   if (lane_id() == 0 && f) atomicOr(&flags[u], f);
@@ -363,26 +413,36 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
               const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
               void* scratch, size_t scratch_bytes, uint64_t* launches);
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C);
-int assign_tc_prepare(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
-                      uint32_t n_units, void* scratch);
+float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n);
 bool assign_tc_supported(uint32_t n, uint32_t C);
 
 // ---------------------------------------------------------------------------
 // host driver
 // ---------------------------------------------------------------------------
 namespace {
+// a view of one of the context's grow-only scratch slots
 struct DevBuf {
   void* p = nullptr;
-  ~DevBuf() { if (p) cudaFree(p); }
   template <typename T> T* as() { return static_cast<T*>(p); }
 };
-int dalloc(DevBuf& b, size_t bytes) {
+int dalloc(ckv_ctx* ctx, int slot, DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc(&b.p, bytes);
-  if (e != cudaSuccess) {
-    set_error(std::string("kmeans: device allocation failed: ") + cudaGetErrorString(e));
-    return CKV_ENOMEM;
+  if (ctx->scratch_cap[slot] < bytes) {
+    if (ctx->scratch[slot]) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->scratch[slot]);
+      ctx->scratch[slot] = nullptr;
+      ctx->scratch_cap[slot] = 0;
+    }
+    cudaError_t e = cudaMalloc(&ctx->scratch[slot], bytes);
+    if (e != cudaSuccess) {
+      ctx->scratch[slot] = nullptr;
+      set_error(std::string("kmeans: device allocation failed: ") + cudaGetErrorString(e));
+      return CKV_ENOMEM;
+    }
+    ctx->scratch_cap[slot] = bytes;
   }
+  b.p = ctx->scratch[slot];
   return CKV_OK;
 }
 }  // namespace
@@ -401,32 +461,32 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   DevBuf b_flags, b_lab1, b_sizes, b_starts, b_sorted, b_dirs, b_dirsbf, b_cnorm, b_deps, b_active,
       b_changed, b_conv, b_iters, b_empty, b_rep, b_replog, b_obj, b_objlog, b_nact, b_tc;
   const uint32_t LS = a.label_stride, CS = a.c_stride;
-  CKV_TRY(dalloc(b_flags, sizeof(int32_t) * U));
-  CKV_TRY(dalloc(b_lab1, sizeof(int32_t) * size_t(U) * LS));
-  CKV_TRY(dalloc(b_sizes, sizeof(uint32_t) * size_t(U) * CS));
-  CKV_TRY(dalloc(b_starts, sizeof(uint32_t) * size_t(U) * (CS + 1)));
-  CKV_TRY(dalloc(b_sorted, sizeof(uint32_t) * size_t(U) * LS));
-  CKV_TRY(dalloc(b_dirs, sizeof(float) * size_t(U) * c_pad * D));
-  CKV_TRY(dalloc(b_dirsbf, sizeof(uint16_t) * size_t(U) * c_pad * D));
-  CKV_TRY(dalloc(b_cnorm, sizeof(double) * size_t(U) * c_pad));
-  CKV_TRY(dalloc(b_deps, sizeof(float) * size_t(U) * c_pad));
-  CKV_TRY(dalloc(b_active, sizeof(int32_t) * U));
-  CKV_TRY(dalloc(b_changed, sizeof(int32_t) * U));
-  CKV_TRY(dalloc(b_conv, sizeof(int32_t) * U));
-  CKV_TRY(dalloc(b_iters, sizeof(uint32_t) * U));
-  CKV_TRY(dalloc(b_empty, sizeof(int32_t) * U));
-  CKV_TRY(dalloc(b_rep, sizeof(uint32_t) * U));
-  CKV_TRY(dalloc(b_replog, sizeof(uint32_t) * size_t(U) * (MI + 1)));
-  CKV_TRY(dalloc(b_obj, sizeof(double) * U));
-  CKV_TRY(dalloc(b_objlog, sizeof(double) * size_t(U) * (MI + 1)));
-  CKV_TRY(dalloc(b_nact, sizeof(int32_t)));
+  CKV_TRY(dalloc(ctx, 1, b_flags, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(ctx, 2, b_lab1, sizeof(int32_t) * size_t(U) * LS));
+  CKV_TRY(dalloc(ctx, 3, b_sizes, sizeof(uint32_t) * size_t(U) * CS));
+  CKV_TRY(dalloc(ctx, 4, b_starts, sizeof(uint32_t) * size_t(U) * (CS + 1)));
+  CKV_TRY(dalloc(ctx, 5, b_sorted, sizeof(uint32_t) * size_t(U) * LS));
+  CKV_TRY(dalloc(ctx, 6, b_dirs, sizeof(float) * size_t(U) * c_pad * D));
+  CKV_TRY(dalloc(ctx, 7, b_dirsbf, sizeof(uint16_t) * size_t(U) * c_pad * D));
+  CKV_TRY(dalloc(ctx, 8, b_cnorm, sizeof(double) * size_t(U) * c_pad));
+  CKV_TRY(dalloc(ctx, 9, b_deps, sizeof(float) * size_t(U) * c_pad));
+  CKV_TRY(dalloc(ctx, 10, b_active, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(ctx, 11, b_changed, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(ctx, 12, b_conv, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(ctx, 13, b_iters, sizeof(uint32_t) * U));
+  CKV_TRY(dalloc(ctx, 14, b_empty, sizeof(int32_t) * U));
+  CKV_TRY(dalloc(ctx, 15, b_rep, sizeof(uint32_t) * U));
+  CKV_TRY(dalloc(ctx, 16, b_replog, sizeof(uint32_t) * size_t(U) * (MI + 1)));
+  CKV_TRY(dalloc(ctx, 17, b_obj, sizeof(double) * U));
+  CKV_TRY(dalloc(ctx, 18, b_objlog, sizeof(double) * size_t(U) * (MI + 1)));
+  CKV_TRY(dalloc(ctx, 19, b_nact, sizeof(int32_t)));
 
   const bool use_tc = !(a.flags & CKV_KM_EXACT_ONLY) && assign_tc_supported(n, C);
   size_t tc_bytes = use_tc ? assign_tc_scratch_bytes(U, n, C) : 0;
+  float* knorm = nullptr;  // key norms for the tensor-core band, filled by k_scan_keys
   if (use_tc) {
-    CKV_TRY(dalloc(b_tc, tc_bytes));
-    CKV_TRY(assign_tc_prepare(st, a.keys, a.key_stride, n, U, b_tc.p));
-    ctx->launches++;
+    CKV_TRY(dalloc(ctx, 20, b_tc, tc_bytes));
+    knorm = assign_tc_knorm(b_tc.p, U, n);
   }
 
   if (!ctx->h_flags || ctx->h_flags_cap < U + 1) {
@@ -439,10 +499,14 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   // ---- validation (clustering.hpp:166-172) -------------------------------
   if (!(a.flags & CKV_KM_NO_VALIDATE)) {
     CKV_CUDA_TRY(cudaMemsetAsync(b_flags.p, 0, sizeof(int32_t) * U, st));
-    dim3 g((n + 255) / 256, U);
-    k_validate<<<g, 256, 0, st>>>(a.keys, a.key_stride, n, b_flags.as<int32_t>());
-    CKV_LAUNCH_CHECK("k_validate");
-    ctx->launches++;
+    k_scan_keys<<<dim3((n + 127) / 128, U), 256, 0, st>>>(a.keys, a.key_stride, n,
+                                                          b_flags.as<int32_t>(), knorm);
+    CKV_LAUNCH_CHECK("k_scan_keys");
+    knorm = nullptr;  // done
+    k_validate_rows<<<dim3((n + 255) / 256, U), 256, 0, st>>>(a.keys, a.key_stride, n,
+                                                              b_flags.as<int32_t>());
+    CKV_LAUNCH_CHECK("k_validate_rows");
+    ctx->launches += 2;
     CKV_CUDA_TRY(cudaMemcpyAsync(hf, b_flags.p, sizeof(int32_t) * U, cudaMemcpyDeviceToHost, st));
     CKV_CUDA_TRY(cudaStreamSynchronize(st));
     for (uint32_t u = 0; u < U; ++u)
@@ -452,6 +516,12 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
         set_error("kmeans: degenerate input, all keys zero-norm");
         return CKV_EINVAL;
       }
+  }
+  if (knorm) {  // validation skipped: the norms still need their pass
+    k_scan_keys<<<dim3((n + 127) / 128, U), 256, 0, st>>>(a.keys, a.key_stride, n, nullptr,
+                                                          knorm);
+    CKV_LAUNCH_CHECK("k_scan_keys");
+    ctx->launches++;
   }
 
   int32_t* lab[2] = {a.labels, b_lab1.as<int32_t>()};
