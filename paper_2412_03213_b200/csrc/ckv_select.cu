@@ -153,31 +153,27 @@ __device__ __forceinline__ void dbg_stamp(uint32_t h, int slot) {
 #endif
 }
 
-__global__ void __launch_bounds__(SW_WARPS * 32)
-k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_base,
-              const float* __restrict__ q, const float* __restrict__ cents,
-              const float* __restrict__ aval, const float* __restrict__ aerr,
-              const uint32_t* __restrict__ n_clusters, const uint32_t* __restrict__ sizes,
-              const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
-              uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
-              uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
-              uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
-              double* __restrict__ scores_out, CacheDev cache, uint32_t warp_bytes) {
-  const int lane = lane_id(), wid = warp_id();
-  const uint32_t h = blockIdx.x * SW_WARPS + wid;
-  if (h >= desc.n_q) return;
+// The selection of one q head h by one warp.  av / ae: the head's approximate
+// scores and their bounds (global scratch after K1, or shared memory in the
+// fused kernel); wbase: the warp's private smem (warp_bytes).
+__device__ __forceinline__ void select_head(
+    uint32_t h, const ckv_select_desc& desc, uint32_t p2, uint32_t row_base,
+    const float* __restrict__ q, const float* __restrict__ cents, const float* av,
+    const float* ae, const uint32_t* __restrict__ n_clusters, const uint32_t* __restrict__ sizes,
+    const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
+    uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, const ckv_runs& runs,
+    uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
+    uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
+    double* __restrict__ scores_out, const CacheDev& cache, unsigned char* wbase, WarpSel& ws) {
+  const int lane = lane_id();
   dbg_stamp(h, 0);
   const uint32_t unit = h / desc.group;
   const uint32_t C = n_clusters[unit];
   const uint32_t B = desc.budget;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  unsigned char* wbase = smraw + size_t(wid) * warp_bytes;
   unsigned long long* xkey = reinterpret_cast<unsigned long long*>(wbase);  // [p2]
   uint32_t* ids = reinterpret_cast<uint32_t*>(xkey + p2);                    // [p2]
   uint32_t* incl = ids + p2;                                                 // [p2]
   float (*stage)[D] = reinterpret_cast<float (*)[D]>(wbase);                 // [SW_STAGE][D]
-  __shared__ WarpSel wsa[SW_WARPS];
-  WarpSel& ws = wsa[wid];
 
   const float* cu = cents + size_t(unit) * desc.c_cap * D;
   const uint32_t* sz = sizes + size_t(unit) * desc.c_cap;
@@ -189,8 +185,6 @@ k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_ba
 
   if (fast) {
     // ---- 1. approximate pops ------------------------------------------------
-    const float* av = aval + size_t(h) * c_pad;
-    const float* ae = aerr + size_t(h) * c_pad;
     unsigned long long kr[SW_KPL];
     uint32_t szr[SW_KPL];
     float er[SW_KPL];
@@ -503,6 +497,104 @@ k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_ba
   dbg_stamp(h, 3);
 }
 
+__global__ void __launch_bounds__(SW_WARPS * 32)
+k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_base,
+              const float* __restrict__ q, const float* __restrict__ cents,
+              const float* __restrict__ aval, const float* __restrict__ aerr,
+              const uint32_t* __restrict__ n_clusters, const uint32_t* __restrict__ sizes,
+              const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
+              uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
+              uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
+              uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
+              double* __restrict__ scores_out, CacheDev cache, uint32_t warp_bytes) {
+  const int wid = warp_id();
+  const uint32_t h = blockIdx.x * SW_WARPS + wid;
+  if (h >= desc.n_q) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ WarpSel wsa[SW_WARPS];
+  select_head(h, desc, p2, row_base, q, cents, aval + size_t(h) * c_pad,
+              aerr + size_t(h) * c_pad, n_clusters, sizes, starts, sorted_ids, token_ids,
+              rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, scores_out, cache,
+              smraw + size_t(wid) * warp_bytes, wsa[wid]);
+}
+
+// ---------------------------------------------------------------------------
+// K1+K2 fused (the decode path): one CTA per kv unit.  All SF_WARPS warps
+// score the unit's centroids for its G q heads into shared memory — lane per
+// centroid row, a sequential fp32 chain per head (any summation order is
+// covered by E, see K1) — then warps 0..G-1 each select one head from those
+// scores.  No score round trip through HBM, and 8 warps per unit stream the
+// centroids instead of 1 per head.
+// ---------------------------------------------------------------------------
+constexpr int SF_WARPS = 8;
+
+template <int G>
+__global__ void __launch_bounds__(SF_WARPS * 32)
+k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_base,
+               const float* __restrict__ q, const float* __restrict__ cents,
+               const uint32_t* __restrict__ n_clusters, const uint32_t* __restrict__ sizes,
+               const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
+               uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
+               uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
+               uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
+               CacheDev cache, uint32_t warp_bytes) {
+  static_assert(G <= SF_WARPS, "one select warp per head");
+  const uint32_t unit = blockIdx.x;
+  const int lane = lane_id(), wid = warp_id();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ WarpSel wsa[G];
+  __shared__ __align__(16) float qs[D][G];  // q interleaved: one LDS per element for all heads
+  __shared__ float qn2[G];
+  float* av_s = reinterpret_cast<float*>(smraw + size_t(G) * warp_bytes);  // [G][c_pad]
+  float* ae_s = av_s + size_t(G) * c_pad;                                  // [G][c_pad]
+  const uint32_t C = n_clusters[unit];
+  const float* qu = q + size_t(unit) * G * D;
+  for (uint32_t i = threadIdx.x; i < uint32_t(G) * D; i += blockDim.x) {
+    const uint32_t g = i / D, j = i % D;
+    qs[j][g] = qu[i];
+  }
+  if (wid < G) {
+    const float4 qv = __ldg(reinterpret_cast<const float4*>(qu + size_t(wid) * D) + lane);
+    const float s2 = warp_sum(qv.x * qv.x + qv.y * qv.y + qv.z * qv.z + qv.w * qv.w);
+    if (lane == 0) qn2[wid] = s2;
+  }
+  __syncthreads();
+  float qnrm[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) qnrm[g] = SEL_ERR * sqrtf(qn2[g]);
+  const float* cu = cents + size_t(unit) * desc.c_cap * D;
+  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+    const float4* row = reinterpret_cast<const float4*>(cu + size_t(c) * D);
+    float acc[G], mn = 0.f;
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g] = 0.f;
+#pragma unroll 8
+    for (int j4 = 0; j4 < D / 4; ++j4) {
+      const float4 m = __ldg(row + j4);
+      const float mm[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        mn = fmaf(mm[e], mm[e], mn);
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] = fmaf(qs[4 * j4 + e][g], mm[e], acc[g]);
+      }
+    }
+    const float ms = sqrtf(mn);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      av_s[size_t(g) * c_pad + c] = acc[g];
+      ae_s[size_t(g) * c_pad + c] = fmaf(qnrm[g], ms, 1e-30f);
+    }
+  }
+  __syncthreads();
+  if (wid >= G) return;
+  const uint32_t h = unit * G + wid;
+  select_head(h, desc, p2, row_base, q, cents, av_s + size_t(wid) * c_pad,
+              ae_s + size_t(wid) * c_pad, n_clusters, sizes, starts, sorted_ids, token_ids,
+              rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, nullptr, cache,
+              smraw + size_t(wid) * warp_bytes, wsa[wid]);
+}
+
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap) {
   const uint32_t c_pad = (c_cap + 31) / 32 * 32;
   return size_t(n_q) * c_pad * 8 + 64;  // aval + aerr
@@ -543,6 +635,37 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   cudaEvent_t ev[3];
   if (dbg) for (auto& e : ev) cudaEventCreate(&e);
   if (dbg) cudaEventRecord(ev[0], st);
+  uint32_t p2 = 64;
+  while (p2 < desc.c_cap) p2 <<= 1;
+  const uint32_t warp_bytes =
+      uint32_t(std::max<size_t>(size_t(p2) * 16, size_t(SW_STAGE) * D * 4));
+  static const bool unfused = getenv("CKV_SELECT_UNFUSED") != nullptr;
+  if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused) {
+    const size_t smem_f = size_t(G) * warp_bytes + size_t(G) * c_pad * 8;
+    if (smem_f <= 200 * 1024) {
+      static int attr_f = -1;
+      int dev_f = 0;
+      cudaGetDevice(&dev_f);
+      if (attr_f != dev_f) {
+        CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_f = dev_f;
+      }
+#define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
+    token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes
+      switch (G) {
+        case 1: k_select_fused<1><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
+        case 2: k_select_fused<2><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
+        case 4: k_select_fused<4><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
+        default: k_select_fused<8><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
+      }
+#undef CKV_SF_ARGS
+      CKV_LAUNCH_CHECK("k_select_fused");
+      return CKV_OK;
+    }
+  }
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES))) {
     const dim3 g1(units, (c_pad + SC_WARPS * SC_ROWS - 1) / (SC_WARPS * SC_ROWS));
     switch (G) {
@@ -554,10 +677,6 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
     CKV_LAUNCH_CHECK("k_score_approx");
   }
   if (dbg) cudaEventRecord(ev[1], st);
-  uint32_t p2 = 64;
-  while (p2 < desc.c_cap) p2 <<= 1;
-  const uint32_t warp_bytes =
-      uint32_t(std::max<size_t>(size_t(p2) * 16, size_t(SW_STAGE) * D * 4));
   const size_t smem = size_t(warp_bytes) * SW_WARPS;
   if (smem > 200 * 1024) {
     set_error("select: cluster capacity too large for the smem ranking buffers");
