@@ -537,25 +537,29 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
                uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
                uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
                uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
-               CacheDev cache, uint32_t warp_bytes) {
+               CacheDev cache, uint32_t warp_bytes, uint32_t mode) {
   static_assert(G <= SF_WARPS, "one select warp per head");
   const uint32_t unit = blockIdx.x;
   const int lane = lane_id(), wid = warp_id();
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ WarpSel wsa[G];
-  __shared__ __align__(16) float qs[D][G];  // q interleaved: one LDS per element for all heads
   __shared__ float qn2[G];
   float* av_s = reinterpret_cast<float*>(smraw + size_t(G) * warp_bytes);  // [G][c_pad]
   float* ae_s = av_s + size_t(G) * c_pad;                                  // [G][c_pad]
   const uint32_t C = n_clusters[unit];
   const float* qu = q + size_t(unit) * G * D;
-  for (uint32_t i = threadIdx.x; i < uint32_t(G) * D; i += blockDim.x) {
-    const uint32_t g = i / D, j = i % D;
-    qs[j][g] = qu[i];
-  }
+  // 8 lanes per centroid row (lane sub holds float4 columns sub, sub+8, +16,
+  // +24: 128 contiguous bytes per row per load), 4 rows per warp step
+  const int sub = lane & 7, rsel = lane >> 3;
+  float4 qv[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      qv[g][k] = __ldg(reinterpret_cast<const float4*>(qu + size_t(g) * D) + sub + 8 * k);
   if (wid < G) {
-    const float4 qv = __ldg(reinterpret_cast<const float4*>(qu + size_t(wid) * D) + lane);
-    const float s2 = warp_sum(qv.x * qv.x + qv.y * qv.y + qv.z * qv.z + qv.w * qv.w);
+    const float4 qw = __ldg(reinterpret_cast<const float4*>(qu + size_t(wid) * D) + lane);
+    const float s2 = warp_sum(qw.x * qw.x + qw.y * qw.y + qw.z * qw.z + qw.w * qw.w);
     if (lane == 0) qn2[wid] = s2;
   }
   __syncthreads();
@@ -563,31 +567,52 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
 #pragma unroll
   for (int g = 0; g < G; ++g) qnrm[g] = SEL_ERR * sqrtf(qn2[g]);
   const float* cu = cents + size_t(unit) * desc.c_cap * D;
-  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
-    const float4* row = reinterpret_cast<const float4*>(cu + size_t(c) * D);
-    float acc[G], mn = 0.f;
+  for (uint32_t c0 = uint32_t(wid) * 8; c0 < C; c0 += SF_WARPS * 8) {  // 2 steps of 4 rows
+    float4 m[2][4];
 #pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = 0.f;
-#pragma unroll 8
-    for (int j4 = 0; j4 < D / 4; ++j4) {
-      const float4 m = __ldg(row + j4);
-      const float mm[4] = {m.x, m.y, m.z, m.w};
+    for (int st2 = 0; st2 < 2; ++st2) {
+      const uint32_t c = c0 + 4 * st2 + rsel;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        mn = fmaf(mm[e], mm[e], mn);
-#pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = fmaf(qs[4 * j4 + e][g], mm[e], acc[g]);
-      }
+      for (int k = 0; k < 4; ++k)
+        m[st2][k] = c < C ? __ldg(reinterpret_cast<const float4*>(cu + size_t(c) * D) + sub + 8 * k)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const float ms = sqrtf(mn);
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      av_s[size_t(g) * c_pad + c] = acc[g];
-      ae_s[size_t(g) * c_pad + c] = fmaf(qnrm[g], ms, 1e-30f);
+    for (int st2 = 0; st2 < 2; ++st2) {
+      float acc[G], mn = 0.f;
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[g] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float4 x = m[st2][k];
+        mn = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, fmaf(x.w, x.w, mn))));
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float4 y = qv[g][k];
+          acc[g] = fmaf(x.x, y.x, fmaf(x.y, y.y, fmaf(x.z, y.z, fmaf(x.w, y.w, acc[g]))));
+        }
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        mn += __shfl_xor_sync(0xffffffffu, mn, o);
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
+      }
+      const uint32_t c = c0 + 4 * st2 + rsel;
+      if (c < C && sub < G) {  // lane sub writes head sub (G <= 8)
+        float a = acc[0];
+#pragma unroll
+        for (int g = 1; g < G; ++g) if (sub == g) a = acc[g];
+        float qn = qnrm[0];
+#pragma unroll
+        for (int g = 1; g < G; ++g) if (sub == g) qn = qnrm[g];
+        av_s[size_t(sub) * c_pad + c] = a;
+        ae_s[size_t(sub) * c_pad + c] = fmaf(qn, sqrtf(mn), 1e-30f);
+      }
     }
   }
   __syncthreads();
-  if (wid >= G) return;
+  if (wid >= G || mode == 1) return;
   const uint32_t h = unit * G + wid;
   select_head(h, desc, p2, row_base, q, cents, av_s + size_t(wid) * c_pad,
               ae_s + size_t(wid) * c_pad, n_clusters, sizes, starts, sorted_ids, token_ids,
@@ -654,7 +679,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         attr_f = dev_f;
       }
 #define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
-    token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes
+    token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode
+      static const uint32_t sel_mode = getenv("CKV_SEL_MODE") ? uint32_t(atoi(getenv("CKV_SEL_MODE"))) : 0u;
       switch (G) {
         case 1: k_select_fused<1><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
         case 2: k_select_fused<2><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
