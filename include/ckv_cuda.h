@@ -141,6 +141,81 @@ int ckv_cluster_decode_batch(ckv_ctx* ctx, const ckv_decode_cluster_desc* desc,
                              uint32_t* iterations_host /* [n_units] or NULL */);
 
 /* ------------------------------------------------------------------ */
+/* sequence-sharded k-means                     */
+/* ------------------------------------------------------------------ */
+/* kmeans_cosine (clustering.hpp:160-263) of one very long head whose N keys
+ * are split into contiguous position shards, one per rank.  Each rank holds
+ * its shard's keys; the caller runs the reference's loop and supplies the
+ * collectives between these per-shard steps (paper_2412_03213_b200/
+ * sharded.py: NCCL over NVLink in production, gloo in the CPU tests):
+ *
+ *   validate            -> allreduce MAX stat[:,1:3]
+ *   init(rows, row_lo)  -> allreduce SUM sums; update(from_init = 1)
+ *   pass 0:  assign(0) -> allreduce SUM counts; repair; finish(0)
+ *   pass t:  partial_sums -> allreduce SUM sums; update(0);
+ *            assign(t) -> allreduce SUM counts; repair;
+ *            finish(t) -> allreduce MAX stat[:,0] (changed), SUM objective
+ *   repair (clustering.hpp:128-153), per unit with an empty cluster, per
+ *            empty id ascending: largest = first argmax of the global
+ *            counts; farthest(unit, largest) on every rank -> all-gather
+ *            (distance, global row) -> max distance, lowest row wins ->
+ *            move() on the owner; counts updated identically everywhere.
+ *
+ * f64 sums of bf16 keys are exact in any order, so the
+ * all-reduced sums, hence the centroids, labels and iteration counts, are
+ * bit-identical to the single-process reference for any shard count.  All
+ * units of one call advance in lock step; set_active freezes the
+ * converged ones. */
+typedef struct ckv_kmshard ckv_kmshard;
+typedef struct {
+  uint32_t n_units;     /* heads clustered together                        */
+  uint32_t n_local;     /* keys of this shard per unit (>= 1)              */
+  uint32_t C;           /* clusters per unit (1 <= C <= global N)          */
+  uint32_t flags;       /* CKV_KM_EXACT_ONLY                               */
+  uint64_t key_stride;  /* elements between consecutive units' keys        */
+} ckv_kmshard_desc;
+
+/* Collective buffers, device memory owned by the caller (the collectives
+ * run on them in place). */
+typedef struct {
+  double* sums;       /* [n_units][C][128] partial member sums  (SUM)      */
+  int32_t* counts;    /* [n_units][C] member counts              (SUM)      */
+  int32_t* stat;      /* [n_units][4]: changed, non-finite, non-zero row, 0 (MAX) */
+  double* objective;  /* [n_units] objective partial             (SUM)      */
+} ckv_kmshard_bufs;
+
+int ckv_kmshard_create(ckv_ctx* ctx, const ckv_kmshard_desc* desc, const uint16_t* keys,
+                       const ckv_kmshard_bufs* bufs, ckv_kmshard** out);
+int ckv_kmshard_destroy(ckv_kmshard* sh);
+/* kmeans_cosine's input checks (clustering.hpp:166-172), this shard's part */
+int ckv_kmshard_validate(ckv_kmshard* sh);
+/* sums[u][c] = key row init_rows_host[u*C + c] (global row ids) if this
+ * shard [row_lo, row_lo + n_local) owns it, else 0 (clustering.hpp:195-198) */
+int ckv_kmshard_init(ckv_kmshard* sh, const uint32_t* init_rows_host, uint64_t row_lo);
+int ckv_kmshard_set_active(ckv_kmshard* sh, const int32_t* active_host);
+/* centroids = float(sums / counts) (/ 1 when from_init), then the next
+ * assignment's directions (clustering.hpp:205-218, 79-83) */
+int ckv_kmshard_update(ckv_kmshard* sh, int from_init);
+/* assignment pass `pass` of the local keys; local member counts -> counts */
+int ckv_kmshard_assign(ckv_kmshard* sh, uint32_t pass);
+/* after the counts all-reduce: any_empty_host[u] = some cluster has 0 members */
+int ckv_kmshard_empty(ckv_kmshard* sh, int32_t* any_empty_host);
+/* the local member of `cluster` farthest from its centroid (first maximum);
+ * *row_host = -1 when no local member beats distance -1 */
+int ckv_kmshard_farthest(ckv_kmshard* sh, uint32_t unit, uint32_t cluster, double* dist_host,
+                         int64_t* row_host);
+int ckv_kmshard_move(ckv_kmshard* sh, uint32_t unit, uint32_t local_row, uint32_t cluster);
+/* local index of the (repaired) labels, changed-vs-previous -> stat[u][0]
+ * (pass > 0), objective partial (want_objective) */
+int ckv_kmshard_finish(ckv_kmshard* sh, uint32_t pass, int want_objective);
+/* f64 member sums of the current labels -> sums */
+int ckv_kmshard_partial_sums(ckv_kmshard* sh);
+/* final model: centroids [n_units][C][128] (replicated), this shard's
+ * labels [n_units][n_local] from pass iters_host[u]; device pointers */
+int ckv_kmshard_result(ckv_kmshard* sh, const uint32_t* iters_host, float* centroids,
+                       int32_t* labels);
+
+/* ------------------------------------------------------------------ */
 /* index (selection.hpp:16-48)                                         */
 /* ------------------------------------------------------------------ */
 /* Stable counting sort of labels[unit][0:n_pos] into the ClusterIndex

@@ -217,6 +217,14 @@ static void assign_all(const float* keys, uint32_t n, uint32_t d, int metric,
   scorer_free(&s);
 }
 
+/* AssignScorer::assign over a key block (clustering.hpp:70-115): the CPU
+ * side of the sequence-sharded k-means tests, where each rank assigns only
+ * its own shard's keys against the replicated centroids. */
+void orc_assign(const float* keys, uint32_t n, uint32_t d, int metric, const float* cents,
+                uint32_t C, int32_t* out) {
+  assign_all(keys, n, d, metric, cents, C, out);
+}
+
 static void count_members(const int32_t* labels, uint32_t n, uint32_t C, uint32_t* counts) {
   memset(counts, 0, sizeof(uint32_t) * C);
   for (uint32_t i = 0; i < n; ++i) counts[(uint32_t)labels[i]]++;

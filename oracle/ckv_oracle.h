@@ -65,6 +65,10 @@ int orc_kmeans(const float* keys, uint32_t n, uint32_t d, uint32_t C,
                double* obj_hist, uint32_t* repair_iters,
                orc_kmeans_info* info);
 
+/* AssignScorer::assign of n keys against C raw centroids (clustering.hpp:70-115) */
+void orc_assign(const float* keys, uint32_t n, uint32_t d, int metric, const float* cents,
+                uint32_t C, int32_t* out);
+
 /* init rows exactly as kmeans_cosine samples them (clustering.hpp:186-193) */
 void orc_kmeans_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows_out);
 

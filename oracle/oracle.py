@@ -146,6 +146,10 @@ class Oracle:
                                      C.c_uint32, C.c_int, C.c_void_p, C.c_uint32, f32p, i32p,
                                      f64p, u32p, C.POINTER(_OrcInfo)]
             L.orc_kmeans_init_rows.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, u32p]
+            L.orc_assign.argtypes = [f32p, C.c_uint32, C.c_uint32, C.c_int, f32p, C.c_uint32,
+                                     i32p]
+            L.orc_cosine_distance.restype = C.c_double
+            L.orc_cosine_distance.argtypes = [f32p, f32p, C.c_uint32]
             L.orc_prefill_cluster_count.restype = C.c_uint32
             L.orc_prefill_cluster_count.argtypes = [C.c_uint32, C.POINTER(_OrcCfg)]
             L.orc_cluster_prefill.argtypes = [f32p, C.c_uint32, C.c_uint32, C.POINTER(_OrcCfg),
@@ -285,6 +289,22 @@ class Oracle:
             raise OracleError(self._err())
         return KMeansResult(cents[:C_], labels, bool(info[2]), int(info[1]), obj[: info[3]],
                             reps[: info[4]], 0, C_)
+
+    def assign(self, keys: np.ndarray, centroids: np.ndarray) -> np.ndarray:
+        """AssignScorer::assign (cosine) of every key row (clustering.hpp:70-115)."""
+        assert self.kind == "port"
+        keys = np.ascontiguousarray(keys, np.float32)
+        cents = np.ascontiguousarray(centroids, np.float32)
+        out = np.zeros(len(keys), np.int32)
+        self.lib.orc_assign(keys, len(keys), keys.shape[1], 0, cents, len(cents), out)
+        return out
+
+    def cosine_distance(self, a: np.ndarray, b: np.ndarray) -> float:
+        """cosine_distance (clustering.hpp:59-65)."""
+        assert self.kind == "port"
+        a = np.ascontiguousarray(a, np.float32)
+        return float(self.lib.orc_cosine_distance(a, np.ascontiguousarray(b, np.float32),
+                                                  len(a)))
 
     def kmeans_init_rows(self, n: int, C_: int, seed: int) -> np.ndarray:
         assert self.kind == "port"

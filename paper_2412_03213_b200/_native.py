@@ -63,6 +63,15 @@ class SessionDesc(C.Structure):
                 ("cluster_seed", u64), ("kv_heads", u32), ("flags", u32)]
 
 
+class KmShardDesc(C.Structure):
+    _fields_ = [("n_units", u32), ("n_local", u32), ("C", u32), ("flags", u32),
+                ("key_stride", u64)]
+
+
+class KmShardBufs(C.Structure):
+    _fields_ = [("sums", vp), ("counts", vp), ("stat", vp), ("objective", vp)]
+
+
 class SessionStats(C.Structure):
     _fields_ = [("n_ctx", u32), ("labeled_end", u32), ("steps", u32), ("max_clusters", u32),
                 ("launches", u64)]
@@ -89,6 +98,21 @@ SIGNATURES = {
     "ckv_cluster_prefill": (C.c_int, [vp, C.POINTER(PrefillDesc), vp, vp, vp, vp, vp, vp, vp, vp]),
     "ckv_cluster_decode_batch": (C.c_int, [vp, C.POINTER(DecodeClusterDesc), vp, vp, vp, vp, vp,
                                            vp]),
+    "ckv_kmshard_create": (C.c_int, [vp, C.POINTER(KmShardDesc), vp, C.POINTER(KmShardBufs),
+                                     C.POINTER(vp)]),
+    "ckv_kmshard_destroy": (C.c_int, [vp]),
+    "ckv_kmshard_validate": (C.c_int, [vp]),
+    "ckv_kmshard_init": (C.c_int, [vp, vp, u64]),
+    "ckv_kmshard_set_active": (C.c_int, [vp, vp]),
+    "ckv_kmshard_update": (C.c_int, [vp, C.c_int]),
+    "ckv_kmshard_assign": (C.c_int, [vp, u32]),
+    "ckv_kmshard_empty": (C.c_int, [vp, vp]),
+    "ckv_kmshard_farthest": (C.c_int, [vp, u32, u32, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_int64)]),
+    "ckv_kmshard_move": (C.c_int, [vp, u32, u32, u32]),
+    "ckv_kmshard_finish": (C.c_int, [vp, u32, C.c_int]),
+    "ckv_kmshard_partial_sums": (C.c_int, [vp]),
+    "ckv_kmshard_result": (C.c_int, [vp, vp, vp, vp]),
     "ckv_build_index": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp]),
     "ckv_select": (C.c_int, [vp, C.POINTER(SelectDesc), vp, vp, vp, vp, vp, vp, vp, vp,
                              C.POINTER(Runs), vp, vp, vp, vp, vp, vp]),

@@ -41,6 +41,23 @@ struct KMeansArgs {
 int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
                double* objective_host, uint32_t* repair_host);
 
+// single kernels of the k-means pass, for the sequence-sharded driver
+// (ckv_kmshard.cu); defined in ckv_kmeans.cu / ckv_assign_tc.cu
+int launch_scan_keys(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
+                     uint32_t n_units, int32_t* flags, float* knorm);
+int launch_assign(cudaStream_t st, bool use_tc, const uint16_t* keys, uint64_t key_stride,
+                  uint32_t n, uint32_t C, uint32_t c_pad, uint32_t n_units,
+                  const uint16_t* dirs_bf, const float* deps, const float* dirs, int32_t* labels,
+                  uint32_t label_stride, const int32_t* active, void* tc_scratch,
+                  size_t tc_bytes, uint64_t* launches);
+int launch_objective(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
+                     uint32_t n_units, uint32_t c_stride, uint32_t c_pad, const int32_t* labels,
+                     uint32_t label_stride, const float* cents, const double* cnorm, double* obj,
+                     const int32_t* active);
+size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C);
+float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n);
+bool assign_tc_supported(uint32_t n, uint32_t C);
+
 }  // namespace ckvb
 
 namespace ckvb {

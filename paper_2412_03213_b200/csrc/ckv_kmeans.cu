@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "ckv_internal.cuh"
+#include "ckv_kmeans_dev.cuh"
 
 namespace ckvb {
 
@@ -226,53 +227,14 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
       }
     }
   }
-  const double dc = double(cnt);
-  float x0 = float(a0 / dc), x1 = float(a1 / dc), x2 = float(a2 / dc), x3 = float(a3 / dc);
-  float* ct = cents + (size_t(u) * c_stride + c) * D;
-  reinterpret_cast<float4*>(ct)[lane] = make_float4(x0, x1, x2, x3);
-  // sequential norm chain over j = 0..127: lane L holds j = 4L..4L+3
-  double s = 0.0;
-  for (int L = 0; L < 32; ++L) {
-    double y0 = __shfl_sync(0xffffffffu, double(x0), L);
-    double y1 = __shfl_sync(0xffffffffu, double(x1), L);
-    double y2 = __shfl_sync(0xffffffffu, double(x2), L);
-    double y3 = __shfl_sync(0xffffffffu, double(x3), L);
-    s = __fma_rn(y0, y0, s);
-    s = __fma_rn(y1, y1, s);
-    s = __fma_rn(y2, y2, s);
-    s = __fma_rn(y3, y3, s);
-  }
-  const double nrm = sqrt(s);
-  if (lane == 0) cnorm[size_t(u) * c_pad + c] = nrm;
-  float d0 = nrm > 0.0 ? float(double(x0) / nrm) : x0;
-  float d1 = nrm > 0.0 ? float(double(x1) / nrm) : x1;
-  float d2 = nrm > 0.0 ? float(double(x2) / nrm) : x2;
-  float d3 = nrm > 0.0 ? float(double(x3) / nrm) : x3;
-  reinterpret_cast<float4*>(dr)[lane] = make_float4(d0, d1, d2, d3);
-  uint2 pk;
-  pk.x = uint32_t(f32_to_bf16_rn(d0)) | (uint32_t(f32_to_bf16_rn(d1)) << 16);
-  pk.y = uint32_t(f32_to_bf16_rn(d2)) | (uint32_t(f32_to_bf16_rn(d3)) << 16);
-  reinterpret_cast<uint2*>(db)[lane] = pk;
-  // |dir - bf16(dir)|: the per-centroid error the tensor-core band uses
-  const double e0 = double(d0) - double(__uint_as_float(pk.x << 16));
-  const double e1 = double(d1) - double(__uint_as_float(pk.x & 0xffff0000u));
-  const double e2 = double(d2) - double(__uint_as_float(pk.y << 16));
-  const double e3 = double(d3) - double(__uint_as_float(pk.y & 0xffff0000u));
-  const double ee = warp_sum(e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
-  if (lane == 0) deps[size_t(u) * c_pad + c] = float(sqrt(ee)) * 1.0001f;
+  finish_centroid(a0, a1, a2, a3, double(cnt), cents + (size_t(u) * c_stride + c) * D, dr, db,
+                  cnorm + size_t(u) * c_pad + c, deps + size_t(u) * c_pad + c);
 }
 
 // ---------------------------------------------------------------------------
 // empty-cluster repair (clustering.hpp:128-153) — one CTA per unit that has
 // an empty cluster; sequential over empty ids as the reference is.
 // ---------------------------------------------------------------------------
-__device__ double cosine_distance_dev(const uint16_t* k, const float* c, double nb) {
-  double na = sqrt(dot_seq_bb(k, k));
-  if (na < 1e-12 || nb < 1e-12) return 1.0;
-  double dd = 1.0 - dot_seq_bf(k, c) / (na * nb);
-  return dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
-}
-
 __global__ void __launch_bounds__(256)
 k_repair(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n, uint32_t C,
          uint32_t c_stride, uint32_t c_pad, int32_t* __restrict__ labels, uint32_t label_stride,
@@ -676,6 +638,55 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
       info_host[u].n_objective = want_obj ? it + 1 : 0;
     }
   }
+  return CKV_OK;
+}
+
+}  // namespace ckvb
+
+// ---------------------------------------------------------------------------
+// launch wrappers for the sequence-sharded driver (ckv_kmshard.cu): the same
+// kernels on one shard's keys
+// ---------------------------------------------------------------------------
+namespace ckvb {
+
+int launch_scan_keys(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
+                     uint32_t n_units, int32_t* flags, float* knorm) {
+  if (n == 0 || n_units == 0) return CKV_OK;
+  k_scan_keys<<<dim3((n + 127) / 128, n_units), 256, 0, st>>>(keys, key_stride, n, flags, knorm);
+  CKV_LAUNCH_CHECK("k_scan_keys");
+  if (flags) {
+    k_validate_rows<<<dim3((n + 255) / 256, n_units), 256, 0, st>>>(keys, key_stride, n, flags);
+    CKV_LAUNCH_CHECK("k_validate_rows");
+  }
+  return CKV_OK;
+}
+
+int launch_assign(cudaStream_t st, bool use_tc, const uint16_t* keys, uint64_t key_stride,
+                  uint32_t n, uint32_t C, uint32_t c_pad, uint32_t n_units,
+                  const uint16_t* dirs_bf, const float* deps, const float* dirs, int32_t* labels,
+                  uint32_t label_stride, const int32_t* active, void* tc_scratch,
+                  size_t tc_bytes, uint64_t* launches) {
+  if (n == 0 || n_units == 0) return CKV_OK;
+  if (use_tc)
+    return assign_tc(st, keys, key_stride, n, C, c_pad, n_units, dirs_bf, deps, dirs, labels,
+                     label_stride, active, tc_scratch, tc_bytes, launches);
+  k_assign_exact<<<dim3((n + 127) / 128, n_units), 128, 0, st>>>(keys, key_stride, n, C, c_pad,
+                                                                 dirs, labels, label_stride,
+                                                                 active);
+  CKV_LAUNCH_CHECK("k_assign_exact");
+  ++*launches;
+  return CKV_OK;
+}
+
+int launch_objective(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
+                     uint32_t n_units, uint32_t c_stride, uint32_t c_pad, const int32_t* labels,
+                     uint32_t label_stride, const float* cents, const double* cnorm, double* obj,
+                     const int32_t* active) {
+  if (n == 0 || n_units == 0) return CKV_OK;
+  k_objective<<<dim3((n + 255) / 256, n_units), 256, 0, st>>>(keys, key_stride, n, c_stride,
+                                                               c_pad, labels, label_stride, cents,
+                                                               cnorm, obj, active);
+  CKV_LAUNCH_CHECK("k_objective");
   return CKV_OK;
 }
 

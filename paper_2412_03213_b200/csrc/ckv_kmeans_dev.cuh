@@ -1,0 +1,67 @@
+// ckv_kmeans_dev.cuh — device pieces of the cosine k-means shared by the
+// single-GPU driver (ckv_kmeans.cu) and the sequence-sharded one
+// (ckv_kmshard.cu), so both produce the same bits.
+#pragma once
+#include "ckv_common.cuh"
+
+namespace ckvb {
+
+// cosine_distance (clustering.hpp:59-65) of a bf16 key and an f32 centroid
+// whose f64 norm nb is precomputed.
+__device__ __forceinline__ double cosine_distance_dev(const uint16_t* k, const float* c,
+                                                      double nb) {
+  double na = sqrt(dot_seq_bb(k, k));
+  if (na < 1e-12 || nb < 1e-12) return 1.0;
+  double dd = 1.0 - dot_seq_bf(k, c) / (na * nb);
+  return dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
+}
+
+// The end of update_centroids for one (unit, cluster) by one warp, lane L
+// holding dims 4L..4L+3 of the f64 member sum: centroid = float(sum / count)
+// (clustering.hpp:214-217), then the next pass's AssignScorer direction
+// normalize(centroid) (common.hpp:141-147; sequential f64 norm chain), its
+// bf16 copy (the tensor-core B operand), the f64 norm (cosine_distance) and
+// |dir - bf16(dir)| (the tensor-core error band).
+__device__ __forceinline__ void finish_centroid(double a0, double a1, double a2, double a3,
+                                                double count, float* __restrict__ ct,
+                                                float* __restrict__ dr,
+                                                uint16_t* __restrict__ db,
+                                                double* __restrict__ cnorm_out,
+                                                float* __restrict__ deps_out) {
+  const int lane = lane_id();
+  float x0 = float(a0 / count), x1 = float(a1 / count), x2 = float(a2 / count),
+        x3 = float(a3 / count);
+  reinterpret_cast<float4*>(ct)[lane] = make_float4(x0, x1, x2, x3);
+  // sequential norm chain over j = 0..127: lane L holds j = 4L..4L+3
+  double s = 0.0;
+  for (int L = 0; L < 32; ++L) {
+    double y0 = __shfl_sync(0xffffffffu, double(x0), L);
+    double y1 = __shfl_sync(0xffffffffu, double(x1), L);
+    double y2 = __shfl_sync(0xffffffffu, double(x2), L);
+    double y3 = __shfl_sync(0xffffffffu, double(x3), L);
+    s = __fma_rn(y0, y0, s);
+    s = __fma_rn(y1, y1, s);
+    s = __fma_rn(y2, y2, s);
+    s = __fma_rn(y3, y3, s);
+  }
+  const double nrm = sqrt(s);
+  if (lane == 0) *cnorm_out = nrm;
+  float d0 = nrm > 0.0 ? float(double(x0) / nrm) : x0;
+  float d1 = nrm > 0.0 ? float(double(x1) / nrm) : x1;
+  float d2 = nrm > 0.0 ? float(double(x2) / nrm) : x2;
+  float d3 = nrm > 0.0 ? float(double(x3) / nrm) : x3;
+  reinterpret_cast<float4*>(dr)[lane] = make_float4(d0, d1, d2, d3);
+  uint2 pk;
+  pk.x = uint32_t(f32_to_bf16_rn(d0)) | (uint32_t(f32_to_bf16_rn(d1)) << 16);
+  pk.y = uint32_t(f32_to_bf16_rn(d2)) | (uint32_t(f32_to_bf16_rn(d3)) << 16);
+  reinterpret_cast<uint2*>(db)[lane] = pk;
+  // |dir - bf16(dir)|: the per-centroid error the tensor-core band uses
+  const double e0 = double(d0) - double(__uint_as_float(pk.x << 16));
+  const double e1 = double(d1) - double(__uint_as_float(pk.x & 0xffff0000u));
+  const double e2 = double(d2) - double(__uint_as_float(pk.y << 16));
+  const double e3 = double(d3) - double(__uint_as_float(pk.y & 0xffff0000u));
+  const double ee = warp_sum(e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
+  if (lane == 0) *deps_out = float(sqrt(ee)) * 1.0001f;
+}
+
+}  // namespace ckvb

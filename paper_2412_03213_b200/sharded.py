@@ -1,0 +1,324 @@
+"""Sequence-sharded ClusterKV path (BASELINE config E).
+
+One very long head (70B shape, 128k context) is split into contiguous
+position shards, one per rank (one process per GPU, torch.distributed over
+NCCL/NVLink for the collectives).  This module is the host side of the
+protocol declared in include/ckv_cuda.h ("sequence-sharded k-means"): it runs
+the reference's kmeans_cosine loop (clustering.hpp:160-263) with the per-shard
+device steps of ckv_kmshard.cu and one collective between them:
+
+  per iteration: all-reduce SUM of the f64 centroid partial sums [C x 128]
+                 and of the counts [C]; all-reduce MAX of a "changed" flag;
+                 an all-gather of (distance, row) per empty-cluster repair.
+
+f64 sums of bf16 keys are exact in any order, so every rank
+ends with centroids, labels and iteration counts bit-identical to the
+single-process reference, for any number of shards.
+
+The local steps sit behind a small interface (`ShardSteps`): `DeviceShard`
+binds the CUDA kernels through the C-ABI (the product path); the CPU tests
+bind a checker built from the oracle (tests/_shard_cpu.py) to exercise this
+protocol with gloo at world_size 2.  There is no CPU fallback here: nothing
+in this module computes a k-means step itself.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Protocol
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from ._native import ValidationError, check, lib
+
+D = 128
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous position shard [lo, hi) of rank `rank`."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+# --------------------------------------------------------------------------
+# collectives
+# --------------------------------------------------------------------------
+class Comm:
+    """The collectives of the sharded path over torch.distributed.
+
+    NCCL reduces device buffers in place over NVLink/NVSwitch.  gloo (the CPU
+    tests, or several ranks sharing one GPU) only takes host tensors, so
+    device buffers are staged through the host.  world_size 1 (no process
+    group) makes every collective the identity.
+    """
+
+    def __init__(self, group=None):
+        self.group = group
+        self.on = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if self.on else 1
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.stage = self.on and dist.get_backend(group) == "gloo"
+
+    def all_reduce(self, t: torch.Tensor, op: str = "sum") -> None:
+        if self.world == 1:
+            return
+        rop = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX}[op]
+        x = t.cpu() if (self.stage and t.is_cuda) else t
+        dist.all_reduce(x, op=rop, group=self.group)
+        if x is not t:
+            t.copy_(x)
+
+    def all_gather(self, t: torch.Tensor) -> list[torch.Tensor]:
+        if self.world == 1:
+            return [t]
+        x = t.cpu() if (self.stage and t.is_cuda) else t
+        out = [torch.empty_like(x) for _ in range(self.world)]
+        dist.all_gather(out, x.contiguous(), group=self.group)
+        return out
+
+
+# --------------------------------------------------------------------------
+# per-shard steps
+# --------------------------------------------------------------------------
+class ShardSteps(Protocol):
+    """One rank's device steps (ckv_kmshard_* in include/ckv_cuda.h)."""
+
+    n_units: int
+    n_local: int
+    C: int
+    sums: torch.Tensor       # [U][C][128] f64
+    counts: torch.Tensor     # [U][C] int32
+    stat: torch.Tensor       # [U][4] int32: changed, non-finite, non-zero row, 0
+    objective: torch.Tensor  # [U] f64
+
+    def validate(self) -> None: ...
+    def init(self, rows: np.ndarray, row_lo: int) -> None: ...
+    def set_active(self, active: np.ndarray) -> None: ...
+    def update(self, from_init: bool) -> None: ...
+    def assign(self, pass_: int) -> None: ...
+    def empty(self) -> np.ndarray: ...
+    def farthest(self, unit: int, cluster: int) -> tuple[float, int]: ...
+    def move(self, unit: int, local_row: int, cluster: int) -> None: ...
+    def finish(self, pass_: int, want_objective: bool) -> None: ...
+    def partial_sums(self) -> None: ...
+    def result(self, iters: np.ndarray) -> tuple[torch.Tensor, torch.Tensor]: ...
+
+
+class DeviceShard:
+    """ShardSteps on the B200 kernels (ckv_kmshard.cu) through the C-ABI.
+
+    keys: device int16/bf16-bits tensor [n_units, n_local, 128] (this rank's
+    contiguous position shard of every unit).
+    """
+
+    def __init__(self, keys: torch.Tensor, C_: int, ctx=None, exact_only: bool = False):
+        from .api import Context
+        if not keys.is_cuda:
+            raise ValueError("DeviceShard: keys must be a CUDA tensor (no CPU fallback)")
+        self.ctx = ctx or Context.default()
+        self.keys = keys.contiguous()
+        U, n, d = self.keys.shape
+        if d != D:
+            raise ValidationError(N.CKV_EINVAL, "head dim must be 128")
+        self.n_units, self.n_local, self.C = U, n, C_
+        dev = keys.device
+        self.sums = torch.zeros((U, C_, D), dtype=torch.float64, device=dev)
+        self.counts = torch.zeros((U, C_), dtype=torch.int32, device=dev)
+        self.stat = torch.zeros((U, 4), dtype=torch.int32, device=dev)
+        self.objective = torch.zeros((U,), dtype=torch.float64, device=dev)
+        desc = N.KmShardDesc(U, n, C_, N.CKV_KM_EXACT_ONLY if exact_only else 0, n * D)
+        bufs = N.KmShardBufs(self.sums.data_ptr(), self.counts.data_ptr(),
+                             self.stat.data_ptr(), self.objective.data_ptr())
+        h = C.c_void_p()
+        check(lib().ckv_kmshard_create(self.ctx.h, C.byref(desc), self.keys.data_ptr(),
+                                       C.byref(bufs), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().ckv_kmshard_destroy(self.h)
+        except Exception:
+            pass
+
+    def validate(self):
+        check(lib().ckv_kmshard_validate(self.h))
+
+    def init(self, rows, row_lo):
+        r = np.ascontiguousarray(rows, np.uint32)
+        check(lib().ckv_kmshard_init(self.h, r.ctypes.data_as(C.c_void_p), row_lo))
+
+    def set_active(self, active):
+        a = np.ascontiguousarray(active, np.int32)
+        check(lib().ckv_kmshard_set_active(self.h, a.ctypes.data_as(C.c_void_p)))
+
+    def update(self, from_init):
+        check(lib().ckv_kmshard_update(self.h, int(from_init)))
+
+    def assign(self, pass_):
+        check(lib().ckv_kmshard_assign(self.h, pass_))
+
+    def empty(self):
+        out = np.zeros(self.n_units, np.int32)
+        check(lib().ckv_kmshard_empty(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def farthest(self, unit, cluster):
+        d, r = C.c_double(), C.c_int64()
+        check(lib().ckv_kmshard_farthest(self.h, unit, cluster, C.byref(d), C.byref(r)))
+        return d.value, r.value
+
+    def move(self, unit, local_row, cluster):
+        check(lib().ckv_kmshard_move(self.h, unit, local_row, cluster))
+
+    def finish(self, pass_, want_objective):
+        check(lib().ckv_kmshard_finish(self.h, pass_, int(want_objective)))
+
+    def partial_sums(self):
+        check(lib().ckv_kmshard_partial_sums(self.h))
+
+    def result(self, iters):
+        it = np.ascontiguousarray(iters, np.uint32)
+        cents = torch.empty((self.n_units, self.C, D), dtype=torch.float32,
+                            device=self.keys.device)
+        labels = torch.empty((self.n_units, self.n_local), dtype=torch.int32,
+                             device=self.keys.device)
+        check(lib().ckv_kmshard_result(self.h, it.ctypes.data_as(C.c_void_p), cents.data_ptr(),
+                                       labels.data_ptr()))
+        self.ctx.sync()
+        return cents, labels
+
+
+# --------------------------------------------------------------------------
+# the protocol (kmeans_cosine, clustering.hpp:160-263, sharded)
+# --------------------------------------------------------------------------
+@dataclass
+class ShardedKMeansResult:
+    """ClusterModel fields of every unit; labels cover this rank's shard."""
+
+    n_clusters: int
+    centroids: torch.Tensor         # [U][C][128] f32, identical on every rank
+    labels: torch.Tensor            # [U][n_local] int32, this shard's positions
+    row_lo: int                     # global row of labels[:, 0]
+    iterations_used: np.ndarray     # [U]
+    converged: np.ndarray           # [U] bool
+    repair_iterations: list = field(default_factory=list)   # per unit
+    objective_history: list = field(default_factory=list)   # per unit
+
+
+def _init_rows(n_total: int, C_: int, seeds) -> np.ndarray:
+    rows = np.zeros((len(seeds), C_), np.uint32)
+    for u, s in enumerate(seeds):
+        check(lib().ckv_kmeans_init_rows(n_total, C_, int(s),
+                                         rows[u].ctypes.data_as(C.c_void_p)))
+    return rows
+
+
+def _repair(shard: ShardSteps, comm: Comm, row_lo: int, n_local: int,
+            active: np.ndarray) -> np.ndarray:
+    """repair_empty_clusters (clustering.hpp:128-153) over the global counts.
+
+    Every rank holds the same all-reduced counts, so every rank takes the
+    same decisions; the victim (the member of the largest cluster farthest
+    from its centroid, first in position order on ties) is found by one
+    all-gather of each shard's local candidate per repair."""
+    U, C_ = shard.n_units, shard.C
+    n_rep = np.zeros(U, np.int64)
+    empty = shard.empty()
+    for u in np.nonzero((empty != 0) & (active != 0))[0]:
+        counts = shard.counts[u].cpu().numpy().astype(np.int64)
+        for c in range(C_):
+            if counts[c] > 0:
+                continue
+            largest = int(np.argmax(counts))  # first maximum
+            if counts[largest] <= 1:
+                continue
+            d, r = shard.farthest(int(u), largest)
+            mine = torch.tensor([d, float(row_lo + r) if r >= 0 else -1.0], dtype=torch.float64)
+            best_d, victim = -1.0, -1
+            for t in comm.all_gather(mine):
+                dd, gg = float(t[0]), int(t[1])
+                if gg >= 0 and (dd > best_d or (dd == best_d and gg < victim)):
+                    best_d, victim = dd, gg
+            if victim < 0:
+                victim = 0  # no member beat distance -1: the reference keeps victim = 0
+            if row_lo <= victim < row_lo + n_local:
+                shard.move(int(u), victim - row_lo, c)
+            counts[largest] -= 1
+            counts[c] += 1
+            n_rep[u] += 1
+        shard.counts[u].copy_(torch.from_numpy(counts.astype(np.int32)))
+    return n_rep
+
+
+def kmeans_cosine_sharded(shard: ShardSteps, n_total: int, row_lo: int, seeds=None,
+                          max_iters: int = 50, init_rows: np.ndarray | None = None,
+                          comm: Comm | None = None,
+                          want_objective: bool = False) -> ShardedKMeansResult:
+    """kmeans_cosine (clustering.hpp:160-263) of n_units heads whose n_total
+    keys are position-sharded over the ranks of `comm`; this rank holds rows
+    [row_lo, row_lo + shard.n_local).  seeds[u] (or init_rows[u]) as the
+    reference.  Raises ValidationError under the reference's predicates."""
+    comm = comm or Comm()
+    U, C_, n_local = shard.n_units, shard.C, shard.n_local
+    if not 1 <= C_ <= n_total:
+        raise ValidationError(N.CKV_EINVAL, "kmeans: need 1 <= C <= N")
+    if max_iters < 1:
+        raise ValidationError(N.CKV_EINVAL, "ClusterConfig: max_iters must be >= 1")
+    shard.validate()
+    comm.all_reduce(shard.stat, "max")
+    st = shard.stat.cpu().numpy()
+    if st[:, 1].any():
+        raise ValidationError(N.CKV_EINVAL, "kmeans: keys must be finite")
+    if not st[:, 2].all():
+        raise ValidationError(N.CKV_EINVAL, "kmeans: degenerate input, all keys zero-norm")
+    if init_rows is not None:
+        rows = np.asarray(init_rows, np.uint32).reshape(U, -1)
+        if rows.shape[1] != C_:
+            raise ValidationError(N.CKV_EINVAL, "kmeans: init_rows size must equal C")
+    else:
+        rows = _init_rows(n_total, C_, seeds)
+
+    shard.init(rows, row_lo)
+    comm.all_reduce(shard.sums)
+    shard.update(True)
+    active = np.ones(U, np.int32)
+    iters = np.zeros(U, np.uint32)
+    converged = np.zeros(U, bool)
+    rep_hist = [[] for _ in range(U)]
+    obj_hist = [[] for _ in range(U)]
+
+    def assign_pass(t: int) -> None:
+        shard.assign(t)
+        comm.all_reduce(shard.counts)
+        reps = _repair(shard, comm, row_lo, n_local, active)
+        shard.finish(t, want_objective)
+        if t > 0:
+            comm.all_reduce(shard.stat, "max")
+        if want_objective:
+            comm.all_reduce(shard.objective)
+        objs = shard.objective.cpu().numpy() if want_objective else None
+        for u in np.nonzero(active)[0]:
+            if reps[u] > 0:
+                rep_hist[u].append(t)
+            if want_objective:
+                obj_hist[u].append(float(objs[u]))
+
+    assign_pass(0)
+    for t in range(1, max_iters + 1):
+        shard.partial_sums()
+        comm.all_reduce(shard.sums)
+        shard.update(False)
+        assign_pass(t)
+        changed = shard.stat[:, 0].cpu().numpy()
+        for u in np.nonzero(active)[0]:
+            if not changed[u]:
+                converged[u], iters[u], active[u] = True, t, 0
+            elif t == max_iters:
+                iters[u], active[u] = t, 0
+        if not active.any():
+            break
+        shard.set_active(active)
+    cents, labels = shard.result(iters)
+    return ShardedKMeansResult(C_, cents, labels, row_lo, iters, converged, rep_hist, obj_hist)
