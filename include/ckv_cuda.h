@@ -313,6 +313,79 @@ int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* desc, const float* q, const 
                const uint16_t* V, const uint32_t* rows, const ckv_runs* runs,
                const uint32_t* n_tokens, float* out, float* weights);
 
+/* Cluster-major relayout of a position-ordered KV store:
+ * dst row r = src row r for r < sink or r >= labeled_end, and src row
+ * sorted_ids[u][r - sink] for sink <= r < labeled_end (sorted_ids from
+ * ckv_build_index over the store's labels).  K2/V2 must not alias K/V. */
+int ckv_relayout_kv(ckv_ctx* ctx, uint32_t n_units, uint32_t p_cap, const uint16_t* K,
+                    const uint16_t* V, uint16_t* K2, uint16_t* V2, const uint32_t* sorted_ids,
+                    uint32_t sink, uint32_t labeled_end, uint32_t n_rows);
+
+/* ------------------------------------------------------------------ */
+/* sequence-sharded decode step                 */
+/* ------------------------------------------------------------------ */
+/* Each rank holds a contiguous position shard of every unit's keys, stored
+ * cluster-major by its LOCAL index (rows [0, sink_rows) sinks on the rank
+ * that owns them, then the local clustered rows in local index order, then
+ * the recency rows on the rank that owns them), plus the replicated
+ * centroids and global cluster sizes.  One step:
+ *   ckv_score_range     this rank's centroid slice [c_lo, c_lo + slice) ->
+ *                       scores [n_q][slice] f64 (score_clusters,
+ *                       selection.hpp:51-57, bit-exact)
+ *   (all-gather)        -> scores [world][n_q][slice]
+ *   ckv_select_scored   the global ranking / budget / trim of select_tokens
+ *                       (selection.hpp:74-111) and this rank's share of I_T
+ *                       as runs of the local store
+ *   ckv_attend_partial  approx_attention over the local share, returning the
+ *                       locally normalised output and its log2-sum-exp2
+ *   (all-gather)        -> outs [world][n_q][128], lses [world][n_q]
+ *   ckv_attend_merge    the global softmax (attention.hpp:20-50) by an LSE
+ *                       merge; the local weights become global weights. */
+typedef struct {
+  uint32_t n_q, group, budget;
+  uint32_t C;          /* clusters per unit (<= 4096)                        */
+  uint32_t c_cap;      /* stride of sizes / prefix / ranked rows              */
+  uint32_t slice;      /* gathered scores: cluster c at rank c / slice,       */
+  uint32_t world;      /*   offset c % slice of [world][n_q][slice]           */
+  uint32_t n_local;    /* local clustered rows per unit (lsorted stride)      */
+  uint32_t sel_cap;    /* token-id slots per q head                           */
+  uint32_t row_base;   /* store row of local index entry 0                    */
+  uint32_t sink_rows;  /* sinks held here: rows [0, sink_rows) = positions 0..*/
+  uint32_t rec_row;    /* recency held here: rows [rec_row, rec_row + n_rec)  */
+  uint32_t rec_pos;    /*   = positions [rec_pos, rec_pos + n_rec)            */
+  uint32_t n_rec;
+  uint32_t pos_base;   /* global position of local clustered row 0            */
+  uint32_t flags;      /* CKV_SEL_FULL_RANK                                   */
+} ckv_shard_select_desc;
+
+/* q: f32 [n_units*group][128]; centroids f32 [n_units][c_cap][128];
+ * group in {1, 2, 4, 8}. */
+int ckv_score_range(ckv_ctx* ctx, uint32_t n_units, uint32_t group, const float* q,
+                    const float* centroids, uint32_t c_cap, uint32_t C, uint32_t c_lo,
+                    uint32_t slice, double* scores);
+/* scores [world][n_q][slice]; gsize = global sizes [unit][c_cap]; lsize,
+ * lstart [unit][c_cap(+1)], lsorted [unit][n_local] = the local index;
+ * prefix [unit][c_cap] = members of each cluster on lower-ranked shards.
+ * Outputs per q head: runs (run_cap >= C + 2), n_tokens = local I_T size,
+ * n_taken / trimmed (global, as SelectionResult), ranked [n_q][c_cap],
+ * token_ids [n_q][sel_cap] (optional, reference positions). */
+int ckv_select_scored(ckv_ctx* ctx, const ckv_shard_select_desc* desc, const double* scores,
+                      const uint32_t* gsize, const uint32_t* lsize, const uint32_t* lstart,
+                      const uint32_t* prefix, const uint32_t* lsorted, const ckv_runs* runs,
+                      uint32_t* token_ids, uint32_t* n_tokens, uint32_t* n_taken,
+                      uint32_t* trimmed, uint32_t* ranked);
+/* ckv_attend over runs, returning out = the locally normalised output and
+ * lse [n_q] = log2 sum 2^(logit * log2 e) of the local logits (-inf and
+ * out = 0 for a q head with no local tokens).  weights optional (local). */
+int ckv_attend_partial(ckv_ctx* ctx, const ckv_attend_desc* desc, const float* q,
+                       const uint16_t* K, const uint16_t* V, const ckv_runs* runs,
+                       const uint32_t* n_tokens, float* out, float* lse, float* weights);
+/* outs [world][n_q][128], lses [world][n_q] -> out [n_q][128]; weights
+ * (optional, this rank's [n_q][sel_cap] local weights) rescaled in place. */
+int ckv_attend_merge(ckv_ctx* ctx, uint32_t n_q, uint32_t world, uint32_t rank,
+                     const float* outs, const float* lses, float* out, float* weights,
+                     const uint32_t* n_tokens, uint32_t sel_cap);
+
 /* ------------------------------------------------------------------ */
 /* session: the batched serving path (simulate_head's ClusterKV branch, */
 /* harness.hpp:155-346, minus the metric oracles), device-resident.     */

@@ -72,6 +72,12 @@ class KmShardBufs(C.Structure):
     _fields_ = [("sums", vp), ("counts", vp), ("stat", vp), ("objective", vp)]
 
 
+class ShardSelectDesc(C.Structure):
+    _fields_ = [(n, u32) for n in ("n_q", "group", "budget", "C", "c_cap", "slice", "world",
+                                   "n_local", "sel_cap", "row_base", "sink_rows", "rec_row",
+                                   "rec_pos", "n_rec", "pos_base", "flags")]
+
+
 class SessionStats(C.Structure):
     _fields_ = [("n_ctx", u32), ("labeled_end", u32), ("steps", u32), ("max_clusters", u32),
                 ("launches", u64)]
@@ -113,6 +119,13 @@ SIGNATURES = {
     "ckv_kmshard_finish": (C.c_int, [vp, u32, C.c_int]),
     "ckv_kmshard_partial_sums": (C.c_int, [vp]),
     "ckv_kmshard_result": (C.c_int, [vp, vp, vp, vp]),
+    "ckv_relayout_kv": (C.c_int, [vp, u32, u32, vp, vp, vp, vp, vp, u32, u32, u32]),
+    "ckv_score_range": (C.c_int, [vp, u32, u32, vp, vp, u32, u32, u32, u32, vp]),
+    "ckv_select_scored": (C.c_int, [vp, C.POINTER(ShardSelectDesc), vp, vp, vp, vp, vp, vp,
+                                    C.POINTER(Runs), vp, vp, vp, vp, vp]),
+    "ckv_attend_partial": (C.c_int, [vp, C.POINTER(AttendDesc), vp, vp, vp, C.POINTER(Runs), vp,
+                                     vp, vp, vp]),
+    "ckv_attend_merge": (C.c_int, [vp, u32, u32, u32, vp, vp, vp, vp, vp, u32]),
     "ckv_build_index": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp]),
     "ckv_select": (C.c_int, [vp, C.POINTER(SelectDesc), vp, vp, vp, vp, vp, vp, vp, vp,
                              C.POINTER(Runs), vp, vp, vp, vp, vp, vp]),

@@ -137,7 +137,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
          const uint16_t* __restrict__ K, const uint16_t* __restrict__ V,
          const uint32_t* __restrict__ rows, ckv_runs runs, const uint32_t* __restrict__ n_tokens,
          float* __restrict__ out, float* __restrict__ logits_ws, float* __restrict__ part,
-         uint32_t* __restrict__ tickets, float* __restrict__ weights) {
+         uint32_t* __restrict__ tickets, float* __restrict__ weights, float* __restrict__ lse) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   AttSmem& sm = *reinterpret_cast<AttSmem*>(sm_raw);
   const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
@@ -352,8 +352,12 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
         L += __ldcg(pb + c * PART + 1) * w;
         o += __ldcg(pb + c * PART + 2 + t) * w;
       }
-      const float invL = 1.f / L;
-      out[size_t(it.h) * D + t] = o * invL;
+      // lse (the sequence-sharded path): this rank's log2-sum-exp2 of the
+      // scaled logits beside its locally normalised output; a q head with no
+      // local tokens contributes out = 0, lse = -inf to the merge
+      const float invL = L > 0.f ? 1.f / L : 0.f;
+      out[size_t(it.h) * D + t] = lse && !(L > 0.f) ? 0.f : o * (lse ? invL : 1.f / L);
+      if (lse && t == 0) lse[it.h] = L > 0.f ? MM + __log2f(L) : -INFINITY;
       if (WEIGHTS) {
         const uint32_t nt = n_tokens[it.h];
         const float* lg = logits_ws + size_t(it.h) * desc.sel_cap;
@@ -375,7 +379,7 @@ uint32_t attend_splits(const ckv_attend_desc& d) {
 int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
                   const uint16_t* K, const uint16_t* V, const uint32_t* rows,
                   const ckv_runs& runs, const uint32_t* n_tokens, float* out, float* weights,
-                  float* logits_ws, float* part, uint32_t* tickets) {
+                  float* logits_ws, float* part, uint32_t* tickets, float* lse) {
   if (!rows && !runs.row) { set_error("attend: need rows or runs"); return CKV_EINVAL; }
   if (desc.n_q == 0 || desc.max_tokens == 0) return CKV_OK;
   const uint32_t splits = attend_splits(desc);
@@ -399,10 +403,10 @@ int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
   const uint32_t grid = std::min<uint32_t>(n_items, uint32_t(std::max(1, per_sm)) * num_sms());
   if (weights)
     k_attend<true><<<grid, AT_THREADS, smem, st>>>(desc, splits, q, K, V, rows, runs, n_tokens,
-                                                   out, logits_ws, part, tickets, weights);
+                                                   out, logits_ws, part, tickets, weights, lse);
   else
     k_attend<false><<<grid, AT_THREADS, smem, st>>>(desc, splits, q, K, V, rows, runs, n_tokens,
-                                                    out, nullptr, part, tickets, nullptr);
+                                                    out, nullptr, part, tickets, nullptr, lse);
   CKV_LAUNCH_CHECK("k_attend");
   return CKV_OK;
 }

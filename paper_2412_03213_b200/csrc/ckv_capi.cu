@@ -499,6 +499,26 @@ int ckv_cache_invalidate(ckv_ctx* ctx, ckv_cache* c, uint32_t slot, const uint32
   return CKV_OK;
 }
 
+int ckv_relayout_kv(ckv_ctx* ctx, uint32_t n_units, uint32_t p_cap, const uint16_t* K,
+                    const uint16_t* V, uint16_t* K2, uint16_t* V2, const uint32_t* sorted_ids,
+                    uint32_t sink, uint32_t labeled_end, uint32_t n_rows) {
+  if (!ctx || !K || !V || !K2 || !V2 || !sorted_ids) {
+    set_error("ckv_relayout_kv: NULL argument");
+    return CKV_EINVAL;
+  }
+  if (sink > labeled_end || labeled_end > n_rows || n_rows > p_cap) {
+    set_error("ckv_relayout_kv: need sink <= labeled_end <= n_rows <= p_cap");
+    return CKV_EINVAL;
+  }
+  if (n_units == 0 || n_rows == 0) return CKV_OK;
+  dim3 g((n_rows + 7) / 8, n_units);
+  k_relayout<<<g, 128, 0, ctx->stream>>>(K, V, K2, V2, sorted_ids, p_cap, sink, labeled_end,
+                                         n_rows);
+  CKV_LAUNCH_CHECK("k_relayout");
+  ctx->launches++;
+  return CKV_OK;
+}
+
 int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q, const uint16_t* K,
                const uint16_t* V, const uint32_t* rows, const ckv_runs* runs,
                const uint32_t* n_tokens, float* out, float* weights) {

@@ -82,7 +82,7 @@ int launch_cache_invalidate(cudaStream_t st, const CacheDev& cache, uint32_t slo
 int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
                   const uint16_t* K, const uint16_t* V, const uint32_t* rows,
                   const ckv_runs& runs, const uint32_t* n_tokens, float* out, float* weights,
-                  float* logits_ws, float* part, uint32_t* tickets);
+                  float* logits_ws, float* part, uint32_t* tickets, float* lse = nullptr);
 size_t attend_part_floats(uint32_t n_q, uint32_t max_tokens);
 uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
 void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows);

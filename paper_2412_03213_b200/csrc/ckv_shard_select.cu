@@ -1,0 +1,352 @@
+// ckv_shard_select.cu — decode-step kernels of the sequence-sharded path
+// (SURVEY §8e, config E): centroid-sharded scoring, the global budgeted
+// top-k over the all-gathered scores, and the log-sum-exp merge of the
+// ranks' partial attention outputs.
+//
+//   k_score_range   exact f64 score_clusters (selection.hpp:51-57) of this
+//                   rank's centroid slice for all q heads: the sequential
+//                   dot_f64 chain, bit-identical to the reference (N2/N6).
+//                   Centroid rows and the unit's G queries are staged in
+//                   smem; one thread per (q head, cluster).
+//   (caller)        all-gather of the slices -> [world][n_q][slice] f64.
+//   k_select_scored one CTA per q head: block bitonic sort of all C scores by
+//                   (score desc, id asc) — select_tokens' comparator
+//                   (selection.hpp:83-87) — prefix of the GLOBAL sizes,
+//                   cut at the budget, and this rank's share of every taken
+//                   cluster: the reference takes a cluster's lowest positions
+//                   first and shards are contiguous in position, so shard s
+//                   keeps clamp(allow_c - prefix_s(c), 0, size_s(c)) of
+//                   cluster c, allow_c = its size, or B - cum for the trimmed
+//                   last one (selection.hpp:91-106).  Emits I_T as runs of
+//                   the local cluster-major store (ckv_attend's input).
+//   k_lse_merge     out = sum_s 2^(lse_s - M) o_s / sum_s 2^(lse_s - M) over
+//                   the ranks' (o_s, lse_s) from ckv_attend_partial; the
+//                   local weights are rescaled to global softmax weights.
+#include "ckv_internal.cuh"
+
+namespace ckvb {
+namespace {
+
+constexpr int SR_THREADS = 256;
+
+__device__ __forceinline__ unsigned long long rank_key_s(double s) {
+  return isnan(s) ? 0ull : dkey(s);  // NaN (empty-cluster centroids) ranks last
+}
+__device__ __forceinline__ bool before(unsigned long long ka, uint32_t ia, unsigned long long kb,
+                                       uint32_t ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+// blockIdx.x = unit, blockIdx.y = a tile of SR_ROWS centroid rows; thread
+// pairs (row, head) stride over the tile's SR_ROWS x G scores
+constexpr int SR_ROWS = 64;
+template <int G>
+__global__ void __launch_bounds__(SR_THREADS)
+k_score_range(const float* __restrict__ q, const float* __restrict__ cents, uint32_t c_cap,
+              uint32_t C, uint32_t c_lo, uint32_t c_hi, uint32_t slice,
+              double* __restrict__ scores) {
+  __shared__ float crow[SR_ROWS][D + 1];  // +1: lanes read one column of 32 rows
+  __shared__ float qs[G][D];
+  const uint32_t u = blockIdx.x;
+  const uint32_t t0 = c_lo + blockIdx.y * SR_ROWS;
+  const uint32_t hi = min(c_hi, C);
+  if (t0 >= hi) return;
+  const uint32_t nrow = min(uint32_t(SR_ROWS), hi - t0);
+  const float* cu = cents + (size_t(u) * c_cap + t0) * D;
+  for (uint32_t e = threadIdx.x; e < nrow * D; e += SR_THREADS) crow[e / D][e % D] = __ldg(cu + e);
+  for (uint32_t e = threadIdx.x; e < G * D; e += SR_THREADS)
+    qs[e / D][e % D] = __ldg(q + size_t(u) * G * D + e);
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < uint32_t(SR_ROWS * G); p += SR_THREADS) {
+    const uint32_t r = p % SR_ROWS, g = p / SR_ROWS;
+    if (r >= nrow) continue;
+    double s = 0.0;
+#pragma unroll 16
+    for (int j = 0; j < D; ++j) s = __fma_rn(double(qs[g][j]), double(crow[r][j]), s);
+    scores[(size_t(u) * G + g) * slice + (t0 + r - c_lo)] = s;
+  }
+}
+
+__global__ void __launch_bounds__(SR_THREADS)
+k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__ scores,
+                const uint32_t* __restrict__ gsize, const uint32_t* __restrict__ lsize,
+                const uint32_t* __restrict__ lstart, const uint32_t* __restrict__ prefix,
+                const uint32_t* __restrict__ lsorted, ckv_runs runs,
+                uint32_t* __restrict__ token_ids, uint32_t* __restrict__ n_tokens,
+                uint32_t* __restrict__ n_taken, uint32_t* __restrict__ trimmed_out,
+                uint32_t* __restrict__ ranked) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smraw);  // [p2]
+  uint32_t* id = reinterpret_cast<uint32_t*>(key + p2);                     // [p2]
+  uint32_t* incl = id + p2;                                                 // [p2]
+  uint32_t* loc = incl + p2;                                                // [p2 + 1]
+  __shared__ uint32_t s_taken, s_wsum[SR_THREADS / 32];
+  const uint32_t h = blockIdx.x, unit = h / d.group;
+  const uint32_t C = d.C, B = d.budget;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // gathered scores: cluster c lives in rank c / slice at offset c % slice
+  for (uint32_t c = tid; c < p2; c += SR_THREADS) {
+    if (c < C) {
+      const uint32_t r = c / d.slice, o = c % d.slice;
+      key[c] = rank_key_s(scores[(size_t(r) * d.n_q + h) * d.slice + o]);
+      id[c] = c;
+    } else {
+      key[c] = 0ull;
+      id[c] = 0xffffffffu;  // padding sorts after every real cluster
+    }
+  }
+  __syncthreads();
+  // block bitonic sort, descending by (key, -id)
+  for (uint32_t k = 2; k <= p2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = tid; i < p2; i += SR_THREADS) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long ka = key[i], kb = key[ixj];
+          const uint32_t ia = id[i], ib = id[ixj];
+          const bool asc = (i & k) == 0;
+          const bool swap = asc ? before(kb, ib, ka, ia) : before(ka, ia, kb, ib);
+          if (swap) { key[i] = kb; key[ixj] = ka; id[i] = ib; id[ixj] = ia; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // inclusive prefix of the global sizes in rank order (chunks of 256)
+  const uint32_t* gs = gsize + size_t(unit) * d.c_cap;
+  if (tid == 0) s_taken = B == 0 ? 0u : C;  // the reference breaks at cum >= B
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < C; b += SR_THREADS) {
+    const uint32_t i = b + tid;
+    uint32_t x = i < C ? __ldg(gs + id[i]) : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[wid] = x;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int w = 0; w < wid; ++w) wpre += s_wsum[w];
+    x += wpre + carry;
+    if (i < C) incl[i] = x;
+    uint32_t tot = 0;
+    for (int w = 0; w < SR_THREADS / 32; ++w) tot += s_wsum[w];
+    __syncthreads();
+    carry += tot;
+  }
+  __syncthreads();
+  // taken = first i with incl[i] >= B, plus one (all of C when the total < B)
+  for (uint32_t i = tid; i < C; i += SR_THREADS)
+    if (B > 0 && incl[i] >= B && (i == 0 || incl[i - 1] < B)) s_taken = i + 1;
+  __syncthreads();
+  const uint32_t taken = s_taken;
+  const uint32_t full_cum = taken ? incl[taken - 1] : 0;
+  const uint32_t trimmed = full_cum > B ? full_cum - B : 0;
+  // this rank's share of each taken cluster
+  const uint32_t* ls = lsize + size_t(unit) * d.c_cap;
+  const uint32_t* pf = prefix + size_t(unit) * d.c_cap;
+  for (uint32_t i = tid; i < taken; i += SR_THREADS) {
+    const uint32_t c = id[i];
+    const uint32_t allow = (i + 1 == taken && trimmed) ? B - (i ? incl[i - 1] : 0u) : __ldg(gs + c);
+    const uint32_t p = __ldg(pf + c), l = __ldg(ls + c);
+    loc[i] = allow > p ? min(allow - p, l) : 0u;
+  }
+  __syncthreads();
+  // exclusive prefix of the local shares -> run offsets (reuse incl[] as out)
+  if (wid == 0) {
+    uint32_t c2 = 0;
+    for (uint32_t b = 0; b < taken; b += 32) {
+      const uint32_t i = b + lane;
+      uint32_t x = i < taken ? loc[i] : 0u;
+      const uint32_t own = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < taken) loc[i] = c2 + x - own;  // exclusive
+      c2 += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) loc[taken] = c2;
+  }
+  __syncthreads();
+  const uint32_t cum = loc[taken];
+  const uint32_t n = cum + d.sink_rows + d.n_rec;
+  const uint32_t* lst = lstart + size_t(unit) * (d.c_cap + 1);
+  uint32_t* rr = runs.row + size_t(h) * runs.run_cap;
+  uint32_t* ro = runs.off + size_t(h) * (runs.run_cap + 1);
+  for (uint32_t i = tid; i < taken; i += SR_THREADS) {
+    rr[i] = d.row_base + __ldg(lst + id[i]);
+    ro[i] = loc[i];
+  }
+  if (tid == 0) {
+    uint32_t nr = taken;
+    if (d.sink_rows) { rr[nr] = 0; ro[nr] = cum; ++nr; }
+    if (d.n_rec) { rr[nr] = d.rec_row; ro[nr] = cum + d.sink_rows; ++nr; }
+    ro[nr] = n;
+    runs.count[h] = nr;
+    n_tokens[h] = n;
+    n_taken[h] = taken;
+    trimmed_out[h] = trimmed;
+  }
+  const uint32_t n_rank = (d.flags & CKV_SEL_FULL_RANK) ? C : taken;
+  for (uint32_t i = tid; i < n_rank; i += SR_THREADS) ranked[size_t(h) * d.c_cap + i] = id[i];
+  if (token_ids) {  // reference positions of this rank's I_T entries
+    uint32_t* out = token_ids + size_t(h) * d.sel_cap;
+    const uint32_t* sid = lsorted + size_t(unit) * d.n_local;
+    for (uint32_t e = tid; e < cum; e += SR_THREADS) {
+      uint32_t lo = 0, hi = taken;  // last run i with loc[i] <= e
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (loc[mid] <= e) lo = mid; else hi = mid;
+      }
+      while (loc[lo + 1] <= e) ++lo;  // skip empty shares
+      out[e] = d.pos_base + __ldg(sid + __ldg(lst + id[lo]) + (e - loc[lo]));
+    }
+    for (uint32_t s2 = tid; s2 < d.sink_rows; s2 += SR_THREADS) out[cum + s2] = s2;
+    for (uint32_t i = tid; i < d.n_rec; i += SR_THREADS) out[cum + d.sink_rows + i] = d.rec_pos + i;
+  }
+}
+
+__global__ void k_lse_merge(uint32_t n_q, uint32_t world, uint32_t rank,
+                            const float* __restrict__ outs, const float* __restrict__ lses,
+                            float* __restrict__ out, float* __restrict__ weights,
+                            const uint32_t* __restrict__ n_tokens, uint32_t sel_cap) {
+  const uint32_t h = blockIdx.x;
+  const int t = threadIdx.x;  // 128 threads = D
+  float M = -INFINITY;
+  for (uint32_t s = 0; s < world; ++s) M = fmaxf(M, lses[size_t(s) * n_q + h]);
+  float L = 0.f, o = 0.f;
+  for (uint32_t s = 0; s < world; ++s) {
+    const float ls = lses[size_t(s) * n_q + h];
+    const float w = ls == -INFINITY ? 0.f : exp2f(ls - M);
+    L += w;
+    o += w * outs[(size_t(s) * n_q + h) * D + t];
+  }
+  out[size_t(h) * D + t] = o / L;
+  if (weights) {
+    const float ls = lses[size_t(rank) * n_q + h];
+    const float sc = ls == -INFINITY ? 0.f : exp2f(ls - M) / L;
+    float* w = weights + size_t(h) * sel_cap;
+    for (uint32_t j = t; j < n_tokens[h]; j += blockDim.x) w[j] *= sc;
+  }
+}
+
+__global__ void k_fill_empty(uint32_t n_q, float* __restrict__ out, float* __restrict__ lse) {
+  const uint32_t h = blockIdx.x;
+  out[size_t(h) * D + threadIdx.x] = 0.f;
+  if (threadIdx.x == 0) lse[h] = -INFINITY;
+}
+
+}  // namespace
+}  // namespace ckvb
+
+using namespace ckvb;
+
+extern "C" {
+
+int ckv_score_range(ckv_ctx* ctx, uint32_t n_units, uint32_t group, const float* q,
+                    const float* centroids, uint32_t c_cap, uint32_t C, uint32_t c_lo,
+                    uint32_t slice, double* scores) {
+  if (!ctx || !q || !centroids || !scores) { set_error("ckv_score_range: NULL argument"); return CKV_EINVAL; }
+  if (c_cap < C || slice == 0) { set_error("ckv_score_range: need c_cap >= C, slice >= 1"); return CKV_EINVAL; }
+  const uint32_t c_hi = c_lo + slice;
+  if (n_units == 0 || c_lo >= C) return CKV_OK;
+  cudaStream_t st = ctx->stream;
+#define CKV_SR(GG)                                                                           \
+  case GG: {                                                                                 \
+    dim3 grid(n_units, (slice + SR_ROWS - 1) / SR_ROWS);                                     \
+    k_score_range<GG><<<grid, SR_THREADS, 0, st>>>(q, centroids, c_cap, C, c_lo, c_hi, slice, \
+                                                   scores);                                  \
+    break;                                                                                   \
+  }
+  switch (group) {
+    CKV_SR(1) CKV_SR(2) CKV_SR(4) CKV_SR(8)
+    default: set_error("ckv_score_range: group must be 1, 2, 4 or 8"); return CKV_EINVAL;
+  }
+#undef CKV_SR
+  CKV_LAUNCH_CHECK("k_score_range");
+  ctx->launches++;
+  return CKV_OK;
+}
+
+int ckv_select_scored(ckv_ctx* ctx, const ckv_shard_select_desc* d, const double* scores,
+                      const uint32_t* gsize, const uint32_t* lsize, const uint32_t* lstart,
+                      const uint32_t* prefix, const uint32_t* lsorted, const ckv_runs* runs,
+                      uint32_t* token_ids, uint32_t* n_tokens, uint32_t* n_taken,
+                      uint32_t* trimmed, uint32_t* ranked) {
+  if (!ctx || !d || !scores || !gsize || !lsize || !lstart || !prefix || !runs || !runs->row ||
+      !n_tokens || !n_taken || !trimmed || !ranked) {
+    set_error("ckv_select_scored: NULL argument");
+    return CKV_EINVAL;
+  }
+  if (d->C == 0 || d->C > 4096 || d->c_cap < d->C || runs->run_cap < d->C + 2 ||
+      d->slice * d->world < d->C || (token_ids && !lsorted)) {
+    set_error("ckv_select_scored: need 1 <= C <= 4096 <= c_cap, run_cap >= C + 2, "
+              "slice * world >= C, lsorted with token_ids");
+    return CKV_EINVAL;
+  }
+  if (d->n_q == 0) return CKV_OK;
+  uint32_t p2 = 32;
+  while (p2 < d->C) p2 <<= 1;
+  const size_t smem = size_t(p2) * 8 + size_t(p2) * 4 * 2 + (size_t(p2) + 1) * 4;
+  static int attr = 0;
+  if (!attr) {
+    CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_scored, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      96 * 1024));
+    attr = 1;
+  }
+  k_select_scored<<<d->n_q, SR_THREADS, smem, ctx->stream>>>(
+      *d, p2, scores, gsize, lsize, lstart, prefix, lsorted, *runs, token_ids, n_tokens, n_taken,
+      trimmed, ranked);
+  CKV_LAUNCH_CHECK("k_select_scored");
+  ctx->launches++;
+  return CKV_OK;
+}
+
+int ckv_attend_partial(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q,
+                       const uint16_t* K, const uint16_t* V, const ckv_runs* runs,
+                       const uint32_t* n_tokens, float* out, float* lse, float* weights) {
+  if (!ctx || !d || !runs || !out || !lse) { set_error("ckv_attend_partial: NULL argument"); return CKV_EINVAL; }
+  cudaStream_t st = ctx->stream;
+  if (d->n_q == 0) return CKV_OK;
+  if (d->max_tokens == 0) {  // no local tokens for any q head
+    k_fill_empty<<<d->n_q, D, 0, st>>>(d->n_q, out, lse);
+    CKV_LAUNCH_CHECK("k_fill_empty");
+    ctx->launches++;
+    return CKV_OK;
+  }
+  const size_t pf = attend_part_floats(d->n_q, d->max_tokens);
+  float* part = nullptr;
+  float* lw = nullptr;
+  uint32_t* tickets = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&part, pf * 4 + 16, st));
+  CKV_CUDA_TRY(cudaMallocAsync(&tickets, size_t(d->n_q) * 4 + 4, st));
+  CKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(d->n_q) * 4 + 4, st));
+  if (weights) CKV_CUDA_TRY(cudaMallocAsync(&lw, size_t(d->n_q) * d->sel_cap * 4 + 16, st));
+  int rc = launch_attend(st, *d, q, K, V, nullptr, *runs, n_tokens, out, weights, lw, part,
+                         tickets, lse);
+  ctx->launches++;
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(tickets, st);
+  if (lw) cudaFreeAsync(lw, st);
+  return rc;
+}
+
+int ckv_attend_merge(ckv_ctx* ctx, uint32_t n_q, uint32_t world, uint32_t rank,
+                     const float* outs, const float* lses, float* out, float* weights,
+                     const uint32_t* n_tokens, uint32_t sel_cap) {
+  if (!ctx || !outs || !lses || !out || (weights && !n_tokens) || rank >= world) {
+    set_error("ckv_attend_merge: bad argument");
+    return CKV_EINVAL;
+  }
+  if (n_q == 0) return CKV_OK;
+  k_lse_merge<<<n_q, D, 0, ctx->stream>>>(n_q, world, rank, outs, lses, out, weights, n_tokens,
+                                          sel_cap);
+  CKV_LAUNCH_CHECK("k_lse_merge");
+  ctx->launches++;
+  return CKV_OK;
+}
+
+}  // extern "C"

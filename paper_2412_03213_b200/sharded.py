@@ -322,3 +322,123 @@ def kmeans_cosine_sharded(shard: ShardSteps, n_total: int, row_lo: int, seeds=No
         shard.set_active(active)
     cents, labels = shard.result(iters)
     return ShardedKMeansResult(C_, cents, labels, row_lo, iters, converged, rep_hist, obj_hist)
+
+
+# --------------------------------------------------------------------------
+# the decode step (select_tokens + approx_attention, sharded)
+# --------------------------------------------------------------------------
+class ShardedDecoder:
+    """One rank's share of the sequence-sharded decode step.
+
+    Built from this rank's k-means result and its KV shard: the shard's
+    clustered rows (global positions sink_tokens + row_lo ...), plus the
+    sinks on the rank that holds positions [0, sink_tokens) and the recency
+    window [rec_pos, rec_pos + n_rec) on the rank that holds it.  The local
+    store is re-laid cluster-major by the LOCAL index, so every rank's share
+    of a selected cluster is one contiguous run.
+
+    step(q): ckv_score_range on this rank's centroid slice -> all-gather of
+    the f64 scores -> ckv_select_scored (global ranking, budget and trim;
+    this rank's share of I_T) -> ckv_attend_partial -> all-gather of
+    (out, lse) -> ckv_attend_merge.  Every rank returns the same output.
+    """
+
+    def __init__(self, km: ShardedKMeansResult, K_shard: torch.Tensor, V_shard: torch.Tensor,
+                 group: int, budget: int, comm: Comm | None = None, sink_K=None, sink_V=None,
+                 rec_K=None, rec_V=None, rec_pos: int = 0, sink_tokens: int = 16, ctx=None):
+        from .api import Context
+        self.ctx = ctx or Context.default()
+        self.comm = comm or Comm()
+        dev = K_shard.device
+        U, n_local = km.labels.shape
+        self.U, self.G, self.n_q, self.C, self.B = U, group, U * group, km.n_clusters, budget
+        self.sink_rows = 0 if sink_K is None else int(sink_K.shape[1])
+        self.n_rec = 0 if rec_K is None else int(rec_K.shape[1])
+        self.rec_pos = rec_pos
+        n_rows = self.sink_rows + n_local + self.n_rec
+        self.p_cap = n_rows
+        i16 = torch.int16
+        parts_k = [t for t in (sink_K, K_shard, rec_K) if t is not None]
+        parts_v = [t for t in (sink_V, V_shard, rec_V) if t is not None]
+        Kp = torch.cat([t.to(dev, i16) for t in parts_k], 1).contiguous()
+        Vp = torch.cat([t.to(dev, i16) for t in parts_v], 1).contiguous()
+        labels = torch.full((U, n_rows), -1, dtype=torch.int32, device=dev)
+        labels[:, self.sink_rows:self.sink_rows + n_local] = km.labels.to(dev)
+        C_ = self.C
+        ncl = torch.full((U,), C_, dtype=torch.int32, device=dev)
+        self.lsize = torch.zeros((U, C_), dtype=torch.int32, device=dev)
+        self.lstart = torch.zeros((U, C_ + 1), dtype=torch.int32, device=dev)
+        self.lsorted = torch.zeros((U, n_rows), dtype=torch.int32, device=dev)
+        check(lib().ckv_build_index(self.ctx.h, U, n_rows, n_rows, C_, labels.data_ptr(),
+                                    ncl.data_ptr(), self.lsize.data_ptr(),
+                                    self.lstart.data_ptr(), self.lsorted.data_ptr()))
+        self.K = torch.empty_like(Kp)
+        self.V = torch.empty_like(Vp)
+        check(lib().ckv_relayout_kv(self.ctx.h, U, n_rows, Kp.data_ptr(), Vp.data_ptr(),
+                                    self.K.data_ptr(), self.V.data_ptr(), self.lsorted.data_ptr(),
+                                    self.sink_rows, self.sink_rows + n_local, n_rows))
+        # global sizes and the members on lower-ranked shards, once per prefill
+        per_rank = [t.to(dev) for t in self.comm.all_gather(self.lsize)]
+        self.gsize = torch.stack(per_rank).sum(0).to(torch.int32).contiguous()
+        self.prefix = (torch.stack(per_rank[: self.comm.rank]).sum(0).to(torch.int32)
+                       if self.comm.rank > 0 else torch.zeros_like(self.lsize)).contiguous()
+        self.cents = km.centroids.to(dev).contiguous()
+        self.slice = (C_ + self.comm.world - 1) // self.comm.world
+        self.c_lo = self.comm.rank * self.slice
+        self.pos_base = sink_tokens + km.row_lo - self.sink_rows
+        self.sel_cap = budget + self.sink_rows + self.n_rec
+        run_cap = C_ + 2
+        nq = self.n_q
+        self.run_row = torch.zeros((nq, run_cap), dtype=torch.int32, device=dev)
+        self.run_off = torch.zeros((nq, run_cap + 1), dtype=torch.int32, device=dev)
+        self.run_cnt = torch.zeros((nq,), dtype=torch.int32, device=dev)
+        self.runs = N.Runs(self.run_row.data_ptr(), self.run_off.data_ptr(),
+                           self.run_cnt.data_ptr(), run_cap)
+        self.n_tokens = torch.zeros((nq,), dtype=torch.int32, device=dev)
+        self.n_taken = torch.zeros((nq,), dtype=torch.int32, device=dev)
+        self.trimmed = torch.zeros((nq,), dtype=torch.int32, device=dev)
+        self.ranked = torch.zeros((nq, C_), dtype=torch.int32, device=dev)
+        self.my_scores = torch.zeros((nq, self.slice), dtype=torch.float64, device=dev)
+        self.out_loc = torch.zeros((nq, D), dtype=torch.float32, device=dev)
+        self.lse = torch.zeros((nq,), dtype=torch.float32, device=dev)
+        self.sdesc = N.ShardSelectDesc(nq, group, budget, C_, C_, self.slice, self.comm.world,
+                                       n_rows, self.sel_cap, self.sink_rows, self.sink_rows,
+                                       self.sink_rows + n_local, rec_pos, self.n_rec,
+                                       self.pos_base, 0)
+        self.adesc = N.AttendDesc(nq, group, n_rows, self.sel_cap, self.sel_cap)
+
+    def step(self, q: torch.Tensor, want_ids: bool = False, want_weights: bool = False,
+             full_rank: bool = False) -> dict:
+        """One decode step for every q head; q: device f32 [n_q][128]."""
+        L, h = lib(), self.ctx.h
+        q = q.contiguous()
+        dev = q.device
+        check(L.ckv_score_range(h, self.U, self.G, q.data_ptr(), self.cents.data_ptr(), self.C,
+                                self.C, self.c_lo, self.slice, self.my_scores.data_ptr()))
+        scores = torch.stack([t.to(dev) for t in self.comm.all_gather(self.my_scores)])
+        ids = (torch.zeros((self.n_q, self.sel_cap), dtype=torch.int32, device=dev)
+               if want_ids else None)
+        self.sdesc.flags = N.CKV_SEL_FULL_RANK if full_rank else 0
+        check(L.ckv_select_scored(h, C.byref(self.sdesc), scores.data_ptr(),
+                                  self.gsize.data_ptr(), self.lsize.data_ptr(),
+                                  self.lstart.data_ptr(), self.prefix.data_ptr(),
+                                  self.lsorted.data_ptr(), C.byref(self.runs),
+                                  None if ids is None else ids.data_ptr(),
+                                  self.n_tokens.data_ptr(), self.n_taken.data_ptr(),
+                                  self.trimmed.data_ptr(), self.ranked.data_ptr()))
+        w = (torch.zeros((self.n_q, self.sel_cap), dtype=torch.float32, device=dev)
+             if want_weights else None)
+        check(L.ckv_attend_partial(h, C.byref(self.adesc), q.data_ptr(), self.K.data_ptr(),
+                                   self.V.data_ptr(), C.byref(self.runs),
+                                   self.n_tokens.data_ptr(), self.out_loc.data_ptr(),
+                                   self.lse.data_ptr(), None if w is None else w.data_ptr()))
+        outs = torch.stack([t.to(dev) for t in self.comm.all_gather(self.out_loc)]).contiguous()
+        lses = torch.stack([t.to(dev) for t in self.comm.all_gather(self.lse)]).contiguous()
+        out = torch.empty((self.n_q, D), dtype=torch.float32, device=dev)
+        check(L.ckv_attend_merge(h, self.n_q, self.comm.world, self.comm.rank, outs.data_ptr(),
+                                 lses.data_ptr(), out.data_ptr(),
+                                 None if w is None else w.data_ptr(), self.n_tokens.data_ptr(),
+                                 self.sel_cap))
+        return dict(out=out, token_ids=ids, weights=w, n_tokens=self.n_tokens,
+                    n_taken=self.n_taken, trimmed=self.trimmed, ranked=self.ranked,
+                    run_off=self.run_off, run_cnt=self.run_cnt)

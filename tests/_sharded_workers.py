@@ -28,3 +28,37 @@ def kmeans_rank(rank, world, keys, C_, seeds, max_iters, init_rows, device):
     return dict(lo=lo, labels=r.labels.cpu().numpy(), centroids=r.centroids.cpu().numpy(),
                 iters=r.iterations_used, converged=r.converged, reps=r.repair_iterations,
                 obj=r.objective_history)
+
+
+def decode_rank(rank, world, K, V, Q, Kr, Vr, C_, seeds, G, budget, device):
+    """Sharded prefill k-means + one sharded decode step (select + attend)
+    on rank `rank`; K, V [U][L][128] prompt, Kr, Vr [U][n_rec][128] the
+    recency rows (positions L..), Q [U*G][128].  Returns this rank's share."""
+    import torch
+
+    from paper_2412_03213_b200.api import Context
+    from paper_2412_03213_b200.sharded import (Comm, DeviceShard, ShardedDecoder,
+                                               kmeans_cosine_sharded, shard_range)
+    from tests._inputs import bf16_bits
+    torch.cuda.set_device(device)
+    ctx = Context(device)
+    comm = Comm()
+    U, L, _ = K.shape
+    n = L - 16
+    lo, hi = shard_range(n, world, rank)
+    dev = torch.device("cuda", device)
+    t = lambda x: torch.from_numpy(bf16_bits(x).view(np.int16)).to(dev)
+    kb = t(K[:, 16 + lo:16 + hi])
+    km = kmeans_cosine_sharded(DeviceShard(kb, C_, ctx=ctx), n, lo, seeds=seeds, comm=comm)
+    dec = ShardedDecoder(km, kb, t(V[:, 16 + lo:16 + hi]), G, budget, comm,
+                         sink_K=t(K[:, :16]) if rank == 0 else None,
+                         sink_V=t(V[:, :16]) if rank == 0 else None,
+                         rec_K=t(Kr) if rank == world - 1 and Kr.shape[1] else None,
+                         rec_V=t(Vr) if rank == world - 1 and Vr.shape[1] else None,
+                         rec_pos=L, ctx=ctx)
+    r = dec.step(torch.from_numpy(Q).to(dev), want_ids=True, want_weights=True, full_rank=True)
+    ctx.sync()
+    g = lambda x: x.cpu().numpy()
+    return dict(out=g(r["out"]), ids=g(r["token_ids"]), w=g(r["weights"]),
+                n_tokens=g(r["n_tokens"]), n_taken=g(r["n_taken"]), trimmed=g(r["trimmed"]),
+                ranked=g(r["ranked"]), off=g(r["run_off"]), iters=km.iterations_used)
