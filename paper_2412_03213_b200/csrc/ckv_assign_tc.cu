@@ -43,12 +43,14 @@ namespace ckvb {
 
 constexpr int TC_M = 128;              // keys per tile (UMMA_M)
 constexpr int TC_BK = 64;              // bf16 columns per 128-B swizzle atom
-constexpr int TC_MAXC = 512;           // C_pad limit: B resident, 2 x 256 TMEM cols
+constexpr int TC_MAXC = 512;           // columns per range: B resident, 2 x 256 TMEM cols
+constexpr int TC_MAXC_ALL = 4096;      // C_pad limit (ranges of <= TC_MAXC columns)
 constexpr int TC_CH = 256;             // columns per MMA chunk / TMEM buffer
 constexpr int TC_EGROUPS = 4;          // epilogue warp groups (4 warps = 128 TMEM lanes each)
 constexpr int TC_THREADS = (2 + 4 * TC_EGROUPS) * 32;
 constexpr uint32_t TC_FULL = 0xffffffffu;
 constexpr int TC_NCAND = 8;            // candidates an epilogue row keeps
+constexpr int TC_MERGE_SLOT = 1023;    // fix_count slot of the merged (C > 512) list
 
 // dynamic smem (1024-B aligned base): A stages [stages][2 k-halves][128 x 128 B],
 // then B [2 k-halves][c_pad x 128 B], then the barriers.  B is the resident
@@ -189,6 +191,11 @@ struct TcArgs {
   const int32_t* unit_list;  // active units
   const int32_t* n_list;     // device count of active units
   uint32_t n, C, c_pad, tiles_per_unit;
+  // C > 512: the columns split into n_ranges ranges of rc (a multiple of 32,
+  // <= 512) columns, each its own work item with a resident B; the epilogue
+  // then writes a per-(key, range) summary and k_assign_merge decides
+  uint32_t n_ranges, rc;
+  float4* summ;                // [unit][n][n_ranges]: M_r, n_in | FULL, 4 ids (u16)
   uint32_t key_rows_per_unit;  // key_stride / 128
   uint32_t label_stride;
   const float* knorm;          // [unit][n] key norms (band scale)
@@ -201,6 +208,22 @@ struct TcArgs {
   uint32_t mode;               // experiment knob (CKV_TC_MODE): 1 = no epilogue math
 };
 
+struct TcWork {
+  uint32_t ui, range, tile;
+};
+__device__ __forceinline__ TcWork tc_work(uint32_t w, const TcArgs& a) {
+  const uint32_t per_u = a.n_ranges * a.tiles_per_unit;
+  TcWork k;
+  k.ui = w / per_u;
+  const uint32_t r = w - k.ui * per_u;
+  k.range = r / a.tiles_per_unit;
+  k.tile = r - k.range * a.tiles_per_unit;
+  return k;
+}
+__device__ __forceinline__ uint32_t tc_cols(uint32_t range, const TcArgs& a) {
+  return min(a.rc, a.c_pad - range * a.rc);
+}
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap dmap,
             TcArgs a) {
@@ -209,16 +232,15 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
       (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   const uint32_t S = a.stages;
   uint8_t* sm_a = sbase;                         // [S][2][TC_M*128]
-  uint8_t* sm_b = sbase + S * TC_ABYTES;         // [2][c_pad*128]
+  uint8_t* sm_b = sbase + S * TC_ABYTES;         // [2][rc*128]
   __shared__ TcBars sm;  // static: the compiler keeps these accesses LDS/STS
   auto A = [&](uint32_t st, uint32_t kh) { return sm_a + st * TC_ABYTES + kh * (TC_M * 128); };
-  auto Bp = [&](uint32_t kh, uint32_t row) { return sm_b + kh * (a.c_pad * 128) + row * 128; };
+  auto Bp = [&](uint32_t kh, uint32_t row) { return sm_b + kh * (a.rc * 128) + row * 128; };
   const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
   const uint32_t n_units = uint32_t(*a.n_list);
-  const uint32_t total = n_units * a.tiles_per_unit;
+  const uint32_t total = n_units * a.n_ranges * a.tiles_per_unit;
   const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
   const uint32_t w0 = min(total, blockIdx.x * per), w1 = min(total, w0 + per);
-  const uint32_t nchunks = (a.c_pad + TC_CH - 1) / TC_CH;
 
   if (t == 0) {
     for (uint32_t s = 0; s < S; ++s) { mb_init(&sm.a_full[s], 1); mb_init(&sm.a_empty[s], 1); }
@@ -241,20 +263,23 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   if (wid == 0) {
     // ============================ TMA producer =================================
     if (lane == 0 && w0 < w1) {
-      uint32_t st = 0, ph = 0, bswitch = 0, cur_unit = TC_FULL;
-      const uint32_t bbytes = a.c_pad * 128 * 2;  // c_pad is a multiple of TC_BOXR
+      uint32_t st = 0, ph = 0, bswitch = 0, cur_key = TC_FULL;
       for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t ui = w / a.tiles_per_unit, tile = w % a.tiles_per_unit;
-        const uint32_t unit = uint32_t(a.unit_list[ui]);
-        if (unit != cur_unit) {
-          // the previous unit's MMAs must be done reading B
-          if (cur_unit != TC_FULL) mb_wait(&sm.b_empty, (bswitch - 1) & 1);
-          mb_expect(&sm.b_full, bbytes);
-          for (uint32_t r0 = 0; r0 < a.c_pad; r0 += TC_BOXR) {
+        const TcWork wk = tc_work(w, a);
+        const uint32_t tile = wk.tile;
+        const uint32_t unit = uint32_t(a.unit_list[wk.ui]);
+        const uint32_t key = wk.ui * a.n_ranges + wk.range;
+        if (key != cur_key) {
+          // the previous (unit, range)'s MMAs must be done reading B
+          if (cur_key != TC_FULL) mb_wait(&sm.b_empty, (bswitch - 1) & 1);
+          const uint32_t cols = tc_cols(wk.range, a);  // a multiple of TC_BOXR
+          mb_expect(&sm.b_full, cols * 128 * 2);
+          for (uint32_t r0 = 0; r0 < cols; r0 += TC_BOXR) {
             for (int kh = 0; kh < 2; ++kh)
-              tma_2d(Bp(kh, r0), &dmap, kh * TC_BK, int(unit * a.c_pad + r0), &sm.b_full);
+              tma_2d(Bp(kh, r0), &dmap, kh * TC_BK,
+                     int(unit * a.c_pad + wk.range * a.rc + r0), &sm.b_full);
           }
-          cur_unit = unit;
+          cur_key = key;
           ++bswitch;
         }
         mb_wait(&sm.a_empty[st], ph ^ 1);
@@ -268,23 +293,28 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   } else if (wid == 1) {
     // ============================ MMA issuer ===================================
     if (lane == 0 && w0 < w1) {
-      uint32_t st = 0, ph = 0, g = 0, bswitch = 0, cur_unit = TC_FULL;
+      uint32_t st = 0, ph = 0, g = 0, bswitch = 0, cur_key = TC_FULL;
       for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t ui = w / a.tiles_per_unit;
-        const uint32_t unit = uint32_t(a.unit_list[ui]);
-        const bool last_of_unit =
-            (w + 1 == w1) || (uint32_t(a.unit_list[(w + 1) / a.tiles_per_unit]) != unit);
-        if (unit != cur_unit) {
+        const TcWork wk = tc_work(w, a);
+        const uint32_t key = wk.ui * a.n_ranges + wk.range;
+        bool last_of_unit = w + 1 == w1;
+        if (!last_of_unit) {
+          const TcWork nx = tc_work(w + 1, a);
+          last_of_unit = nx.ui * a.n_ranges + nx.range != key;
+        }
+        if (key != cur_key) {
           mb_wait(&sm.b_full, bswitch & 1);
-          cur_unit = unit;
+          cur_key = key;
           ++bswitch;
         }
         mb_wait(&sm.a_full[st], ph);
         tc_fence_after();
+        const uint32_t cols = tc_cols(wk.range, a);
+        const uint32_t nchunks = (cols + TC_CH - 1) / TC_CH;
         for (uint32_t ch = 0; ch < nchunks; ++ch, ++g) {
           const uint32_t buf = g & 1, bph = (g >> 1) & 1;
           const uint32_t c0 = ch * TC_CH;
-          const uint32_t nc = min(uint32_t(TC_CH), a.c_pad - c0);
+          const uint32_t nc = min(uint32_t(TC_CH), cols - c0);
           mb_wait(&sm.acc_empty[buf], bph ^ 1);
           tc_fence_after();
           const uint32_t idesc = idesc_bf16_f32(TC_M, nc);
@@ -322,38 +352,34 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     uint32_t g = 0;
     if (grp == 0)
       for (int ch = 0; ch < 2; ++ch) sm.n_ch[ch][lane_row] = 0;
-    // (unit, tile) advance incrementally; the next tile's key norm is loaded
-    // one tile ahead so its latency hides behind this tile's work
-    uint32_t ui = w0 / a.tiles_per_unit, tile = w0 % a.tiles_per_unit;
-    uint32_t unit = w0 < w1 ? uint32_t(a.unit_list[ui]) : 0u;
-    float eps = w0 < w1 ? a.eps_u[unit] : 0.f;
+    // the next work item's key norm is loaded one item ahead so its latency
+    // hides behind this item's work
     float kn_next = 0.f;
-    if (w0 < w1 && tile * TC_M + lane_row < a.n)
-      kn_next = a.knorm[size_t(unit) * a.n + tile * TC_M + lane_row];
+    if (w0 < w1) {
+      const TcWork k0 = tc_work(w0, a);
+      if (k0.tile * TC_M + lane_row < a.n)
+        kn_next = a.knorm[size_t(a.unit_list[k0.ui]) * a.n + k0.tile * TC_M + lane_row];
+    }
     for (uint32_t w = w0; w < w1; ++w) {
-      if (w > w0) {
-        if (++tile == a.tiles_per_unit) {
-          tile = 0;
-          ++ui;
-          unit = uint32_t(a.unit_list[ui]);
-          eps = a.eps_u[unit];
-        }
-      }
+      const TcWork wk = tc_work(w, a);
+      const uint32_t unit = uint32_t(a.unit_list[wk.ui]), tile = wk.tile;
+      const float eps = a.eps_u[unit];
       const uint32_t row = tile * TC_M + lane_row;
       const float kn = kn_next;
       if (w + 1 < w1) {
-        uint32_t t2 = tile + 1, u2 = unit;
-        if (t2 == a.tiles_per_unit) { t2 = 0; u2 = uint32_t(a.unit_list[ui + 1]); }
-        const uint32_t r2 = t2 * TC_M + lane_row;
-        kn_next = r2 < a.n ? a.knorm[size_t(u2) * a.n + r2] : 0.f;
+        const TcWork k2 = tc_work(w + 1, a);
+        const uint32_t r2 = k2.tile * TC_M + lane_row;
+        kn_next = r2 < a.n ? a.knorm[size_t(a.unit_list[k2.ui]) * a.n + r2] : 0.f;
       }
       const float band = kn * (2.0f * eps + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
+      const uint32_t cols = tc_cols(wk.range, a), cbase = wk.range * a.rc;
+      const uint32_t nchunks = (cols + TC_CH - 1) / TC_CH;
 #pragma unroll 1
       for (uint32_t ch = 0; ch < nchunks; ++ch) {
         const uint32_t buf = g & 1, bph = (g >> 1) & 1;
         ++g;
-        const uint32_t c0 = ch * TC_CH;
-        const uint32_t nb = min(uint32_t(TC_CH), a.c_pad - c0) / 32;  // blocks in chunk
+        const uint32_t c0 = cbase + ch * TC_CH;  // global column of the chunk
+        const uint32_t nb = min(uint32_t(TC_CH), cols - ch * TC_CH) / 32;  // blocks in chunk
         const uint32_t b0 = grp, b1 = grp + TC_EGROUPS;               // my blocks
         const bool h0 = b0 < nb, h1 = b1 < nb;                         // warp-uniform
         float v[64];
@@ -455,7 +481,21 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
           }
           if (nin > uint32_t(TC_NCAND)) full = true;
           int32_t* lab = a.labels + size_t(unit) * a.label_stride + row;
-          if (!full && nin == 1) {
+          if (a.n_ranges > 1) {
+            // this range's summary: its max and its (<= 4) in-band ids;
+            // k_assign_merge combines the ranges of the key
+            uint32_t ids[4] = {0u, 0u, 0u, 0u}, k2 = 0;
+            if (nin > 4u) full = true;
+            if (!full)
+              for (uint32_t ch = 0; ch < nchunks; ++ch)
+                if (sm.m_ch[ch][lane_row] >= M - band)
+                  for (uint32_t k = 0; k < sm.n_ch[ch][lane_row]; ++k)
+                    ids[k2++] = sm.id_ch[ch][k][lane_row];
+            a.summ[(size_t(unit) * a.n + row) * a.n_ranges + wk.range] =
+                make_float4(M, __uint_as_float(full ? TC_FULL : nin),
+                            __uint_as_float(ids[0] | (ids[1] << 16)),
+                            __uint_as_float(ids[2] | (ids[3] << 16)));
+          } else if (!full && nin == 1) {
             *lab = int32_t(single);
           } else {
             *lab = -1;
@@ -609,6 +649,58 @@ __global__ void k_eps_max(const float* __restrict__ deps, uint32_t c_pad, uint32
   if (lane_id() == 0) eps_u[u] = m;
 }
 
+// C > 512: combine a key's per-range summaries (k_assign_tc, n_ranges > 1).
+// M = max_r M_r; a range with M_r < M - band holds no candidate; the others
+// contribute their in-band ids (each a superset of that range's share of
+// {c : S_c >= M - band}).  One candidate -> the label; otherwise the key goes
+// to the fix-up list (one region, warp-aggregated slots) with its <= 8
+// candidates, or FULL.
+__global__ void __launch_bounds__(256)
+k_assign_merge(const float4* __restrict__ summ, uint32_t n_ranges, uint32_t n,
+               const int32_t* __restrict__ unit_list, const int32_t* __restrict__ n_list,
+               const float* __restrict__ knorm, const float* __restrict__ eps_u,
+               int32_t* __restrict__ labels, uint32_t label_stride, uint4* __restrict__ fix_list,
+               uint32_t* __restrict__ fix_ids, uint32_t* __restrict__ fix_n, uint32_t fix_cap) {
+  const uint32_t ui = blockIdx.y;
+  if (ui >= uint32_t(*n_list)) return;
+  const uint32_t unit = uint32_t(unit_list[ui]);
+  const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
+  bool need = false, full = false;
+  uint32_t nin = 0, ids[TC_NCAND];
+  if (row < n) {
+    const float4* sp = summ + (size_t(unit) * n + row) * n_ranges;
+    const float band = knorm[size_t(unit) * n + row] * (2.0f * eps_u[unit] + (1.0f / 8192.0f)) *
+                       1.01f + 1e-30f;
+    float M = -INFINITY;
+    for (uint32_t r = 0; r < n_ranges; ++r) M = fmaxf(M, sp[r].x);
+    full = !(M > -INFINITY);
+    for (uint32_t r = 0; r < n_ranges && !full; ++r) {
+      const float4 sr = sp[r];
+      if (!(sr.x >= M - band)) continue;
+      const uint32_t nr = __float_as_uint(sr.y);
+      if (nr == TC_FULL || nin + nr > uint32_t(TC_NCAND)) { full = true; break; }
+      const uint32_t pk[2] = {__float_as_uint(sr.z), __float_as_uint(sr.w)};
+      for (uint32_t k = 0; k < nr; ++k) ids[nin++] = (pk[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+    }
+    int32_t* lab = labels + size_t(unit) * label_stride + row;
+    if (!full && nin == 1) *lab = int32_t(ids[0]);
+    else { *lab = -1; need = true; }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  if (!m) return;
+  uint32_t base = 0;
+  if (lane_id() == 0) base = atomicAdd(fix_n, uint32_t(__popc(m)));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (need) {
+    const uint32_t slot = base + __popc(m & ((1u << lane_id()) - 1u));
+    if (slot < fix_cap) {
+      fix_list[slot] = make_uint4(unit, row, full ? TC_FULL : nin, 0u);
+      if (!full)
+        for (uint32_t k = 0; k < nin; ++k) fix_ids[size_t(slot) * TC_NCAND + k] = ids[k];
+    }
+  }
+}
+
 __global__ void k_compact_active(const int32_t* __restrict__ active, uint32_t n_units,
                                   int32_t* __restrict__ list, int32_t* __restrict__ count,
                                   uint32_t* __restrict__ fix_count) {
@@ -618,6 +710,7 @@ __global__ void k_compact_active(const int32_t* __restrict__ active, uint32_t n_
       if (!active || active[u]) list[n++] = int32_t(u);
     *count = n;
     *fix_count = 0;
+    fix_count[TC_MERGE_SLOT] = 0;  // k_assign_merge's single region
   }
 }
 
@@ -626,7 +719,7 @@ __global__ void k_compact_active(const int32_t* __restrict__ active, uint32_t n_
 // ---------------------------------------------------------------------------
 bool assign_tc_supported(uint32_t n, uint32_t C) {
   const uint32_t c_pad = (C + 31) / 32 * 32;
-  return C >= 32 && c_pad <= uint32_t(TC_MAXC) && n >= uint32_t(TC_M);
+  return C >= 32 && c_pad <= uint32_t(TC_MAXC_ALL) && n >= uint32_t(TC_M);
 }
 
 namespace {
@@ -638,8 +731,15 @@ struct TcScratch {
   uint32_t* fix_ids;
   float* knorm;
   float* eps_u;
+  float4* summ;  // C > 512 only: per-(key, range) summaries
   uint32_t fix_cap;
 };
+// column ranges of <= TC_MAXC columns, balanced, multiples of 32
+void tc_ranges(uint32_t c_pad, uint32_t* n_ranges, uint32_t* rc) {
+  const uint32_t nr = (c_pad + TC_MAXC - 1) / TC_MAXC;
+  *n_ranges = nr;
+  *rc = ((c_pad + nr - 1) / nr + 31) / 32 * 32;
+}
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 TcScratch carve(void* base, uint32_t n_units, uint32_t n) {
   TcScratch s;
@@ -658,6 +758,8 @@ TcScratch carve(void* base, uint32_t n_units, uint32_t n) {
   s.knorm = reinterpret_cast<float*>(p);
   p += align256(size_t(n_units) * n * 4);
   s.eps_u = reinterpret_cast<float*>(p);
+  p += align256(size_t(n_units) * 4) + 256;
+  s.summ = reinterpret_cast<float4*>(p);  // sized by assign_tc_scratch_bytes
   return s;
 }
 int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
@@ -704,10 +806,12 @@ float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n) {
 }
 
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
-  (void)C;
   const size_t cap = size_t(n_units) * ((n + TC_M - 1) / TC_M) * TC_M;
+  uint32_t nr = 1, rc = 0;
+  tc_ranges((C + 31) / 32 * 32, &nr, &rc);
+  const size_t summ = nr > 1 ? size_t(n_units) * n * nr * 16 : 0;
   return align256(size_t(n_units) * 4) + 256 + 4096 + align256(cap * 16) + align256(cap * 32) + align256(size_t(n_units) * n * 4) +
-         align256(size_t(n_units) * 4) + 256;
+         align256(size_t(n_units) * 4) + 256 + summ;
 }
 
 int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
@@ -744,6 +848,8 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   ta.fix_list = s.fix_list;
   ta.fix_cap = s.fix_cap;
   ta.fix_ids = s.fix_ids;
+  tc_ranges(c_pad, &ta.n_ranges, &ta.rc);
+  ta.summ = s.summ;
   static size_t max_dyn = 0;  // opt-in per-CTA smem minus the kernel's static part
   static int attr_dev = -1;
   int dev = 0;
@@ -760,7 +866,7 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   }
   static const uint32_t tc_mode = getenv("CKV_TC_MODE") ? uint32_t(atoi(getenv("CKV_TC_MODE"))) : 0u;
   ta.mode = tc_mode;
-  const size_t fixed = 1024 + 2 * size_t(c_pad) * 128;
+  const size_t fixed = 1024 + 2 * size_t(ta.rc) * 128;
   ta.stages = uint32_t(std::min<size_t>(4, (max_dyn - fixed) / TC_ABYTES));
   if (ta.stages < 2) {
     set_error("assign_tc: not enough shared memory for two key-tile stages");
@@ -769,15 +875,30 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   const size_t smem = fixed + size_t(ta.stages) * TC_ABYTES;
   k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
   CKV_LAUNCH_CHECK("k_assign_tc");
-  k_fixup<<<dim3(8, num_sms()), 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, s.count,
-                                               ta.tiles_per_unit, keys, key_stride,
-                                          dirs, C, c_pad, s.knorm, n, labels, label_stride);
-  CKV_LAUNCH_CHECK("k_fixup");
+  if (ta.n_ranges == 1) {
+    k_fixup<<<dim3(8, num_sms()), 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, s.count,
+                                                 ta.tiles_per_unit, keys, key_stride, dirs, C,
+                                                 c_pad, s.knorm, n, labels, label_stride);
+    CKV_LAUNCH_CHECK("k_fixup");
+  } else {
+    k_assign_merge<<<dim3((n + 255) / 256, n_units), 256, 0, st>>>(
+        s.summ, ta.n_ranges, n, s.list, s.count, s.knorm, s.eps_u, labels, label_stride,
+        s.fix_list, s.fix_ids, s.fix_count + TC_MERGE_SLOT, s.fix_cap);
+    CKV_LAUNCH_CHECK("k_assign_merge");
+    // one region (gridDim.y = 1) holding the merged list
+    k_fixup<<<dim3(8 * num_sms(), 1), 256, 0, st>>>(s.fix_list, s.fix_ids,
+                                                     s.fix_count + TC_MERGE_SLOT, s.count,
+                                                     ta.tiles_per_unit, keys, key_stride, dirs,
+                                                     C, c_pad, s.knorm, n, labels, label_stride);
+    CKV_LAUNCH_CHECK("k_fixup");
+    ++*launches;
+  }
   *launches += 4;
   static const bool dbg = getenv("CKV_DEBUG_KMEANS") != nullptr;
   if (dbg) {
-    std::vector<uint32_t> cnts(num_sms());
-    cudaMemcpyAsync(cnts.data(), s.fix_count, 4 * cnts.size(), cudaMemcpyDeviceToHost, st);
+    std::vector<uint32_t> cnts(ta.n_ranges == 1 ? num_sms() : 1);
+    cudaMemcpyAsync(cnts.data(), ta.n_ranges == 1 ? s.fix_count : s.fix_count + TC_MERGE_SLOT,
+                    4 * cnts.size(), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     uint32_t nfix = 0;
     for (uint32_t c : cnts) nfix += c;

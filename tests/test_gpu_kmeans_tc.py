@@ -70,3 +70,38 @@ def test_tc_path_near_ties(gpu_ctx):
     c2, l2, i2 = _batched_kmeans(keys[None], 96, seeds, 30, N.CKV_KM_EXACT_ONLY)
     assert i1 == i2 and np.array_equal(l1, l2)
     assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+
+
+@pytest.mark.parametrize("Cn,n,U", [(513, 4096, 2), (1638, 8192, 2), (1100, 3000, 3)])
+def test_tc_multi_range_equals_exact_path(gpu_ctx, Cn, n, U):
+    """C > 512 (config E: C0 = 1638): column ranges with their own resident
+    B, per-range summaries merged by k_assign_merge, then the fix-up."""
+    from paper_2412_03213_b200 import _native as N
+    keys = np.stack([head(19, 0, u, n + 16)["K"][16:] for u in range(U)])
+    seeds = [port().mix_seed(0, 3, u) for u in range(U)]
+    c1, l1, i1 = _batched_kmeans(keys, Cn, seeds, 6, 0)
+    c2, l2, i2 = _batched_kmeans(keys, Cn, seeds, 6, N.CKV_KM_EXACT_ONLY)
+    assert i1 == i2
+    assert np.array_equal(l1, l2)
+    assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+
+
+def test_tc_multi_range_near_ties(gpu_ctx):
+    rng = np.random.default_rng(5)
+    base = rng.standard_normal((700, 128)).astype(np.float32)
+    keys = base[rng.integers(0, 700, 6000)] + 1e-3 * rng.standard_normal((6000, 128)).astype(np.float32)
+    keys = to_bf16_representable(keys)
+    from paper_2412_03213_b200 import _native as N
+    c1, l1, i1 = _batched_kmeans(keys[None], 900, [5], 8, 0)
+    c2, l2, i2 = _batched_kmeans(keys[None], 900, [5], 8, N.CKV_KM_EXACT_ONLY)
+    assert i1 == i2 and np.array_equal(l1, l2)
+    assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+
+
+def test_tc_multi_range_vs_oracle(gpu_ctx):
+    keys = head(29, 0, 1, 6000 + 16)["K"][16:]
+    c, l, info = _batched_kmeans(keys[None], 700, [77], 4, 0)
+    o = port().kmeans(keys, 700, 77, 4)
+    assert info[0] == (o.iterations_used, o.converged)
+    assert np.array_equal(l[0], o.labels)
+    assert np.array_equal(c[0].view(np.uint32), o.centroids.view(np.uint32))
