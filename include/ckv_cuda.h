@@ -316,7 +316,9 @@ int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* desc, const float* q, const 
 /* Cluster-major relayout of a position-ordered KV store:
  * dst row r = src row r for r < sink or r >= labeled_end, and src row
  * sorted_ids[u][r - sink] for sink <= r < labeled_end (sorted_ids from
- * ckv_build_index over the store's labels).  K2/V2 must not alias K/V. */
+ * ckv_build_index over the store's labels).  K2 == K and V2 == V re-lay in
+ * place through a bounded (<= 1 GiB) staging buffer, chunk of units by
+ * chunk, so a store filling most of HBM is never held twice. */
 int ckv_relayout_kv(ckv_ctx* ctx, uint32_t n_units, uint32_t p_cap, const uint16_t* K,
                     const uint16_t* V, uint16_t* K2, uint16_t* V2, const uint32_t* sorted_ids,
                     uint32_t sink, uint32_t labeled_end, uint32_t n_rows);

@@ -510,13 +510,46 @@ int ckv_relayout_kv(ckv_ctx* ctx, uint32_t n_units, uint32_t p_cap, const uint16
     set_error("ckv_relayout_kv: need sink <= labeled_end <= n_rows <= p_cap");
     return CKV_EINVAL;
   }
+  if ((K2 == K) != (V2 == V)) {
+    set_error("ckv_relayout_kv: K and V must both be in place or both out of place");
+    return CKV_EINVAL;
+  }
   if (n_units == 0 || n_rows == 0) return CKV_OK;
-  dim3 g((n_rows + 7) / 8, n_units);
-  k_relayout<<<g, 128, 0, ctx->stream>>>(K, V, K2, V2, sorted_ids, p_cap, sink, labeled_end,
-                                         n_rows);
-  CKV_LAUNCH_CHECK("k_relayout");
-  ctx->launches++;
-  return CKV_OK;
+  cudaStream_t st = ctx->stream;
+  if (K2 != K) {
+    dim3 g((n_rows + 7) / 8, n_units);
+    k_relayout<<<g, 128, 0, st>>>(K, V, K2, V2, sorted_ids, p_cap, sink, labeled_end, n_rows);
+    CKV_LAUNCH_CHECK("k_relayout");
+    ctx->launches++;
+    return CKV_OK;
+  }
+  // in place: chunks of units through a bounded staging buffer, so a store
+  // that fills most of HBM (config C: 128 GiB of KV) never needs a second copy
+  const size_t unit_bytes = size_t(p_cap) * D * 2;
+  const uint32_t chunk = uint32_t(std::max<size_t>(1, std::min<size_t>(
+      n_units, (size_t(1) << 30) / unit_bytes)));
+  uint16_t *tK = nullptr, *tV = nullptr;
+  CKV_CUDA_TRY(cudaMallocAsync(&tK, chunk * unit_bytes, st));
+  CKV_CUDA_TRY(cudaMallocAsync(&tV, chunk * unit_bytes, st));
+  int rc = CKV_OK;
+  for (uint32_t u0 = 0; u0 < n_units && rc == CKV_OK; u0 += chunk) {
+    const uint32_t nu = std::min(chunk, n_units - u0);
+    const size_t off = size_t(u0) * p_cap * D;
+    dim3 g((n_rows + 7) / 8, nu);
+    k_relayout<<<g, 128, 0, st>>>(K + off, V + off, tK, tV, sorted_ids + size_t(u0) * p_cap,
+                                  p_cap, sink, labeled_end, n_rows);
+    if (cudaGetLastError() != cudaSuccess) { rc = cuda_status(cudaErrorLaunchFailure, "k_relayout"); break; }
+    ctx->launches++;
+    for (int kv = 0; kv < 2 && rc == CKV_OK; ++kv) {
+      cudaError_t e = cudaMemcpy2DAsync(kv ? K2 + off : V2 + off, unit_bytes, kv ? tK : tV,
+                                        unit_bytes, size_t(n_rows) * D * 2, nu,
+                                        cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) rc = cuda_status(e, "ckv_relayout_kv copy-back");
+    }
+  }
+  cudaFreeAsync(tK, st);
+  cudaFreeAsync(tV, st);
+  return rc;
 }
 
 int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q, const uint16_t* K,
@@ -701,23 +734,9 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
   // relay the KV store cluster-major: row sink + j <- position sorted[j]
   const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
   const uint32_t N = s->labeled_end - sink;
-  if (N > 0) {
-    uint16_t *K2 = nullptr, *V2 = nullptr;
-    const size_t kv = size_t(s->U) * s->p_cap * D;
-    CKV_TRY(salloc(&K2, kv));
-    int rc = salloc(&V2, kv);
-    if (rc) { cudaFree(K2); return rc; }
-    dim3 g((s->p_cap + 7) / 8, s->U);
-    k_relayout<<<g, 128, 0, s->ctx->stream>>>(s->K, s->V, K2, V2, s->sorted, s->p_cap, sink,
-                                              s->labeled_end, s->n_ctx);
-    CKV_LAUNCH_CHECK("k_relayout");
-    s->ctx->launches++;
-    CKV_CUDA_TRY(cudaStreamSynchronize(s->ctx->stream));
-    cudaFree(s->K);
-    cudaFree(s->V);
-    s->K = K2;
-    s->V = V2;
-  }
+  if (N > 0)  // in place (bounded staging), so the store is never held twice
+    CKV_TRY(ckv_relayout_kv(s->ctx, s->U, s->p_cap, s->K, s->V, s->K, s->V, s->sorted, sink,
+                            s->labeled_end, s->n_ctx));
   s->prefilled = true;
   return ckv_ctx_sync(s->ctx);
 }

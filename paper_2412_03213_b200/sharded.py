@@ -110,7 +110,8 @@ class DeviceShard:
     """ShardSteps on the B200 kernels (ckv_kmshard.cu) through the C-ABI.
 
     keys: device int16/bf16-bits tensor [n_units, n_local, 128] (this rank's
-    contiguous position shard of every unit).
+    contiguous position shard of every unit); rows must be contiguous, the
+    unit stride is free, so it may be a view into the rank's KV store.
     """
 
     def __init__(self, keys: torch.Tensor, C_: int, ctx=None, exact_only: bool = False):
@@ -118,7 +119,9 @@ class DeviceShard:
         if not keys.is_cuda:
             raise ValueError("DeviceShard: keys must be a CUDA tensor (no CPU fallback)")
         self.ctx = ctx or Context.default()
-        self.keys = keys.contiguous()
+        if keys.stride(2) != 1 or keys.stride(1) != D:
+            keys = keys.contiguous()
+        self.keys = keys
         U, n, d = self.keys.shape
         if d != D:
             raise ValidationError(N.CKV_EINVAL, "head dim must be 128")
@@ -128,7 +131,8 @@ class DeviceShard:
         self.counts = torch.zeros((U, C_), dtype=torch.int32, device=dev)
         self.stat = torch.zeros((U, 4), dtype=torch.int32, device=dev)
         self.objective = torch.zeros((U,), dtype=torch.float64, device=dev)
-        desc = N.KmShardDesc(U, n, C_, N.CKV_KM_EXACT_ONLY if exact_only else 0, n * D)
+        desc = N.KmShardDesc(U, n, C_, N.CKV_KM_EXACT_ONLY if exact_only else 0,
+                             self.keys.stride(0))
         bufs = N.KmShardBufs(self.sums.data_ptr(), self.counts.data_ptr(),
                              self.stat.data_ptr(), self.objective.data_ptr())
         h = C.c_void_p()
@@ -343,40 +347,41 @@ class ShardedDecoder:
     (out, lse) -> ckv_attend_merge.  Every rank returns the same output.
     """
 
-    def __init__(self, km: ShardedKMeansResult, K_shard: torch.Tensor, V_shard: torch.Tensor,
-                 group: int, budget: int, comm: Comm | None = None, sink_K=None, sink_V=None,
-                 rec_K=None, rec_V=None, rec_pos: int = 0, sink_tokens: int = 16, ctx=None):
+    def __init__(self, km: ShardedKMeansResult, K_store: torch.Tensor, V_store: torch.Tensor,
+                 group: int, budget: int, comm: Comm | None = None, sink_rows: int = 0,
+                 n_rec: int = 0, rec_pos: int = 0, sink_tokens: int = 16, ctx=None):
+        """K_store / V_store: device bf16-bits [U][p_cap][128] in position
+        order — rows [0, sink_rows) the sinks this rank holds, then its
+        n_local shard rows, then n_rec recency rows.  Re-laid cluster-major IN
+        PLACE (the decoder keeps them)."""
         from .api import Context
         self.ctx = ctx or Context.default()
         self.comm = comm or Comm()
-        dev = K_shard.device
+        dev = K_store.device
         U, n_local = km.labels.shape
         self.U, self.G, self.n_q, self.C, self.B = U, group, U * group, km.n_clusters, budget
-        self.sink_rows = 0 if sink_K is None else int(sink_K.shape[1])
-        self.n_rec = 0 if rec_K is None else int(rec_K.shape[1])
-        self.rec_pos = rec_pos
-        n_rows = self.sink_rows + n_local + self.n_rec
-        self.p_cap = n_rows
-        i16 = torch.int16
-        parts_k = [t for t in (sink_K, K_shard, rec_K) if t is not None]
-        parts_v = [t for t in (sink_V, V_shard, rec_V) if t is not None]
-        Kp = torch.cat([t.to(dev, i16) for t in parts_k], 1).contiguous()
-        Vp = torch.cat([t.to(dev, i16) for t in parts_v], 1).contiguous()
-        labels = torch.full((U, n_rows), -1, dtype=torch.int32, device=dev)
-        labels[:, self.sink_rows:self.sink_rows + n_local] = km.labels.to(dev)
+        self.sink_rows, self.n_rec, self.rec_pos = sink_rows, n_rec, rec_pos
+        n_rows = sink_rows + n_local + n_rec
+        if K_store.shape != V_store.shape or K_store.shape[0] != U or K_store.shape[1] < n_rows \
+                or not K_store.is_contiguous() or not V_store.is_contiguous():
+            raise ValueError("ShardedDecoder: K/V store must be contiguous [U][>= rows][128]")
+        self.p_cap = int(K_store.shape[1])
+        labels = torch.full((U, self.p_cap), -1, dtype=torch.int32, device=dev)
+        labels[:, sink_rows:sink_rows + n_local] = km.labels.to(dev)
         C_ = self.C
         ncl = torch.full((U,), C_, dtype=torch.int32, device=dev)
         self.lsize = torch.zeros((U, C_), dtype=torch.int32, device=dev)
         self.lstart = torch.zeros((U, C_ + 1), dtype=torch.int32, device=dev)
-        self.lsorted = torch.zeros((U, n_rows), dtype=torch.int32, device=dev)
-        check(lib().ckv_build_index(self.ctx.h, U, n_rows, n_rows, C_, labels.data_ptr(),
+        self.lsorted = torch.zeros((U, self.p_cap), dtype=torch.int32, device=dev)
+        check(lib().ckv_build_index(self.ctx.h, U, n_rows, self.p_cap, C_, labels.data_ptr(),
                                     ncl.data_ptr(), self.lsize.data_ptr(),
                                     self.lstart.data_ptr(), self.lsorted.data_ptr()))
-        self.K = torch.empty_like(Kp)
-        self.V = torch.empty_like(Vp)
-        check(lib().ckv_relayout_kv(self.ctx.h, U, n_rows, Kp.data_ptr(), Vp.data_ptr(),
-                                    self.K.data_ptr(), self.V.data_ptr(), self.lsorted.data_ptr(),
-                                    self.sink_rows, self.sink_rows + n_local, n_rows))
+        del labels
+        self.K, self.V = K_store, V_store
+        check(lib().ckv_relayout_kv(self.ctx.h, U, self.p_cap, self.K.data_ptr(),
+                                    self.V.data_ptr(), self.K.data_ptr(), self.V.data_ptr(),
+                                    self.lsorted.data_ptr(), sink_rows, sink_rows + n_local,
+                                    n_rows))
         # global sizes and the members on lower-ranked shards, once per prefill
         per_rank = [t.to(dev) for t in self.comm.all_gather(self.lsize)]
         self.gsize = torch.stack(per_rank).sum(0).to(torch.int32).contiguous()
@@ -402,10 +407,10 @@ class ShardedDecoder:
         self.out_loc = torch.zeros((nq, D), dtype=torch.float32, device=dev)
         self.lse = torch.zeros((nq,), dtype=torch.float32, device=dev)
         self.sdesc = N.ShardSelectDesc(nq, group, budget, C_, C_, self.slice, self.comm.world,
-                                       n_rows, self.sel_cap, self.sink_rows, self.sink_rows,
+                                       self.p_cap, self.sel_cap, self.sink_rows, self.sink_rows,
                                        self.sink_rows + n_local, rec_pos, self.n_rec,
                                        self.pos_base, 0)
-        self.adesc = N.AttendDesc(nq, group, n_rows, self.sel_cap, self.sel_cap)
+        self.adesc = N.AttendDesc(nq, group, self.p_cap, self.sel_cap, self.sel_cap)
 
     def step(self, q: torch.Tensor, want_ids: bool = False, want_weights: bool = False,
              full_rank: bool = False) -> dict:

@@ -48,13 +48,17 @@ def decode_rank(rank, world, K, V, Q, Kr, Vr, C_, seeds, G, budget, device):
     lo, hi = shard_range(n, world, rank)
     dev = torch.device("cuda", device)
     t = lambda x: torch.from_numpy(bf16_bits(x).view(np.int16)).to(dev)
-    kb = t(K[:, 16 + lo:16 + hi])
-    km = kmeans_cosine_sharded(DeviceShard(kb, C_, ctx=ctx), n, lo, seeds=seeds, comm=comm)
-    dec = ShardedDecoder(km, kb, t(V[:, 16 + lo:16 + hi]), G, budget, comm,
-                         sink_K=t(K[:, :16]) if rank == 0 else None,
-                         sink_V=t(V[:, :16]) if rank == 0 else None,
-                         rec_K=t(Kr) if rank == world - 1 and Kr.shape[1] else None,
-                         rec_V=t(Vr) if rank == world - 1 and Vr.shape[1] else None,
+    # the rank's KV store in position order: sinks (rank 0), shard, recency
+    # (last rank); the k-means reads its shard rows in place
+    sink_rows = 16 if rank == 0 else 0
+    n_rec = Kr.shape[1] if rank == world - 1 else 0
+    Ks = np.concatenate([K[:, :sink_rows], K[:, 16 + lo:16 + hi], Kr[:, :n_rec]], 1)
+    Vs = np.concatenate([V[:, :sink_rows], V[:, 16 + lo:16 + hi], Vr[:, :n_rec]], 1)
+    Kst, Vst = t(Ks).contiguous(), t(Vs).contiguous()
+    shard = DeviceShard(Kst[:, sink_rows:sink_rows + hi - lo], C_, ctx=ctx)
+    km = kmeans_cosine_sharded(shard, n, lo, seeds=seeds, comm=comm)
+    del shard
+    dec = ShardedDecoder(km, Kst, Vst, G, budget, comm, sink_rows=sink_rows, n_rec=n_rec,
                          rec_pos=L, ctx=ctx)
     r = dec.step(torch.from_numpy(Q).to(dev), want_ids=True, want_weights=True, full_rank=True)
     ctx.sync()
