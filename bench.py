@@ -270,6 +270,281 @@ def run_reference(args, rank, world):
 
 
 # --------------------------------------------------------------------------
+# secondary workloads (BASELINE.json configs[2..4]); the headline is config B
+# --------------------------------------------------------------------------
+def _events(torch, n):
+    return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+
+
+def _max_over_ranks(torch, dev, world, vals):
+    if world == 1:
+        return vals
+    import torch.distributed as dist
+    t = torch.tensor(vals, device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def unique_kv_rows(torch, run_row, run_off, run_cnt, group, p_cap):
+    """Unique (kv unit, store row) pairs read by one attention launch, from
+    the I_T run lists: the q heads of a GQA group share their unit's rows
+    through L2, so unique rows (not the per-head sum) are the algorithmic
+    bytes."""
+    n_q, run_cap = run_row.shape
+    live = torch.arange(run_cap, device=run_row.device)[None] < run_cnt.to(torch.int64)[:, None]
+    lens = ((run_off[:, 1:] - run_off[:, :-1]).to(torch.int64) * live).flatten()
+    total = int(lens.sum().item())
+    if total == 0:
+        return 0, 0
+    rid = torch.repeat_interleave(torch.arange(n_q * run_cap, device=run_row.device), lens)
+    first = torch.repeat_interleave(torch.cumsum(lens, 0) - lens, lens)
+    rows = run_row.flatten().to(torch.int64)[rid] + (torch.arange(total, device=rid.device) - first)
+    key = (rid // run_cap // group) * p_cap + rows
+    return int(torch.unique(key).numel()), total
+
+
+def run_config_D(torch, dev, ctx, args):
+    """configs[3]: 32k prompt + 4096 generated tokens, decode-batch clustering
+    every 320 steps (harness.hpp:325-333), cluster cache R = 1 and 2.  Every
+    step goes through ckv_session_step (select + attend + append + the
+    clustering event when due); per-step CUDA events split event steps from
+    the rest."""
+    from paper_2412_03213_b200.api import ClusterConfig
+    from paper_2412_03213_b200.session import Session
+    U, G, L, B, T = args.layers * args.kv_heads, args.group, args.L, args.budget, args.gen_tokens
+    g, centers = gen_inputs(torch, dev, U, G, L, T, seed=11)
+    q_all, kn_all, vn_all = gen_decode(torch, dev, g, centers, G, T)
+    out = torch.empty((U * G, D), dtype=torch.float32, device=dev)
+    res = {"workload": f"config D: {args.layers} layers x {args.kv_heads} kv x {G} q heads, "
+                       f"{L} prompt + {T} generated, B={B}, decode-batch clustering every 320 steps",
+           "tokens": T}
+    for R in (1, 2):
+        sess = Session(U, G, L, T, B, retention=R, cfg=ClusterConfig(), kv_heads=args.kv_heads,
+                       ctx=ctx)
+        gk = torch.Generator(device=dev)
+        gk.manual_seed(12)
+        fill_kv(torch, dev, gk, centers, sess.K, sess.V, L)
+        sess.prefill()
+        ev = _events(torch, T + 1)
+        ev[0].record()
+        for t in range(T):
+            sess.step(q_all[t], kn_all[t], vn_all[t], out)
+            ev[t + 1].record()
+        torch.cuda.synchronize()
+        ms = np.array([ev[t].elapsed_time(ev[t + 1]) for t in range(T)])
+        st = sess.stats()
+        m = 320
+        ev_steps = np.array([(t + 1) % m == 0 for t in range(T)])
+        ctr = sess.cache_counters().astype(np.float64)
+        res[f"R{R}"] = {
+            "hit_rate": float(ctr[:, 1].sum() / max(1.0, ctr[:, 0].sum())),
+            "miss_tokens_per_q_head_step": float(ctr[:, 2].sum() / (U * G * T)),
+            "step_us_mean": float(ms.mean() * 1e3),
+            "step_us_plain": float(ms[~ev_steps].mean() * 1e3),
+            "step_us_event": float(ms[ev_steps].mean() * 1e3) if ev_steps.any() else None,
+            "clustering_events": int(ev_steps.sum()),
+            "clustering_us_per_event": float((ms[ev_steps].mean() - ms[~ev_steps].mean()) * 1e3)
+            if ev_steps.any() else None,
+            "amortised_overhead_us_per_step": float((ms.sum() - ms[~ev_steps].mean() * T) / T * 1e3),
+            "labeled_end": int(st.labeled_end), "n_ctx": int(st.n_ctx),
+            "tokens_per_s": float(1000.0 / ms.mean()),
+        }
+        del sess
+        torch.cuda.synchronize()
+    del q_all, kn_all, vn_all
+    return res
+
+
+def run_config_C(args, rank, world, torch, dev, ctx, hbm):
+    """configs[2]: Llama-3-8B shape, 32k context, B = 2048, global batch 32,
+    batch-sharded over the ranks (strong scaling: 32 / world sequences each).
+    Decode steps through ckv_session_step on HBM-resident inputs."""
+    from paper_2412_03213_b200.api import ClusterConfig
+    from paper_2412_03213_b200.session import Session
+    batch_total = 32
+    if batch_total % world:
+        raise SystemExit("config C needs world | 32")
+    batch = batch_total // world
+    G, L, B = 4, args.L, 2048
+    U = batch * args.layers * args.kv_heads
+    T = args.warmup + args.steps + 2
+    sess = Session(U, G, L, T, B, retention=1, cfg=ClusterConfig(), kv_heads=args.kv_heads,
+                   ctx=ctx)
+    g, centers = gen_inputs(torch, dev, U, G, L, T, seed=7 + rank)
+    fill_kv(torch, dev, g, centers, sess.K, sess.V, L)
+    q_all, kn_all, vn_all = gen_decode(torch, dev, g, centers, G, T)
+    torch.cuda.synchronize()
+    e = _events(torch, 2)
+    e[0].record()
+    info = sess.prefill()
+    e[1].record()
+    torch.cuda.synchronize()
+    prefill_ms = e[0].elapsed_time(e[1])
+    out = torch.empty((U * G, D), dtype=torch.float32, device=dev)
+    t = 0
+    for _ in range(args.warmup):
+        sess.step(q_all[t], kn_all[t], vn_all[t], out)
+        t += 1
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    with ClockSampler(int(str(dev).split(":")[-1])) as clk:
+        e[0].record()
+        for _ in range(args.steps):
+            sess.step(q_all[t], kn_all[t], vn_all[t], out)
+            t += 1
+        e[1].record()
+        torch.cuda.synchronize()
+    step_ms = e[0].elapsed_time(e[1]) / args.steps
+    st = sess.state()
+    ntok = int(st["n_tokens"].to(torch.int64).sum().item())
+    ncl = int(st["n_clusters"].to(torch.int64).sum().item())
+    # the last step's selection as runs (one untimed select) -> unique rows
+    from paper_2412_03213_b200 import _native as N
+    n_q, c_cap, sel_cap = U * G, st["c_cap"], st["sel_cap"]
+    stats = sess.stats()
+    sd = N.SelectDesc(n_q, G, B, 16, sess.p_cap, c_cap, sel_cap, stats.labeled_end, stats.n_ctx,
+                      0, 16)
+    ptrs = [C.c_void_p() for _ in range(8)]
+    cc, scap = C.c_uint32(), C.c_uint32()
+    N.lib().ckv_session_state(sess.h, *[C.byref(p) for p in ptrs], C.byref(cc), C.byref(scap))
+    rr = torch.zeros((n_q, c_cap + 2), dtype=torch.int32, device=dev)
+    ro = torch.zeros((n_q, c_cap + 3), dtype=torch.int32, device=dev)
+    rc_ = torch.zeros(n_q, dtype=torch.int32, device=dev)
+    runs = N.Runs(rr.data_ptr(), ro.data_ptr(), rc_.data_ptr(), c_cap + 2)
+    tmp = [torch.zeros(n_q, dtype=torch.int32, device=dev) for _ in range(3)]
+    rk = torch.zeros((n_q, c_cap), dtype=torch.int32, device=dev)
+    N.check(N.lib().ckv_select(ctx.h, C.byref(sd), q_all[t - 1].data_ptr(), ptrs[0], ptrs[2],
+                               ptrs[3], ptrs[4], ptrs[5], None, None, C.byref(runs),
+                               tmp[0].data_ptr(), tmp[1].data_ptr(), tmp[2].data_ptr(),
+                               rk.data_ptr(), None, None))
+    uniq, _ = unique_kv_rows(torch, rr, ro, rc_, G, sess.p_cap)
+    n_runs = int(rc_.sum().item())
+    step_bytes = uniq * D * 2 * 2 + ncl * D * 4 + ncl * 8 + n_runs * 8 + U * G * D * 8
+    step_bytes_nodd = ntok * D * 2 * 2 + ncl * D * 4 + ncl * 8 + n_runs * 8 + U * G * D * 8
+    step_ms, prefill_ms = _max_over_ranks(torch, dev, world, [step_ms, prefill_ms])
+    gbs = step_bytes / (step_ms * 1e-3) / 1e9
+    return {"metric": "decode tokens/s (select+gather+attend, 32k ctx, B=2048, batch 32)",
+            "value": batch_total * 1000.0 / step_ms, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16 KV, f32/f64 math",
+            "data": "synthetic (device draw with trace.hpp generator distributions, bf16)",
+            "config": {"workload": f"config C: Llama-3-8B shape, {args.layers} layers x "
+                                   f"{args.kv_heads} kv x {G} q heads, {L} ctx, B={B}, "
+                                   f"batch {batch_total} ({batch} per GPU), R=1",
+                       "global_batch": batch_total, "seq_len": L,
+                       "parallelism": f"batch-sharded x{world}",
+                       "l2": f"per-step working set ~{step_bytes / 1e9:.0f} GB >> L2"},
+            "step_roofline": {"achieved_gbs": gbs, "frac": gbs / hbm,
+                              "bytes_per_step": step_bytes,
+                              "bytes_rule": "unique (kv unit, row) K+V rows + f32 centroids + "
+                                            "sizes/starts + runs + q/out",
+                              "bytes_per_step_no_dedupe": step_bytes_nodd},
+            "prefill": {"ms": prefill_ms, "units": U,
+                        "iters_max": max(i for i, _ in info)},
+            "clocks": clk.summary()}
+
+
+def run_config_E(args, rank, world, torch, dev, ctx, hbm):
+    """configs[4]: Llama-3-70B shape (80 layers x 8 kv x 8 q heads), 128k
+    context, B = 2048, one sequence SEQUENCE-sharded over the ranks
+    (paper_2412_03213_b200/sharded.py): sharded k-means with all-reduced f64
+    centroid sums, then decode steps with centroid-sharded scoring, an
+    all-gather of the scores for the global top-k, local sparse attention
+    and an LSE merge.  Timing: prefill = the whole sharded k-means; a step =
+    ShardedDecoder.step (score + all-gather + select + attend + merge) at a
+    fixed context (no append)."""
+    from paper_2412_03213_b200.sharded import (Comm, DeviceShard, ShardedDecoder,
+                                               kmeans_cosine_sharded, shard_range)
+    layers, kvh, G, L, B = 80, 8, 8, args.L_E, 2048
+    U = layers * kvh
+    N = L - 16
+    lo, hi = shard_range(N, world, rank)
+    sink_rows = 16 if rank == 0 else 0
+    rows = sink_rows + hi - lo
+    comm = Comm()
+    K = torch.empty((U, rows, D), dtype=torch.int16, device=dev)
+    V = torch.empty_like(K)
+    g, centers = gen_inputs(torch, dev, U, G, L, 0, seed=7)  # centres shared by all ranks
+    g.manual_seed(100 + rank)
+    fill_kv(torch, dev, g, centers, K, V, rows)
+    C0 = int(N_lib().ckv_prefill_cluster_count(L, 80, 16, 0))
+    seeds = [int(N_lib().ckv_mix_seed(0, u // kvh, u % kvh)) for u in range(U)]
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e = _events(torch, 2)
+    e[0].record()
+    shard = DeviceShard(K[:, sink_rows:], C0, ctx=ctx)
+    km = kmeans_cosine_sharded(shard, N, lo, seeds=seeds, comm=comm)
+    e[1].record()
+    torch.cuda.synchronize()
+    prefill_ms = e[0].elapsed_time(e[1])
+    del shard
+    dec = ShardedDecoder(km, K, V, G, B, comm, sink_rows=sink_rows, ctx=ctx)
+    T = args.warmup + args.steps
+    ar = torch.arange(U, device=dev)
+    qs = []
+    for _ in range(T):
+        c = centers[ar.repeat_interleave(G), torch.randint(0, centers.shape[1], (U * G,),
+                                                            device=dev, generator=g)]
+        qq = c + 0.15 * torch.randn(U * G, D, device=dev, generator=g)
+        qs.append((2.0 * math.sqrt(D) * qq / qq.norm(dim=-1, keepdim=True))
+                  .to(torch.bfloat16).float().contiguous())
+    for t in range(args.warmup):
+        dec.step(qs[t])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(int(str(dev).split(":")[-1])) as clk:
+        e[0].record()
+        for t in range(args.warmup, T):
+            dec.step(qs[t])
+        e[1].record()
+        torch.cuda.synchronize()
+    step_ms = e[0].elapsed_time(e[1]) / args.steps
+    ntok = int(dec.n_tokens.to(torch.int64).sum().item())
+    uniq, _ = unique_kv_rows(torch, dec.run_row, dec.run_off, dec.run_cnt, G, dec.p_cap)
+    n_runs = int(dec.run_cnt.sum().item())
+    # this rank's bytes: unique KV rows + its centroid slice + the gathered
+    # f64 scores + global sizes / prefix / local index + runs + q / out
+    rest = U * dec.slice * D * 4 + U * G * C0 * 8 + U * C0 * 4 * 4 + n_runs * 8 + U * G * D * 8
+    step_bytes = uniq * D * 2 * 2 + rest
+    step_bytes_nodd = ntok * D * 2 * 2 + rest
+    iters = km.iterations_used
+    passes = int(sum(int(i) + 1 for i in iters))
+    flops = 2.0 * (hi - lo) * C0 * D * passes
+    step_ms, prefill_ms = _max_over_ranks(torch, dev, world, [step_ms, prefill_ms])
+    gbs = step_bytes / (step_ms * 1e-3) / 1e9
+    return {"metric": "decode select+attend us/step (70B shape, 128k ctx, B=2048, "
+                      "sequence-sharded)",
+            "value": step_ms * 1e3, "unit": "us/step", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16 KV, f32/f64 math",
+            "data": "synthetic (device draw with trace.hpp generator distributions, bf16)",
+            "config": {"workload": f"config E: Llama-3-70B shape, {layers} layers x {kvh} kv x "
+                                   f"{G} q heads, {L} ctx, B={B}, one sequence "
+                                   f"sequence-sharded x{world}",
+                       "global_batch": 1, "seq_len": L, "parallelism": f"sequence-sharded x{world}"},
+            "tokens_per_s": 1000.0 / step_ms,
+            "step_roofline_rank0": {"achieved_gbs": gbs, "frac": gbs / hbm,
+                                    "bytes_per_step": step_bytes,
+                                    "bytes_per_step_no_dedupe": step_bytes_nodd},
+            "prefill": {"ms": prefill_ms, "units": U, "C0": C0, "iters_min": int(min(iters)),
+                        "iters_max": int(max(iters)), "passes": passes,
+                        "assign_tflops_rank0": flops / (prefill_ms * 1e-3) / 1e12},
+            "clocks": clk.summary()}
+
+
+def N_lib():
+    from paper_2412_03213_b200 import _native as N
+    return N.lib()
+
+
+# --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
 def main():
@@ -286,6 +561,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exact-kmeans", action="store_true")
+    ap.add_argument("--config", default="B", choices=["B", "C", "D", "E"],
+                    help="B = the headline (configs[1], plus a config D block); C / D / E "
+                         "print their own line")
+    ap.add_argument("--gen-tokens", type=int, default=4096, help="config D generated tokens")
+    ap.add_argument("--L-E", type=int, default=131072, help="config E context")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config D block")
     ap.add_argument("--max-iters", type=int, default=50,
                     help="k-means cap (profiling only; the bench default is the reference's 50)")
     args = ap.parse_args()
@@ -307,6 +588,19 @@ def main():
     from paper_2412_03213_b200.session import Session
 
     hbm, bf16_peak, bf16_sus, peak_kind = peaks()
+    if args.config in ("C", "E", "D"):
+        ctx = Context(local)
+        if args.config == "D":
+            line = run_config_D(torch, dev, ctx, args) if rank == 0 else None
+        elif args.config == "C":
+            line = run_config_C(args, rank, world, torch, dev, ctx, hbm)
+        else:
+            line = run_config_E(args, rank, world, torch, dev, ctx, hbm)
+        if rank == 0:
+            print(json.dumps(line))
+        if world > 1:
+            dist.destroy_process_group()
+        return
     U = args.layers * args.kv_heads
     G, L, B = args.group, args.L, args.budget
     T = args.warmup + args.steps + args.e2e_steps + 2
@@ -552,6 +846,10 @@ def main():
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
+    if not args.no_extra and world == 1:
+        del sess
+        torch.cuda.synchronize()
+        line["config_D"] = run_config_D(torch, dev, ctx, args)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

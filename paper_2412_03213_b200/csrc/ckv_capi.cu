@@ -346,8 +346,36 @@ int ckv_cluster_decode_batch(ckv_ctx* ctx, const ckv_decode_cluster_desc* d,
   int32_t* tmp_l = nullptr;
   CKV_CUDA_TRY(cudaMallocAsync(&d_init, init.size() * 4, st));
   CKV_CUDA_TRY(cudaMallocAsync(&tmp_c, size_t(U) * C * D * 4, st));
-  CKV_CUDA_TRY(cudaMallocAsync(&tmp_l, size_t(U) * rows * 4, st));
+  CKV_CUDA_TRY(cudaMallocAsync(&tmp_l, size_t(U) * std::max(rows, 2u) * 4, st));
   CKV_CUDA_TRY(cudaMemcpyAsync(d_init, init.data(), init.size() * 4, cudaMemcpyHostToDevice, st));
+  if (kmeans_small_supported(rows, C)) {
+    // the whole k-means of every unit's batch in one launch (ckv_kmeans.cu)
+    uint32_t* d_it = reinterpret_cast<uint32_t*>(tmp_l);  // scratch reuse: [U] + [U]
+    int32_t* d_st = tmp_l + U;
+    int rc = launch_kmeans_small(st, keys + size_t(d->pos0) * D, uint64_t(d->p_cap) * D, U,
+                                 rows, C, d->max_iters, d_init, centroids, d->c_cap,
+                                 labels + d->pos0, d->p_cap, n_clusters, d_it, d_st);
+    ctx->launches++;
+    std::vector<int32_t> hb(2 * size_t(U));
+    if (rc == CKV_OK) {
+      cudaError_t e = cudaMemcpyAsync(hb.data(), tmp_l, 8 * size_t(U), cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = cuda_status(e, "cluster_decode_batch");
+    }
+    cudaFreeAsync(d_init, st);
+    cudaFreeAsync(tmp_c, st);
+    cudaFreeAsync(tmp_l, st);
+    if (rc) return rc;
+    for (uint32_t u = 0; u < U; ++u) {
+      if (hb[U + u] == 1) { set_error("kmeans: keys must be finite"); return CKV_EINVAL; }
+      if (hb[U + u] == 2) {
+        set_error("kmeans: degenerate input, all keys zero-norm");
+        return CKV_EINVAL;
+      }
+      if (iterations_host) iterations_host[u] = uint32_t(hb[u]) & 0x7fffffffu;
+    }
+    return CKV_OK;
+  }
   KMeansArgs a;
   a.n_units = U;
   a.n = rows;

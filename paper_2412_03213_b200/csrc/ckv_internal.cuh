@@ -55,6 +55,13 @@ int launch_objective(cudaStream_t st, const uint16_t* keys, uint64_t key_stride,
                      uint32_t label_stride, const float* cents, const double* cnorm, double* obj,
                      const int32_t* active);
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C);
+// cluster_decode_batch's k-means in one launch (rows <= 512, C <= 32)
+bool kmeans_small_supported(uint32_t rows, uint32_t C);
+int launch_kmeans_small(cudaStream_t st, const uint16_t* keys, uint64_t key_stride,
+                        uint32_t n_units, uint32_t rows, uint32_t C, uint32_t max_iters,
+                        const uint32_t* init_rows, float* cents, uint32_t c_cap,
+                        int32_t* labels, uint32_t label_stride, uint32_t* n_clusters,
+                        uint32_t* iters, int32_t* status);
 float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n);
 bool assign_tc_supported(uint32_t n, uint32_t C);
 

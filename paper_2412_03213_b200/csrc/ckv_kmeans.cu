@@ -691,3 +691,218 @@ int launch_objective(cudaStream_t st, const uint16_t* keys, uint64_t key_stride,
 }
 
 }  // namespace ckvb
+
+// ---------------------------------------------------------------------------
+// K4 fused: cluster_decode_batch's whole kmeans_cosine (clustering.hpp:160-263
+// on one decode batch, 310-332) in ONE launch, one CTA per unit, everything
+// in shared memory: no per-iteration host round trip (the generic driver
+// above pays ~2 launches + a sync per pass, ~3.5 ms per event at config D).
+// Same numerics as the generic path, so the same bits: normalize() and
+// float(sum / count) through finish_centroid, exact sequential f64
+// assignment with strict '>', f64 member sums in position order, the
+// reference's repair, convergence on label equality after repair.
+// ---------------------------------------------------------------------------
+namespace ckvb {
+
+constexpr int KS_THREADS = 256;
+constexpr uint32_t KS_MAX_ROWS = 512;
+constexpr uint32_t KS_MAX_C = 32;
+
+__global__ void __launch_bounds__(KS_THREADS)
+k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t rows,
+               uint32_t C, uint32_t max_iters, const uint32_t* __restrict__ init_rows,
+               float* __restrict__ out_cents, uint32_t c_cap, int32_t* __restrict__ out_labels,
+               uint32_t label_stride, uint32_t* __restrict__ n_clusters,
+               uint32_t* __restrict__ iters_out, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char ks_raw[];
+  const uint32_t u = blockIdx.x;
+  const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+  double* cnorm = reinterpret_cast<double*>(ks_raw);                   // [C]
+  float* cent = reinterpret_cast<float*>(cnorm + KS_MAX_C);             // [C][D]
+  float* dir = cent + KS_MAX_C * D;                                     // [C][D]
+  uint16_t* dbf = reinterpret_cast<uint16_t*>(dir + KS_MAX_C * D);      // [C][D] (unused)
+  float* deps = reinterpret_cast<float*>(dbf + KS_MAX_C * D);           // [C]  (unused)
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(deps + KS_MAX_C);         // [C]
+  int32_t* lab0 = reinterpret_cast<int32_t*>(cnt + KS_MAX_C);           // [rows]
+  int32_t* lab1 = lab0 + KS_MAX_ROWS;                                   // [rows]
+  uint16_t* kt = reinterpret_cast<uint16_t*>(lab1 + KS_MAX_ROWS);       // [D][rows] transposed
+  __shared__ int s_flag, s_bad;
+  __shared__ uint32_t s_largest, s_lcnt, s_victim;
+  __shared__ double s_wd[KS_THREADS / 32];
+  __shared__ uint32_t s_wi[KS_THREADS / 32];
+  const uint16_t* kb = keys + u * key_stride;
+
+  // stage the batch transposed (thread t reads rows t, t+256: conflict-free)
+  // and run kmeans_cosine's input checks (clustering.hpp:166-172)
+  if (tid == 0) { s_flag = 0; s_bad = 0; }
+  __syncthreads();
+  int bad = 0, nonzero = 0;
+  for (uint32_t e = tid; e < rows * D; e += KS_THREADS) {
+    const uint32_t r = e / D, j = e % D;
+    const uint16_t b = kb[size_t(r) * D + j];
+    kt[j * rows + r] = b;
+    if ((b & 0x7f80u) == 0x7f80u) bad = 1;
+  }
+  __syncthreads();
+  for (uint32_t r = tid; r < rows; r += KS_THREADS) {
+    double s = 0.0;
+    for (int j = 0; j < D; ++j) {
+      const double x = double(bf16_to_f32(kt[j * rows + r]));
+      s = __fma_rn(x, x, s);
+    }
+    if (sqrt(s) >= 1e-12) nonzero = 1;
+  }
+  bad = __syncthreads_or(bad);
+  nonzero = __syncthreads_or(nonzero);
+  if (bad || !nonzero) {
+    if (tid == 0) status[u] = bad ? 1 : 2;
+    return;
+  }
+  // init: centroid c = key row init_rows[c]; dirs = normalize (count 1)
+  for (uint32_t c = wid; c < C; c += KS_THREADS / 32) {
+    const uint32_t r = init_rows[size_t(u) * C + c];
+    double x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = double(bf16_to_f32(kt[(4 * lane + k) * rows + r]));
+    finish_centroid(x[0], x[1], x[2], x[3], 1.0, cent + c * D, dir + c * D, dbf + c * D,
+                    cnorm + c, deps + c);
+  }
+  __syncthreads();
+
+  int32_t* lab[2] = {lab0, lab1};
+  uint32_t it = 0;
+  int converged = 0;
+  for (uint32_t t = 0;; ++t) {
+    int32_t* cur = lab[t & 1];
+    const int32_t* prev = lab[(t & 1) ^ 1];
+    // assign (AssignScorer::assign): sequential f64 chain per (key, c), strict '>'
+    for (uint32_t r = tid; r < rows; r += KS_THREADS) {
+      uint32_t best = 0;
+      double bs = -INFINITY;
+      for (uint32_t c = 0; c < C; ++c) {
+        const float* dc = dir + c * D;
+        double s = 0.0;
+#pragma unroll 16
+        for (int j = 0; j < D; ++j) s = __fma_rn(double(bf16_to_f32(kt[j * rows + r])), double(dc[j]), s);
+        if (s > bs) { bs = s; best = c; }
+      }
+      cur[r] = int32_t(best);
+    }
+    if (tid < int(C)) cnt[tid] = 0;
+    __syncthreads();
+    for (uint32_t r = tid; r < rows; r += KS_THREADS) atomicAdd(&cnt[cur[r]], 1u);
+    __syncthreads();
+    // repair_empty_clusters (clustering.hpp:128-153), sequential over ids
+    for (uint32_t c = 0; c < C; ++c) {
+      if (cnt[c] > 0) continue;  // uniform: cnt is shared and stable here
+      if (tid == 0) {
+        uint32_t l = 0;
+        for (uint32_t k = 1; k < C; ++k) if (cnt[k] > cnt[l]) l = k;
+        s_largest = l;
+        s_lcnt = cnt[l];
+      }
+      __syncthreads();
+      const uint32_t largest = s_largest;
+      if (s_lcnt > 1) {
+        double bd = -1.0;
+        uint32_t bv = 0xffffffffu;
+        for (uint32_t r = tid; r < rows; r += KS_THREADS) {
+          if (uint32_t(cur[r]) != largest) continue;
+          double na = 0.0, dd = 0.0;
+          for (int j = 0; j < D; ++j) {
+            const double x = double(bf16_to_f32(kt[j * rows + r]));
+            na = __fma_rn(x, x, na);
+            dd = __fma_rn(x, double(cent[largest * D + j]), dd);
+          }
+          na = sqrt(na);
+          const double nb = cnorm[largest];
+          double dist = 1.0;
+          if (!(na < 1e-12 || nb < 1e-12)) {
+            dist = 1.0 - dd / (na * nb);
+            dist = dist < 0.0 ? 0.0 : (dist > 2.0 ? 2.0 : dist);
+          }
+          if (dist > bd) { bd = dist; bv = r; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const uint32_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          if (od > bd || (od == bd && ov < bv)) { bd = od; bv = ov; }
+        }
+        if (lane == 0) { s_wd[wid] = bd; s_wi[wid] = bv; }
+        __syncthreads();
+        if (tid == 0) {
+          double b = s_wd[0];
+          uint32_t v = s_wi[0];
+          for (int w = 1; w < KS_THREADS / 32; ++w)
+            if (s_wd[w] > b || (s_wd[w] == b && s_wi[w] < v)) { b = s_wd[w]; v = s_wi[w]; }
+          s_victim = v == 0xffffffffu ? 0u : v;  // no member beat -1: victim stays 0
+          cur[s_victim] = int32_t(c);
+          cnt[largest]--;
+          cnt[c]++;
+        }
+      }
+      __syncthreads();
+    }
+    // convergence: next == labels (after repair)
+    if (t > 0) {
+      int ch = 0;
+      for (uint32_t r = tid; r < rows; r += KS_THREADS) ch |= cur[r] != prev[r];
+      ch = __syncthreads_or(ch);
+      if (!ch) { converged = 1; it = t; break; }
+      if (t == max_iters) { it = t; break; }
+    }
+    // update_centroids from `cur` (clustering.hpp:205-218): per (c, 4 dims)
+    // a lane, members in position order, then the next directions
+    for (uint32_t c = wid; c < C; c += KS_THREADS / 32) {
+      double a[4] = {0.0, 0.0, 0.0, 0.0};
+      for (uint32_t r = 0; r < rows; ++r) {
+        if (uint32_t(cur[r]) != c) continue;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] += double(bf16_to_f32(kt[(4 * lane + k) * rows + r]));
+      }
+      finish_centroid(a[0], a[1], a[2], a[3], double(cnt[c]), cent + c * D, dir + c * D,
+                      dbf + c * D, cnorm + c, deps + c);
+    }
+    __syncthreads();
+  }
+  // final labels = the last assignment (equal to the previous one when
+  // converged); append (cluster_decode_batch: fresh ids from n_clusters)
+  const int32_t* fin = lab[it & 1];
+  const uint32_t base = n_clusters[u];
+  for (uint32_t e = tid; e < C * D; e += KS_THREADS)
+    out_cents[(size_t(u) * c_cap + base) * D + e] = cent[e];
+  for (uint32_t r = tid; r < rows; r += KS_THREADS)
+    out_labels[size_t(u) * label_stride + r] = fin[r] + int32_t(base);
+  __syncthreads();
+  if (tid == 0) {
+    n_clusters[u] = base + C;
+    iters_out[u] = it | (converged ? 0x80000000u : 0u);
+    status[u] = 0;
+  }
+}
+
+bool kmeans_small_supported(uint32_t rows, uint32_t C) {
+  return rows >= 1 && rows <= KS_MAX_ROWS && C >= 1 && C <= KS_MAX_C;
+}
+
+int launch_kmeans_small(cudaStream_t st, const uint16_t* keys, uint64_t key_stride,
+                        uint32_t n_units, uint32_t rows, uint32_t C, uint32_t max_iters,
+                        const uint32_t* init_rows, float* cents, uint32_t c_cap,
+                        int32_t* labels, uint32_t label_stride, uint32_t* n_clusters,
+                        uint32_t* iters, int32_t* status) {
+  const size_t smem = KS_MAX_C * 8 + 2 * KS_MAX_C * D * 4 + KS_MAX_C * D * 2 + KS_MAX_C * 4 +
+                      KS_MAX_C * 4 + 2 * KS_MAX_ROWS * 4 + size_t(D) * rows * 2;
+  static bool attr = false;
+  if (!attr) {
+    CKV_CUDA_TRY(cudaFuncSetAttribute(k_kmeans_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+    attr = true;
+  }
+  k_kmeans_small<<<n_units, KS_THREADS, smem, st>>>(keys, key_stride, rows, C, max_iters,
+                                                     init_rows, cents, c_cap, labels,
+                                                     label_stride, n_clusters, iters, status);
+  CKV_LAUNCH_CHECK("k_kmeans_small");
+  return CKV_OK;
+}
+
+}  // namespace ckvb
