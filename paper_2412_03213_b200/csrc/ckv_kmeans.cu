@@ -717,15 +717,17 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
   extern __shared__ __align__(16) unsigned char ks_raw[];
   const uint32_t u = blockIdx.x;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+  // layout sized by (C, rows) so two CTAs fit an SM at the decode-batch shape
+  const uint32_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u;
   double* cnorm = reinterpret_cast<double*>(ks_raw);                   // [C]
-  float* cent = reinterpret_cast<float*>(cnorm + KS_MAX_C);             // [C][D]
-  float* dir = cent + KS_MAX_C * D;                                     // [C][D]
-  uint16_t* dbf = reinterpret_cast<uint16_t*>(dir + KS_MAX_C * D);      // [C][D] (unused)
-  float* deps = reinterpret_cast<float*>(dbf + KS_MAX_C * D);           // [C]  (unused)
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(deps + KS_MAX_C);         // [C]
-  int32_t* lab0 = reinterpret_cast<int32_t*>(cnt + KS_MAX_C);           // [rows]
-  int32_t* lab1 = lab0 + KS_MAX_ROWS;                                   // [rows]
-  uint16_t* kt = reinterpret_cast<uint16_t*>(lab1 + KS_MAX_ROWS);       // [D][rows] transposed
+  float* cent = reinterpret_cast<float*>(cnorm + C4);                   // [C][D]
+  float* dir = cent + C4 * D;                                           // [C][D]
+  uint16_t* dbf = reinterpret_cast<uint16_t*>(dir + C4 * D);            // [C][D] (unused)
+  float* deps = reinterpret_cast<float*>(dbf + C4 * D);                 // [C]  (unused)
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(deps + C4);               // [C]
+  int32_t* lab0 = reinterpret_cast<int32_t*>(cnt + C4);                 // [rows]
+  int32_t* lab1 = lab0 + R2;                                            // [rows]
+  uint16_t* kt = reinterpret_cast<uint16_t*>(lab1 + R2);                // [D][rows] transposed
   __shared__ int s_flag, s_bad;
   __shared__ uint32_t s_largest, s_lcnt, s_victim;
   __shared__ double s_wd[KS_THREADS / 32];
@@ -775,16 +777,23 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
   for (uint32_t t = 0;; ++t) {
     int32_t* cur = lab[t & 1];
     const int32_t* prev = lab[(t & 1) ^ 1];
-    // assign (AssignScorer::assign): sequential f64 chain per (key, c), strict '>'
+    // assign (AssignScorer::assign): a sequential f64 chain per (key, c),
+    // four clusters' chains interleaved for ILP; strict '>' in id order
     for (uint32_t r = tid; r < rows; r += KS_THREADS) {
       uint32_t best = 0;
       double bs = -INFINITY;
-      for (uint32_t c = 0; c < C; ++c) {
-        const float* dc = dir + c * D;
-        double s = 0.0;
-#pragma unroll 16
-        for (int j = 0; j < D; ++j) s = __fma_rn(double(bf16_to_f32(kt[j * rows + r])), double(dc[j]), s);
-        if (s > bs) { bs = s; best = c; }
+      for (uint32_t c0 = 0; c0 < C; c0 += 4) {
+        const float* d0 = dir + c0 * D;  // c0 + k < C4: padded rows are never read past
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+        for (int j = 0; j < D; ++j) {
+          const double x = double(bf16_to_f32(kt[j * rows + r]));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) s[k] = __fma_rn(x, double(d0[k * D + j]), s[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (c0 + k < C && s[k] > bs) { bs = s[k]; best = c0 + k; }
       }
       cur[r] = int32_t(best);
     }
@@ -890,8 +899,9 @@ int launch_kmeans_small(cudaStream_t st, const uint16_t* keys, uint64_t key_stri
                         const uint32_t* init_rows, float* cents, uint32_t c_cap,
                         int32_t* labels, uint32_t label_stride, uint32_t* n_clusters,
                         uint32_t* iters, int32_t* status) {
-  const size_t smem = KS_MAX_C * 8 + 2 * KS_MAX_C * D * 4 + KS_MAX_C * D * 2 + KS_MAX_C * 4 +
-                      KS_MAX_C * 4 + 2 * KS_MAX_ROWS * 4 + size_t(D) * rows * 2;
+  const size_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u;
+  const size_t smem = C4 * 8 + 2 * C4 * D * 4 + C4 * D * 2 + C4 * 4 + C4 * 4 + 2 * R2 * 4 +
+                      size_t(D) * rows * 2;
   static bool attr = false;
   if (!attr) {
     CKV_CUDA_TRY(cudaFuncSetAttribute(k_kmeans_small, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -37,33 +37,91 @@ __device__ __forceinline__ bool before(unsigned long long ka, uint32_t ia, unsig
   return ka > kb || (ka == kb && ia < ib);
 }
 
-// blockIdx.x = unit, blockIdx.y = a tile of SR_ROWS centroid rows; thread
-// pairs (row, head) stride over the tile's SR_ROWS x G scores
-constexpr int SR_ROWS = 64;
+// blockIdx.x = unit, blockIdx.y = a tile of SR_ROWS centroid rows.  A thread
+// owns one centroid row and runs the G heads' sequential f64 chains side by
+// side (G independent FMA chains hide the f64 latency; one 16-B smem load of
+// the row feeds 4G FMAs, the query quads are broadcasts).
+constexpr int SR_ROWS = 128;
+constexpr int SR_LD = D + 4;  // row stride in floats: 16-B aligned rows
 template <int G>
-__global__ void __launch_bounds__(SR_THREADS)
+__global__ void __launch_bounds__(SR_ROWS)
 k_score_range(const float* __restrict__ q, const float* __restrict__ cents, uint32_t c_cap,
               uint32_t C, uint32_t c_lo, uint32_t c_hi, uint32_t slice,
               double* __restrict__ scores) {
-  __shared__ float crow[SR_ROWS][D + 1];  // +1: lanes read one column of 32 rows
-  __shared__ float qs[G][D];
+  extern __shared__ __align__(16) float sr_sm[];
+  float* crow = sr_sm;                  // [SR_ROWS][SR_LD]
+  float* qs = sr_sm + SR_ROWS * SR_LD;  // [G][D]
   const uint32_t u = blockIdx.x;
   const uint32_t t0 = c_lo + blockIdx.y * SR_ROWS;
   const uint32_t hi = min(c_hi, C);
   if (t0 >= hi) return;
   const uint32_t nrow = min(uint32_t(SR_ROWS), hi - t0);
-  const float* cu = cents + (size_t(u) * c_cap + t0) * D;
-  for (uint32_t e = threadIdx.x; e < nrow * D; e += SR_THREADS) crow[e / D][e % D] = __ldg(cu + e);
-  for (uint32_t e = threadIdx.x; e < G * D; e += SR_THREADS)
-    qs[e / D][e % D] = __ldg(q + size_t(u) * G * D + e);
+  const float4* cu = reinterpret_cast<const float4*>(cents + (size_t(u) * c_cap + t0) * D);
+  for (uint32_t e = threadIdx.x; e < nrow * (D / 4); e += SR_ROWS)
+    *reinterpret_cast<float4*>(crow + (e / (D / 4)) * SR_LD + 4 * (e % (D / 4))) = __ldg(cu + e);
+  const float4* qu = reinterpret_cast<const float4*>(q + size_t(u) * G * D);
+  for (uint32_t e = threadIdx.x; e < G * D / 4; e += SR_ROWS)
+    reinterpret_cast<float4*>(qs)[e] = __ldg(qu + e);
   __syncthreads();
-  for (uint32_t p = threadIdx.x; p < uint32_t(SR_ROWS * G); p += SR_THREADS) {
-    const uint32_t r = p % SR_ROWS, g = p / SR_ROWS;
-    if (r >= nrow) continue;
-    double s = 0.0;
-#pragma unroll 16
-    for (int j = 0; j < D; ++j) s = __fma_rn(double(qs[g][j]), double(crow[r][j]), s);
-    scores[(size_t(u) * G + g) * slice + (t0 + r - c_lo)] = s;
+  const uint32_t r = threadIdx.x;
+  if (r >= nrow) return;
+  double s[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) s[g] = 0.0;
+  const float* row = crow + r * SR_LD;
+#pragma unroll 2
+  for (int j = 0; j < D; j += 4) {
+    const float4 m = *reinterpret_cast<const float4*>(row + j);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float4 x = *reinterpret_cast<const float4*>(qs + g * D + j);
+      s[g] = __fma_rn(double(x.x), double(m.x), s[g]);
+      s[g] = __fma_rn(double(x.y), double(m.y), s[g]);
+      s[g] = __fma_rn(double(x.z), double(m.z), s[g]);
+      s[g] = __fma_rn(double(x.w), double(m.w), s[g]);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) scores[(size_t(u) * G + g) * slice + (t0 + r - c_lo)] = s[g];
+}
+
+// block-wide inclusive scan of one u32 per thread (SR_THREADS threads)
+__device__ __forceinline__ uint32_t block_incl_scan(uint32_t x, uint32_t* wsum,
+                                                    uint32_t* total = nullptr) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  uint32_t pre = 0, tot = 0;
+  for (int w = 0; w < SR_THREADS / 32; ++w) {
+    if (w < wid) pre += wsum[w];
+    tot += wsum[w];
+  }
+  __syncthreads();
+  if (total) *total = tot;
+  return x + pre;
+}
+
+// block bitonic sort of key[0..n2) / id[0..n2) by before() (n2 a power of 2)
+__device__ __forceinline__ void block_sort(unsigned long long* key, uint32_t* id, uint32_t n2) {
+  for (uint32_t k = 2; k <= n2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < n2; i += SR_THREADS) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long ka = key[i], kb = key[ixj];
+          const uint32_t ia = id[i], ib = id[ixj];
+          const bool asc = (i & k) == 0;
+          const bool swap = asc ? before(kb, ib, ka, ia) : before(ka, ia, kb, ib);
+          if (swap) { key[i] = kb; key[ixj] = ka; id[i] = ib; id[ixj] = ia; }
+        }
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -80,64 +138,112 @@ k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__
   uint32_t* id = reinterpret_cast<uint32_t*>(key + p2);                     // [p2]
   uint32_t* incl = id + p2;                                                 // [p2]
   uint32_t* loc = incl + p2;                                                // [p2 + 1]
-  __shared__ uint32_t s_taken, s_wsum[SR_THREADS / 32];
+  uint32_t* sz = loc + p2 + 1;                                              // [p2]
+  uint32_t* tid2 = sz + p2;                                                 // [p2]
+  unsigned long long* tk = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(tid2 + p2) + 7) & ~uintptr_t(7));        // [p2]
+  __shared__ uint32_t s_taken, s_wsum[SR_THREADS / 32], s_hist[256], s_n, s_bin, s_above;
   const uint32_t h = blockIdx.x, unit = h / d.group;
   const uint32_t C = d.C, B = d.budget;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t* gs = gsize + size_t(unit) * d.c_cap;
   // gathered scores: cluster c lives in rank c / slice at offset c % slice
+  uint32_t tot = 0;
   for (uint32_t c = tid; c < p2; c += SR_THREADS) {
     if (c < C) {
       const uint32_t r = c / d.slice, o = c % d.slice;
       key[c] = rank_key_s(scores[(size_t(r) * d.n_q + h) * d.slice + o]);
       id[c] = c;
+      sz[c] = __ldg(gs + c);
+      tot += sz[c];
     } else {
       key[c] = 0ull;
       id[c] = 0xffffffffu;  // padding sorts after every real cluster
+      sz[c] = 0u;
     }
   }
+  tot = __reduce_add_sync(0xffffffffu, tot);
+  if ((tid & 31) == 0) s_wsum[tid >> 5] = tot;
   __syncthreads();
-  // block bitonic sort, descending by (key, -id)
-  for (uint32_t k = 2; k <= p2; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = tid; i < p2; i += SR_THREADS) {
-        const uint32_t ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long ka = key[i], kb = key[ixj];
-          const uint32_t ia = id[i], ib = id[ixj];
-          const bool asc = (i & k) == 0;
-          const bool swap = asc ? before(kb, ib, ka, ia) : before(ka, ia, kb, ib);
-          if (swap) { key[i] = kb; key[ixj] = ka; id[i] = ib; id[ixj] = ia; }
-        }
-      }
+  tot = 0;
+  for (int w = 0; w < SR_THREADS / 32; ++w) tot += s_wsum[w];
+  __syncthreads();
+  uint32_t n_sorted = C;
+  if (!(d.flags & CKV_SEL_FULL_RANK) && B > 0 && tot >= B) {
+    // ---- size-weighted radix select on the 64-bit rank keys: tau with
+    // W(key > tau) < B <= W(key >= tau); only the clusters ranked at or above
+    // the cutoff need sorting (~B / mean size of them, not all C)
+    unsigned long long prefix_k = 0ull;
+    uint32_t above = 0;
+    for (int pass = 0; pass < 8; ++pass) {
+      const int sh = 56 - 8 * pass;
+      s_hist[tid] = 0u;  // SR_THREADS == 256 bins
+      __syncthreads();
+      const unsigned long long hm = pass == 0 ? 0ull : (~0ull << (sh + 8));
+      for (uint32_t c = tid; c < C; c += SR_THREADS)
+        if (((key[c] ^ prefix_k) & hm) == 0ull && sz[c])
+          atomicAdd(&s_hist[(key[c] >> sh) & 255u], sz[c]);
+      __syncthreads();
+      // bins from high to low: thread t holds bin 255 - t
+      const uint32_t v = s_hist[255 - tid];
+      const uint32_t inc = block_incl_scan(v, s_wsum);
+      if (above + inc >= B && above + inc - v < B) { s_bin = 255 - tid; s_above = above + inc - v; }
+      __syncthreads();
+      prefix_k |= (unsigned long long)s_bin << sh;
+      above = s_above;
       __syncthreads();
     }
+    // T = {key > tau} plus the ties at tau, in id order, until the budget
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    for (uint32_t c = tid; c < C; c += SR_THREADS) {
+      if (key[c] > prefix_k) {
+        const uint32_t slot = atomicAdd(&s_n, 1u);
+        tk[slot] = key[c];
+        tid2[slot] = c;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // ties at tau, ascending id (ids ascend with c): the reference's walk
+      // takes them while cum < B (selection.hpp:90-104)
+      uint32_t cum = above, n = s_n;
+      for (uint32_t c = 0; c < C && cum < B; ++c) {
+        if (key[c] != prefix_k) continue;
+        tk[n] = key[c];
+        tid2[n] = c;
+        ++n;
+        cum += sz[c];
+      }
+      s_n = n;
+    }
+    __syncthreads();
+    n_sorted = s_n;
+    uint32_t n2 = 32;
+    while (n2 < n_sorted) n2 <<= 1;
+    for (uint32_t i = tid; i < n2; i += SR_THREADS) {
+      const bool v2 = i < n_sorted;
+      key[i] = v2 ? tk[i] : 0ull;
+      id[i] = v2 ? tid2[i] : 0xffffffffu;
+    }
+    __syncthreads();
+    block_sort(key, id, n2);
+  } else {
+    block_sort(key, id, p2);
   }
   // inclusive prefix of the global sizes in rank order (chunks of 256)
-  const uint32_t* gs = gsize + size_t(unit) * d.c_cap;
-  if (tid == 0) s_taken = B == 0 ? 0u : C;  // the reference breaks at cum >= B
+  if (tid == 0) s_taken = B == 0 ? 0u : n_sorted;  // the reference breaks at cum >= B
   uint32_t carry = 0;
-  for (uint32_t b = 0; b < C; b += SR_THREADS) {
+  for (uint32_t b = 0; b < n_sorted; b += SR_THREADS) {
     const uint32_t i = b + tid;
-    uint32_t x = i < C ? __ldg(gs + id[i]) : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_wsum[wid] = x;
-    __syncthreads();
-    uint32_t wpre = 0;
-    for (int w = 0; w < wid; ++w) wpre += s_wsum[w];
-    x += wpre + carry;
-    if (i < C) incl[i] = x;
-    uint32_t tot = 0;
-    for (int w = 0; w < SR_THREADS / 32; ++w) tot += s_wsum[w];
-    __syncthreads();
-    carry += tot;
+    uint32_t chunk_tot;
+    const uint32_t x = block_incl_scan(i < n_sorted ? __ldg(gs + id[i]) : 0u, s_wsum, &chunk_tot);
+    if (i < n_sorted) incl[i] = x + carry;
+    carry += chunk_tot;
   }
   __syncthreads();
   // taken = first i with incl[i] >= B, plus one (all of C when the total < B)
-  for (uint32_t i = tid; i < C; i += SR_THREADS)
+  for (uint32_t i = tid; i < n_sorted; i += SR_THREADS)
     if (B > 0 && incl[i] >= B && (i == 0 || incl[i - 1] < B)) s_taken = i + 1;
   __syncthreads();
   const uint32_t taken = s_taken;
@@ -257,9 +363,17 @@ int ckv_score_range(ckv_ctx* ctx, uint32_t n_units, uint32_t group, const float*
 #define CKV_SR(GG)                                                                           \
   case GG: {                                                                                 \
     dim3 grid(n_units, (slice + SR_ROWS - 1) / SR_ROWS);                                     \
-    k_score_range<GG><<<grid, SR_THREADS, 0, st>>>(q, centroids, c_cap, C, c_lo, c_hi, slice, \
-                                                   scores);                                  \
+    const size_t sm = (SR_ROWS * SR_LD + GG * D) * 4;                                        \
+    k_score_range<GG><<<grid, SR_ROWS, sm, st>>>(q, centroids, c_cap, C, c_lo, c_hi, slice,   \
+                                                 scores);                                    \
     break;                                                                                   \
+  }
+  static bool attr = false;
+  if (!attr) {
+    for (auto fn : {k_score_range<1>, k_score_range<2>, k_score_range<4>, k_score_range<8>})
+      CKV_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (SR_ROWS * SR_LD + 8 * D) * 4));
+    attr = true;
   }
   switch (group) {
     CKV_SR(1) CKV_SR(2) CKV_SR(4) CKV_SR(8)
@@ -290,11 +404,11 @@ int ckv_select_scored(ckv_ctx* ctx, const ckv_shard_select_desc* d, const double
   if (d->n_q == 0) return CKV_OK;
   uint32_t p2 = 32;
   while (p2 < d->C) p2 <<= 1;
-  const size_t smem = size_t(p2) * 8 + size_t(p2) * 4 * 2 + (size_t(p2) + 1) * 4;
+  const size_t smem = size_t(p2) * 8 * 2 + size_t(p2) * 4 * 5 + 4 + 8;
   static int attr = 0;
   if (!attr) {
     CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_scored, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      96 * 1024));
+                                      200 * 1024));
     attr = 1;
   }
   k_select_scored<<<d->n_q, SR_THREADS, smem, ctx->stream>>>(

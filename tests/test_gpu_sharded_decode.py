@@ -30,9 +30,10 @@ def _assemble(res, key, h, n_taken):
     return np.concatenate(parts)
 
 
-@pytest.mark.parametrize("world,L,budget", [(1, 1040, 256), (2, 1040, 256), (3, 2064, 300),
-                                            (2, 2064, 5000)])
-def test_gpu_sharded_decode_matches_reference(gpu_ctx, world, L, budget):
+@pytest.mark.parametrize("world,L,budget,full_rank", [
+    (1, 1040, 256, True), (2, 1040, 256, True), (3, 2064, 300, True), (2, 2064, 5000, True),
+    (1, 1040, 256, False), (2, 2064, 300, False), (3, 4112, 1000, False), (2, 2064, 5000, False)])
+def test_gpu_sharded_decode_matches_reference(gpu_ctx, world, L, budget, full_rank):
     from oracle.oracle import ClusterConfig as OCfg
     G, U, n_rec = 2, 2, 5
     hs = [head(9, 0, u, L, T=64) for u in range(U)]
@@ -44,7 +45,7 @@ def test_gpu_sharded_decode_matches_reference(gpu_ctx, world, L, budget):
     seeds = [port().mix_seed(0, 0, u) for u in range(U)]
     C0 = port().prefill_cluster_count(L, OCfg())
     res = run_world(world, "tests._sharded_workers", "decode_rank", K, V, Q, Kr, Vr, C0, seeds,
-                    G, budget, 0)
+                    G, budget, 0, full_rank)
     for u in range(U):
         o = port().cluster_prefill(K[u], OCfg(seed=seeds[u]))
         assert all(int(r["iters"][u]) == o.iterations_used for r in res)
@@ -57,7 +58,8 @@ def test_gpu_sharded_decode_matches_reference(gpu_ctx, world, L, budget):
             for r in res:
                 assert int(r["n_taken"][h]) == sel.n_clusters_taken
                 assert int(r["trimmed"][h]) == sel.trimmed_from_last
-                assert np.array_equal(r["ranked"][h][:C0], sel.ranked_clusters)
+                nr = C0 if full_rank else sel.n_clusters_taken
+                assert np.array_equal(r["ranked"][h][:nr], sel.ranked_clusters[:nr])
             ids = _assemble(res, "ids", h, sel.n_clusters_taken)
             assert np.array_equal(ids, sel.token_ids), f"I_T differs for q head {h}"
             oo, ow = port().approx_attention(Q[h], Kall, Vall, sel.token_ids)
