@@ -718,7 +718,9 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
   const uint32_t u = blockIdx.x;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
   // layout sized by (C, rows) so two CTAs fit an SM at the decode-batch shape
-  const uint32_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u;
+  // kt row stride RS = 1 (mod 16) u16: the update's lanes (4 dims apart)
+  // then hit 16 distinct banks instead of one
+  const uint32_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u, RS = ((rows + 15) & ~15u) + 1;
   double* cnorm = reinterpret_cast<double*>(ks_raw);                   // [C]
   float* cent = reinterpret_cast<float*>(cnorm + C4);                   // [C][D]
   float* dir = cent + C4 * D;                                           // [C][D]
@@ -742,14 +744,14 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
   for (uint32_t e = tid; e < rows * D; e += KS_THREADS) {
     const uint32_t r = e / D, j = e % D;
     const uint16_t b = kb[size_t(r) * D + j];
-    kt[j * rows + r] = b;
+    kt[j * RS + r] = b;
     if ((b & 0x7f80u) == 0x7f80u) bad = 1;
   }
   __syncthreads();
   for (uint32_t r = tid; r < rows; r += KS_THREADS) {
     double s = 0.0;
     for (int j = 0; j < D; ++j) {
-      const double x = double(bf16_to_f32(kt[j * rows + r]));
+      const double x = double(bf16_to_f32(kt[j * RS + r]));
       s = __fma_rn(x, x, s);
     }
     if (sqrt(s) >= 1e-12) nonzero = 1;
@@ -765,7 +767,7 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
     const uint32_t r = init_rows[size_t(u) * C + c];
     double x[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) x[k] = double(bf16_to_f32(kt[(4 * lane + k) * rows + r]));
+    for (int k = 0; k < 4; ++k) x[k] = double(bf16_to_f32(kt[(4 * lane + k) * RS + r]));
     finish_centroid(x[0], x[1], x[2], x[3], 1.0, cent + c * D, dir + c * D, dbf + c * D,
                     cnorm + c, deps + c);
   }
@@ -787,7 +789,7 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
         double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 8
         for (int j = 0; j < D; ++j) {
-          const double x = double(bf16_to_f32(kt[j * rows + r]));
+          const double x = double(bf16_to_f32(kt[j * RS + r]));
 #pragma unroll
           for (int k = 0; k < 4; ++k) s[k] = __fma_rn(x, double(d0[k * D + j]), s[k]);
         }
@@ -819,7 +821,7 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
           if (uint32_t(cur[r]) != largest) continue;
           double na = 0.0, dd = 0.0;
           for (int j = 0; j < D; ++j) {
-            const double x = double(bf16_to_f32(kt[j * rows + r]));
+            const double x = double(bf16_to_f32(kt[j * RS + r]));
             na = __fma_rn(x, x, na);
             dd = __fma_rn(x, double(cent[largest * D + j]), dd);
           }
@@ -867,7 +869,7 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
       for (uint32_t r = 0; r < rows; ++r) {
         if (uint32_t(cur[r]) != c) continue;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] += double(bf16_to_f32(kt[(4 * lane + k) * rows + r]));
+        for (int k = 0; k < 4; ++k) a[k] += double(bf16_to_f32(kt[(4 * lane + k) * RS + r]));
       }
       finish_centroid(a[0], a[1], a[2], a[3], double(cnt[c]), cent + c * D, dir + c * D,
                       dbf + c * D, cnorm + c, deps + c);
@@ -899,9 +901,9 @@ int launch_kmeans_small(cudaStream_t st, const uint16_t* keys, uint64_t key_stri
                         const uint32_t* init_rows, float* cents, uint32_t c_cap,
                         int32_t* labels, uint32_t label_stride, uint32_t* n_clusters,
                         uint32_t* iters, int32_t* status) {
-  const size_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u;
+  const size_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u, RS = ((rows + 15) & ~15u) + 1;
   const size_t smem = C4 * 8 + 2 * C4 * D * 4 + C4 * D * 2 + C4 * 4 + C4 * 4 + 2 * R2 * 4 +
-                      size_t(D) * rows * 2;
+                      size_t(D) * RS * 2;
   static bool attr = false;
   if (!attr) {
     CKV_CUDA_TRY(cudaFuncSetAttribute(k_kmeans_small, cudaFuncAttributeMaxDynamicSharedMemorySize,

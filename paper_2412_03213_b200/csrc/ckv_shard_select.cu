@@ -180,9 +180,16 @@ k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__
       s_hist[tid] = 0u;  // SR_THREADS == 256 bins
       __syncthreads();
       const unsigned long long hm = pass == 0 ? 0ull : (~0ull << (sh + 8));
-      for (uint32_t c = tid; c < C; c += SR_THREADS)
-        if (((key[c] ^ prefix_k) & hm) == 0ull && sz[c])
-          atomicAdd(&s_hist[(key[c] >> sh) & 255u], sz[c]);
+      // warp-aggregated: the scores share their high bytes, so most lanes hit
+      // the same bin; one smem atomic per distinct bin per warp
+      for (uint32_t c0 = tid - lane; c0 < C; c0 += SR_THREADS) {
+        const uint32_t c = c0 + lane;
+        const bool in = c < C && sz[c] && ((key[c] ^ prefix_k) & hm) == 0ull;
+        const uint32_t bin = in ? uint32_t(key[c] >> sh) & 255u : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        const uint32_t w = __reduce_add_sync(peers, in ? sz[c] : 0u);
+        if (in && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], w);
+      }
       __syncthreads();
       // bins from high to low: thread t holds bin 255 - t
       const uint32_t v = s_hist[255 - tid];
@@ -194,22 +201,36 @@ k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__
       __syncthreads();
     }
     // T = {key > tau} plus the ties at tau, in id order, until the budget
-    if (tid == 0) s_n = 0;
+    __shared__ uint32_t s_nt;
+    if (tid == 0) { s_n = 0; s_nt = 0; }
     __syncthreads();
     for (uint32_t c = tid; c < C; c += SR_THREADS) {
       if (key[c] > prefix_k) {
         const uint32_t slot = atomicAdd(&s_n, 1u);
         tk[slot] = key[c];
         tid2[slot] = c;
+      } else if (key[c] == prefix_k) {
+        loc[atomicAdd(&s_nt, 1u)] = c;  // the ties at tau (usually one)
       }
     }
     __syncthreads();
+    const uint32_t nt = s_nt;
+    if (nt > 1) {  // ascending id: rank by counting (incl[] is free scratch here)
+      for (uint32_t i = tid; i < nt; i += SR_THREADS) {
+        const uint32_t ci = loc[i];
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < nt; ++j) r += loc[j] < ci;
+        incl[r] = ci;
+      }
+      __syncthreads();
+      for (uint32_t i = tid; i < nt; i += SR_THREADS) loc[i] = incl[i];
+      __syncthreads();
+    }
     if (tid == 0) {
-      // ties at tau, ascending id (ids ascend with c): the reference's walk
-      // takes them while cum < B (selection.hpp:90-104)
+      // the reference's walk takes the ties while cum < B (selection.hpp:90-104)
       uint32_t cum = above, n = s_n;
-      for (uint32_t c = 0; c < C && cum < B; ++c) {
-        if (key[c] != prefix_k) continue;
+      for (uint32_t i = 0; i < nt && cum < B; ++i) {
+        const uint32_t c = loc[i];
         tk[n] = key[c];
         tid2[n] = c;
         ++n;
