@@ -303,6 +303,23 @@ def unique_kv_rows(torch, run_row, run_off, run_cnt, group, p_cap):
     return int(torch.unique(key).numel()), total
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes of one launch of `kernel` from the newest committed ncu
+    --set full summary (tools/profile_summary.py); None if absent."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_decode_kernels.json")))
+    if not files:
+        return None
+    try:
+        d = json.load(open(files[-1]))
+        for k, v in d.items():
+            if k.startswith(kernel) and v.get("dram_traffic_bytes"):
+                return float(v["dram_traffic_bytes"])
+    except Exception:
+        return None
+    return None
+
+
 def run_config_D(torch, dev, ctx, args):
     """configs[3]: 32k prompt + 4096 generated tokens, decode-batch clustering
     every 320 steps (harness.hpp:325-333), cluster cache R = 1 and 2.  Every
@@ -822,7 +839,10 @@ def main():
                    "l2": "per-step working set ~0.6 GB >> 126 MB L2 (no flush needed)"},
         "select_attend_us_per_step": step_ms * 1e3,
         "roofline": {"bound": "hbm", "kernel": "k_attend", "achieved": att_gbs, "peak": hbm,
-                     "unit": "GB/s", "frac": att_gbs / hbm, "traffic": None,
+                     "unit": "GB/s", "frac": att_gbs / hbm, "traffic": ncu_traffic("k_attend"),
+                     "traffic_source": "ncu --set full dram__bytes_read.sum + "
+                                       "dram__bytes_write.sum of one k_attend launch of this "
+                                       "workload, newest profiles/r*_decode_kernels.json",
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": attend_bytes_unique,
                      "bytes_rule": "unique (kv unit, row) K+V bf16 rows + I_T runs + q/out",
