@@ -9,7 +9,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libckv_b200.so")
+# CKV_LIB: load an experiment build instead (tools/build_variant.py); the
+# product build is libckv_b200.so next to this file
+LIB_PATH = os.environ.get("CKV_LIB") or os.path.join(_HERE, "libckv_b200.so")
 
 CKV_OK, CKV_EINVAL, CKV_ECUDA, CKV_ENOMEM, CKV_ENCCL = 0, 1, 2, 3, 4
 CKV_KM_OBJECTIVE, CKV_KM_EXACT_ONLY, CKV_KM_NO_VALIDATE = 1, 2, 4

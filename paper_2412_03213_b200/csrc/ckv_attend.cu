@@ -6,7 +6,7 @@
 //   work item  = (q head h, slice s): I_T entries [nt*s/S, nt*(s+1)/S).
 //   producer   = warp 4, one elected lane.  For each item it stages the q
 //                head's run list (I_T as runs of consecutive KV-store rows,
-//                ckv_select) in smem, then for each 32-row tile waits for a
+//                ckv_select) in smem, then for each 64-row tile waits for a
 //                free ring stage and issues one TMA bulk copy
 //                (cp.async.bulk ... mbarrier::complete_tx) per contiguous run
 //                segment for K and for V; the stage's mbarrier completes when
@@ -29,8 +29,15 @@ namespace ckvb {
 
 constexpr int AT_CWARPS = 4;                      // consumer warps
 constexpr int AT_THREADS = (AT_CWARPS + 1) * 32;  // + producer warp
-constexpr int AT_TILE = 32;                       // rows per stage
-constexpr int AT_STAGES = 4;
+#ifndef CKV_AT_TILE
+#define CKV_AT_TILE 64
+#endif
+#ifndef CKV_AT_STAGES
+#define CKV_AT_STAGES 2
+#endif
+constexpr int AT_TILE = CKV_AT_TILE;              // rows per stage (multiple of 8)
+constexpr int AT_STAGES = CKV_AT_STAGES;
+constexpr int AT_RPH = AT_TILE / 8;               // rows per half-warp per tile
 constexpr int AT_RUNS = 256;                      // runs staged in smem
 constexpr int PART = 2 + D;                       // partial: m (log2 domain), l, acc[128]
 
@@ -107,8 +114,8 @@ __device__ __forceinline__ void axpy8(float p, const uint4 v, float* acc) {
 }
 
 struct __align__(128) AttSmem {
-  uint4 k[AT_STAGES][AT_TILE][16];  // 8 KB per stage
-  uint4 v[AT_STAGES][AT_TILE][16];  // 8 KB per stage
+  uint4 k[AT_STAGES][AT_TILE][16];  // AT_TILE x 256 B per stage
+  uint4 v[AT_STAGES][AT_TILE][16];
   float q[2][D];                    // query ring
   uint64_t full[AT_STAGES], empty[AT_STAGES], qfull[2], qempty[2];
   uint32_t roff[AT_RUNS + 1], rrow[AT_RUNS];  // producer: runs of the current item
@@ -248,10 +255,10 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
     for (uint32_t e = it.e0; e < it.e1; e += AT_TILE) {
       mbar_wait(&sm.full[st], ph);
       const bool full_tile = e + AT_TILE <= it.e1;
-      float s[4];
-      uint4 vv[4];
+      float s[AT_RPH];
+      uint4 vv[AT_RPH];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < AT_RPH; ++kk) {
         const int r = hw + 8 * kk;
         const uint4 kr = sm.k[st][r][hl];
         vv[kk] = sm.v[st][r][hl];
@@ -268,14 +275,16 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       if (full_tile) {
         if (WEIGHTS && hl == 0)
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) lw[e + hw + 8 * kk] = s[kk];
-        const float mn = fmaxf(fmaxf(m, fmaxf(s[0], s[1])), fmaxf(s[2], s[3]));
+          for (int kk = 0; kk < AT_RPH; ++kk) lw[e + hw + 8 * kk] = s[kk];
+        float mn = m;
+#pragma unroll
+        for (int kk = 0; kk < AT_RPH; ++kk) mn = fmaxf(mn, s[kk]);
         const float sc = ex2(m - mn);  // m = -inf -> 0
         l *= sc;
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] *= sc;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
+        for (int kk = 0; kk < AT_RPH; ++kk) {
           const float p = ex2(s[kk] - mn);
           l += p;
           axpy8(p, vv[kk], acc);
@@ -284,7 +293,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       } else {  // the slice's last, partial tile: rows past its end hold stale data
         float tmax = -INFINITY;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
+        for (int kk = 0; kk < AT_RPH; ++kk) {
           const bool ok = e + hw + 8 * kk < it.e1;
           if (WEIGHTS && ok && hl == 0) lw[e + hw + 8 * kk] = s[kk];
           s[kk] = ok ? s[kk] : -INFINITY;
@@ -297,7 +306,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] *= sc;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
+          for (int kk = 0; kk < AT_RPH; ++kk) {
             if (s[kk] != -INFINITY) {
               const float p = ex2(s[kk] - mn);
               l += p;
@@ -371,8 +380,14 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
 }
 
 uint32_t attend_splits(const ckv_attend_desc& d) {
-  // ~16 tiles per work item: few per-item epilogues, enough items to balance
-  const uint32_t s = (d.max_tokens + 16 * AT_TILE - 1) / (16 * AT_TILE);
+  // ~1024 rows per work item: few per-item epilogues and merges, enough items
+  // to balance.  Tile / stage / item sizes were swept on B200 at config B
+  // (tools/attend_sweep.sh): 64-row tiles x 2 stages (64 KB ring, 3 CTAs per
+  // SM) with 1024-row items gave 94.5 us vs 102 us for 32 x 4 with 512.
+#ifndef CKV_AT_ITEM_ROWS
+#define CKV_AT_ITEM_ROWS 1024
+#endif
+  const uint32_t s = (d.max_tokens + CKV_AT_ITEM_ROWS - 1) / CKV_AT_ITEM_ROWS;
   return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 

@@ -18,6 +18,43 @@ int cuda_status(cudaError_t e, const char* where) {
   g_err = std::string(where) + ": " + cudaGetErrorString(e);
   return e == cudaErrorMemoryAllocation ? CKV_ENOMEM : CKV_ECUDA;
 }
+// grow-only scratch slot of the context (slots 0-20: k-means, 24-26: attend);
+// zero_new: zero the bytes when (re)allocated
+int ctx_scratch(ckv_ctx* ctx, int slot, size_t bytes, bool zero_new, void** out) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->scratch_cap[slot] < bytes) {
+    if (ctx->scratch[slot]) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->scratch[slot]);
+      ctx->scratch[slot] = nullptr;
+      ctx->scratch_cap[slot] = 0;
+    }
+    cudaError_t e = cudaMalloc(&ctx->scratch[slot], bytes);
+    if (e != cudaSuccess) {
+      ctx->scratch[slot] = nullptr;
+      return cuda_status(e, "context scratch allocation");
+    }
+    ctx->scratch_cap[slot] = bytes;
+    if (zero_new) CKV_CUDA_TRY(cudaMemsetAsync(ctx->scratch[slot], 0, bytes, ctx->stream));
+  }
+  *out = ctx->scratch[slot];
+  return CKV_OK;
+}
+
+// persistent split-K partials, merge tickets (zeroed once; k_attend re-arms
+// them) and the parity-mode logits of ckv_attend / ckv_attend_partial
+int attend_scratch(ckv_ctx* ctx, const ckv_attend_desc& d, bool weights, float** part,
+                   uint32_t** tickets, float** lw) {
+  void *p = nullptr, *t = nullptr, *w = nullptr;
+  CKV_TRY(ctx_scratch(ctx, 24, attend_part_floats(d.n_q, d.max_tokens) * 4 + 16, false, &p));
+  CKV_TRY(ctx_scratch(ctx, 25, size_t(d.n_q) * 4 + 4, true, &t));
+  if (weights) CKV_TRY(ctx_scratch(ctx, 26, size_t(d.n_q) * d.sel_cap * 4 + 16, false, &w));
+  *part = static_cast<float*>(p);
+  *tickets = static_cast<uint32_t*>(t);
+  *lw = static_cast<float*>(w);
+  return CKV_OK;
+}
+
 int num_sms() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -592,20 +629,12 @@ int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q, const uin
     for (uint32_t v : nt)
       if (v == 0) { set_error("approx_attention: empty selection"); return CKV_EINVAL; }
   }
-  const size_t pf = attend_part_floats(d->n_q, d->max_tokens);
-  float* part = nullptr;
-  float* lw = nullptr;
+  float *part = nullptr, *lw = nullptr;
   uint32_t* tickets = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&part, pf * 4 + 16, st));
-  CKV_CUDA_TRY(cudaMallocAsync(&tickets, size_t(d->n_q) * 4 + 4, st));
-  CKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(d->n_q) * 4 + 4, st));
-  if (weights) CKV_CUDA_TRY(cudaMallocAsync(&lw, size_t(d->n_q) * d->sel_cap * 4 + 16, st));
+  CKV_TRY(attend_scratch(ctx, *d, weights != nullptr, &part, &tickets, &lw));
   int rc = launch_attend(st, *d, q, K, V, rows, runs ? *runs : null_runs(), n_tokens, out,
                          weights, lw, part, tickets);
   ctx->launches++;
-  cudaFreeAsync(part, st);
-  cudaFreeAsync(tickets, st);
-  if (lw) cudaFreeAsync(lw, st);
   return rc;
 }
 

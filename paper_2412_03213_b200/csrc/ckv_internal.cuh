@@ -91,6 +91,9 @@ int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
                   const ckv_runs& runs, const uint32_t* n_tokens, float* out, float* weights,
                   float* logits_ws, float* part, uint32_t* tickets, float* lse = nullptr);
 size_t attend_part_floats(uint32_t n_q, uint32_t max_tokens);
+int ctx_scratch(ckv_ctx* ctx, int slot, size_t bytes, bool zero_new, void** out);
+int attend_scratch(ckv_ctx* ctx, const ckv_attend_desc& d, bool weights, float** part,
+                   uint32_t** tickets, float** lw);
 uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
 void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows);
 }  // namespace ckvb

@@ -452,20 +452,12 @@ int ckv_attend_partial(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q,
     ctx->launches++;
     return CKV_OK;
   }
-  const size_t pf = attend_part_floats(d->n_q, d->max_tokens);
-  float* part = nullptr;
-  float* lw = nullptr;
+  float *part = nullptr, *lw = nullptr;
   uint32_t* tickets = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&part, pf * 4 + 16, st));
-  CKV_CUDA_TRY(cudaMallocAsync(&tickets, size_t(d->n_q) * 4 + 4, st));
-  CKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(d->n_q) * 4 + 4, st));
-  if (weights) CKV_CUDA_TRY(cudaMallocAsync(&lw, size_t(d->n_q) * d->sel_cap * 4 + 16, st));
+  CKV_TRY(attend_scratch(ctx, *d, weights != nullptr, &part, &tickets, &lw));
   int rc = launch_attend(st, *d, q, K, V, nullptr, *runs, n_tokens, out, weights, lw, part,
                          tickets, lse);
   ctx->launches++;
-  cudaFreeAsync(part, st);
-  cudaFreeAsync(tickets, st);
-  if (lw) cudaFreeAsync(lw, st);
   return rc;
 }
 
