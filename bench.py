@@ -622,9 +622,10 @@ def main():
     G, L, B = args.group, args.L, args.budget
     T = args.warmup + args.steps + args.e2e_steps + 2
     ctx = Context(local)
+    sess_flags = (N.CKV_KM_EXACT_ONLY if args.exact_kmeans else 0) | \
+        (N.CKV_SESSION_L2_PERSIST if os.environ.get("CKV_L2_PERSIST") else 0)
     sess = Session(U, G, L, T, B, retention=1, cfg=ClusterConfig(max_iters=args.max_iters),
-                   kv_heads=args.kv_heads,
-                   flags=N.CKV_KM_EXACT_ONLY if args.exact_kmeans else 0, ctx=ctx)
+                   kv_heads=args.kv_heads, flags=sess_flags, ctx=ctx)
     g, centers = gen_inputs(torch, dev, U, G, L, T, seed=7 + rank)
     fill_kv(torch, dev, g, centers, sess.K, sess.V, L)
     q_all, kn_all, vn_all = gen_decode(torch, dev, g, centers, G, T)
@@ -717,7 +718,8 @@ def main():
     ncl = st["n_clusters"].to(torch.int64)
     stats = sess.stats()
     rec_begin, rec_end = stats.labeled_end, stats.n_ctx
-    sd = N.SelectDesc(n_q, G, B, 16, sess.p_cap, c_cap, sel_cap, rec_begin, rec_end, 0, 16)
+    sd = N.SelectDesc(n_q, G, B, 16, sess.p_cap, c_cap, sel_cap, rec_begin, rec_end,
+                      N.CKV_SEL_L2_PERSIST if sess_flags & N.CKV_SESSION_L2_PERSIST else 0, 16)
     ad = N.AttendDesc(n_q, G, sess.p_cap, sel_cap, min(B, rec_begin) + 16 + (rec_end - rec_begin))
     st_ptrs = [C.c_void_p() for _ in range(8)]
     cc, scap = C.c_uint32(), C.c_uint32()

@@ -243,6 +243,9 @@ typedef struct {
 
 #define CKV_SEL_FULL_RANK 1u  /* write ranked_clusters for every cluster   */
 #define CKV_SEL_SCORES 2u     /* write the f64 scores (score_clusters)     */
+#define CKV_SEL_L2_PERSIST 4u /* read the centroids through a persisting L2
+                                 window (needs cudaLimitPersistingL2CacheSize
+                                 > 0; the session sets it)                  */
 
 /* I_T as runs of consecutive KV-store rows (the cluster-major store makes
  * every taken cluster one run; sinks and the recency window are one run
@@ -412,6 +415,10 @@ typedef struct {
  * (ckv_session_state's token_ids); the attention itself consumes the run
  * list, so this is only needed for introspection / parity checks. */
 #define CKV_SESSION_TOKEN_IDS 0x100u
+/* Keep the centroids L2-resident across steps: sets aside persisting L2
+ * (cudaLimitPersistingL2CacheSize, device-wide, restored at destroy) and
+ * selects with CKV_SEL_L2_PERSIST. */
+#define CKV_SESSION_L2_PERSIST 0x200u
 
 int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* desc, ckv_session** out);
 int ckv_session_destroy(ckv_session* s);

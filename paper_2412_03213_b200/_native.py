@@ -17,6 +17,8 @@ CKV_OK, CKV_EINVAL, CKV_ECUDA, CKV_ENOMEM, CKV_ENCCL = 0, 1, 2, 3, 4
 CKV_KM_OBJECTIVE, CKV_KM_EXACT_ONLY, CKV_KM_NO_VALIDATE = 1, 2, 4
 CKV_SEL_FULL_RANK, CKV_SEL_SCORES = 1, 2
 CKV_SESSION_TOKEN_IDS = 0x100
+CKV_SESSION_L2_PERSIST = 0x200
+CKV_SEL_L2_PERSIST = 4
 
 vp, u32, u64, i32, f32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32, C.c_float
 

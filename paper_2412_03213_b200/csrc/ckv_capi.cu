@@ -664,6 +664,7 @@ struct ckv_session {
   std::vector<uint64_t> seeds;
   uint32_t n_ctx = 0, labeled_end = 0, steps = 0, pending = 0, C_cur = 0;
   bool prefilled = false;
+  bool l2_persist = false;
 };
 
 namespace {
@@ -725,6 +726,14 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   if (rc) { ckv_session_destroy(s); return CKV_ENOMEM; }
   cudaMemsetAsync(s->tickets, 0, size_t(s->n_q) * 4, ctx->stream);
   cudaMemsetAsync(s->n_clusters, 0, size_t(s->U) * 4, ctx->stream);
+  if (d->flags & CKV_SESSION_L2_PERSIST) {  // device-wide; restored at destroy
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+    const size_t want = std::min<size_t>(size_t(maxp), size_t(s->U) * s->c_cap * D * 4);
+    if (want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+      s->l2_persist = true;
+    cudaGetLastError();
+  }
   if (d->retention > 0) {
     rc = ckv_cache_create(ctx, s->n_q, s->c_cap, d->retention, D, &s->cache);
     if (rc) { ckv_session_destroy(s); return rc; }
@@ -751,6 +760,10 @@ int ckv_session_destroy(ckv_session* s) {
   cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
   cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
   ckv_cache_destroy(s->cache);
+  if (s->l2_persist) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
   delete s;
   return CKV_OK;
 }
@@ -809,7 +822,7 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
   sd.sel_cap = s->sel_cap;
   sd.rec_begin = s->labeled_end;
   sd.rec_end = s->n_ctx;
-  sd.flags = 0;
+  sd.flags = (s->d.flags & CKV_SESSION_L2_PERSIST) ? CKV_SEL_L2_PERSIST : 0u;
   sd.row_base = sd.sink_count;
   const bool want_ids = (s->d.flags & CKV_SESSION_TOKEN_IDS) != 0;
   CKV_TRY(launch_select(s->ctx->stream, sd, q_dev, s->cents, s->n_clusters, s->sizes, s->starts,

@@ -24,7 +24,7 @@ k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint
         uint32_t* __restrict__ sizes, uint32_t* __restrict__ starts,
         uint32_t* __restrict__ sorted_ids, const int32_t* __restrict__ prev_labels,
         int32_t* __restrict__ changed, const int32_t* __restrict__ active,
-        int32_t* __restrict__ any_empty) {
+        int32_t* __restrict__ any_empty, uint8_t* __restrict__ dirty) {
   const uint32_t u = blockIdx.x;
   if (active && !active[u]) return;
   const uint32_t C = n_clusters ? n_clusters[u] : c_uniform;
@@ -37,6 +37,12 @@ k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint
 
   const int32_t* lab = labels + size_t(u) * p_cap;
   for (uint32_t i = threadIdx.x; i < uint32_t(W) * C; i += blockDim.x) hist[i] = 0;
+  // dirty[c]: cluster c's member set differs from the previous labels' (the
+  // k-means update recomputes only those centroids; the others are
+  // bit-identical by construction)
+  uint8_t* dty = dirty ? dirty + size_t(u) * c_cap : nullptr;
+  if (dty)
+    for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) dty[c] = 0;
   if (threadIdx.x == 0) { s_changed = 0; s_empty = 0; }
   __syncthreads();
 
@@ -44,10 +50,17 @@ k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint
   const uint32_t p0 = min(n_pos, seg * w), p1 = min(n_pos, p0 + seg);
   int my_changed = 0;
   const int32_t* prev = prev_labels ? prev_labels + size_t(u) * p_cap : nullptr;
+  if (dty) __syncthreads();  // zeroed before any mark
   for (uint32_t p = p0 + lane; p < p1; p += 32) {
     int32_t l = lab[p];
     if (l >= 0) atomicAdd(&hist[w * C + l], 1u);
-    if (prev && prev[p] != l) my_changed = 1;
+    if (prev && prev[p] != l) {
+      my_changed = 1;
+      if (dty) {
+        if (l >= 0) dty[l] = 1;
+        if (prev[p] >= 0) dty[prev[p]] = 1;
+      }
+    }
   }
   if (prev && __any_sync(0xffffffffu, my_changed) && lane == 0) s_changed = 1;
   __syncthreads();
@@ -115,7 +128,7 @@ int launch_index(cudaStream_t st, uint32_t n_units, const int32_t* labels, uint3
                  uint32_t p_cap, uint32_t c_cap, const uint32_t* n_clusters,
                  uint32_t c_uniform, uint32_t* sizes, uint32_t* starts, uint32_t* sorted_ids,
                  const int32_t* prev_labels, int32_t* changed, const int32_t* active,
-                 int32_t* any_empty) {
+                 int32_t* any_empty, uint8_t* dirty) {
   if (n_units == 0) return CKV_OK;
   // warps per CTA limited by the smem histogram [W][c_cap]
   const size_t budget = 200 * 1024;
@@ -134,7 +147,7 @@ int launch_index(cudaStream_t st, uint32_t n_units, const int32_t* labels, uint3
   }
   k_index<<<n_units, W * 32, smem, st>>>(labels, n_pos, p_cap, c_cap, n_clusters, c_uniform,
                                          sizes, starts, sorted_ids, prev_labels, changed, active,
-                                         any_empty);
+                                         any_empty, dirty);
   CKV_LAUNCH_CHECK("k_index");
   return CKV_OK;
 }

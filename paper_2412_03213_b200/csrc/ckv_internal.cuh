@@ -24,7 +24,7 @@ int launch_index(cudaStream_t st, uint32_t n_units, const int32_t* labels, uint3
                  uint32_t p_cap, uint32_t c_cap, const uint32_t* n_clusters,
                  uint32_t c_uniform, uint32_t* sizes, uint32_t* starts, uint32_t* sorted_ids,
                  const int32_t* prev_labels, int32_t* changed, const int32_t* active,
-                 int32_t* any_empty);
+                 int32_t* any_empty, uint8_t* dirty = nullptr);
 
 // k-means driver (ckv_kmeans.cu); keys may be strided per unit
 struct KMeansArgs {

@@ -186,12 +186,16 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
          uint32_t c_pad, uint32_t label_stride, const uint32_t* __restrict__ sizes,
          const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
          float* __restrict__ cents, float* __restrict__ dirs, uint16_t* __restrict__ dirs_bf,
-         double* __restrict__ cnorm, float* __restrict__ deps, const int32_t* __restrict__ active) {
+         double* __restrict__ cnorm, float* __restrict__ deps, const int32_t* __restrict__ active,
+         const uint8_t* __restrict__ dirty) {
   const uint32_t u = blockIdx.y;
   if (active && !active[u]) return;
   const uint32_t c = blockIdx.x * (blockDim.x >> 5) + warp_id();
   const int lane = lane_id();
   if (c >= c_pad) return;
+  // same members as the centroid's last computation -> the same f64 sums,
+  // centroid, direction, norm and band: nothing to do
+  if (dirty && (c >= C || !dirty[size_t(u) * c_stride + c])) return;
   float* dr = dirs + (size_t(u) * c_pad + c) * D;
   uint16_t* db = dirs_bf + (size_t(u) * c_pad + c) * D;
   if (c >= C) {
@@ -421,7 +425,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
 
   // ---- scratch ----------------------------------------------------------
   DevBuf b_flags, b_lab1, b_sizes, b_starts, b_sorted, b_dirs, b_dirsbf, b_cnorm, b_deps, b_active,
-      b_changed, b_conv, b_iters, b_empty, b_rep, b_replog, b_obj, b_objlog, b_nact, b_tc;
+      b_changed, b_conv, b_iters, b_empty, b_rep, b_replog, b_obj, b_objlog, b_nact, b_tc, b_dirty;
   const uint32_t LS = a.label_stride, CS = a.c_stride;
   CKV_TRY(dalloc(ctx, 1, b_flags, sizeof(int32_t) * U));
   CKV_TRY(dalloc(ctx, 2, b_lab1, sizeof(int32_t) * size_t(U) * LS));
@@ -442,6 +446,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   CKV_TRY(dalloc(ctx, 17, b_obj, sizeof(double) * U));
   CKV_TRY(dalloc(ctx, 18, b_objlog, sizeof(double) * size_t(U) * (MI + 1)));
   CKV_TRY(dalloc(ctx, 19, b_nact, sizeof(int32_t)));
+  CKV_TRY(dalloc(ctx, 21, b_dirty, size_t(U) * CS));
 
   const bool use_tc = !(a.flags & CKV_KM_EXACT_ONLY) && assign_tc_supported(n, C);
   size_t tc_bytes = use_tc ? assign_tc_scratch_bytes(U, n, C) : 0;
@@ -530,7 +535,8 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   auto count_repair = [&](int32_t* cur, const int32_t* prev) -> int {
     CKV_TRY(launch_index(st, U, cur, n, LS, CS, nullptr, C, b_sizes.as<uint32_t>(),
                          b_starts.as<uint32_t>(), b_sorted.as<uint32_t>(), prev,
-                         b_changed.as<int32_t>(), active, b_empty.as<int32_t>()));
+                         b_changed.as<int32_t>(), active, b_empty.as<int32_t>(),
+                         prev ? b_dirty.as<uint8_t>() : nullptr));
     k_repair<<<U, 256, 0, st>>>(a.keys, a.key_stride, n, C, CS, c_pad, cur, LS,
                                 b_sizes.as<uint32_t>(), a.centroids, cnorm,
                                 b_empty.as<int32_t>(), b_rep.as<uint32_t>());
@@ -538,7 +544,8 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     // re-sort (and re-compare) the units that were repaired
     CKV_TRY(launch_index(st, U, cur, n, LS, CS, nullptr, C, b_sizes.as<uint32_t>(),
                          b_starts.as<uint32_t>(), b_sorted.as<uint32_t>(), prev,
-                         b_changed.as<int32_t>(), b_empty.as<int32_t>(), nullptr));
+                         b_changed.as<int32_t>(), b_empty.as<int32_t>(), nullptr,
+                         prev ? b_dirty.as<uint8_t>() : nullptr));
     ctx->launches += 3;
     if (want_obj) {
       k_objective<<<dim3((n + 255) / 256, U), 256, 0, st>>>(a.keys, a.key_stride, n, CS, c_pad,
@@ -580,7 +587,8 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     // update from the previous labels (sizes/starts/sorted hold its sort)
     k_update<<<dim3((c_pad + 7) / 8, U), 256, 0, st>>>(
         a.keys, a.key_stride, C, CS, c_pad, LS, b_sizes.as<uint32_t>(), b_starts.as<uint32_t>(),
-        b_sorted.as<uint32_t>(), a.centroids, dirs, dirs_bf, cnorm, deps, active);
+        b_sorted.as<uint32_t>(), a.centroids, dirs, dirs_bf, cnorm, deps, active,
+        t == 1 ? nullptr : b_dirty.as<uint8_t>());
     CKV_LAUNCH_CHECK("k_update");
     ctx->launches++;
     if (dbg) cudaEventRecord(dev_[1], st);

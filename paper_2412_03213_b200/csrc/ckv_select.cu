@@ -671,6 +671,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       static int attr_f = -1;
       int dev_f = 0;
       cudaGetDevice(&dev_f);
+      (void)dev_f;
       if (attr_f != dev_f) {
         CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -681,11 +682,41 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
 #define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
     token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode
       static const uint32_t sel_mode = getenv("CKV_SEL_MODE") ? uint32_t(atoi(getenv("CKV_SEL_MODE"))) : 0u;
+      // CKV_SEL_L2_PERSIST: the centroids (read by every step, ~60 MB at
+      // config B) are accessed through a persisting L2 window, so the KV
+      // stream of the attention between two steps does not evict them and the
+      // next select reads them from L2 instead of HBM.
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(units);
+      cfg.blockDim = dim3(SF_WARPS * 32);
+      cfg.dynamicSmemBytes = smem_f;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      if (desc.flags & CKV_SEL_L2_PERSIST) {
+        static size_t max_win = 0;
+        if (!max_win) {
+          int v = 0;
+          cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev_f);
+          max_win = size_t(v);
+        }
+        size_t persist = 0;
+        cudaDeviceGetLimit(&persist, cudaLimitPersistingL2CacheSize);
+        const size_t bytes = std::min(max_win, size_t(units) * desc.c_cap * D * 4);
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<float*>(cents);
+        attr[0].val.accessPolicyWindow.num_bytes = bytes;
+        attr[0].val.accessPolicyWindow.hitRatio =
+            bytes ? float(std::min(1.0, double(persist) / double(bytes))) : 0.f;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = persist && bytes ? 1 : 0;
+      }
       switch (G) {
-        case 1: k_select_fused<1><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
-        case 2: k_select_fused<2><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
-        case 4: k_select_fused<4><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
-        default: k_select_fused<8><<<units, SF_WARPS * 32, smem_f, st>>>(CKV_SF_ARGS); break;
+        case 1: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<1>, CKV_SF_ARGS)); break;
+        case 2: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<2>, CKV_SF_ARGS)); break;
+        case 4: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<4>, CKV_SF_ARGS)); break;
+        default: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<8>, CKV_SF_ARGS)); break;
       }
 #undef CKV_SF_ARGS
       CKV_LAUNCH_CHECK("k_select_fused");
