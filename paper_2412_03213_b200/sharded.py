@@ -331,6 +331,27 @@ def kmeans_cosine_sharded(shard: ShardSteps, n_total: int, row_lo: int, seeds=No
 # --------------------------------------------------------------------------
 # the decode step (select_tokens + approx_attention, sharded)
 # --------------------------------------------------------------------------
+def global_sizes(comm: Comm, lsize: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """From each rank's local cluster sizes [U][C]: the global sizes (what
+    build_index over the whole head gives, selection.hpp:29-48) and this
+    rank's prefix = members of each cluster on lower-ranked shards, which
+    decides its share of a trimmed cluster (the reference keeps the lowest
+    positions, selection.hpp:98-101).  One all-gather per prefill."""
+    per_rank = [t.to(lsize.device) for t in comm.all_gather(lsize)]
+    gsize = torch.stack(per_rank).sum(0).to(torch.int32).contiguous()
+    prefix = (torch.stack(per_rank[: comm.rank]).sum(0).to(torch.int32)
+              if comm.rank > 0 else torch.zeros_like(lsize)).contiguous()
+    return gsize, prefix
+
+
+def score_slice(C_: int, world: int, rank: int) -> tuple[int, int]:
+    """Rank `rank` scores clusters [c_lo, c_lo + slice) (equal slices so the
+    all-gathered buffer is [world][n_q][slice]; cluster c sits in rank
+    c // slice at offset c % slice)."""
+    slice_ = (C_ + world - 1) // world
+    return slice_, rank * slice_
+
+
 class ShardedDecoder:
     """One rank's share of the sequence-sharded decode step.
 
@@ -383,13 +404,9 @@ class ShardedDecoder:
                                     self.lsorted.data_ptr(), sink_rows, sink_rows + n_local,
                                     n_rows))
         # global sizes and the members on lower-ranked shards, once per prefill
-        per_rank = [t.to(dev) for t in self.comm.all_gather(self.lsize)]
-        self.gsize = torch.stack(per_rank).sum(0).to(torch.int32).contiguous()
-        self.prefix = (torch.stack(per_rank[: self.comm.rank]).sum(0).to(torch.int32)
-                       if self.comm.rank > 0 else torch.zeros_like(self.lsize)).contiguous()
+        self.gsize, self.prefix = global_sizes(self.comm, self.lsize)
         self.cents = km.centroids.to(dev).contiguous()
-        self.slice = (C_ + self.comm.world - 1) // self.comm.world
-        self.c_lo = self.comm.rank * self.slice
+        self.slice, self.c_lo = score_slice(C_, self.comm.world, self.comm.rank)
         self.pos_base = sink_tokens + km.row_lo - self.sink_rows
         self.sel_cap = budget + self.sink_rows + self.n_rec
         run_cap = C_ + 2

@@ -66,3 +66,16 @@ def decode_rank(rank, world, K, V, Q, Kr, Vr, C_, seeds, G, budget, device, full
     return dict(out=g(r["out"]), ids=g(r["token_ids"]), w=g(r["weights"]),
                 n_tokens=g(r["n_tokens"]), n_taken=g(r["n_taken"]), trimmed=g(r["trimmed"]),
                 ranked=g(r["ranked"]), off=g(r["run_off"]), iters=km.iterations_used)
+
+
+def sizes_rank(rank, world, labels_all, C_):
+    """global_sizes / score_slice on CPU: each rank counts its shard's labels."""
+    import torch
+
+    from paper_2412_03213_b200.sharded import Comm, global_sizes, score_slice, shard_range
+    U, n = labels_all.shape
+    lo, hi = shard_range(n, world, rank)
+    lsize = torch.from_numpy(np.stack([np.bincount(labels_all[u, lo:hi], minlength=C_)
+                                       for u in range(U)]).astype(np.int32))
+    g, p = global_sizes(Comm(), lsize)
+    return dict(g=g.numpy(), p=p.numpy(), lsize=lsize.numpy(), slice=score_slice(C_, world, rank))

@@ -71,3 +71,38 @@ def test_sharded_kmeans_validation():
     keys = np.stack([head(7, 0, 0, 80)["K"][16:]])
     with pytest.raises(RuntimeError, match="need 1 <= C <= N"):
         run_world(2, "tests._sharded_workers", "kmeans_rank", keys, 65, [1], 50, None, None)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_decode_sizes_and_trim_shares(world):
+    """Host side of the sharded decode step under gloo: the all-gathered
+    global sizes equal build_index's over the whole head, every rank's prefix
+    is the members on lower shards, and the per-rank shares of a trimmed
+    cluster (k_select_scored's clamp(allow - prefix, 0, local)) reassemble the
+    reference's lowest-position trim."""
+    rng = np.random.default_rng(world)
+    C_, n = 37, 1000
+    labels = rng.integers(0, C_, (2, n)).astype(np.int32)
+    res = run_world(world, "tests._sharded_workers", "sizes_rank", labels, C_)
+    for u in range(2):
+        sizes, _, sorted_ids = port().build_index(labels[u], C_)
+        for r in res:
+            assert np.array_equal(r["g"][u], sizes)
+        acc = np.zeros(C_, np.int64)
+        for r in res:
+            assert np.array_equal(r["p"][u], acc)
+            acc += r["lsize"][u]
+        for c in range(C_):
+            for allow in (0, 1, int(sizes[c]) // 2, int(sizes[c])):
+                allow = min(allow, int(sizes[c]))
+                take = [min(max(allow - int(r["p"][u][c]), 0), int(r["lsize"][u][c])) for r in res]
+                assert sum(take) == allow
+                # shard s's share = its lowest-position members of c, in rank order
+                members = np.nonzero(labels[u] == c)[0]
+                got = np.concatenate([members[(members >= k * n // world) &
+                                              (members < (k + 1) * n // world)][:take[k]]
+                                      for k in range(world)])
+                assert np.array_equal(got, members[:allow])
+    slices = [r["slice"] for r in res]
+    assert all(s[0] * world >= C_ for s in slices) and [s[1] for s in slices] == \
+        [k * slices[0][0] for k in range(world)]
