@@ -175,10 +175,10 @@ k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__
     // the cutoff need sorting (~B / mean size of them, not all C)
     unsigned long long prefix_k = 0ull;
     uint32_t above = 0;
+    s_hist[tid] = 0u;  // SR_THREADS == 256 bins; warp 0 re-zeroes them per pass
+    __syncthreads();
     for (int pass = 0; pass < 8; ++pass) {
       const int sh = 56 - 8 * pass;
-      s_hist[tid] = 0u;  // SR_THREADS == 256 bins
-      __syncthreads();
       const unsigned long long hm = pass == 0 ? 0ull : (~0ull << (sh + 8));
       // warp-aggregated: the scores share their high bytes, so most lanes hit
       // the same bin; one smem atomic per distinct bin per warp
@@ -191,14 +191,38 @@ k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__
         if (in && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], w);
       }
       __syncthreads();
-      // bins from high to low: thread t holds bin 255 - t
-      const uint32_t v = s_hist[255 - tid];
-      const uint32_t inc = block_incl_scan(v, s_wsum);
-      if (above + inc >= B && above + inc - v < B) { s_bin = 255 - tid; s_above = above + inc - v; }
+      if (wid == 0) {
+        // one warp scans the 256 bins from high to low: lane L holds bins
+        // 255 - 8L .. 248 - 8L; the first bin where the running weight
+        // reaches B holds the cutoff
+        uint32_t v[8], ls = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[k] = s_hist[255 - 8 * lane - k];
+          s_hist[255 - 8 * lane - k] = 0u;  // ready for the next pass
+          ls += v[k];
+        }
+        uint32_t x = ls;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        uint32_t run = above + x - ls;  // weight of the bins above my 8
+        int found = -1;
+        uint32_t above_sel = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (found < 0 && run + v[k] >= B) { found = 255 - 8 * lane - k; above_sel = run; }
+          run += v[k];
+        }
+        const unsigned f = __ballot_sync(0xffffffffu, found >= 0);
+        const int src = __ffs(f) - 1;  // the highest bin reaching B
+        if (lane == src) { s_bin = uint32_t(found); s_above = above_sel; }
+      }
       __syncthreads();
       prefix_k |= (unsigned long long)s_bin << sh;
       above = s_above;
-      __syncthreads();
     }
     // T = {key > tau} plus the ties at tau, in id order, until the budget
     __shared__ uint32_t s_nt;
@@ -248,19 +272,57 @@ k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__
       id[i] = v2 ? tid2[i] : 0xffffffffu;
     }
     __syncthreads();
-    block_sort(key, id, n2);
+    if (n2 <= 256) {  // the taken prefix is small: one warp sorts it, no block barriers
+      if (wid == 0) {
+        for (uint32_t k = 2; k <= n2; k <<= 1) {
+          for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = lane; i < n2; i += 32) {
+              const uint32_t ixj = i ^ j;
+              if (ixj > i) {
+                const unsigned long long ka = key[i], kb = key[ixj];
+                const uint32_t ia = id[i], ib = id[ixj];
+                const bool asc = (i & k) == 0;
+                const bool swap = asc ? before(kb, ib, ka, ia) : before(ka, ia, kb, ib);
+                if (swap) { key[i] = kb; key[ixj] = ka; id[i] = ib; id[ixj] = ia; }
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+      __syncthreads();
+    } else {
+      block_sort(key, id, n2);
+    }
   } else {
     block_sort(key, id, p2);
   }
   // inclusive prefix of the global sizes in rank order (chunks of 256)
   if (tid == 0) s_taken = B == 0 ? 0u : n_sorted;  // the reference breaks at cum >= B
-  uint32_t carry = 0;
-  for (uint32_t b = 0; b < n_sorted; b += SR_THREADS) {
-    const uint32_t i = b + tid;
-    uint32_t chunk_tot;
-    const uint32_t x = block_incl_scan(i < n_sorted ? __ldg(gs + id[i]) : 0u, s_wsum, &chunk_tot);
-    if (i < n_sorted) incl[i] = x + carry;
-    carry += chunk_tot;
+  if (n_sorted <= 256) {  // one warp, no block barriers
+    if (wid == 0) {
+      uint32_t c2 = 0;
+      for (uint32_t b = 0; b < n_sorted; b += 32) {
+        const uint32_t i = b + lane;
+        uint32_t x = i < n_sorted ? sz[id[i]] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (i < n_sorted) incl[i] = c2 + x;
+        c2 += __shfl_sync(0xffffffffu, x, 31);
+      }
+    }
+  } else {
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < n_sorted; b += SR_THREADS) {
+      const uint32_t i = b + tid;
+      uint32_t chunk_tot;
+      const uint32_t x = block_incl_scan(i < n_sorted ? __ldg(gs + id[i]) : 0u, s_wsum, &chunk_tot);
+      if (i < n_sorted) incl[i] = x + carry;
+      carry += chunk_tot;
+    }
   }
   __syncthreads();
   // taken = first i with incl[i] >= B, plus one (all of C when the total < B)
