@@ -352,24 +352,30 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     uint32_t g = 0;
     if (grp == 0)
       for (int ch = 0; ch < 2; ++ch) sm.n_ch[ch][lane_row] = 0;
-    // the next work item's key norm is loaded one item ahead so its latency
-    // hides behind this item's work
+    // (unit, range, tile) advance incrementally (no integer divisions per
+    // item); the next item's key norm is loaded one item ahead so its
+    // latency hides behind this item's work
+    TcWork wk = tc_work(w0, a), nx = wk;
+    auto advance = [&](TcWork& k) {
+      if (++k.tile == a.tiles_per_unit) {
+        k.tile = 0;
+        if (++k.range == a.n_ranges) { k.range = 0; ++k.ui; }
+      }
+    };
     float kn_next = 0.f;
-    if (w0 < w1) {
-      const TcWork k0 = tc_work(w0, a);
-      if (k0.tile * TC_M + lane_row < a.n)
-        kn_next = a.knorm[size_t(a.unit_list[k0.ui]) * a.n + k0.tile * TC_M + lane_row];
-    }
+    if (w0 < w1 && wk.tile * TC_M + lane_row < a.n)
+      kn_next = a.knorm[size_t(a.unit_list[wk.ui]) * a.n + wk.tile * TC_M + lane_row];
     for (uint32_t w = w0; w < w1; ++w) {
-      const TcWork wk = tc_work(w, a);
+      if (w > w0) advance(wk);
       const uint32_t unit = uint32_t(a.unit_list[wk.ui]), tile = wk.tile;
       const float eps = a.eps_u[unit];
       const uint32_t row = tile * TC_M + lane_row;
       const float kn = kn_next;
       if (w + 1 < w1) {
-        const TcWork k2 = tc_work(w + 1, a);
-        const uint32_t r2 = k2.tile * TC_M + lane_row;
-        kn_next = r2 < a.n ? a.knorm[size_t(a.unit_list[k2.ui]) * a.n + r2] : 0.f;
+        nx = wk;
+        advance(nx);
+        const uint32_t r2 = nx.tile * TC_M + lane_row;
+        kn_next = r2 < a.n ? a.knorm[size_t(a.unit_list[nx.ui]) * a.n + r2] : 0.f;
       }
       const float band = kn * (2.0f * eps + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
       const uint32_t cols = tc_cols(wk.range, a), cbase = wk.range * a.rc;
