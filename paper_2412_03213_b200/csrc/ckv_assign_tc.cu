@@ -442,7 +442,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
 #pragma unroll
         for (int q = 1; q < TC_EGROUPS; ++q) mc = fmaxf(mc, sm.m_part[q][lane_row]);
         if (grp == 0) sm.m_ch[ch][lane_row] = mc;
-        const float lo = mc - band;
+        // band relative to the running max of the tile's chunks so far: a
+        // later chunk far below an earlier one contributes no candidates
+        // (still a superset of {c : S_c >= M - band}, M the final max)
+        const float lo = (ch > 0 ? fmaxf(mc, sm.m_ch[0][lane_row]) : mc) - band;
         // (2) in-band mask: sign of S - lo (FADD, FMA pipe) funnel-shifted into
         // a word (SHF, ALU pipe): bit 31-j set  <=>  S_j < lo
         uint32_t in0 = 0u, in1 = 0u;
