@@ -195,7 +195,12 @@ struct TcArgs {
   // <= 512) columns, each its own work item with a resident B; the epilogue
   // then writes a per-(key, range) summary and k_assign_merge decides
   uint32_t n_ranges, rc;
-  float4* summ;                // [unit][n][n_ranges]: M_r, n_in | FULL, 4 ids (u16)
+  float4* summ;                // [unit][n][n_slots]: M_r, n_in | FULL, 4 ids (u16)
+  uint32_t n_slots;            // summary slots per key (n_ranges, or the work list's)
+  // explicit work list (the moved-cluster pass, ckv_assign_mcr.cu): item =
+  // {unit, tile, first column, columns | slot << 16}; summaries only
+  const uint4* wlist;
+  const int32_t* n_wlist;
   uint32_t key_rows_per_unit;  // key_stride / 128
   uint32_t label_stride;
   const float* knorm;          // [unit][n] key norms (band scale)
@@ -223,6 +228,21 @@ __device__ __forceinline__ TcWork tc_work(uint32_t w, const TcArgs& a) {
 __device__ __forceinline__ uint32_t tc_cols(uint32_t range, const TcArgs& a) {
   return min(a.rc, a.c_pad - range * a.rc);
 }
+// one work item: a 128-key tile of `unit` against columns [cbeg, cbeg + ccnt)
+struct TcItem {
+  uint32_t unit, tile, cbeg, ccnt, slot;
+};
+__device__ __forceinline__ TcItem tc_item_of(const TcWork& k, const TcArgs& a) {
+  return TcItem{uint32_t(a.unit_list[k.ui]), k.tile, k.range * a.rc, tc_cols(k.range, a),
+                k.range};
+}
+__device__ __forceinline__ TcItem tc_item(uint32_t w, const TcArgs& a) {
+  if (a.wlist) {
+    const uint4 x = a.wlist[w];
+    return TcItem{x.x, x.y, x.z, x.w & 0xffffu, x.w >> 16};
+  }
+  return tc_item_of(tc_work(w, a), a);
+}
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap dmap,
@@ -238,7 +258,8 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   auto Bp = [&](uint32_t kh, uint32_t row) { return sm_b + kh * (a.rc * 128) + row * 128; };
   const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
   const uint32_t n_units = uint32_t(*a.n_list);
-  const uint32_t total = n_units * a.n_ranges * a.tiles_per_unit;
+  const uint32_t total = a.wlist ? uint32_t(*a.n_wlist) : n_units * a.n_ranges * a.tiles_per_unit;
+  const bool summary = a.summ && (a.n_ranges > 1 || a.wlist);
   const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
   const uint32_t w0 = min(total, blockIdx.x * per), w1 = min(total, w0 + per);
 
@@ -263,21 +284,21 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   if (wid == 0) {
     // ============================ TMA producer =================================
     if (lane == 0 && w0 < w1) {
-      uint32_t st = 0, ph = 0, bswitch = 0, cur_key = TC_FULL;
+      uint32_t st = 0, ph = 0, bswitch = 0;
+      unsigned long long cur_key = ~0ull;
       for (uint32_t w = w0; w < w1; ++w) {
-        const TcWork wk = tc_work(w, a);
-        const uint32_t tile = wk.tile;
-        const uint32_t unit = uint32_t(a.unit_list[wk.ui]);
-        const uint32_t key = wk.ui * a.n_ranges + wk.range;
+        const TcItem it = tc_item(w, a);
+        const uint32_t tile = it.tile, unit = it.unit;
+        const unsigned long long key = (unsigned long long)unit << 32 | it.cbeg;
         if (key != cur_key) {
-          // the previous (unit, range)'s MMAs must be done reading B
-          if (cur_key != TC_FULL) mb_wait(&sm.b_empty, (bswitch - 1) & 1);
-          const uint32_t cols = tc_cols(wk.range, a);  // a multiple of TC_BOXR
+          // the previous (unit, columns)'s MMAs must be done reading B
+          if (cur_key != ~0ull) mb_wait(&sm.b_empty, (bswitch - 1) & 1);
+          const uint32_t cols = it.ccnt;  // a multiple of TC_BOXR
           mb_expect(&sm.b_full, cols * 128 * 2);
           for (uint32_t r0 = 0; r0 < cols; r0 += TC_BOXR) {
             for (int kh = 0; kh < 2; ++kh)
-              tma_2d(Bp(kh, r0), &dmap, kh * TC_BK,
-                     int(unit * a.c_pad + wk.range * a.rc + r0), &sm.b_full);
+              tma_2d(Bp(kh, r0), &dmap, kh * TC_BK, int(unit * a.c_pad + it.cbeg + r0),
+                     &sm.b_full);
           }
           cur_key = key;
           ++bswitch;
@@ -293,14 +314,15 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   } else if (wid == 1) {
     // ============================ MMA issuer ===================================
     if (lane == 0 && w0 < w1) {
-      uint32_t st = 0, ph = 0, g = 0, bswitch = 0, cur_key = TC_FULL;
+      uint32_t st = 0, ph = 0, g = 0, bswitch = 0;
+      unsigned long long cur_key = ~0ull;
       for (uint32_t w = w0; w < w1; ++w) {
-        const TcWork wk = tc_work(w, a);
-        const uint32_t key = wk.ui * a.n_ranges + wk.range;
+        const TcItem it = tc_item(w, a);
+        const unsigned long long key = (unsigned long long)it.unit << 32 | it.cbeg;
         bool last_of_unit = w + 1 == w1;
         if (!last_of_unit) {
-          const TcWork nx = tc_work(w + 1, a);
-          last_of_unit = nx.ui * a.n_ranges + nx.range != key;
+          const TcItem nx = tc_item(w + 1, a);
+          last_of_unit = ((unsigned long long)nx.unit << 32 | nx.cbeg) != key;
         }
         if (key != cur_key) {
           mb_wait(&sm.b_full, bswitch & 1);
@@ -309,7 +331,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
         }
         mb_wait(&sm.a_full[st], ph);
         tc_fence_after();
-        const uint32_t cols = tc_cols(wk.range, a);
+        const uint32_t cols = it.ccnt;
         const uint32_t nchunks = (cols + TC_CH - 1) / TC_CH;
         for (uint32_t ch = 0; ch < nchunks; ++ch, ++g) {
           const uint32_t buf = g & 1, bph = (g >> 1) & 1;
@@ -362,23 +384,30 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
         if (++k.range == a.n_ranges) { k.range = 0; ++k.ui; }
       }
     };
+    TcItem itn = w0 < w1 ? tc_item(w0, a) : TcItem{0, 0, 0, 0, 0};
     float kn_next = 0.f;
-    if (w0 < w1 && wk.tile * TC_M + lane_row < a.n)
-      kn_next = a.knorm[size_t(a.unit_list[wk.ui]) * a.n + wk.tile * TC_M + lane_row];
+    if (w0 < w1 && itn.tile * TC_M + lane_row < a.n)
+      kn_next = a.knorm[size_t(itn.unit) * a.n + itn.tile * TC_M + lane_row];
     for (uint32_t w = w0; w < w1; ++w) {
-      if (w > w0) advance(wk);
-      const uint32_t unit = uint32_t(a.unit_list[wk.ui]), tile = wk.tile;
+      if (w > w0 && !a.wlist) advance(wk);
+      const TcItem it = a.wlist ? itn : tc_item_of(wk, a);
+      const uint32_t unit = it.unit, tile = it.tile;
       const float eps = a.eps_u[unit];
       const uint32_t row = tile * TC_M + lane_row;
       const float kn = kn_next;
       if (w + 1 < w1) {
-        nx = wk;
-        advance(nx);
-        const uint32_t r2 = nx.tile * TC_M + lane_row;
-        kn_next = r2 < a.n ? a.knorm[size_t(a.unit_list[nx.ui]) * a.n + r2] : 0.f;
+        if (a.wlist) {
+          itn = tc_item(w + 1, a);
+        } else {
+          nx = wk;
+          advance(nx);
+          itn = tc_item_of(nx, a);
+        }
+        const uint32_t r2 = itn.tile * TC_M + lane_row;
+        kn_next = r2 < a.n ? a.knorm[size_t(itn.unit) * a.n + r2] : 0.f;
       }
       const float band = kn * (2.0f * eps + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
-      const uint32_t cols = tc_cols(wk.range, a), cbase = wk.range * a.rc;
+      const uint32_t cols = it.ccnt, cbase = it.cbeg;
       const uint32_t nchunks = (cols + TC_CH - 1) / TC_CH;
 #pragma unroll 1
       for (uint32_t ch = 0; ch < nchunks; ++ch) {
@@ -490,7 +519,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
           }
           if (nin > uint32_t(TC_NCAND)) full = true;
           int32_t* lab = a.labels + size_t(unit) * a.label_stride + row;
-          if (a.n_ranges > 1) {
+          if (summary) {
             // this range's summary: its max and its (<= 4) in-band ids;
             // k_assign_merge combines the ranges of the key
             uint32_t ids[4] = {0u, 0u, 0u, 0u}, k2 = 0;
@@ -500,7 +529,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
                 if (sm.m_ch[ch][lane_row] >= M - band)
                   for (uint32_t k = 0; k < sm.n_ch[ch][lane_row]; ++k)
                     ids[k2++] = sm.id_ch[ch][k][lane_row];
-            a.summ[(size_t(unit) * a.n + row) * a.n_ranges + wk.range] =
+            a.summ[(size_t(unit) * a.n + row) * a.n_slots + it.slot] =
                 make_float4(M, __uint_as_float(full ? TC_FULL : nin),
                             __uint_as_float(ids[0] | (ids[1] << 16)),
                             __uint_as_float(ids[2] | (ids[3] << 16)));
@@ -859,6 +888,9 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   ta.fix_ids = s.fix_ids;
   tc_ranges(c_pad, &ta.n_ranges, &ta.rc);
   ta.summ = s.summ;
+  ta.n_slots = ta.n_ranges;
+  ta.wlist = nullptr;
+  ta.n_wlist = nullptr;
   static size_t max_dyn = 0;  // opt-in per-CTA smem minus the kernel's static part
   static int attr_dev = -1;
   int dev = 0;
