@@ -852,6 +852,37 @@ size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
          align256(size_t(n_units) * 4) + 256 + summ;
 }
 
+// k_assign_tc with as many key-tile stages as fit next to B (rc columns)
+static int launch_tc(cudaStream_t st, const CUtensorMap& kmap, const CUtensorMap& dmap,
+                     TcArgs& ta) {
+  static size_t max_dyn = 0;  // opt-in per-CTA smem minus the kernel's static part
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    int optin = 0;
+    cudaFuncAttributes fa;
+    CKV_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CKV_CUDA_TRY(cudaFuncGetAttributes(&fa, k_assign_tc));
+    max_dyn = size_t(optin) - fa.sharedSizeBytes;
+    CKV_CUDA_TRY(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(max_dyn)));
+    attr_dev = dev;
+  }
+  static const uint32_t tc_mode = getenv("CKV_TC_MODE") ? uint32_t(atoi(getenv("CKV_TC_MODE"))) : 0u;
+  ta.mode = tc_mode;
+  const size_t fixed = 1024 + 2 * size_t(ta.rc) * 128;
+  ta.stages = uint32_t(std::min<size_t>(4, (max_dyn - fixed) / TC_ABYTES));
+  if (ta.stages < 2) {
+    set_error("assign_tc: not enough shared memory for two key-tile stages");
+    return CKV_EINVAL;
+  }
+  const size_t smem = fixed + size_t(ta.stages) * TC_ABYTES;
+  k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
+  CKV_LAUNCH_CHECK("k_assign_tc");
+  return CKV_OK;
+}
+
 int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
               uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs_bf,
               const float* deps, const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
@@ -891,31 +922,7 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   ta.n_slots = ta.n_ranges;
   ta.wlist = nullptr;
   ta.n_wlist = nullptr;
-  static size_t max_dyn = 0;  // opt-in per-CTA smem minus the kernel's static part
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    int optin = 0;
-    cudaFuncAttributes fa;
-    CKV_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    CKV_CUDA_TRY(cudaFuncGetAttributes(&fa, k_assign_tc));
-    max_dyn = size_t(optin) - fa.sharedSizeBytes;
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(max_dyn)));
-    attr_dev = dev;
-  }
-  static const uint32_t tc_mode = getenv("CKV_TC_MODE") ? uint32_t(atoi(getenv("CKV_TC_MODE"))) : 0u;
-  ta.mode = tc_mode;
-  const size_t fixed = 1024 + 2 * size_t(ta.rc) * 128;
-  ta.stages = uint32_t(std::min<size_t>(4, (max_dyn - fixed) / TC_ABYTES));
-  if (ta.stages < 2) {
-    set_error("assign_tc: not enough shared memory for two key-tile stages");
-    return CKV_EINVAL;
-  }
-  const size_t smem = fixed + size_t(ta.stages) * TC_ABYTES;
-  k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
-  CKV_LAUNCH_CHECK("k_assign_tc");
+  CKV_TRY(launch_tc(st, kmap, dmap, ta));
   if (ta.n_ranges == 1) {
     k_fixup<<<dim3(8, num_sms()), 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, s.count,
                                                  ta.tiles_per_unit, keys, key_stride, dirs, C,
@@ -949,4 +956,421 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   return CKV_OK;
 }
 
+
+// ===========================================================================
+// Moved-cluster reduced assignment (MCR), passes t >= 2 of the k-means.
+//
+// The update of pass t recomputes only the clusters whose member set changed
+// (k_update's dirty flags); every other centroid -- hence its direction and
+// bf16 operand -- is bit-identical to the one the previous pass scored.  For a
+// key whose current label a did not move, s(i, c) is unchanged for every
+// unmoved c, and a was the first maximum over all c last pass; so the new
+// first maximum lies in {a} U moved.  Such a key ("R") is scored against the
+// moved columns only and compared with its exact f64 score of a.  Keys whose
+// own cluster moved ("F") are scored against every column.
+//
+// Keys are gathered into cluster-major order (the previous labels' index) so
+// 128-key tiles are mostly all-F or all-R; a tile with any F key is scored
+// fully (exact either way).  Columns are permuted moved-first per unit, so an
+// R tile's work is one contiguous column block.  k_assign_tc runs from an
+// explicit work list in summary mode; k_mcr_merge decides each key (label, or
+// the exact f64 fix-up list).  Per unit: no moved cluster -> labels copied;
+// too many F tiles -> the dense path.
+// ===========================================================================
+constexpr int32_t MCR_OFF = 0, MCR_DENSE = 1, MCR_ON = 2, MCR_COPY = 3;
+
+__global__ void __launch_bounds__(256)
+k_mcr_plan(uint32_t n, uint32_t C, uint32_t c_pad, uint32_t c_stride, uint32_t label_stride,
+           uint32_t tiles, uint32_t rc, uint32_t n_ranges, const int32_t* __restrict__ active,
+           const uint8_t* __restrict__ moved, const int32_t* __restrict__ prev,
+           const uint32_t* __restrict__ sorted, uint32_t* __restrict__ cperm,
+           uint8_t* __restrict__ tclass, int32_t* __restrict__ mode, uint32_t* __restrict__ cnt,
+           uint32_t* __restrict__ mpad_out) {
+  extern __shared__ uint32_t pre[];  // [C + 1] moved prefix
+  __shared__ uint32_t s_w[8], s_nf;
+  const uint32_t u = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (!active[u]) {
+    if (tid == 0) { mode[u] = MCR_OFF; cnt[u] = 0; }
+    return;
+  }
+  const uint8_t* mv = moved + size_t(u) * c_stride;
+  // exclusive prefix of the moved flags (256-wide chunks)
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < C; b += 256) {
+    const uint32_t c = b + tid;
+    const uint32_t f = c < C ? uint32_t(mv[c] != 0) : 0u;
+    uint32_t x = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    uint32_t wp = 0, tot = 0;
+    for (int w = 0; w < 8; ++w) { if (w < wid) wp += s_w[w]; tot += s_w[w]; }
+    if (c < C) pre[c] = carry + wp + x - f;
+    __syncthreads();
+    carry += tot;
+  }
+  if (tid == 0) { pre[C] = carry; s_nf = 0; }
+  __syncthreads();
+  const uint32_t m = pre[C];
+  // moved clusters first (ascending), then the unmoved ones (ascending)
+  uint32_t* cp = cperm + size_t(u) * c_pad;
+  for (uint32_t c = tid; c < C; c += 256)
+    cp[mv[c] ? pre[c] : m + (c - pre[c])] = c;
+  // tile classes over the cluster-major order of the previous labels
+  const int32_t* pl = prev + size_t(u) * label_stride;
+  const uint32_t* so = sorted + size_t(u) * label_stride;
+  uint32_t nf = 0;
+  for (uint32_t T = tid; T < tiles; T += 256) {
+    const uint32_t r0 = T * TC_M, r1 = min(n, r0 + TC_M) - 1;
+    const uint32_t lf = uint32_t(pl[so[r0]]), ll = uint32_t(pl[so[r1]]);
+    const bool F = pre[ll + 1] > pre[lf];
+    tclass[size_t(u) * tiles + T] = F ? 1 : 0;
+    nf += F;
+  }
+  nf = __reduce_add_sync(0xffffffffu, nf);
+  if (lane == 0) atomicAdd(&s_nf, nf);
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t mpad = (m + 31) / 32 * 32;
+    const uint32_t r_chunks = (mpad + rc - 1) / rc;
+    int32_t md = MCR_ON;
+    if (m == 0) md = MCR_COPY;
+    else if (10ull * s_nf > 6ull * tiles || mpad * 10 > c_pad * 6) md = MCR_DENSE;
+    mode[u] = md;
+    mpad_out[u] = mpad;
+    cnt[u] = md == MCR_ON ? s_nf * n_ranges + (tiles - s_nf) * r_chunks : 0u;
+  }
+}
+
+// work list of the ON units (F tiles x every column range, then R tiles x
+// the moved columns), the permuted bf16 B operand, the dense-unit mask
+__global__ void __launch_bounds__(256)
+k_mcr_emit(uint32_t U, uint32_t C, uint32_t c_pad, uint32_t tiles, uint32_t rc,
+           uint32_t n_ranges, const int32_t* __restrict__ mode, const uint32_t* __restrict__ cnt,
+           const uint32_t* __restrict__ mpad, const uint8_t* __restrict__ tclass,
+           const uint32_t* __restrict__ cperm, const uint16_t* __restrict__ dirs_bf,
+           uint16_t* __restrict__ bperm, uint4* __restrict__ wlist, int32_t* __restrict__ n_wlist,
+           int32_t* __restrict__ dense_active) {
+  __shared__ uint32_t s_off, s_w[8], s_nf;
+  const uint32_t u = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) dense_active[u] = mode[u] == MCR_DENSE;
+  // offset of this unit's items (and the total, by the last unit)
+  uint32_t part = 0, all = 0;
+  for (uint32_t v = tid; v < U; v += 256) {
+    if (v < u) part += cnt[v];
+    all += cnt[v];
+  }
+  part = __reduce_add_sync(0xffffffffu, part);
+  all = __reduce_add_sync(0xffffffffu, all);
+  if (tid == 0) { s_off = 0; s_nf = 0; }
+  __syncthreads();
+  if (lane == 0) { atomicAdd(&s_off, part); if (u == U - 1) atomicAdd(n_wlist, int32_t(all)); }
+  __syncthreads();
+  if (mode[u] != MCR_ON) return;
+  const uint32_t off = s_off;
+  // B operand in permuted column order (padding rows zero)
+  const uint32_t* cp = cperm + size_t(u) * c_pad;
+  for (uint32_t e = tid; e < c_pad * (D / 8); e += 256) {
+    const uint32_t j = e / (D / 8), q = e % (D / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (j < C) v = __ldg(reinterpret_cast<const uint4*>(dirs_bf + (size_t(u) * c_pad + cp[j]) * D) + q);
+    reinterpret_cast<uint4*>(bperm + (size_t(u) * c_pad + j) * D)[q] = v;
+  }
+  // F tiles (compacted, in order) for each range, then R tiles for the moved block
+  const uint8_t* tc = tclass + size_t(u) * tiles;
+  const uint32_t m_pad = mpad[u];
+  uint32_t nF = 0;
+  for (uint32_t T = tid; T < tiles; T += 256) nF += tc[T];
+  nF = __reduce_add_sync(0xffffffffu, nF);
+  if (lane == 0) atomicAdd(&s_nf, nF);
+  __syncthreads();
+  nF = s_nf;
+  // emission (second pass with the totals known)
+  const uint32_t totF = nF;
+  const uint32_t r_chunks = (m_pad + rc - 1) / rc;
+  uint32_t cF = 0, cR = 0;
+  for (uint32_t b = 0; b < tiles; b += 256) {
+    const uint32_t T = b + tid;
+    const uint32_t f = T < tiles ? tc[T] : 0u, r = T < tiles ? 1u - f : 0u;
+    uint32_t xf = f, xr = r;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t yf = __shfl_up_sync(0xffffffffu, xf, o);
+      const uint32_t yr = __shfl_up_sync(0xffffffffu, xr, o);
+      if (lane >= o) { xf += yf; xr += yr; }
+    }
+    __shared__ uint32_t s_ef[8], s_er[8];
+    if (lane == 31) { s_ef[wid] = xf; s_er[wid] = xr; }
+    __syncthreads();
+    uint32_t pf = 0, pr = 0, tf = 0, tr = 0;
+    for (int w = 0; w < 8; ++w) {
+      if (w < wid) { pf += s_ef[w]; pr += s_er[w]; }
+      tf += s_ef[w];
+      tr += s_er[w];
+    }
+    __syncthreads();
+    const uint32_t iF = cF + pf + xf - f, iR = cR + pr + xr - r;
+    cF += tf;
+    cR += tr;
+    if (T < tiles) {
+      if (f) {
+        for (uint32_t rg = 0; rg < n_ranges; ++rg)
+          wlist[off + rg * totF + iF] =
+              make_uint4(u, T, rg * rc, min(rc, c_pad - rg * rc) | (rg << 16));
+      } else {
+        for (uint32_t k = 0; k < r_chunks; ++k)
+          wlist[off + n_ranges * totF + k * (tiles - totF) + iR] =
+              make_uint4(u, T, k * rc, min(rc, m_pad - k * rc) | (k << 16));
+      }
+    }
+  }
+}
+
+// keys (and their norms) of the ON units in cluster-major order
+__global__ void __launch_bounds__(256)
+k_mcr_gather(const int32_t* __restrict__ mode, const uint16_t* __restrict__ keys,
+             uint64_t key_stride, uint32_t n, uint32_t npad, const uint32_t* __restrict__ sorted,
+             uint32_t label_stride, const float* __restrict__ knorm, uint16_t* __restrict__ kperm,
+             float* __restrict__ knp) {
+  const uint32_t u = blockIdx.y;
+  if (mode[u] != MCR_ON) return;
+  const uint32_t r = blockIdx.x * 16 + (threadIdx.x >> 4), q = threadIdx.x & 15;
+  if (r >= npad) return;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  uint32_t src = 0;
+  if (r < n) {
+    src = __ldg(sorted + size_t(u) * label_stride + r);
+    v = __ldg(reinterpret_cast<const uint4*>(keys + u * key_stride + size_t(src) * D) + q);
+  }
+  reinterpret_cast<uint4*>(kperm + (size_t(u) * npad + r) * D)[q] = v;
+  if (q == 0 && r < n) knp[size_t(u) * n + r] = __ldg(knorm + size_t(u) * n + src);
+}
+
+__global__ void k_mcr_copy(const int32_t* __restrict__ mode, const int32_t* __restrict__ prev,
+                           int32_t* __restrict__ cur, uint32_t n, uint32_t label_stride) {
+  const uint32_t u = blockIdx.y;
+  if (mode[u] != MCR_COPY) return;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    cur[size_t(u) * label_stride + i] = prev[size_t(u) * label_stride + i];
+}
+
+// per key of an ON unit (row j of the cluster-major order, position sorted[j])
+__global__ void __launch_bounds__(256)
+k_mcr_merge(const int32_t* __restrict__ mode, uint32_t n, uint32_t tiles, uint32_t n_ranges,
+            uint32_t rc, const uint32_t* __restrict__ mpad, const uint8_t* __restrict__ tclass,
+            const float4* __restrict__ summ, uint32_t n_slots, const uint32_t* __restrict__ cperm,
+            uint32_t c_pad, const uint32_t* __restrict__ sorted, uint32_t label_stride,
+            const int32_t* __restrict__ prev, int32_t* __restrict__ cur,
+            const uint16_t* __restrict__ keys, uint64_t key_stride, const float* __restrict__ dirs,
+            const float* __restrict__ knp, const float* __restrict__ eps_u,
+            uint4* __restrict__ fix_list, uint32_t* __restrict__ fix_ids,
+            uint32_t* __restrict__ fix_n, uint32_t fix_cap) {
+  const uint32_t u = blockIdx.y;
+  if (mode[u] != MCR_ON) return;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  bool need = false, full = false;
+  uint32_t nin = 0, ids[TC_NCAND], pos = 0;
+  if (j < n) {
+    pos = __ldg(sorted + size_t(u) * label_stride + j);
+    const uint32_t a = uint32_t(prev[size_t(u) * label_stride + pos]);
+    const float4* sp = summ + (size_t(u) * n + j) * n_slots;
+    // err = one score's rigorous bound; band = 2 err (as k_assign_tc's epilogue)
+    const float band = knp[size_t(u) * n + j] * (2.0f * eps_u[u] + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
+    const bool F = tclass[size_t(u) * tiles + j / TC_M] != 0;
+    const uint32_t nsl = F ? n_ranges : (mpad[u] + rc - 1) / rc;
+    const uint32_t* cp = cperm + size_t(u) * c_pad;
+    float M = -INFINITY;
+    for (uint32_t r = 0; r < nsl; ++r) M = fmaxf(M, sp[r].x);
+    bool any = M > -INFINITY;
+    for (uint32_t r = 0; r < nsl && any && !full; ++r) {
+      const float4 sr = sp[r];
+      if (!(sr.x >= M - band)) continue;
+      const uint32_t nr = __float_as_uint(sr.y);
+      if (nr == TC_FULL || nin + nr > uint32_t(TC_NCAND)) { full = true; break; }
+      const uint32_t pk[2] = {__float_as_uint(sr.z), __float_as_uint(sr.w)};
+      for (uint32_t k = 0; k < nr; ++k) ids[nin++] = cp[(pk[k >> 1] >> (16 * (k & 1))) & 0xffffu];
+    }
+    int32_t lab = -1;
+    if (F) {
+      full |= !any;
+      if (!full && nin == 1) lab = int32_t(ids[0]);
+    } else {
+      // exact f64 score of the current label (dot_f64's sequential chain)
+      const double sa = exact_dot(keys + u * key_stride + size_t(pos) * D,
+                                  dirs + (size_t(u) * c_pad + a) * D);
+      const double err = 0.5 * double(band);
+      if (!any || double(M) + err < sa) {
+        lab = int32_t(a);  // every moved score is below s_a; unmoved ones never beat a
+      } else if (!full && nin == 1 && sa < double(M) - err) {
+        lab = int32_t(ids[0]);  // a is beaten and one moved column is in band
+      } else if (!full) {
+        if (nin + 1 > uint32_t(TC_NCAND)) full = true;
+        else ids[nin++] = a;
+      }
+    }
+    if (lab >= 0) cur[size_t(u) * label_stride + pos] = lab;
+    else { cur[size_t(u) * label_stride + pos] = -1; need = true; }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  if (!m) return;
+  uint32_t base = 0;
+  if (lane_id() == 0) base = atomicAdd(fix_n, uint32_t(__popc(m)));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (need) {
+    const uint32_t slot = base + __popc(m & ((1u << lane_id()) - 1u));
+    if (slot < fix_cap) {
+      // ids ascending is not required: k_fixup takes the first maximum over
+      // the exact scores with the lowest id on ties
+      fix_list[slot] = make_uint4(u, pos, full ? TC_FULL : nin, 0u);
+      if (!full)
+        for (uint32_t k = 0; k < nin; ++k) fix_ids[size_t(slot) * TC_NCAND + k] = ids[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side of MCR
+// ---------------------------------------------------------------------------
+namespace {
+int mcr_alloc(ckv_ctx* ctx, int slot, size_t bytes, void** p) {
+  return ctx_scratch(ctx, slot, bytes, false, p);
+}
+}  // namespace
+
+// Opt-in (CKV_MCR=1): exact, but on config B the per-pass cluster-major key
+// gather costs more than the reduced columns save (145 vs 100 ms prefill,
+// DESIGN.md §8); kept for the amortised-permutation follow-up.
+bool mcr_enabled() {
+  static const bool on = getenv("CKV_MCR") != nullptr;
+  return on;
+}
+
+int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t n, uint32_t C,
+               uint32_t c_pad, uint32_t n_units, uint32_t c_stride, const uint16_t* dirs_bf,
+               const float* deps, const float* dirs, const int32_t* prev, int32_t* cur,
+               uint32_t label_stride, const int32_t* active, const uint8_t* moved,
+               const uint32_t* sorted, void* tc_scratch, size_t tc_bytes) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t U = n_units, tiles = (n + TC_M - 1) / TC_M, npad = tiles * TC_M;
+  uint32_t n_ranges = 1, rc = 0;
+  tc_ranges(c_pad, &n_ranges, &rc);
+  TcScratch ts = carve(tc_scratch, U, n);  // key norms (positional) live here
+  // scratch: small state, permutations, permuted keys, work list + summaries, fix list
+  const size_t a256 = 256;
+  auto al = [&](size_t x) { return (x + a256 - 1) / a256 * a256; };
+  const size_t b_small = al(U * 4) * 4 + al(U * 4) + 512;
+  const size_t b_perm = al(size_t(U) * c_pad * 4) + al(size_t(U) * tiles) + al(size_t(U) * c_pad * D * 2);
+  const size_t b_keys = al(size_t(U) * npad * D * 2) + al(size_t(U) * n * 4);
+  const size_t n_items = size_t(U) * tiles * (n_ranges + 1);
+  const size_t b_work = al(n_items * 16) + al(size_t(U) * n * n_ranges * 16);
+  const size_t fix_cap = size_t(U) * n;
+  const size_t b_fix = al(fix_cap * 16) + al(fix_cap * TC_NCAND * 4);
+  void *p_small, *p_perm, *p_keys, *p_work, *p_fix;
+  CKV_TRY(mcr_alloc(ctx, 27, b_small, &p_small));
+  CKV_TRY(mcr_alloc(ctx, 28, b_perm, &p_perm));
+  CKV_TRY(mcr_alloc(ctx, 29, b_keys, &p_keys));
+  CKV_TRY(mcr_alloc(ctx, 30, b_work, &p_work));
+  CKV_TRY(mcr_alloc(ctx, 31, b_fix, &p_fix));
+  uint8_t* q = static_cast<uint8_t*>(p_small);
+  int32_t* mode = reinterpret_cast<int32_t*>(q); q += al(U * 4);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(q); q += al(U * 4);
+  uint32_t* mpad = reinterpret_cast<uint32_t*>(q); q += al(U * 4);
+  int32_t* dense = reinterpret_cast<int32_t*>(q); q += al(U * 4);
+  float* eps_u = reinterpret_cast<float*>(q); q += al(U * 4);
+  int32_t* n_wlist = reinterpret_cast<int32_t*>(q);
+  uint32_t* fix_n = reinterpret_cast<uint32_t*>(q + 64);
+  int32_t* n_one = reinterpret_cast<int32_t*>(q + 128);  // n_list for the work-list launch
+  q = static_cast<uint8_t*>(p_perm);
+  uint32_t* cperm = reinterpret_cast<uint32_t*>(q); q += al(size_t(U) * c_pad * 4);
+  uint8_t* tclass = q; q += al(size_t(U) * tiles);
+  uint16_t* bperm = reinterpret_cast<uint16_t*>(q);
+  q = static_cast<uint8_t*>(p_keys);
+  uint16_t* kperm = reinterpret_cast<uint16_t*>(q); q += al(size_t(U) * npad * D * 2);
+  float* knp = reinterpret_cast<float*>(q);
+  q = static_cast<uint8_t*>(p_work);
+  uint4* wlist = reinterpret_cast<uint4*>(q); q += al(n_items * 16);
+  float4* summ = reinterpret_cast<float4*>(q);
+  q = static_cast<uint8_t*>(p_fix);
+  uint4* fix_list = reinterpret_cast<uint4*>(q); q += al(fix_cap * 16);
+  uint32_t* fix_ids = reinterpret_cast<uint32_t*>(q);
+
+  CKV_CUDA_TRY(cudaMemsetAsync(n_wlist, 0, 192, st));  // n_wlist, fix_n, n_one
+  k_mcr_plan<<<U, 256, (C + 1) * 4, st>>>(n, C, c_pad, c_stride, label_stride, tiles, rc,
+                                           n_ranges, active, moved, prev, sorted, cperm, tclass,
+                                           mode, cnt, mpad);
+  CKV_LAUNCH_CHECK("k_mcr_plan");
+  k_mcr_emit<<<U, 256, 0, st>>>(U, C, c_pad, tiles, rc, n_ranges, mode, cnt, mpad, tclass, cperm,
+                                dirs_bf, bperm, wlist, n_wlist, dense);
+  CKV_LAUNCH_CHECK("k_mcr_emit");
+  k_mcr_copy<<<dim3(8, U), 256, 0, st>>>(mode, prev, cur, n, label_stride);
+  CKV_LAUNCH_CHECK("k_mcr_copy");
+  k_mcr_gather<<<dim3((npad + 15) / 16, U), 256, 0, st>>>(mode, keys, key_stride, n, npad, sorted,
+                                                          label_stride, ts.knorm, kperm, knp);
+  CKV_LAUNCH_CHECK("k_mcr_gather");
+  k_eps_max<<<(U + 7) / 8, 256, 0, st>>>(deps, c_pad, U, eps_u);
+  CKV_LAUNCH_CHECK("k_eps_max");
+  ctx->launches += 5;
+  // the reduced / full tiles of the ON units, from the work list
+  CUtensorMap kmap, dmap;
+  CKV_TRY(encode_2d(&kmap, kperm, uint64_t(U) * npad, TC_M));
+  CKV_TRY(encode_2d(&dmap, bperm, uint64_t(U) * c_pad, TC_BOXR));
+  TcArgs ta;
+  ta.unit_list = mode;  // unused with a work list
+  ta.n_list = n_one;
+  ta.n = n;
+  ta.C = C;
+  ta.c_pad = c_pad;
+  ta.tiles_per_unit = tiles;
+  ta.key_rows_per_unit = npad;
+  ta.label_stride = label_stride;
+  ta.knorm = knp;
+  ta.eps_u = eps_u;
+  ta.labels = cur;  // not written in summary mode
+  ta.fix_count = ts.fix_count;
+  ta.fix_list = nullptr;
+  ta.fix_cap = 0;
+  ta.fix_ids = nullptr;
+  ta.n_ranges = n_ranges;
+  ta.rc = rc;
+  ta.summ = summ;
+  ta.n_slots = n_ranges;
+  ta.wlist = wlist;
+  ta.n_wlist = n_wlist;
+  CKV_TRY(launch_tc(st, kmap, dmap, ta));
+  k_mcr_merge<<<dim3((n + 255) / 256, U), 256, 0, st>>>(
+      mode, n, tiles, n_ranges, rc, mpad, tclass, summ, n_ranges, cperm, c_pad, sorted,
+      label_stride, prev, cur, keys, key_stride, dirs, knp, eps_u, fix_list, fix_ids, fix_n,
+      uint32_t(fix_cap));
+  CKV_LAUNCH_CHECK("k_mcr_merge");
+  k_fixup<<<dim3(8 * num_sms(), 1), 256, 0, st>>>(fix_list, fix_ids, fix_n, n_one, tiles, keys,
+                                                   key_stride, dirs, C, c_pad, ts.knorm, n, cur,
+                                                   label_stride);
+  CKV_LAUNCH_CHECK("k_fixup");
+  ctx->launches += 3;
+  // the DENSE units through the ordinary path
+  CKV_TRY(assign_tc(st, keys, key_stride, n, C, c_pad, U, dirs_bf, deps, dirs, cur, label_stride,
+                    dense, tc_scratch, tc_bytes, &ctx->launches));
+  static const bool dbg = getenv("CKV_DEBUG_KMEANS") != nullptr;
+  if (dbg) {
+    std::vector<int32_t> md(U);
+    int32_t nw = 0;
+    uint32_t nfx = 0;
+    cudaMemcpyAsync(md.data(), mode, 4 * U, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&nw, n_wlist, 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&nfx, fix_n, 4, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    uint32_t c[4] = {0, 0, 0, 0};
+    for (int32_t v : md) c[v]++;
+    fprintf(stderr, "[kmeans dbg] MCR units on %u dense %u copy %u off %u | items %d of %u "
+            "dense-equivalent | merge fix-ups %u\n", c[MCR_ON], c[MCR_DENSE], c[MCR_COPY],
+            c[MCR_OFF], nw, c[MCR_ON] * tiles * n_ranges, nfx);
+  }
+  return CKV_OK;
+}
 }  // namespace ckvb

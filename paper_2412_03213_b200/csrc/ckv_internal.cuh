@@ -64,6 +64,13 @@ int launch_kmeans_small(cudaStream_t st, const uint16_t* keys, uint64_t key_stri
                         uint32_t* iters, int32_t* status);
 float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n);
 bool assign_tc_supported(uint32_t n, uint32_t C);
+// moved-cluster reduced assignment (ckv_assign_tc.cu), passes t >= 2
+bool mcr_enabled();
+int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t n, uint32_t C,
+               uint32_t c_pad, uint32_t n_units, uint32_t c_stride, const uint16_t* dirs_bf,
+               const float* deps, const float* dirs, const int32_t* prev, int32_t* cur,
+               uint32_t label_stride, const int32_t* active, const uint8_t* moved,
+               const uint32_t* sorted, void* tc_scratch, size_t tc_bytes);
 
 }  // namespace ckvb
 

@@ -592,7 +592,17 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     CKV_LAUNCH_CHECK("k_update");
     ctx->launches++;
     if (dbg) cudaEventRecord(dev_[1], st);
-    CKV_TRY(assign(cur));
+    // passes >= 2: only the clusters recomputed by this update moved, so the
+    // moved-cluster reduced assignment applies (exact; ckv_assign_tc.cu);
+    // bounded by its permuted-key staging (<= 8 GB)
+    const bool mcr = use_tc && t >= 2 && mcr_enabled() &&
+                     size_t(U) * ((n + 127) / 128 * 128) * D * 2 <= (size_t(8) << 30);
+    if (mcr)
+      CKV_TRY(assign_mcr(ctx, a.keys, a.key_stride, n, C, c_pad, U, CS, dirs_bf, deps, dirs,
+                         prev, cur, LS, active, b_dirty.as<uint8_t>(), b_sorted.as<uint32_t>(),
+                         b_tc.p, tc_bytes));
+    else
+      CKV_TRY(assign(cur));
     if (dbg) cudaEventRecord(dev_[2], st);
     CKV_TRY(count_repair(cur, prev));
     if (dbg) cudaEventRecord(dev_[3], st);
