@@ -6,6 +6,7 @@
 #include <random>
 #include <unordered_map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ckv_internal.cuh"
@@ -78,21 +79,47 @@ uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b) {
 // uniform_below is rng() % n, common.hpp:124-126)
 void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows) {
   // the reference's partial Fisher-Yates over pool = 0..n-1, with the pool
-  // kept sparse (only the <= 2C touched slots), so a unit costs O(C) not O(n)
+  // kept sparse (only the <= 2C touched slots, an open-addressing table), so
+  // a unit costs O(C) not O(n)
   std::mt19937_64 rng(seed);
-  std::unordered_map<uint32_t, uint32_t> pool;
-  pool.reserve(size_t(2) * C);
+  uint32_t cap = 64;
+  while (cap < 4 * C) cap <<= 1;
+  std::vector<uint32_t> key(cap, 0xffffffffu), val(cap);
+  auto slot = [&](uint32_t i) {
+    uint32_t h = (i * 2654435761u) & (cap - 1);
+    while (key[h] != 0xffffffffu && key[h] != i) h = (h + 1) & (cap - 1);
+    return h;
+  };
   auto get = [&](uint32_t i) {
-    auto it = pool.find(i);
-    return it == pool.end() ? i : it->second;
+    const uint32_t h = slot(i);
+    return key[h] == i ? val[h] : i;
+  };
+  auto put = [&](uint32_t i, uint32_t v) {
+    const uint32_t h = slot(i);
+    key[h] = i;
+    val[h] = v;
   };
   for (uint32_t c = 0; c < C; ++c) {
     const uint32_t j = c + uint32_t(rng() % uint64_t(n - c));
     const uint32_t pc = get(c), pj = get(j);
-    pool[c] = pj;
-    pool[j] = pc;
+    put(c, pj);
+    put(j, pc);
     rows[c] = pj;
   }
+}
+
+// host_init_rows for many units on host threads (units are independent)
+void host_init_rows_batch(uint32_t n_units, uint32_t n, uint32_t C, const uint64_t* seeds,
+                          uint32_t* rows) {
+  const uint32_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const uint32_t nt = std::min(hw, std::max(1u, n_units / 8));
+  auto work = [&](uint32_t t0) {
+    for (uint32_t u = t0; u < n_units; u += nt) host_init_rows(n, C, seeds[u], rows + size_t(u) * C);
+  };
+  if (nt == 1) { work(0); return; }
+  std::vector<std::thread> th;
+  for (uint32_t t = 0; t < nt; ++t) th.emplace_back(work, t);
+  for (auto& x : th) x.join();
 }
 
 // ---------------------------------------------------------------------------
@@ -342,7 +369,7 @@ int ckv_cluster_prefill(ckv_ctx* ctx, const ckv_prefill_desc* d, const uint16_t*
   if (C0 > d->c_cap) { set_error("cluster_prefill: C0 exceeds c_cap"); return CKV_EINVAL; }
   const uint32_t n = L - sink;
   std::vector<uint32_t> rows(size_t(U) * C0);
-  for (uint32_t u = 0; u < U; ++u) host_init_rows(n, C0, seeds[u], rows.data() + size_t(u) * C0);
+  host_init_rows_batch(U, n, C0, seeds, rows.data());
   uint32_t* d_rows = nullptr;
   CKV_CUDA_TRY(cudaMallocAsync(&d_rows, rows.size() * 4, st));
   CKV_CUDA_TRY(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st));

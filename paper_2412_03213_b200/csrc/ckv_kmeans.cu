@@ -557,7 +557,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     return CKV_OK;
   };
 
-  auto control = [&](uint32_t t, int32_t* n_active_host) -> int {
+  auto control = [&](uint32_t t, int32_t* n_active_host, bool read_back) -> int {
     CKV_CUDA_TRY(cudaMemsetAsync(b_nact.p, 0, sizeof(int32_t), st));
     k_control<<<(U + 127) / 128, 128, 0, st>>>(
         U, t, MI, active, b_changed.as<int32_t>(), b_conv.as<int32_t>(), b_iters.as<uint32_t>(),
@@ -565,6 +565,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
         b_objlog.as<double>(), b_nact.as<int32_t>());
     CKV_LAUNCH_CHECK("k_control");
     ctx->launches++;
+    if (!read_back) return CKV_OK;
     CKV_CUDA_TRY(cudaMemcpyAsync(n_active_host, b_nact.p, sizeof(int32_t),
                                  cudaMemcpyDeviceToHost, st));
     CKV_CUDA_TRY(cudaStreamSynchronize(st));
@@ -574,7 +575,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   // pass 0: initial assignment, count, repair, objective
   CKV_TRY(assign(lab[0]));
   CKV_TRY(count_repair(lab[0], nullptr));
-  CKV_TRY(control(0, &hf[U]));
+  CKV_TRY(control(0, &hf[U], true));
 
   // CKV_DEBUG_KMEANS=1: per-phase device times of each pass on stderr
   static const bool dbg = getenv("CKV_DEBUG_KMEANS") != nullptr;
@@ -607,7 +608,12 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     CKV_TRY(count_repair(cur, prev));
     if (dbg) cudaEventRecord(dev_[3], st);
     const int32_t active_before = hf[U];
-    CKV_TRY(control(t, &hf[U]));
+    // the host reads the active count back only every KM_SYNC passes: the
+    // passes queued after the last unit converged are no-ops (every kernel
+    // skips inactive units), and the launch queue stays ahead of the GPU
+    // instead of draining on a host round trip per pass
+    constexpr uint32_t KM_SYNC = 4;
+    CKV_TRY(control(t, &hf[U], dbg || t % KM_SYNC == 0 || t == MI));
     if (dbg) {
       cudaEventRecord(dev_[4], st);
       cudaEventSynchronize(dev_[4]);
