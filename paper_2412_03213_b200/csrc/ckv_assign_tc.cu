@@ -607,26 +607,30 @@ k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
         const float* __restrict__ knorm, uint32_t n, int32_t* __restrict__ labels,
         uint32_t label_stride) {
   // region r = blockIdx.y holds count[r] entries from index r * per * 128
-  // (k_assign_tc's CTA r processed tiles [r * per, (r + 1) * per))
+  // (k_assign_tc's CTA r processed tiles [r * per, (r + 1) * per)).
+  // A half-warp per key (lane hl holds dims 8hl..8hl+7): two keys per warp,
+  // 4 shuffle levels per candidate instead of 5 over a whole warp.
   const uint32_t r = blockIdx.y;
   const uint32_t total = uint32_t(*n_active) * tiles_per_unit;
   const uint32_t per = (total + gridDim.y - 1) / gridDim.y;
   const uint32_t nfix = count[r];
   const uint32_t rbase = r * per * TC_M;
-  const int lane = lane_id();
-  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t e0 = blockIdx.x * (blockDim.x >> 5) + warp_id(); e0 < nfix; e0 += nw) {
+  const int lane = lane_id(), hl = lane & 15;
+  const unsigned hmask = (lane < 16) ? 0x0000ffffu : 0xffff0000u;
+  const uint32_t nh = gridDim.x * (blockDim.x >> 4);  // half-warps in the grid
+  for (uint32_t e0 = (blockIdx.x * (blockDim.x >> 5) + warp_id()) * 2 + (lane >> 4); e0 < nfix;
+       e0 += nh) {
     const uint32_t e = rbase + e0;
     const uint4 it = list[e];
     const uint32_t u = it.x, row = it.y;
     const bool full = it.z == TC_FULL;
     const uint32_t nc = full ? C : it.z;
     const uint16_t* kr = keys + u * key_stride + size_t(row) * D;
-    const uint2 kv = __ldg(reinterpret_cast<const uint2*>(kr) + lane);
-    const double k[4] = {double(__uint_as_float(kv.x << 16)),
-                         double(__uint_as_float(kv.x & 0xffff0000u)),
-                         double(__uint_as_float(kv.y << 16)),
-                         double(__uint_as_float(kv.y & 0xffff0000u))};
+    const uint4 kv = __ldg(reinterpret_cast<const uint4*>(kr) + hl);
+    const double k[8] = {double(__uint_as_float(kv.x << 16)), double(__uint_as_float(kv.x & 0xffff0000u)),
+                         double(__uint_as_float(kv.y << 16)), double(__uint_as_float(kv.y & 0xffff0000u)),
+                         double(__uint_as_float(kv.z << 16)), double(__uint_as_float(kv.z & 0xffff0000u)),
+                         double(__uint_as_float(kv.w << 16)), double(__uint_as_float(kv.w & 0xffff0000u))};
     const float* du = dirs + size_t(u) * c_pad * D;
     const uint32_t* cid = ids + size_t(e) * TC_NCAND;
     double best = -INFINITY, second = -INFINITY;
@@ -635,15 +639,19 @@ k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
       double p[TC_NCAND];
       uint32_t c[TC_NCAND];
 #pragma unroll
-      for (int j = 0; j < TC_NCAND; ++j) {  // 8 independent loads + partials
+      for (int j = 0; j < TC_NCAND; ++j) {  // 8 independent row loads + partials
         c[j] = j0 + j < nc ? (full ? j0 + j : __ldg(cid + j0 + j)) : 0u;
-        const float4 d = __ldg(reinterpret_cast<const float4*>(du + size_t(c[j]) * D) + lane);
-        p[j] = lane_partial(k, d);
+        const float4* dr = reinterpret_cast<const float4*>(du + size_t(c[j]) * D) + 2 * hl;
+        const float4 x = __ldg(dr), y = __ldg(dr + 1);
+        p[j] = __fma_rn(k[7], double(y.w), __fma_rn(k[6], double(y.z),
+               __fma_rn(k[5], double(y.y), __fma_rn(k[4], double(y.x),
+               __fma_rn(k[3], double(x.w), __fma_rn(k[2], double(x.z),
+               __fma_rn(k[1], double(x.y), k[0] * double(x.x))))))));
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+      for (int o = 8; o > 0; o >>= 1)
 #pragma unroll
-        for (int j = 0; j < TC_NCAND; ++j) p[j] += __shfl_xor_sync(0xffffffffu, p[j], o);
+        for (int j = 0; j < TC_NCAND; ++j) p[j] += __shfl_xor_sync(hmask, p[j], o);
 #pragma unroll
       for (int j = 0; j < TC_NCAND; ++j) {
         if (j0 + j >= nc) break;
@@ -659,20 +667,20 @@ k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
       // lanes split the candidates, first maximum per lane, then lowest id
       double b2 = -INFINITY;
       uint32_t i2 = 0xffffffffu;
-      for (uint32_t j = lane; j < nc; j += 32) {
+      for (uint32_t j = hl; j < nc; j += 16) {
         const uint32_t cj = full ? j : cid[j];
         const double sj = exact_dot(kr, du + size_t(cj) * D);
         if (sj > b2) { b2 = sj; i2 = cj; }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double os = __shfl_xor_sync(0xffffffffu, b2, o);
-        const uint32_t oi = __shfl_xor_sync(0xffffffffu, i2, o);
+      for (int o = 8; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(hmask, b2, o);
+        const uint32_t oi = __shfl_xor_sync(hmask, i2, o);
         if (os > b2 || (os == b2 && oi < i2)) { b2 = os; i2 = oi; }
       }
       bid = i2;
     }
-    if (lane == 0)
+    if (hl == 0)
       labels[size_t(u) * label_stride + row] = int32_t(bid == 0xffffffffu ? 0 : bid);
   }
 }
