@@ -161,6 +161,10 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // launched with programmatic stream serialization: the CTAs start (and set
+  // up their barriers) while the selection kernel drains; its run lists and
+  // token counts are read only after this wait (a no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (wid == AT_CWARPS) {
     // ======================= producer warp =====================================
@@ -416,12 +420,23 @@ int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
   }
   const uint32_t n_items = desc.n_q * splits;
   const uint32_t grid = std::min<uint32_t>(n_items, uint32_t(std::max(1, per_sm)) * num_sms());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(AT_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (weights)
-    k_attend<true><<<grid, AT_THREADS, smem, st>>>(desc, splits, q, K, V, rows, runs, n_tokens,
-                                                   out, logits_ws, part, tickets, weights, lse);
+    CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_attend<true>, desc, splits, q, K, V, rows, runs,
+                                    n_tokens, out, logits_ws, part, tickets, weights, lse));
   else
-    k_attend<false><<<grid, AT_THREADS, smem, st>>>(desc, splits, q, K, V, rows, runs, n_tokens,
-                                                    out, nullptr, part, tickets, nullptr, lse);
+    CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_attend<false>, desc, splits, q, K, V, rows, runs,
+                                    n_tokens, out, static_cast<float*>(nullptr), part, tickets,
+                                    static_cast<float*>(nullptr), lse));
   CKV_LAUNCH_CHECK("k_attend");
   return CKV_OK;
 }

@@ -544,6 +544,10 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ WarpSel wsa[G];
   __shared__ float qn2[G];
+  // programmatic stream serialization: launched while the previous kernel
+  // (the last step's append / clustering) drains; nothing is read before it
+  // completes (a no-op for a normal launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   float* av_s = reinterpret_cast<float*>(smraw + size_t(G) * warp_bytes);  // [G][c_pad]
   float* ae_s = av_s + size_t(G) * c_pad;                                  // [G][c_pad]
   const uint32_t C = n_clusters[unit];
@@ -691,7 +695,11 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       cfg.blockDim = dim3(SF_WARPS * 32);
       cfg.dynamicSmemBytes = smem_f;
       cfg.stream = st;
-      cudaLaunchAttribute attr[1];
+      cudaLaunchAttribute attr[2];
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr + 1;
+      cfg.numAttrs = 1;
       if (desc.flags & CKV_SEL_L2_PERSIST) {
         static size_t max_win = 0;
         if (!max_win) {
@@ -710,7 +718,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.attrs = attr;
-        cfg.numAttrs = persist && bytes ? 1 : 0;
+        cfg.numAttrs = persist && bytes ? 2 : 1;
+        if (cfg.numAttrs == 1) cfg.attrs = attr + 1;
       }
       switch (G) {
         case 1: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<1>, CKV_SF_ARGS)); break;
