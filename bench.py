@@ -556,6 +556,91 @@ def run_config_E(args, rank, world, torch, dev, ctx, hbm):
             "clocks": clk.summary()}
 
 
+def run_config_A(args, torch, dev, ctx):
+    """configs[0]: the reference's own CPU-runnable case — one layer of the
+    Llama-3-8B shape (8 kv / 32 q heads), 4k prompt, cosine k-means (C0 = 51),
+    then decode steps at B = 1024.  The same synthetic heads (the reference
+    generator, trace.hpp:134-198, rounded to bf16) run through our session on
+    the GPU and through the compiled reference (oracle/_ref) on all host
+    threads: prefill (cluster_prefill of every head) and one decode step
+    (select_tokens + approx_attention of every q head)."""
+    from oracle.oracle import ClusterConfig as OCfg
+    from oracle.oracle import Oracle, build, ref_available, to_bf16_representable
+    from paper_2412_03213_b200.api import ClusterConfig
+    from paper_2412_03213_b200.session import Session
+    if not ref_available():
+        build(ref=True)
+    P, R = Oracle("port"), Oracle("reference")
+    n_kv, G, L, B, T = 8, 4, 4096, 1024, 256
+    heads = [P.generate_head(P.mix_seed(7, 0, h), L, T) for h in range(n_kv)]
+    K = np.stack([to_bf16_representable(h.prompt_keys) for h in heads])
+    V = np.stack([to_bf16_representable(h.prompt_values) for h in heads])
+    Q = [np.stack([to_bf16_representable(h.decode_queries[(t + r * (T // G)) % T])
+                   for h in heads for r in range(G)]) for t in range(T)]
+    bits = lambda x: (np.ascontiguousarray(x, np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    cores = int(R.lib.ref_hardware_concurrency())
+    # ---- CPU reference -----------------------------------------------------
+    seeds = np.array([P.mix_seed(0, 0, h) for h in range(n_kv)], np.uint64)
+    kptr = (C.c_void_p * n_kv)(*[K[h].ctypes.data for h in range(n_kv)])
+    passes = np.zeros(1, np.uint64)
+    cpu_prefill = float(np.median([R.lib.ref_prefill_cpu(kptr, n_kv, L, D, seeds, 50, cores,
+                                                         passes) for _ in range(3)]))
+    models = [R.cluster_prefill(K[h], OCfg(seed=P.mix_seed(0, 0, h))) for h in range(n_kv)]
+    sample = ([np.ascontiguousarray(m.centroids) for m in models],
+              np.array([m.n_clusters for m in models], np.uint32),
+              [np.ascontiguousarray(m.labels) for m in models], list(K), list(V),
+              np.ascontiguousarray(Q[0]))
+    cpu_decode_reps = [cpu_reference_decode(sample, cores, G, L, B) for _ in range(6)]
+    cpu_step = float(np.median(cpu_decode_reps[1:]))  # one layer = one step here
+    # ---- GPU ------------------------------------------------------------------
+    steps = args.steps
+    gpu_prefill = []
+    for rep in range(4):  # the session re-lays its store, so reload the prompt each time
+        sess = Session(n_kv, G, L, steps + args.warmup + 2, B, retention=1, cfg=ClusterConfig(),
+                       kv_heads=n_kv, ctx=ctx)
+        sess.load_prompt_host(bits(K), bits(V))
+        e = _events(torch, 2)
+        e[0].record()
+        sess.prefill()
+        e[1].record()
+        torch.cuda.synchronize()
+        if rep:
+            gpu_prefill.append(e[0].elapsed_time(e[1]))
+    qd = [torch.from_numpy(Q[t]).to(dev) for t in range(steps + args.warmup)]
+    kn = torch.from_numpy(bits(np.stack([h.decode_keys[0] for h in heads])).view(np.int16)).to(dev)
+    vn = torch.from_numpy(bits(np.stack([h.decode_values[0] for h in heads])).view(np.int16)).to(dev)
+    out = torch.empty((n_kv * G, D), dtype=torch.float32, device=dev)
+    for t in range(args.warmup):
+        sess.step(qd[t], kn, vn, out)
+    e = _events(torch, 2)
+    torch.cuda.synchronize()
+    e[0].record()
+    for t in range(steps):
+        sess.step(qd[args.warmup + t], kn, vn, out)
+    e[1].record()
+    torch.cuda.synchronize()
+    gpu_step = e[0].elapsed_time(e[1]) / steps
+    gp = float(np.median(gpu_prefill))
+    return {"metric": "config A: prefill ms and decode step us (1 layer, 8 kv / 32 q, 4k, "
+                      "B=1024), GPU vs the compiled reference on host threads",
+            "value": gpu_step * 1e3, "unit": "us/step", "n_gpus": 1, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": gpu_step, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 KV, f32/f64 math",
+            "data": "synthetic (the reference generator, trace.hpp, seed 7; bf16-rounded)",
+            "config": {"workload": "config A: Llama-3-8B head shape, 1 layer, 8 kv x 4 q heads, "
+                                   "4096-token prompt, C0 = 51, B = 1024",
+                       "global_batch": 1, "seq_len": L},
+            "prefill": {"gpu_ms": gp, "cpu_reference_ms": cpu_prefill,
+                        "speedup": cpu_prefill / gp, "passes": int(passes[0])},
+            "decode": {"gpu_us": gpu_step * 1e3, "cpu_reference_us": cpu_step * 1e3,
+                       "speedup": cpu_step / gpu_step},
+            "cpu_baseline": {"value": cpu_step * 1e3, "unit": "us/step", "cores": cores,
+                             "kind": "reference",
+                             "sample": "the whole config-A step: select_tokens + "
+                                       "approx_attention of all 32 q heads (median of 5), and "
+                                       "cluster_prefill of all 8 heads (median of 3)"}}
+
+
 def N_lib():
     from paper_2412_03213_b200 import _native as N
     return N.lib()
@@ -578,7 +663,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exact-kmeans", action="store_true")
-    ap.add_argument("--config", default="B", choices=["B", "C", "D", "E"],
+    ap.add_argument("--config", default="B", choices=["A", "B", "C", "D", "E"],
                     help="B = the headline (configs[1], plus a config D block); C / D / E "
                          "print their own line")
     ap.add_argument("--gen-tokens", type=int, default=4096, help="config D generated tokens")
@@ -605,9 +690,11 @@ def main():
     from paper_2412_03213_b200.session import Session
 
     hbm, bf16_peak, bf16_sus, peak_kind = peaks()
-    if args.config in ("C", "E", "D"):
+    if args.config in ("A", "C", "E", "D"):
         ctx = Context(local)
-        if args.config == "D":
+        if args.config == "A":
+            line = run_config_A(args, torch, dev, ctx) if rank == 0 else None
+        elif args.config == "D":
             line = run_config_D(torch, dev, ctx, args) if rank == 0 else None
         elif args.config == "C":
             line = run_config_C(args, rank, world, torch, dev, ctx, hbm)
