@@ -387,9 +387,26 @@ def run_config_C(args, rank, world, torch, dev, ctx, hbm):
     T = args.warmup + args.steps + 2
     sess = Session(U, G, L, T, B, retention=1, cfg=ClusterConfig(), kv_heads=args.kv_heads,
                    ctx=ctx)
-    g, centers = gen_inputs(torch, dev, U, G, L, T, seed=7 + rank)
-    fill_kv(torch, dev, g, centers, sess.K, sess.V, L)
-    q_all, kn_all, vn_all = gen_decode(torch, dev, g, centers, G, T)
+    if args.trace:  # a CKVT file's heads instead of the synthetic draw
+        from paper_2412_03213_b200 import trace as TR
+        tb = TR.read_trace(args.trace)
+        Kt, Vt, Qt, dKt, dVt = TR.to_device(tb, dev, decode_kv=True)
+        if Kt.shape[0] != U or Kt.shape[1] != L:
+            raise SystemExit(f"--trace: need {U} heads of L = {L} (pass --layers/--kv-heads/--L); "
+                             f"the file has {Kt.shape[0]} heads of L = {Kt.shape[1]}")
+        sess.K[:, :L].copy_(Kt)
+        sess.V[:, :L].copy_(Vt)
+        Tt = Qt.shape[1]
+        rows = (torch.arange(T, device=dev)[:, None] + torch.arange(G, device=dev)[None, :] *
+                max(1, Tt // G)) % Tt  # the GQA row offset of SURVEY §8d
+        q_all = Qt[:, rows].permute(1, 0, 2, 3).reshape(T, U * G, D).contiguous()
+        kn_all = dKt[:, torch.arange(T, device=dev) % Tt].permute(1, 0, 2).contiguous()
+        vn_all = dVt[:, torch.arange(T, device=dev) % Tt].permute(1, 0, 2).contiguous()
+        del Kt, Vt, Qt, dKt, dVt
+    else:
+        g, centers = gen_inputs(torch, dev, U, G, L, T, seed=7 + rank)
+        fill_kv(torch, dev, g, centers, sess.K, sess.V, L)
+        q_all, kn_all, vn_all = gen_decode(torch, dev, g, centers, G, T)
     torch.cuda.synchronize()
     e = _events(torch, 2)
     e[0].record()
@@ -669,6 +686,9 @@ def main():
     ap.add_argument("--gen-tokens", type=int, default=4096, help="config D generated tokens")
     ap.add_argument("--L-E", type=int, default=131072, help="config E context")
     ap.add_argument("--no-extra", action="store_true", help="skip the config D block")
+    ap.add_argument("--trace", default=None,
+                    help="a CKVT trace file (trace.hpp format): its heads are the units "
+                         "of the decode bench instead of the synthetic draw")
     ap.add_argument("--max-iters", type=int, default=50,
                     help="k-means cap (profiling only; the bench default is the reference's 50)")
     args = ap.parse_args()
@@ -713,9 +733,26 @@ def main():
         (N.CKV_SESSION_L2_PERSIST if os.environ.get("CKV_L2_PERSIST") else 0)
     sess = Session(U, G, L, T, B, retention=1, cfg=ClusterConfig(max_iters=args.max_iters),
                    kv_heads=args.kv_heads, flags=sess_flags, ctx=ctx)
-    g, centers = gen_inputs(torch, dev, U, G, L, T, seed=7 + rank)
-    fill_kv(torch, dev, g, centers, sess.K, sess.V, L)
-    q_all, kn_all, vn_all = gen_decode(torch, dev, g, centers, G, T)
+    if args.trace:  # a CKVT file's heads instead of the synthetic draw
+        from paper_2412_03213_b200 import trace as TR
+        tb = TR.read_trace(args.trace)
+        Kt, Vt, Qt, dKt, dVt = TR.to_device(tb, dev, decode_kv=True)
+        if Kt.shape[0] != U or Kt.shape[1] != L:
+            raise SystemExit(f"--trace: need {U} heads of L = {L} (pass --layers/--kv-heads/--L); "
+                             f"the file has {Kt.shape[0]} heads of L = {Kt.shape[1]}")
+        sess.K[:, :L].copy_(Kt)
+        sess.V[:, :L].copy_(Vt)
+        Tt = Qt.shape[1]
+        rows = (torch.arange(T, device=dev)[:, None] + torch.arange(G, device=dev)[None, :] *
+                max(1, Tt // G)) % Tt  # the GQA row offset of SURVEY §8d
+        q_all = Qt[:, rows].permute(1, 0, 2, 3).reshape(T, U * G, D).contiguous()
+        kn_all = dKt[:, torch.arange(T, device=dev) % Tt].permute(1, 0, 2).contiguous()
+        vn_all = dVt[:, torch.arange(T, device=dev) % Tt].permute(1, 0, 2).contiguous()
+        del Kt, Vt, Qt, dKt, dVt
+    else:
+        g, centers = gen_inputs(torch, dev, U, G, L, T, seed=7 + rank)
+        fill_kv(torch, dev, g, centers, sess.K, sess.V, L)
+        q_all, kn_all, vn_all = gen_decode(torch, dev, g, centers, G, T)
     torch.cuda.synchronize()
 
     # ---- prefill clustering --------------------------------------------
@@ -920,7 +957,8 @@ def main():
         "value": tps, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16 KV, f32/f64 math",
-        "data": "synthetic (device draw with trace.hpp generator distributions, bf16)",
+        "data": (f"CKVT trace {os.path.basename(args.trace)} (bf16-rounded)" if args.trace else
+                 "synthetic (device draw with trace.hpp generator distributions, bf16)"),
         "config": {"workload": f"config B: Llama-3-8B shape, {args.layers} layers x "
                                f"{args.kv_heads} kv x {G} q heads, {L} ctx, B={B}, batch 1/GPU, "
                                "R=1 cache; all layers of a step in one select + one attend launch",

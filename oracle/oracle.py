@@ -222,6 +222,10 @@ class Oracle:
             L.ref_prefill_cpu.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, u64p,
                                           C.c_uint32, C.c_uint32, u64p]
             L.ref_hardware_concurrency.restype = C.c_uint
+            L.ref_write_synthetic_trace.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64,
+                                                    C.c_uint32, C.c_uint32, C.c_uint32,
+                                                    C.c_uint32, C.c_uint32]
+            L.ref_read_trace_status.argtypes = [C.c_char_p]
 
     def _err(self) -> str:
         f = self.lib.orc_last_error if self.kind == "port" else self.lib.ref_last_error

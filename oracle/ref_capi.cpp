@@ -86,6 +86,46 @@ void ref_generate_head(uint32_t n_centers, float center_spread, float intra_spre
   std::memcpy(dv, tr.decode_values.data.data(), sizeof(float) * size_t(T) * d);
 }
 
+// generate_synthetic + write_trace (trace.hpp:200-225, 268-303): the
+// reference's own CKVT file, for the trace reader/writer golden fixtures.
+// Returns 0, or 1 with ref_last_error() set.
+int ref_write_synthetic_trace(const char* path, uint32_t n_centers, uint64_t seed, uint32_t L,
+                              uint32_t T, uint32_t d, uint32_t n_layers, uint32_t n_heads) {
+  try {
+    R::SynthSpec s;
+    s.n_centers = n_centers;
+    s.seed = seed;
+    s.prompt_len = L;
+    s.decode_len = T;
+    s.d = d;
+    s.n_layers = n_layers;
+    s.n_heads = n_heads;
+    R::write_trace(R::generate_synthetic(s), path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// read_trace (trace.hpp:305-367) and return its error class / ParseError code:
+// 0 ok, 1 + code for ParseError, 100 IoError, 200 ValidationError
+int ref_read_trace_status(const char* path) {
+  try {
+    R::read_trace(path);
+    return 0;
+  } catch (const R::ParseError& e) {
+    g_err = e.what();
+    return 1 + int(e.code());
+  } catch (const R::IoError& e) {
+    g_err = e.what();
+    return 100;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 200;
+  }
+}
+
 // info[6] as export_model
 int ref_kmeans(const float* keys, uint32_t n, uint32_t d, uint32_t C, uint64_t seed,
                uint32_t max_iters, int metric, const uint32_t* init_rows, uint32_t n_init,
