@@ -392,6 +392,32 @@ int ckv_attend_merge(ckv_ctx* ctx, uint32_t n_q, uint32_t world, uint32_t rank,
                      const uint32_t* n_tokens, uint32_t sel_cap);
 
 /* ------------------------------------------------------------------ */
+/* page-select baseline (selection.hpp:136-194)      */
+/* ------------------------------------------------------------------ */
+/* The Quest-style comparison point: consecutive pages of page_size tokens of
+ * a POSITION-ordered KV store, scored through per-channel representatives. */
+typedef struct {
+  uint32_t n_q, group;
+  uint32_t n;          /* tokens per unit                                    */
+  uint32_t page_size;
+  uint32_t budget;     /* B: n_sel = min(n_pages, B / page_size) pages       */
+  uint32_t pages_cap;  /* representative rows per unit                        */
+  uint32_t sel_cap;    /* token-id slots per q head (>= n_sel * page_size)    */
+  uint32_t maxmin;     /* 0 = PageRepr::Max, 1 = PageRepr::MaxMin             */
+} ckv_page_desc;
+
+/* per (unit, page) elementwise max (and min, when rep_min != NULL) of the
+ * page's keys; keys bf16 [unit][p_cap][128], reps f32 [unit][pages_cap][128] */
+int ckv_page_reps(ckv_ctx* ctx, uint32_t n_units, uint32_t n, uint32_t p_cap, uint32_t page_size,
+                  uint32_t pages_cap, const uint16_t* keys, float* rep_max, float* rep_min);
+/* page_select for n_q queries (q f32 [n_q][128]): the selected pages' tokens
+ * as runs of the position-ordered store (ascending ids; adjacent pages merge;
+ * run_cap > n_sel), n_tokens [n_q], token_ids [n_q][sel_cap] optional. */
+int ckv_page_select(ckv_ctx* ctx, const ckv_page_desc* desc, const float* q, const float* rep_max,
+                    const float* rep_min, const ckv_runs* runs, uint32_t* token_ids,
+                    uint32_t* n_tokens);
+
+/* ------------------------------------------------------------------ */
 /* session: the batched serving path (simulate_head's ClusterKV branch, */
 /* harness.hpp:155-346, minus the metric oracles), device-resident.     */
 /* ------------------------------------------------------------------ */

@@ -458,6 +458,62 @@ static int u32_cmp(const void* pa, const void* pb) {
 }
 
 /* selection.hpp:115-132 (the recall oracle; not on the hot path) */
+/* selection.hpp:136-194 page_select: consecutive pages scored through a
+ * per-channel representative (elementwise max; MaxMin: sum_j max(q*max, q*min)
+ * in f64, sequential), top n_sel = min(n_pages, budget / page_size) pages by
+ * (score desc, id asc), their ids ascending.  Returns the id count, or
+ * (uint32_t)-1 for page_size < 1 (ValidationError). */
+static const double* g_page_scores;
+static int page_cmp(const void* pa, const void* pb) {
+  uint32_t a = *(const uint32_t*)pa, b = *(const uint32_t*)pb;
+  if (g_page_scores[a] != g_page_scores[b]) return g_page_scores[a] > g_page_scores[b] ? -1 : 1;
+  return a < b ? -1 : (a > b);
+}
+uint32_t orc_page_select(const float* q, const float* keys, uint32_t n, uint32_t d,
+                         uint32_t budget, uint32_t page_size, int maxmin, uint32_t* ids_out) {
+  if (page_size < 1) { fail("page_select: page_size must be >= 1"); return (uint32_t)-1; }
+  const uint32_t n_pages = (n + page_size - 1) / page_size;
+  uint32_t n_sel = budget / page_size;
+  if (n_sel > n_pages) n_sel = n_pages;
+  double* sc = (double*)malloc(sizeof(double) * (n_pages ? n_pages : 1));
+  uint32_t* pages = (uint32_t*)malloc(sizeof(uint32_t) * (n_pages ? n_pages : 1));
+  float* mx = (float*)malloc(sizeof(float) * d);
+  float* mn = (float*)malloc(sizeof(float) * d);
+  for (uint32_t p = 0; p < n_pages; ++p) {
+    const uint32_t b = p * page_size, e = b + page_size < n ? b + page_size : n;
+    memcpy(mx, keys + (size_t)b * d, sizeof(float) * d);
+    memcpy(mn, keys + (size_t)b * d, sizeof(float) * d);
+    for (uint32_t i = b + 1; i < e; ++i)
+      for (uint32_t j = 0; j < d; ++j) {
+        const float v = keys[(size_t)i * d + j];
+        if (v > mx[j]) mx[j] = v;   /* std::max(a, b): b only if a < b */
+        if (v < mn[j]) mn[j] = v;
+      }
+    if (!maxmin) {
+      sc[p] = orc_dot_f64(q, mx, d);
+    } else {
+      double s = 0.0;
+      for (uint32_t j = 0; j < d; ++j) {
+        const double a = (double)q[j] * (double)mx[j], c = (double)q[j] * (double)mn[j];
+        s += a < c ? c : a;       /* std::max(a, c) */
+      }
+      sc[p] = s;
+    }
+    pages[p] = p;
+  }
+  g_page_scores = sc;
+  qsort(pages, n_pages, sizeof(uint32_t), page_cmp);
+  /* the selected pages' ids, ascending: sort the n_sel page ids, expand */
+  qsort(pages, n_sel, sizeof(uint32_t), u32_cmp);
+  uint32_t k = 0;
+  for (uint32_t t = 0; t < n_sel; ++t) {
+    const uint32_t b = pages[t] * page_size, e = b + page_size < n ? b + page_size : n;
+    for (uint32_t i = b; i < e; ++i) ids_out[k++] = i;
+  }
+  free(sc); free(pages); free(mx); free(mn);
+  return k;
+}
+
 void orc_exact_topb(const float* q, const float* keys, uint32_t n, uint32_t d, uint32_t budget,
                     uint32_t* ids_out) {
   double* s = (double*)malloc(sizeof(double) * n);

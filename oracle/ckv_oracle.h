@@ -116,6 +116,12 @@ uint32_t orc_select_tokens(const float* q, const float* centroids, uint32_t C,
                            uint32_t* ranked_out, uint32_t* n_taken_out,
                            uint32_t* trimmed_out, uint32_t* token_ids_out);
 
+/* selection.hpp:136-194 (maxmin = PageRepr::MaxMin); ids_out needs
+ * min(n_pages, budget/page_size) * page_size slots; returns the count or
+ * (uint32_t)-1 on a ValidationError */
+uint32_t orc_page_select(const float* q, const float* keys, uint32_t n, uint32_t d,
+                         uint32_t budget, uint32_t page_size, int maxmin, uint32_t* ids_out);
+
 void orc_exact_topb(const float* q, const float* keys, uint32_t n, uint32_t d,
                     uint32_t budget, uint32_t* ids_out /* min(budget,n) */);
 

@@ -166,6 +166,9 @@ class Oracle:
                                             C.c_uint32, C.c_uint32, u32p, C.c_uint32, u32p,
                                             C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), u32p]
             L.orc_exact_topb.argtypes = [f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32, u32p]
+            L.orc_page_select.restype = C.c_uint32
+            L.orc_page_select.argtypes = [f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, C.c_int, u32p]
             L.orc_attention_over.argtypes = [f32p, f32p, f32p, C.c_uint32, u32p, C.c_uint32,
                                              f32p, C.c_void_p]
             L.orc_cache_new.restype = C.c_void_p
@@ -226,6 +229,9 @@ class Oracle:
                                                     C.c_uint32, C.c_uint32, C.c_uint32,
                                                     C.c_uint32, C.c_uint32]
             L.ref_read_trace_status.argtypes = [C.c_char_p]
+            L.ref_page_select.restype = C.c_int64
+            L.ref_page_select.argtypes = [f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, C.c_int, u32p]
 
     def _err(self) -> str:
         f = self.lib.orc_last_error if self.kind == "port" else self.lib.ref_last_error
@@ -426,6 +432,24 @@ class Oracle:
         self.lib.orc_exact_topb(np.ascontiguousarray(q, np.float32), keys, keys.shape[0],
                                 keys.shape[1], budget, out)
         return out
+
+    def page_select(self, q, keys, budget: int, page_size: int, maxmin: bool = False):
+        """page_select (selection.hpp:141-194): sorted token ids."""
+        q = np.ascontiguousarray(q, np.float32)
+        keys = np.ascontiguousarray(keys, np.float32)
+        n, d = keys.shape
+        n_pages = (n + page_size - 1) // page_size if page_size else 0
+        out = np.zeros(max(1, min(n_pages, budget // max(page_size, 1)) * max(page_size, 1)),
+                       np.uint32)
+        if self.kind == "port":
+            k = self.lib.orc_page_select(q, keys, n, d, budget, page_size, int(maxmin), out)
+            if k == 0xFFFFFFFF:
+                raise OracleError(self._err())
+        else:
+            k = self.lib.ref_page_select(q, keys, n, d, budget, page_size, int(maxmin), out)
+            if k < 0:
+                raise OracleError(self._err())
+        return out[:k]
 
     def approx_attention(self, q, K, V, rows, want_weights: bool = True):
         q = np.ascontiguousarray(q, np.float32)

@@ -224,6 +224,20 @@ uint32_t ref_select_tokens(const float* q, const float* cents, uint32_t C, uint3
   return uint32_t(r.token_ids.size());
 }
 
+// page_select (selection.hpp:141-194); returns the id count, -1 on error
+int64_t ref_page_select(const float* q, const float* keys, uint32_t n, uint32_t d,
+                        uint32_t budget, uint32_t page_size, int maxmin, uint32_t* ids_out) {
+  try {
+    auto ids = R::page_select(std::span<const float>(q, d), as_matrix(keys, n, d), budget,
+                              page_size, maxmin ? R::PageRepr::MaxMin : R::PageRepr::Max);
+    std::memcpy(ids_out, ids.data(), sizeof(uint32_t) * ids.size());
+    return int64_t(ids.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 int ref_approx_attention(const float* q, const float* K, const float* V, uint32_t n_ctx,
                          uint32_t d, const uint32_t* rows, uint32_t n_rows, float* out,
                          float* weights) {

@@ -82,6 +82,11 @@ class ShardSelectDesc(C.Structure):
                                    "rec_pos", "n_rec", "pos_base", "flags")]
 
 
+class PageDesc(C.Structure):
+    _fields_ = [(n, u32) for n in ("n_q", "group", "n", "page_size", "budget", "pages_cap",
+                                   "sel_cap", "maxmin")]
+
+
 class SessionStats(C.Structure):
     _fields_ = [("n_ctx", u32), ("labeled_end", u32), ("steps", u32), ("max_clusters", u32),
                 ("launches", u64)]
@@ -130,6 +135,8 @@ SIGNATURES = {
     "ckv_attend_partial": (C.c_int, [vp, C.POINTER(AttendDesc), vp, vp, vp, C.POINTER(Runs), vp,
                                      vp, vp, vp]),
     "ckv_attend_merge": (C.c_int, [vp, u32, u32, u32, vp, vp, vp, vp, vp, u32]),
+    "ckv_page_reps": (C.c_int, [vp, u32, u32, u32, u32, u32, vp, vp, vp]),
+    "ckv_page_select": (C.c_int, [vp, C.POINTER(PageDesc), vp, vp, vp, C.POINTER(Runs), vp, vp]),
     "ckv_build_index": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp]),
     "ckv_select": (C.c_int, [vp, C.POINTER(SelectDesc), vp, vp, vp, vp, vp, vp, vp, vp,
                              C.POINTER(Runs), vp, vp, vp, vp, vp, vp]),

@@ -367,6 +367,46 @@ def approx_attention(q: np.ndarray, keys: np.ndarray, values: np.ndarray,
 
 
 # --------------------------------------------------------------------------
+# page-select baseline (selection.hpp:136-194)
+# --------------------------------------------------------------------------
+PAGE_MAX, PAGE_MAXMIN = 0, 1  # PageRepr
+
+
+def page_select(q: np.ndarray, keys: np.ndarray, budget: int, page_size: int,
+                repr: int = PAGE_MAX, ctx: Context | None = None) -> np.ndarray:
+    """selection.hpp:141-194: the ids of the top min(n_pages, budget /
+    page_size) pages by their representative score, ascending."""
+    ctx = ctx or Context.default()
+    if page_size < 1:
+        raise ValidationError(1, "page_select: page_size must be >= 1")
+    keys = np.ascontiguousarray(keys, np.float32)
+    _check_d(keys, "page_select")
+    n = keys.shape[0]
+    n_pages = (n + page_size - 1) // page_size
+    n_sel = min(n_pages, budget // page_size)
+    if n_sel == 0:
+        return np.zeros(0, np.uint32)
+    kb = _to_bf16_device(ctx, keys, "page_select keys")
+    dev = ctx.device
+    rmax = torch.empty((n_pages, D), dtype=torch.float32, device=dev)
+    rmin = torch.empty((n_pages, D), dtype=torch.float32, device=dev) if repr else None
+    check(lib().ckv_page_reps(ctx.h, 1, n, n, page_size, n_pages, kb.data_ptr(),
+                              rmax.data_ptr(), _ptr(rmin)))
+    qd = torch.from_numpy(np.ascontiguousarray(q, np.float32).reshape(1, D)).to(dev)
+    rr = torch.zeros((1, n_sel + 1), dtype=torch.int32, device=dev)
+    ro = torch.zeros((1, n_sel + 2), dtype=torch.int32, device=dev)
+    rc = torch.zeros(1, dtype=torch.int32, device=dev)
+    runs = N.Runs(rr.data_ptr(), ro.data_ptr(), rc.data_ptr(), n_sel + 1)
+    ids = torch.zeros((1, n_sel * page_size), dtype=torch.int32, device=dev)
+    nt = torch.zeros(1, dtype=torch.int32, device=dev)
+    desc = N.PageDesc(1, 1, n, page_size, budget, n_pages, n_sel * page_size, int(repr))
+    check(lib().ckv_page_select(ctx.h, C.byref(desc), qd.data_ptr(), rmax.data_ptr(), _ptr(rmin),
+                                C.byref(runs), ids.data_ptr(), nt.data_ptr()))
+    k = int(nt.item())
+    return ids[0, :k].cpu().numpy().view(np.uint32).copy()
+
+
+# --------------------------------------------------------------------------
 # cluster cache (cache.hpp:25-93)
 # --------------------------------------------------------------------------
 class ClusterCache:

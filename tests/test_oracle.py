@@ -126,3 +126,15 @@ def test_golden_fixtures(port):
     assert np.array_equal(c.counters(), g["cache_counters"])
     cc, ll, it = port.cluster_decode_batch(m.centroids, m.labels, g["dec_keys"], cfg)
     assert np.array_equal(cc, g["dec_centroids"]) and np.array_equal(ll, g["dec_labels"])
+
+
+def test_page_select_port_matches_reference(ref):
+    """orc_page_select restates selection.hpp:141-194 bit for bit."""
+    from oracle.oracle import Oracle, to_bf16_representable
+    P = Oracle("port")
+    rng = np.random.default_rng(0)
+    for n, B, ps, mm in ((1000, 256, 16, 0), (1000, 256, 16, 1), (37, 100, 7, 1),
+                         (4096, 1024, 32, 0), (10, 5, 16, 0), (200, 64, 16, 1)):
+        K = to_bf16_representable(rng.standard_normal((n, 128)).astype(np.float32))
+        q = to_bf16_representable(rng.standard_normal(128).astype(np.float32))
+        assert np.array_equal(P.page_select(q, K, B, ps, mm), ref.page_select(q, K, B, ps, mm))
