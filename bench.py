@@ -658,6 +658,108 @@ def run_config_A(args, torch, dev, ctx):
                                        "cluster_prefill of all 8 heads (median of 3)"}}
 
 
+def run_page_baseline(torch, dev, ctx, sess, U, G, L, B, q, hbm, ps=16, kv_heads=8):
+    """the page-select baseline (selection.hpp:136-194) on the
+    same prompts, same queries, same budget: GPU latency of page select +
+    attend over a position-ordered store, and the recall of both selections
+    against the exact top-B (exact_topb, selection.hpp:115-132) on a sample
+    (the first layer's q heads; CPU oracle)."""
+    from oracle.oracle import Oracle
+    from paper_2412_03213_b200 import _native as N
+    st = sess.state()
+    n = L - 16
+    n_q = U * G
+    # the prompt back in position order (the session's store is cluster-major)
+    srt = st["sorted_ids"][:, :n].to(torch.int64)
+    Kp = torch.empty((U, L, D), dtype=torch.int16, device=dev)
+    Vp = torch.empty_like(Kp)
+    for dst, store in ((Kp, sess.K), (Vp, sess.V)):
+        dst[:, :16] = store[:, :16]
+        dst.scatter_(1, srt[..., None].expand(-1, -1, D), store[:, 16:L])
+    n_pages = (L + ps - 1) // ps
+    n_sel = min(n_pages, B // ps)
+    rmax = torch.empty((U, n_pages, D), dtype=torch.float32, device=dev)
+    e = _events(torch, 2)
+    e[0].record()
+    N.check(N.lib().ckv_page_reps(ctx.h, U, L, L, ps, n_pages, Kp.data_ptr(), rmax.data_ptr(),
+                                  None))
+    e[1].record()
+    torch.cuda.synchronize()
+    reps_ms = e[0].elapsed_time(e[1])
+    rr = torch.zeros((n_q, n_sel + 1), dtype=torch.int32, device=dev)
+    ro = torch.zeros((n_q, n_sel + 2), dtype=torch.int32, device=dev)
+    rc = torch.zeros(n_q, dtype=torch.int32, device=dev)
+    runs = N.Runs(rr.data_ptr(), ro.data_ptr(), rc.data_ptr(), n_sel + 1)
+    ids = torch.zeros((n_q, n_sel * ps), dtype=torch.int32, device=dev)
+    nt = torch.zeros(n_q, dtype=torch.int32, device=dev)
+    pd = N.PageDesc(n_q, G, L, ps, B, n_pages, n_sel * ps, 0)
+    ad = N.AttendDesc(n_q, G, L, n_sel * ps, n_sel * ps)
+    out = torch.empty((n_q, D), dtype=torch.float32, device=dev)
+    qd = q.contiguous()
+
+    def sel(with_ids=False):
+        N.check(N.lib().ckv_page_select(ctx.h, C.byref(pd), qd.data_ptr(), rmax.data_ptr(), None,
+                                        C.byref(runs), ids.data_ptr() if with_ids else None,
+                                        nt.data_ptr()))
+
+    def att():
+        N.check(N.lib().ckv_attend(ctx.h, C.byref(ad), qd.data_ptr(), Kp.data_ptr(), Vp.data_ptr(),
+                                   None, C.byref(runs), nt.data_ptr(), out.data_ptr(), None))
+
+    for _ in range(3):
+        sel()
+        att()
+    ev = _events(torch, 3 * 10)
+    for i in range(10):
+        ev[3 * i].record()
+        sel()
+        ev[3 * i + 1].record()
+        att()
+        ev[3 * i + 2].record()
+    torch.cuda.synchronize()
+    sel_us = float(np.mean([ev[3 * i].elapsed_time(ev[3 * i + 1]) for i in range(10)])) * 1e3
+    att_us = float(np.mean([ev[3 * i + 1].elapsed_time(ev[3 * i + 2]) for i in range(10)])) * 1e3
+    # recall sample: the first layer's q heads, cluster vs page selection
+    sel(True)
+    c_cap, sel_cap = st["c_cap"], st["sel_cap"]
+    sd = N.SelectDesc(n_q, G, B, 16, sess.p_cap, c_cap, sel_cap, L, L, 0, 16)
+    ptrs = [C.c_void_p() for _ in range(8)]
+    cc, scap = C.c_uint32(), C.c_uint32()
+    N.lib().ckv_session_state(sess.h, *[C.byref(p) for p in ptrs], C.byref(cc), C.byref(scap))
+    tok = torch.zeros((n_q, sel_cap), dtype=torch.int32, device=dev)
+    ntc = torch.zeros(n_q, dtype=torch.int32, device=dev)
+    tmp = [torch.zeros(n_q, dtype=torch.int32, device=dev) for _ in range(2)]
+    rk = torch.zeros((n_q, c_cap), dtype=torch.int32, device=dev)
+    rr2 = torch.zeros((n_q, c_cap + 2), dtype=torch.int32, device=dev)
+    ro2 = torch.zeros((n_q, c_cap + 3), dtype=torch.int32, device=dev)
+    rc2 = torch.zeros(n_q, dtype=torch.int32, device=dev)
+    runs2 = N.Runs(rr2.data_ptr(), ro2.data_ptr(), rc2.data_ptr(), c_cap + 2)
+    N.check(N.lib().ckv_select(ctx.h, C.byref(sd), qd.data_ptr(), ptrs[0], ptrs[2], ptrs[3],
+                               ptrs[4], ptrs[5], tok.data_ptr(), None, C.byref(runs2),
+                               ntc.data_ptr(), tmp[0].data_ptr(), tmp[1].data_ptr(),
+                               rk.data_ptr(), None, None))
+    P = Oracle("port")
+    bf = lambda t16: (t16.to(torch.int32) << 16).view(torch.float32).cpu().numpy()
+    rc_, rp_ = [], []
+    for u in range(kv_heads):
+        Kh = np.ascontiguousarray(bf(Kp[u]))
+        for g in range(G):
+            h = u * G + g
+            truth = P.exact_topb(qd[h].cpu().numpy(), Kh, B)
+            ts = set(truth.tolist())
+            cl = tok[h, :int(ntc[h].item())].cpu().numpy()
+            pg = ids[h, :int(nt[h].item())].cpu().numpy()
+            rc_.append(len(ts & set(cl.tolist())) / len(ts))
+            rp_.append(len(ts & set(pg.tolist())) / len(ts))
+    del Kp, Vp, rmax
+    return {"page_size": ps, "repr": "max", "budget": B,
+            "page_select_us": sel_us, "page_attend_us": att_us,
+            "page_step_us": sel_us + att_us, "page_reps_ms_once": reps_ms,
+            "recall_sample": f"exact top-{B} (exact_topb, CPU oracle) of the first layer's "
+                             f"{kv_heads * G} q heads at the prompt context",
+            "recall_cluster": float(np.mean(rc_)), "recall_page": float(np.mean(rp_))}
+
+
 def N_lib():
     from paper_2412_03213_b200 import _native as N
     return N.lib()
@@ -895,6 +997,14 @@ def main():
     sel_ms = float(np.mean([evs[3 * i].elapsed_time(evs[3 * i + 1]) for i in range(2, reps)]))
     att_ms = float(np.mean([evs[3 * i + 1].elapsed_time(evs[3 * i + 2]) for i in range(2, reps)]))
 
+    page_block = None
+    if not args.no_extra and world == 1:
+        try:
+            page_block = run_page_baseline(torch, dev, ctx, sess, U, G, L, B, q_all[t - 1], hbm,
+                                           kv_heads=args.kv_heads)
+        except Exception as ex:  # reported, never silently dropped
+            page_block = {"failed": repr(ex)}
+
     # ---- e2e through the public step API with host buffers --------------
     qh = torch.empty((n_q, D), dtype=torch.float32).pin_memory()
     kh = torch.empty((U, D), dtype=torch.int16).pin_memory()
@@ -993,6 +1103,8 @@ def main():
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
+    if page_block is not None:
+        line["page_baseline"] = page_block
     if not args.no_extra and world == 1:
         del sess
         torch.cuda.synchronize()

@@ -54,8 +54,8 @@ __device__ __forceinline__ unsigned long long pkey(double s) {
 
 __global__ void __launch_bounds__(PG_THREADS)
 k_page_select(ckv_page_desc d, const float* __restrict__ q, const float* __restrict__ rmax,
-              const float* __restrict__ rmin, ckv_runs runs, uint32_t* __restrict__ token_ids,
-              uint32_t* __restrict__ n_tokens) {
+              const float* __restrict__ rmin, const double* __restrict__ scores, ckv_runs runs,
+              uint32_t* __restrict__ token_ids, uint32_t* __restrict__ n_tokens) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const uint32_t n_pages = (d.n + d.page_size - 1) / d.page_size;
   unsigned long long* key = reinterpret_cast<unsigned long long*>(smraw);  // [n_pages]
@@ -70,7 +70,9 @@ k_page_select(ckv_page_desc d, const float* __restrict__ q, const float* __restr
   // ---- scores (exact: products of floats are exact in f64, summed in j order)
   const float* rx = rmax + size_t(unit) * d.pages_cap * D;
   const float* rn = rmin ? rmin + size_t(unit) * d.pages_cap * D : nullptr;
-  for (uint32_t p = tid; p < n_pages; p += PG_THREADS) {
+  for (uint32_t p = tid; p < n_pages && scores; p += PG_THREADS)  // precomputed (Max)
+    key[p] = pkey(scores[size_t(h) * n_pages + p]);
+  for (uint32_t p = tid; p < n_pages && !scores; p += PG_THREADS) {
     const float4* mx = reinterpret_cast<const float4*>(rx + size_t(p) * D);
     double s = 0.0;
     if (!d.maxmin) {
@@ -267,7 +269,17 @@ int ckv_page_select(ckv_ctx* ctx, const ckv_page_desc* d, const float* q, const 
                                       96 * 1024));
     attr = true;
   }
-  k_page_select<<<d->n_q, PG_THREADS, smem, ctx->stream>>>(*d, q, rep_max, rep_min, *runs,
+  // PageRepr::Max scores are dot_f64(q, max_rep): the register-blocked exact
+  // scorer of the sharded path (all G heads of a unit per centroid-row read)
+  double* sc = nullptr;
+  if (!d->maxmin && (d->group == 1 || d->group == 2 || d->group == 4 || d->group == 8)) {
+    void* p = nullptr;
+    CKV_TRY(ctx_scratch(ctx, 23, size_t(d->n_q) * n_pages * 8, false, &p));
+    sc = static_cast<double*>(p);
+    CKV_TRY(ckv_score_range(ctx, d->n_q / d->group, d->group, q, rep_max, d->pages_cap, n_pages,
+                            0, n_pages, sc));
+  }
+  k_page_select<<<d->n_q, PG_THREADS, smem, ctx->stream>>>(*d, q, rep_max, rep_min, sc, *runs,
                                                             token_ids, n_tokens);
   CKV_LAUNCH_CHECK("k_page_select");
   ctx->launches++;
