@@ -176,6 +176,14 @@ struct AttentionOutput {
   std::vector<float> out;
   std::vector<float> weights;
 };
+// selection.hpp:136-194 — the page-based baseline (Quest-style)
+enum class PageRepr {
+  Max,     // elementwise max over member keys
+  MaxMin,  // score = sum_ch max(q*max_k, q*min_k)
+};
+std::vector<uint32_t> page_select(std::span<const float> q, const Matrix& keys, uint32_t budget,
+                                  uint32_t page_size, PageRepr repr = PageRepr::Max);
+
 AttentionOutput approx_attention(std::span<const float> q, const Matrix& keys,
                                  const Matrix& values,
                                  std::span<const uint32_t> selected);      // attention.hpp:63

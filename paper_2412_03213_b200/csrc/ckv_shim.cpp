@@ -267,6 +267,37 @@ SelectionResult select_tokens(std::span<const float> q, const ClusterModel& mode
 }
 
 // ---------------------------------------------------------------------------
+// selection.hpp:141-194
+std::vector<uint32_t> page_select(std::span<const float> q, const Matrix& keys, uint32_t budget,
+                                  uint32_t page_size, PageRepr repr) {
+  if (page_size < 1) throw ValidationError("page_select: page_size must be >= 1");
+  require_d128(keys, "page_select");
+  if (q.size() != kD) throw ValidationError("page_select: the B200 kernels specialise d = 128");
+  const uint32_t n = keys.rows, n_pages = (n + page_size - 1) / page_size;
+  const uint32_t n_sel = std::min(n_pages, budget / page_size);
+  if (n_sel == 0) return {};
+  const std::vector<uint16_t> kb = to_bf16(keys, "page_select keys");
+  const bool mm = repr == PageRepr::MaxMin;
+  Dev dk(kb.size() * 2), dq(kD * 4), dmax(size_t(n_pages) * kD * 4),
+      dmin(mm ? size_t(n_pages) * kD * 4 : 16), drow(size_t(n_sel + 1) * 4),
+      doff(size_t(n_sel + 2) * 4), dcnt(4), dids(size_t(n_sel) * page_size * 4), dnt(4);
+  put(dk, kb.data(), kb.size());
+  put(dq, q.data(), kD);
+  check(ckv_page_reps(ctx(), 1, n, n, page_size, n_pages, dk.as<uint16_t>(), dmax.as<float>(),
+                      mm ? dmin.as<float>() : nullptr));
+  ckv_runs runs{drow.as<uint32_t>(), doff.as<uint32_t>(), dcnt.as<uint32_t>(), n_sel + 1};
+  ckv_page_desc d{1, 1, n, page_size, budget, n_pages, n_sel * page_size, mm ? 1u : 0u};
+  check(ckv_page_select(ctx(), &d, dq.as<float>(), dmax.as<float>(),
+                        mm ? dmin.as<float>() : nullptr, &runs, dids.as<uint32_t>(),
+                        dnt.as<uint32_t>()));
+  uint32_t k = 0;
+  get(&k, dnt, 1);
+  std::vector<uint32_t> ids(k);
+  get(ids.data(), dids, k);
+  return ids;
+}
+
+// ---------------------------------------------------------------------------
 // attention.hpp:63-69
 AttentionOutput approx_attention(std::span<const float> q, const Matrix& keys,
                                  const Matrix& values, std::span<const uint32_t> selected) {

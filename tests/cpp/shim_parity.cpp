@@ -162,6 +162,19 @@ int main() {
     orc_cache_free(occ);
   }
 
+  // ---- page_select (selection.hpp:141-194), both representatives ----
+  for (int mm = 0; mm < 2; ++mm) {
+    for (uint32_t t = 0; t < 3; ++t) {
+      const auto got = ckv::page_select(Q.row(t), K, 512, 16,
+                                        mm ? ckv::PageRepr::MaxMin : ckv::PageRepr::Max);
+      std::vector<uint32_t> exp(512);
+      const uint32_t k = orc_page_select(Q.row(t).data(), K.data.data(), L, d, 512, 16, mm,
+                                         exp.data());
+      exp.resize(k);
+      CHECK(got == exp, "page_select repr %d step %u", mm, t);
+    }
+  }
+
   // ---- ValidationError predicates (clustering.hpp:166-172, attention.hpp:66) ----
   auto throws = [](auto&& f) {
     try {
@@ -174,6 +187,7 @@ int main() {
   CHECK(throws([&] { ckv::kmeans_cosine(K, L + 1, 0); }), "C > N must throw");
   CHECK(throws([&] { ckv::kmeans_cosine(K, 0, 0); }), "C = 0 must throw");
   CHECK(throws([&] { ckv::approx_attention(Q.row(0), K, V, {}); }), "empty selection must throw");
+  CHECK(throws([&] { ckv::page_select(Q.row(0), K, 64, 0); }), "page_size 0 must throw");
   CHECK(throws([&] { ckv::kmeans_cosine(ckv::Matrix(32, d), 4, 0); }), "all-zero keys must throw");
   CHECK(throws([&] {
           ckv::ClusterCache c(0, d);
