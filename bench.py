@@ -1108,7 +1108,10 @@ def main():
     if not args.no_extra and world == 1:
         del sess
         torch.cuda.synchronize()
-        line["config_D"] = run_config_D(torch, dev, ctx, args)
+        try:
+            line["config_D"] = run_config_D(torch, dev, ctx, args)
+        except Exception as ex:  # reported, never silently dropped
+            line["config_D"] = {"failed": repr(ex)}
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
