@@ -379,6 +379,21 @@ int ckv_select_scored(ckv_ctx* ctx, const ckv_shard_select_desc* desc, const dou
                       const uint32_t* prefix, const uint32_t* lsorted, const ckv_runs* runs,
                       uint32_t* token_ids, uint32_t* n_tokens, uint32_t* n_taken,
                       uint32_t* trimmed, uint32_t* ranked);
+/* The decode step's default scoring: approximate f32 scores of this rank's
+ * centroid slice with rigorous bounds (|a - s| <= 2^-14 |q| |mu|, s the
+ * dot_f64 score): out f32 [2][n_q][slice] (a, then the bound), all-gathered
+ * into [world][2][n_q][slice] for ckv_select_approx, which re-scores exactly
+ * (from the replicated centroids) only the clusters that can reach the
+ * budget cut — the same ranking, trim and shares as ckv_select_scored. */
+int ckv_score_range_approx(ckv_ctx* ctx, uint32_t n_units, uint32_t group, const float* q,
+                           const float* centroids, uint32_t c_cap, uint32_t C, uint32_t c_lo,
+                           uint32_t slice, float* out);
+int ckv_select_approx(ckv_ctx* ctx, const ckv_shard_select_desc* desc, const float* ascores,
+                      const float* q, const float* centroids, const uint32_t* gsize,
+                      const uint32_t* lsize, const uint32_t* lstart, const uint32_t* prefix,
+                      const uint32_t* lsorted, const ckv_runs* runs, uint32_t* token_ids,
+                      uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed,
+                      uint32_t* ranked);
 /* ckv_attend over runs, returning out = the locally normalised output and
  * lse [n_q] = log2 sum 2^(logit * log2 e) of the local logits (-inf and
  * out = 0 for a q head with no local tokens).  weights optional (local). */

@@ -132,6 +132,9 @@ SIGNATURES = {
     "ckv_score_range": (C.c_int, [vp, u32, u32, vp, vp, u32, u32, u32, u32, vp]),
     "ckv_select_scored": (C.c_int, [vp, C.POINTER(ShardSelectDesc), vp, vp, vp, vp, vp, vp,
                                     C.POINTER(Runs), vp, vp, vp, vp, vp]),
+    "ckv_score_range_approx": (C.c_int, [vp, u32, u32, vp, vp, u32, u32, u32, u32, vp]),
+    "ckv_select_approx": (C.c_int, [vp, C.POINTER(ShardSelectDesc), vp, vp, vp, vp, vp, vp, vp,
+                                    vp, C.POINTER(Runs), vp, vp, vp, vp, vp]),
     "ckv_attend_partial": (C.c_int, [vp, C.POINTER(AttendDesc), vp, vp, vp, C.POINTER(Runs), vp,
                                      vp, vp, vp]),
     "ckv_attend_merge": (C.c_int, [vp, u32, u32, u32, vp, vp, vp, vp, vp, u32]),

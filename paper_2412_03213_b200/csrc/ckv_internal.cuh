@@ -88,6 +88,9 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
                   const CacheDev& cache, void* scratch);
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap);
+int launch_score_approx(cudaStream_t st, uint32_t G, uint32_t n_units, const float* q,
+                        const float* cents, const uint32_t* counts, uint32_t c_cap,
+                        uint32_t c_pad, float* aval, float* aerr);
 int launch_cache_lookup(cudaStream_t st, const CacheDev& cache, uint32_t slot,
                         const uint32_t* sel, uint32_t n_sel, const uint32_t* sizes,
                         uint32_t* hit, uint32_t* miss, uint32_t* counts);

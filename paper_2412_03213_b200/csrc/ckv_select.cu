@@ -644,6 +644,25 @@ static void dbg_report(uint32_t n, const unsigned long long* dbuf, float k1_ms, 
           nfast ? ph[1] / nfast * 1e-3 : 0, ph[2] / n * 1e-3, nfast, n);
 }
 
+// approximate scores + rigorous bounds of a centroid block (the sharded
+// decode step's per-rank slice): cents points at the block's first row of
+// unit 0 (unit stride c_cap rows), counts[u] = rows of the block, outputs
+// [n_q][c_pad] (K1 above)
+int launch_score_approx(cudaStream_t st, uint32_t G, uint32_t n_units, const float* q,
+                        const float* cents, const uint32_t* counts, uint32_t c_cap,
+                        uint32_t c_pad, float* aval, float* aerr) {
+  const dim3 g1(n_units, (c_pad + SC_WARPS * SC_ROWS - 1) / (SC_WARPS * SC_ROWS));
+  switch (G) {
+    case 1: k_score_approx<1><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, counts, c_cap, c_pad, aval, aerr); break;
+    case 2: k_score_approx<2><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, counts, c_cap, c_pad, aval, aerr); break;
+    case 4: k_score_approx<4><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, counts, c_cap, c_pad, aval, aerr); break;
+    case 8: k_score_approx<8><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, counts, c_cap, c_pad, aval, aerr); break;
+    default: set_error("score_approx: group must be 1, 2, 4 or 8"); return CKV_EINVAL;
+  }
+  CKV_LAUNCH_CHECK("k_score_approx");
+  return CKV_OK;
+}
+
 int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const float* cents, const uint32_t* n_clusters, const uint32_t* sizes,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,

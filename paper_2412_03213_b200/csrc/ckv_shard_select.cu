@@ -32,6 +32,10 @@ constexpr int SR_THREADS = 256;
 __device__ __forceinline__ unsigned long long rank_key_s(double s) {
   return isnan(s) ? 0ull : dkey(s);  // NaN (empty-cluster centroids) ranks last
 }
+__device__ __forceinline__ uint32_t fkey32(float x) {  // order-preserving f32 -> u32
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
 __device__ __forceinline__ bool before(unsigned long long ka, uint32_t ia, unsigned long long kb,
                                        uint32_t ib) {
   return ka > kb || (ka == kb && ia < ib);
@@ -398,6 +402,289 @@ k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__
   }
 }
 
+__global__ void __launch_bounds__(SR_THREADS)
+k_select_approx(ckv_shard_select_desc d, uint32_t p2, const float* __restrict__ ascores,
+                const float* __restrict__ q, const float* __restrict__ cents,
+                const uint32_t* __restrict__ gsize, const uint32_t* __restrict__ lsize,
+                const uint32_t* __restrict__ lstart, const uint32_t* __restrict__ prefix,
+                const uint32_t* __restrict__ lsorted, ckv_runs runs,
+                uint32_t* __restrict__ token_ids, uint32_t* __restrict__ n_tokens,
+                uint32_t* __restrict__ n_taken, uint32_t* __restrict__ trimmed_out,
+                uint32_t* __restrict__ ranked) {
+  // ascores: [world][2][n_q][slice] — approximate score a and its rigorous
+  // bound e (|a - s| <= e, s = dot_f64) of every cluster, all-gathered.  The
+  // cutoff is found on a (size-weighted radix select), then only the
+  // clusters that can reach the exact taken prefix, S = {c : a_c + e_c >= L}
+  // with L = min over the approximate top set of (a - e), are re-scored
+  // exactly (the replicated centroids) and ranked: the exact prefix lies in S
+  // and ranks before everything outside it (the argument of k_select_warp,
+  // ckv_select.cu).  FULL_RANK, non-finite scores, a total below B or an
+  // oversized S take the exhaustive exact path.
+  extern __shared__ __align__(16) unsigned char smraw[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smraw);  // [p2]
+  uint32_t* id = reinterpret_cast<uint32_t*>(key + p2);                     // [p2]
+  uint32_t* incl = id + p2;                                                 // [p2]
+  uint32_t* loc = incl + p2;                                                // [p2 + 1]
+  uint32_t* sz = loc + p2 + 1;                                              // [p2]
+  float* av = reinterpret_cast<float*>(sz + p2);                            // [p2]
+  float* ev = av + p2;                                                      // [p2]
+  __shared__ uint32_t s_taken, s_wsum[SR_THREADS / 32], s_hist[256], s_n, s_bin, s_above;
+  __shared__ float s_lo[SR_THREADS / 32];
+  __shared__ int s_bad;
+  __shared__ float qsm[D];
+  const uint32_t h = blockIdx.x, unit = h / d.group;
+  const uint32_t C = d.C, B = d.budget;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t* gs = gsize + size_t(unit) * d.c_cap;
+  const float* cu = cents + size_t(unit) * d.c_cap * D;
+  if (tid < D) qsm[tid] = q[size_t(h) * D + tid];
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  uint32_t tot = 0;
+  int bad = 0;
+  for (uint32_t c = tid; c < C; c += SR_THREADS) {
+    const uint32_t r = c / d.slice, o = c % d.slice;
+    const float a = ascores[((size_t(r) * 2 + 0) * d.n_q + h) * d.slice + o];
+    const float e = ascores[((size_t(r) * 2 + 1) * d.n_q + h) * d.slice + o];
+    av[c] = a;
+    ev[c] = e;
+    sz[c] = __ldg(gs + c);
+    tot += sz[c];
+    bad |= !(isfinite(a) && isfinite(e));
+  }
+  tot = __reduce_add_sync(0xffffffffu, tot);
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) { s_wsum[wid] = tot; if (bad) s_bad = 1; }
+  __syncthreads();
+  tot = 0;
+  for (int w = 0; w < SR_THREADS / 32; ++w) tot += s_wsum[w];
+  __syncthreads();
+  auto exact = [&](uint32_t c) {  // dot_f64's sequential chain
+    const float4* row = reinterpret_cast<const float4*>(cu + size_t(c) * D);
+    double acc = 0.0;
+#pragma unroll 4
+    for (int j4 = 0; j4 < D / 4; ++j4) {
+      const float4 m = __ldg(row + j4);
+      acc = __fma_rn(double(qsm[4 * j4 + 0]), double(m.x), acc);
+      acc = __fma_rn(double(qsm[4 * j4 + 1]), double(m.y), acc);
+      acc = __fma_rn(double(qsm[4 * j4 + 2]), double(m.z), acc);
+      acc = __fma_rn(double(qsm[4 * j4 + 3]), double(m.w), acc);
+    }
+    return acc;
+  };
+  uint32_t n_sorted = C;
+  bool fast = !(d.flags & CKV_SEL_FULL_RANK) && B > 0 && tot >= B && !s_bad;
+  if (fast) {
+    // ---- size-weighted radix select on the fp32 approximate keys ----------
+    uint32_t prefix_k = 0, above = 0;
+    s_hist[tid] = 0u;
+    __syncthreads();
+    for (int pass = 0; pass < 4; ++pass) {
+      const int sh = 24 - 8 * pass;
+      const uint32_t hm = pass == 0 ? 0u : (~0u << (sh + 8));
+      for (uint32_t c = tid; c < C; c += SR_THREADS) {
+        const uint32_t k = fkey32(av[c]);
+        if (sz[c] && ((k ^ prefix_k) & hm) == 0u) atomicAdd(&s_hist[(k >> sh) & 255u], sz[c]);
+      }
+      __syncthreads();
+      if (wid == 0) {
+        uint32_t v[8], ls = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[k] = s_hist[255 - 8 * lane - k];
+          s_hist[255 - 8 * lane - k] = 0u;
+          ls += v[k];
+        }
+        uint32_t x = ls;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        uint32_t run = above + x - ls;
+        int found = -1;
+        uint32_t above_sel = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (found < 0 && run + v[k] >= B) { found = 255 - 8 * lane - k; above_sel = run; }
+          run += v[k];
+        }
+        const unsigned f = __ballot_sync(0xffffffffu, found >= 0);
+        const int src = __ffs(f) - 1;
+        if (lane == src) { s_bin = uint32_t(found); s_above = above_sel; }
+      }
+      __syncthreads();
+      prefix_k |= s_bin << sh;
+      above = s_above;
+    }
+    // ---- L = min over U = {key >= tau} of (a - e); S = {c : a + e >= L} ------
+    float lo = INFINITY;
+    for (uint32_t c = tid; c < C; c += SR_THREADS)
+      if (fkey32(av[c]) >= prefix_k) lo = fminf(lo, av[c] - ev[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    if (lane == 0) s_lo[wid] = lo;
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    lo = s_lo[0];
+    for (int w = 1; w < SR_THREADS / 32; ++w) lo = fminf(lo, s_lo[w]);
+    for (uint32_t c = tid; c < C; c += SR_THREADS)
+      if (av[c] + ev[c] >= lo) {
+        const uint32_t slot = atomicAdd(&s_n, 1u);
+        if (slot < uint32_t(SR_THREADS)) loc[slot] = c;
+      }
+    __syncthreads();
+    const uint32_t ns = s_n;
+    if (ns <= uint32_t(SR_THREADS)) {
+      // ---- exact f64 re-score of S, then its exact order --------------------
+      uint32_t n2 = 32;
+      while (n2 < ns) n2 <<= 1;
+      if (uint32_t(tid) < n2) {
+        if (uint32_t(tid) < ns) {
+          const uint32_t c = loc[tid];
+          key[tid] = rank_key_s(exact(c));
+          id[tid] = c;
+        } else {
+          key[tid] = 0ull;
+          id[tid] = 0xffffffffu;
+        }
+      }
+      __syncthreads();
+      if (wid == 0) {
+        for (uint32_t k = 2; k <= n2; k <<= 1) {
+          for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = lane; i < n2; i += 32) {
+              const uint32_t ixj = i ^ j;
+              if (ixj > i) {
+                const unsigned long long ka = key[i], kb = key[ixj];
+                const uint32_t ia = id[i], ib = id[ixj];
+                const bool asc = (i & k) == 0;
+                const bool swap = asc ? before(kb, ib, ka, ia) : before(ka, ia, kb, ib);
+                if (swap) { key[i] = kb; key[ixj] = ka; id[i] = ib; id[ixj] = ia; }
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+      __syncthreads();
+      n_sorted = ns;
+    } else {
+      fast = false;
+    }
+  }
+  if (!fast) {
+    // ---- exhaustive: exact f64 scores of every cluster, full sort -------------
+    for (uint32_t c = tid; c < p2; c += SR_THREADS) {
+      if (c < C) { key[c] = rank_key_s(exact(c)); id[c] = c; }
+      else { key[c] = 0ull; id[c] = 0xffffffffu; }
+    }
+    __syncthreads();
+    block_sort(key, id, p2);
+    n_sorted = C;
+  }
+  // inclusive prefix of the global sizes in rank order (chunks of 256)
+  if (tid == 0) s_taken = B == 0 ? 0u : n_sorted;  // the reference breaks at cum >= B
+  if (n_sorted <= 256) {  // one warp, no block barriers
+    if (wid == 0) {
+      uint32_t c2 = 0;
+      for (uint32_t b = 0; b < n_sorted; b += 32) {
+        const uint32_t i = b + lane;
+        uint32_t x = i < n_sorted ? sz[id[i]] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (i < n_sorted) incl[i] = c2 + x;
+        c2 += __shfl_sync(0xffffffffu, x, 31);
+      }
+    }
+  } else {
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < n_sorted; b += SR_THREADS) {
+      const uint32_t i = b + tid;
+      uint32_t chunk_tot;
+      const uint32_t x = block_incl_scan(i < n_sorted ? __ldg(gs + id[i]) : 0u, s_wsum, &chunk_tot);
+      if (i < n_sorted) incl[i] = x + carry;
+      carry += chunk_tot;
+    }
+  }
+  __syncthreads();
+  // taken = first i with incl[i] >= B, plus one (all of C when the total < B)
+  for (uint32_t i = tid; i < n_sorted; i += SR_THREADS)
+    if (B > 0 && incl[i] >= B && (i == 0 || incl[i - 1] < B)) s_taken = i + 1;
+  __syncthreads();
+  const uint32_t taken = s_taken;
+  const uint32_t full_cum = taken ? incl[taken - 1] : 0;
+  const uint32_t trimmed = full_cum > B ? full_cum - B : 0;
+  // this rank's share of each taken cluster
+  const uint32_t* ls = lsize + size_t(unit) * d.c_cap;
+  const uint32_t* pf = prefix + size_t(unit) * d.c_cap;
+  for (uint32_t i = tid; i < taken; i += SR_THREADS) {
+    const uint32_t c = id[i];
+    const uint32_t allow = (i + 1 == taken && trimmed) ? B - (i ? incl[i - 1] : 0u) : __ldg(gs + c);
+    const uint32_t p = __ldg(pf + c), l = __ldg(ls + c);
+    loc[i] = allow > p ? min(allow - p, l) : 0u;
+  }
+  __syncthreads();
+  // exclusive prefix of the local shares -> run offsets (reuse incl[] as out)
+  if (wid == 0) {
+    uint32_t c2 = 0;
+    for (uint32_t b = 0; b < taken; b += 32) {
+      const uint32_t i = b + lane;
+      uint32_t x = i < taken ? loc[i] : 0u;
+      const uint32_t own = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < taken) loc[i] = c2 + x - own;  // exclusive
+      c2 += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) loc[taken] = c2;
+  }
+  __syncthreads();
+  const uint32_t cum = loc[taken];
+  const uint32_t n = cum + d.sink_rows + d.n_rec;
+  const uint32_t* lst = lstart + size_t(unit) * (d.c_cap + 1);
+  uint32_t* rr = runs.row + size_t(h) * runs.run_cap;
+  uint32_t* ro = runs.off + size_t(h) * (runs.run_cap + 1);
+  for (uint32_t i = tid; i < taken; i += SR_THREADS) {
+    rr[i] = d.row_base + __ldg(lst + id[i]);
+    ro[i] = loc[i];
+  }
+  if (tid == 0) {
+    uint32_t nr = taken;
+    if (d.sink_rows) { rr[nr] = 0; ro[nr] = cum; ++nr; }
+    if (d.n_rec) { rr[nr] = d.rec_row; ro[nr] = cum + d.sink_rows; ++nr; }
+    ro[nr] = n;
+    runs.count[h] = nr;
+    n_tokens[h] = n;
+    n_taken[h] = taken;
+    trimmed_out[h] = trimmed;
+  }
+  const uint32_t n_rank = (d.flags & CKV_SEL_FULL_RANK) ? C : taken;
+  for (uint32_t i = tid; i < n_rank; i += SR_THREADS) ranked[size_t(h) * d.c_cap + i] = id[i];
+  if (token_ids) {  // reference positions of this rank's I_T entries
+    uint32_t* out = token_ids + size_t(h) * d.sel_cap;
+    const uint32_t* sid = lsorted + size_t(unit) * d.n_local;
+    for (uint32_t e = tid; e < cum; e += SR_THREADS) {
+      uint32_t lo = 0, hi = taken;  // last run i with loc[i] <= e
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (loc[mid] <= e) lo = mid; else hi = mid;
+      }
+      while (loc[lo + 1] <= e) ++lo;  // skip empty shares
+      out[e] = d.pos_base + __ldg(sid + __ldg(lst + id[lo]) + (e - loc[lo]));
+    }
+    for (uint32_t s2 = tid; s2 < d.sink_rows; s2 += SR_THREADS) out[cum + s2] = s2;
+    for (uint32_t i = tid; i < d.n_rec; i += SR_THREADS) out[cum + d.sink_rows + i] = d.rec_pos + i;
+  }
+}
+
+
 __global__ void k_lse_merge(uint32_t n_q, uint32_t world, uint32_t rank,
                             const float* __restrict__ outs, const float* __restrict__ lses,
                             float* __restrict__ out, float* __restrict__ weights,
@@ -420,6 +707,11 @@ __global__ void k_lse_merge(uint32_t n_q, uint32_t world, uint32_t rank,
     float* w = weights + size_t(h) * sel_cap;
     for (uint32_t j = t; j < n_tokens[h]; j += blockDim.x) w[j] *= sc;
   }
+}
+
+__global__ void k_fill_u32(uint32_t* __restrict__ p, uint32_t n, uint32_t v) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
 }
 
 __global__ void k_fill_empty(uint32_t n_q, float* __restrict__ out, float* __restrict__ lse) {
@@ -498,6 +790,67 @@ int ckv_select_scored(ckv_ctx* ctx, const ckv_shard_select_desc* d, const double
       *d, p2, scores, gsize, lsize, lstart, prefix, lsorted, *runs, token_ids, n_tokens, n_taken,
       trimmed, ranked);
   CKV_LAUNCH_CHECK("k_select_scored");
+  ctx->launches++;
+  return CKV_OK;
+}
+
+int ckv_score_range_approx(ckv_ctx* ctx, uint32_t n_units, uint32_t group, const float* q,
+                           const float* centroids, uint32_t c_cap, uint32_t C, uint32_t c_lo,
+                           uint32_t slice, float* out) {
+  if (!ctx || !q || !centroids || !out) {
+    set_error("ckv_score_range_approx: NULL argument");
+    return CKV_EINVAL;
+  }
+  if (c_cap < C || slice == 0) {
+    set_error("ckv_score_range_approx: need c_cap >= C, slice >= 1");
+    return CKV_EINVAL;
+  }
+  if (n_units == 0 || c_lo >= C) return CKV_OK;
+  cudaStream_t st = ctx->stream;
+  void* cnt = nullptr;
+  CKV_TRY(ctx_scratch(ctx, 22, size_t(n_units) * 4, false, &cnt));
+  const uint32_t rows = std::min(slice, C - c_lo);
+  k_fill_u32<<<(n_units + 255) / 256, 256, 0, st>>>(static_cast<uint32_t*>(cnt), n_units, rows);
+  CKV_LAUNCH_CHECK("k_fill_u32");
+  const size_t nq_slice = size_t(n_units) * group * slice;
+  CKV_TRY(launch_score_approx(st, group, n_units, q, centroids + size_t(c_lo) * D,
+                              static_cast<const uint32_t*>(cnt), c_cap, slice, out,
+                              out + nq_slice));
+  ctx->launches += 2;
+  return CKV_OK;
+}
+
+int ckv_select_approx(ckv_ctx* ctx, const ckv_shard_select_desc* d, const float* ascores,
+                      const float* q, const float* centroids, const uint32_t* gsize,
+                      const uint32_t* lsize, const uint32_t* lstart, const uint32_t* prefix,
+                      const uint32_t* lsorted, const ckv_runs* runs, uint32_t* token_ids,
+                      uint32_t* n_tokens, uint32_t* n_taken, uint32_t* trimmed,
+                      uint32_t* ranked) {
+  if (!ctx || !d || !ascores || !q || !centroids || !gsize || !lsize || !lstart || !prefix ||
+      !runs || !runs->row || !n_tokens || !n_taken || !trimmed || !ranked) {
+    set_error("ckv_select_approx: NULL argument");
+    return CKV_EINVAL;
+  }
+  if (d->C == 0 || d->C > 4096 || d->c_cap < d->C || runs->run_cap < d->C + 2 ||
+      d->slice * d->world < d->C || (token_ids && !lsorted)) {
+    set_error("ckv_select_approx: need 1 <= C <= 4096 <= c_cap, run_cap >= C + 2, "
+              "slice * world >= C, lsorted with token_ids");
+    return CKV_EINVAL;
+  }
+  if (d->n_q == 0) return CKV_OK;
+  uint32_t p2 = 32;
+  while (p2 < d->C) p2 <<= 1;
+  const size_t smem = size_t(p2) * 8 + size_t(p2) * 4 * 4 + 4 + size_t(p2) * 4 * 2 + 16;
+  static int attr = 0;
+  if (!attr) {
+    CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_approx, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+    attr = 1;
+  }
+  k_select_approx<<<d->n_q, SR_THREADS, smem, ctx->stream>>>(
+      *d, p2, ascores, q, centroids, gsize, lsize, lstart, prefix, lsorted, *runs, token_ids,
+      n_tokens, n_taken, trimmed, ranked);
+  CKV_LAUNCH_CHECK("k_select_approx");
   ctx->launches++;
   return CKV_OK;
 }

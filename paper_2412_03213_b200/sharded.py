@@ -421,6 +421,7 @@ class ShardedDecoder:
         self.trimmed = torch.zeros((nq,), dtype=torch.int32, device=dev)
         self.ranked = torch.zeros((nq, C_), dtype=torch.int32, device=dev)
         self.my_scores = torch.zeros((nq, self.slice), dtype=torch.float64, device=dev)
+        self.my_approx = torch.zeros((2, nq, self.slice), dtype=torch.float32, device=dev)
         self.out_loc = torch.zeros((nq, D), dtype=torch.float32, device=dev)
         self.lse = torch.zeros((nq,), dtype=torch.float32, device=dev)
         self.sdesc = N.ShardSelectDesc(nq, group, budget, C_, C_, self.slice, self.comm.world,
@@ -430,24 +431,36 @@ class ShardedDecoder:
         self.adesc = N.AttendDesc(nq, group, self.p_cap, self.sel_cap, self.sel_cap)
 
     def step(self, q: torch.Tensor, want_ids: bool = False, want_weights: bool = False,
-             full_rank: bool = False) -> dict:
-        """One decode step for every q head; q: device f32 [n_q][128]."""
+             full_rank: bool = False, exact_scores: bool = False) -> dict:
+        """One decode step for every q head; q: device f32 [n_q][128].
+
+        The all-gathered scores are approximate f32 values with rigorous bounds
+        (ckv_score_range_approx; the selection re-scores the few clusters near
+        the budget cut exactly), or, with exact_scores, the exact f64 scores
+        (ckv_score_range) — the same selection either way."""
         L, h = lib(), self.ctx.h
         q = q.contiguous()
         dev = q.device
-        check(L.ckv_score_range(h, self.U, self.G, q.data_ptr(), self.cents.data_ptr(), self.C,
-                                self.C, self.c_lo, self.slice, self.my_scores.data_ptr()))
-        scores = torch.stack([t.to(dev) for t in self.comm.all_gather(self.my_scores)])
         ids = (torch.zeros((self.n_q, self.sel_cap), dtype=torch.int32, device=dev)
                if want_ids else None)
         self.sdesc.flags = N.CKV_SEL_FULL_RANK if full_rank else 0
-        check(L.ckv_select_scored(h, C.byref(self.sdesc), scores.data_ptr(),
-                                  self.gsize.data_ptr(), self.lsize.data_ptr(),
-                                  self.lstart.data_ptr(), self.prefix.data_ptr(),
-                                  self.lsorted.data_ptr(), C.byref(self.runs),
-                                  None if ids is None else ids.data_ptr(),
-                                  self.n_tokens.data_ptr(), self.n_taken.data_ptr(),
-                                  self.trimmed.data_ptr(), self.ranked.data_ptr()))
+        common = (self.gsize.data_ptr(), self.lsize.data_ptr(), self.lstart.data_ptr(),
+                  self.prefix.data_ptr(), self.lsorted.data_ptr(), C.byref(self.runs),
+                  None if ids is None else ids.data_ptr(), self.n_tokens.data_ptr(),
+                  self.n_taken.data_ptr(), self.trimmed.data_ptr(), self.ranked.data_ptr())
+        if exact_scores:
+            check(L.ckv_score_range(h, self.U, self.G, q.data_ptr(), self.cents.data_ptr(),
+                                    self.C, self.C, self.c_lo, self.slice,
+                                    self.my_scores.data_ptr()))
+            scores = torch.stack([t.to(dev) for t in self.comm.all_gather(self.my_scores)])
+            check(L.ckv_select_scored(h, C.byref(self.sdesc), scores.data_ptr(), *common))
+        else:
+            check(L.ckv_score_range_approx(h, self.U, self.G, q.data_ptr(), self.cents.data_ptr(),
+                                           self.C, self.C, self.c_lo, self.slice,
+                                           self.my_approx.data_ptr()))
+            scores = torch.stack([t.to(dev) for t in self.comm.all_gather(self.my_approx)])
+            check(L.ckv_select_approx(h, C.byref(self.sdesc), scores.data_ptr(), q.data_ptr(),
+                                      self.cents.data_ptr(), *common))
         w = (torch.zeros((self.n_q, self.sel_cap), dtype=torch.float32, device=dev)
              if want_weights else None)
         check(L.ckv_attend_partial(h, C.byref(self.adesc), q.data_ptr(), self.K.data_ptr(),

@@ -30,7 +30,8 @@ def kmeans_rank(rank, world, keys, C_, seeds, max_iters, init_rows, device):
                 obj=r.objective_history)
 
 
-def decode_rank(rank, world, K, V, Q, Kr, Vr, C_, seeds, G, budget, device, full_rank=True):
+def decode_rank(rank, world, K, V, Q, Kr, Vr, C_, seeds, G, budget, device, full_rank=True,
+                exact_scores=False):
     """Sharded prefill k-means + one sharded decode step (select + attend)
     on rank `rank`; K, V [U][L][128] prompt, Kr, Vr [U][n_rec][128] the
     recency rows (positions L..), Q [U*G][128].  Returns this rank's share."""
@@ -60,7 +61,8 @@ def decode_rank(rank, world, K, V, Q, Kr, Vr, C_, seeds, G, budget, device, full
     del shard
     dec = ShardedDecoder(km, Kst, Vst, G, budget, comm, sink_rows=sink_rows, n_rec=n_rec,
                          rec_pos=L, ctx=ctx)
-    r = dec.step(torch.from_numpy(Q).to(dev), want_ids=True, want_weights=True, full_rank=full_rank)
+    r = dec.step(torch.from_numpy(Q).to(dev), want_ids=True, want_weights=True, full_rank=full_rank,
+                 exact_scores=exact_scores)
     ctx.sync()
     g = lambda x: x.cpu().numpy()
     return dict(out=g(r["out"]), ids=g(r["token_ids"]), w=g(r["weights"]),

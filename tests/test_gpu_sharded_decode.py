@@ -30,10 +30,11 @@ def _assemble(res, key, h, n_taken):
     return np.concatenate(parts)
 
 
-@pytest.mark.parametrize("world,L,budget,full_rank", [
-    (1, 1040, 256, True), (2, 1040, 256, True), (3, 2064, 300, True), (2, 2064, 5000, True),
-    (1, 1040, 256, False), (2, 2064, 300, False), (3, 4112, 1000, False), (2, 2064, 5000, False)])
-def test_gpu_sharded_decode_matches_reference(gpu_ctx, world, L, budget, full_rank):
+@pytest.mark.parametrize("world,L,budget,full_rank,exact", [
+    (1, 1040, 256, True, False), (2, 1040, 256, True, False), (3, 2064, 300, True, True),
+    (2, 2064, 5000, True, False), (1, 1040, 256, False, False), (2, 2064, 300, False, False),
+    (3, 4112, 1000, False, False), (2, 2064, 5000, False, False), (2, 4112, 700, False, True)])
+def test_gpu_sharded_decode_matches_reference(gpu_ctx, world, L, budget, full_rank, exact):
     from oracle.oracle import ClusterConfig as OCfg
     G, U, n_rec = 2, 2, 5
     hs = [head(9, 0, u, L, T=64) for u in range(U)]
@@ -45,7 +46,7 @@ def test_gpu_sharded_decode_matches_reference(gpu_ctx, world, L, budget, full_ra
     seeds = [port().mix_seed(0, 0, u) for u in range(U)]
     C0 = port().prefill_cluster_count(L, OCfg())
     res = run_world(world, "tests._sharded_workers", "decode_rank", K, V, Q, Kr, Vr, C0, seeds,
-                    G, budget, 0, full_rank)
+                    G, budget, 0, full_rank, exact)
     for u in range(U):
         o = port().cluster_prefill(K[u], OCfg(seed=seeds[u]))
         assert all(int(r["iters"][u]) == o.iterations_used for r in res)
