@@ -129,6 +129,69 @@ __device__ __forceinline__ void block_sort(unsigned long long* key, uint32_t* id
   }
 }
 
+// approximate scores of a centroid slice for the sharded decode step: the
+// same smem-staged layout as k_score_range (a thread per centroid row, the G
+// heads' chains side by side) in f32, plus the rigorous bound
+// e = 2^-14 |q| |mu| >= |a - dot_f64| (an f32 chain of 128 products errs by
+// <= 127 u sum |q_j mu_j| <= 2^-17 |q| |mu|; the factor 8 covers the rounding
+// of the norms).  out [2][n_q][slice]: a, then e.
+constexpr float SA_ERR = 1.0f / 16384.0f;
+template <int G>
+__global__ void __launch_bounds__(SR_ROWS)
+k_score_range_f32(const float* __restrict__ q, const float* __restrict__ cents, uint32_t c_cap,
+                  uint32_t C, uint32_t c_lo, uint32_t c_hi, uint32_t slice, uint32_t n_q,
+                  float* __restrict__ out) {
+  extern __shared__ __align__(16) float sr_sm[];
+  float* crow = sr_sm;                  // [SR_ROWS][SR_LD]
+  float* qs = sr_sm + SR_ROWS * SR_LD;  // [G][D]
+  __shared__ float qn[G];
+  const uint32_t u = blockIdx.x;
+  const uint32_t t0 = c_lo + blockIdx.y * SR_ROWS;
+  const uint32_t hi = min(c_hi, C);
+  if (t0 >= hi) return;
+  const uint32_t nrow = min(uint32_t(SR_ROWS), hi - t0);
+  const float4* cu = reinterpret_cast<const float4*>(cents + (size_t(u) * c_cap + t0) * D);
+  for (uint32_t e = threadIdx.x; e < nrow * (D / 4); e += SR_ROWS)
+    *reinterpret_cast<float4*>(crow + (e / (D / 4)) * SR_LD + 4 * (e % (D / 4))) = __ldg(cu + e);
+  const float4* qu = reinterpret_cast<const float4*>(q + size_t(u) * G * D);
+  for (uint32_t e = threadIdx.x; e < G * D / 4; e += SR_ROWS)
+    reinterpret_cast<float4*>(qs)[e] = __ldg(qu + e);
+  __syncthreads();
+  if (threadIdx.x < G) {
+    float n2 = 0.f;
+    for (int j = 0; j < D; ++j) n2 = fmaf(qs[threadIdx.x * D + j], qs[threadIdx.x * D + j], n2);
+    qn[threadIdx.x] = SA_ERR * sqrtf(n2);
+  }
+  __syncthreads();
+  const uint32_t r = threadIdx.x;
+  if (r >= nrow) return;
+  float sacc[G], mn2 = 0.f;
+#pragma unroll
+  for (int g = 0; g < G; ++g) sacc[g] = 0.f;
+  const float* row = crow + r * SR_LD;
+#pragma unroll 4
+  for (int j = 0; j < D; j += 4) {
+    const float4 m = *reinterpret_cast<const float4*>(row + j);
+    mn2 = fmaf(m.x, m.x, fmaf(m.y, m.y, fmaf(m.z, m.z, fmaf(m.w, m.w, mn2))));
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float4 x = *reinterpret_cast<const float4*>(qs + g * D + j);
+      sacc[g] = fmaf(x.x, m.x, sacc[g]);
+      sacc[g] = fmaf(x.y, m.y, sacc[g]);
+      sacc[g] = fmaf(x.z, m.z, sacc[g]);
+      sacc[g] = fmaf(x.w, m.w, sacc[g]);
+    }
+  }
+  const float mn = sqrtf(mn2);
+  const size_t plane = size_t(n_q) * slice;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const size_t o = (size_t(u) * G + g) * slice + (t0 + r - c_lo);
+    out[o] = sacc[g];
+    out[plane + o] = fmaf(qn[g], mn, 1e-30f);
+  }
+}
+
 __global__ void __launch_bounds__(SR_THREADS)
 k_select_scored(ckv_shard_select_desc d, uint32_t p2, const double* __restrict__ scores,
                 const uint32_t* __restrict__ gsize, const uint32_t* __restrict__ lsize,
@@ -709,11 +772,6 @@ __global__ void k_lse_merge(uint32_t n_q, uint32_t world, uint32_t rank,
   }
 }
 
-__global__ void k_fill_u32(uint32_t* __restrict__ p, uint32_t n, uint32_t v) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
-}
-
 __global__ void k_fill_empty(uint32_t n_q, float* __restrict__ out, float* __restrict__ lse) {
   const uint32_t h = blockIdx.x;
   out[size_t(h) * D + threadIdx.x] = 0.f;
@@ -807,16 +865,30 @@ int ckv_score_range_approx(ckv_ctx* ctx, uint32_t n_units, uint32_t group, const
   }
   if (n_units == 0 || c_lo >= C) return CKV_OK;
   cudaStream_t st = ctx->stream;
-  void* cnt = nullptr;
-  CKV_TRY(ctx_scratch(ctx, 22, size_t(n_units) * 4, false, &cnt));
-  const uint32_t rows = std::min(slice, C - c_lo);
-  k_fill_u32<<<(n_units + 255) / 256, 256, 0, st>>>(static_cast<uint32_t*>(cnt), n_units, rows);
-  CKV_LAUNCH_CHECK("k_fill_u32");
-  const size_t nq_slice = size_t(n_units) * group * slice;
-  CKV_TRY(launch_score_approx(st, group, n_units, q, centroids + size_t(c_lo) * D,
-                              static_cast<const uint32_t*>(cnt), c_cap, slice, out,
-                              out + nq_slice));
-  ctx->launches += 2;
+  const uint32_t n_q = n_units * group, c_hi = c_lo + slice;
+  static bool attr = false;
+  if (!attr) {
+    for (auto fn : {k_score_range_f32<1>, k_score_range_f32<2>, k_score_range_f32<4>,
+                    k_score_range_f32<8>})
+      CKV_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (SR_ROWS * SR_LD + 8 * D) * 4));
+    attr = true;
+  }
+#define CKV_SA(GG)                                                                           \
+  case GG: {                                                                                 \
+    dim3 grid(n_units, (slice + SR_ROWS - 1) / SR_ROWS);                                     \
+    const size_t sm = (SR_ROWS * SR_LD + GG * D) * 4;                                        \
+    k_score_range_f32<GG><<<grid, SR_ROWS, sm, st>>>(q, centroids, c_cap, C, c_lo, c_hi,      \
+                                                     slice, n_q, out);                       \
+    break;                                                                                   \
+  }
+  switch (group) {
+    CKV_SA(1) CKV_SA(2) CKV_SA(4) CKV_SA(8)
+    default: set_error("ckv_score_range_approx: group must be 1, 2, 4 or 8"); return CKV_EINVAL;
+  }
+#undef CKV_SA
+  CKV_LAUNCH_CHECK("k_score_range_f32");
+  ctx->launches++;
   return CKV_OK;
 }
 
