@@ -576,46 +576,31 @@ def run_config_E(args, rank, world, torch, dev, ctx, hbm):
 def run_config_A(args, torch, dev, ctx):
     """configs[0]: the reference's own CPU-runnable case — one layer of the
     Llama-3-8B shape (8 kv / 32 q heads), 4k prompt, cosine k-means (C0 = 51),
-    then decode steps at B = 1024.  The same synthetic heads (the reference
-    generator, trace.hpp:134-198, rounded to bf16) run through our session on
-    the GPU and through the compiled reference (oracle/_ref) on all host
-    threads: prefill (cluster_prefill of every head) and one decode step
+    then decode steps at B = 1024.  The same synthetic heads (drawn on the
+    device with the reference generator's distributions, trace.hpp:134-198,
+    rounded to bf16) run through our session on the GPU and — copied to the
+    host — through the compiled reference (oracle/_ref) on all host threads:
+    prefill (cluster_prefill of every head) and one decode step
     (select_tokens + approx_attention of every q head)."""
-    from oracle.oracle import ClusterConfig as OCfg
-    from oracle.oracle import Oracle, build, ref_available, to_bf16_representable
+    from paper_2412_03213_b200 import _native as N
     from paper_2412_03213_b200.api import ClusterConfig
     from paper_2412_03213_b200.session import Session
-    if not ref_available():
-        build(ref=True)
-    P, R = Oracle("port"), Oracle("reference")
-    n_kv, G, L, B, T = 8, 4, 4096, 1024, 256
-    heads = [P.generate_head(P.mix_seed(7, 0, h), L, T) for h in range(n_kv)]
-    K = np.stack([to_bf16_representable(h.prompt_keys) for h in heads])
-    V = np.stack([to_bf16_representable(h.prompt_values) for h in heads])
-    Q = [np.stack([to_bf16_representable(h.decode_queries[(t + r * (T // G)) % T])
-                   for h in heads for r in range(G)]) for t in range(T)]
-    bits = lambda x: (np.ascontiguousarray(x, np.float32).view(np.uint32) >> 16).astype(np.uint16)
-    cores = int(R.lib.ref_hardware_concurrency())
-    # ---- CPU reference -----------------------------------------------------
-    seeds = np.array([P.mix_seed(0, 0, h) for h in range(n_kv)], np.uint64)
-    kptr = (C.c_void_p * n_kv)(*[K[h].ctypes.data for h in range(n_kv)])
-    passes = np.zeros(1, np.uint64)
-    cpu_prefill = float(np.median([R.lib.ref_prefill_cpu(kptr, n_kv, L, D, seeds, 50, cores,
-                                                         passes) for _ in range(3)]))
-    models = [R.cluster_prefill(K[h], OCfg(seed=P.mix_seed(0, 0, h))) for h in range(n_kv)]
-    sample = ([np.ascontiguousarray(m.centroids) for m in models],
-              np.array([m.n_clusters for m in models], np.uint32),
-              [np.ascontiguousarray(m.labels) for m in models], list(K), list(V),
-              np.ascontiguousarray(Q[0]))
-    cpu_decode_reps = [cpu_reference_decode(sample, cores, G, L, B) for _ in range(6)]
-    cpu_step = float(np.median(cpu_decode_reps[1:]))  # one layer = one step here
-    # ---- GPU ------------------------------------------------------------------
+    n_kv, G, L, B = 8, 4, 4096, 1024
     steps = args.steps
+    T = steps + args.warmup + 2
+    g, centers = gen_inputs(torch, dev, n_kv, G, L, T, seed=7)
+    K = torch.empty((n_kv, L, D), dtype=torch.int16, device=dev)
+    V = torch.empty_like(K)
+    fill_kv(torch, dev, g, centers, K, V, L)
+    q_all, kn_all, vn_all = gen_decode(torch, dev, g, centers, G, T)
+    seeds = [int(N.lib().ckv_mix_seed(0, 0, h)) for h in range(n_kv)]
+    # ---- GPU ------------------------------------------------------------------
     gpu_prefill = []
-    for rep in range(4):  # the session re-lays its store, so reload the prompt each time
-        sess = Session(n_kv, G, L, steps + args.warmup + 2, B, retention=1, cfg=ClusterConfig(),
-                       kv_heads=n_kv, ctx=ctx)
-        sess.load_prompt_host(bits(K), bits(V))
+    for rep in range(4):  # the session re-lays its store: a fresh one per prefill
+        sess = Session(n_kv, G, L, T, B, retention=1, cfg=ClusterConfig(), kv_heads=n_kv,
+                       ctx=ctx)
+        sess.K[:, :L].copy_(K)
+        sess.V[:, :L].copy_(V)
         e = _events(torch, 2)
         e[0].record()
         sess.prefill()
@@ -623,27 +608,45 @@ def run_config_A(args, torch, dev, ctx):
         torch.cuda.synchronize()
         if rep:
             gpu_prefill.append(e[0].elapsed_time(e[1]))
-    qd = [torch.from_numpy(Q[t]).to(dev) for t in range(steps + args.warmup)]
-    kn = torch.from_numpy(bits(np.stack([h.decode_keys[0] for h in heads])).view(np.int16)).to(dev)
-    vn = torch.from_numpy(bits(np.stack([h.decode_values[0] for h in heads])).view(np.int16)).to(dev)
     out = torch.empty((n_kv * G, D), dtype=torch.float32, device=dev)
     for t in range(args.warmup):
-        sess.step(qd[t], kn, vn, out)
+        sess.step(q_all[t], kn_all[t], vn_all[t], out)
     e = _events(torch, 2)
     torch.cuda.synchronize()
     e[0].record()
     for t in range(steps):
-        sess.step(qd[args.warmup + t], kn, vn, out)
+        sess.step(q_all[args.warmup + t], kn_all[args.warmup + t], vn_all[args.warmup + t], out)
     e[1].record()
     torch.cuda.synchronize()
     gpu_step = e[0].elapsed_time(e[1]) / steps
     gp = float(np.median(gpu_prefill))
+    # ---- CPU reference (the cpu_baseline leg) -----------------------------------
+    from oracle.oracle import ClusterConfig as OCfg
+    from oracle.oracle import Oracle, build, ref_available
+    if not ref_available():
+        build(ref=True)
+    R = Oracle("reference")
+    cores = int(R.lib.ref_hardware_concurrency())
+    f32 = lambda t16: np.ascontiguousarray((t16.to(torch.int32) << 16).view(torch.float32).cpu().numpy())
+    Kh, Vh = f32(K), f32(V)
+    seeds_np = np.array(seeds, np.uint64)
+    kptr = (C.c_void_p * n_kv)(*[Kh[h].ctypes.data for h in range(n_kv)])
+    passes = np.zeros(1, np.uint64)
+    cpu_prefill = float(np.median([R.lib.ref_prefill_cpu(kptr, n_kv, L, D, seeds_np, 50, cores,
+                                                         passes) for _ in range(3)]))
+    models = [R.cluster_prefill(Kh[h], OCfg(seed=seeds[h])) for h in range(n_kv)]
+    sample = ([np.ascontiguousarray(m.centroids) for m in models],
+              np.array([m.n_clusters for m in models], np.uint32),
+              [np.ascontiguousarray(m.labels) for m in models], list(Kh), list(Vh),
+              np.ascontiguousarray(q_all[0].cpu().numpy()))
+    cpu_decode_reps = [cpu_reference_decode(sample, cores, G, L, B) for _ in range(6)]
+    cpu_step = float(np.median(cpu_decode_reps[1:]))  # one layer = one step here
     return {"metric": "config A: prefill ms and decode step us (1 layer, 8 kv / 32 q, 4k, "
                       "B=1024), GPU vs the compiled reference on host threads",
             "value": gpu_step * 1e3, "unit": "us/step", "n_gpus": 1, "steps": steps,
             "warmup": args.warmup, "ms_per_step": gpu_step, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16 KV, f32/f64 math",
-            "data": "synthetic (the reference generator, trace.hpp, seed 7; bf16-rounded)",
+            "data": "synthetic (device draw with trace.hpp generator distributions, bf16)",
             "config": {"workload": "config A: Llama-3-8B head shape, 1 layer, 8 kv x 4 q heads, "
                                    "4096-token prompt, C0 = 51, B = 1024",
                        "global_batch": 1, "seq_len": L},
@@ -655,16 +658,17 @@ def run_config_A(args, torch, dev, ctx):
                              "kind": "reference",
                              "sample": "the whole config-A step: select_tokens + "
                                        "approx_attention of all 32 q heads (median of 5), and "
-                                       "cluster_prefill of all 8 heads (median of 3)"}}
+                                       "cluster_prefill of all 8 heads (median of 3), on the "
+                                       "same bf16 heads copied to the host"}}
 
 
 def run_page_baseline(torch, dev, ctx, sess, U, G, L, B, q, hbm, ps=16, kv_heads=8):
     """the page-select baseline (selection.hpp:136-194) on the
     same prompts, same queries, same budget: GPU latency of page select +
-    attend over a position-ordered store, and the recall of both selections
-    against the exact top-B (exact_topb, selection.hpp:115-132) on a sample
-    (the first layer's q heads; CPU oracle)."""
-    from oracle.oracle import Oracle
+    attend over a position-ordered store, and the quality of both selections
+    for every q head on the GPU (ckv_metrics.cu): recall against the exact
+    top-B (exact_topb, selection.hpp:115-132) and the output error against
+    full attention (harness.hpp:228-310)."""
     from paper_2412_03213_b200 import _native as N
     st = sess.state()
     n = L - 16
@@ -738,26 +742,33 @@ def run_page_baseline(torch, dev, ctx, sess, U, G, L, B, q, hbm, ps=16, kv_heads
                                ptrs[4], ptrs[5], tok.data_ptr(), None, C.byref(runs2),
                                ntc.data_ptr(), tmp[0].data_ptr(), tmp[1].data_ptr(),
                                rk.data_ptr(), None, None))
-    P = Oracle("port")
-    bf = lambda t16: (t16.to(torch.int32) << 16).view(torch.float32).cpu().numpy()
-    rc_, rp_ = [], []
-    for u in range(kv_heads):
-        Kh = np.ascontiguousarray(bf(Kp[u]))
-        for g in range(G):
-            h = u * G + g
-            truth = P.exact_topb(qd[h].cpu().numpy(), Kh, B)
-            ts = set(truth.tolist())
-            cl = tok[h, :int(ntc[h].item())].cpu().numpy()
-            pg = ids[h, :int(nt[h].item())].cpu().numpy()
-            rc_.append(len(ts & set(cl.tolist())) / len(ts))
-            rp_.append(len(ts & set(pg.tolist())) / len(ts))
-    del Kp, Vp, rmax
+    # the cluster selection's attention over the session's cluster-major store
+    cl_out = torch.empty((n_q, D), dtype=torch.float32, device=dev)
+    adc = N.AttendDesc(n_q, G, sess.p_cap, sel_cap, B + 16)
+    N.check(N.lib().ckv_attend(ctx.h, C.byref(adc), qd.data_ptr(), sess.K.data_ptr(),
+                               sess.V.data_ptr(), None, C.byref(runs2), ntc.data_ptr(),
+                               cl_out.data_ptr(), None))
+    # quality of both selections on the device (ckv_metrics.cu), every q head
+    from paper_2412_03213_b200.metrics import StepQuality
+    sq = StepQuality(Kp, Vp, L, G, B, ctx)
+    e = _events(torch, 2)
+    e[0].record()
+    qc = sq(qd, tok, ntc, cl_out)
+    e[1].record()
+    torch.cuda.synchronize()
+    quality_ms = e[0].elapsed_time(e[1])
+    rc_m, lc_m = float(qc["recall"].mean().item()), float(qc["l2_rel"].mean().item())
+    qp = sq(qd, ids, nt, out)
+    rp_m, lp_m = float(qp["recall"].mean().item()), float(qp["l2_rel"].mean().item())
+    del Kp, Vp, rmax, sq
     return {"page_size": ps, "repr": "max", "budget": B,
             "page_select_us": sel_us, "page_attend_us": att_us,
             "page_step_us": sel_us + att_us, "page_reps_ms_once": reps_ms,
-            "recall_sample": f"exact top-{B} (exact_topb, CPU oracle) of the first layer's "
-                             f"{kv_heads * G} q heads at the prompt context",
-            "recall_cluster": float(np.mean(rc_)), "recall_page": float(np.mean(rp_))}
+            "quality": f"every q head ({n_q}) at the prompt context, sinks included in the "
+                       f"cluster selection: recall vs exact top-{B} (exact_topb) and l2_rel vs "
+                       "full attention, on the GPU (ckv_metrics.cu)",
+            "recall_cluster": rc_m, "recall_page": rp_m,
+            "l2_rel_cluster": lc_m, "l2_rel_page": lp_m, "quality_eval_ms": quality_ms}
 
 
 def N_lib():

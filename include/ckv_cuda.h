@@ -433,6 +433,30 @@ int ckv_page_select(ckv_ctx* ctx, const ckv_page_desc* desc, const float* q, con
                     uint32_t* n_tokens);
 
 /* ------------------------------------------------------------------ */
+/* quality metrics (harness.hpp:228-310)             */
+/* ------------------------------------------------------------------ */
+/* exact_topb (selection.hpp:115-132) for n_q queries over a POSITION-ordered
+ * store (keys bf16 [unit][p_cap][128], q head h reads unit h / group): the
+ * min(B, n) positions with the largest dot_f64(q, k), ties to the lower
+ * position, ascending, in ids [n_q][ids_cap].  n <= 49152. */
+int ckv_exact_topb(ckv_ctx* ctx, uint32_t n_q, uint32_t group, uint32_t n, uint32_t p_cap,
+                   const float* q, const uint16_t* keys, uint32_t budget, uint32_t* ids,
+                   uint32_t ids_cap);
+/* recall_rate (attention.hpp:70-93) per q head: |sel ∩ truth| / n_truth;
+ * truth [n_q][truth_cap] ascending (ckv_exact_topb's order), the n_sel[h]
+ * selected ids distinct; recall f64 [n_q]. */
+int ckv_recall(ckv_ctx* ctx, uint32_t n_q, const uint32_t* sel, uint32_t sel_cap,
+               const uint32_t* n_sel, const uint32_t* truth, uint32_t truth_cap, uint32_t n_truth,
+               double* recall);
+/* output_error (attention.hpp:101-131) per q head: l2_rel, cos_sim (f64). */
+int ckv_output_error(ckv_ctx* ctx, uint32_t n_q, const float* approx, const float* exact,
+                     double* l2_rel, double* cos_sim);
+/* one run [0, n) per q head: ckv_attend over it is full_attention
+ * (attention.hpp:53-60) on a position-ordered store. */
+int ckv_full_runs(ckv_ctx* ctx, uint32_t n_q, uint32_t n, const ckv_runs* runs,
+                  uint32_t* n_tokens);
+
+/* ------------------------------------------------------------------ */
 /* session: the batched serving path (simulate_head's ClusterKV branch, */
 /* harness.hpp:155-346, minus the metric oracles), device-resident.     */
 /* ------------------------------------------------------------------ */

@@ -140,6 +140,10 @@ SIGNATURES = {
     "ckv_attend_merge": (C.c_int, [vp, u32, u32, u32, vp, vp, vp, vp, vp, u32]),
     "ckv_page_reps": (C.c_int, [vp, u32, u32, u32, u32, u32, vp, vp, vp]),
     "ckv_page_select": (C.c_int, [vp, C.POINTER(PageDesc), vp, vp, vp, C.POINTER(Runs), vp, vp]),
+    "ckv_exact_topb": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, u32, vp, u32]),
+    "ckv_recall": (C.c_int, [vp, u32, vp, u32, vp, vp, u32, u32, vp]),
+    "ckv_output_error": (C.c_int, [vp, u32, vp, vp, vp, vp]),
+    "ckv_full_runs": (C.c_int, [vp, u32, u32, C.POINTER(Runs), vp]),
     "ckv_build_index": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp]),
     "ckv_select": (C.c_int, [vp, C.POINTER(SelectDesc), vp, vp, vp, vp, vp, vp, vp, vp,
                              C.POINTER(Runs), vp, vp, vp, vp, vp, vp]),
