@@ -66,6 +66,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// Every consumer thread arrives on a ring slot's empty barrier (count
+// AT_CWARPS * 32) instead of one elected lane after __syncwarp: the same
+// ordering, but expressed per thread so compute-sanitizer's racecheck can see
+// it (it does not treat __syncwarp as ordering a lane's reads before another
+// lane's arrive).  Measured: 118.8-119.1 vs 118.4-118.9 us per config B step.
+#ifndef CKV_AT_ARRIVE_ALL
+#define CKV_AT_ARRIVE_ALL 1
+#endif
+constexpr uint32_t AT_EMPTY_COUNT = CKV_AT_ARRIVE_ALL ? AT_CWARPS * 32 : AT_CWARPS;
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
@@ -152,11 +161,11 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
   if (t == 0) {
     for (int s = 0; s < AT_STAGES; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], AT_CWARPS);
+      mbar_init(&sm.empty[s], AT_EMPTY_COUNT);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.qfull[s], 1);
-      mbar_init(&sm.qempty[s], AT_CWARPS);
+      mbar_init(&sm.qempty[s], AT_EMPTY_COUNT);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -209,7 +218,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
         for (uint32_t e = it.e0; e < it.e1; e += AT_TILE) {
           const uint32_t te = min(e + AT_TILE, it.e1);
           mbar_wait(&sm.empty[st], ph ^ 1);
-          mbar_expect_tx(&sm.full[st], (te - e) * D * 2 * 2);
+            mbar_expect_tx(&sm.full[st], (te - e) * D * 2 * 2);
           for (uint32_t x = e; x < te;) {
             uint32_t row, n;
             if (rows) {
@@ -251,8 +260,12 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       qv[0] = a.x * qscale; qv[1] = a.y * qscale; qv[2] = a.z * qscale; qv[3] = a.w * qscale;
       qv[4] = b.x * qscale; qv[5] = b.y * qscale; qv[6] = b.z * qscale; qv[7] = b.w * qscale;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.qempty[qs]);
+    if (CKV_AT_ARRIVE_ALL) {
+      mbar_arrive(&sm.qempty[qs]);
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.qempty[qs]);
+    }
     float m = -INFINITY, l = 0.f;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float* lw = WEIGHTS ? logits_ws + size_t(it.h) * desc.sel_cap : nullptr;
@@ -273,8 +286,12 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
         x += __shfl_xor_sync(0xffffffffu, x, 1);
         s[kk] = x;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[st]);  // stage data is in registers now
+      if (CKV_AT_ARRIVE_ALL) {
+        mbar_arrive(&sm.empty[st]);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[st]);
+      }  // stage data is in registers now
       if (++st == AT_STAGES) { st = 0; ph ^= 1; }
       if (full_tile) {
         if (WEIGHTS && hl == 0)
