@@ -3,27 +3,34 @@
 //
 // The reference labels key i with argmax_c dot_f64(k_i, dir_c) (ties -> lowest
 // c), dir_c = normalize(mu_c) in f32.  On B200:
-//   1. a bf16 GEMM S = K . bf16(dir)^T on the 5th-gen tensor cores
+//   1. an fp16 GEMM S = h(K) . h(dir)^T on the 5th-gen tensor cores
 //      (tcgen05.mma kind::f16, fp32 accumulation in TMEM), 128 keys x all C
-//      columns per tile;
+//      columns per tile.  h() = fp16 round-to-nearest, saturated, tiny values
+//      flushed to zero (f32_to_f16_tc): fp16's 11-bit significand makes the
+//      operand error 8x smaller than bf16's, so the band below is ~6x
+//      narrower and ~6x fewer keys need the f64 fix-up.  The bf16 keys are
+//      converted once per k-means run (k_scan_keys), exactly in the normal
+//      range; whatever is lost is measured per key and enters the band;
 //   2. the epilogue (tcgen05.ld, ONE pass over the accumulator) keeps a
 //      running max M and the columns within a band of it.  The error of a
-//      tensor-core score is |S_c - s_c| <= |k| |dir_c - bf16(dir_c)| (the
-//      operand rounding, Cauchy-Schwarz) + |k| 2^-14 (fp32 accumulation of
-//      128 products, conservatively), so the exact argmax lies in
-//      {c : S_c >= M - band}, band = |k| (2 eps_u + 2^-13) * 1.01 with eps_u
-//      = max_c |dir_c - bf16(dir_c)| of the unit (computed exactly when the
-//      dirs are made).  One candidate in band -> that is the label.
+//      tensor-core score is |S_c - s_c| <= |h(k)| |dir_c - h(dir_c)| + |k -
+//      h(k)| |dir_c| (operand rounding, Cauchy-Schwarz) + |h(k)| 2^-14 (fp32
+//      accumulation of 128 exact products, conservatively), so the exact
+//      argmax lies in {c : S_c >= M - band}, band = kn (2 eps_u + 2^-13) *
+//      1.01 + 2.02 kerr_u, kn = |k| + |k - h(k)| (rounded up), eps_u = max_c
+//      |dir_c - h(dir_c)| and kerr_u = max_k |k - h(k)| of the unit (both
+//      computed exactly when the operands are made).  One candidate in band
+//      -> that is the label.
 //      Otherwise the key goes to a fix-up list with its <= 8 candidates (or
 //      "all" when more were in band) and k_fixup decides with f64 dot
-//      products — the sequential dot_f64 chain itself whenever two
-//      candidates are closer than the f64 rounding could separate — taking
-//      the first maximum.  Labels are therefore bit-exact for every key
-//      while the tensor FLOPs stay at 1x.
+//      products of the ORIGINAL bf16 key and f32 dirs — the sequential
+//      dot_f64 chain itself whenever two candidates are closer than the f64
+//      rounding could separate — taking the first maximum.  Labels are
+//      therefore bit-exact for every key while the tensor FLOPs stay at 1x.
 //
 // Kernel anatomy (persistent, one CTA per SM, 6 warps):
 //   warp 0  TMA producer: key tiles (2 stages, 128B-swizzled boxes of
-//           128 rows x 64 cols) and, at each unit change, the unit's bf16
+//           128 rows x 64 cols) and, at each unit change, the unit's fp16
 //           directions (resident B operand, up to 512 rows).
 //   warp 1  TMEM allocator + MMA issuer (one elected thread): per tile and
 //           256-column chunk, 8 K=16 steps into TMEM buffer (chunk & 1).
@@ -42,7 +49,7 @@
 namespace ckvb {
 
 constexpr int TC_M = 128;              // keys per tile (UMMA_M)
-constexpr int TC_BK = 64;              // bf16 columns per 128-B swizzle atom
+constexpr int TC_BK = 64;              // 16-bit columns per 128-B swizzle atom
 constexpr int TC_MAXC = 512;           // columns per range: B resident, 2 x 256 TMEM cols
 constexpr int TC_MAXC_ALL = 4096;      // C_pad limit (ranges of <= TC_MAXC columns)
 constexpr int TC_CH = 256;             // columns per MMA chunk / TMEM buffer
@@ -93,6 +100,28 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
         : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
   } while (!done);
 }
+// bit 31-j of the result set <=> x[j] < lo (the sign of the rounded x[j] - lo;
+// x[j] >= lo gives a difference >= +0).  FADD2 + four interleaved SHF chains.
+__device__ __forceinline__ uint32_t below_mask32(const float* x, float lo) {
+  uint32_t b[4] = {0u, 0u, 0u, 0u};
+  unsigned long long l2;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(l2) : "f"(lo));
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      unsigned long long a2, d2;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(a2) : "f"(x[8 * c + j]), "f"(x[8 * c + j + 1]));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d2) : "l"(a2), "l"(l2));
+      uint32_t r0, r1;
+      asm("mov.b64 {%0, %1}, %2;" : "=r"(r0), "=r"(r1) : "l"(d2));
+      b[c] = __funnelshift_l(r0, b[c], 1);
+      b[c] = __funnelshift_l(r1, b[c], 1);
+    }
+  }
+  // b[c] holds x[8c .. 8c+7] in bits 7..0: word = b0.b1.b2.b3 (bytes, high first)
+  return __byte_perm(__byte_perm(b[3], b[2], 0x0040), __byte_perm(b[1], b[0], 0x0040), 0x5410);
+}
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                        uint64_t* bar) {
   asm volatile(
@@ -111,11 +140,11 @@ __device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
   d |= uint64_t(2) << 61;  // SWIZZLE_128B
   return d;
 }
-// instruction descriptor: kind::f16, A/B bf16, D f32, K-major A and B
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+// instruction descriptor: kind::f16, A/B f16 (format 0), D f32, K-major A and B
+__host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N) {
+  return (1u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{ .reg .pred p; setp.ne.b32 p, %4, 0; "
@@ -204,14 +233,21 @@ struct TcArgs {
   uint32_t key_rows_per_unit;  // key_stride / 128
   uint32_t label_stride;
   const float* knorm;          // [unit][n] key norms (band scale)
-  const float* eps_u;          // [unit] max_c |dir_c - bf16(dir_c)|
+  const float* eps_u;          // [unit] max_c |dir_c - h(dir_c)|
+  const float* kerr_u;         // [unit] max_k |k - h(k)| (k_scan_keys)
   int32_t* labels;
   uint32_t* fix_count;         // [gridDim.x] per-CTA fix-up counts (region = w0 * 128)
   uint4* fix_list;             // {unit, row, n_cand | FULL, 0}
   uint32_t fix_cap;
   uint32_t* fix_ids;           // [fix_cap][8] candidate ids
-  uint32_t mode;               // experiment knob (CKV_TC_MODE): 1 = no epilogue math
+  uint32_t mode;               // experiment knob (CKV_TC_MODE): 1 = no epilogue math,
+                               // 2 = no TMEM reads either (producer + MMA only)
 };
+
+// the score band of a key (see the header): twice one score's error bound
+__device__ __forceinline__ float tc_band(float kn, float eps, float kerr) {
+  return kn * (2.0f * eps + (1.0f / 8192.0f)) * 1.01f + 2.02f * kerr + 1e-30f;
+}
 
 struct TcWork {
   uint32_t ui, range, tile;
@@ -339,13 +375,13 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
           const uint32_t nc = min(uint32_t(TC_CH), cols - c0);
           mb_wait(&sm.acc_empty[buf], bph ^ 1);
           tc_fence_after();
-          const uint32_t idesc = idesc_bf16_f32(TC_M, nc);
+          const uint32_t idesc = idesc_f16_f32(TC_M, nc);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const int kh = kk >> 2, ko = (kk & 3) * 32;  // 16 bf16 = 32 B per K step
+            const int kh = kk >> 2, ko = (kk & 3) * 32;  // 16 halves = 32 B per K step
             const uint64_t ad = kmajor_sw128_desc(su32(A(st, kh)) + ko);
             const uint64_t bd = kmajor_sw128_desc(su32(Bp(kh, c0)) + ko);
-            umma_bf16(tmem + buf * TC_CH, ad, bd, idesc, kk > 0 ? 1u : 0u);
+            umma_f16(tmem + buf * TC_CH, ad, bd, idesc, kk > 0 ? 1u : 0u);
           }
           umma_commit(&sm.acc_full[buf]);
         }
@@ -362,7 +398,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     // Per chunk: (1) block maxima -> m_part; named barrier of the quarter;
     // (2) chunk max M_ch = max of the 4 parts; in-band mask S >= M_ch - band
     // per block; the (rare) in-band ids go to the row's chunk list; barrier.
-    // After the tile's last chunk the quarter's first warp decides each row:
+    // After the tile's last chunk the quarter's last warp decides each row:
     // M = max_ch M_ch; the chunks with M_ch >= M - band contribute their
     // in-band ids (a superset of {c : S_c >= M - band}; it only differs when
     // two chunks are both in band, i.e. the row has >= 2 candidates anyway).
@@ -370,43 +406,61 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
     const uint32_t grp = uint32_t(wid - 2) >> 2;    // 0..3: column share
     const uint32_t lane_row = quarter * 32 + lane;
     const uint32_t bar_id = 1 + quarter;            // named barrier per quarter
+    // the group that records chunk maxima and decides each row after the
+    // tile: the last one, which holds the fewest blocks of a partial last
+    // chunk (blocks are dealt round-robin from group 0)
+    constexpr uint32_t kDecider = TC_EGROUPS - 1;
     auto qbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(4 * 32) : "memory"); };
     uint32_t g = 0;
-    if (grp == 0)
+    if (grp == kDecider)
       for (int ch = 0; ch < 2; ++ch) sm.n_ch[ch][lane_row] = 0;
     // (unit, range, tile) advance incrementally (no integer divisions per
-    // item); the next item's key norm is loaded one item ahead so its
-    // latency hides behind this item's work
-    TcWork wk = tc_work(w0, a), nx = wk;
+    // item).  The NEXT item is resolved one item ahead: its unit id and eps
+    // are re-read only when the unit changes (every tiles_per_unit x n_ranges
+    // items; otherwise the unit_list -> eps_u / knorm loads form a dependent
+    // global chain on every item), and its key norm load is issued one item
+    // before it is used so the latency hides behind this item's chunks.
+    TcWork nx = tc_work(w0, a);
     auto advance = [&](TcWork& k) {
       if (++k.tile == a.tiles_per_unit) {
         k.tile = 0;
         if (++k.range == a.n_ranges) { k.range = 0; ++k.ui; }
       }
     };
-    TcItem itn = w0 < w1 ? tc_item(w0, a) : TcItem{0, 0, 0, 0, 0};
-    float kn_next = 0.f;
-    if (w0 < w1 && itn.tile * TC_M + lane_row < a.n)
-      kn_next = a.knorm[size_t(itn.unit) * a.n + itn.tile * TC_M + lane_row];
-    for (uint32_t w = w0; w < w1; ++w) {
-      if (w > w0 && !a.wlist) advance(wk);
-      const TcItem it = a.wlist ? itn : tc_item_of(wk, a);
-      const uint32_t unit = it.unit, tile = it.tile;
-      const float eps = a.eps_u[unit];
-      const uint32_t row = tile * TC_M + lane_row;
-      const float kn = kn_next;
-      if (w + 1 < w1) {
-        if (a.wlist) {
-          itn = tc_item(w + 1, a);
-        } else {
-          nx = wk;
-          advance(nx);
-          itn = tc_item_of(nx, a);
+    uint32_t nx_ui = ~0u;
+    TcItem itn = TcItem{0, 0, 0, 0, 0};
+    float kn_next = 0.f, eps_next = 0.f, kerr_next = 0.f;
+    auto resolve_next = [&](uint32_t w) {
+      if (a.wlist) {
+        itn = tc_item(w, a);
+        eps_next = a.eps_u[itn.unit];
+        kerr_next = a.kerr_u[itn.unit];
+      } else {
+        if (nx.ui != nx_ui) {
+          nx_ui = nx.ui;
+          itn.unit = uint32_t(a.unit_list[nx.ui]);
+          eps_next = a.eps_u[itn.unit];
+          kerr_next = a.kerr_u[itn.unit];
         }
-        const uint32_t r2 = itn.tile * TC_M + lane_row;
-        kn_next = r2 < a.n ? a.knorm[size_t(itn.unit) * a.n + r2] : 0.f;
+        itn.tile = nx.tile;
+        itn.cbeg = nx.range * a.rc;
+        itn.ccnt = tc_cols(nx.range, a);
+        itn.slot = nx.range;
       }
-      const float band = kn * (2.0f * eps + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
+      const uint32_t r2 = itn.tile * TC_M + lane_row;
+      kn_next = r2 < a.n ? a.knorm[size_t(itn.unit) * a.n + r2] : 0.f;
+    };
+    if (w0 < w1) resolve_next(w0);
+    for (uint32_t w = w0; w < w1; ++w) {
+      const TcItem it = itn;
+      const float eps = eps_next, kn = kn_next, kerr = kerr_next;
+      const uint32_t unit = it.unit, tile = it.tile;
+      const uint32_t row = tile * TC_M + lane_row;
+      if (w + 1 < w1) {
+        if (!a.wlist) advance(nx);
+        resolve_next(w + 1);
+      }
+      const float band = tc_band(kn, eps, kerr);
       const uint32_t cols = it.ccnt, cbase = it.cbeg;
       const uint32_t nchunks = (cols + TC_CH - 1) / TC_CH;
 #pragma unroll 1
@@ -420,6 +474,12 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
         float v[64];
         mb_wait(&sm.acc_full[buf], bph);
         tc_fence_after();
+        if (a.mode == 2) {  // experiment: producer + MMA rate only
+          __syncwarp();
+          if (lane == 0) mb_arrive(&sm.acc_empty[buf]);
+          if (grp == kDecider) sm.m_ch[ch][lane_row] = 0.f;
+          continue;
+        }
         const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * TC_CH;
         if (h0) tmem_ld32_nw(taddr + b0 * 32, v);
         if (h1) tmem_ld32_nw(taddr + b1 * 32, v + 32);
@@ -429,7 +489,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
         if (lane == 0) mb_arrive(&sm.acc_empty[buf]);  // scores now live in registers
         const uint32_t cb0 = c0 + b0 * 32, cb1 = c0 + b1 * 32;
         if (a.mode == 1) {
-          if (grp == 0) sm.m_ch[ch][lane_row] = 0.f;
+          if (grp == kDecider) sm.m_ch[ch][lane_row] = 0.f;
           qbar();
           qbar();
           continue;
@@ -470,26 +530,22 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
         float mc = sm.m_part[0][lane_row];
 #pragma unroll
         for (int q = 1; q < TC_EGROUPS; ++q) mc = fmaxf(mc, sm.m_part[q][lane_row]);
-        if (grp == 0) sm.m_ch[ch][lane_row] = mc;
+        if (grp == kDecider) sm.m_ch[ch][lane_row] = mc;
         // band relative to the running max of the tile's chunks so far: a
         // later chunk far below an earlier one contributes no candidates
         // (still a superset of {c : S_c >= M - band}, M the final max)
         const float lo = (ch > 0 ? fmaxf(mc, sm.m_ch[0][lane_row]) : mc) - band;
-        // (2) in-band mask: sign of S - lo (FADD, FMA pipe) funnel-shifted into
-        // a word (SHF, ALU pipe): bit 31-j set  <=>  S_j < lo
+        // (2) in-band mask: sign of S - lo (FADD2, two scores per FMA-pipe op)
+        // funnel-shifted into a word (SHF, ALU pipe): bit 31-j set <=> S_j < lo.
+        // Four independent 8-bit chains per block (joined by PRMT) so the
+        // shifts do not form one 32-long dependency chain; both blocks' chains
+        // sit in one basic block so they interleave.
         uint32_t in0 = 0u, in1 = 0u;
-        if (h0) {
-          uint32_t below = 0u;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) below = __funnelshift_l(__float_as_uint(v[j] - lo), below, 1);
-          in0 = ~below;
-        }
         if (h1) {
-          uint32_t below = 0u;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            below = __funnelshift_l(__float_as_uint(v[32 + j] - lo), below, 1);
-          in1 = ~below;
+          in0 = ~below_mask32(v, lo);
+          in1 = ~below_mask32(v + 32, lo);
+        } else if (h0) {
+          in0 = ~below_mask32(v, lo);
         }
         // (3) the rare in-band columns -> the row's chunk list
         while (in0 | in1) {
@@ -503,7 +559,7 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
         }
         qbar();
       }
-      if (grp == 0) {
+      if (grp == kDecider) {
         if (row < a.n && a.mode == 0) {
           float M = sm.m_ch[0][lane_row];
           if (nchunks > 1) M = fmaxf(M, sm.m_ch[1][lane_row]);
@@ -705,6 +761,7 @@ __global__ void __launch_bounds__(256)
 k_assign_merge(const float4* __restrict__ summ, uint32_t n_ranges, uint32_t n,
                const int32_t* __restrict__ unit_list, const int32_t* __restrict__ n_list,
                const float* __restrict__ knorm, const float* __restrict__ eps_u,
+               const float* __restrict__ kerr_u,
                int32_t* __restrict__ labels, uint32_t label_stride, uint4* __restrict__ fix_list,
                uint32_t* __restrict__ fix_ids, uint32_t* __restrict__ fix_n, uint32_t fix_cap) {
   const uint32_t ui = blockIdx.y;
@@ -715,8 +772,7 @@ k_assign_merge(const float4* __restrict__ summ, uint32_t n_ranges, uint32_t n,
   uint32_t nin = 0, ids[TC_NCAND];
   if (row < n) {
     const float4* sp = summ + (size_t(unit) * n + row) * n_ranges;
-    const float band = knorm[size_t(unit) * n + row] * (2.0f * eps_u[unit] + (1.0f / 8192.0f)) *
-                       1.01f + 1e-30f;
+    const float band = tc_band(knorm[size_t(unit) * n + row], eps_u[unit], kerr_u[unit]);
     float M = -INFINITY;
     for (uint32_t r = 0; r < n_ranges; ++r) M = fmaxf(M, sp[r].x);
     full = !(M > -INFINITY);
@@ -777,6 +833,9 @@ struct TcScratch {
   uint32_t* fix_ids;
   float* knorm;
   float* eps_u;
+  float* kerr;     // [unit] max_k |k - h(k)| (float bits, atomicMax'd as u32)
+  uint16_t* k16;   // [unit][n_pad][128] the fp16 tensor-core copy of the keys
+  uint32_t n_pad;
   float4* summ;  // C > 512 only: per-(key, range) summaries
   uint32_t fix_cap;
 };
@@ -805,6 +864,11 @@ TcScratch carve(void* base, uint32_t n_units, uint32_t n) {
   p += align256(size_t(n_units) * n * 4);
   s.eps_u = reinterpret_cast<float*>(p);
   p += align256(size_t(n_units) * 4) + 256;
+  s.kerr = reinterpret_cast<float*>(p);
+  p += align256(size_t(n_units) * 4);
+  s.n_pad = (n + TC_M - 1) / TC_M * TC_M;
+  s.k16 = reinterpret_cast<uint16_t*>(p);
+  p += align256(size_t(n_units) * s.n_pad * D * 2);
   s.summ = reinterpret_cast<float4*>(p);  // sized by assign_tc_scratch_bytes
   return s;
 }
@@ -832,7 +896,7 @@ int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows
     set_error("cuTensorMapEncodeTiled unavailable from the driver");
     return CKV_ECUDA;
   }
-  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                                       const_cast<void*>(base), dims, strides, box, estr,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -845,10 +909,12 @@ int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows
 }
 }  // namespace
 
-// key norms (the band scale) live in the scratch; k_scan_keys (ckv_kmeans.cu)
-// fills them once per k-means run, keys never change
-float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n) {
-  return carve(scratch, n_units, n).knorm;
+// the tensor-core key operands live in the scratch: k_scan_keys (ckv_kmeans.cu)
+// fills the fp16 copy, the band norms and the per-unit conversion error once
+// per k-means run (keys never change); kerr must be zeroed before it runs
+TcKeyPrep assign_tc_keyprep(void* scratch, uint32_t n_units, uint32_t n) {
+  const TcScratch s = carve(scratch, n_units, n);
+  return TcKeyPrep{s.knorm, s.k16, s.n_pad, reinterpret_cast<uint32_t*>(s.kerr)};
 }
 
 size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
@@ -857,7 +923,8 @@ size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
   tc_ranges((C + 31) / 32 * 32, &nr, &rc);
   const size_t summ = nr > 1 ? size_t(n_units) * n * nr * 16 : 0;
   return align256(size_t(n_units) * 4) + 256 + 4096 + align256(cap * 16) + align256(cap * 32) + align256(size_t(n_units) * n * 4) +
-         align256(size_t(n_units) * 4) + 256 + summ;
+         align256(size_t(n_units) * 4) + 256 + align256(size_t(n_units) * 4) +
+         align256(cap * D * 2) + summ;
 }
 
 // k_assign_tc with as many key-tile stages as fit next to B (rc columns)
@@ -892,7 +959,7 @@ static int launch_tc(cudaStream_t st, const CUtensorMap& kmap, const CUtensorMap
 }
 
 int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
-              uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs_bf,
+              uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs16,
               const float* deps, const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
               void* scratch, size_t scratch_bytes, uint64_t* launches) {
   (void)scratch_bytes;
@@ -905,10 +972,12 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   CKV_LAUNCH_CHECK("k_compact_active");
   k_eps_max<<<(n_units + 7) / 8, 256, 0, st>>>(deps, c_pad, n_units, s.eps_u);
   CKV_LAUNCH_CHECK("k_eps_max");
+  // A operand: the fp16 key copy (k_scan_keys), [unit][n_pad][128]; the
+  // fix-up keeps scoring the original bf16 keys
   CUtensorMap kmap, dmap;
-  const uint32_t rows_per_unit = uint32_t(key_stride / D);
-  CKV_TRY(encode_2d(&kmap, keys, uint64_t(n_units - 1) * rows_per_unit + n, TC_M));
-  CKV_TRY(encode_2d(&dmap, dirs_bf, uint64_t(n_units) * c_pad, TC_BOXR));
+  const uint32_t rows_per_unit = s.n_pad;
+  CKV_TRY(encode_2d(&kmap, s.k16, uint64_t(n_units) * rows_per_unit, TC_M));
+  CKV_TRY(encode_2d(&dmap, dirs16, uint64_t(n_units) * c_pad, TC_BOXR));
   TcArgs ta;
   ta.unit_list = s.list;
   ta.n_list = s.count;
@@ -920,6 +989,7 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   ta.label_stride = label_stride;
   ta.knorm = s.knorm;
   ta.eps_u = s.eps_u;
+  ta.kerr_u = s.kerr;
   ta.labels = labels;
   ta.fix_count = s.fix_count;
   ta.fix_list = s.fix_list;
@@ -938,7 +1008,7 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
     CKV_LAUNCH_CHECK("k_fixup");
   } else {
     k_assign_merge<<<dim3((n + 255) / 256, n_units), 256, 0, st>>>(
-        s.summ, ta.n_ranges, n, s.list, s.count, s.knorm, s.eps_u, labels, label_stride,
+        s.summ, ta.n_ranges, n, s.list, s.count, s.knorm, s.eps_u, s.kerr, labels, label_stride,
         s.fix_list, s.fix_ids, s.fix_count + TC_MERGE_SLOT, s.fix_cap);
     CKV_LAUNCH_CHECK("k_assign_merge");
     // one region (gridDim.y = 1) holding the merged list
@@ -1061,7 +1131,7 @@ __global__ void __launch_bounds__(256)
 k_mcr_emit(uint32_t U, uint32_t C, uint32_t c_pad, uint32_t tiles, uint32_t rc,
            uint32_t n_ranges, const int32_t* __restrict__ mode, const uint32_t* __restrict__ cnt,
            const uint32_t* __restrict__ mpad, const uint8_t* __restrict__ tclass,
-           const uint32_t* __restrict__ cperm, const uint16_t* __restrict__ dirs_bf,
+           const uint32_t* __restrict__ cperm, const uint16_t* __restrict__ dirs16,
            uint16_t* __restrict__ bperm, uint4* __restrict__ wlist, int32_t* __restrict__ n_wlist,
            int32_t* __restrict__ dense_active) {
   __shared__ uint32_t s_off, s_w[8], s_nf;
@@ -1087,7 +1157,7 @@ k_mcr_emit(uint32_t U, uint32_t C, uint32_t c_pad, uint32_t tiles, uint32_t rc,
   for (uint32_t e = tid; e < c_pad * (D / 8); e += 256) {
     const uint32_t j = e / (D / 8), q = e % (D / 8);
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (j < C) v = __ldg(reinterpret_cast<const uint4*>(dirs_bf + (size_t(u) * c_pad + cp[j]) * D) + q);
+    if (j < C) v = __ldg(reinterpret_cast<const uint4*>(dirs16 + (size_t(u) * c_pad + cp[j]) * D) + q);
     reinterpret_cast<uint4*>(bperm + (size_t(u) * c_pad + j) * D)[q] = v;
   }
   // F tiles (compacted, in order) for each range, then R tiles for the moved block
@@ -1177,6 +1247,7 @@ k_mcr_merge(const int32_t* __restrict__ mode, uint32_t n, uint32_t tiles, uint32
             const int32_t* __restrict__ prev, int32_t* __restrict__ cur,
             const uint16_t* __restrict__ keys, uint64_t key_stride, const float* __restrict__ dirs,
             const float* __restrict__ knp, const float* __restrict__ eps_u,
+            const float* __restrict__ kerr_u,
             uint4* __restrict__ fix_list, uint32_t* __restrict__ fix_ids,
             uint32_t* __restrict__ fix_n, uint32_t fix_cap) {
   const uint32_t u = blockIdx.y;
@@ -1189,7 +1260,7 @@ k_mcr_merge(const int32_t* __restrict__ mode, uint32_t n, uint32_t tiles, uint32
     const uint32_t a = uint32_t(prev[size_t(u) * label_stride + pos]);
     const float4* sp = summ + (size_t(u) * n + j) * n_slots;
     // err = one score's rigorous bound; band = 2 err (as k_assign_tc's epilogue)
-    const float band = knp[size_t(u) * n + j] * (2.0f * eps_u[u] + (1.0f / 8192.0f)) * 1.01f + 1e-30f;
+    const float band = tc_band(knp[size_t(u) * n + j], eps_u[u], kerr_u[u]);
     const bool F = tclass[size_t(u) * tiles + j / TC_M] != 0;
     const uint32_t nsl = F ? n_ranges : (mpad[u] + rc - 1) / rc;
     const uint32_t* cp = cperm + size_t(u) * c_pad;
@@ -1260,7 +1331,7 @@ bool mcr_enabled() {
 }
 
 int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t n, uint32_t C,
-               uint32_t c_pad, uint32_t n_units, uint32_t c_stride, const uint16_t* dirs_bf,
+               uint32_t c_pad, uint32_t n_units, uint32_t c_stride, const uint16_t* dirs16,
                const float* deps, const float* dirs, const int32_t* prev, int32_t* cur,
                uint32_t label_stride, const int32_t* active, const uint8_t* moved,
                const uint32_t* sorted, void* tc_scratch, size_t tc_bytes) {
@@ -1314,12 +1385,13 @@ int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t
                                            mode, cnt, mpad);
   CKV_LAUNCH_CHECK("k_mcr_plan");
   k_mcr_emit<<<U, 256, 0, st>>>(U, C, c_pad, tiles, rc, n_ranges, mode, cnt, mpad, tclass, cperm,
-                                dirs_bf, bperm, wlist, n_wlist, dense);
+                                dirs16, bperm, wlist, n_wlist, dense);
   CKV_LAUNCH_CHECK("k_mcr_emit");
   k_mcr_copy<<<dim3(8, U), 256, 0, st>>>(mode, prev, cur, n, label_stride);
   CKV_LAUNCH_CHECK("k_mcr_copy");
-  k_mcr_gather<<<dim3((npad + 15) / 16, U), 256, 0, st>>>(mode, keys, key_stride, n, npad, sorted,
-                                                          label_stride, ts.knorm, kperm, knp);
+  k_mcr_gather<<<dim3((npad + 15) / 16, U), 256, 0, st>>>(mode, ts.k16, uint64_t(ts.n_pad) * D, n,
+                                                          npad, sorted, label_stride, ts.knorm,
+                                                          kperm, knp);
   CKV_LAUNCH_CHECK("k_mcr_gather");
   k_eps_max<<<(U + 7) / 8, 256, 0, st>>>(deps, c_pad, U, eps_u);
   CKV_LAUNCH_CHECK("k_eps_max");
@@ -1339,6 +1411,7 @@ int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t
   ta.label_stride = label_stride;
   ta.knorm = knp;
   ta.eps_u = eps_u;
+  ta.kerr_u = ts.kerr;
   ta.labels = cur;  // not written in summary mode
   ta.fix_count = ts.fix_count;
   ta.fix_list = nullptr;
@@ -1353,7 +1426,7 @@ int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t
   CKV_TRY(launch_tc(st, kmap, dmap, ta));
   k_mcr_merge<<<dim3((n + 255) / 256, U), 256, 0, st>>>(
       mode, n, tiles, n_ranges, rc, mpad, tclass, summ, n_ranges, cperm, c_pad, sorted,
-      label_stride, prev, cur, keys, key_stride, dirs, knp, eps_u, fix_list, fix_ids, fix_n,
+      label_stride, prev, cur, keys, key_stride, dirs, knp, eps_u, ts.kerr, fix_list, fix_ids, fix_n,
       uint32_t(fix_cap));
   CKV_LAUNCH_CHECK("k_mcr_merge");
   k_fixup<<<dim3(8 * num_sms(), 1), 256, 0, st>>>(fix_list, fix_ids, fix_n, n_one, tiles, keys,
@@ -1362,7 +1435,7 @@ int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t
   CKV_LAUNCH_CHECK("k_fixup");
   ctx->launches += 3;
   // the DENSE units through the ordinary path
-  CKV_TRY(assign_tc(st, keys, key_stride, n, C, c_pad, U, dirs_bf, deps, dirs, cur, label_stride,
+  CKV_TRY(assign_tc(st, keys, key_stride, n, C, c_pad, U, dirs16, deps, dirs, cur, label_stride,
                     dense, tc_scratch, tc_bytes, &ctx->launches));
   static const bool dbg = getenv("CKV_DEBUG_KMEANS") != nullptr;
   if (dbg) {

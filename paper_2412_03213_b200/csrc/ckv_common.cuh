@@ -6,6 +6,8 @@
 
 #include <string>
 
+#include <cuda_fp16.h>
+
 #include "ckv_cuda.h"
 
 namespace ckvb {
@@ -43,6 +45,20 @@ int cuda_status(cudaError_t e, const char* where);
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float bf16_to_f32(uint16_t b) {
   return __uint_as_float(uint32_t(b) << 16);
+}
+
+// f32 -> the fp16 tensor-core operand (ckv_assign_tc.cu): round to nearest
+// even, saturated to +-65504, results below the normal range (|h| < 2^-14)
+// flushed to signed zero so no subnormal reaches the tensor cores.  Callers
+// measure |x - f16_to_f32(h)| themselves: that is the error the band carries.
+__device__ __forceinline__ uint16_t f32_to_f16_tc(float f) {
+  f = fminf(fmaxf(f, -65504.f), 65504.f);
+  uint16_t b = __half_as_ushort(__float2half_rn(f));
+  if ((b & 0x7c00u) == 0u) b &= 0x8000u;
+  return b;
+}
+__device__ __forceinline__ float f16_to_f32(uint16_t b) {
+  return __half2float(__ushort_as_half(b));
 }
 
 __device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {

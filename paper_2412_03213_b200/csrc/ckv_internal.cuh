@@ -43,11 +43,18 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
 
 // single kernels of the k-means pass, for the sequence-sharded driver
 // (ckv_kmshard.cu); defined in ckv_kmeans.cu / ckv_assign_tc.cu
+// the tensor-core key operands in assign_tc's scratch (assign_tc_keyprep)
+struct TcKeyPrep {
+  float* knorm;    // [unit][n] |k| + |k - h(k)|, rounded up (band scale)
+  uint16_t* k16;   // [unit][n_pad][128] h(k), fp16 bits
+  uint32_t n_pad;
+  uint32_t* kerr;  // [unit] max_k |k - h(k)| as float bits (zero before the scan)
+};
 int launch_scan_keys(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
-                     uint32_t n_units, int32_t* flags, float* knorm);
+                     uint32_t n_units, int32_t* flags, const TcKeyPrep* prep);
 int launch_assign(cudaStream_t st, bool use_tc, const uint16_t* keys, uint64_t key_stride,
                   uint32_t n, uint32_t C, uint32_t c_pad, uint32_t n_units,
-                  const uint16_t* dirs_bf, const float* deps, const float* dirs, int32_t* labels,
+                  const uint16_t* dirs16, const float* deps, const float* dirs, int32_t* labels,
                   uint32_t label_stride, const int32_t* active, void* tc_scratch,
                   size_t tc_bytes, uint64_t* launches);
 int launch_objective(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
@@ -62,12 +69,12 @@ int launch_kmeans_small(cudaStream_t st, const uint16_t* keys, uint64_t key_stri
                         const uint32_t* init_rows, float* cents, uint32_t c_cap,
                         int32_t* labels, uint32_t label_stride, uint32_t* n_clusters,
                         uint32_t* iters, int32_t* status);
-float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n);
+TcKeyPrep assign_tc_keyprep(void* scratch, uint32_t n_units, uint32_t n);
 bool assign_tc_supported(uint32_t n, uint32_t C);
 // moved-cluster reduced assignment (ckv_assign_tc.cu), passes t >= 2
 bool mcr_enabled();
 int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t n, uint32_t C,
-               uint32_t c_pad, uint32_t n_units, uint32_t c_stride, const uint16_t* dirs_bf,
+               uint32_t c_pad, uint32_t n_units, uint32_t c_stride, const uint16_t* dirs16,
                const float* deps, const float* dirs, const int32_t* prev, int32_t* cur,
                uint32_t label_stride, const int32_t* active, const uint8_t* moved,
                const uint32_t* sorted, void* tc_scratch, size_t tc_bytes);

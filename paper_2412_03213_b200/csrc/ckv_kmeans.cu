@@ -31,10 +31,14 @@ namespace ckvb {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
 k_scan_keys(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
-            int32_t* __restrict__ flags, float* __restrict__ knorm) {
-  // one pass over the keys: validation flags (if flags) and the f32 key norms
-  // the tensor-core band scales with (if knorm).  A warp takes 16 rows, a
-  // half-warp one row per step (16 lanes x 16 B), all 8 loads in flight.
+            int32_t* __restrict__ flags, float* __restrict__ knorm, uint16_t* __restrict__ k16,
+            uint32_t n_pad, uint32_t* __restrict__ kerr) {
+  // one pass over the keys: validation flags (if flags) and the tensor-core
+  // key operands (if knorm): the fp16 copy h(k) (k16), the band scale |k| +
+  // |k - h(k)| (knorm) and the unit's max |k - h(k)| (kerr, float bits; zero
+  // for keys inside fp16's normal range, where bf16 -> fp16 is exact).
+  // A warp takes 16 rows, a half-warp one row per step (16 lanes x 16 B),
+  // all 8 loads in flight.
   const uint32_t u = blockIdx.y;
   const int lane = lane_id(), half = lane >> 4, hl = lane & 15;
   const uint32_t r0 = (blockIdx.x * (blockDim.x >> 5) + warp_id()) * 16;
@@ -50,12 +54,15 @@ k_scan_keys(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
                  : make_uint4(0, 0, 0, 0);
   }
   int f = 0;
+  float emax = 0.f;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t w[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
-    float ss = 0.f;
+    float ss = 0.f, es = 0.f;
+    uint32_t hw[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      uint32_t hk = 0u;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint32_t b = h ? (w[k] >> 16) : (w[k] & 0xffffu);
@@ -64,12 +71,30 @@ k_scan_keys(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
         if ((b & 0x7f80u) == 0x7f80u) f |= 1;
         if (b & 0x7fffu) f |= 4;
         if (fabsf(x) >= big) f |= 2;
+        const uint16_t hb = f32_to_f16_tc(x);
+        const float d = x - f16_to_f32(hb);  // exact (both are f32 values)
+        es = fmaf(d, d, es);
+        hk |= uint32_t(hb) << (16 * h);
       }
+      hw[k] = hk;
     }
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    for (int o = 8; o > 0; o >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      es += __shfl_xor_sync(0xffffffffu, es, o);
+    }
     const uint32_t r = r0 + 2 * i + half;
-    if (knorm && hl == 0 && r < n) knorm[size_t(u) * n + r] = sqrtf(ss) * 1.0001f;  // rounding margin
+    if (knorm && r < n) {
+      reinterpret_cast<uint4*>(k16 + (size_t(u) * n_pad + r) * D)[hl] =
+          make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      const float e = es > 0.f ? sqrtf(es) * 1.0001f : 0.f;  // rounding margin
+      if (hl == 0) knorm[size_t(u) * n + r] = (sqrtf(ss) + e) * 1.0001f;
+      emax = fmaxf(emax, e);
+    }
+  }
+  if (knorm) {
+    emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, 16));
+    if (lane == 0 && emax > 0.f) atomicMax(kerr + u, __float_as_uint(emax));
   }
   if (flags) {
     f = __reduce_or_sync(0xffffffffu, f);
@@ -108,10 +133,10 @@ __global__ void k_init_centroids(const uint16_t* __restrict__ keys, uint64_t key
 }
 
 // normalize() (common.hpp:141-147) of every centroid -> f32 dirs (exact),
-// bf16 dirs (tensor-core B operand), f64 norms (for cosine_distance).
+// fp16 dirs (tensor-core B operand), f64 norms (for cosine_distance).
 // One thread per centroid: the norm is a sequential f64 chain by contract.
 __global__ void k_dirs(const float* __restrict__ cents, uint32_t C, uint32_t c_stride,
-                       uint32_t c_pad, float* __restrict__ dirs, uint16_t* __restrict__ dirs_bf,
+                       uint32_t c_pad, float* __restrict__ dirs, uint16_t* __restrict__ dirs16,
                        double* __restrict__ cnorm, float* __restrict__ deps,
                        const int32_t* __restrict__ active) {
   const uint32_t u = blockIdx.y;
@@ -119,7 +144,7 @@ __global__ void k_dirs(const float* __restrict__ cents, uint32_t C, uint32_t c_s
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= c_pad) return;
   float* dr = dirs + (size_t(u) * c_pad + c) * D;
-  uint16_t* db = dirs_bf + (size_t(u) * c_pad + c) * D;
+  uint16_t* db = dirs16 + (size_t(u) * c_pad + c) * D;
   if (c >= C) {  // padding columns of the MMA operand
     for (int j = 0; j < D; ++j) { dr[j] = 0.f; db[j] = 0; }
     deps[size_t(u) * c_pad + c] = 0.f;
@@ -133,9 +158,9 @@ __global__ void k_dirs(const float* __restrict__ cents, uint32_t C, uint32_t c_s
     float x = src[j];
     float y = nrm > 0.0 ? float(double(x) / nrm) : x;
     dr[j] = y;
-    const uint16_t b = f32_to_bf16_rn(y);
+    const uint16_t b = f32_to_f16_tc(y);
     db[j] = b;
-    const double e = double(y) - double(bf16_to_f32(b));
+    const double e = double(y) - double(f16_to_f32(b));
     e2 += e * e;
   }
   deps[size_t(u) * c_pad + c] = float(sqrt(e2)) * 1.0001f;
@@ -185,7 +210,7 @@ __global__ void __launch_bounds__(256)
 k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uint32_t c_stride,
          uint32_t c_pad, uint32_t label_stride, const uint32_t* __restrict__ sizes,
          const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
-         float* __restrict__ cents, float* __restrict__ dirs, uint16_t* __restrict__ dirs_bf,
+         float* __restrict__ cents, float* __restrict__ dirs, uint16_t* __restrict__ dirs16,
          double* __restrict__ cnorm, float* __restrict__ deps, const int32_t* __restrict__ active,
          const uint8_t* __restrict__ dirty) {
   const uint32_t u = blockIdx.y;
@@ -197,7 +222,7 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
   // centroid, direction, norm and band: nothing to do
   if (dirty && (c >= C || !dirty[size_t(u) * c_stride + c])) return;
   float* dr = dirs + (size_t(u) * c_pad + c) * D;
-  uint16_t* db = dirs_bf + (size_t(u) * c_pad + c) * D;
+  uint16_t* db = dirs16 + (size_t(u) * c_pad + c) * D;
   if (c >= C) {
     for (int j = lane; j < D; j += 32) { dr[j] = 0.f; db[j] = 0; }
     if (lane == 0) deps[size_t(u) * c_pad + c] = 0.f;
@@ -374,13 +399,10 @@ __global__ void k_copy_labels(const int32_t* __restrict__ src, int32_t* __restri
 // tensor-core assignment (ckv_assign_tc.cu); returns CKV_EINVAL if the shape
 // is unsupported so the caller falls back to the exact path
 int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
-              uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs_bf,
+              uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs16,
               const float* deps,
               const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
               void* scratch, size_t scratch_bytes, uint64_t* launches);
-size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C);
-float* assign_tc_knorm(void* scratch, uint32_t n_units, uint32_t n);
-bool assign_tc_supported(uint32_t n, uint32_t C);
 
 // ---------------------------------------------------------------------------
 // host driver
@@ -424,7 +446,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   const bool want_obj = (a.flags & CKV_KM_OBJECTIVE) != 0;
 
   // ---- scratch ----------------------------------------------------------
-  DevBuf b_flags, b_lab1, b_sizes, b_starts, b_sorted, b_dirs, b_dirsbf, b_cnorm, b_deps, b_active,
+  DevBuf b_flags, b_lab1, b_sizes, b_starts, b_sorted, b_dirs, b_dirs16, b_cnorm, b_deps, b_active,
       b_changed, b_conv, b_iters, b_empty, b_rep, b_replog, b_obj, b_objlog, b_nact, b_tc, b_dirty;
   const uint32_t LS = a.label_stride, CS = a.c_stride;
   CKV_TRY(dalloc(ctx, 1, b_flags, sizeof(int32_t) * U));
@@ -433,7 +455,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   CKV_TRY(dalloc(ctx, 4, b_starts, sizeof(uint32_t) * size_t(U) * (CS + 1)));
   CKV_TRY(dalloc(ctx, 5, b_sorted, sizeof(uint32_t) * size_t(U) * LS));
   CKV_TRY(dalloc(ctx, 6, b_dirs, sizeof(float) * size_t(U) * c_pad * D));
-  CKV_TRY(dalloc(ctx, 7, b_dirsbf, sizeof(uint16_t) * size_t(U) * c_pad * D));
+  CKV_TRY(dalloc(ctx, 7, b_dirs16, sizeof(uint16_t) * size_t(U) * c_pad * D));
   CKV_TRY(dalloc(ctx, 8, b_cnorm, sizeof(double) * size_t(U) * c_pad));
   CKV_TRY(dalloc(ctx, 9, b_deps, sizeof(float) * size_t(U) * c_pad));
   CKV_TRY(dalloc(ctx, 10, b_active, sizeof(int32_t) * U));
@@ -450,11 +472,15 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
 
   const bool use_tc = !(a.flags & CKV_KM_EXACT_ONLY) && assign_tc_supported(n, C);
   size_t tc_bytes = use_tc ? assign_tc_scratch_bytes(U, n, C) : 0;
-  float* knorm = nullptr;  // key norms for the tensor-core band, filled by k_scan_keys
+  // the tensor-core key operands (fp16 copy, band norms, conversion error),
+  // filled by k_scan_keys
+  TcKeyPrep prep{};
   if (use_tc) {
     CKV_TRY(dalloc(ctx, 20, b_tc, tc_bytes));
-    knorm = assign_tc_knorm(b_tc.p, U, n);
+    prep = assign_tc_keyprep(b_tc.p, U, n);
+    CKV_CUDA_TRY(cudaMemsetAsync(prep.kerr, 0, sizeof(uint32_t) * U, st));
   }
+  float* knorm = prep.knorm;
 
   if (!ctx->h_flags || ctx->h_flags_cap < U + 1) {
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
@@ -467,7 +493,8 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   if (!(a.flags & CKV_KM_NO_VALIDATE)) {
     CKV_CUDA_TRY(cudaMemsetAsync(b_flags.p, 0, sizeof(int32_t) * U, st));
     k_scan_keys<<<dim3((n + 127) / 128, U), 256, 0, st>>>(a.keys, a.key_stride, n,
-                                                          b_flags.as<int32_t>(), knorm);
+                                                          b_flags.as<int32_t>(), knorm, prep.k16,
+                                                          prep.n_pad, prep.kerr);
     CKV_LAUNCH_CHECK("k_scan_keys");
     knorm = nullptr;  // done
     k_validate_rows<<<dim3((n + 255) / 256, U), 256, 0, st>>>(a.keys, a.key_stride, n,
@@ -486,14 +513,14 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   }
   if (knorm) {  // validation skipped: the norms still need their pass
     k_scan_keys<<<dim3((n + 127) / 128, U), 256, 0, st>>>(a.keys, a.key_stride, n, nullptr,
-                                                          knorm);
+                                                          knorm, prep.k16, prep.n_pad, prep.kerr);
     CKV_LAUNCH_CHECK("k_scan_keys");
     ctx->launches++;
   }
 
   int32_t* lab[2] = {a.labels, b_lab1.as<int32_t>()};
   float* dirs = b_dirs.as<float>();
-  uint16_t* dirs_bf = b_dirsbf.as<uint16_t>();
+  uint16_t* dirs16 = b_dirs16.as<uint16_t>();
   double* cnorm = b_cnorm.as<double>();
   float* deps = b_deps.as<float>();
   int32_t* active = b_active.as<int32_t>();
@@ -516,14 +543,14 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   k_init_centroids<<<dim3(C, U), 128, 0, st>>>(a.keys, a.key_stride, a.init_rows, C, CS,
                                                 a.centroids);
   CKV_LAUNCH_CHECK("k_init_centroids");
-  k_dirs<<<dim3((c_pad + 127) / 128, U), 128, 0, st>>>(a.centroids, C, CS, c_pad, dirs, dirs_bf,
+  k_dirs<<<dim3((c_pad + 127) / 128, U), 128, 0, st>>>(a.centroids, C, CS, c_pad, dirs, dirs16,
                                                        cnorm, deps, active);
   CKV_LAUNCH_CHECK("k_dirs");
   ctx->launches += 2;
 
   auto assign = [&](int32_t* out) -> int {
     if (use_tc)
-      return assign_tc(st, a.keys, a.key_stride, n, C, c_pad, U, dirs_bf, deps, dirs, out, LS, active,
+      return assign_tc(st, a.keys, a.key_stride, n, C, c_pad, U, dirs16, deps, dirs, out, LS, active,
                        b_tc.p, tc_bytes, &ctx->launches);
     k_assign_exact<<<dim3((n + 127) / 128, U), 128, 0, st>>>(a.keys, a.key_stride, n, C, c_pad,
                                                             dirs, out, LS, active);
@@ -588,7 +615,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     // update from the previous labels (sizes/starts/sorted hold its sort)
     k_update<<<dim3((c_pad + 7) / 8, U), 256, 0, st>>>(
         a.keys, a.key_stride, C, CS, c_pad, LS, b_sizes.as<uint32_t>(), b_starts.as<uint32_t>(),
-        b_sorted.as<uint32_t>(), a.centroids, dirs, dirs_bf, cnorm, deps, active,
+        b_sorted.as<uint32_t>(), a.centroids, dirs, dirs16, cnorm, deps, active,
         t == 1 ? nullptr : b_dirty.as<uint8_t>());
     CKV_LAUNCH_CHECK("k_update");
     ctx->launches++;
@@ -599,7 +626,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     const bool mcr = use_tc && t >= 2 && mcr_enabled() &&
                      size_t(U) * ((n + 127) / 128 * 128) * D * 2 <= (size_t(8) << 30);
     if (mcr)
-      CKV_TRY(assign_mcr(ctx, a.keys, a.key_stride, n, C, c_pad, U, CS, dirs_bf, deps, dirs,
+      CKV_TRY(assign_mcr(ctx, a.keys, a.key_stride, n, C, c_pad, U, CS, dirs16, deps, dirs,
                          prev, cur, LS, active, b_dirty.as<uint8_t>(), b_sorted.as<uint32_t>(),
                          b_tc.p, tc_bytes));
     else
@@ -674,9 +701,12 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
 namespace ckvb {
 
 int launch_scan_keys(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
-                     uint32_t n_units, int32_t* flags, float* knorm) {
+                     uint32_t n_units, int32_t* flags, const TcKeyPrep* prep) {
   if (n == 0 || n_units == 0) return CKV_OK;
-  k_scan_keys<<<dim3((n + 127) / 128, n_units), 256, 0, st>>>(keys, key_stride, n, flags, knorm);
+  if (prep) CKV_CUDA_TRY(cudaMemsetAsync(prep->kerr, 0, sizeof(uint32_t) * n_units, st));
+  k_scan_keys<<<dim3((n + 127) / 128, n_units), 256, 0, st>>>(
+      keys, key_stride, n, flags, prep ? prep->knorm : nullptr, prep ? prep->k16 : nullptr,
+      prep ? prep->n_pad : 0u, prep ? prep->kerr : nullptr);
   CKV_LAUNCH_CHECK("k_scan_keys");
   if (flags) {
     k_validate_rows<<<dim3((n + 255) / 256, n_units), 256, 0, st>>>(keys, key_stride, n, flags);
@@ -687,12 +717,12 @@ int launch_scan_keys(cudaStream_t st, const uint16_t* keys, uint64_t key_stride,
 
 int launch_assign(cudaStream_t st, bool use_tc, const uint16_t* keys, uint64_t key_stride,
                   uint32_t n, uint32_t C, uint32_t c_pad, uint32_t n_units,
-                  const uint16_t* dirs_bf, const float* deps, const float* dirs, int32_t* labels,
+                  const uint16_t* dirs16, const float* deps, const float* dirs, int32_t* labels,
                   uint32_t label_stride, const int32_t* active, void* tc_scratch,
                   size_t tc_bytes, uint64_t* launches) {
   if (n == 0 || n_units == 0) return CKV_OK;
   if (use_tc)
-    return assign_tc(st, keys, key_stride, n, C, c_pad, n_units, dirs_bf, deps, dirs, labels,
+    return assign_tc(st, keys, key_stride, n, C, c_pad, n_units, dirs16, deps, dirs, labels,
                      label_stride, active, tc_scratch, tc_bytes, launches);
   k_assign_exact<<<dim3((n + 127) / 128, n_units), 128, 0, st>>>(keys, key_stride, n, C, c_pad,
                                                                  dirs, labels, label_stride,

@@ -20,8 +20,8 @@ __device__ __forceinline__ double cosine_distance_dev(const uint16_t* k, const f
 // holding dims 4L..4L+3 of the f64 member sum: centroid = float(sum / count)
 // (clustering.hpp:214-217), then the next pass's AssignScorer direction
 // normalize(centroid) (common.hpp:141-147; sequential f64 norm chain), its
-// bf16 copy (the tensor-core B operand), the f64 norm (cosine_distance) and
-// |dir - bf16(dir)| (the tensor-core error band).
+// fp16 copy h(dir) (the tensor-core B operand), the f64 norm (cosine_distance)
+// and |dir - h(dir)| (the tensor-core error band).
 __device__ __forceinline__ void finish_centroid(double a0, double a1, double a2, double a3,
                                                 double count, float* __restrict__ ct,
                                                 float* __restrict__ dr,
@@ -52,14 +52,16 @@ __device__ __forceinline__ void finish_centroid(double a0, double a1, double a2,
   float d3 = nrm > 0.0 ? float(double(x3) / nrm) : x3;
   reinterpret_cast<float4*>(dr)[lane] = make_float4(d0, d1, d2, d3);
   uint2 pk;
-  pk.x = uint32_t(f32_to_bf16_rn(d0)) | (uint32_t(f32_to_bf16_rn(d1)) << 16);
-  pk.y = uint32_t(f32_to_bf16_rn(d2)) | (uint32_t(f32_to_bf16_rn(d3)) << 16);
+  const uint16_t h0 = f32_to_f16_tc(d0), h1 = f32_to_f16_tc(d1), h2 = f32_to_f16_tc(d2),
+                 h3 = f32_to_f16_tc(d3);
+  pk.x = uint32_t(h0) | (uint32_t(h1) << 16);
+  pk.y = uint32_t(h2) | (uint32_t(h3) << 16);
   reinterpret_cast<uint2*>(db)[lane] = pk;
-  // |dir - bf16(dir)|: the per-centroid error the tensor-core band uses
-  const double e0 = double(d0) - double(__uint_as_float(pk.x << 16));
-  const double e1 = double(d1) - double(__uint_as_float(pk.x & 0xffff0000u));
-  const double e2 = double(d2) - double(__uint_as_float(pk.y << 16));
-  const double e3 = double(d3) - double(__uint_as_float(pk.y & 0xffff0000u));
+  // |dir - h(dir)|: the per-centroid error the tensor-core band uses
+  const double e0 = double(d0) - double(f16_to_f32(h0));
+  const double e1 = double(d1) - double(f16_to_f32(h1));
+  const double e2 = double(d2) - double(f16_to_f32(h2));
+  const double e3 = double(d3) - double(f16_to_f32(h3));
   const double ee = warp_sum(e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
   if (lane == 0) *deps_out = float(sqrt(ee)) * 1.0001f;
 }

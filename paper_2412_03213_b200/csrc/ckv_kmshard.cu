@@ -33,7 +33,7 @@ struct ckv_kmshard {
   uint32_t* lstarts = nullptr;
   uint32_t* lsorted = nullptr;
   float* dirs = nullptr;       // [U][c_pad][128]
-  uint16_t* dirs_bf = nullptr;
+  uint16_t* dirs16 = nullptr;
   double* cnorm = nullptr;     // [U][c_pad]
   float* deps = nullptr;
   int32_t* active = nullptr;   // [U]
@@ -104,7 +104,7 @@ k_shard_sums(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C,
 __global__ void __launch_bounds__(256)
 k_shard_finalize(const double* __restrict__ sums, const int32_t* __restrict__ counts, uint32_t C,
                  uint32_t c_pad, float* __restrict__ cents, float* __restrict__ dirs,
-                 uint16_t* __restrict__ dirs_bf, double* __restrict__ cnorm,
+                 uint16_t* __restrict__ dirs16, double* __restrict__ cnorm,
                  float* __restrict__ deps, const int32_t* __restrict__ active) {
   const uint32_t u = blockIdx.y;
   if (!active[u]) return;
@@ -112,7 +112,7 @@ k_shard_finalize(const double* __restrict__ sums, const int32_t* __restrict__ co
   if (c >= c_pad) return;
   const int lane = lane_id();
   float* dr = dirs + (size_t(u) * c_pad + c) * D;
-  uint16_t* db = dirs_bf + (size_t(u) * c_pad + c) * D;
+  uint16_t* db = dirs16 + (size_t(u) * c_pad + c) * D;
   if (c >= C) {  // padding columns of the MMA operand
     for (int j = lane; j < D; j += 32) { dr[j] = 0.f; db[j] = 0; }
     if (lane == 0) deps[size_t(u) * c_pad + c] = 0.f;
@@ -260,7 +260,7 @@ int ckv_kmshard_create(ckv_ctx* ctx, const ckv_kmshard_desc* d, const uint16_t* 
   A(salloc(s, &s->lstarts, size_t(U) * (C + 1)));
   A(salloc(s, &s->lsorted, size_t(U) * n));
   A(salloc(s, &s->dirs, size_t(U) * s->c_pad * D));
-  A(salloc(s, &s->dirs_bf, size_t(U) * s->c_pad * D));
+  A(salloc(s, &s->dirs16, size_t(U) * s->c_pad * D));
   A(salloc(s, &s->cnorm, size_t(U) * s->c_pad));
   A(salloc(s, &s->deps, size_t(U) * s->c_pad));
   A(salloc(s, &s->active, U));
@@ -280,8 +280,8 @@ int ckv_kmshard_create(ckv_ctx* ctx, const ckv_kmshard_desc* d, const uint16_t* 
   if (rc != CKV_OK) { set_error("kmshard: init copy failed"); ckv_kmshard_destroy(s); return rc; }
   // key norms for the tensor-core band (keys never change)
   if (s->use_tc) {
-    rc = launch_scan_keys(ctx->stream, keys, d->key_stride, n, U, nullptr,
-                          assign_tc_knorm(s->tc, U, n));
+    const TcKeyPrep prep = assign_tc_keyprep(s->tc, U, n);
+    rc = launch_scan_keys(ctx->stream, keys, d->key_stride, n, U, nullptr, &prep);
     if (rc != CKV_OK) { ckv_kmshard_destroy(s); return rc; }
     ctx->launches++;
   }
@@ -322,7 +322,7 @@ int ckv_kmshard_update(ckv_kmshard* s, int from_init) {
   cudaStream_t st = s->ctx->stream;
   const uint32_t U = s->d.n_units, C = s->d.C;
   k_shard_finalize<<<dim3((s->c_pad + 7) / 8, U), 256, 0, st>>>(
-      s->b.sums, from_init ? nullptr : s->b.counts, C, s->c_pad, s->cents, s->dirs, s->dirs_bf,
+      s->b.sums, from_init ? nullptr : s->b.counts, C, s->c_pad, s->cents, s->dirs, s->dirs16,
       s->cnorm, s->deps, s->active);
   CKV_LAUNCH_CHECK("k_shard_finalize");
   s->ctx->launches++;
@@ -333,7 +333,7 @@ int ckv_kmshard_assign(ckv_kmshard* s, uint32_t pass) {
   cudaStream_t st = s->ctx->stream;
   const uint32_t U = s->d.n_units, C = s->d.C, n = s->d.n_local;
   s->cur = pass & 1;
-  CKV_TRY(launch_assign(st, s->use_tc, s->keys, s->d.key_stride, n, C, s->c_pad, U, s->dirs_bf,
+  CKV_TRY(launch_assign(st, s->use_tc, s->keys, s->d.key_stride, n, C, s->c_pad, U, s->dirs16,
                         s->deps, s->dirs, s->lab[s->cur], n, s->active, s->tc, s->tc_bytes,
                         &s->ctx->launches));
   CKV_TRY(launch_index(st, U, s->lab[s->cur], n, n, C, nullptr, C, s->lsizes, s->lstarts,
