@@ -51,14 +51,26 @@ k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint
   int my_changed = 0;
   const int32_t* prev = prev_labels ? prev_labels + size_t(u) * p_cap : nullptr;
   if (dty) __syncthreads();  // zeroed before any mark
-  for (uint32_t p = p0 + lane; p < p1; p += 32) {
-    int32_t l = lab[p];
-    if (l >= 0) atomicAdd(&hist[w * C + l], 1u);
-    if (prev && prev[p] != l) {
-      my_changed = 1;
-      if (dty) {
-        if (l >= 0) dty[l] = 1;
-        if (prev[p] >= 0) dty[prev[p]] = 1;
+  // IX_BATCH rounds of 32 labels (and previous labels) are loaded before
+  // any is used, so a warp keeps that many loads in flight
+  constexpr int IX_BATCH = 8;
+  for (uint32_t p = p0 + lane; p < p1; p += 32 * IX_BATCH) {
+    int32_t l[IX_BATCH], pv[IX_BATCH];
+#pragma unroll
+    for (int k = 0; k < IX_BATCH; ++k) {
+      const uint32_t q = p + 32 * k;
+      l[k] = q < p1 ? __ldg(lab + q) : -1;
+      pv[k] = prev && q < p1 ? __ldg(prev + q) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < IX_BATCH; ++k) {
+      if (l[k] >= 0) atomicAdd(&hist[w * C + l[k]], 1u);
+      if (prev && pv[k] != l[k]) {
+        my_changed = 1;
+        if (dty) {
+          if (l[k] >= 0) dty[l[k]] = 1;
+          if (pv[k] >= 0) dty[pv[k]] = 1;
+        }
       }
     }
   }
@@ -105,18 +117,27 @@ k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint
   // stable scatter: warp w walks its segment in order
   uint32_t* out = sorted_ids + size_t(u) * p_cap;
   uint32_t* cur = hist + w * C;
-  for (uint32_t b = p0; b < p1; b += 32) {
-    uint32_t p = b + lane;
-    int32_t l = p < p1 ? lab[p] : -1;
-    unsigned valid = __ballot_sync(0xffffffffu, l >= 0);
-    if (l >= 0) {
-      unsigned peers = __match_any_sync(valid, l);
-      unsigned rank = __popc(peers & ((1u << lane) - 1u));
-      out[cur[l] + rank] = p;
-      __syncwarp(valid);
-      if (rank == 0) cur[l] += __popc(peers);
+  for (uint32_t b0 = p0; b0 < p1; b0 += 32 * IX_BATCH) {
+    int32_t lb[IX_BATCH];
+#pragma unroll
+    for (int k = 0; k < IX_BATCH; ++k) {
+      const uint32_t q = b0 + 32 * k + lane;
+      lb[k] = q < p1 ? __ldg(lab + q) : -1;
     }
-    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < IX_BATCH; ++k) {
+      const uint32_t p = b0 + 32 * k + lane;
+      const int32_t l = lb[k];
+      unsigned valid = __ballot_sync(0xffffffffu, l >= 0);
+      if (l >= 0) {
+        unsigned peers = __match_any_sync(valid, l);
+        unsigned rank = __popc(peers & ((1u << lane) - 1u));
+        out[cur[l] + rank] = p;
+        __syncwarp(valid);
+        if (rank == 0) cur[l] += __popc(peers);
+      }
+      __syncwarp();
+    }
   }
   if (threadIdx.x == 0) {
     if (changed && prev) changed[u] = s_changed;

@@ -32,18 +32,22 @@ __device__ __forceinline__ void finish_centroid(double a0, double a1, double a2,
   float x0 = float(a0 / count), x1 = float(a1 / count), x2 = float(a2 / count),
         x3 = float(a3 / count);
   reinterpret_cast<float4*>(ct)[lane] = make_float4(x0, x1, x2, x3);
-  // sequential norm chain over j = 0..127: lane L holds j = 4L..4L+3
+  // sequential norm chain over j = 0..127 (lane L holds j = 4L..4L+3): the
+  // values are staged once in shared memory as f64 and every lane walks them
+  // with broadcast 16-B loads (64 LDS per warp instead of 256 shuffles)
+  __shared__ __align__(16) double fc_stage[8][D];  // callers run <= 8 warps per block
+  double* stg = fc_stage[warp_id()];
+  reinterpret_cast<double2*>(stg)[2 * lane] = make_double2(double(x0), double(x1));
+  reinterpret_cast<double2*>(stg)[2 * lane + 1] = make_double2(double(x2), double(x3));
+  __syncwarp();
   double s = 0.0;
-  for (int L = 0; L < 32; ++L) {
-    double y0 = __shfl_sync(0xffffffffu, double(x0), L);
-    double y1 = __shfl_sync(0xffffffffu, double(x1), L);
-    double y2 = __shfl_sync(0xffffffffu, double(x2), L);
-    double y3 = __shfl_sync(0xffffffffu, double(x3), L);
-    s = __fma_rn(y0, y0, s);
-    s = __fma_rn(y1, y1, s);
-    s = __fma_rn(y2, y2, s);
-    s = __fma_rn(y3, y3, s);
+#pragma unroll 16
+  for (int j = 0; j < D / 2; ++j) {
+    const double2 y = reinterpret_cast<const double2*>(stg)[j];
+    s = __fma_rn(y.x, y.x, s);
+    s = __fma_rn(y.y, y.y, s);
   }
+  __syncwarp();  // the stage is free for the warp's next call
   const double nrm = sqrt(s);
   if (lane == 0) *cnorm_out = nrm;
   float d0 = nrm > 0.0 ? float(double(x0) / nrm) : x0;
