@@ -13,6 +13,7 @@
 //   control  : convergence / max_iters bookkeeping, one 4-byte read-back
 // Every integer result (labels, iterations, converged, repair iterations)
 // and every centroid bit equals the reference for identical inputs.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -435,8 +436,39 @@ int dalloc(ckv_ctx* ctx, int slot, DevBuf& b, size_t bytes) {
 }
 }  // namespace
 
+static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
+                            double* objective_host, uint32_t* repair_host);
+
+// Units are independent, so a call whose scratch (dominated by the fp16 key
+// copy of the tensor-core path, ~n * 256 B per unit) would not fit next to
+// the caller's data runs its units in batches, each a complete k-means run.
 int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
                double* objective_host, uint32_t* repair_host) {
+  const uint32_t U = a.n_units;
+  const size_t per_unit = assign_tc_scratch_bytes(1, a.n, a.C) + size_t(a.label_stride) * 16 +
+                          size_t(a.c_stride) * D * 24;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+  const size_t budget = std::max<size_t>(size_t(16) << 30, free_b / 10 * 6);
+  const uint32_t ub = uint32_t(std::max<size_t>(1, std::min<size_t>(U, budget / per_unit)));
+  if (ub >= U) return kmeans_run_units(ctx, a, info_host, objective_host, repair_host);
+  const size_t MI1 = size_t(a.max_iters) + 1;
+  for (uint32_t u0 = 0; u0 < U; u0 += ub) {
+    KMeansArgs b = a;
+    b.n_units = std::min(ub, U - u0);
+    b.keys = a.keys + size_t(u0) * a.key_stride;
+    b.init_rows = a.init_rows + size_t(u0) * a.C;
+    b.centroids = a.centroids + size_t(u0) * a.c_stride * D;
+    b.labels = a.labels + size_t(u0) * a.label_stride;
+    CKV_TRY(kmeans_run_units(ctx, b, info_host ? info_host + u0 : nullptr,
+                             objective_host ? objective_host + u0 * MI1 : nullptr,
+                             repair_host ? repair_host + u0 * MI1 : nullptr));
+  }
+  return CKV_OK;
+}
+
+static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
+                            double* objective_host, uint32_t* repair_host) {
   cudaStream_t st = ctx->stream;
   const uint32_t U = a.n_units, n = a.n, C = a.C, MI = a.max_iters;
   if (U == 0) return CKV_OK;

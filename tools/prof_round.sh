@@ -17,6 +17,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none \
 ncu --set full --import-source on --clock-control none -k regex:"k_assign_tc" --launch-skip 20 -c 1 \
     -o $O/prof_assign -f $B > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none \
-    -k regex:"k_score_range|k_select_scored|k_attend|k_lse_merge|k_fill" \
+    -k regex:"k_score_range|k_select_scored|k_select_approx|k_attend|k_lse_merge|k_fill" \
     --csv --log-file $O/launch_cfgE.csv python bench.py --config E --steps 3 --warmup 2 > /dev/null 2>&1
 ls -la $O

@@ -9,6 +9,7 @@ python bench.py --impl reference --steps 3 --warmup 3 > $O/eval_bench_ref.json 2
 python bench.py --config C --steps 10 --warmup 3 > $O/eval_cfgC.json 2> $O/eval_cfgC.err
 python bench.py --config D > $O/eval_cfgD.json 2> $O/eval_cfgD.err
 python bench.py --config E --steps 10 --warmup 3 > $O/eval_cfgE.json 2> $O/eval_cfgE.err
+python bench.py --config A > $O/eval_cfgA.json 2> $O/eval_cfgA.err
 B="python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu --no-extra"
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_select|k_score|k_attend|k_append" \
     --csv --log-file $O/launch_decode.csv $B > /dev/null 2>&1
