@@ -207,7 +207,10 @@ k_assign_exact(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
 // f64 sums over the members in sorted (= position) order, then
 // float(sum / count), then the next pass's dirs (normalize, fused).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
+#ifndef CKV_UPD_MINB
+#define CKV_UPD_MINB 4  // 64 registers: 2x the resident warps of the latency-bound tail (measured 634 vs 872 us per all-dirty pass)
+#endif
+__global__ void __launch_bounds__(256, CKV_UPD_MINB)
 k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uint32_t c_stride,
          uint32_t c_pad, uint32_t label_stride, const uint32_t* __restrict__ sizes,
          const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
