@@ -4,7 +4,8 @@
 // One CTA per unit.  W warps each own a contiguous segment of positions:
 //   1. per-warp histograms hist[w][c] (smem atomics);
 //   2. column scan: starts[c] = sum_{c'<c} size[c'], and per-warp write
-//      cursors off[w][c] = starts[c] + sum_{w'<w} hist[w'][c];
+//      cursors off[w][c] = starts[c] + sum_{w'<w} hist[w'][c] (columns in
+//      parallel, the scan over clusters by one warp);
 //   3. each warp walks its segment in order, 32 positions at a time, ranks
 //      equal labels with __match_any_sync and scatters position ids.
 // Warp w's ids precede warp w+1's for every cluster and each warp scatters
@@ -18,7 +19,7 @@
 
 namespace ckvb {
 
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint32_t c_cap,
         const uint32_t* __restrict__ n_clusters, uint32_t c_uniform,
         uint32_t* __restrict__ sizes, uint32_t* __restrict__ starts,
@@ -77,40 +78,45 @@ k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint
   if (prev && __any_sync(0xffffffffu, my_changed) && lane == 0) s_changed = 1;
   __syncthreads();
 
-  // column totals -> exclusive scan over clusters (chunked, one warp per
-  // 32 clusters at a time, serial carry through the block)
+  // column totals and intra-column offsets (every thread, one column at a
+  // time), then the exclusive scan of the totals over clusters (warp 0,
+  // 32 clusters per step), then the starts added back into the offsets
   uint32_t* sz = sizes + size_t(u) * c_cap;
   uint32_t* st = starts + size_t(u) * (c_cap + 1);
+  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+    uint32_t run = 0;
+    for (int ww = 0; ww < W; ++ww) {
+      const uint32_t h = hist[ww * C + c];
+      hist[ww * C + c] = run;  // becomes the intra-column offset
+      run += h;
+    }
+    sz[c] = run;  // the column total (this block reads it back below)
+  }
+  __syncthreads();
   if (w == 0) {
     uint32_t carry = 0;
     for (uint32_t c0 = 0; c0 < C; c0 += 32) {
-      uint32_t c = c0 + lane;
-      uint32_t tot = 0;
-      if (c < C) {
-        uint32_t run = 0;
-        for (int ww = 0; ww < W; ++ww) {
-          uint32_t h = hist[ww * C + c];
-          hist[ww * C + c] = run;  // becomes the intra-column offset
-          run += h;
-        }
-        tot = run;
-      }
+      const uint32_t c = c0 + lane;
+      const uint32_t tot = c < C ? sz[c] : 0u;
       uint32_t incl = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
       }
-      uint32_t excl = carry + incl - tot;
+      const uint32_t excl = carry + incl - tot;
       if (c < C) {
-        sz[c] = tot;
         st[c] = excl;
         if (tot == 0) s_empty = 1;
-        for (int ww = 0; ww < W; ++ww) hist[ww * C + c] += excl;
       }
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) { st[C] = carry; s_total = carry; }
+  }
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+    const uint32_t e = st[c];
+    for (int ww = 0; ww < W; ++ww) hist[ww * C + c] += e;
   }
   __syncthreads();
 
@@ -153,7 +159,7 @@ int launch_index(cudaStream_t st, uint32_t n_units, const int32_t* labels, uint3
   if (n_units == 0) return CKV_OK;
   // warps per CTA limited by the smem histogram [W][c_cap]
   const size_t budget = 200 * 1024;
-  int W = 16;
+  int W = 32;
   while (W > 1 && size_t(W) * c_cap * 4 > budget) W >>= 1;
   if (size_t(W) * c_cap * 4 > budget) {
     set_error("build_index: cluster capacity exceeds the 51200-cluster smem limit");
