@@ -838,7 +838,10 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
   return ckv_ctx_sync(s->ctx);
 }
 
-static int session_select_attend(ckv_session* s, const float* q_dev, float* out_dev) {
+// q_copy: when q is mapped host memory, the selection leaves a device copy
+// of it there and the attention reads that (its bulk copies stay on HBM)
+static int session_select_attend(ckv_session* s, const float* q_dev, float* out_dev,
+                                 float* q_copy = nullptr) {
   ckv_select_desc sd{};
   sd.n_q = s->n_q;
   sd.group = s->d.group;
@@ -855,15 +858,15 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
   CKV_TRY(launch_select(s->ctx->stream, sd, q_dev, s->cents, s->n_clusters, s->sizes, s->starts,
                         s->sorted, want_ids ? s->token_ids : nullptr, nullptr, s->runs,
                         sd.row_base, s->n_tokens, s->n_taken, s->trimmed, s->ranked, nullptr,
-                        s->cache ? s->cache->dev : null_cache(), s->sel_scratch));
+                        s->cache ? s->cache->dev : null_cache(), s->sel_scratch, q_copy));
   ckv_attend_desc ad{};
   ad.n_q = s->n_q;
   ad.group = s->d.group;
   ad.p_cap = s->p_cap;
   ad.sel_cap = s->sel_cap;
   ad.max_tokens = std::min(s->d.budget, s->labeled_end) + sd.sink_count + (s->n_ctx - s->labeled_end);
-  CKV_TRY(launch_attend(s->ctx->stream, ad, q_dev, s->K, s->V, nullptr, s->runs, s->n_tokens,
-                        out_dev, nullptr, nullptr, s->part, s->tickets));
+  CKV_TRY(launch_attend(s->ctx->stream, ad, q_copy ? q_copy : q_dev, s->K, s->V, nullptr,
+                        s->runs, s->n_tokens, out_dev, nullptr, nullptr, s->part, s->tickets));
   s->ctx->launches += 3;
   return CKV_OK;
 }
@@ -881,16 +884,34 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
   const float* qd = q;
   const uint16_t *kd = kn, *vd = vn;
   float* od = out;
+  float* q_copy = nullptr;
+  bool zero_copy = false;
   if (!on_device) {
-    CKV_CUDA_TRY(cudaMemcpyAsync(s->q_dev, q, size_t(s->n_q) * D * 4, cudaMemcpyHostToDevice, st));
-    CKV_CUDA_TRY(cudaMemcpyAsync(s->kn_dev, kn, size_t(s->U) * D * 2, cudaMemcpyHostToDevice, st));
-    CKV_CUDA_TRY(cudaMemcpyAsync(s->vn_dev, vn, size_t(s->U) * D * 2, cudaMemcpyHostToDevice, st));
-    qd = s->q_dev;
-    kd = s->kn_dev;
-    vd = s->vn_dev;
-    od = s->out_dev;
+    // pinned (page-locked, device-mapped) host buffers are read and written
+    // by the kernels in place over PCIe: the selection reads q and leaves a
+    // device copy, the attention writes out, the append reads the new k/v;
+    // no copy-engine transfers or their latencies on the step's path.
+    // Pageable buffers take the staged copies.
+    auto mapped = [](const void* p) -> const void* {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+      return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+    };
+    const void *mq = mapped(q), *mk = mapped(kn), *mv = mapped(vn), *mo = mapped(out);
+    zero_copy = mq && mk && mv && mo && mq == q && mk == kn && mv == vn && mo == out;
+    if (zero_copy) {
+      q_copy = s->q_dev;
+    } else {
+      CKV_CUDA_TRY(cudaMemcpyAsync(s->q_dev, q, size_t(s->n_q) * D * 4, cudaMemcpyHostToDevice, st));
+      CKV_CUDA_TRY(cudaMemcpyAsync(s->kn_dev, kn, size_t(s->U) * D * 2, cudaMemcpyHostToDevice, st));
+      CKV_CUDA_TRY(cudaMemcpyAsync(s->vn_dev, vn, size_t(s->U) * D * 2, cudaMemcpyHostToDevice, st));
+      qd = s->q_dev;
+      kd = s->kn_dev;
+      vd = s->vn_dev;
+      od = s->out_dev;
+    }
   }
-  CKV_TRY(session_select_attend(s, qd, od));
+  CKV_TRY(session_select_attend(s, qd, od, q_copy));
   // append this step's token (harness.hpp:318-320)
   k_append_kv<<<s->U, 16, 0, st>>>(kd, vd, s->K, s->V, s->n_ctx, s->p_cap);
   CKV_LAUNCH_CHECK("k_append_kv");
@@ -923,8 +944,9 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
     s->ctx->launches++;
   }
   if (!on_device) {
-    CKV_CUDA_TRY(cudaMemcpyAsync(out, s->out_dev, size_t(s->n_q) * D * 4, cudaMemcpyDeviceToHost,
-                                 st));
+    if (!zero_copy)
+      CKV_CUDA_TRY(cudaMemcpyAsync(out, s->out_dev, size_t(s->n_q) * D * 4,
+                                   cudaMemcpyDeviceToHost, st));
     CKV_CUDA_TRY(cudaStreamSynchronize(st));
   }
   return CKV_OK;

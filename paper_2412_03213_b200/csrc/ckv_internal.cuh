@@ -93,7 +93,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
                   uint32_t* rows, const ckv_runs& runs, uint32_t row_base, uint32_t* n_tokens,
                   uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
-                  const CacheDev& cache, void* scratch);
+                  const CacheDev& cache, void* scratch, float* q_copy = nullptr);
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap);
 int launch_score_approx(cudaStream_t st, uint32_t G, uint32_t n_units, const float* q,
                         const float* cents, const uint32_t* counts, uint32_t c_cap,

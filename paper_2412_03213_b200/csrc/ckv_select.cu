@@ -537,7 +537,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
                uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
                uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
                uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
-               CacheDev cache, uint32_t warp_bytes, uint32_t mode) {
+               CacheDev cache, uint32_t warp_bytes, uint32_t mode, float* __restrict__ q_copy) {
   static_assert(G <= SF_WARPS, "one select warp per head");
   const uint32_t unit = blockIdx.x;
   const int lane = lane_id(), wid = warp_id();
@@ -565,6 +565,9 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     const float4 qw = __ldg(reinterpret_cast<const float4*>(qu + size_t(wid) * D) + lane);
     const float s2 = warp_sum(qw.x * qw.x + qw.y * qw.y + qw.z * qw.z + qw.w * qw.w);
     if (lane == 0) qn2[wid] = s2;
+    // q read from mapped host memory (the session's zero-copy step): leave a
+    // device copy for the attention kernel
+    if (q_copy) reinterpret_cast<float4*>(q_copy + (size_t(unit) * G + wid) * D)[lane] = qw;
   }
   __syncthreads();
   float qnrm[G];
@@ -668,7 +671,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
                   uint32_t* rows, const ckv_runs& runs, uint32_t row_base, uint32_t* n_tokens,
                   uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
-                  const CacheDev& cache, void* scratch) {
+                  const CacheDev& cache, void* scratch, float* q_copy) {
   const uint32_t G = desc.group;
   if (G < 1 || desc.n_q % G || !(G == 1 || G == 2 || G == 4 || G == 8)) {
     set_error("select: group must be 1, 2, 4 or 8 and divide n_q");
@@ -703,7 +706,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         attr_f = dev_f;
       }
 #define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
-    token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode
+    token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode, q_copy
       static const uint32_t sel_mode = getenv("CKV_SEL_MODE") ? uint32_t(atoi(getenv("CKV_SEL_MODE"))) : 0u;
       // CKV_SEL_L2_PERSIST: the centroids (read by every step, ~60 MB at
       // config B) are accessed through a persisting L2 window, so the KV
@@ -750,6 +753,10 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       CKV_LAUNCH_CHECK("k_select_fused");
       return CKV_OK;
     }
+  }
+  if (q_copy) {  // the unfused kernels read q from the device copy
+    CKV_CUDA_TRY(cudaMemcpyAsync(q_copy, q, size_t(desc.n_q) * D * 4, cudaMemcpyDefault, st));
+    q = q_copy;
   }
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES))) {
     const dim3 g1(units, (c_pad + SC_WARPS * SC_ROWS - 1) / (SC_WARPS * SC_ROWS));

@@ -86,3 +86,46 @@ def test_session_vs_oracle_decode_loop(gpu_ctx):
     ctr = s.cache_counters()
     for hq in range(U * G):
         assert [int(x) for x in ctr[hq]] == [int(x) for x in caches[hq].counters()]
+
+
+def test_session_host_buffer_paths_match_device(gpu_ctx):
+    """The host-buffer step (pinned: zero-copy kernels reading q / k / v and
+    writing out over PCIe; pageable: staged copies) gives exactly the
+    device-buffer step's outputs, step after step (decode batches included)."""
+    import torch
+    from paper_2412_03213_b200 import api
+    from paper_2412_03213_b200 import _native as N
+    from paper_2412_03213_b200.session import Session
+
+    U, G, L, T, B = 4, 2, 600, 30, 64
+    heads = [head(9, u, 0, L, T) for u in range(U)]
+    cfg = api.ClusterConfig(decode_batch=12, c0_divisor=40)
+    Kb = np.stack([bf16_bits(h["K"]) for h in heads])
+    Vb = np.stack([bf16_bits(h["V"]) for h in heads])
+    ss = []
+    for _ in range(3):
+        s = Session(U, G, L, T, B, retention=2, cfg=cfg, kv_heads=U)
+        s.load_prompt_host(Kb, Vb)
+        s.prefill()
+        ss.append(s)
+    dev = gpu_ctx.device
+    qp = torch.empty((U * G, 128), dtype=torch.float32).pin_memory()
+    kp = torch.empty((U, 128), dtype=torch.int16).pin_memory()
+    vp = torch.empty((U, 128), dtype=torch.int16).pin_memory()
+    op = torch.empty((U * G, 128), dtype=torch.float32).pin_memory()
+    for t in range(T):
+        q = np.stack([heads[u]["Q"][(t + r) % T] for u in range(U) for r in range(G)])
+        kn = np.stack([bf16_bits(heads[u]["dK"][t]) for u in range(U)]).view(np.int16)
+        vn = np.stack([bf16_bits(heads[u]["dV"][t]) for u in range(U)]).view(np.int16)
+        o_dev = ss[0].step(torch.from_numpy(q).to(dev), torch.from_numpy(kn).to(dev),
+                           torch.from_numpy(vn).to(dev)).cpu().numpy()
+        qp.copy_(torch.from_numpy(q)); kp.copy_(torch.from_numpy(kn)); vp.copy_(torch.from_numpy(vn))
+        N.check(N.lib().ckv_session_step(ss[1].h, qp.data_ptr(), kp.data_ptr(), vp.data_ptr(),
+                                         op.data_ptr(), 0))
+        o_pin = op.numpy().copy()
+        o_page = np.zeros_like(o_pin)
+        qq, kk, vv = q.copy(), kn.copy(), vn.copy()
+        N.check(N.lib().ckv_session_step(ss[2].h, qq.ctypes.data, kk.ctypes.data, vv.ctypes.data,
+                                         o_page.ctypes.data, 0))
+        assert np.array_equal(o_pin, o_dev), t
+        assert np.array_equal(o_page, o_dev), t
