@@ -1,6 +1,8 @@
 // ckv_capi.cu — the extern "C" boundary (include/ckv_cuda.h) and the
 // device-resident decode session.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <random>
@@ -616,13 +618,17 @@ int ckv_relayout_kv(ckv_ctx* ctx, uint32_t n_units, uint32_t p_cap, const uint16
     return CKV_OK;
   }
   // in place: chunks of units through a bounded staging buffer, so a store
-  // that fills most of HBM (config C: 128 GiB of KV) never needs a second copy
+  // that fills most of HBM (config C: 128 GiB of KV) never needs a second
+  // copy.  The staging is the context's grow-only slot 22 (a stream-ordered
+  // allocation per call re-commits its pages every prefill: ~170 ms at
+  // config B for 2 GiB).
   const size_t unit_bytes = size_t(p_cap) * D * 2;
   const uint32_t chunk = uint32_t(std::max<size_t>(1, std::min<size_t>(
-      n_units, (size_t(1) << 30) / unit_bytes)));
-  uint16_t *tK = nullptr, *tV = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&tK, chunk * unit_bytes, st));
-  CKV_CUDA_TRY(cudaMallocAsync(&tV, chunk * unit_bytes, st));
+      n_units, (size_t(256) << 20) / unit_bytes)));
+  void* stage = nullptr;
+  CKV_TRY(ctx_scratch(ctx, 22, 2 * size_t(chunk) * unit_bytes, false, &stage));
+  uint16_t* tK = static_cast<uint16_t*>(stage);
+  uint16_t* tV = tK + size_t(chunk) * p_cap * D;
   int rc = CKV_OK;
   for (uint32_t u0 = 0; u0 < n_units && rc == CKV_OK; u0 += chunk) {
     const uint32_t nu = std::min(chunk, n_units - u0);
@@ -639,8 +645,6 @@ int ckv_relayout_kv(ckv_ctx* ctx, uint32_t n_units, uint32_t p_cap, const uint16
       if (e != cudaSuccess) rc = cuda_status(e, "ckv_relayout_kv copy-back");
     }
   }
-  cudaFreeAsync(tK, st);
-  cudaFreeAsync(tV, st);
   return rc;
 }
 
@@ -823,11 +827,20 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
   pd.max_iters = s->d.max_iters;
   pd.c0_override = 0;
   pd.flags = s->d.flags;
+  // CKV_DEBUG_TIMING=1: host wall time of the three phases on stderr
+  static const bool dbg = getenv("CKV_DEBUG_TIMING") != nullptr;
+  auto now = [&]() {
+    if (dbg) cudaStreamSynchronize(s->ctx->stream);
+    return std::chrono::steady_clock::now();
+  };
+  const auto t0 = now();
   CKV_TRY(ckv_cluster_prefill(s->ctx, &pd, s->K, s->seeds.data(), s->cents, s->labels,
                               s->n_clusters, info, nullptr, nullptr));
+  const auto t1 = now();
   s->C_cur = ckv_prefill_cluster_count(pd.L, pd.c0_divisor, pd.sink_tokens, 0);
   CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
                           s->n_clusters, s->sizes, s->starts, s->sorted));
+  const auto t2 = now();
   // relay the KV store cluster-major: row sink + j <- position sorted[j]
   const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
   const uint32_t N = s->labeled_end - sink;
@@ -835,7 +848,14 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
     CKV_TRY(ckv_relayout_kv(s->ctx, s->U, s->p_cap, s->K, s->V, s->K, s->V, s->sorted, sink,
                             s->labeled_end, s->n_ctx));
   s->prefilled = true;
-  return ckv_ctx_sync(s->ctx);
+  const int rc = ckv_ctx_sync(s->ctx);
+  if (dbg) {
+    const auto t3 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "[session prefill] kmeans %.2f ms, index %.2f ms, relayout %.2f ms\n",
+            ms(t0, t1), ms(t1, t2), ms(t2, t3));
+  }
+  return rc;
 }
 
 // q_copy: when q is mapped host memory, the selection leaves a device copy
