@@ -503,8 +503,13 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info_host);
  *   select (budget, sinks, recency window [labeled_end, n_ctx)) + cache,
  *   approx attention, append (k_t, v_t), decode-batch clustering every m.
  * q: f32 [n_q][128]; k_new, v_new: bf16 [n_units][128]; out: f32 [n_q][128].
- * on_device != 0: all four are device pointers; otherwise host pointers
- * (copied in/out on the session stream inside the call). */
+ * on_device != 0: all four are device pointers; otherwise host pointers:
+ * page-locked (cudaHostAlloc / pinned) buffers are read and written by the
+ * kernels in place over PCIe (zero-copy: the selection reads q and leaves a
+ * device copy for the attention, the attention writes out, the append reads
+ * k/v); pageable buffers are staged by copies on the session stream.  Both
+ * give the device path's results bit for bit; the call returns after out is
+ * complete. */
 int ckv_session_step(ckv_session* s, const float* q, const uint16_t* k_new,
                      const uint16_t* v_new, float* out, int on_device);
 /* Select + attend only (no append/cluster), device pointers, for timing
