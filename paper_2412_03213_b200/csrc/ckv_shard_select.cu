@@ -157,10 +157,14 @@ k_score_range_f32(const float* __restrict__ q, const float* __restrict__ cents, 
   for (uint32_t e = threadIdx.x; e < G * D / 4; e += SR_ROWS)
     reinterpret_cast<float4*>(qs)[e] = __ldg(qu + e);
   __syncthreads();
-  if (threadIdx.x < G) {
-    float n2 = 0.f;
-    for (int j = 0; j < D; ++j) n2 = fmaf(qs[threadIdx.x * D + j], qs[threadIdx.x * D + j], n2);
-    qn[threadIdx.x] = SA_ERR * sqrtf(n2);
+  // |q| of each head by a warp (a lane per 4 dims + shuffles), not one
+  // thread's 128-long dependent chain that the whole block would wait for
+  for (int g = threadIdx.x >> 5; g < G; g += SR_ROWS / 32) {
+    const float4 x = reinterpret_cast<const float4*>(qs + g * D)[threadIdx.x & 31];
+    float n2 = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, x.w * x.w)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    if ((threadIdx.x & 31) == 0) qn[g] = SA_ERR * sqrtf(n2);
   }
   __syncthreads();
   const uint32_t r = threadIdx.x;
