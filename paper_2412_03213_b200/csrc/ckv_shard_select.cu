@@ -47,6 +47,13 @@ __device__ __forceinline__ bool before(unsigned long long ka, uint32_t ia, unsig
 // the row feeds 4G FMAs, the query quads are broadcasts).
 constexpr int SR_ROWS = 128;
 constexpr int SR_LD = D + 4;  // row stride in floats: 16-B aligned rows
+__device__ __forceinline__ void sr_cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+
 template <int G>
 __global__ void __launch_bounds__(SR_ROWS)
 k_score_range(const float* __restrict__ q, const float* __restrict__ cents, uint32_t c_cap,
@@ -61,11 +68,13 @@ k_score_range(const float* __restrict__ q, const float* __restrict__ cents, uint
   if (t0 >= hi) return;
   const uint32_t nrow = min(uint32_t(SR_ROWS), hi - t0);
   const float4* cu = reinterpret_cast<const float4*>(cents + (size_t(u) * c_cap + t0) * D);
+  // tile and q to shared memory by cp.async, all pieces in flight at once
   for (uint32_t e = threadIdx.x; e < nrow * (D / 4); e += SR_ROWS)
-    *reinterpret_cast<float4*>(crow + (e / (D / 4)) * SR_LD + 4 * (e % (D / 4))) = __ldg(cu + e);
+    sr_cp_async16(crow + (e / (D / 4)) * SR_LD + 4 * (e % (D / 4)), cu + e);
   const float4* qu = reinterpret_cast<const float4*>(q + size_t(u) * G * D);
   for (uint32_t e = threadIdx.x; e < G * D / 4; e += SR_ROWS)
-    reinterpret_cast<float4*>(qs)[e] = __ldg(qu + e);
+    sr_cp_async16(qs + 4 * e, qu + e);
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   const uint32_t r = threadIdx.x;
   if (r >= nrow) return;
@@ -151,11 +160,14 @@ k_score_range_f32(const float* __restrict__ q, const float* __restrict__ cents, 
   if (t0 >= hi) return;
   const uint32_t nrow = min(uint32_t(SR_ROWS), hi - t0);
   const float4* cu = reinterpret_cast<const float4*>(cents + (size_t(u) * c_cap + t0) * D);
+  // the tile and q go to shared memory by cp.async: every 16-B piece of the
+  // 64 KB tile is in flight at once (a load-then-store loop keeps one)
   for (uint32_t e = threadIdx.x; e < nrow * (D / 4); e += SR_ROWS)
-    *reinterpret_cast<float4*>(crow + (e / (D / 4)) * SR_LD + 4 * (e % (D / 4))) = __ldg(cu + e);
+    sr_cp_async16(crow + (e / (D / 4)) * SR_LD + 4 * (e % (D / 4)), cu + e);
   const float4* qu = reinterpret_cast<const float4*>(q + size_t(u) * G * D);
   for (uint32_t e = threadIdx.x; e < G * D / 4; e += SR_ROWS)
-    reinterpret_cast<float4*>(qs)[e] = __ldg(qu + e);
+    sr_cp_async16(qs + 4 * e, qu + e);
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   // |q| of each head by a warp (a lane per 4 dims + shuffles), not one
   // thread's 128-long dependent chain that the whole block would wait for
