@@ -830,11 +830,31 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
   if (tid == 0) { s_flag = 0; s_bad = 0; }
   __syncthreads();
   int bad = 0, nonzero = 0;
-  for (uint32_t e = tid; e < rows * D; e += KS_THREADS) {
-    const uint32_t r = e / D, j = e % D;
-    const uint16_t b = kb[size_t(r) * D + j];
-    kt[j * RS + r] = b;
-    if ((b & 0x7f80u) == 0x7f80u) bad = 1;
+  // 16-B loads, four rounds in flight per thread before any is stored (a
+  // load-then-store loop of 2-B elements serialises ~160 global latencies)
+  const uint4* kb4 = reinterpret_cast<const uint4*>(kb);
+  const uint32_t n4 = rows * (D / 8);
+  for (uint32_t v0 = tid; v0 < n4; v0 += 4 * KS_THREADS) {
+    uint4 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t v = v0 + k * KS_THREADS;
+      x[k] = v < n4 ? __ldg(kb4 + v) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t v = v0 + k * KS_THREADS;
+      if (v < n4) {
+        const uint32_t r = v / (D / 8), j0 = (v % (D / 8)) * 8;
+        const uint32_t w[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint16_t b = uint16_t(w[i >> 1] >> (16 * (i & 1)));
+          kt[(j0 + i) * RS + r] = b;
+          if ((b & 0x7f80u) == 0x7f80u) bad = 1;
+        }
+      }
+    }
   }
   __syncthreads();
   for (uint32_t r = tid; r < rows; r += KS_THREADS) {
