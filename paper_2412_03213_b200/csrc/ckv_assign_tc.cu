@@ -1040,7 +1040,7 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
 //
 // The update of pass t recomputes only the clusters whose member set changed
 // (k_update's dirty flags); every other centroid -- hence its direction and
-// bf16 operand -- is bit-identical to the one the previous pass scored.  For a
+// fp16 operand -- is bit-identical to the one the previous pass scored.  For a
 // key whose current label a did not move, s(i, c) is unchanged for every
 // unmoved c, and a was the first maximum over all c last pass; so the new
 // first maximum lies in {a} U moved.  Such a key ("R") is scored against the
@@ -1126,7 +1126,7 @@ k_mcr_plan(uint32_t n, uint32_t C, uint32_t c_pad, uint32_t c_stride, uint32_t l
 }
 
 // work list of the ON units (F tiles x every column range, then R tiles x
-// the moved columns), the permuted bf16 B operand, the dense-unit mask
+// the moved columns), the permuted fp16 B operand, the dense-unit mask
 __global__ void __launch_bounds__(256)
 k_mcr_emit(uint32_t U, uint32_t C, uint32_t c_pad, uint32_t tiles, uint32_t rc,
            uint32_t n_ranges, const int32_t* __restrict__ mode, const uint32_t* __restrict__ cnt,
