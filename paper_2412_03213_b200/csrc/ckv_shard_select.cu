@@ -505,7 +505,11 @@ k_select_approx(ckv_shard_select_desc d, uint32_t p2, const float* __restrict__ 
   uint32_t* incl = id + p2;                                                 // [p2]
   uint32_t* loc = incl + p2;                                                // [p2 + 1]
   uint32_t* sz = loc + p2 + 1;                                              // [p2]
-  float* av = reinterpret_cast<float*>(sz + p2);                            // [p2]
+  // the approximate scores and bounds share the key array's bytes: they are
+  // last read (the candidate set S) before the barrier that precedes the
+  // first key write, and the exhaustive path never reads them (a quarter
+  // less shared memory per head: 4 instead of 3 heads per SM at C = 1638)
+  float* av = reinterpret_cast<float*>(smraw);                              // [p2]
   float* ev = av + p2;                                                      // [p2]
   __shared__ uint32_t s_taken, s_wsum[SR_THREADS / 32], s_hist[256], s_n, s_bin, s_above;
   __shared__ float s_lo[SR_THREADS / 32];
@@ -928,7 +932,7 @@ int ckv_select_approx(ckv_ctx* ctx, const ckv_shard_select_desc* d, const float*
   if (d->n_q == 0) return CKV_OK;
   uint32_t p2 = 32;
   while (p2 < d->C) p2 <<= 1;
-  const size_t smem = size_t(p2) * 8 + size_t(p2) * 4 * 4 + 4 + size_t(p2) * 4 * 2 + 16;
+  const size_t smem = size_t(p2) * 8 + size_t(p2) * 4 * 4 + 4 + 16;  // av/ev alias key
   static int attr = 0;
   if (!attr) {
     CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_approx, cudaFuncAttributeMaxDynamicSharedMemorySize,
