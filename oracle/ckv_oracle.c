@@ -14,6 +14,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
+#include <unistd.h>
 
 static __thread char g_err[256];
 static int fail(const char* msg) {
@@ -209,11 +210,93 @@ void orc_kmeans_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows_
   free(pool);
 }
 
+/* Cosine assignment of keys [i0, i1) with four centroids' dot_f64 chains
+ * interleaved.  Each chain is still the sequential f64 sum of
+ * common.hpp:86-90 (no contraction: -ffp-contract=off), and the candidates
+ * are compared in ascending id with strict '>', so the result equals
+ * scorer_assign bit for bit; the interleave only hides the add latency so
+ * the checker finishes the headline shapes (32k / 128k keys) in seconds. */
+static void assign_cosine_range(const scorer_t* s, const float* keys, uint32_t i0, uint32_t i1,
+                                int32_t* out) {
+  const uint32_t C = s->C, d = s->d;
+  double* kd = (double*)malloc(sizeof(double) * d);
+  for (uint32_t i = i0; i < i1; ++i) {
+    const float* key = keys + (size_t)i * d;
+    for (uint32_t j = 0; j < d; ++j) kd[j] = (double)key[j];
+    uint32_t best = 0;
+    double best_score = -INFINITY;
+    uint32_t c = 0;
+    for (; c + 4 <= C; c += 4) {
+      const float* d0 = s->dirs + (size_t)c * d;
+      const float* d1 = d0 + d;
+      const float* d2 = d1 + d;
+      const float* d3 = d2 + d;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (uint32_t j = 0; j < d; ++j) {
+        a0 += kd[j] * (double)d0[j];
+        a1 += kd[j] * (double)d1[j];
+        a2 += kd[j] * (double)d2[j];
+        a3 += kd[j] * (double)d3[j];
+      }
+      if (a0 > best_score) { best_score = a0; best = c; }
+      if (a1 > best_score) { best_score = a1; best = c + 1; }
+      if (a2 > best_score) { best_score = a2; best = c + 2; }
+      if (a3 > best_score) { best_score = a3; best = c + 3; }
+    }
+    for (; c < C; ++c) {
+      double v = orc_dot_f64(key, s->dirs + (size_t)c * d, d);
+      if (v > best_score) { best_score = v; best = c; }
+    }
+    out[i] = (int32_t)best;
+  }
+  free(kd);
+}
+
+typedef struct {
+  const scorer_t* s;
+  const float* keys;
+  uint32_t i0, i1;
+  int32_t* out;
+} assign_job_t;
+
+static void* assign_job(void* p) {
+  const assign_job_t* j = (const assign_job_t*)p;
+  assign_cosine_range(j->s, j->keys, j->i0, j->i1, j->out);
+  return NULL;
+}
+
+/* host threads for the checker's large assignments: ORC_THREADS, else all
+ * online cores */
+static uint32_t oracle_threads(void) {
+  const char* e = getenv("ORC_THREADS");
+  long n = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+  if (n < 1) n = 1;
+  if (n > 256) n = 256;
+  return (uint32_t)n;
+}
+
 static void assign_all(const float* keys, uint32_t n, uint32_t d, int metric,
                        const float* cents, uint32_t C, int32_t* out) {
   scorer_t s;
   scorer_init(&s, metric, cents, C, d);
-  for (uint32_t i = 0; i < n; ++i) out[i] = (int32_t)scorer_assign(&s, keys + (size_t)i * d);
+  if (metric != ORC_METRIC_COSINE) {
+    for (uint32_t i = 0; i < n; ++i) out[i] = (int32_t)scorer_assign(&s, keys + (size_t)i * d);
+    scorer_free(&s);
+    return;
+  }
+  uint32_t nt = oracle_threads();
+  if ((uint64_t)n * C < (1ull << 21) || nt == 1 || n < 2 * nt) {
+    assign_cosine_range(&s, keys, 0, n, out);
+  } else {
+    pthread_t th[256];
+    assign_job_t jobs[256];
+    for (uint32_t t = 0; t < nt; ++t) {
+      jobs[t] = (assign_job_t){&s, keys, (uint32_t)((uint64_t)n * t / nt),
+                               (uint32_t)((uint64_t)n * (t + 1) / nt), out};
+      pthread_create(&th[t], NULL, assign_job, &jobs[t]);
+    }
+    for (uint32_t t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+  }
   scorer_free(&s);
 }
 

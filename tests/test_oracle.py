@@ -69,6 +69,20 @@ def test_kmeans_select_attention_port_vs_reference(port, ref, L, seed):
         assert np.array_equal(oa, ob) and np.array_equal(wa, wb)
 
 
+@pytest.mark.parametrize("n,C_", [(16384, 205), (9000, 403)])
+def test_threaded_assign_port_vs_reference(port, ref, n, C_):
+    """The port's multi-threaded, 4-chain-interleaved cosine assignment (the
+    path large checks take, n*C >= 2^21) equals the reference's sequential
+    AssignScorer (clustering.hpp:104-115) — C odd and not a multiple of 4
+    exercises the tail chain."""
+    tr = port.generate_head(port.mix_seed(7, 3, n), n + 16, 4)
+    K = to_bf16_representable(tr.prompt_keys[16:])
+    a, b = port.kmeans(K, C_, 5, 2), ref.kmeans(K, C_, 5, 2)
+    assert a.iterations_used == b.iterations_used == 2
+    assert np.array_equal(a.labels, b.labels)
+    assert np.array_equal(a.centroids.view(np.uint32), b.centroids.view(np.uint32))
+
+
 def test_repair_and_decode_batch_port_vs_reference(port, ref):
     rng = np.random.default_rng(5)
     base = rng.standard_normal((6, 128)).astype(np.float32)
