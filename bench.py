@@ -277,12 +277,46 @@ def _events(torch, n):
 
 
 def _max_over_ranks(torch, dev, world, vals):
+    """Max over ranks of per-rank device-timed values (NCCL on the device;
+    host tensors under gloo, i.e. CKV_BENCH_SHARE_GPU)."""
     if world == 1:
-        return vals
+        return list(vals)
     import torch.distributed as dist
-    t = torch.tensor(vals, device=dev, dtype=torch.float64)
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor(vals, device=dev if on_dev else "cpu", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(x) for x in t.tolist()]
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_world(n: int) -> None:
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run with N local ranks (one per GPU, 127.0.0.1
+    rendezvous).  Fails loudly when fewer than N GPUs are visible, unless
+    CKV_BENCH_SHARE_GPU=1 (test mode: every rank on cuda:0, gloo)."""
+    if os.environ.get("CKV_BENCH_SHARE_GPU") != "1":
+        import torch
+        vis = torch.cuda.device_count()
+        if vis < n:
+            raise SystemExit(f"bench.py --gpus {n}: only {vis} visible GPU(s); "
+                             "one rank per GPU is required")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def rank_device(local: int) -> int:
+    """CUDA device of this rank: LOCAL_RANK, or 0 for every rank in the
+    shared-GPU test mode."""
+    return 0 if os.environ.get("CKV_BENCH_SHARE_GPU") == "1" else local
 
 
 def unique_kv_rows(torch, run_row, run_off, run_cnt, group, p_cap):
@@ -806,9 +840,13 @@ def main():
                     help="k-means cap (profiling only; the bench default is the reference's 50)")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return spawn_world(args.gpus)  # one process per GPU (torchrun re-exec)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus and args.impl == "ours":
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    local = rank_device(int(os.environ.get("LOCAL_RANK", "0")))
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -817,7 +855,10 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("CKV_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_2412_03213_b200 import _native as N
     from paper_2412_03213_b200.api import ClusterConfig, Context
     from paper_2412_03213_b200.session import Session
@@ -946,9 +987,7 @@ def main():
         soak(0.2)
     step_ms = ev[0].elapsed_time(ev[1]) / args.steps
     if world > 1:
-        tt = torch.tensor([step_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        step_ms = float(tt.item())
+        step_ms = _max_over_ranks(torch, dev, world, [step_ms])[0]
         dist.barrier()
 
     # ---- per-kernel timing of one step's select and attend --------------
@@ -1041,9 +1080,7 @@ def main():
         t += 1
     e2e_ms = float(np.mean(e2e_times[1:] if len(e2e_times) > 1 else e2e_times))
     if world > 1:
-        tt = torch.tensor([e2e_ms, prefill_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms, prefill_ms = float(tt[0].item()), float(tt[1].item())
+        e2e_ms, prefill_ms = _max_over_ranks(torch, dev, world, [e2e_ms, prefill_ms])
 
     # ---- CPU baseline (rank 0, N=1 only) ---------------------------------
     cpu = None

@@ -216,6 +216,7 @@ class Oracle:
                                                       C.c_uint32, u32p, C.POINTER(C.c_uint32),
                                                       u32p, C.POINTER(C.c_uint32)]
             L.ref_cache_counters.argtypes = [C.c_void_p, u64p]
+            L.ref_cache_invalidate.argtypes = [C.c_void_p, u32p, C.c_uint32]
             L.ref_decode_step_cpu.restype = C.c_double
             L.ref_decode_step_cpu.argtypes = [f32p, u32p, C.c_uint32, C.c_void_p, u32p,
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
@@ -504,6 +505,13 @@ class OracleCache:
             self.o.lib.ref_cache_lookup_and_update(self.h, s, n, z, len(sizes), hit, C.byref(nh),
                                                    miss, C.byref(nm))
         return hit[: nh.value], miss[: nm.value]
+
+    def invalidate_on_recluster(self, retired, fresh=()):
+        """cache.hpp:65-76: drop retired ids from every retained set."""
+        r = np.ascontiguousarray(retired, np.uint32)
+        if len(r):
+            (self.o.lib.orc_cache_invalidate if self.o.kind == "port"
+             else self.o.lib.ref_cache_invalidate)(self.h, r, len(r))
 
     def counters(self) -> np.ndarray:
         out = np.zeros(4, np.uint64)

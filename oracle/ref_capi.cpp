@@ -266,6 +266,10 @@ void ref_cache_lookup_and_update(void* c, const uint32_t* sel, uint32_t n_sel,
   *n_hit = uint32_t(r.hit_ids.size());
   *n_miss = uint32_t(r.miss_ids.size());
 }
+void ref_cache_invalidate(void* c, const uint32_t* retired, uint32_t n) {
+  static_cast<R::ClusterCache*>(c)->invalidate_on_recluster(
+      std::span<const uint32_t>(retired, n), std::span<const uint32_t>());
+}
 void ref_cache_counters(void* c, uint64_t* out) {
   const auto& k = static_cast<R::ClusterCache*>(c)->counters();
   out[0] = k.clusters_requested;

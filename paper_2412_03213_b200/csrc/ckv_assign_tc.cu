@@ -930,20 +930,20 @@ size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
 // k_assign_tc with as many key-tile stages as fit next to B (rc columns)
 static int launch_tc(cudaStream_t st, const CUtensorMap& kmap, const CUtensorMap& dmap,
                      TcArgs& ta) {
-  static size_t max_dyn = 0;  // opt-in per-CTA smem minus the kernel's static part
-  static int attr_dev = -1;
+  // opt-in per-CTA smem minus the kernel's static part, per device
+  static size_t max_dyn_dev[64];
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
+  CKV_CUDA_TRY(cudaGetDevice(&dev));
+  size_t max_dyn = max_dyn_dev[dev & 63];
+  if (max_dyn == 0) {
     int optin = 0;
     cudaFuncAttributes fa;
     CKV_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     CKV_CUDA_TRY(cudaFuncGetAttributes(&fa, k_assign_tc));
     max_dyn = size_t(optin) - fa.sharedSizeBytes;
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(max_dyn)));
-    attr_dev = dev;
   }
+  CKV_CUDA_TRY(smem_optin((const void*)k_assign_tc, int(max_dyn)));
+  max_dyn_dev[dev & 63] = max_dyn;
   static const uint32_t tc_mode = getenv("CKV_TC_MODE") ? uint32_t(atoi(getenv("CKV_TC_MODE"))) : 0u;
   ta.mode = tc_mode;
   const size_t fixed = 1024 + 2 * size_t(ta.rc) * 128;

@@ -420,20 +420,17 @@ int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
   if (desc.n_q == 0 || desc.max_tokens == 0) return CKV_OK;
   const uint32_t splits = attend_splits(desc);
   const size_t smem = sizeof(AttSmem);
-  static int attr_dev = -1;
-  static int per_sm = 1;
+  static int per_sm_dev[64];  // resident CTAs per SM, per device (0 = not queried yet)
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    for (auto fn : {k_attend<false>, k_attend<true>}) {
-      CKV_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(smem)));
-      CKV_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        cudaSharedmemCarveoutMaxShared));
-    }
+  CKV_CUDA_TRY(cudaGetDevice(&dev));
+  for (const void* fn : {(const void*)k_attend<false>, (const void*)k_attend<true>})
+    CKV_CUDA_TRY(smem_optin(fn, int(smem), true));
+  int per_sm = per_sm_dev[dev & 63];
+  if (per_sm == 0) {
     CKV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<false>,
                                                                AT_THREADS, smem));
-    attr_dev = dev;
+    per_sm = per_sm < 1 ? 1 : per_sm;
+    per_sm_dev[dev & 63] = per_sm;
   }
   const uint32_t n_items = desc.n_q * splits;
   const uint32_t grid = std::min<uint32_t>(n_items, uint32_t(std::max(1, per_sm)) * num_sms());

@@ -5,7 +5,10 @@
 #include <cstdio>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <random>
+#include <set>
+#include <tuple>
 #include <unordered_map>
 #include <string>
 #include <thread>
@@ -72,6 +75,23 @@ static uint64_t splitmix64(uint64_t x) {
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
   return x ^ (x >> 31);
 }
+cudaError_t smem_optin(const void* fn, int bytes, bool max_carveout) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  const auto key = std::make_tuple(fn, dev, bytes);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && max_carveout)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
+}
+
 uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b) {
   uint64_t h = splitmix64(seed);
   h = splitmix64(h ^ (a + 0x9e3779b97f4a7c15ull));
@@ -515,6 +535,18 @@ int ckv_select(ckv_ctx* ctx, const ckv_select_desc* d, const float* q, const flo
     set_error("ckv_select: runs.run_cap must be >= c_cap + 2");
     return CKV_EINVAL;
   }
+  if (cache && cache->dev.c_cap < d->c_cap) {
+    set_error("ckv_select: cache c_cap is smaller than the selection's c_cap");
+    return CKV_EINVAL;
+  }
+  if (token_ids || rows) {  // |I_T| <= min(B, labeled) + sinks + recency (selection.hpp:88-89)
+    const uint64_t need = uint64_t(std::min(d->budget, d->p_cap)) + d->sink_count +
+                          (d->rec_end > d->rec_begin ? d->rec_end - d->rec_begin : 0);
+    if (d->sel_cap < need) {
+      set_error("ckv_select: sel_cap < min(budget, p_cap) + sink_count + (rec_end - rec_begin)");
+      return CKV_EINVAL;
+    }
+  }
   void* scratch = nullptr;
   CKV_CUDA_TRY(cudaMallocAsync(&scratch, select_scratch_bytes(d->n_q, d->c_cap), ctx->stream));
   int rc = launch_select(ctx->stream, *d, q, centroids, n_clusters, sizes, starts, sorted_ids,
@@ -652,6 +684,10 @@ int ckv_attend(ckv_ctx* ctx, const ckv_attend_desc* d, const float* q, const uin
                const uint16_t* V, const uint32_t* rows, const ckv_runs* runs,
                const uint32_t* n_tokens, float* out, float* weights) {
   cudaStream_t st = ctx->stream;
+  if (weights && d->max_tokens > d->sel_cap) {  // weights rows are sel_cap apart
+    set_error("ckv_attend: max_tokens > sel_cap with a weights output");
+    return CKV_EINVAL;
+  }
   if (weights) {  // parity mode: approx_attention's empty-selection check
     std::vector<uint32_t> nt(d->n_q);
     CKV_CUDA_TRY(cudaMemcpyAsync(nt.data(), n_tokens, 4 * size_t(d->n_q),
@@ -709,6 +745,34 @@ int salloc(T** p, size_t count) {
 
 extern "C" {
 
+// The persisting-L2 limit is device-wide state: reference-count the sessions
+// that raised it, remember the caller's value before the first one, and
+// restore it (and drop the persisting lines) only when the last one goes.
+static std::mutex g_l2_mu;
+static int g_l2_refs[64];
+static size_t g_l2_saved[64];
+
+static bool l2_persist_acquire(int dev, size_t want) {
+  std::lock_guard<std::mutex> lock(g_l2_mu);
+  const int i = dev & 63;
+  size_t cur = 0;
+  if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess) return false;
+  if (g_l2_refs[i] == 0) g_l2_saved[i] = cur;
+  if (want > cur && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess)
+    return false;
+  ++g_l2_refs[i];
+  return true;
+}
+
+static void l2_persist_release(int dev) {
+  std::lock_guard<std::mutex> lock(g_l2_mu);
+  const int i = dev & 63;
+  if (g_l2_refs[i] > 0 && --g_l2_refs[i] == 0) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_saved[i]);
+  }
+}
+
 int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** out) {
   if (d->group < 1 || d->budget < 1 || d->decode_batch < 1 || d->c_plus < 1 ||
       d->max_iters < 1 || d->c0_divisor < 1) {
@@ -757,12 +821,11 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   if (rc) { ckv_session_destroy(s); return CKV_ENOMEM; }
   cudaMemsetAsync(s->tickets, 0, size_t(s->n_q) * 4, ctx->stream);
   cudaMemsetAsync(s->n_clusters, 0, size_t(s->U) * 4, ctx->stream);
-  if (d->flags & CKV_SESSION_L2_PERSIST) {  // device-wide; restored at destroy
+  if (d->flags & CKV_SESSION_L2_PERSIST) {  // device-wide; restored by the last user
     int maxp = 0;
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
     const size_t want = std::min<size_t>(size_t(maxp), size_t(s->U) * s->c_cap * D * 4);
-    if (want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
-      s->l2_persist = true;
+    s->l2_persist = want && l2_persist_acquire(ctx->device, want);
     cudaGetLastError();
   }
   if (d->retention > 0) {
@@ -791,10 +854,7 @@ int ckv_session_destroy(ckv_session* s) {
   cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
   cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
   ckv_cache_destroy(s->cache);
-  if (s->l2_persist) {
-    cudaCtxResetPersistingL2Cache();
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-  }
+  if (s->l2_persist) l2_persist_release(s->ctx->device);
   delete s;
   return CKV_OK;
 }

@@ -166,12 +166,7 @@ int launch_index(cudaStream_t st, uint32_t n_units, const int32_t* labels, uint3
     return CKV_EINVAL;
   }
   size_t smem = size_t(W) * c_cap * 4;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_index, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(budget)));
-    attr_set = true;
-  }
+  CKV_CUDA_TRY(smem_optin((const void*)k_index, int(budget)));
   k_index<<<n_units, W * 32, smem, st>>>(labels, n_pos, p_cap, c_cap, n_clusters, c_uniform,
                                          sizes, starts, sorted_ids, prev_labels, changed, active,
                                          any_empty, dirty);

@@ -112,6 +112,10 @@ int ctx_scratch(ckv_ctx* ctx, int slot, size_t bytes, bool zero_new, void** out)
 int attend_scratch(ckv_ctx* ctx, const ckv_attend_desc& d, bool weights, float** part,
                    uint32_t** tickets, float** lw);
 uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
+// cudaFuncSetAttribute(fn, MaxDynamicSharedMemorySize, bytes) (plus the
+// max-shared carveout when asked) once per (kernel, device, bytes); safe to
+// call from several host threads and for contexts on different devices
+cudaError_t smem_optin(const void* fn, int bytes, bool max_carveout = false);
 void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows);
 }  // namespace ckvb
 

@@ -1013,12 +1013,7 @@ int launch_kmeans_small(cudaStream_t st, const uint16_t* keys, uint64_t key_stri
   const size_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u, RS = ((rows + 15) & ~15u) + 1;
   const size_t smem = C4 * 8 + 2 * C4 * D * 4 + C4 * D * 2 + C4 * 4 + C4 * 4 + 2 * R2 * 4 +
                       size_t(D) * RS * 2;
-  static bool attr = false;
-  if (!attr) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_kmeans_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-    attr = true;
-  }
+  CKV_CUDA_TRY(smem_optin((const void*)k_kmeans_small, 200 * 1024));
   k_kmeans_small<<<n_units, KS_THREADS, smem, st>>>(keys, key_stride, rows, C, max_iters,
                                                      init_rows, cents, c_cap, labels,
                                                      label_stride, n_clusters, iters, status);

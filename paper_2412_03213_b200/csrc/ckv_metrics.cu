@@ -292,12 +292,7 @@ int ckv_exact_topb(ckv_ctx* ctx, uint32_t n_q, uint32_t group, uint32_t n, uint3
   uint32_t n2 = 1;
   while (n2 < Bn) n2 <<= 1;
   const size_t smem = std::max<size_t>(size_t(n) * 4, size_t(n2) * 4);
-  static bool attr = false;
-  if (!attr) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_exact_topb, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-    attr = true;
-  }
+  CKV_CUDA_TRY(smem_optin((const void*)k_exact_topb, 200 * 1024));
   k_exact_topb<<<n_q, MT_THREADS, smem, ctx->stream>>>(
       group, n, p_cap, q, keys, budget, ids, ids_cap, static_cast<unsigned long long*>(sk),
       static_cast<uint32_t*>(si));

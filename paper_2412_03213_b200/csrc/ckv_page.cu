@@ -263,12 +263,7 @@ int ckv_page_select(ckv_ctx* ctx, const ckv_page_desc* d, const float* q, const 
   if (d->n_q == 0) return CKV_OK;
   // keys [n_pages] u64 + selection [4096] + tie scratch [n_pages] u32
   const size_t smem = size_t(n_pages) * 8 + 4096 * 4 + size_t(n_pages) * 4;
-  static bool attr = false;
-  if (!attr) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_page_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      96 * 1024));
-    attr = true;
-  }
+  CKV_CUDA_TRY(smem_optin((const void*)k_page_select, 96 * 1024));
   // PageRepr::Max scores are dot_f64(q, max_rep): the register-blocked exact
   // scorer of the sharded path (all G heads of a unit per centroid-row read)
   double* sc = nullptr;

@@ -180,7 +180,9 @@ __device__ __forceinline__ void select_head(
   const uint32_t* stt = starts + size_t(unit) * (desc.c_cap + 1);
   const float4* qh4 = reinterpret_cast<const float4*>(q + size_t(h) * D);
   const bool exhaustive_req = (desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) != 0;
-  bool fast = !exhaustive_req && C <= 32u * SW_KPL;
+  // budget 0 takes no cluster (selection.hpp:91: the loop breaks at once);
+  // the exhaustive path still ranks every cluster for CKV_SEL_FULL_RANK
+  bool fast = !exhaustive_req && C <= 32u * SW_KPL && B > 0;
   uint32_t taken = 0;
 
   if (fast) {
@@ -389,6 +391,7 @@ __device__ __forceinline__ void select_head(
   dbg_stamp(h, 2);
 
   // ---- outputs ---------------------------------------------------------------
+  if (B == 0) taken = 0;
   const uint32_t full_cum = taken ? incl[taken - 1] : 0;
   const uint32_t cum = full_cum < B ? full_cum : B;
   const uint32_t trimmed = full_cum > B ? full_cum - B : 0;
@@ -677,7 +680,6 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
     set_error("select: group must be 1, 2, 4 or 8 and divide n_q");
     return CKV_EINVAL;
   }
-  if (desc.budget < 1) { set_error("select: budget must be >= 1"); return CKV_EINVAL; }
   const uint32_t units = desc.n_q / G;
   const uint32_t c_pad = (desc.c_cap + 31) / 32 * 32;
   float* aval = static_cast<float*>(scratch);
@@ -694,17 +696,9 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused) {
     const size_t smem_f = size_t(G) * warp_bytes + size_t(G) * c_pad * 8;
     if (smem_f <= 200 * 1024) {
-      static int attr_f = -1;
-      int dev_f = 0;
-      cudaGetDevice(&dev_f);
-      (void)dev_f;
-      if (attr_f != dev_f) {
-        CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_f = dev_f;
-      }
+      for (const void* fn : {(const void*)k_select_fused<1>, (const void*)k_select_fused<2>,
+                             (const void*)k_select_fused<4>, (const void*)k_select_fused<8>})
+        CKV_CUDA_TRY(smem_optin(fn, 200 * 1024));
 #define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
     token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode, q_copy
       static const uint32_t sel_mode = getenv("CKV_SEL_MODE") ? uint32_t(atoi(getenv("CKV_SEL_MODE"))) : 0u;
@@ -723,12 +717,10 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       cfg.attrs = attr + 1;
       cfg.numAttrs = 1;
       if (desc.flags & CKV_SEL_L2_PERSIST) {
-        static size_t max_win = 0;
-        if (!max_win) {
-          int v = 0;
-          cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev_f);
-          max_win = size_t(v);
-        }
+        int dev_w = 0, v = 0;
+        cudaGetDevice(&dev_w);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev_w);
+        const size_t max_win = size_t(v);
         size_t persist = 0;
         cudaDeviceGetLimit(&persist, cudaLimitPersistingL2CacheSize);
         const size_t bytes = std::min(max_win, size_t(units) * desc.c_cap * D * 4);
@@ -774,14 +766,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
     set_error("select: cluster capacity too large for the smem ranking buffers");
     return CKV_EINVAL;
   }
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-    attr_dev = dev;
-  }
+  CKV_CUDA_TRY(smem_optin((const void*)k_select_warp, 200 * 1024));
   unsigned long long* dbuf = nullptr;
   if (dbg) {
     cudaMalloc(&dbuf, size_t(desc.n_q) * 64);

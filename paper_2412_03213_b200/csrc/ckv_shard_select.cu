@@ -821,13 +821,9 @@ int ckv_score_range(ckv_ctx* ctx, uint32_t n_units, uint32_t group, const float*
                                                  scores);                                    \
     break;                                                                                   \
   }
-  static bool attr = false;
-  if (!attr) {
-    for (auto fn : {k_score_range<1>, k_score_range<2>, k_score_range<4>, k_score_range<8>})
-      CKV_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (SR_ROWS * SR_LD + 8 * D) * 4));
-    attr = true;
-  }
+  for (const void* fn : {(const void*)k_score_range<1>, (const void*)k_score_range<2>,
+                         (const void*)k_score_range<4>, (const void*)k_score_range<8>})
+    CKV_CUDA_TRY(smem_optin(fn, (SR_ROWS * SR_LD + 8 * D) * 4));
   switch (group) {
     CKV_SR(1) CKV_SR(2) CKV_SR(4) CKV_SR(8)
     default: set_error("ckv_score_range: group must be 1, 2, 4 or 8"); return CKV_EINVAL;
@@ -854,16 +850,15 @@ int ckv_select_scored(ckv_ctx* ctx, const ckv_shard_select_desc* d, const double
               "slice * world >= C, lsorted with token_ids");
     return CKV_EINVAL;
   }
+  if (token_ids && uint64_t(d->sel_cap) < uint64_t(d->budget) + d->sink_rows + d->n_rec) {
+    set_error("ckv_select_scored: sel_cap < budget + sink_rows + n_rec");
+    return CKV_EINVAL;
+  }
   if (d->n_q == 0) return CKV_OK;
   uint32_t p2 = 32;
   while (p2 < d->C) p2 <<= 1;
   const size_t smem = size_t(p2) * 8 * 2 + size_t(p2) * 4 * 5 + 4 + 8;
-  static int attr = 0;
-  if (!attr) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_scored, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-    attr = 1;
-  }
+  CKV_CUDA_TRY(smem_optin((const void*)k_select_scored, 200 * 1024));
   k_select_scored<<<d->n_q, SR_THREADS, smem, ctx->stream>>>(
       *d, p2, scores, gsize, lsize, lstart, prefix, lsorted, *runs, token_ids, n_tokens, n_taken,
       trimmed, ranked);
@@ -886,14 +881,9 @@ int ckv_score_range_approx(ckv_ctx* ctx, uint32_t n_units, uint32_t group, const
   if (n_units == 0 || c_lo >= C) return CKV_OK;
   cudaStream_t st = ctx->stream;
   const uint32_t n_q = n_units * group, c_hi = c_lo + slice;
-  static bool attr = false;
-  if (!attr) {
-    for (auto fn : {k_score_range_f32<1>, k_score_range_f32<2>, k_score_range_f32<4>,
-                    k_score_range_f32<8>})
-      CKV_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (SR_ROWS * SR_LD + 8 * D) * 4));
-    attr = true;
-  }
+  for (const void* fn : {(const void*)k_score_range_f32<1>, (const void*)k_score_range_f32<2>,
+                         (const void*)k_score_range_f32<4>, (const void*)k_score_range_f32<8>})
+    CKV_CUDA_TRY(smem_optin(fn, (SR_ROWS * SR_LD + 8 * D) * 4));
 #define CKV_SA(GG)                                                                           \
   case GG: {                                                                                 \
     dim3 grid(n_units, (slice + SR_ROWS - 1) / SR_ROWS);                                     \
@@ -929,16 +919,15 @@ int ckv_select_approx(ckv_ctx* ctx, const ckv_shard_select_desc* d, const float*
               "slice * world >= C, lsorted with token_ids");
     return CKV_EINVAL;
   }
+  if (token_ids && uint64_t(d->sel_cap) < uint64_t(d->budget) + d->sink_rows + d->n_rec) {
+    set_error("ckv_select_approx: sel_cap < budget + sink_rows + n_rec");
+    return CKV_EINVAL;
+  }
   if (d->n_q == 0) return CKV_OK;
   uint32_t p2 = 32;
   while (p2 < d->C) p2 <<= 1;
   const size_t smem = size_t(p2) * 8 + size_t(p2) * 4 * 4 + 4 + 16;  // av/ev alias key
-  static int attr = 0;
-  if (!attr) {
-    CKV_CUDA_TRY(cudaFuncSetAttribute(k_select_approx, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-    attr = 1;
-  }
+  CKV_CUDA_TRY(smem_optin((const void*)k_select_approx, 200 * 1024));
   k_select_approx<<<d->n_q, SR_THREADS, smem, ctx->stream>>>(
       *d, p2, ascores, q, centroids, gsize, lsize, lstart, prefix, lsorted, *runs, token_ids,
       n_tokens, n_taken, trimmed, ranked);

@@ -144,14 +144,16 @@ def read_trace(path: str, mmap: bool = True) -> TraceBundle:
         meta = fh.read(meta_len)
         if len(meta) != meta_len:
             raise ParseError(ParseCode.Truncated, "trace file: truncated payload")
+        # the reference parses the metadata before its trailing-byte check
+        # (trace.hpp:353-365), so corrupt metadata wins over extra bytes
+        try:
+            md = json.loads(meta.decode("utf-8"))
+            if not isinstance(md, dict) or not all(isinstance(v, str) for v in md.values()):
+                raise ValueError
+        except (ValueError, UnicodeDecodeError):
+            raise ParseError(ParseCode.BadMetadata, "trace file: corrupt metadata block")
         if fh.read(1):
             raise ParseError(ParseCode.TrailingData, "trace file: trailing data")
-    try:
-        md = json.loads(meta.decode("utf-8"))
-        if not isinstance(md, dict) or not all(isinstance(v, str) for v in md.values()):
-            raise ValueError
-    except (ValueError, UnicodeDecodeError):
-        raise ParseError(ParseCode.BadMetadata, "trace file: corrupt metadata block")
     traces = []
     off = 0
     for _ in range(heads):

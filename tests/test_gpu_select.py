@@ -112,3 +112,81 @@ def test_cache_sequence_vs_oracle(gpu_ctx):
                 c["bytes_transferred"]] == [int(x) for x in oc]
     with pytest.raises(ValueError):
         api.ClusterCache(0, 128)
+
+
+def test_select_budget_zero_vs_oracle(gpu_ctx):
+    """Budget 0 takes no cluster (selection.hpp:91 breaks at once): I_T is
+    the sinks then the recency, the full ranking is still returned."""
+    from paper_2412_03213_b200 import api
+    h = head(7, 0, 1, 2048, T=8)
+    seed = port().mix_seed(0, 0, 1)
+    o = port().cluster_prefill(h["K"], OCfg(seed=seed))
+    m = _model(o.labels, o.centroids, o.sink_count)
+    ix = api.build_index(m)
+    rec = np.arange(2048, 2048 + 5, dtype=np.uint32)
+    g = api.select_tokens(h["Q"][3], m, ix, 0, rec)
+    r = port().select_tokens(h["Q"][3], o.centroids, o.labels, o.sink_count, 0, rec)
+    assert g.n_clusters_taken == r.n_clusters_taken == 0 and g.trimmed_from_last == 0
+    assert np.array_equal(g.token_ids, r.token_ids)
+    assert np.array_equal(g.ranked_clusters, r.ranked_clusters)
+
+
+def test_select_capacity_checks(gpu_ctx):
+    """The C-ABI rejects a token / row buffer too small for min(B, p_cap) +
+    sinks + recency, and a cache narrower than the selection's c_cap, before
+    any kernel could write out of range (CKV_EINVAL)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2412_03213_b200 import _native as N
+    dev = gpu_ctx.device
+    n_q, c_cap, p_cap, B = 2, 64, 512, 100
+    z = lambda n, dt=torch.int32: torch.zeros(n, dtype=dt, device=dev)
+    q, cents = z(n_q * 128, torch.float32), z(n_q * c_cap * 128, torch.float32)
+    ncl, sizes, starts, srt = z(n_q), z(n_q * c_cap), z(n_q * (c_cap + 1)), z(n_q * p_cap)
+    outs = [z(n_q) for _ in range(3)]
+    ranked = z(n_q * c_cap)
+    for sel_cap, ok in ((B + 16 + 4, True), (B + 16 + 3, False)):
+        tok = z(n_q * sel_cap)
+        sd = N.SelectDesc(n_q, 1, B, 16, p_cap, c_cap, sel_cap, 600, 604, 0, 0)
+        rc = N.lib().ckv_select(gpu_ctx.h, C.byref(sd), q.data_ptr(), cents.data_ptr(),
+                                ncl.data_ptr(), sizes.data_ptr(), starts.data_ptr(),
+                                srt.data_ptr(), tok.data_ptr(), None, None,
+                                *[o.data_ptr() for o in outs], ranked.data_ptr(), None, None)
+        assert (rc == N.CKV_OK) == ok, (sel_cap, rc)
+    cache = C.c_void_p()
+    N.check(N.lib().ckv_cache_create(gpu_ctx.h, n_q, c_cap // 2, 1, 128, C.byref(cache)))
+    try:
+        sd = N.SelectDesc(n_q, 1, B, 16, p_cap, c_cap, B + 20, 600, 604, 0, 0)
+        rc = N.lib().ckv_select(gpu_ctx.h, C.byref(sd), q.data_ptr(), cents.data_ptr(),
+                                ncl.data_ptr(), sizes.data_ptr(), starts.data_ptr(),
+                                srt.data_ptr(), None, None, None, *[o.data_ptr() for o in outs],
+                                ranked.data_ptr(), None, cache)
+        assert rc == N.CKV_EINVAL
+    finally:
+        N.lib().ckv_cache_destroy(cache)
+    torch.cuda.synchronize()
+
+
+def test_cache_invalidate_on_recluster_vs_oracle(gpu_ctx):
+    """cache.hpp:65-76: retired ids leave every retained set; later lookups
+    (hits, misses, counters) match the reference's ClusterCache."""
+    from paper_2412_03213_b200 import api
+    rng = np.random.default_rng(3)
+    sizes = rng.integers(1, 90, 300).astype(np.uint32)
+    for R in (1, 2, 3):
+        g = api.ClusterCache(R, 128, c_cap=320)
+        o = port().cache(R)
+        for t in range(30):
+            sel = np.sort(rng.choice(300, rng.integers(1, 25), replace=False)).astype(np.uint32)
+            gh, gm = g.lookup_and_update(sel, sizes)
+            oh, om = o.lookup_and_update(sel, sizes)
+            assert np.array_equal(gh, oh) and np.array_equal(gm, om), (R, t)
+            if t % 3 == 1:
+                dead = rng.choice(300, 40, replace=False).astype(np.uint32)
+                g.invalidate_on_recluster(dead)
+                o.invalidate_on_recluster(dead)
+        c = g.counters()
+        assert [c["clusters_requested"], c["clusters_hit"], c["tokens_transferred"],
+                c["bytes_transferred"]] == [int(x) for x in o.counters()]

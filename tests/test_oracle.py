@@ -109,6 +109,9 @@ def test_cache_port_vs_reference(port, ref):
             sel = np.sort(rng.choice(100, 10, replace=False)).astype(np.uint32)
             ha, hb = a.lookup_and_update(sel, sizes), b.lookup_and_update(sel, sizes)
             assert all(np.array_equal(p, q) for p, q in zip(ha, hb))
+            dead = rng.choice(100, 6, replace=False).astype(np.uint32)
+            a.invalidate_on_recluster(dead)
+            b.invalidate_on_recluster(dead)
         assert np.array_equal(a.counters(), b.counters())
 
 

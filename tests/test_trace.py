@@ -60,6 +60,8 @@ CASES = {
     "short_header": (lambda r: r[:10], T.ParseCode.Truncated),
     "trailing": (lambda r: r + b"x", T.ParseCode.TrailingData),
     "bad_meta": (lambda r: r[:-3] + b"}}}", T.ParseCode.BadMetadata),
+    # corrupt metadata AND trailing bytes: the reference reports the metadata
+    "bad_meta_trailing": (lambda r: r[:-3] + b"}}}" + b"xy", T.ParseCode.BadMetadata),
 }
 
 
