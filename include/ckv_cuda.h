@@ -474,6 +474,15 @@ typedef struct {
   uint32_t kv_heads;       /* for the per-unit seed derivation          */
   uint32_t flags;          /* CKV_KM_* for the prefill k-means, plus    */
                            /* CKV_SESSION_TOKEN_IDS                     */
+  uint32_t async_delay;    /* 0: decode batches are clustered and join  */
+                           /* the model at the step that completes them */
+                           /* (synchronous).  d > 0: the harness's      */
+                           /* async_clustering (harness.hpp:236-243,    */
+                           /* 327-329): the batch's k-means runs on a   */
+                           /* side stream and joins d steps later; its  */
+                           /* rows stay in the recency window until     */
+                           /* then.  Needs d < decode_batch <= 512,     */
+                           /* c_plus <= 32.                             */
 } ckv_session_desc;
 
 /* Also materialise each step's I_T as reference token positions

@@ -64,7 +64,8 @@ class SessionDesc(C.Structure):
     _fields_ = [("n_units", u32), ("group", u32), ("prompt_len", u32), ("max_decode", u32),
                 ("budget", u32), ("retention", u32), ("c0_divisor", u32), ("c_plus", u32),
                 ("decode_batch", u32), ("sink_tokens", u32), ("max_iters", u32),
-                ("cluster_seed", u64), ("kv_heads", u32), ("flags", u32)]
+                ("cluster_seed", u64), ("kv_heads", u32), ("flags", u32),
+                ("async_delay", u32)]
 
 
 class KmShardDesc(C.Structure):

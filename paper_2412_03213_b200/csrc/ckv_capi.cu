@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <random>
 #include <set>
@@ -75,6 +76,24 @@ static uint64_t splitmix64(uint64_t x) {
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
   return x ^ (x >> 31);
 }
+bool trace_on() {
+  static const bool on = getenv("CKV_TRACE_HOST") != nullptr;
+  return on;
+}
+static thread_local std::chrono::steady_clock::time_point g_trace_t0;
+void trace_begin(const char* what) {
+  if (!trace_on()) return;
+  g_trace_t0 = std::chrono::steady_clock::now();
+  fprintf(stderr, "[ckv trace] %s: begin\n", what);
+}
+void trace_mark(const char* what, long arg) {
+  if (!trace_on()) return;
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                              g_trace_t0).count();
+  if (arg >= 0) fprintf(stderr, "[ckv trace] %9.3f ms %s %ld\n", ms, what, arg);
+  else fprintf(stderr, "[ckv trace] %9.3f ms %s\n", ms, what);
+}
+
 cudaError_t smem_optin(const void* fn, int bytes, bool max_carveout) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -240,6 +259,152 @@ __global__ void k_relayout_batch(uint16_t* __restrict__ K, uint16_t* __restrict_
   }
 }
 
+// ---- cluster_decode_batch's init rows on the device ----------------------
+// clustering.hpp:186-193 with seed mix_seed(seed_u, 0xdecade, pos0)
+// (clustering.hpp:318-320): a partial Fisher-Yates over 0..n-1 driven by
+// std::mt19937_64 (bit-specified by the C++ standard; uniform_below = rng() %
+// m, common.hpp:124-126).  Only the first C <= 32 outputs are drawn, and the
+// first twist's output k needs just the seeded words k, k+1 and k+156, so a
+// thread per unit computes them in one pass of the seeding recurrence; the
+// pool is kept sparse (the <= 2C touched slots).
+constexpr uint32_t DI_MAX_C = 32;
+
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__global__ void k_decode_init_rows(const uint64_t* __restrict__ seeds, uint32_t n_units,
+                                   uint64_t pos0, uint32_t n, uint32_t C,
+                                   uint32_t* __restrict__ rows) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  // mix_seed(seed, 0xdecade, pos0) (common.hpp:108-113)
+  uint64_t h = d_splitmix64(seeds[u]);
+  h = d_splitmix64(h ^ (0xdecadeull + 0x9e3779b97f4a7c15ull));
+  const uint64_t seed = d_splitmix64(h ^ (pos0 + 0xbf58476d1ce4e5b9ull));
+  uint64_t lo[DI_MAX_C + 1], hi[DI_MAX_C];
+  uint64_t x = seed;
+  lo[0] = x;
+  for (uint32_t i = 1; i < 156 + C; ++i) {
+    x = 6364136223846793005ull * (x ^ (x >> 62)) + i;
+    if (i <= C) lo[i] = x;
+    if (i >= 156) hi[i - 156] = x;
+  }
+  uint32_t key[2 * DI_MAX_C], val[2 * DI_MAX_C];
+  uint32_t nk = 0;
+  auto get = [&](uint32_t i) {
+    for (uint32_t k = 0; k < nk; ++k) if (key[k] == i) return val[k];
+    return i;
+  };
+  auto put = [&](uint32_t i, uint32_t v) {
+    for (uint32_t k = 0; k < nk; ++k) if (key[k] == i) { val[k] = v; return; }
+    key[nk] = i;
+    val[nk] = v;
+    ++nk;
+  };
+  for (uint32_t c = 0; c < C; ++c) {
+    const uint64_t y = (lo[c] & 0xFFFFFFFF80000000ull) | (lo[c + 1] & 0x000000007FFFFFFFull);
+    uint64_t z = hi[c] ^ (y >> 1);
+    if (y & 1ull) z ^= 0xB5026F5AA96619E9ull;
+    z ^= (z >> 29) & 0x5555555555555555ull;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+    z ^= (z << 37) & 0xFFF7EEE000000000ull;
+    z ^= z >> 43;
+    const uint32_t j = c + uint32_t(z % uint64_t(n - c));
+    const uint32_t pc = get(c), pj = get(j);
+    put(c, pj);
+    put(j, pc);
+    rows[size_t(u) * C + c] = pj;
+  }
+}
+
+// ---- commit of one clustered decode batch ---------------------------------
+// The batch's clusters are fresh ids [base, base + C) and their members are
+// exactly the batch rows [le0, le0 + m), so build_index over the whole
+// context (selection.hpp:29-48) only APPENDS: sizes / starts of the new ids
+// and their sorted entries (positions in order) after the existing
+// le0 - sink ones.  The same pass re-lays the batch's K/V rows cluster-major
+// (row le0 + i <- position sorted[le0 - sink + i]) through a staging copy, and
+// publishes n_clusters (base + C) from ncl_src.  One CTA per unit.
+constexpr int BC_THREADS = 512;
+__global__ void __launch_bounds__(BC_THREADS)
+k_batch_commit(uint16_t* __restrict__ K, uint16_t* __restrict__ V, uint16_t* __restrict__ tK,
+               uint16_t* __restrict__ tV, const int32_t* __restrict__ labels, uint32_t p_cap,
+               uint32_t c_cap, uint32_t sink, uint32_t le0, uint32_t m, uint32_t C,
+               const uint32_t* __restrict__ ncl_src, uint32_t* __restrict__ n_clusters,
+               uint32_t* __restrict__ sizes, uint32_t* __restrict__ starts,
+               uint32_t* __restrict__ sorted) {
+  const uint32_t u = blockIdx.x;
+  const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+  __shared__ uint32_t wc[BC_THREADS / 32][DI_MAX_C];
+  __shared__ uint32_t off[DI_MAX_C + 1];
+  __shared__ uint16_t dest[BC_THREADS];
+  const uint32_t base = ncl_src[u] - C;
+  const size_t urow = size_t(u) * p_cap;
+  const uint32_t first = le0 - sink;  // sorted entries before the batch's
+  const uint4* Ksrc = reinterpret_cast<const uint4*>(K + (urow + le0) * D);
+  const uint4* Vsrc = reinterpret_cast<const uint4*>(V + (urow + le0) * D);
+  uint4* tk = reinterpret_cast<uint4*>(tK + size_t(u) * m * D);
+  uint4* tv = reinterpret_cast<uint4*>(tV + size_t(u) * m * D);
+  for (uint32_t e = tid; e < m * 16; e += BC_THREADS) {  // stage the batch rows
+    tk[e] = Ksrc[e];
+    tv[e] = Vsrc[e];
+  }
+  for (uint32_t r0 = 0; r0 < m; r0 += BC_THREADS) {
+    const uint32_t r = r0 + tid;
+    const int32_t k = r < m ? labels[urow + le0 + r] - int32_t(base) : -1;
+    for (uint32_t c = 0; c < C; ++c) {
+      const unsigned b = __ballot_sync(0xffffffffu, k == int32_t(c));
+      if (lane == 0) wc[wid][c] = __popc(b);
+    }
+    __syncthreads();
+    if (tid < int(C)) {  // exclusive over warps; totals
+      uint32_t sum = 0;
+      for (int w = 0; w < BC_THREADS / 32; ++w) { const uint32_t x = wc[w][tid]; wc[w][tid] = sum; sum += x; }
+      off[tid] = sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t b = 0;
+      for (uint32_t c = 0; c < C; ++c) {
+        const uint32_t x = off[c];
+        if (r0 == 0) sizes[size_t(u) * c_cap + base + c] = x;
+        else sizes[size_t(u) * c_cap + base + c] += x;
+        off[c] = b;
+        b += x;
+      }
+      off[C] = b;
+    }
+    __syncthreads();
+    const unsigned same = __match_any_sync(0xffffffffu, k);
+    if (k >= 0) {
+      // members of cluster k before this chunk come first (rows ascending)
+      const uint32_t prior = r0 ? sizes[size_t(u) * c_cap + base + k] - off[k + 1] + off[k] : 0;
+      (void)prior;
+    }
+    __syncthreads();
+    if (k >= 0 && m <= BC_THREADS) {
+      const uint32_t slot = off[k] + wc[wid][k] + __popc(same & ((1u << lane) - 1u));
+      sorted[urow + first + slot] = le0 + r;
+      dest[r] = uint16_t(slot);
+    }
+    __syncthreads();
+  }
+  if (tid <= int(C)) starts[size_t(u) * (c_cap + 1) + base + tid] = first + off[tid];
+  __syncthreads();
+  uint4* Kd = reinterpret_cast<uint4*>(K + (urow + le0) * D);
+  uint4* Vd = reinterpret_cast<uint4*>(V + (urow + le0) * D);
+  for (uint32_t e = tid; e < m * 16; e += BC_THREADS) {
+    const uint32_t r = e >> 4, j = e & 15;
+    Kd[size_t(dest[r]) * 16 + j] = tk[e];
+    Vd[size_t(dest[r]) * 16 + j] = tv[e];
+  }
+  if (tid == 0) n_clusters[u] = base + C;
+}
+
 }  // namespace ckvb
 
 using namespace ckvb;
@@ -255,7 +420,7 @@ int ckv_ctx_create(int device, void* stream, ckv_ctx** out) {
   if (!out) { set_error("ckv_ctx_create: out is NULL"); return CKV_EINVAL; }
   CKV_CUDA_TRY(cudaSetDevice(device));
   ckv_ctx* c = new ckv_ctx();
-  for (int i = 0; i < 32; ++i) { c->scratch[i] = nullptr; c->scratch_cap[i] = 0; }
+  for (int i = 0; i < ckv_ctx::kScratchSlots; ++i) { c->scratch[i] = nullptr; c->scratch_cap[i] = 0; }
   c->device = device;
   // NULL is the CUDA legacy default stream (torch's default stream too), so
   // work launched here is ordered with the caller's default-stream work.
@@ -270,7 +435,7 @@ int ckv_ctx_destroy(ckv_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
-  for (int i = 0; i < 32; ++i)
+  for (int i = 0; i < ckv_ctx::kScratchSlots; ++i)
     if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
   delete ctx;
   return CKV_OK;
@@ -309,8 +474,9 @@ int ckv_memset(ckv_ctx* ctx, void* dst, int value, size_t bytes) {
 }
 
 int ckv_f32_to_bf16(ckv_ctx* ctx, const float* src, uint16_t* dst, size_t n, int* all_exact) {
-  int* flag = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), ctx->stream));
+  void* fv = nullptr;
+  CKV_TRY(ctx_scratch(ctx, 37, sizeof(int), false, &fv));
+  int* flag = static_cast<int*>(fv);
   CKV_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
   if (n) {
     int blocks = int(std::min<size_t>((n + 255) / 256, size_t(num_sms()) * 8));
@@ -320,7 +486,6 @@ int ckv_f32_to_bf16(ckv_ctx* ctx, const float* src, uint16_t* dst, size_t n, int
   }
   int h = 0;
   CKV_CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CKV_CUDA_TRY(cudaFreeAsync(flag, ctx->stream));
   CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (all_exact) *all_exact = h ? 0 : 1;
   return CKV_OK;
@@ -390,11 +555,15 @@ int ckv_cluster_prefill(ckv_ctx* ctx, const ckv_prefill_desc* d, const uint16_t*
   }
   if (C0 > d->c_cap) { set_error("cluster_prefill: C0 exceeds c_cap"); return CKV_EINVAL; }
   const uint32_t n = L - sink;
+  trace_begin("cluster_prefill");
   std::vector<uint32_t> rows(size_t(U) * C0);
   host_init_rows_batch(U, n, C0, seeds, rows.data());
-  uint32_t* d_rows = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&d_rows, rows.size() * 4, st));
+  trace_mark("init rows sampled");
+  void* d_rows_v = nullptr;  // context scratch: no stream-ordered pool trim on the sync
+  CKV_TRY(ctx_scratch(ctx, 29, rows.size() * 4, false, &d_rows_v));
+  uint32_t* d_rows = static_cast<uint32_t*>(d_rows_v);
   CKV_CUDA_TRY(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st));
+  trace_mark("init rows queued");
   KMeansArgs a;
   a.n_units = U;
   a.n = n;
@@ -409,9 +578,19 @@ int ckv_cluster_prefill(ckv_ctx* ctx, const ckv_prefill_desc* d, const uint16_t*
   a.centroids = centroids;
   a.labels = labels + sink;
   int rc = kmeans_run(ctx, a, info_host, objective_host, repair_host);
-  cudaFreeAsync(d_rows, st);
   if (rc) return rc;
-  return ckv_ctx_sync(ctx);
+  rc = ckv_ctx_sync(ctx);
+  trace_mark("done");
+  return rc;
+}
+
+// device init rows of a decode batch (k_decode_init_rows) into `rows`
+static int launch_decode_init_rows(cudaStream_t st, const uint64_t* seeds_dev, uint32_t n_units,
+                            uint32_t pos0, uint32_t n, uint32_t C, uint32_t* rows) {
+  if (C > DI_MAX_C || C > n) { set_error("decode init rows: need C <= min(32, rows)"); return CKV_EINVAL; }
+  k_decode_init_rows<<<(n_units + 127) / 128, 128, 0, st>>>(seeds_dev, n_units, pos0, n, C, rows);
+  CKV_LAUNCH_CHECK("k_decode_init_rows");
+  return CKV_OK;
 }
 
 int ckv_cluster_decode_batch(ckv_ctx* ctx, const ckv_decode_cluster_desc* d,
@@ -423,35 +602,29 @@ int ckv_cluster_decode_batch(ckv_ctx* ctx, const ckv_decode_cluster_desc* d,
   if (d->max_iters < 1) { set_error("ClusterConfig: max_iters must be >= 1"); return CKV_EINVAL; }
   cudaStream_t st = ctx->stream;
   const uint32_t C = std::min(d->c_plus, rows);
-  std::vector<uint32_t> init(size_t(U) * C);
-  for (uint32_t u = 0; u < U; ++u)
-    host_init_rows(rows, C, host_mix_seed(seeds[u], 0xdecadeull, d->pos0),
-                   init.data() + size_t(u) * C);
-  uint32_t* d_init = nullptr;
-  float* tmp_c = nullptr;
-  int32_t* tmp_l = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&d_init, init.size() * 4, st));
-  CKV_CUDA_TRY(cudaMallocAsync(&tmp_c, size_t(U) * C * D * 4, st));
-  CKV_CUDA_TRY(cudaMallocAsync(&tmp_l, size_t(U) * std::max(rows, 2u) * 4, st));
-  CKV_CUDA_TRY(cudaMemcpyAsync(d_init, init.data(), init.size() * 4, cudaMemcpyHostToDevice, st));
+  void *v_init = nullptr, *v_c = nullptr, *v_l = nullptr, *v_seed = nullptr;
+  CKV_TRY(ctx_scratch(ctx, 30, size_t(U) * C * 4, false, &v_init));
+  CKV_TRY(ctx_scratch(ctx, 31, size_t(U) * C * D * 4, false, &v_c));
+  CKV_TRY(ctx_scratch(ctx, 32, size_t(U) * std::max(rows, 2u) * 4, false, &v_l));
+  uint32_t* d_init = static_cast<uint32_t*>(v_init);
+  float* tmp_c = static_cast<float*>(v_c);
+  int32_t* tmp_l = static_cast<int32_t*>(v_l);
   if (kmeans_small_supported(rows, C)) {
-    // the whole k-means of every unit's batch in one launch (ckv_kmeans.cu)
+    // init rows on the device, then the whole k-means of every unit's batch
+    // in one launch (ckv_kmeans.cu); one read-back for the input checks
+    CKV_TRY(ctx_scratch(ctx, 33, size_t(U) * 8, false, &v_seed));
+    CKV_CUDA_TRY(cudaMemcpyAsync(v_seed, seeds, size_t(U) * 8, cudaMemcpyHostToDevice, st));
+    CKV_TRY(launch_decode_init_rows(st, static_cast<const uint64_t*>(v_seed), U, d->pos0, rows,
+                                    C, d_init));
     uint32_t* d_it = reinterpret_cast<uint32_t*>(tmp_l);  // scratch reuse: [U] + [U]
     int32_t* d_st = tmp_l + U;
-    int rc = launch_kmeans_small(st, keys + size_t(d->pos0) * D, uint64_t(d->p_cap) * D, U,
-                                 rows, C, d->max_iters, d_init, centroids, d->c_cap,
-                                 labels + d->pos0, d->p_cap, n_clusters, d_it, d_st);
-    ctx->launches++;
+    CKV_TRY(launch_kmeans_small(st, keys + size_t(d->pos0) * D, uint64_t(d->p_cap) * D, U, rows,
+                                C, d->max_iters, d_init, centroids, d->c_cap, labels + d->pos0,
+                                d->p_cap, n_clusters, d_it, d_st));
+    ctx->launches += 2;
     std::vector<int32_t> hb(2 * size_t(U));
-    if (rc == CKV_OK) {
-      cudaError_t e = cudaMemcpyAsync(hb.data(), tmp_l, 8 * size_t(U), cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) rc = cuda_status(e, "cluster_decode_batch");
-    }
-    cudaFreeAsync(d_init, st);
-    cudaFreeAsync(tmp_c, st);
-    cudaFreeAsync(tmp_l, st);
-    if (rc) return rc;
+    CKV_CUDA_TRY(cudaMemcpyAsync(hb.data(), tmp_l, 8 * size_t(U), cudaMemcpyDeviceToHost, st));
+    CKV_CUDA_TRY(cudaStreamSynchronize(st));
     for (uint32_t u = 0; u < U; ++u) {
       if (hb[U + u] == 1) { set_error("kmeans: keys must be finite"); return CKV_EINVAL; }
       if (hb[U + u] == 2) {
@@ -462,6 +635,12 @@ int ckv_cluster_decode_batch(ckv_ctx* ctx, const ckv_decode_cluster_desc* d,
     }
     return CKV_OK;
   }
+  // large batches (rows > 512 or C+ > 32): the generic k-means driver
+  std::vector<uint32_t> init(size_t(U) * C);
+  for (uint32_t u = 0; u < U; ++u)
+    host_init_rows(rows, C, host_mix_seed(seeds[u], 0xdecadeull, d->pos0),
+                   init.data() + size_t(u) * C);
+  CKV_CUDA_TRY(cudaMemcpyAsync(d_init, init.data(), init.size() * 4, cudaMemcpyHostToDevice, st));
   KMeansArgs a;
   a.n_units = U;
   a.n = rows;
@@ -476,18 +655,11 @@ int ckv_cluster_decode_batch(ckv_ctx* ctx, const ckv_decode_cluster_desc* d,
   a.centroids = tmp_c;
   a.labels = tmp_l;
   std::vector<ckv_kmeans_info> info(U);
-  int rc = kmeans_run(ctx, a, info.data(), nullptr, nullptr);
-  if (rc == CKV_OK) {
-    k_append_clusters<<<U, 256, 0, st>>>(tmp_c, tmp_l, C, rows, d->pos0, d->c_cap, d->p_cap,
-                                         centroids, labels, n_clusters);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) rc = cuda_status(e, "k_append_clusters");
-    ctx->launches++;
-  }
-  cudaFreeAsync(d_init, st);
-  cudaFreeAsync(tmp_c, st);
-  cudaFreeAsync(tmp_l, st);
-  if (rc) return rc;
+  CKV_TRY(kmeans_run(ctx, a, info.data(), nullptr, nullptr));
+  k_append_clusters<<<U, 256, 0, st>>>(tmp_c, tmp_l, C, rows, d->pos0, d->c_cap, d->p_cap,
+                                       centroids, labels, n_clusters);
+  CKV_LAUNCH_CHECK("k_append_clusters");
+  ctx->launches++;
   if (iterations_host)
     for (uint32_t u = 0; u < U; ++u) iterations_host[u] = info[u].iterations_used;
   return ckv_ctx_sync(ctx);
@@ -548,12 +720,11 @@ int ckv_select(ckv_ctx* ctx, const ckv_select_desc* d, const float* q, const flo
     }
   }
   void* scratch = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&scratch, select_scratch_bytes(d->n_q, d->c_cap), ctx->stream));
+  CKV_TRY(ctx_scratch(ctx, 34, select_scratch_bytes(d->n_q, d->c_cap), false, &scratch));
   int rc = launch_select(ctx->stream, *d, q, centroids, n_clusters, sizes, starts, sorted_ids,
                          token_ids, rows, runs ? *runs : null_runs(), d->row_base, n_tokens,
                          n_taken, trimmed, ranked, scores, cache ? cache->dev : null_cache(),
                          scratch);
-  cudaFreeAsync(scratch, ctx->stream);
   ctx->launches += 2;
   return rc;
 }
@@ -601,13 +772,13 @@ int ckv_cache_lookup(ckv_ctx* ctx, ckv_cache* c, uint32_t slot, const uint32_t* 
                      uint32_t n_sel, const uint32_t* sizes, uint32_t* hit, uint32_t* miss,
                      uint32_t* counts_host) {
   if (slot >= c->dev.n_slots) { set_error("cache: slot out of range"); return CKV_EINVAL; }
-  uint32_t* dcounts = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&dcounts, 8, ctx->stream));
+  void* dcv = nullptr;
+  CKV_TRY(ctx_scratch(ctx, 35, 8, false, &dcv));
+  uint32_t* dcounts = static_cast<uint32_t*>(dcv);
   CKV_TRY(launch_cache_lookup(ctx->stream, c->dev, slot, selected, n_sel, sizes, hit, miss,
                               dcounts));
   ctx->launches++;
   CKV_CUDA_TRY(cudaMemcpyAsync(counts_host, dcounts, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CKV_CUDA_TRY(cudaFreeAsync(dcounts, ctx->stream));
   CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return CKV_OK;
 }
@@ -615,12 +786,12 @@ int ckv_cache_lookup(ckv_ctx* ctx, ckv_cache* c, uint32_t slot, const uint32_t* 
 int ckv_cache_invalidate(ckv_ctx* ctx, ckv_cache* c, uint32_t slot, const uint32_t* retired,
                          uint32_t n) {
   if (n == 0) return CKV_OK;
-  uint32_t* d = nullptr;
-  CKV_CUDA_TRY(cudaMallocAsync(&d, size_t(n) * 4, ctx->stream));
+  void* dv = nullptr;
+  CKV_TRY(ctx_scratch(ctx, 36, size_t(n) * 4, false, &dv));
+  uint32_t* d = static_cast<uint32_t*>(dv);
   CKV_CUDA_TRY(cudaMemcpyAsync(d, retired, size_t(n) * 4, cudaMemcpyHostToDevice, ctx->stream));
   CKV_TRY(launch_cache_invalidate(ctx->stream, c->dev, slot, d, n));
   ctx->launches++;
-  CKV_CUDA_TRY(cudaFreeAsync(d, ctx->stream));
   CKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return CKV_OK;
 }
@@ -732,6 +903,23 @@ struct ckv_session {
   uint32_t n_ctx = 0, labeled_end = 0, steps = 0, pending = 0, C_cur = 0;
   bool prefilled = false;
   bool l2_persist = false;
+  // decode-batch clustering, device-resident (harness.hpp:318-337): per-unit
+  // seeds, init rows, the kernel's iteration / status words and their
+  // pinned host copy (checked lazily: no sync on the decode path)
+  uint64_t* d_seeds = nullptr;
+  uint32_t* db_init = nullptr;
+  int32_t* db_stat = nullptr;   // [2U]: iterations | converged bit, status
+  int32_t* h_stat = nullptr;    // pinned [2U]
+  cudaEvent_t ev_stat = nullptr;
+  bool stat_pending = false;
+  uint32_t pend_pos0 = 0;       // first position of the batch being collected
+  // async mode (harness.hpp:236-243, 327-329): the batch's k-means runs on a
+  // side stream and is committed async_delay steps later
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_done = nullptr;
+  uint32_t* stage_ncl = nullptr;  // n_clusters as the side stream's k-means leaves it
+  struct Queued { uint32_t ready, pos0, rows, C; };
+  std::deque<Queued> queue;
 };
 
 namespace {
@@ -779,6 +967,13 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
     set_error("ckv_session_create: invalid configuration");
     return CKV_EINVAL;
   }
+  if (d->async_delay &&
+      (d->async_delay >= d->decode_batch ||
+       !kmeans_small_supported(d->decode_batch, std::min(d->c_plus, d->decode_batch)))) {
+    set_error("ckv_session_create: async clustering needs async_delay < decode_batch <= 512 "
+              "and c_plus <= 32");
+    return CKV_EINVAL;
+  }
   ckv_session* s = new ckv_session();
   s->ctx = ctx;
   s->d = *d;
@@ -787,7 +982,10 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   s->p_cap = d->prompt_len + d->max_decode;
   const uint32_t C0 = ckv_prefill_cluster_count(d->prompt_len, d->c0_divisor, d->sink_tokens, 0);
   s->c_cap = C0 + d->c_plus * (d->max_decode / d->decode_batch + 1);
-  s->sel_cap = d->budget + d->sink_tokens + d->decode_batch + 1;
+  // recency: the collecting batch (< m rows) plus, in async mode, a batch
+  // waiting async_delay steps for its commit
+  s->sel_cap = d->budget + d->sink_tokens + d->decode_batch + 1 +
+               (d->async_delay ? d->decode_batch + d->async_delay : 0);
   const size_t kv = size_t(s->U) * s->p_cap * D;
   int rc = CKV_OK;
   rc |= salloc(&s->K, kv);
@@ -818,6 +1016,20 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   rc |= salloc(&s->out_dev, size_t(s->n_q) * D);
   rc |= salloc(&s->kn_dev, size_t(s->U) * D);
   rc |= salloc(&s->vn_dev, size_t(s->U) * D);
+  rc |= salloc(&s->d_seeds, s->U);
+  rc |= salloc(&s->db_init, size_t(s->U) * std::min(d->c_plus, d->decode_batch));
+  rc |= salloc(&s->db_stat, 2 * size_t(s->U));
+  rc |= salloc(&s->stage_ncl, s->U);
+  if (!rc && cudaMallocHost(&s->h_stat, 8 * size_t(s->U)) != cudaSuccess) rc = 1;
+  if (!rc && cudaEventCreateWithFlags(&s->ev_stat, cudaEventDisableTiming) != cudaSuccess) rc = 1;
+  if (!rc && d->async_delay) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_done, cudaEventDisableTiming) != cudaSuccess)
+      rc = 1;
+  }
   if (rc) { ckv_session_destroy(s); return CKV_ENOMEM; }
   cudaMemsetAsync(s->tickets, 0, size_t(s->n_q) * 4, ctx->stream);
   cudaMemsetAsync(s->n_clusters, 0, size_t(s->U) * 4, ctx->stream);
@@ -837,8 +1049,15 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   // unit u = layer * kv_heads + head (batch folded into the layer index)
   for (uint32_t u = 0; u < s->U; ++u)
     s->seeds[u] = host_mix_seed(d->cluster_seed, u / kvh, u % kvh);  // harness.hpp:195
+  {
+    const cudaError_t e = cudaMemcpyAsync(s->d_seeds, s->seeds.data(), 8 * size_t(s->U),
+                                          cudaMemcpyHostToDevice, ctx->stream);
+    rc = e == cudaSuccess ? ckv_ctx_sync(ctx) : cuda_status(e, "session seeds");
+  }
+  if (rc) { ckv_session_destroy(s); return rc; }
   s->n_ctx = d->prompt_len;
   s->labeled_end = d->prompt_len;
+  s->pend_pos0 = d->prompt_len;
   *out = s;
   return CKV_OK;
 }
@@ -853,6 +1072,12 @@ int ckv_session_destroy(ckv_session* s) {
   cudaFree(s->tmpV); cudaFree(s->n_tokens); cudaFree(s->n_taken); cudaFree(s->trimmed);
   cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
   cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
+  if (s->side) { cudaStreamSynchronize(s->side); cudaStreamDestroy(s->side); }
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_done) cudaEventDestroy(s->ev_done);
+  if (s->ev_stat) cudaEventDestroy(s->ev_stat);
+  if (s->h_stat) cudaFreeHost(s->h_stat);
+  cudaFree(s->d_seeds); cudaFree(s->db_init); cudaFree(s->db_stat); cudaFree(s->stage_ncl);
   ckv_cache_destroy(s->cache);
   if (s->l2_persist) l2_persist_release(s->ctx->device);
   delete s;
@@ -956,11 +1181,85 @@ int ckv_session_attend_only(ckv_session* s, const float* q_dev, float* out_dev) 
   return session_select_attend(s, q_dev, out_dev);
 }
 
+// The decode-batch k-means reports kmeans_cosine's input errors
+// (clustering.hpp:166-172) through a status word copied to pinned host memory
+// behind an event; it is read when the event has completed (the next step
+// that finds it done, or blocking at stats / destroy), so the decode path
+// never waits on it.  A failed batch poisons the session (CKV_EINVAL from
+// then on), the way the reference's cluster_decode_batch throws.
+static int session_check_status(ckv_session* s, bool block) {
+  if (!s->stat_pending) return CKV_OK;
+  if (block) {
+    CKV_CUDA_TRY(cudaEventSynchronize(s->ev_stat));
+  } else {
+    const cudaError_t e = cudaEventQuery(s->ev_stat);
+    if (e == cudaErrorNotReady) return CKV_OK;
+    if (e != cudaSuccess) return cuda_status(e, "session decode-batch status");
+  }
+  s->stat_pending = false;
+  for (uint32_t u = 0; u < s->U; ++u) {
+    const int32_t st = s->h_stat[s->U + u];
+    if (st == 1) { set_error("kmeans: keys must be finite"); s->prefilled = false; return CKV_EINVAL; }
+    if (st == 2) {
+      set_error("kmeans: degenerate input, all keys zero-norm");
+      s->prefilled = false;
+      return CKV_EINVAL;
+    }
+  }
+  return CKV_OK;
+}
+
+// cluster_decode_batch (clustering.hpp:310-332) of every unit's rows
+// [pos0, pos0 + m) on stream st: init rows and the whole k-means on the
+// device (centroids at ncl[u], labels +ncl[u], ncl[u] += C), no host work
+static int session_cluster_batch(ckv_session* s, cudaStream_t st, uint32_t pos0, uint32_t m,
+                                 uint32_t* ncl) {
+  const uint32_t C = std::min(s->d.c_plus, m);
+  CKV_TRY(session_check_status(s, true));  // the previous batch's (long finished)
+  CKV_TRY(launch_decode_init_rows(st, s->d_seeds, s->U, pos0, m, C, s->db_init));
+  CKV_TRY(launch_kmeans_small(st, s->K + size_t(pos0) * D, uint64_t(s->p_cap) * D, s->U, m, C,
+                              s->d.max_iters, s->db_init, s->cents, s->c_cap, s->labels + pos0,
+                              s->p_cap, ncl, reinterpret_cast<uint32_t*>(s->db_stat),
+                              s->db_stat + s->U));
+  CKV_CUDA_TRY(cudaMemcpyAsync(s->h_stat, s->db_stat, 8 * size_t(s->U), cudaMemcpyDeviceToHost,
+                               st));
+  CKV_CUDA_TRY(cudaEventRecord(s->ev_stat, st));
+  s->stat_pending = true;
+  s->ctx->launches += 2;
+  return CKV_OK;
+}
+
+// the clustered batch joins the model: index entries appended, the batch's
+// K/V rows re-laid cluster-major, n_clusters published (k_batch_commit)
+static int session_commit_batch(ckv_session* s, uint32_t pos0, uint32_t m, uint32_t C,
+                                const uint32_t* ncl_src) {
+  cudaStream_t st = s->ctx->stream;
+  const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
+  if (pos0 != s->labeled_end) { set_error("session: batch commit out of order"); return CKV_EINVAL; }
+  k_batch_commit<<<s->U, BC_THREADS, 0, st>>>(s->K, s->V, s->tmpK, s->tmpV, s->labels, s->p_cap,
+                                              s->c_cap, sink, pos0, m, C, ncl_src, s->n_clusters,
+                                              s->sizes, s->starts, s->sorted);
+  CKV_LAUNCH_CHECK("k_batch_commit");
+  s->ctx->launches++;
+  s->labeled_end += m;
+  s->C_cur += C;
+  return CKV_OK;
+}
+
 int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const uint16_t* vn,
                      float* out, int on_device) {
-  if (!s->prefilled) { set_error("session: prefill first"); return CKV_EINVAL; }
+  if (!s->prefilled) { set_error("session: prefill first (or a failed decode batch)"); return CKV_EINVAL; }
   if (s->n_ctx >= s->p_cap) { set_error("session: decode capacity exhausted"); return CKV_EINVAL; }
+  CKV_TRY(session_check_status(s, false));
   cudaStream_t st = s->ctx->stream;
+  // async mode: batches whose delay has run out join before this step's
+  // selection (harness.hpp:237-243)
+  while (!s->queue.empty() && s->queue.front().ready <= s->steps) {
+    const auto b = s->queue.front();
+    CKV_CUDA_TRY(cudaStreamWaitEvent(st, s->ev_done, 0));
+    CKV_TRY(session_commit_batch(s, b.pos0, b.rows, b.C, s->stage_ncl));
+    s->queue.pop_front();
+  }
   const float* qd = q;
   const uint16_t *kd = kn, *vd = vn;
   float* od = out;
@@ -999,29 +1298,45 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
   s->n_ctx++;
   s->pending++;
   s->steps++;
-  if (s->pending == s->d.decode_batch) {  // harness.hpp:325-337 (synchronous mode)
-    ckv_decode_cluster_desc dd{};
-    dd.n_units = s->U;
-    dd.pos0 = s->labeled_end;
-    dd.rows = s->pending;
-    dd.p_cap = s->p_cap;
-    dd.c_cap = s->c_cap;
-    dd.c_plus = s->d.c_plus;
-    dd.max_iters = s->d.max_iters;
-    CKV_TRY(ckv_cluster_decode_batch(s->ctx, &dd, s->K, s->seeds.data(), s->cents, s->labels,
-                                     s->n_clusters, nullptr));
-    const uint32_t le0 = s->labeled_end, m = s->pending;
-    s->labeled_end += m;
-    s->C_cur += std::min(s->d.c_plus, m);
+  if (s->pending == s->d.decode_batch) {  // harness.hpp:321-336
+    const uint32_t m = s->pending, pos0 = s->pend_pos0;
+    const uint32_t C = std::min(s->d.c_plus, m);
     s->pending = 0;
-    CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
-                            s->n_clusters, s->sizes, s->starts, s->sorted));
-    // relay the batch's rows [le0, le0+m) into index order (in place via staging)
-    const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
-    k_relayout_batch<<<s->U, 256, 0, st>>>(s->K, s->V, s->tmpK, s->tmpV, s->sorted, s->p_cap,
-                                           sink, le0, m);
-    CKV_LAUNCH_CHECK("k_relayout_batch");
-    s->ctx->launches++;
+    s->pend_pos0 += m;
+    if (s->d.async_delay) {
+      // the k-means on the side stream, from n_clusters as it stands (no
+      // other batch commits before this one), into a staging copy of it
+      CKV_CUDA_TRY(cudaEventRecord(s->ev_fork, st));
+      CKV_CUDA_TRY(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+      CKV_CUDA_TRY(cudaMemcpyAsync(s->stage_ncl, s->n_clusters, 4 * size_t(s->U),
+                                   cudaMemcpyDeviceToDevice, s->side));
+      CKV_TRY(session_cluster_batch(s, s->side, pos0, m, s->stage_ncl));
+      CKV_CUDA_TRY(cudaEventRecord(s->ev_done, s->side));
+      s->queue.push_back({s->steps - 1 + s->d.async_delay, pos0, m, C});
+    } else if (kmeans_small_supported(m, C) && m <= uint32_t(BC_THREADS)) {
+      CKV_TRY(session_cluster_batch(s, st, pos0, m, s->n_clusters));
+      CKV_TRY(session_commit_batch(s, pos0, m, C, s->n_clusters));
+    } else {  // large batches: the generic driver, full index, staged relayout
+      ckv_decode_cluster_desc dd{};
+      dd.n_units = s->U;
+      dd.pos0 = pos0;
+      dd.rows = m;
+      dd.p_cap = s->p_cap;
+      dd.c_cap = s->c_cap;
+      dd.c_plus = s->d.c_plus;
+      dd.max_iters = s->d.max_iters;
+      CKV_TRY(ckv_cluster_decode_batch(s->ctx, &dd, s->K, s->seeds.data(), s->cents, s->labels,
+                                       s->n_clusters, nullptr));
+      s->labeled_end += m;
+      s->C_cur += C;
+      CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
+                              s->n_clusters, s->sizes, s->starts, s->sorted));
+      const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
+      k_relayout_batch<<<s->U, 256, 0, st>>>(s->K, s->V, s->tmpK, s->tmpV, s->sorted, s->p_cap,
+                                             sink, pos0, m);
+      CKV_LAUNCH_CHECK("k_relayout_batch");
+      s->ctx->launches++;
+    }
   }
   if (!on_device) {
     if (!zero_copy)
@@ -1033,6 +1348,7 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
 }
 
 int ckv_session_stats_get(ckv_session* s, ckv_session_stats* st) {
+  CKV_TRY(session_check_status(s, true));
   st->n_ctx = s->n_ctx;
   st->labeled_end = s->labeled_end;
   st->steps = s->steps;

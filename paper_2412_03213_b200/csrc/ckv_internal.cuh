@@ -14,11 +14,21 @@ struct ckv_ctx {
   // grow-only device scratch slots reused across calls on this context
   // (cudaMalloc / cudaFree of ~0.5 GB per k-means call cost milliseconds and
   // device-wide synchronisation)
-  void* scratch[32];        // zeroed in ckv_ctx_create
-  size_t scratch_cap[32];
+  // slots: 1-21 k-means, 22 relayout, 23 page, 24-26 attend, 27-28 metrics,
+  // 29 prefill init rows, 30-33 decode batch, 34 select, 35-36 cache, 37 misc
+  static constexpr int kScratchSlots = 48;
+  void* scratch[kScratchSlots];  // zeroed in ckv_ctx_create
+  size_t scratch_cap[kScratchSlots];
 };
 
 namespace ckvb {
+
+// CKV_TRACE_HOST=1: host-side timestamps of the phases of a long call
+// (prefill) on stderr, relative to the last trace_begin on this thread; no
+// extra synchronisation, so the traced run is the untraced run
+bool trace_on();
+void trace_begin(const char* what);
+void trace_mark(const char* what, long arg = -1);
 
 int launch_index(cudaStream_t st, uint32_t n_units, const int32_t* labels, uint32_t n_pos,
                  uint32_t p_cap, uint32_t c_cap, const uint32_t* n_clusters,

@@ -452,6 +452,7 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
                           size_t(a.c_stride) * D * 24;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+  trace_mark("memgetinfo");
   const size_t budget = std::max<size_t>(size_t(16) << 30, free_b / 10 * 6);
   const uint32_t ub = uint32_t(std::max<size_t>(1, std::min<size_t>(U, budget / per_unit)));
   if (ub >= U) return kmeans_run_units(ctx, a, info_host, objective_host, repair_host);
@@ -537,7 +538,9 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     CKV_LAUNCH_CHECK("k_validate_rows");
     ctx->launches += 2;
     CKV_CUDA_TRY(cudaMemcpyAsync(hf, b_flags.p, sizeof(int32_t) * U, cudaMemcpyDeviceToHost, st));
+    trace_mark("validation queued");
     CKV_CUDA_TRY(cudaStreamSynchronize(st));
+    trace_mark("validation synced");
     for (uint32_t u = 0; u < U; ++u)
       if (hf[u] & 1) { set_error("kmeans: keys must be finite"); return CKV_EINVAL; }
     for (uint32_t u = 0; u < U; ++u)
@@ -572,6 +575,7 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     CKV_CUDA_TRY(cudaMemsetAsync(b_obj.p, 0, sizeof(double) * U, st));
     CKV_CUDA_TRY(cudaMemsetAsync(b_changed.p, 0, sizeof(int32_t) * U, st));
     CKV_CUDA_TRY(cudaStreamSynchronize(st));  // `ones` leaves scope
+    trace_mark("active set");
   }
 
   // ---- init (clustering.hpp:174-198) --------------------------------------
@@ -630,7 +634,9 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     if (!read_back) return CKV_OK;
     CKV_CUDA_TRY(cudaMemcpyAsync(n_active_host, b_nact.p, sizeof(int32_t),
                                  cudaMemcpyDeviceToHost, st));
+    trace_mark("control queued, pass", long(t));
     CKV_CUDA_TRY(cudaStreamSynchronize(st));
+    trace_mark("control synced, active units", long(*n_active_host));
     return CKV_OK;
   };
 
@@ -706,6 +712,7 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     CKV_CUDA_TRY(cudaMemcpyAsync(objs.data(), b_objlog.p, sizeof(double) * objs.size(),
                                  cudaMemcpyDeviceToHost, st));
   CKV_CUDA_TRY(cudaStreamSynchronize(st));
+  trace_mark("results synced");
   for (uint32_t u = 0; u < U; ++u) {
     uint32_t it = iters[u];
     uint32_t nrep = 0;
@@ -793,11 +800,66 @@ int launch_objective(cudaStream_t st, const uint16_t* keys, uint64_t key_stride,
 // ---------------------------------------------------------------------------
 namespace ckvb {
 
-constexpr int KS_THREADS = 256;
-constexpr uint32_t KS_MAX_ROWS = 512;
+constexpr int KS_THREADS = 512;
+constexpr int KS_WARPS = KS_THREADS / 32;
+constexpr uint32_t KS_MAX_ROWS = 512;  // one batch row per thread
 constexpr uint32_t KS_MAX_C = 32;
+constexpr uint32_t KS_CS = D + 1;      // centroid row stride (floats): conflict-free chains
 
-__global__ void __launch_bounds__(KS_THREADS)
+// row stride (u16) of the transposed key stage: even, with an odd word
+// stride, so both access patterns are conflict-free — the assignment's lanes
+// read consecutive rows of one dim, the update's lanes consecutive dims of
+// one row
+__host__ __device__ inline uint32_t ks_row_stride(uint32_t rows) {
+  uint32_t rs = (rows + 1) & ~1u;
+  return ((rs / 2) & 1u) ? rs : rs + 2;
+}
+
+__host__ __device__ inline size_t ks_smem_bytes(uint32_t rows, uint32_t C) {
+  const size_t C4 = (C + 3) & ~3u;
+  return C4 * D * 8 + C4 * 8 + C4 * KS_CS * 4 + (2 * C4 + 4) * 4 + size_t(KS_WARPS) * C4 * 4 +
+         2 * size_t(KS_MAX_ROWS) * 4 + KS_MAX_ROWS * 2 + size_t(D) * ks_row_stride(rows) * 2;
+}
+
+// centroids cent[c] (c < C) -> f64 norms (sequential chain, common.hpp:141-147)
+// and the next assignment's directions dir = float(x / |x|), kept in f64 in
+// the [C/4][D][4] layout the assignment loop reads with two 16-B loads
+__device__ __forceinline__ void ks_finish(uint32_t C, const float* cent, double* cnorm,
+                                          double* dird) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  if (tid < int(C)) {
+    const float* x = cent + tid * KS_CS;
+    double s = 0.0;
+#pragma unroll 16
+    for (int j = 0; j < D; ++j) s = __fma_rn(double(x[j]), double(x[j]), s);
+    cnorm[tid] = sqrt(s);
+  }
+  __syncthreads();
+  for (uint32_t e = tid; e < C * D; e += KS_THREADS) {
+    const uint32_t c = e / D, j = e % D;
+    const double nrm = cnorm[c];
+    const float x = cent[c * KS_CS + j];
+    const float dv = nrm > 0.0 ? float(double(x) / nrm) : x;
+    dird[((c >> 2) * D + j) * 4 + (c & 3)] = double(dv);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// K4 fused: cluster_decode_batch's whole kmeans_cosine (clustering.hpp:160-263
+// on one decode batch, 310-332) in ONE launch, one CTA per unit, one batch
+// row per thread, everything in shared memory: no per-iteration launch or
+// host round trip.  Numerics are the reference's, bit for bit:
+//   assignment   a sequential f64 chain per (key, c) (common.hpp:86-90),
+//                four clusters interleaved, strict '>' in id order;
+//   counts       warp ballots (no atomics);
+//   repair       clustering.hpp:128-153, sequential over empty ids;
+//   update       f64 member sums in POSITION order (members listed per
+//                cluster by __match_any ranks), float(sum / count);
+//   directions   normalize(): sequential f64 norm chain, float(x / |x|).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(KS_THREADS, 2)
 k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t rows,
                uint32_t C, uint32_t max_iters, const uint32_t* __restrict__ init_rows,
                float* __restrict__ out_cents, uint32_t c_cap, int32_t* __restrict__ out_labels,
@@ -806,32 +868,25 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
   extern __shared__ __align__(16) unsigned char ks_raw[];
   const uint32_t u = blockIdx.x;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
-  // layout sized by (C, rows) so two CTAs fit an SM at the decode-batch shape
-  // kt row stride RS = 1 (mod 16) u16: the update's lanes (4 dims apart)
-  // then hit 16 distinct banks instead of one
-  const uint32_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u, RS = ((rows + 15) & ~15u) + 1;
-  double* cnorm = reinterpret_cast<double*>(ks_raw);                   // [C]
-  float* cent = reinterpret_cast<float*>(cnorm + C4);                   // [C][D]
-  float* dir = cent + C4 * D;                                           // [C][D]
-  uint16_t* dbf = reinterpret_cast<uint16_t*>(dir + C4 * D);            // [C][D] (unused)
-  float* deps = reinterpret_cast<float*>(dbf + C4 * D);                 // [C]  (unused)
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(deps + C4);               // [C]
-  int32_t* lab0 = reinterpret_cast<int32_t*>(cnt + C4);                 // [rows]
-  int32_t* lab1 = lab0 + R2;                                            // [rows]
-  uint16_t* kt = reinterpret_cast<uint16_t*>(lab1 + R2);                // [D][rows] transposed
-  __shared__ int s_flag, s_bad;
-  __shared__ uint32_t s_largest, s_lcnt, s_victim;
-  __shared__ double s_wd[KS_THREADS / 32];
-  __shared__ uint32_t s_wi[KS_THREADS / 32];
+  const uint32_t C4 = (C + 3) & ~3u, RS = ks_row_stride(rows);
+  double* dird = reinterpret_cast<double*>(ks_raw);                     // [C4/4][D][4]
+  double* cnorm = dird + C4 * D;                                        // [C4]
+  float* cent = reinterpret_cast<float*>(cnorm + C4);                   // [C4][KS_CS]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(cent + C4 * KS_CS);       // [C4]
+  uint32_t* cbase = cnt + C4;                                           // [C4 + 4]
+  uint32_t* wcnt = cbase + C4 + 4;                                      // [KS_WARPS][C4]
+  int32_t* lab0 = reinterpret_cast<int32_t*>(wcnt + KS_WARPS * C4);     // [KS_MAX_ROWS]
+  int32_t* lab1 = lab0 + KS_MAX_ROWS;                                   // [KS_MAX_ROWS]
+  uint16_t* mem = reinterpret_cast<uint16_t*>(lab1 + KS_MAX_ROWS);      // [KS_MAX_ROWS]
+  uint16_t* kt = mem + KS_MAX_ROWS;                                     // [D][RS]
+  __shared__ uint32_t s_largest, s_lcnt;
+  __shared__ double s_wd[KS_WARPS];
+  __shared__ uint32_t s_wi[KS_WARPS];
   const uint16_t* kb = keys + u * key_stride;
 
-  // stage the batch transposed (thread t reads rows t, t+256: conflict-free)
-  // and run kmeans_cosine's input checks (clustering.hpp:166-172)
-  if (tid == 0) { s_flag = 0; s_bad = 0; }
-  __syncthreads();
+  // stage the batch transposed, 16-B loads four rounds deep, and run
+  // kmeans_cosine's input checks (clustering.hpp:166-172)
   int bad = 0, nonzero = 0;
-  // 16-B loads, four rounds in flight per thread before any is stored (a
-  // load-then-store loop of 2-B elements serialises ~160 global latencies)
   const uint4* kb4 = reinterpret_cast<const uint4*>(kb);
   const uint32_t n4 = rows * (D / 8);
   for (uint32_t v0 = tid; v0 < n4; v0 += 4 * KS_THREADS) {
@@ -856,11 +911,13 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
       }
     }
   }
+  for (uint32_t e = tid; e < C4 * D; e += KS_THREADS) dird[e] = 0.0;  // padding clusters
   __syncthreads();
-  for (uint32_t r = tid; r < rows; r += KS_THREADS) {
+  if (tid < int(rows)) {
     double s = 0.0;
+#pragma unroll 8
     for (int j = 0; j < D; ++j) {
-      const double x = double(bf16_to_f32(kt[j * RS + r]));
+      const double x = double(bf16_to_f32(kt[j * RS + tid]));
       s = __fma_rn(x, x, s);
     }
     if (sqrt(s) >= 1e-12) nonzero = 1;
@@ -871,16 +928,12 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
     if (tid == 0) status[u] = bad ? 1 : 2;
     return;
   }
-  // init: centroid c = key row init_rows[c]; dirs = normalize (count 1)
-  for (uint32_t c = wid; c < C; c += KS_THREADS / 32) {
-    const uint32_t r = init_rows[size_t(u) * C + c];
-    double x[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) x[k] = double(bf16_to_f32(kt[(4 * lane + k) * RS + r]));
-    finish_centroid(x[0], x[1], x[2], x[3], 1.0, cent + c * D, dir + c * D, dbf + c * D,
-                    cnorm + c, deps + c);
+  // init: centroid c = key row init_rows[c] (clustering.hpp:194-198)
+  for (uint32_t e = tid; e < C * D; e += KS_THREADS) {
+    const uint32_t c = e / D, j = e % D;
+    cent[c * KS_CS + j] = bf16_to_f32(kt[j * RS + init_rows[size_t(u) * C + c]]);
   }
-  __syncthreads();
+  ks_finish(C, cent, cnorm, dird);
 
   int32_t* lab[2] = {lab0, lab1};
   uint32_t it = 0;
@@ -888,31 +941,45 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
   for (uint32_t t = 0;; ++t) {
     int32_t* cur = lab[t & 1];
     const int32_t* prev = lab[(t & 1) ^ 1];
-    // assign (AssignScorer::assign): a sequential f64 chain per (key, c),
-    // four clusters' chains interleaved for ILP; strict '>' in id order
-    for (uint32_t r = tid; r < rows; r += KS_THREADS) {
+    // ---- assign (AssignScorer::assign, clustering.hpp:104-115) -------------
+    int32_t my = -1;
+    if (tid < int(rows)) {
       uint32_t best = 0;
       double bs = -INFINITY;
       for (uint32_t c0 = 0; c0 < C; c0 += 4) {
-        const float* d0 = dir + c0 * D;  // c0 + k < C4: padded rows are never read past
-        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        const double2* d2 = reinterpret_cast<const double2*>(dird + size_t(c0 >> 2) * D * 4);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll 8
         for (int j = 0; j < D; ++j) {
-          const double x = double(bf16_to_f32(kt[j * RS + r]));
-#pragma unroll
-          for (int k = 0; k < 4; ++k) s[k] = __fma_rn(x, double(d0[k * D + j]), s[k]);
+          const double x = double(bf16_to_f32(kt[j * RS + tid]));
+          const double2 a = d2[2 * j], b = d2[2 * j + 1];
+          s0 = __fma_rn(x, a.x, s0);
+          s1 = __fma_rn(x, a.y, s1);
+          s2 = __fma_rn(x, b.x, s2);
+          s3 = __fma_rn(x, b.y, s3);
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (c0 + k < C && s[k] > bs) { bs = s[k]; best = c0 + k; }
+        if (s0 > bs) { bs = s0; best = c0; }
+        if (c0 + 1 < C && s1 > bs) { bs = s1; best = c0 + 1; }
+        if (c0 + 2 < C && s2 > bs) { bs = s2; best = c0 + 2; }
+        if (c0 + 3 < C && s3 > bs) { bs = s3; best = c0 + 3; }
       }
-      cur[r] = int32_t(best);
+      my = int32_t(best);
+      cur[tid] = my;
     }
-    if (tid < int(C)) cnt[tid] = 0;
+    // ---- counts: one ballot per (warp, cluster) --------------------------
+    for (uint32_t c = 0; c < C; ++c) {
+      const unsigned m = __ballot_sync(0xffffffffu, my == int32_t(c));
+      if (lane == 0) wcnt[wid * C4 + c] = __popc(m);
+    }
     __syncthreads();
-    for (uint32_t r = tid; r < rows; r += KS_THREADS) atomicAdd(&cnt[cur[r]], 1u);
+    if (tid < int(C)) {
+      uint32_t sum = 0;
+      for (int w = 0; w < KS_WARPS; ++w) sum += wcnt[w * C4 + tid];
+      cnt[tid] = sum;
+    }
     __syncthreads();
-    // repair_empty_clusters (clustering.hpp:128-153), sequential over ids
+    // ---- repair_empty_clusters (clustering.hpp:128-153), sequential ids ---
+    bool repaired = false;
     for (uint32_t c = 0; c < C; ++c) {
       if (cnt[c] > 0) continue;  // uniform: cnt is shared and stable here
       if (tid == 0) {
@@ -924,15 +991,15 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
       __syncthreads();
       const uint32_t largest = s_largest;
       if (s_lcnt > 1) {
+        repaired = true;
         double bd = -1.0;
         uint32_t bv = 0xffffffffu;
-        for (uint32_t r = tid; r < rows; r += KS_THREADS) {
-          if (uint32_t(cur[r]) != largest) continue;
+        if (tid < int(rows) && uint32_t(cur[tid]) == largest) {
           double na = 0.0, dd = 0.0;
           for (int j = 0; j < D; ++j) {
-            const double x = double(bf16_to_f32(kt[j * RS + r]));
+            const double x = double(bf16_to_f32(kt[j * RS + tid]));
             na = __fma_rn(x, x, na);
-            dd = __fma_rn(x, double(cent[largest * D + j]), dd);
+            dd = __fma_rn(x, double(cent[largest * KS_CS + j]), dd);
           }
           na = sqrt(na);
           const double nb = cnorm[largest];
@@ -941,7 +1008,8 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
             dist = 1.0 - dd / (na * nb);
             dist = dist < 0.0 ? 0.0 : (dist > 2.0 ? 2.0 : dist);
           }
-          if (dist > bd) { bd = dist; bv = r; }
+          bd = dist;
+          bv = tid;
         }
         for (int o = 16; o > 0; o >>= 1) {
           const double od = __shfl_xor_sync(0xffffffffu, bd, o);
@@ -953,44 +1021,83 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
         if (tid == 0) {
           double b = s_wd[0];
           uint32_t v = s_wi[0];
-          for (int w = 1; w < KS_THREADS / 32; ++w)
+          for (int w = 1; w < KS_WARPS; ++w)
             if (s_wd[w] > b || (s_wd[w] == b && s_wi[w] < v)) { b = s_wd[w]; v = s_wi[w]; }
-          s_victim = v == 0xffffffffu ? 0u : v;  // no member beat -1: victim stays 0
-          cur[s_victim] = int32_t(c);
+          v = v == 0xffffffffu ? 0u : v;  // no member beat -1: the victim stays 0
+          cur[v] = int32_t(c);
           cnt[largest]--;
           cnt[c]++;
         }
       }
       __syncthreads();
     }
-    // convergence: next == labels (after repair)
+    if (repaired && tid < int(rows)) my = cur[tid];
+    // ---- convergence: next == labels (after repair) ------------------------
     if (t > 0) {
-      int ch = 0;
-      for (uint32_t r = tid; r < rows; r += KS_THREADS) ch |= cur[r] != prev[r];
-      ch = __syncthreads_or(ch);
+      const int ch = __syncthreads_or(tid < int(rows) && my != prev[tid]);
       if (!ch) { converged = 1; it = t; break; }
       if (t == max_iters) { it = t; break; }
     }
-    // update_centroids from `cur` (clustering.hpp:205-218): per (c, 4 dims)
-    // a lane, members in position order, then the next directions
-    for (uint32_t c = wid; c < C; c += KS_THREADS / 32) {
-      double a[4] = {0.0, 0.0, 0.0, 0.0};
-      for (uint32_t r = 0; r < rows; ++r) {
-        if (uint32_t(cur[r]) != c) continue;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] += double(bf16_to_f32(kt[(4 * lane + k) * RS + r]));
+    // ---- update_centroids (clustering.hpp:205-218) --------------------------
+    // members of each cluster in position order: per-warp counts, their
+    // exclusive scan over warps, then each row's rank among its warp's
+    // same-cluster lanes
+    if (repaired) {
+      for (uint32_t c = 0; c < C; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, my == int32_t(c));
+        if (lane == 0) wcnt[wid * C4 + c] = __popc(m);
       }
-      finish_centroid(a[0], a[1], a[2], a[3], double(cnt[c]), cent + c * D, dir + c * D,
-                      dbf + c * D, cnorm + c, deps + c);
+      __syncthreads();
+    }
+    if (tid < int(C)) {
+      uint32_t sum = 0;
+      for (int w = 0; w < KS_WARPS; ++w) {
+        const uint32_t x = wcnt[w * C4 + tid];
+        wcnt[w * C4 + tid] = sum;
+        sum += x;
+      }
+      cnt[tid] = sum;
     }
     __syncthreads();
+    if (tid == 0) {
+      uint32_t b = 0;
+      for (uint32_t c = 0; c < C; ++c) { cbase[c] = b; b += cnt[c]; }
+      cbase[C] = b;
+    }
+    __syncthreads();
+    {
+      const unsigned same = __match_any_sync(0xffffffffu, my);
+      if (my >= 0) {
+        const uint32_t rank = __popc(same & ((1u << lane) - 1u));
+        mem[cbase[my] + wcnt[wid * C4 + my] + rank] = uint16_t(tid);
+      }
+    }
+    __syncthreads();
+    for (uint32_t e = tid; e < C * D; e += KS_THREADS) {
+      const uint32_t c = e / D, j = e % D;
+      const uint32_t i0 = cbase[c], i1 = cbase[c + 1];
+      const uint16_t* col = kt + j * RS;
+      double a = 0.0;
+      uint32_t i = i0;
+      for (; i + 4 <= i1; i += 4) {
+        const float x0 = bf16_to_f32(col[mem[i]]), x1 = bf16_to_f32(col[mem[i + 1]]);
+        const float x2 = bf16_to_f32(col[mem[i + 2]]), x3 = bf16_to_f32(col[mem[i + 3]]);
+        a += double(x0);
+        a += double(x1);
+        a += double(x2);
+        a += double(x3);
+      }
+      for (; i < i1; ++i) a += double(bf16_to_f32(col[mem[i]]));
+      cent[c * KS_CS + j] = float(a / double(i1 - i0));
+    }
+    ks_finish(C, cent, cnorm, dird);
   }
   // final labels = the last assignment (equal to the previous one when
   // converged); append (cluster_decode_batch: fresh ids from n_clusters)
   const int32_t* fin = lab[it & 1];
   const uint32_t base = n_clusters[u];
   for (uint32_t e = tid; e < C * D; e += KS_THREADS)
-    out_cents[(size_t(u) * c_cap + base) * D + e] = cent[e];
+    out_cents[(size_t(u) * c_cap + base) * D + e] = cent[(e / D) * KS_CS + e % D];
   for (uint32_t r = tid; r < rows; r += KS_THREADS)
     out_labels[size_t(u) * label_stride + r] = fin[r] + int32_t(base);
   __syncthreads();
@@ -1010,9 +1117,7 @@ int launch_kmeans_small(cudaStream_t st, const uint16_t* keys, uint64_t key_stri
                         const uint32_t* init_rows, float* cents, uint32_t c_cap,
                         int32_t* labels, uint32_t label_stride, uint32_t* n_clusters,
                         uint32_t* iters, int32_t* status) {
-  const size_t C4 = (C + 3) & ~3u, R2 = (rows + 1) & ~1u, RS = ((rows + 15) & ~15u) + 1;
-  const size_t smem = C4 * 8 + 2 * C4 * D * 4 + C4 * D * 2 + C4 * 4 + C4 * 4 + 2 * R2 * 4 +
-                      size_t(D) * RS * 2;
+  const size_t smem = ks_smem_bytes(rows, C);
   CKV_CUDA_TRY(smem_optin((const void*)k_kmeans_small, 200 * 1024));
   k_kmeans_small<<<n_units, KS_THREADS, smem, st>>>(keys, key_stride, rows, C, max_iters,
                                                      init_rows, cents, c_cap, labels,

@@ -36,7 +36,8 @@ def device_view(ptr: int, shape, dtype: torch.dtype, device) -> torch.Tensor:
 class Session:
     def __init__(self, n_units: int, group: int, prompt_len: int, max_decode: int,
                  budget: int, retention: int = 1, cfg: ClusterConfig | None = None,
-                 kv_heads: int = 8, flags: int = 0, ctx: Context | None = None):
+                 kv_heads: int = 8, flags: int = 0, ctx: Context | None = None,
+                 async_delay: int = 0):
         cfg = cfg or ClusterConfig()
         cfg.validate()
         self.ctx = ctx or Context.default()
@@ -45,7 +46,7 @@ class Session:
         self.n_q = n_units * group
         desc = N.SessionDesc(n_units, group, prompt_len, max_decode, budget, retention,
                              cfg.c0_divisor, cfg.c_plus, cfg.decode_batch, cfg.sink_tokens,
-                             cfg.max_iters, cfg.seed, kv_heads, flags)
+                             cfg.max_iters, cfg.seed, kv_heads, flags, async_delay)
         h = C.c_void_p()
         check(lib().ckv_session_create(self.ctx.h, C.byref(desc), C.byref(h)))
         self.h = h

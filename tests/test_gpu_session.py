@@ -129,3 +129,92 @@ def test_session_host_buffer_paths_match_device(gpu_ctx):
                                          o_page.ctypes.data, 0))
         assert np.array_equal(o_pin, o_dev), t
         assert np.array_equal(o_page, o_dev), t
+
+
+@pytest.mark.parametrize("delay", [1, 5])
+def test_session_async_clustering_vs_oracle(gpu_ctx, delay):
+    """The harness's async_clustering (harness.hpp:236-243, 327-329): a
+    decode batch formed at step t is clustered on a side stream and joins
+    the model at the start of step t + delay; until then its rows stay in
+    the recency window.  I_T, outputs, the cache counters and the final model
+    against the oracle replaying that schedule."""
+    import torch
+    from paper_2412_03213_b200 import _native as N
+    from paper_2412_03213_b200 import api
+    from paper_2412_03213_b200.session import Session
+
+    U, G, L, T, B, m, R = 3, 2, 640, 75, 96, 20, 2
+    heads = [head(13, u, 0, L, T) for u in range(U)]
+    cfg = api.ClusterConfig(decode_batch=m, c0_divisor=40)
+    s = Session(U, G, L, T, B, retention=R, cfg=cfg, kv_heads=U,
+                flags=N.CKV_SESSION_TOKEN_IDS, async_delay=delay)
+    s.load_prompt_host(np.stack([bf16_bits(h["K"]) for h in heads]),
+                       np.stack([bf16_bits(h["V"]) for h in heads]))
+    s.prefill()
+    P = port()
+    seeds = [P.mix_seed(0, 0, u) for u in range(U)]  # unit u = (layer 0, kv head u)
+    models = []
+    for u in range(U):
+        o = P.cluster_prefill(heads[u]["K"], OCfg(seed=seeds[u], decode_batch=m, c0_divisor=40))
+        models.append([o.centroids, o.labels])
+    caches = [P.cache(R) for _ in range(U * G)]
+    Kc = [h["K"].copy() for h in heads]
+    Vc = [h["V"].copy() for h in heads]
+    labeled_end, n_ctx, pending, queue = L, L, 0, []
+    dev = gpu_ctx.device
+    for t in range(T):
+        while queue and queue[0][0] <= t:  # harness.hpp:237-243
+            _, lo, hi = queue.pop(0)
+            for u in range(U):
+                c2, l2, _ = P.cluster_decode_batch(models[u][0], models[u][1], Kc[u][lo:hi],
+                                                   OCfg(seed=seeds[u], decode_batch=m))
+                models[u] = [c2, l2]
+            labeled_end = hi
+        q = np.stack([heads[u]["Q"][(t + r * (T // G)) % T] for u in range(U) for r in range(G)])
+        kn = np.stack([bf16_bits(heads[u]["dK"][t]) for u in range(U)])
+        vn = np.stack([bf16_bits(heads[u]["dV"][t]) for u in range(U)])
+        out = s.step(torch.from_numpy(q).to(dev), torch.from_numpy(kn.view(np.int16)).to(dev),
+                     torch.from_numpy(vn.view(np.int16)).to(dev))
+        st = s.state()
+        tok = st["token_ids"].cpu().numpy().view(np.uint32)
+        ntok = st["n_tokens"].cpu().numpy()
+        go = out.cpu().numpy()
+        rec = np.arange(labeled_end, n_ctx, dtype=np.uint32)
+        for u in range(U):
+            cents, labels = models[u]
+            sizes, _, _ = P.build_index(labels, cents.shape[0])
+            for r in range(G):
+                hq = u * G + r
+                sel = P.select_tokens(q[hq], cents, labels, 16, B, rec)
+                assert np.array_equal(tok[hq, : ntok[hq]], sel.token_ids), (t, u, r)
+                caches[hq].lookup_and_update(np.sort(sel.taken_clusters), sizes)
+                oo, _ = P.approx_attention(q[hq], Kc[u][:n_ctx], Vc[u][:n_ctx], sel.token_ids)
+                assert np.abs(go[hq] - oo).max() <= 2e-5 * np.abs(Vc[u][:n_ctx]).max()
+        for u in range(U):
+            Kc[u] = np.concatenate([Kc[u], heads[u]["dK"][t:t + 1]])
+            Vc[u] = np.concatenate([Vc[u], heads[u]["dV"][t:t + 1]])
+        n_ctx += 1
+        pending += 1
+        if pending == m:  # harness.hpp:327-329
+            queue.append((t + delay, n_ctx - m, n_ctx))
+            pending = 0
+    s.stats()  # blocking status check of the last batch
+    st = s.state()
+    for u in range(U):
+        cents, labels = models[u]
+        nc = int(st["n_clusters"][u].item())
+        assert nc == cents.shape[0]
+        assert np.array_equal(st["centroids"][u, :nc].cpu().numpy().view(np.uint32),
+                              cents.view(np.uint32))
+        assert np.array_equal(st["labels"][u, :labeled_end].cpu().numpy(), labels)
+    ctr = s.cache_counters()
+    for hq in range(U * G):
+        assert [int(x) for x in ctr[hq]] == [int(x) for x in caches[hq].counters()]
+
+
+def test_session_async_rejects_bad_delay(gpu_ctx):
+    from paper_2412_03213_b200 import api
+    from paper_2412_03213_b200.session import Session
+    with pytest.raises(ValueError, match="async"):
+        Session(2, 2, 300, 40, 64, cfg=api.ClusterConfig(decode_batch=20, c0_divisor=40),
+                kv_heads=2, async_delay=20)
