@@ -369,9 +369,9 @@ def run_config_D(torch, dev, ctx, args):
     res = {"workload": f"config D: {args.layers} layers x {args.kv_heads} kv x {G} q heads, "
                        f"{L} prompt + {T} generated, B={B}, decode-batch clustering every 320 steps",
            "tokens": T}
-    for R in (1, 2):
+    for R, delay in ((1, 0), (2, 0), (1, 8)):
         sess = Session(U, G, L, T, B, retention=R, cfg=ClusterConfig(), kv_heads=args.kv_heads,
-                       ctx=ctx)
+                       ctx=ctx, async_delay=delay)
         gk = torch.Generator(device=dev)
         gk.manual_seed(12)
         fill_kv(torch, dev, gk, centers, sess.K, sess.V, L)
@@ -385,9 +385,14 @@ def run_config_D(torch, dev, ctx, args):
         ms = np.array([ev[t].elapsed_time(ev[t + 1]) for t in range(T)])
         st = sess.stats()
         m = 320
-        ev_steps = np.array([(t + 1) % m == 0 for t in range(T)])
+        # synchronous: the step that completes a batch clusters and commits
+        # it; async (harness.hpp:236-243): that step launches the k-means on
+        # the side stream, the step `delay` later commits it
+        ev_steps = np.array([(t + 1) % m == 0 or (delay and (t + 1 - delay) % m == 0 and t >= delay)
+                             for t in range(T)])
         ctr = sess.cache_counters().astype(np.float64)
-        res[f"R{R}"] = {
+        key = f"R{R}" + (f"_async{delay}" if delay else "")
+        res[key] = {
             "hit_rate": float(ctr[:, 1].sum() / max(1.0, ctr[:, 0].sum())),
             "miss_tokens_per_q_head_step": float(ctr[:, 2].sum() / (U * G * T)),
             "step_us_mean": float(ms.mean() * 1e3),
@@ -400,6 +405,8 @@ def run_config_D(torch, dev, ctx, args):
             "labeled_end": int(st.labeled_end), "n_ctx": int(st.n_ctx),
             "tokens_per_s": float(1000.0 / ms.mean()),
         }
+        if delay:
+            res[key]["async_delay"] = delay
         del sess
         torch.cuda.synchronize()
     del q_all, kn_all, vn_all
