@@ -888,7 +888,7 @@ def main():
         return
     U = args.layers * args.kv_heads
     G, L, B = args.group, args.L, args.budget
-    T = args.warmup + args.steps + args.e2e_steps + 2
+    T = 2 * (args.warmup + args.steps) + args.e2e_steps + 2
     ctx = Context(local)
     sess_flags = (N.CKV_KM_EXACT_ONLY if args.exact_kmeans else 0) | \
         (N.CKV_SESSION_L2_PERSIST if os.environ.get("CKV_L2_PERSIST") else 0)
@@ -996,6 +996,27 @@ def main():
     if world > 1:
         step_ms = _max_over_ranks(torch, dev, world, [step_ms])[0]
         dist.barrier()
+
+    # ---- layer mode: one (select, attend) pair per layer, in layer order --
+    # (a decoder's dependency order: layer l+1's queries need layer l's
+    # output), vs the layer-batched step above (the harness's independent
+    # (layer, head) fan-out, harness.hpp:362-378)
+    sess.set_layer_units(args.kv_heads)
+    for _ in range(args.warmup):
+        sess.step(q_all[t], kn_all[t], vn_all[t], out)
+        t += 1
+    torch.cuda.synchronize()
+    evl = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    evl[0].record()
+    for _ in range(args.steps):
+        sess.step(q_all[t], kn_all[t], vn_all[t], out)
+        t += 1
+    evl[1].record()
+    torch.cuda.synchronize()
+    layer_step_ms = evl[0].elapsed_time(evl[1]) / args.steps
+    sess.set_layer_units(0)
+    if world > 1:
+        layer_step_ms = _max_over_ranks(torch, dev, world, [layer_step_ms])[0]
 
     # ---- per-kernel timing of one step's select and attend --------------
     st = sess.state()
@@ -1146,6 +1167,12 @@ def main():
                           "bytes_per_step": step_bytes_unique,
                           "bytes_per_step_no_dedupe": attend_bytes_perq + select_bytes},
         "kernels_us": {"k_select": sel_ms * 1e3, "k_attend": att_ms * 1e3},
+        "per_layer": {"ms_per_step": layer_step_ms, "tokens_per_s": world * 1000.0 / layer_step_ms,
+                      "us_per_layer": layer_step_ms * 1e3 / args.layers,
+                      "vs_layer_batched": layer_step_ms / step_ms,
+                      "step_roofline_frac": step_bytes_unique / (layer_step_ms * 1e-3) / 1e9 / hbm,
+                      "mode": f"{args.layers} sequential (select, attend) launch pairs per step, "
+                              f"{args.kv_heads} kv units each (ckv_session_set_layer_units)"},
         "prefill": {"ms": prefill_ms, "session_ms": session_prefill_ms,
                     "timing": "ckv_cluster_prefill of all units, median of 9 after 2 warm-ups",
                     "ms_all": [round(x, 2) for x in km_ms],

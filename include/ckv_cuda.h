@@ -524,6 +524,13 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* k_new,
 /* Select + attend only (no append/cluster), device pointers, for timing
  * the steady-state hot path.  Equivalent to the first half of step. */
 int ckv_session_attend_only(ckv_session* s, const float* q_dev, float* out_dev);
+/* Layer mode: each step's select + attend runs one launch pair per slice of
+ * layer_units consecutive units (a model layer's kv heads), slices in order —
+ * the dependency order of a decoder, where layer l+1's queries come from
+ * layer l's output.  0 (default): one pair for all units (the reference
+ * harness's independent (layer, head) fan-out).  layer_units must divide
+ * n_units. */
+int ckv_session_set_layer_units(ckv_session* s, uint32_t layer_units);
 /* Introspection for tests / bench. */
 typedef struct {
   uint32_t n_ctx, labeled_end, steps;

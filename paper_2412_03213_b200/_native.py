@@ -162,6 +162,7 @@ SIGNATURES = {
     "ckv_session_prefill": (C.c_int, [vp, vp]),
     "ckv_session_step": (C.c_int, [vp, vp, vp, vp, vp, C.c_int]),
     "ckv_session_attend_only": (C.c_int, [vp, vp, vp]),
+    "ckv_session_set_layer_units": (C.c_int, [vp, u32]),
     "ckv_session_stats_get": (C.c_int, [vp, C.POINTER(SessionStats)]),
     "ckv_session_state": (C.c_int, [vp] + [C.POINTER(vp)] * 8 + [C.POINTER(u32)] * 2),
     "ckv_session_cache": (vp, [vp]),

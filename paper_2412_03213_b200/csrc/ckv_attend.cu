@@ -400,6 +400,20 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
   }
 }
 
+// work items that fill the GPU twice over at 3 resident CTAs per SM
+static uint32_t attend_target_items() {
+  static int sms_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int n = sms_dev[dev & 63];
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    n = n < 1 ? 148 : n;
+    sms_dev[dev & 63] = n;
+  }
+  return uint32_t(n) * 6;
+}
+
 uint32_t attend_splits(const ckv_attend_desc& d) {
   // ~1024 rows per work item: few per-item epilogues and merges, enough items
   // to balance.  Tile / stage / item sizes were swept on B200 at config B
@@ -408,7 +422,15 @@ uint32_t attend_splits(const ckv_attend_desc& d) {
 #ifndef CKV_AT_ITEM_ROWS
 #define CKV_AT_ITEM_ROWS 1024
 #endif
-  const uint32_t s = (d.max_tokens + CKV_AT_ITEM_ROWS - 1) / CKV_AT_ITEM_ROWS;
+  uint32_t s = (d.max_tokens + CKV_AT_ITEM_ROWS - 1) / CKV_AT_ITEM_ROWS;
+  // few q heads (one layer's launch in layer mode): split finer, down to
+  // 128-row items, so ~2 waves of items cover the SMs (3 CTAs each)
+  const uint32_t target = attend_target_items();
+  if (d.n_q && uint64_t(d.n_q) * s < target) {
+    const uint32_t want = (target + d.n_q - 1) / d.n_q;
+    const uint32_t cap = (d.max_tokens + 127) / 128;
+    s = std::max(s, std::min(want, cap));
+  }
   return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 
@@ -459,7 +481,9 @@ size_t attend_part_floats(uint32_t n_q, uint32_t max_tokens) {
   ckv_attend_desc d{};
   d.n_q = n_q;
   d.max_tokens = max_tokens;
-  return size_t(n_q) * attend_splits(d) * PART;
+  // a launch over any subset of these q heads (layer mode) fits too: it
+  // needs <= max(n_q * splits, target + n_q) partials
+  return std::max(size_t(n_q) * attend_splits(d), size_t(attend_target_items()) + n_q) * PART;
 }
 
 }  // namespace ckvb

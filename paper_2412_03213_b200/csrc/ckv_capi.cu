@@ -920,6 +920,7 @@ struct ckv_session {
   uint32_t* stage_ncl = nullptr;  // n_clusters as the side stream's k-means leaves it
   struct Queued { uint32_t ready, pos0, rows, C; };
   std::deque<Queued> queue;
+  uint32_t layer_units = 0;  // 0: one select + attend for all units; else per slice
 };
 
 namespace {
@@ -1143,13 +1144,16 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
   return rc;
 }
 
-// q_copy: when q is mapped host memory, the selection leaves a device copy
-// of it there and the attention reads that (its bulk copies stay on HBM)
-static int session_select_attend(ckv_session* s, const float* q_dev, float* out_dev,
-                                 float* q_copy = nullptr) {
+// select + attend of units [u0, u0 + nu) (all offsets are per unit / per q
+// head, so a slice is a sub-session).  q_copy: when q is mapped host memory,
+// the selection leaves a device copy of it there and the attention reads that
+// (its bulk copies stay on HBM)
+static int session_select_attend_slice(ckv_session* s, uint32_t u0, uint32_t nu,
+                                       const float* q_dev, float* out_dev, float* q_copy) {
+  const uint32_t G = s->d.group, h0 = u0 * G;
   ckv_select_desc sd{};
-  sd.n_q = s->n_q;
-  sd.group = s->d.group;
+  sd.n_q = nu * G;
+  sd.group = G;
   sd.budget = s->d.budget;
   sd.sink_count = std::min(s->d.sink_tokens, s->d.prompt_len);
   sd.p_cap = s->p_cap;
@@ -1160,19 +1164,56 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
   sd.flags = (s->d.flags & CKV_SESSION_L2_PERSIST) ? CKV_SEL_L2_PERSIST : 0u;
   sd.row_base = sd.sink_count;
   const bool want_ids = (s->d.flags & CKV_SESSION_TOKEN_IDS) != 0;
-  CKV_TRY(launch_select(s->ctx->stream, sd, q_dev, s->cents, s->n_clusters, s->sizes, s->starts,
-                        s->sorted, want_ids ? s->token_ids : nullptr, nullptr, s->runs,
-                        sd.row_base, s->n_tokens, s->n_taken, s->trimmed, s->ranked, nullptr,
-                        s->cache ? s->cache->dev : null_cache(), s->sel_scratch, q_copy));
+  ckv_runs runs = s->runs;
+  runs.row += size_t(h0) * runs.run_cap;
+  runs.off += size_t(h0) * (runs.run_cap + 1);
+  runs.count += h0;
+  CacheDev cache = s->cache ? s->cache->dev : null_cache();
+  if (cache.bits) {
+    cache.bits += size_t(h0) * cache.retention * cache.words;
+    cache.ring += size_t(h0) * 2;
+    cache.counters += size_t(h0) * 4;
+    cache.n_slots = sd.n_q;
+  }
+  const float* qs = q_dev + size_t(h0) * D;
+  float* qc = q_copy ? q_copy + size_t(h0) * D : nullptr;
+  CKV_TRY(launch_select(s->ctx->stream, sd, qs, s->cents + size_t(u0) * s->c_cap * D,
+                        s->n_clusters + u0, s->sizes + size_t(u0) * s->c_cap,
+                        s->starts + size_t(u0) * (s->c_cap + 1), s->sorted + size_t(u0) * s->p_cap,
+                        want_ids ? s->token_ids + size_t(h0) * s->sel_cap : nullptr, nullptr, runs,
+                        sd.row_base, s->n_tokens + h0, s->n_taken + h0, s->trimmed + h0,
+                        s->ranked + size_t(h0) * s->c_cap, nullptr, cache, s->sel_scratch, qc));
   ckv_attend_desc ad{};
-  ad.n_q = s->n_q;
-  ad.group = s->d.group;
+  ad.n_q = sd.n_q;
+  ad.group = G;
   ad.p_cap = s->p_cap;
   ad.sel_cap = s->sel_cap;
   ad.max_tokens = std::min(s->d.budget, s->labeled_end) + sd.sink_count + (s->n_ctx - s->labeled_end);
-  CKV_TRY(launch_attend(s->ctx->stream, ad, q_copy ? q_copy : q_dev, s->K, s->V, nullptr,
-                        s->runs, s->n_tokens, out_dev, nullptr, nullptr, s->part, s->tickets));
+  CKV_TRY(launch_attend(s->ctx->stream, ad, qc ? qc : qs, s->K + size_t(u0) * s->p_cap * D,
+                        s->V + size_t(u0) * s->p_cap * D, nullptr, runs, s->n_tokens + h0,
+                        out_dev + size_t(h0) * D, nullptr, nullptr, s->part, s->tickets));
   s->ctx->launches += 3;
+  return CKV_OK;
+}
+
+// one step's select + attend: every unit in one launch pair, or (layer mode,
+// ckv_session_set_layer_units) one pair per layer slice in layer order — the
+// dependency order of a model, where layer l+1's queries need layer l's output
+static int session_select_attend(ckv_session* s, const float* q_dev, float* out_dev,
+                                 float* q_copy = nullptr) {
+  const uint32_t lu = s->layer_units;
+  if (lu == 0 || lu >= s->U) return session_select_attend_slice(s, 0, s->U, q_dev, out_dev, q_copy);
+  for (uint32_t u0 = 0; u0 < s->U; u0 += lu)
+    CKV_TRY(session_select_attend_slice(s, u0, std::min(lu, s->U - u0), q_dev, out_dev, q_copy));
+  return CKV_OK;
+}
+
+int ckv_session_set_layer_units(ckv_session* s, uint32_t layer_units) {
+  if (layer_units && s->U % layer_units) {
+    set_error("ckv_session_set_layer_units: must divide n_units");
+    return CKV_EINVAL;
+  }
+  s->layer_units = layer_units;
   return CKV_OK;
 }
 

@@ -692,8 +692,11 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   while (p2 < desc.c_cap) p2 <<= 1;
   const uint32_t warp_bytes =
       uint32_t(std::max<size_t>(size_t(p2) * 16, size_t(SW_STAGE) * D * 4));
+  // fused (one CTA per unit: score + select) when the units fill the GPU;
+  // a layer-sized launch (few units) scores with many CTAs per unit instead
   static const bool unfused = getenv("CKV_SELECT_UNFUSED") != nullptr;
-  if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused) {
+  const bool few_units = units * 2 < uint32_t(num_sms());
+  if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused && !few_units) {
     const size_t smem_f = size_t(G) * warp_bytes + size_t(G) * c_pad * 8;
     if (smem_f <= 200 * 1024) {
       for (const void* fn : {(const void*)k_select_fused<1>, (const void*)k_select_fused<2>,

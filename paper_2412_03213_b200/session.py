@@ -102,6 +102,11 @@ class Session:
         check(lib().ckv_session_attend_only(self.h, q.data_ptr(), out.data_ptr()))
         return out
 
+    def set_layer_units(self, layer_units: int) -> None:
+        """Layer mode (ckv_session_set_layer_units): one select + attend per
+        slice of layer_units units, in order; 0 = all units at once."""
+        check(lib().ckv_session_set_layer_units(self.h, layer_units))
+
     def stats(self) -> N.SessionStats:
         st = N.SessionStats()
         check(lib().ckv_session_stats_get(self.h, C.byref(st)))

@@ -218,3 +218,85 @@ def test_session_async_rejects_bad_delay(gpu_ctx):
     with pytest.raises(ValueError, match="async"):
         Session(2, 2, 300, 40, 64, cfg=api.ClusterConfig(decode_batch=20, c0_divisor=40),
                 kv_heads=2, async_delay=20)
+
+
+def test_session_layer_mode_matches_batched(gpu_ctx):
+    """ckv_session_set_layer_units: one (select, attend) pair per layer slice
+    gives the same outputs, token ids and cache counters as the all-units
+    launch pair, bit for bit, across a decode-batch event."""
+    import torch
+    from paper_2412_03213_b200 import _native as N
+    from paper_2412_03213_b200 import api
+    from paper_2412_03213_b200.session import Session
+
+    layers, kvh, G, L, T, B = 3, 2, 2, 500, 30, 80
+    U = layers * kvh
+    heads = [head(21, u // kvh, u % kvh, L, T) for u in range(U)]
+    cfg = api.ClusterConfig(decode_batch=12, c0_divisor=40)
+    ss = []
+    for lu in (0, kvh):
+        s = Session(U, G, L, T, B, retention=2, cfg=cfg, kv_heads=kvh,
+                    flags=N.CKV_SESSION_TOKEN_IDS)
+        s.load_prompt_host(np.stack([bf16_bits(h["K"]) for h in heads]),
+                           np.stack([bf16_bits(h["V"]) for h in heads]))
+        s.prefill()
+        s.set_layer_units(lu)
+        ss.append(s)
+    dev = gpu_ctx.device
+    for t in range(T):
+        q = np.stack([heads[u]["Q"][(t + r) % T] for u in range(U) for r in range(G)])
+        kn = torch.from_numpy(np.stack([bf16_bits(heads[u]["dK"][t]) for u in range(U)]).view(np.int16)).to(dev)
+        vn = torch.from_numpy(np.stack([bf16_bits(heads[u]["dV"][t]) for u in range(U)]).view(np.int16)).to(dev)
+        qd = torch.from_numpy(q).to(dev)
+        o = [s.step(qd, kn, vn).cpu().numpy() for s in ss]
+        assert np.array_equal(o[0], o[1]), t
+        st = [s.state() for s in ss]
+        assert torch.equal(st[0]["n_tokens"], st[1]["n_tokens"])
+        nt = st[0]["n_tokens"].cpu().numpy()
+        a, b = st[0]["token_ids"].cpu().numpy(), st[1]["token_ids"].cpu().numpy()
+        for hq in range(U * G):
+            assert np.array_equal(a[hq, :nt[hq]], b[hq, :nt[hq]]), (t, hq)
+    assert np.array_equal(ss[0].cache_counters(), ss[1].cache_counters())
+    with pytest.raises(ValueError):
+        ss[0].set_layer_units(4)  # does not divide 6
+
+
+def test_session_fused_and_split_select_paths(gpu_ctx):
+    """A session of 80 units selects with the fused kernel (one CTA per unit:
+    scoring + selection, k_select_fused); its layer mode (8-unit slices)
+    selects with the split kernels (k_score_approx over many CTAs per unit,
+    then k_select_warp).  Both against select_tokens on the oracle's models."""
+    import torch
+    from paper_2412_03213_b200 import _native as N
+    from paper_2412_03213_b200 import api
+    from paper_2412_03213_b200.session import Session
+
+    layers, kvh, G, L, T, B = 10, 8, 2, 400, 4, 64
+    U = layers * kvh
+    heads = [head(31, u // kvh, u % kvh, L, T) for u in range(U)]
+    cfg = api.ClusterConfig(decode_batch=50, c0_divisor=40)
+    s = Session(U, G, L, T, B, retention=1, cfg=cfg, kv_heads=kvh, flags=N.CKV_SESSION_TOKEN_IDS)
+    s.load_prompt_host(np.stack([bf16_bits(h["K"]) for h in heads]),
+                       np.stack([bf16_bits(h["V"]) for h in heads]))
+    s.prefill()
+    P = port()
+    models = [P.cluster_prefill(heads[u]["K"], OCfg(seed=P.mix_seed(0, u // kvh, u % kvh),
+                                                     c0_divisor=40)) for u in range(U)]
+    Kc = [h["K"].copy() for h in heads]
+    dev = gpu_ctx.device
+    for t in range(T):
+        s.set_layer_units(kvh if t % 2 else 0)
+        q = np.stack([heads[u]["Q"][(t + 3 * r) % T] for u in range(U) for r in range(G)])
+        kn = np.stack([bf16_bits(heads[u]["dK"][t]) for u in range(U)]).view(np.int16)
+        vn = np.stack([bf16_bits(heads[u]["dV"][t]) for u in range(U)]).view(np.int16)
+        s.step(torch.from_numpy(q).to(dev), torch.from_numpy(kn).to(dev),
+               torch.from_numpy(vn).to(dev))
+        st = s.state()
+        tok = st["token_ids"].cpu().numpy().view(np.uint32)
+        ntok = st["n_tokens"].cpu().numpy()
+        rec = np.arange(L, L + t, dtype=np.uint32)
+        for u in range(U):
+            for r in range(G):
+                hq = u * G + r
+                sel = P.select_tokens(q[hq], models[u].centroids, models[u].labels, 16, B, rec)
+                assert np.array_equal(tok[hq, : ntok[hq]], sel.token_ids), (t, u, r)
