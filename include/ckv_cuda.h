@@ -483,6 +483,7 @@ typedef struct {
                            /* rows stay in the recency window until     */
                            /* then.  Needs d < decode_batch <= 512,     */
                            /* c_plus <= 32.                             */
+  uint32_t c0_override;    /* ClusterConfig::c0_override (0 = the rule) */
 } ckv_session_desc;
 
 /* Also materialise each step's I_T as reference token positions
@@ -531,6 +532,10 @@ int ckv_session_attend_only(ckv_session* s, const float* q_dev, float* out_dev);
  * harness's independent (layer, head) fan-out).  layer_units must divide
  * n_units. */
 int ckv_session_set_layer_units(ckv_session* s, uint32_t layer_units);
+/* k-means iterations (ClusterModel::invocation_iterations' last entry,
+ * clustering.hpp:330) of every unit's most recent decode batch; waits for
+ * that batch's k-means and reports its input errors. */
+int ckv_session_batch_iterations(ckv_session* s, uint32_t* iterations_host);
 /* Introspection for tests / bench. */
 typedef struct {
   uint32_t n_ctx, labeled_end, steps;

@@ -217,6 +217,10 @@ class Oracle:
                                                       u32p, C.POINTER(C.c_uint32)]
             L.ref_cache_counters.argtypes = [C.c_void_p, u64p]
             L.ref_cache_invalidate.argtypes = [C.c_void_p, u32p, C.c_uint32]
+            L.ref_run_simulation_synth.restype = C.c_long
+            L.ref_run_simulation_synth.argtypes = (
+                [C.c_uint32, C.c_uint64] + [C.c_uint32] * 8 + [C.c_int, C.c_uint32, C.c_int] +
+                [f64p, u64p, f64p, u64p, u32p, C.c_uint32])
             L.ref_decode_step_cpu.restype = C.c_double
             L.ref_decode_step_cpu.argtypes = [f32p, u32p, C.c_uint32, C.c_void_p, u32p,
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
@@ -469,6 +473,28 @@ class Oracle:
         if rc:
             raise OracleError(self._err())
         return out, w[: len(rows)]
+
+    def run_simulation_synth(self, spec: dict, budget: int, retention: int = 1,
+                             decode_batch: int = 320, c0_divisor: int = 80,
+                             async_clustering: bool = False, async_delay: int = 8,
+                             recency_window: bool = True) -> dict:
+        """The reference harness (run_simulation, harness.hpp:362-410; ClusterKV
+        policy) on generate_synthetic(spec) rounded to bf16.  Reference only."""
+        assert self.kind == "reference"
+        n_rows = spec["n_layers"] * spec["n_heads"] * spec["T"]
+        rows_f = np.zeros((n_rows, 3), np.float64)
+        rows_u = np.zeros((n_rows, 6), np.uint64)
+        summ_f = np.zeros(4, np.float64)
+        summ_u = np.zeros(2, np.uint64)
+        hist = np.zeros(64, np.uint32)
+        n = self.lib.ref_run_simulation_synth(
+            spec["n_centers"], spec["seed"], spec["L"], spec["T"], spec["n_layers"],
+            spec["n_heads"], budget, retention, decode_batch, c0_divisor, int(async_clustering),
+            async_delay, int(recency_window), rows_f, rows_u, summ_f, summ_u, hist, len(hist))
+        if n < 0:
+            raise OracleError(self._err())
+        return dict(rows_f=rows_f[:n], rows_u=rows_u[:n], summ_f=summ_f, summ_u=summ_u,
+                    hist=hist)
 
     def cache(self, retention: int, d: int = 128) -> "OracleCache":
         return OracleCache(self, retention, d)

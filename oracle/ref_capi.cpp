@@ -19,6 +19,7 @@
 #include "clusterkv/clustering.hpp"
 #include "clusterkv/selection.hpp"
 #include "clusterkv/trace.hpp"
+#include "clusterkv/harness.hpp"
 
 namespace R = ckv_ref;
 
@@ -373,5 +374,80 @@ double ref_prefill_cpu(const float* const* keys, uint32_t units, uint32_t L, uin
 }
 
 unsigned ref_hardware_concurrency() { return std::max(1u, std::thread::hardware_concurrency()); }
+
+// The reference harness itself (run_simulation, harness.hpp:362-410, over
+// simulate_head, :155-346) on generate_synthetic(spec) with every matrix
+// rounded to bf16 (RNE; the GPU store is bf16): the oracle of
+// the GPU decode-loop quality driver (paper_2412_03213_b200/quality.py).
+// ClusterKV policy.  rows_f [n_rows][3] = recall, l2_rel, cos_sim; rows_u
+// [n_rows][6] = step, layer, head, clusters_hit, clusters_requested,
+// tokens_transferred; summ_f [4] = mean recall, l2_rel, cos_sim, hit_rate;
+// summ_u [2] = tokens, bytes transferred; hist [hist_cap] k-means iteration
+// histogram.  Returns the row count, or -1 with ref_last_error().
+static float bf16_rne(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = uint32_t((uint64_t(u) + (((u >> 16) & 1u) + 0x7fffu)) >> 16) << 16;
+  std::memcpy(&x, &u, 4);
+  return x;
+}
+
+long ref_run_simulation_synth(uint32_t n_centers, uint64_t seed, uint32_t L, uint32_t T,
+                              uint32_t n_layers, uint32_t n_heads, uint32_t budget,
+                              uint32_t retention, uint32_t decode_batch, uint32_t c0_divisor,
+                              int async_clustering, uint32_t async_delay, int recency_window,
+                              double* rows_f, uint64_t* rows_u, double* summ_f, uint64_t* summ_u,
+                              uint32_t* hist, uint32_t hist_cap) {
+  try {
+    R::SynthSpec s;
+    s.n_centers = n_centers;
+    s.seed = seed;
+    s.prompt_len = L;
+    s.decode_len = T;
+    s.d = 128;
+    s.n_layers = n_layers;
+    s.n_heads = n_heads;
+    R::TraceBundle b = R::generate_synthetic(s);
+    for (auto& tr : b.traces)
+      for (R::Matrix* m : {&tr.prompt_keys, &tr.prompt_values, &tr.decode_queries,
+                           &tr.decode_keys, &tr.decode_values})
+        for (float& x : m->data) x = bf16_rne(x);
+    R::PolicyConfig cfg;
+    cfg.policy = R::Policy::ClusterKV;
+    cfg.budget = budget;
+    cfg.retention = retention;
+    cfg.cluster.decode_batch = decode_batch;
+    cfg.cluster.c0_divisor = c0_divisor;
+    cfg.async_clustering = async_clustering != 0;
+    cfg.async_delay = async_delay;
+    cfg.recency_window = recency_window != 0;
+    R::RunReport rep = R::run_simulation(b, cfg);
+    for (size_t i = 0; i < rep.rows.size(); ++i) {
+      const auto& r = rep.rows[i];
+      rows_f[3 * i] = r.recall;
+      rows_f[3 * i + 1] = r.l2_rel;
+      rows_f[3 * i + 2] = r.cos_sim;
+      rows_u[6 * i] = r.step;
+      rows_u[6 * i + 1] = r.layer;
+      rows_u[6 * i + 2] = r.head;
+      rows_u[6 * i + 3] = r.clusters_hit;
+      rows_u[6 * i + 4] = r.clusters_requested;
+      rows_u[6 * i + 5] = r.tokens_transferred;
+    }
+    summ_f[0] = rep.summary.mean_recall;
+    summ_f[1] = rep.summary.mean_l2_rel;
+    summ_f[2] = rep.summary.mean_cos_sim;
+    summ_f[3] = rep.summary.hit_rate;
+    summ_u[0] = rep.summary.tokens_transferred;
+    summ_u[1] = rep.summary.bytes_transferred;
+    for (uint32_t i = 0; i < hist_cap; ++i) hist[i] = 0;
+    for (const auto& [it, n] : rep.summary.iteration_histogram)
+      if (it < hist_cap) hist[it] = n;
+    return long(rep.rows.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
 
 }  // extern "C"

@@ -65,7 +65,7 @@ class SessionDesc(C.Structure):
                 ("budget", u32), ("retention", u32), ("c0_divisor", u32), ("c_plus", u32),
                 ("decode_batch", u32), ("sink_tokens", u32), ("max_iters", u32),
                 ("cluster_seed", u64), ("kv_heads", u32), ("flags", u32),
-                ("async_delay", u32)]
+                ("async_delay", u32), ("c0_override", u32)]
 
 
 class KmShardDesc(C.Structure):
@@ -163,6 +163,7 @@ SIGNATURES = {
     "ckv_session_step": (C.c_int, [vp, vp, vp, vp, vp, C.c_int]),
     "ckv_session_attend_only": (C.c_int, [vp, vp, vp]),
     "ckv_session_set_layer_units": (C.c_int, [vp, u32]),
+    "ckv_session_batch_iterations": (C.c_int, [vp, vp]),
     "ckv_session_stats_get": (C.c_int, [vp, C.POINTER(SessionStats)]),
     "ckv_session_state": (C.c_int, [vp] + [C.POINTER(vp)] * 8 + [C.POINTER(u32)] * 2),
     "ckv_session_cache": (vp, [vp]),

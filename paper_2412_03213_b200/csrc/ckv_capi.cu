@@ -921,6 +921,7 @@ struct ckv_session {
   struct Queued { uint32_t ready, pos0, rows, C; };
   std::deque<Queued> queue;
   uint32_t layer_units = 0;  // 0: one select + attend for all units; else per slice
+  uint32_t n_batches = 0;    // decode batches launched (device path)
 };
 
 namespace {
@@ -981,7 +982,8 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   s->U = d->n_units;
   s->n_q = d->n_units * d->group;
   s->p_cap = d->prompt_len + d->max_decode;
-  const uint32_t C0 = ckv_prefill_cluster_count(d->prompt_len, d->c0_divisor, d->sink_tokens, 0);
+  const uint32_t C0 = ckv_prefill_cluster_count(d->prompt_len, d->c0_divisor, d->sink_tokens,
+                                                d->c0_override);
   s->c_cap = C0 + d->c_plus * (d->max_decode / d->decode_batch + 1);
   // recency: the collecting batch (< m rows) plus, in async mode, a batch
   // waiting async_delay steps for its commit
@@ -1111,7 +1113,7 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
   pd.c0_divisor = s->d.c0_divisor;
   pd.sink_tokens = s->d.sink_tokens;
   pd.max_iters = s->d.max_iters;
-  pd.c0_override = 0;
+  pd.c0_override = s->d.c0_override;
   pd.flags = s->d.flags;
   // CKV_DEBUG_TIMING=1: host wall time of the three phases on stderr
   static const bool dbg = getenv("CKV_DEBUG_TIMING") != nullptr;
@@ -1123,7 +1125,7 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
   CKV_TRY(ckv_cluster_prefill(s->ctx, &pd, s->K, s->seeds.data(), s->cents, s->labels,
                               s->n_clusters, info, nullptr, nullptr));
   const auto t1 = now();
-  s->C_cur = ckv_prefill_cluster_count(pd.L, pd.c0_divisor, pd.sink_tokens, 0);
+  s->C_cur = ckv_prefill_cluster_count(pd.L, pd.c0_divisor, pd.sink_tokens, pd.c0_override);
   CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
                           s->n_clusters, s->sizes, s->starts, s->sorted));
   const auto t2 = now();
@@ -1266,6 +1268,7 @@ static int session_cluster_batch(ckv_session* s, cudaStream_t st, uint32_t pos0,
                                st));
   CKV_CUDA_TRY(cudaEventRecord(s->ev_stat, st));
   s->stat_pending = true;
+  s->n_batches++;
   s->ctx->launches += 2;
   return CKV_OK;
 }
@@ -1412,6 +1415,14 @@ int ckv_session_state(ckv_session* s, float** cents, int32_t** labels, uint32_t*
   if (n_tokens) *n_tokens = s->n_tokens;
   if (c_cap) *c_cap = s->c_cap;
   if (sel_cap) *sel_cap = s->sel_cap;
+  return CKV_OK;
+}
+
+int ckv_session_batch_iterations(ckv_session* s, uint32_t* iterations_host) {
+  if (s->n_batches == 0) { set_error("session: no decode batch yet"); return CKV_EINVAL; }
+  CKV_TRY(session_check_status(s, true));
+  for (uint32_t u = 0; u < s->U; ++u)
+    iterations_host[u] = uint32_t(s->h_stat[u]) & 0x7fffffffu;
   return CKV_OK;
 }
 

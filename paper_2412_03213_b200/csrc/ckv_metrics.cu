@@ -106,8 +106,12 @@ k_exact_topb(uint32_t group, uint32_t n, uint32_t p_cap, const float* __restrict
 #pragma unroll
   for (int k = 0; k < 8; ++k) qv[k] = qs[8 * hl + k];
   float kmax2 = 0.f;
-  for (uint32_t r = (tid >> 4); r < n; r += MT_THREADS / 16) {
-    const uint4 kv = __ldg(reinterpret_cast<const uint4*>(ku + size_t(r) * D) + hl);
+  // both half-warps stay in the loop to the end (the shuffles are warp-wide);
+  // a half-warp past the last row scores zeros and stores nothing
+  for (uint32_t r0 = (tid >> 5) * 2; r0 < n; r0 += MT_THREADS / 16) {
+    const uint32_t r = r0 + ((tid >> 4) & 1);
+    const uint4 kv = r < n ? __ldg(reinterpret_cast<const uint4*>(ku + size_t(r) * D) + hl)
+                           : make_uint4(0u, 0u, 0u, 0u);
     const float x[8] = {__uint_as_float(kv.x << 16), __uint_as_float(kv.x & 0xffff0000u),
                         __uint_as_float(kv.y << 16), __uint_as_float(kv.y & 0xffff0000u),
                         __uint_as_float(kv.z << 16), __uint_as_float(kv.z & 0xffff0000u),
@@ -120,7 +124,7 @@ k_exact_topb(uint32_t group, uint32_t n, uint32_t p_cap, const float* __restrict
       a += __shfl_xor_sync(0xffffffffu, a, o);
       k2 += __shfl_xor_sync(0xffffffffu, k2, o);
     }
-    if (hl == 0) akey[r] = fkey32m(a);
+    if (hl == 0 && r < n) akey[r] = fkey32m(a);
     kmax2 = fmaxf(kmax2, k2);
   }
   kmax2 = warp_max(kmax2);

@@ -40,13 +40,16 @@ class Session:
                  async_delay: int = 0):
         cfg = cfg or ClusterConfig()
         cfg.validate()
+        if cfg.metric != 0:
+            raise N.ValidationError(1, "Session: cosine assignment only (DESIGN.md §1)")
         self.ctx = ctx or Context.default()
         self.cfg = cfg
         self.n_units, self.group = n_units, group
         self.n_q = n_units * group
         desc = N.SessionDesc(n_units, group, prompt_len, max_decode, budget, retention,
                              cfg.c0_divisor, cfg.c_plus, cfg.decode_batch, cfg.sink_tokens,
-                             cfg.max_iters, cfg.seed, kv_heads, flags, async_delay)
+                             cfg.max_iters, cfg.seed, kv_heads, flags, async_delay,
+                             cfg.c0_override)
         h = C.c_void_p()
         check(lib().ckv_session_create(self.ctx.h, C.byref(desc), C.byref(h)))
         self.h = h
@@ -106,6 +109,12 @@ class Session:
         """Layer mode (ckv_session_set_layer_units): one select + attend per
         slice of layer_units units, in order; 0 = all units at once."""
         check(lib().ckv_session_set_layer_units(self.h, layer_units))
+
+    def batch_iterations(self) -> np.ndarray:
+        """k-means iterations of each unit's most recent decode batch."""
+        out = np.zeros(self.n_units, np.uint32)
+        check(lib().ckv_session_batch_iterations(self.h, out.ctypes.data))
+        return out
 
     def stats(self) -> N.SessionStats:
         st = N.SessionStats()

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("n,B", [(1000, 256), (4096, 1024), (300, 1000), (32768, 1024),
-                                 (5000, 1)])
+                                 (5000, 1), (601, 96), (33, 7), (4097, 1024)])
 def test_exact_topb_matches_oracle(gpu_ctx, n, B):
     from paper_2412_03213_b200 import metrics
     h = head(4, 0, 2, max(n, 64), T=8)

@@ -155,3 +155,16 @@ def test_page_select_port_matches_reference(ref):
         K = to_bf16_representable(rng.standard_normal((n, 128)).astype(np.float32))
         q = to_bf16_representable(rng.standard_normal(128).astype(np.float32))
         assert np.array_equal(P.page_select(q, K, B, ps, mm), ref.page_select(q, K, B, ps, mm))
+
+
+def test_generate_synthetic_bundle_port_vs_reference(port, ref, tmp_path):
+    """orc_generate_synthetic (the whole bundle, per-head sub-seeds) equals
+    the reference's generate_synthetic, read back from its own CKVT file."""
+    from paper_2412_03213_b200 import trace as T
+    p = tmp_path / "b.ckvt"
+    assert ref.lib.ref_write_synthetic_trace(str(p).encode(), 8, 7, 300, 20, 128, 2, 3) == 0
+    b = T.read_trace(str(p))
+    tr = port.generate_synthetic(7, 2, 3, 300, 20)
+    for u in range(6):
+        for name in T.NAMES:
+            assert np.array_equal(getattr(b.traces[u], name), getattr(tr, name)[u]), (u, name)
