@@ -413,6 +413,37 @@ def run_config_D(torch, dev, ctx, args):
     return res
 
 
+def run_quality(torch, dev, ctx, args, budgets=(128, 256, 512, 1024, 2048), T=32):
+    """Selection quality vs budget: the GPU port of the
+    reference harness's run_simulation + sweep (paper_2412_03213_b200/
+    quality.py, pinned to the compiled reference in tests/test_gpu_quality.py)
+    on one layer (8 kv heads) of the bench's synthetic 32k draw, T decode
+    steps each: mean recall against the exact top-B, output error against
+    full attention, cluster-cache hit rate."""
+    from paper_2412_03213_b200 import quality as Q
+    from paper_2412_03213_b200.trace import HeadTrace, TraceBundle
+    U, L = args.kv_heads, args.L
+    g, centers = gen_inputs(torch, dev, U, 1, L, T, seed=21)
+    K = torch.empty((U, L, D), dtype=torch.int16, device=dev)
+    V = torch.empty_like(K)
+    fill_kv(torch, dev, g, centers, K, V, L)
+    q, kn, vn = gen_decode(torch, dev, g, centers, 1, T)  # [T, U, D]
+    f32 = lambda b: ((b.to(torch.int32) & 0xffff) << 16).view(torch.float32).cpu().numpy()
+    Kf, Vf, dKf, dVf = f32(K), f32(V), f32(kn.transpose(0, 1)), f32(vn.transpose(0, 1))
+    Qf = q.transpose(0, 1).contiguous().cpu().numpy()
+    bundle = TraceBundle(1, U, [HeadTrace(Kf[u], Vf[u], Qf[u], dKf[u], dVf[u]) for u in range(U)])
+    t0 = time.perf_counter()
+    reps = Q.sweep(bundle, Q.PolicyConfig(), "budget", list(budgets), ctx=ctx)
+    return {"workload": f"{U} kv heads (one layer), {L} ctx, {T} decode steps per budget; "
+                        "quality.run_simulation (reference harness semantics, GPU metrics)",
+            "budget": list(budgets),
+            "mean_recall": [r.summary.mean_recall for r in reps],
+            "mean_l2_rel": [r.summary.mean_l2_rel for r in reps],
+            "mean_cos_sim": [r.summary.mean_cos_sim for r in reps],
+            "hit_rate": [r.summary.hit_rate for r in reps],
+            "sweep_ms": (time.perf_counter() - t0) * 1e3}
+
+
 def run_config_C(args, rank, world, torch, dev, ctx, hbm):
     """configs[2]: Llama-3-8B shape, 32k context, B = 2048, global batch 32,
     batch-sharded over the ranks (strong scaling: 32 / world sequences each).
@@ -1190,6 +1221,11 @@ def main():
     }
     if page_block is not None:
         line["page_baseline"] = page_block
+    if not args.no_extra and world == 1:
+        try:
+            line["quality"] = run_quality(torch, dev, ctx, args)
+        except Exception as ex:  # reported, never silently dropped
+            line["quality"] = {"failed": repr(ex)}
     if not args.no_extra and world == 1:
         del sess
         torch.cuda.synchronize()
