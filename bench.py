@@ -388,8 +388,9 @@ def run_config_D(torch, dev, ctx, args):
         # synchronous: the step that completes a batch clusters and commits
         # it; async (harness.hpp:236-243): that step launches the k-means on
         # the side stream, the step `delay` later commits it
-        ev_steps = np.array([(t + 1) % m == 0 or (delay and (t + 1 - delay) % m == 0 and t >= delay)
-                             for t in range(T)])
+        ev_steps = np.array([bool((t + 1) % m == 0 or
+                                  (delay and (t + 1 - delay) % m == 0 and t >= delay))
+                             for t in range(T)], dtype=bool)
         ctr = sess.cache_counters().astype(np.float64)
         key = f"R{R}" + (f"_async{delay}" if delay else "")
         res[key] = {

@@ -494,6 +494,14 @@ typedef struct {
  * (cudaLimitPersistingL2CacheSize, device-wide, restored at destroy) and
  * selects with CKV_SEL_L2_PERSIST. */
 #define CKV_SESSION_L2_PERSIST 0x200u
+/* Physical two-tier cluster cache (cache.hpp:25-93; ckv_tier.cu): each step
+ * the selected clusters missing from a per-unit page pool in HBM are copied
+ * into it from the backing tier and the attention reads the pool pages.
+ * TIERED: the backing tier is the session's HBM store; TIER_HOST: a
+ * host-pinned mirror of it (misses are PCIe reads, the offload setting).
+ * Residency: clusters the unit selected in the last `retention` steps. */
+#define CKV_SESSION_TIERED 0x800u
+#define CKV_SESSION_TIER_HOST 0x1000u
 
 int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* desc, ckv_session** out);
 int ckv_session_destroy(ckv_session* s);
@@ -536,6 +544,9 @@ int ckv_session_set_layer_units(ckv_session* s, uint32_t layer_units);
  * clustering.hpp:330) of every unit's most recent decode batch; waits for
  * that batch's k-means and reports its input errors. */
 int ckv_session_batch_iterations(ckv_session* s, uint32_t* iterations_host);
+/* Tiered sessions: out[5] = rows fetched, clusters fetched, clusters
+ * selected (per unit, summed), evictions, pool rows per unit. */
+int ckv_session_tier_stats(ckv_session* s, uint64_t* out);
 /* Introspection for tests / bench. */
 typedef struct {
   uint32_t n_ctx, labeled_end, steps;

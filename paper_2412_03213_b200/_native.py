@@ -18,6 +18,8 @@ CKV_KM_OBJECTIVE, CKV_KM_EXACT_ONLY, CKV_KM_NO_VALIDATE = 1, 2, 4
 CKV_SEL_FULL_RANK, CKV_SEL_SCORES = 1, 2
 CKV_SESSION_TOKEN_IDS = 0x100
 CKV_SESSION_L2_PERSIST = 0x200
+CKV_SESSION_TIERED = 0x800
+CKV_SESSION_TIER_HOST = 0x1000
 CKV_SEL_L2_PERSIST = 4
 
 vp, u32, u64, i32, f32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32, C.c_float
@@ -164,6 +166,7 @@ SIGNATURES = {
     "ckv_session_attend_only": (C.c_int, [vp, vp, vp]),
     "ckv_session_set_layer_units": (C.c_int, [vp, u32]),
     "ckv_session_batch_iterations": (C.c_int, [vp, vp]),
+    "ckv_session_tier_stats": (C.c_int, [vp, vp]),
     "ckv_session_stats_get": (C.c_int, [vp, C.POINTER(SessionStats)]),
     "ckv_session_state": (C.c_int, [vp] + [C.POINTER(vp)] * 8 + [C.POINTER(u32)] * 2),
     "ckv_session_cache": (vp, [vp]),

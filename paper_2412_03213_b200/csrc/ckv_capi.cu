@@ -921,6 +921,11 @@ struct ckv_session {
   struct Queued { uint32_t ready, pos0, rows, C; };
   std::deque<Queued> queue;
   uint32_t layer_units = 0;  // 0: one select + attend for all units; else per slice
+  // physical two-tier cache (CKV_SESSION_TIERED / _TIER_HOST, ckv_tier.cu)
+  bool tiered = false;
+  TierArgs tier{};
+  ckv_runs truns{};            // page runs the attention reads in tiered mode
+  uint16_t *hK = nullptr, *hV = nullptr;  // host-pinned backing mirror (TIER_HOST)
   uint32_t n_batches = 0;    // decode batches launched (device path)
 };
 
@@ -989,7 +994,16 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   // waiting async_delay steps for its commit
   s->sel_cap = d->budget + d->sink_tokens + d->decode_batch + 1 +
                (d->async_delay ? d->decode_batch + d->async_delay : 0);
-  const size_t kv = size_t(s->U) * s->p_cap * D;
+  s->tiered = (d->flags & (CKV_SESSION_TIERED | CKV_SESSION_TIER_HOST)) != 0;
+  // tiered: every unit's page pool sits after all units' store rows (pool
+  // rows are addressed relative to a unit's store base, ckv_tier.cu); sized
+  // for R steps of the unit's heads' selections (whole clusters, page
+  // rounding) with slack — the fetch evicts harder before it ever fails
+  uint32_t np = 0;
+  if (s->tiered)
+    np = std::max<uint32_t>(1, d->retention) * d->group * ((d->budget + 512) / TIER_PAGE_ROWS + 64) +
+         64;
+  const size_t kv = size_t(s->U) * (s->p_cap + size_t(np) * TIER_PAGE_ROWS) * D;
   int rc = CKV_OK;
   rc |= salloc(&s->K, kv);
   rc |= salloc(&s->V, kv);
@@ -1032,6 +1046,47 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
         cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->ev_done, cudaEventDisableTiming) != cudaSuccess)
       rc = 1;
+  }
+  if (!rc && s->tiered) {
+    TierArgs& t = s->tier;
+    t.n_units_total = s->U;
+    t.p_cap = s->p_cap;
+    t.c_cap = s->c_cap;
+    t.np = np;
+    t.group = d->group;
+    t.retention = std::max<uint32_t>(1, d->retention);
+    t.sink = std::min(d->sink_tokens, d->prompt_len);
+    t.n_clusters = s->n_clusters;
+    t.sizes = s->sizes;
+    t.starts = s->starts;
+    rc |= salloc(&t.cpage, size_t(s->U) * s->c_cap);
+    rc |= salloc(&t.last, size_t(s->U) * s->c_cap);
+    rc |= salloc(&t.next, size_t(s->U) * np);
+    rc |= salloc(&t.free_stack, size_t(s->U) * np);
+    rc |= salloc(&t.n_free, s->U);
+    rc |= salloc(&t.stats, size_t(s->U) * 4);
+    rc |= salloc(&t.status, 1);
+    s->truns.run_cap = s->c_cap + (d->budget + TIER_PAGE_ROWS - 1) / TIER_PAGE_ROWS + 3;
+    rc |= salloc(&s->truns.row, size_t(s->n_q) * s->truns.run_cap);
+    rc |= salloc(&s->truns.off, size_t(s->n_q) * (s->truns.run_cap + 1));
+    rc |= salloc(&s->truns.count, s->n_q);
+    if (!rc && (d->flags & CKV_SESSION_TIER_HOST)) {
+      const size_t bytes = size_t(s->U) * s->p_cap * D * 2;
+      void *hk = nullptr, *hv = nullptr, *dk = nullptr, *dv = nullptr;
+      if (cudaHostAlloc(&hk, bytes, cudaHostAllocMapped) != cudaSuccess ||
+          cudaHostAlloc(&hv, bytes, cudaHostAllocMapped) != cudaSuccess ||
+          cudaHostGetDevicePointer(&dk, hk, 0) != cudaSuccess ||
+          cudaHostGetDevicePointer(&dv, hv, 0) != cudaSuccess)
+        rc = 1;
+      s->hK = static_cast<uint16_t*>(hk);
+      s->hV = static_cast<uint16_t*>(hv);
+      t.back_K = static_cast<const uint16_t*>(dk);
+      t.back_V = static_cast<const uint16_t*>(dv);
+    } else {
+      t.back_K = s->K;  // secondary-HBM backing: the store itself
+      t.back_V = s->V;
+    }
+    if (!rc) cudaMemsetAsync(t.status, 0, 4, ctx->stream);
   }
   if (rc) { ckv_session_destroy(s); return CKV_ENOMEM; }
   cudaMemsetAsync(s->tickets, 0, size_t(s->n_q) * 4, ctx->stream);
@@ -1081,6 +1136,12 @@ int ckv_session_destroy(ckv_session* s) {
   if (s->ev_stat) cudaEventDestroy(s->ev_stat);
   if (s->h_stat) cudaFreeHost(s->h_stat);
   cudaFree(s->d_seeds); cudaFree(s->db_init); cudaFree(s->db_stat); cudaFree(s->stage_ncl);
+  cudaFree(s->tier.cpage); cudaFree(s->tier.last); cudaFree(s->tier.next);
+  cudaFree(s->tier.free_stack); cudaFree(s->tier.n_free); cudaFree(s->tier.stats);
+  cudaFree(s->tier.status);
+  cudaFree(s->truns.row); cudaFree(s->truns.off); cudaFree(s->truns.count);
+  if (s->hK) cudaFreeHost(s->hK);
+  if (s->hV) cudaFreeHost(s->hV);
   ckv_cache_destroy(s->cache);
   if (s->l2_persist) l2_persist_release(s->ctx->device);
   delete s;
@@ -1135,6 +1196,14 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
   if (N > 0)  // in place (bounded staging), so the store is never held twice
     CKV_TRY(ckv_relayout_kv(s->ctx, s->U, s->p_cap, s->K, s->V, s->K, s->V, s->sorted, sink,
                             s->labeled_end, s->n_ctx));
+  if (s->tiered) {
+    CKV_TRY(launch_tier_init(s->ctx->stream, s->tier, s->U));
+    if (s->hK) {  // the clustered store to the host tier
+      const size_t bytes = size_t(s->U) * s->p_cap * D * 2;
+      CKV_CUDA_TRY(cudaMemcpyAsync(s->hK, s->K, bytes, cudaMemcpyDeviceToHost, s->ctx->stream));
+      CKV_CUDA_TRY(cudaMemcpyAsync(s->hV, s->V, bytes, cudaMemcpyDeviceToHost, s->ctx->stream));
+    }
+  }
   s->prefilled = true;
   const int rc = ckv_ctx_sync(s->ctx);
   if (dbg) {
@@ -1191,6 +1260,16 @@ static int session_select_attend_slice(ckv_session* s, uint32_t u0, uint32_t nu,
   ad.p_cap = s->p_cap;
   ad.sel_cap = s->sel_cap;
   ad.max_tokens = std::min(s->d.budget, s->labeled_end) + sd.sink_count + (s->n_ctx - s->labeled_end);
+  if (s->tiered) {  // misses backing -> page pool; the attention reads page runs
+    ckv_runs tr = s->truns;
+    tr.row += size_t(h0) * tr.run_cap;
+    tr.off += size_t(h0) * (tr.run_cap + 1);
+    tr.count += h0;
+    CKV_TRY(launch_tier_fetch(s->ctx->stream, s->tier, u0, nu, s->steps, runs, tr,
+                              s->ranked + size_t(h0) * s->c_cap, s->n_taken + h0, s->K, s->V));
+    s->ctx->launches++;
+    runs = tr;
+  }
   CKV_TRY(launch_attend(s->ctx->stream, ad, qc ? qc : qs, s->K + size_t(u0) * s->p_cap * D,
                         s->V + size_t(u0) * s->p_cap * D, nullptr, runs, s->n_tokens + h0,
                         out_dev + size_t(h0) * D, nullptr, nullptr, s->part, s->tickets));
@@ -1285,6 +1364,13 @@ static int session_commit_batch(ckv_session* s, uint32_t pos0, uint32_t m, uint3
                                               s->sizes, s->starts, s->sorted);
   CKV_LAUNCH_CHECK("k_batch_commit");
   s->ctx->launches++;
+  if (s->hK) {  // the re-laid batch rows join the host tier
+    const size_t pitch = size_t(s->p_cap) * D * 2, w = size_t(m) * D * 2, o = size_t(pos0) * D;
+    CKV_CUDA_TRY(cudaMemcpy2DAsync(s->hK + o, pitch, s->K + o, pitch, w, s->U,
+                                   cudaMemcpyDeviceToHost, st));
+    CKV_CUDA_TRY(cudaMemcpy2DAsync(s->hV + o, pitch, s->V + o, pitch, w, s->U,
+                                   cudaMemcpyDeviceToHost, st));
+  }
   s->labeled_end += m;
   s->C_cur += C;
   return CKV_OK;
@@ -1427,5 +1513,21 @@ int ckv_session_batch_iterations(ckv_session* s, uint32_t* iterations_host) {
 }
 
 ckv_cache* ckv_session_cache(ckv_session* s) { return s->cache; }
+
+int ckv_session_tier_stats(ckv_session* s, uint64_t* out) {
+  if (!s->tiered) { set_error("session: not tiered"); return CKV_EINVAL; }
+  std::vector<unsigned long long> st(size_t(s->U) * 4);
+  int32_t status = 0;
+  CKV_CUDA_TRY(cudaMemcpyAsync(st.data(), s->tier.stats, st.size() * 8, cudaMemcpyDeviceToHost,
+                               s->ctx->stream));
+  CKV_CUDA_TRY(cudaMemcpyAsync(&status, s->tier.status, 4, cudaMemcpyDeviceToHost, s->ctx->stream));
+  CKV_CUDA_TRY(cudaStreamSynchronize(s->ctx->stream));
+  if (status) { set_error("session: tier page pool exhausted"); return CKV_EINVAL; }
+  for (int k = 0; k < 4; ++k) out[k] = 0;
+  for (uint32_t u = 0; u < s->U; ++u)
+    for (int k = 0; k < 4; ++k) out[k] += st[size_t(u) * 4 + k];
+  out[4] = uint64_t(s->tier.np) * TIER_PAGE_ROWS;  // pool rows per unit
+  return CKV_OK;
+}
 
 }  // extern "C"

@@ -129,6 +129,31 @@ cudaError_t smem_optin(const void* fn, int bytes, bool max_carveout = false);
 void host_init_rows(uint32_t n, uint32_t C, uint64_t seed, uint32_t* rows);
 }  // namespace ckvb
 
+namespace ckvb {
+// the physical two-tier cluster cache (ckv_tier.cu)
+constexpr uint32_t TIER_PAGE_ROWS = 16;
+struct TierArgs {
+  uint32_t n_units_total, p_cap, c_cap, np, group, retention, sink;
+  const uint32_t* n_clusters;
+  const uint32_t* sizes;
+  const uint32_t* starts;
+  const uint16_t* back_K;  // backing tier: [unit][p_cap][128] (device store or mapped host mirror)
+  const uint16_t* back_V;
+  int32_t* cpage;          // [unit][c_cap] first pool page of a resident cluster, -1 if absent
+  uint32_t* last;          // [unit][c_cap] last step the unit selected the cluster
+  int32_t* next;           // [unit][np] page chain
+  int32_t* free_stack;     // [unit][np]
+  int32_t* n_free;         // [unit]
+  unsigned long long* stats;  // [unit][4]: rows fetched, clusters fetched, clusters selected, evictions
+  int32_t* status;         // pool exhausted -> 1
+};
+int launch_tier_init(cudaStream_t st, const TierArgs& a, uint32_t n_units);
+int launch_tier_fetch(cudaStream_t st, const TierArgs& a, uint32_t u0, uint32_t n_units,
+                      uint32_t step, const ckv_runs& runs, const ckv_runs& out,
+                      const uint32_t* ranked, const uint32_t* n_taken, uint16_t* K,
+                      uint16_t* V);
+}  // namespace ckvb
+
 struct ckv_cache {
   ckv_ctx* ctx;
   ckvb::CacheDev dev;

@@ -116,6 +116,15 @@ class Session:
         check(lib().ckv_session_batch_iterations(self.h, out.ctypes.data))
         return out
 
+    def tier_stats(self) -> dict:
+        """Physical two-tier cache counters (tiered sessions)."""
+        out = np.zeros(5, np.uint64)
+        check(lib().ckv_session_tier_stats(self.h, out.ctypes.data))
+        return dict(rows_fetched=int(out[0]), clusters_fetched=int(out[1]),
+                    clusters_selected=int(out[2]), evictions=int(out[3]),
+                    pool_rows_per_unit=int(out[4]),
+                    bytes_fetched=int(out[0]) * D * 2 * 2)
+
     def stats(self) -> N.SessionStats:
         st = N.SessionStats()
         check(lib().ckv_session_stats_get(self.h, C.byref(st)))

@@ -300,3 +300,46 @@ def test_session_fused_and_split_select_paths(gpu_ctx):
                 hq = u * G + r
                 sel = P.select_tokens(q[hq], models[u].centroids, models[u].labels, 16, B, rec)
                 assert np.array_equal(tok[hq, : ntok[hq]], sel.token_ids), (t, u, r)
+
+
+@pytest.mark.parametrize("flag,R,layer_mode", [("TIERED", 1, False), ("TIER_HOST", 2, False),
+                                               ("TIERED", 2, True)])
+def test_session_two_tier_cache_matches_flat(gpu_ctx, flag, R, layer_mode):
+    """The physical two-tier cache (ckv_tier.cu): misses copied from the
+    backing tier (HBM store or the host-pinned mirror) into the page pool,
+    attention over page runs — outputs, I_T and the reference cache
+    counters equal the flat session's bit for bit, across decode batches; the
+    physical counters are consistent (fetched <= selected, bytes = rows x 512)."""
+    import torch
+    from paper_2412_03213_b200 import _native as N
+    from paper_2412_03213_b200 import api
+    from paper_2412_03213_b200.session import Session
+
+    layers, kvh, G, L, T, B = 2, 3, 2, 700, 45, 96
+    U = layers * kvh
+    heads = [head(41, u // kvh, u % kvh, L, T) for u in range(U)]
+    cfg = api.ClusterConfig(decode_batch=15, c0_divisor=40)
+    ss = []
+    for extra in (0, getattr(N, f"CKV_SESSION_{flag}")):
+        s = Session(U, G, L, T, B, retention=R, cfg=cfg, kv_heads=kvh,
+                    flags=N.CKV_SESSION_TOKEN_IDS | extra)
+        s.load_prompt_host(np.stack([bf16_bits(h["K"]) for h in heads]),
+                           np.stack([bf16_bits(h["V"]) for h in heads]))
+        s.prefill()
+        if layer_mode:
+            s.set_layer_units(kvh)
+        ss.append(s)
+    dev = gpu_ctx.device
+    for t in range(T):
+        q = torch.from_numpy(np.stack([heads[u]["Q"][(t + 5 * r) % T] for u in range(U)
+                                       for r in range(G)])).to(dev)
+        kn = torch.from_numpy(np.stack([bf16_bits(heads[u]["dK"][t]) for u in range(U)]).view(np.int16)).to(dev)
+        vn = torch.from_numpy(np.stack([bf16_bits(heads[u]["dV"][t]) for u in range(U)]).view(np.int16)).to(dev)
+        o = [s.step(q, kn, vn).cpu().numpy() for s in ss]
+        assert np.array_equal(o[0], o[1]), t
+        st = [s.state() for s in ss]
+        assert torch.equal(st[0]["n_tokens"], st[1]["n_tokens"])
+    assert np.array_equal(ss[0].cache_counters(), ss[1].cache_counters())
+    ts = ss[1].tier_stats()
+    assert 0 < ts["clusters_fetched"] <= ts["clusters_selected"]
+    assert ts["rows_fetched"] > 0 and ts["bytes_fetched"] == ts["rows_fetched"] * 512
