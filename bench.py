@@ -369,9 +369,33 @@ def run_config_D(torch, dev, ctx, args):
     res = {"workload": f"config D: {args.layers} layers x {args.kv_heads} kv x {G} q heads, "
                        f"{L} prompt + {T} generated, B={B}, decode-batch clustering every 320 steps",
            "tokens": T}
-    for R, delay in ((1, 0), (2, 0), (1, 8)):
+    from paper_2412_03213_b200 import _native as N
+    # flat (every cluster HBM-resident), async clustering, and the physical
+    # two-tier cache: backing tier in HBM (secondary store) or host-pinned
+    # memory (the offload setting, misses over PCIe), R = 1 and 2
+    variants = ((1, 0, 0, ""), (2, 0, 0, ""), (1, 8, 0, ""),
+                (1, 0, N.CKV_SESSION_TIERED, "_tier_hbm"), (2, 0, N.CKV_SESSION_TIERED, "_tier_hbm"),
+                (1, 0, N.CKV_SESSION_TIER_HOST, "_tier_host"),
+                (2, 0, N.CKV_SESSION_TIER_HOST, "_tier_host"))
+    flat_us = {}
+    # warm-up: a small session per mode runs decode-batch events first, so the
+    # timed runs do not pay one-time kernel loading / attribute setup
+    gw = torch.Generator(device=dev)
+    gw.manual_seed(13)
+    for _, delay, tflag, _ in variants:
+        ws = Session(args.kv_heads, G, 1024, 12, 64, retention=2,
+                     cfg=ClusterConfig(decode_batch=4, c0_divisor=40), kv_heads=args.kv_heads,
+                     ctx=ctx, async_delay=min(delay, 3), flags=tflag)
+        fill_kv(torch, dev, gw, centers[: args.kv_heads], ws.K, ws.V, 1024)
+        ws.prefill()
+        for t in range(12):
+            ws.step(q_all[t, : args.kv_heads * G], kn_all[t, : args.kv_heads],
+                    vn_all[t, : args.kv_heads], out[: args.kv_heads * G])
+        del ws
+    torch.cuda.synchronize()
+    for R, delay, tflag, tname in variants:
         sess = Session(U, G, L, T, B, retention=R, cfg=ClusterConfig(), kv_heads=args.kv_heads,
-                       ctx=ctx, async_delay=delay)
+                       ctx=ctx, async_delay=delay, flags=tflag)
         gk = torch.Generator(device=dev)
         gk.manual_seed(12)
         fill_kv(torch, dev, gk, centers, sess.K, sess.V, L)
@@ -392,7 +416,7 @@ def run_config_D(torch, dev, ctx, args):
                                   (delay and (t + 1 - delay) % m == 0 and t >= delay))
                              for t in range(T)], dtype=bool)
         ctr = sess.cache_counters().astype(np.float64)
-        key = f"R{R}" + (f"_async{delay}" if delay else "")
+        key = f"R{R}" + (f"_async{delay}" if delay else "") + tname
         res[key] = {
             "hit_rate": float(ctr[:, 1].sum() / max(1.0, ctr[:, 0].sum())),
             "miss_tokens_per_q_head_step": float(ctr[:, 2].sum() / (U * G * T)),
@@ -408,6 +432,19 @@ def run_config_D(torch, dev, ctx, args):
         }
         if delay:
             res[key]["async_delay"] = delay
+        if not tflag and not delay:
+            flat_us[R] = float(ms.mean() * 1e3)
+        if tflag:
+            ts = sess.tier_stats()
+            extra = float(ms.mean() * 1e3) - flat_us.get(R, float("nan"))
+            res[key]["tier"] = {
+                "backing": "host-pinned (PCIe)" if tflag == N.CKV_SESSION_TIER_HOST else "HBM",
+                "pool_rows_per_unit": ts["pool_rows_per_unit"],
+                "rows_fetched_per_step": ts["rows_fetched"] / T,
+                "bytes_fetched_per_step": ts["bytes_fetched"] / T,
+                "physical_hit_rate": 1.0 - ts["clusters_fetched"] / max(1, ts["clusters_selected"]),
+                "transfer_us_per_step": extra,
+                "transfer_gbs": ts["bytes_fetched"] / T / (extra * 1e-6) / 1e9 if extra > 0 else None}
         del sess
         torch.cuda.synchronize()
     del q_all, kn_all, vn_all
