@@ -621,6 +621,417 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
   }
 }
 
+// ===========================================================================
+// k_assign_tc2: the same assignment filter with a barrier-free epilogue.
+//
+// k_assign_tc's 16 epilogue warps split each chunk's columns, so every row's
+// maximum needs two named barriers per chunk and one warp decides all rows
+// after the tile: the epilogue, not the tensor pipe, set the pass time.
+// Here the epilogue warps split TILES, not columns:
+//   * T2_CG epilogue warps per TMEM lane quarter; warp g takes the items
+//     s = g, g + CG, ... of the CTA, and each of its threads owns one key row
+//     across ALL columns of the item, so the row's decision needs no exchange
+//     with any other warp (no barrier, no shared state);
+//   * per row the thread keeps an exact running state: the two best entries
+//     {score, first column, in-band mask of a 32-column block} and the
+//     largest score displaced from them.  A block's entry lists its columns
+//     >= (running max - band) with the block maximum as their score;
+//   * accumulator chunks are 256 columns (two TMEM buffers): the SS-mode MMA
+//     re-reads the A tile from shared memory once per chunk, and at K = 128
+//     the shared-memory operand traffic bounds the producer + MMA rate
+//     (measured: 128-column chunks cost 1.5x).  A warp reads a chunk in
+//     groups of 4 blocks (128 registers) and releases it after the last
+//     group's loads; the other warp of the quarter works on the next item
+//     meanwhile.
+// Exactness: a column c with S_c >= M - band is >= (running max - band) when
+// its block is scanned (the running max never exceeds M), so it enters an
+// entry; it can only leave by being displaced, which records a dropped score
+// >= S_c.  Listed scores are upper bounds of the true S, so the final filter
+// (entries with score >= M - band) is a superset of {c : S_c >= M - band} --
+// which contains the exact argmax (see the header) -- and a single survivor
+// is the label.  Padding columns (>= C) score exactly 0 (zero operand rows);
+// a surviving one makes the row FULL (exact fix-up over all C).
+// ===========================================================================
+constexpr int T2_CW = 256;                       // columns per TMEM chunk buffer
+constexpr int T2_NBUF = 512 / T2_CW;             // chunk buffers (512 TMEM columns)
+constexpr int T2_CG = T2_NBUF;                   // epilogue warps per lane quarter: one per buffer
+constexpr int T2_GB = 4;                         // blocks a warp holds in registers at once
+constexpr int T2_THREADS = (2 + 4 * T2_CG) * 32;
+struct T2Bars {
+  uint64_t a_full[4], a_empty[4];
+  uint64_t b_full, b_empty;
+  // TMEM buffer g belongs to epilogue group g (items of parity g)
+  uint64_t acc_full[T2_NBUF][1], acc_empty[T2_NBUF];
+  uint32_t tmem_base;
+  uint32_t fix_n;
+};
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+
+// Waits that back off with __nanosleep between probes: a spinning single-
+// thread producer / MMA warp otherwise issues a probe every few cycles on
+// the same SM sub-partition as two column warps (measured: 22% of the
+// kernel's instructions).  The MMA thread sleeps briefly (its wake-up delay
+// hides under the chunk the tensor pipe is still computing), the producer
+// longer (it runs stages ahead).
+template <uint32_t NS>
+__device__ __forceinline__ void mb_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
+  while (!done) {
+    __nanosleep(NS);
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
+  }
+}
+#ifndef CKV_T2_NS_MMA
+#define CKV_T2_NS_MMA 64
+#endif
+#ifndef CKV_T2_NS_PROD
+#define CKV_T2_NS_PROD 256
+#endif
+#ifndef CKV_T2_NS_EPI
+#define CKV_T2_NS_EPI 0
+#endif
+__device__ __forceinline__ void mb_wait_epi(uint64_t* b, uint32_t parity) {
+  if (CKV_T2_NS_EPI > 0) mb_wait_sleep<CKV_T2_NS_EPI>(b, parity); else mb_wait(b, parity);
+}
+__device__ __forceinline__ void mb_wait_mma(uint64_t* b, uint32_t parity) {
+  mb_wait_sleep<CKV_T2_NS_MMA>(b, parity);
+}
+__device__ __forceinline__ void mb_wait_prod(uint64_t* b, uint32_t parity) {
+  mb_wait_sleep<CKV_T2_NS_PROD>(b, parity);
+}
+// CKV_T2_PROF builds: cycles each role spends in its waits, summed over CTAs
+// ([0] producer a_empty, [1] MMA a_full, [2] MMA acc_empty, [3] epilogue
+// acc_full, [5] MMA b_full, [6] kernel cycles, [7] epilogue warp lifetime),
+// printed after every launch by t2_prof_dump()
+#ifdef CKV_T2_PROF
+__device__ unsigned long long g_t2prof[8];
+#define T2P_BEGIN(v) const long long v = clock64();
+#define T2P_END(v, slot) acc_[slot] += clock64() - v;
+#else
+#define T2P_BEGIN(v)
+#define T2P_END(v, slot)
+#endif
+
+// 10 warps: 3 share an SM sub-partition's 16K-register file, so <= 168 registers
+__global__ void __launch_bounds__(T2_THREADS, 1)
+k_assign_tc2(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap dmap,
+             TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sbase = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  const uint32_t S = a.stages;
+  uint8_t* sm_a = sbase;                         // [S][2][TC_M*128]
+  uint8_t* sm_b = sbase + S * TC_ABYTES;         // [2][rc*128]
+  __shared__ T2Bars sm;
+  auto A = [&](uint32_t st, uint32_t kh) { return sm_a + st * TC_ABYTES + kh * (TC_M * 128); };
+  auto Bp = [&](uint32_t kh, uint32_t row) { return sm_b + kh * (a.rc * 128) + row * 128; };
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
+#ifdef CKV_T2_PROF
+  unsigned long long acc_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long tk0_ = clock64();
+#endif
+  const uint32_t n_units = uint32_t(*a.n_list);
+  const uint32_t total = n_units * a.n_ranges * a.tiles_per_unit;
+  const bool summary = a.summ && a.n_ranges > 1;
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t w0 = min(total, blockIdx.x * per), w1 = min(total, w0 + per);
+  auto next_work = [&](TcWork& k) {
+    if (++k.tile == a.tiles_per_unit) {
+      k.tile = 0;
+      if (++k.range == a.n_ranges) { k.range = 0; ++k.ui; }
+    }
+  };
+
+  if (t == 0) {
+    for (uint32_t s = 0; s < S; ++s) { mb_init(&sm.a_full[s], 1); mb_init(&sm.a_empty[s], 1); }
+    mb_init(&sm.b_full, 1);
+    mb_init(&sm.b_empty, 1);
+    // one consuming warp per lane quarter per chunk
+    for (int s = 0; s < T2_NBUF; ++s) { mb_init(&sm.acc_full[s][0], 1); mb_init(&sm.acc_empty[s], 4); }
+    sm.fix_n = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (wid == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     su32(&sm.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (wid == 0) {
+    // ============================ TMA producer =================================
+    if (lane == 0 && w0 < w1) {
+      uint32_t st = 0, ph = 0, bswitch = 0;
+      unsigned long long cur_key = ~0ull;
+      TcWork k = tc_work(w0, a);
+      uint32_t unit = uint32_t(a.unit_list[k.ui]), cur_ui = k.ui;
+      for (uint32_t w = w0; w < w1; ++w) {
+        if (k.ui != cur_ui) { cur_ui = k.ui; unit = uint32_t(a.unit_list[k.ui]); }
+        const uint32_t cbeg = k.range * a.rc;
+        const unsigned long long key = (unsigned long long)unit << 32 | cbeg;
+        // the key tile first: at a B switch it streams in while the last
+        // MMAs on the old B drain
+        T2P_BEGIN(t0_) mb_wait_prod(&sm.a_empty[st], ph ^ 1); T2P_END(t0_, 0)
+        mb_expect(&sm.a_full[st], TC_ABYTES);
+        const int row = int(unit * a.key_rows_per_unit + k.tile * TC_M);
+        tma_2d(A(st, 0), &kmap, 0, row, &sm.a_full[st]);
+        tma_2d(A(st, 1), &kmap, TC_BK, row, &sm.a_full[st]);
+        if (key != cur_key) {
+          if (cur_key != ~0ull) mb_wait_prod(&sm.b_empty, (bswitch - 1) & 1);
+          const uint32_t cols = tc_cols(k.range, a);
+          mb_expect(&sm.b_full, cols * 128 * 2);
+          for (uint32_t r0 = 0; r0 < cols; r0 += TC_BOXR)
+            for (int kh = 0; kh < 2; ++kh)
+              tma_2d(Bp(kh, r0), &dmap, kh * TC_BK, int(unit * a.c_pad + cbeg + r0), &sm.b_full);
+          cur_key = key;
+          ++bswitch;
+        }
+        if (++st == S) { st = 0; ph ^= 1; }
+        next_work(k);
+      }
+    }
+  } else if (wid == 1) {
+    // ============================ MMA issuer ===================================
+    // Items alternate between the two epilogue groups (item parity) and group
+    // g owns TMEM buffer g.  Consecutive items on the same B are issued as a
+    // pair with their chunks interleaved (A_w, A_w+1, B_w, B_w+1, ...), so the
+    // tensor pipe works for one group while the other drains its buffer.
+    if (lane == 0 && w0 < w1) {
+      uint32_t st = 0, ph = 0, bswitch = 0, ue0 = 0, ue1 = 0;
+      unsigned long long cur_key = ~0ull;
+      TcWork k = tc_work(w0, a);
+      uint32_t unit = uint32_t(a.unit_list[k.ui]), cur_ui = k.ui;
+      auto key_of = [&](const TcWork& kw, uint32_t u) {
+        return (unsigned long long)u << 32 | (kw.range * a.rc);
+      };
+      for (uint32_t w = w0; w < w1;) {
+        if (k.ui != cur_ui) { cur_ui = k.ui; unit = uint32_t(a.unit_list[k.ui]); }
+        const unsigned long long key = key_of(k, unit);
+        TcWork k2 = k;
+        next_work(k2);
+        // the pair shares B: same unit and column range (a tile change only)
+        const bool pair = w + 1 < w1 && k2.tile != 0;
+        TcWork k3 = k2;
+        if (pair) next_work(k3);
+        const uint32_t nit = pair ? 2u : 1u;
+        // last items on this B: the item after them changes the range or unit
+        const bool last_b = w + nit >= w1 || (pair ? k3.tile == 0 : k2.tile == 0);
+        if (key != cur_key) {
+          T2P_BEGIN(t0_) mb_wait_mma(&sm.b_full, bswitch & 1); T2P_END(t0_, 5)
+          cur_key = key;
+          ++bswitch;
+        }
+        const uint32_t cols = tc_cols(k.range, a);
+        uint32_t stq[2];
+        for (uint32_t x = 0; x < nit; ++x) {
+          stq[x] = st;
+          T2P_BEGIN(t1_) mb_wait_mma(&sm.a_full[st], ph); T2P_END(t1_, 1)
+          if (++st == S) { st = 0; ph ^= 1; }
+        }
+        tc_fence_after();
+        for (uint32_t c0 = 0; c0 < cols; c0 += T2_CW) {
+          const uint32_t nc = min(uint32_t(T2_CW), cols - c0);
+          const uint32_t idesc = idesc_f16_f32(TC_M, nc);
+          for (uint32_t x = 0; x < nit; ++x) {
+            const uint32_t buf = (w + x - w0) & 1;
+            const uint32_t bph = ((buf ? ue1 : ue0) & 1) ^ 1;
+            if (buf) ++ue1; else ++ue0;
+            T2P_BEGIN(t2_) mb_wait_mma(&sm.acc_empty[buf], bph); T2P_END(t2_, 2)
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const int kh = kk >> 2, ko = (kk & 3) * 32;
+              const uint64_t ad = kmajor_sw128_desc(su32(A(stq[x], kh)) + ko);
+              const uint64_t bd = kmajor_sw128_desc(su32(Bp(kh, c0)) + ko);
+              umma_f16(tmem + buf * T2_CW, ad, bd, idesc, kk > 0 ? 1u : 0u);
+            }
+            umma_commit(&sm.acc_full[buf][0]);
+          }
+        }
+        for (uint32_t x = 0; x < nit; ++x) umma_commit(&sm.a_empty[stq[x]]);
+        if (last_b) umma_commit(&sm.b_empty);
+        w += nit;
+        k = pair ? k3 : k2;
+      }
+    }
+  } else {
+    // ============================ epilogue warps ===============================
+    const uint32_t quarter = wid & 3, grp = uint32_t(wid - 2) >> 2;
+    const uint32_t lane_row = quarter * 32 + lane;
+    const uint32_t tq = tmem + ((quarter * 32) << 16);
+    TcWork k = tc_work(w0, a);
+    uint32_t uses = 0;  // chunks of this group so far (acc_full phases of buffer grp)
+    uint32_t cur_ui = ~0u, unit = 0;
+    float eps = 0.f, kerr = 0.f;
+    if (grp == 1) next_work(k);  // this warp's first item
+    for (uint32_t w = w0 + grp; w < w1; w += T2_CG) {
+      const uint32_t cols = tc_cols(k.range, a);
+      const uint32_t nch = (cols + T2_CW - 1) / T2_CW;
+      if (k.ui != cur_ui) {
+        cur_ui = k.ui;
+        unit = uint32_t(a.unit_list[k.ui]);
+        eps = a.eps_u[unit];
+        kerr = a.kerr_u[unit];
+      }
+      const uint32_t row = k.tile * TC_M + lane_row, cbeg = k.range * a.rc, range = k.range;
+      // issued now, first used after the accumulator wait (which hides it);
+      // rows past n: a negative band admits no candidate (lo > block max)
+      const float kn = row < a.n ? __ldg(a.knorm + size_t(unit) * a.n + row) : -1.f;
+      float band = 0.f;
+      // two best entries {score, first column, in-band mask} and the largest
+      // score displaced from them
+      float e0s = -INFINITY, e1s = -INFINITY, dmax = -INFINITY;
+      uint32_t e0c = 0u, e0m = 0u, e1c = 0u, e1m = 0u;
+#pragma unroll 1
+      for (uint32_t ch = 0; ch < nch; ++ch) {
+        const uint32_t cc = ch * T2_CW;
+        const uint32_t nbk = min(uint32_t(T2_CW), cols - cc) / 32;
+        const uint32_t buf = grp, bph = uses++ & 1;
+        T2P_BEGIN(t0_) mb_wait_epi(&sm.acc_full[buf][0], bph); T2P_END(t0_, 3)
+        tc_fence_after();
+        if (ch == 0) band = kn < 0.f ? -1.f : tc_band(kn, eps, kerr);
+        if (a.mode == 2) {
+          __syncwarp();
+          if (lane == 0) mb_arrive(&sm.acc_empty[buf]);
+          continue;
+        }
+        const uint32_t taddr = tq + buf * T2_CW;
+#pragma unroll 1
+        for (uint32_t b0 = 0; b0 < nbk; b0 += T2_GB) {
+          // T2_GB blocks in registers at once; a slot past the chunk's last
+          // block re-reads it and is masked out, so the code is straight-line
+          // (no per-block branches: the blocks' chains interleave)
+          float v[T2_GB][32];
+#pragma unroll
+          for (int q = 0; q < T2_GB; ++q) tmem_ld32_nw(taddr + min(b0 + q, nbk - 1) * 32, v[q]);
+          tmem_wait();
+          if (b0 + T2_GB >= nbk) {  // the chunk's last group: buffer back to the MMA
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(&sm.acc_empty[buf]);
+          }
+          if (a.mode == 1) continue;
+          // block maxima (FMNMX3 trees), ONE threshold for the group:
+          // lo = max(running max, the group's maxima) - band <= M - band
+          float bmq[T2_GB];
+#pragma unroll
+          for (int q = 0; q < T2_GB; ++q) {
+            const float* x = v[q];
+            float t1[11];
+#pragma unroll
+            for (int y = 0; y < 10; ++y) t1[y] = max3f(x[3 * y], x[3 * y + 1], x[3 * y + 2]);
+            t1[10] = fmaxf(x[30], x[31]);
+            const float t2a = max3f(t1[0], t1[1], t1[2]), t2b = max3f(t1[3], t1[4], t1[5]);
+            const float t2c = max3f(t1[6], t1[7], t1[8]), t2d = fmaxf(t1[9], t1[10]);
+            bmq[q] = fmaxf(max3f(t2a, t2b, t2c), t2d);
+          }
+          const float lo = fmaxf(max3f(e0s, bmq[0], bmq[1]), max3f(bmq[2], bmq[3], -INFINITY)) - band;
+          uint32_t inq[T2_GB];
+#pragma unroll
+          for (int q = 0; q < T2_GB; ++q) {
+            inq[q] = ~below_mask32(v[q], lo);  // bit 31-x <=> v[x] >= lo
+            if (b0 + q >= nbk) inq[q] = 0u;
+          }
+          // branch-free pair update per block: entry {bm, first column, mask}
+#pragma unroll
+          for (int q = 0; q < T2_GB; ++q) {
+            const float bm = bmq[q];
+            const uint32_t in = inq[q], col = cbeg + cc + (b0 + q) * 32;
+            const bool p = in != 0u, gt1 = p && bm > e1s, gt0 = p && bm > e0s;
+            dmax = p ? fmaxf(dmax, gt1 ? e1s : bm) : dmax;
+            e1s = gt0 ? e0s : (gt1 ? bm : e1s);
+            e1c = gt0 ? e0c : (gt1 ? col : e1c);
+            e1m = gt0 ? e0m : (gt1 ? in : e1m);
+            e0s = gt0 ? bm : e0s;
+            e0c = gt0 ? col : e0c;
+            e0m = gt0 ? in : e0m;
+          }
+        }
+      }
+      // the row's decision: M = e0s; candidates = entries with score >= M - band
+      if (row < a.n && a.mode == 0) {
+        const float M = e0s, lo = M - band;
+        const bool u1 = e1s >= lo;
+        bool full = !(M > -INFINITY) || dmax >= lo;
+        const uint32_t nin = __popc(e0m) + (u1 ? __popc(e1m) : 0u);
+        if (e0c + 32 - __ffs(e0m) >= a.C) full = true;  // a padding column survived
+        if (u1 && e1c + 32 - __ffs(e1m) >= a.C) full = true;
+        auto emit = [&](auto&& put) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (e == 1 && !u1) break;
+            uint32_t m = e ? e1m : e0m;
+            const uint32_t c = e ? e1c : e0c;
+            while (m) {
+              const uint32_t jj = __clz(m);
+              m &= ~(0x80000000u >> jj);
+              put(c + jj);
+            }
+          }
+        };
+        if (summary) {
+          if (nin > 4u) full = true;
+          uint32_t i01 = 0u, i23 = 0u, k2 = 0;
+          if (!full)
+            emit([&](uint32_t c) {
+              if (k2 == 0) i01 |= c; else if (k2 == 1) i01 |= c << 16;
+              else if (k2 == 2) i23 |= c; else i23 |= c << 16;
+              ++k2;
+            });
+          a.summ[(size_t(unit) * a.n + row) * a.n_slots + range] =
+              make_float4(M, __uint_as_float(full ? TC_FULL : nin), __uint_as_float(i01),
+                          __uint_as_float(i23));
+        } else {
+          int32_t* lab = a.labels + size_t(unit) * a.label_stride + row;
+          if (nin > uint32_t(TC_NCAND)) full = true;
+          if (!full && nin == 1) {
+            *lab = int32_t(e0c + __clz(e0m));
+          } else {
+            *lab = -1;
+            const uint32_t slot = w0 * TC_M + atomicAdd(&sm.fix_n, 1u);
+            if (slot < a.fix_cap) {
+              a.fix_list[slot] = make_uint4(unit, row, full ? TC_FULL : nin, 0u);
+              if (!full) {
+                uint32_t* fi = a.fix_ids + size_t(slot) * TC_NCAND;
+                uint32_t k2 = 0;
+                emit([&](uint32_t c) { fi[k2++] = c; });
+              }
+            }
+          }
+        }
+      }
+      next_work(k);
+      next_work(k);
+    }
+  }
+#ifdef CKV_T2_PROF
+  if (lane == 0) {
+    if (wid >= 2) acc_[7] += clock64() - tk0_;
+    if (t == 0) acc_[6] += clock64() - tk0_;
+    for (int x = 0; x < 8; ++x) if (acc_[x]) atomicAdd(&g_t2prof[x], acc_[x]);
+  }
+#endif
+  __syncthreads();
+  if (t == 0) a.fix_count[blockIdx.x] = sm.fix_n;
+  if (wid == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // exact re-score of the fix-up keys (clustering.hpp:104-115: argmax of
 // dot_f64(key, dir_c), strict >, so ties go to the lowest id).
 // One warp per key; lane L holds dims 4L..4L+3.  Every candidate's score is
@@ -927,23 +1338,42 @@ size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
          align256(cap * D * 2) + summ;
 }
 
+#ifdef CKV_T2_PROF
+void t2_prof_dump() {
+  unsigned long long h[8];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, g_t2prof, sizeof(h));
+  fprintf(stderr, "[t2prof] kernel %.3g | prod a_empty %.3g | mma a_full %.3g acc_empty %.3g "
+          "b_full %.3g | epilogue acc_full %.3g of lifetime %.3g (cycles, summed over CTAs)\n",
+          double(h[6]), double(h[0]), double(h[1]), double(h[2]), double(h[5]), double(h[3]),
+          double(h[7]));
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_t2prof, z, sizeof(z));
+}
+#endif
+
 // k_assign_tc with as many key-tile stages as fit next to B (rc columns)
 static int launch_tc(cudaStream_t st, const CUtensorMap& kmap, const CUtensorMap& dmap,
                      TcArgs& ta) {
-  // opt-in per-CTA smem minus the kernel's static part, per device
-  static size_t max_dyn_dev[64];
+  // k_assign_tc2 (barrier-free epilogue) for the dense and range passes;
+  // k_assign_tc for the MCR work lists (CKV_TC_V1=1 forces it everywhere)
+  static const bool v1 = getenv("CKV_TC_V1") != nullptr;
+  const bool use2 = !ta.wlist && !v1;
+  const void* fn = use2 ? (const void*)k_assign_tc2 : (const void*)k_assign_tc;
+  // opt-in per-CTA smem minus the kernel's static part, per device and kernel
+  static size_t max_dyn_dev[2][64];
   int dev = 0;
   CKV_CUDA_TRY(cudaGetDevice(&dev));
-  size_t max_dyn = max_dyn_dev[dev & 63];
+  size_t max_dyn = max_dyn_dev[use2][dev & 63];
   if (max_dyn == 0) {
     int optin = 0;
     cudaFuncAttributes fa;
     CKV_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    CKV_CUDA_TRY(cudaFuncGetAttributes(&fa, k_assign_tc));
+    CKV_CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
     max_dyn = size_t(optin) - fa.sharedSizeBytes;
   }
-  CKV_CUDA_TRY(smem_optin((const void*)k_assign_tc, int(max_dyn)));
-  max_dyn_dev[dev & 63] = max_dyn;
+  CKV_CUDA_TRY(smem_optin(fn, int(max_dyn)));
+  max_dyn_dev[use2][dev & 63] = max_dyn;
   static const uint32_t tc_mode = getenv("CKV_TC_MODE") ? uint32_t(atoi(getenv("CKV_TC_MODE"))) : 0u;
   ta.mode = tc_mode;
   const size_t fixed = 1024 + 2 * size_t(ta.rc) * 128;
@@ -953,8 +1383,16 @@ static int launch_tc(cudaStream_t st, const CUtensorMap& kmap, const CUtensorMap
     return CKV_EINVAL;
   }
   const size_t smem = fixed + size_t(ta.stages) * TC_ABYTES;
-  k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
-  CKV_LAUNCH_CHECK("k_assign_tc");
+  if (use2) {
+    k_assign_tc2<<<num_sms(), T2_THREADS, smem, st>>>(kmap, dmap, ta);
+    CKV_LAUNCH_CHECK("k_assign_tc2");
+#ifdef CKV_T2_PROF
+    t2_prof_dump();
+#endif
+  } else {
+    k_assign_tc<<<num_sms(), TC_THREADS, smem, st>>>(kmap, dmap, ta);
+    CKV_LAUNCH_CHECK("k_assign_tc");
+  }
   return CKV_OK;
 }
 
