@@ -172,8 +172,10 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
   __syncthreads();
   // launched with programmatic stream serialization: the CTAs start (and set
   // up their barriers) while the selection kernel drains; its run lists and
-  // token counts are read only after this wait (a no-op otherwise)
+  // token counts are read only after this wait (a no-op otherwise).  The next
+  // kernel may launch now: it waits for this grid before its dependent reads.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (wid == AT_CWARPS) {
     // ======================= producer warp =====================================

@@ -450,10 +450,16 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   const uint32_t U = a.n_units;
   const size_t per_unit = assign_tc_scratch_bytes(1, a.n, a.C) + size_t(a.label_stride) * 16 +
                           size_t(a.c_stride) * D * 24;
+  // the budget is at least 16 GiB: only a call that needs more asks the
+  // driver for the free memory (cudaMemGetInfo measured 5-9 ms on some calls,
+  // the prefill's largest source of call-to-call jitter)
+  const size_t floor_b = size_t(16) << 30;
   size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
-  trace_mark("memgetinfo");
-  const size_t budget = std::max<size_t>(size_t(16) << 30, free_b / 10 * 6);
+  if (size_t(U) * per_unit > floor_b) {
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+    trace_mark("memgetinfo");
+  }
+  const size_t budget = std::max<size_t>(floor_b, free_b / 10 * 6);
   const uint32_t ub = uint32_t(std::max<size_t>(1, std::min<size_t>(U, budget / per_unit)));
   if (ub >= U) return kmeans_run_units(ctx, a, info_host, objective_host, repair_host);
   const size_t MI1 = size_t(a.max_iters) + 1;

@@ -72,6 +72,10 @@ k_score_approx(const float* __restrict__ q, const float* __restrict__ cents,
   const uint32_t unit = blockIdx.x;
   const int lane = lane_id();
   const uint32_t c0 = (blockIdx.y * SC_WARPS + warp_id()) * SC_ROWS;
+  // programmatic launch (layer mode): everything read here may come from the
+  // previous kernels; the selection kernel may start its own prologue now
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t C = n_clusters[unit];
   if (c0 >= C) return;
   const float* cu = cents + size_t(unit) * c_cap * D;
@@ -153,9 +157,42 @@ __device__ __forceinline__ void dbg_stamp(uint32_t h, int slot) {
 #endif
 }
 
+// The cache state of head h, loaded once up front so the lookups and the
+// update need no dependent global round trips: lane w < words holds word w of
+// every retained bitmap (R <= 4; more retention reads global memory), lane
+// j < 4 holds counter j.
+struct SelCachePre {
+  uint32_t cbits[4];
+  uint32_t rhead, rlen;
+  unsigned long long ctr;
+  bool creg;
+};
+__device__ __forceinline__ SelCachePre cache_prefetch(uint32_t h, const CacheDev& cache) {
+  SelCachePre p{{0u, 0u, 0u, 0u}, 0u, 0u, 0ull, false};
+  if (!cache.bits) return p;
+  const int lane = lane_id();
+  p.creg = cache.retention <= 4 && cache.words <= 32;
+  const uint32_t* bits = cache.bits + size_t(h) * cache.retention * cache.words;
+  if (p.creg && uint32_t(lane) < cache.words)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (uint32_t(k) < cache.retention) p.cbits[k] = bits[size_t(k) * cache.words + lane];
+  p.rhead = cache.ring[size_t(h) * 2];
+  p.rlen = cache.ring[size_t(h) * 2 + 1];
+  if (lane < 4) p.ctr = cache.counters[size_t(h) * 4 + lane];
+  return p;
+}
+
 // The selection of one q head h by one warp.  av / ae: the head's approximate
 // scores and their bounds (global scratch after K1, or shared memory in the
 // fused kernel); wbase: the warp's private smem (warp_bytes).
+// SM_META: sizes / starts point at the unit's shared-memory copies (the
+// fused kernel stages them while it scores), else at global memory.
+template <bool SM_META>
+__device__ __forceinline__ uint32_t meta_ld(const uint32_t* p) {
+  if constexpr (SM_META) return *p; else return __ldg(p);
+}
+template <bool SM_META>
 __device__ __forceinline__ void select_head(
     uint32_t h, const ckv_select_desc& desc, uint32_t p2, uint32_t row_base,
     const float* __restrict__ q, const float* __restrict__ cents, const float* av,
@@ -164,7 +201,8 @@ __device__ __forceinline__ void select_head(
     uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, const ckv_runs& runs,
     uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
     uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
-    double* __restrict__ scores_out, const CacheDev& cache, unsigned char* wbase, WarpSel& ws) {
+    double* __restrict__ scores_out, const CacheDev& cache, const SelCachePre& cpre,
+    unsigned char* wbase, WarpSel& ws) {
   const int lane = lane_id();
   dbg_stamp(h, 0);
   const uint32_t unit = h / desc.group;
@@ -176,8 +214,8 @@ __device__ __forceinline__ void select_head(
   float (*stage)[D] = reinterpret_cast<float (*)[D]>(wbase);                 // [SW_STAGE][D]
 
   const float* cu = cents + size_t(unit) * desc.c_cap * D;
-  const uint32_t* sz = sizes + size_t(unit) * desc.c_cap;
-  const uint32_t* stt = starts + size_t(unit) * (desc.c_cap + 1);
+  const uint32_t* sz = SM_META ? sizes : sizes + size_t(unit) * desc.c_cap;
+  const uint32_t* stt = SM_META ? starts : starts + size_t(unit) * (desc.c_cap + 1);
   const float4* qh4 = reinterpret_cast<const float4*>(q + size_t(h) * D);
   const bool exhaustive_req = (desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) != 0;
   // budget 0 takes no cluster (selection.hpp:91: the loop breaks at once);
@@ -185,80 +223,116 @@ __device__ __forceinline__ void select_head(
   bool fast = !exhaustive_req && C <= 32u * SW_KPL && B > 0;
   uint32_t taken = 0;
 
+  // cluster starts of this lane's 16 columns (runs output; fast path only)
+  uint32_t str[SW_KPL];
+  const bool creg = cpre.creg;
+  uint32_t rhead = cpre.rhead, rlen = cpre.rlen;
+  const bool have_str = fast;  // str[] filled below
   if (fast) {
-    // ---- 1. approximate pops ------------------------------------------------
-    unsigned long long kr[SW_KPL];
+    // ---- 1. a set U of top clusters whose sizes reach B ----------------------
+    // Any U with total size >= B gives a valid L = min_U (a - E) (step 2), so
+    // U need not be the minimal prefix: a 64-bin histogram of the approximate
+    // scores over [min, max] (one pass, a second one inside the boundary bin
+    // when it holds many clusters) replaces an exact size-weighted select.
+    float ar[SW_KPL], er[SW_KPL];
     uint32_t szr[SW_KPL];
-    float er[SW_KPL];
     bool bad = false;  // non-finite scores (NaN centroids): exhaustive path
+    float amax = -INFINITY, amin = INFINITY;
+    uint32_t total = 0;
 #pragma unroll
     for (int k = 0; k < SW_KPL; ++k) {
       const uint32_t c = lane + 32 * k;
-      const float a = c < C ? av[c] : 0.f;
-      er[k] = c < C ? ae[c] : 0.f;
-      kr[k] = c < C ? ((unsigned long long)fkey(a) << 32) | (0xffffffffu - c) : 0ull;
-      szr[k] = c < C ? __ldg(sz + c) : 0u;
-      bad |= c < C && !(isfinite(a) && isfinite(er[k]));
+      const bool v = c < C;
+      ar[k] = v ? av[c] : 0.f;
+      er[k] = v ? ae[c] : 0.f;
+      szr[k] = v ? meta_ld<SM_META>(sz + c) : 0u;
+      str[k] = v ? meta_ld<SM_META>(stt + c) : 0u;
+      bad |= v && !(isfinite(ar[k]) && isfinite(er[k]));
+      if (v) { amax = fmaxf(amax, ar[k]); amin = fminf(amin, ar[k]); }
+      total += szr[k];
     }
-    // size-weighted radix select on the fp32 keys: tau = the largest key with
-    // sum_{key >= tau} size >= B (U = {key >= tau}); all of C when the total
-    // labeled size is below B.  Four 8-bit passes over warp-private bins.
-    uint32_t* hist = ws.hist;
-    uint32_t prefix = 0, above = 0;
-    uint32_t total = 0;
-#pragma unroll
-    for (int k = 0; k < SW_KPL; ++k) total += szr[k];
     total = __reduce_add_sync(0xffffffffu, total);
-    uint32_t tau = 0;
-    if (total > B) {
-      for (int pass = 0; pass < 4; ++pass) {
-        const int sh = 24 - 8 * pass;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < SW_KPL; ++k) {
-          const uint32_t key = uint32_t(kr[k] >> 32);
-          const bool match = pass == 0 || (key >> (sh + 8)) == (prefix >> (sh + 8));
-          if (szr[k] && match) atomicAdd(&hist[(key >> sh) & 255u], szr[k]);
-        }
-        __syncwarp();
-        uint32_t loc[8], lsum = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) { loc[i] = hist[lane * 8 + i]; lsum += loc[i]; }
-        // suffix sum over lanes above me
-        uint32_t suf = lsum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_down_sync(0xffffffffu, suf, o);
-          if (lane + o < 32) suf += y;
-        }
-        uint32_t run = above + suf - lsum;  // weight of bins above my 8
-        int dsel = -1;
-        uint32_t above_sel = 0;
-#pragma unroll
-        for (int i = 7; i >= 0; --i) {
-          if (dsel < 0 && run + loc[i] >= B) { dsel = lane * 8 + i; above_sel = run; }
-          run += loc[i];
-        }
-        // the highest digit reaching B: the highest lane that found one
-        const unsigned found = __ballot_sync(0xffffffffu, dsel >= 0);
-        const int src = 31 - __clz(found);
-        const int d = __shfl_sync(0xffffffffu, dsel, src);
-        above = __shfl_sync(0xffffffffu, above_sel, src);
-        prefix |= uint32_t(d) << sh;
-        __syncwarp();
-      }
-      tau = prefix;
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, o));
     }
     fast = !__any_sync(0xffffffffu, bad);
+    dbg_stamp(h, 4);
+    // membership code per column: bin (0..63) in pass 1; 64 + sub-bin (0..63)
+    // for the boundary bin after pass 2; members: code >= cut
+    uint32_t code[SW_KPL];
+    uint32_t cut = 0;  // everyone (total <= B, or all scores equal)
+    uint32_t* hist = ws.hist;
+    // weighted histogram of codes[k] in [base, base + 64) -> the highest bin
+    // whose suffix weight (plus `above`) reaches B
+    auto pick = [&](uint32_t base, uint32_t above) -> uint32_t {
+      hist[2 * lane] = 0u;
+      hist[2 * lane + 1] = 0u;
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < SW_KPL; ++k)
+        if (szr[k] && code[k] >= base && code[k] < base + 64u) atomicAdd(&hist[code[k] - base], szr[k]);
+      __syncwarp();
+      const uint32_t h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
+      uint32_t suf = h0 + h1;  // suffix over lanes >= mine
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, suf, o);
+        if (lane + o < 32) suf += y;
+      }
+      suf += above;
+      const int my = (suf - h0 >= B) ? 2 * lane + 1 : (suf >= B ? 2 * lane : -1);
+      const unsigned f = __ballot_sync(0xffffffffu, my >= 0);
+      __syncwarp();
+      return f ? base + uint32_t(__shfl_sync(0xffffffffu, my, 31 - __clz(f))) : base;
+    };
+    if (fast && total > B && amax > amin) {
+      const float inv = 64.f / (amax - amin);
+#pragma unroll
+      for (int k = 0; k < SW_KPL; ++k)
+        code[k] = lane + 32 * k < C ? min(63u, uint32_t((ar[k] - amin) * inv)) : 0u;
+      const uint32_t b1 = pick(0u, 0u);
+      dbg_stamp(h, 5);
+      // the boundary bin's population and the weight strictly above it
+      uint32_t n_at = 0, above = 0;
+      float lo2 = INFINITY, hi2 = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < SW_KPL; ++k) {
+        const bool v = lane + 32 * k < C;
+        if (v && code[k] == b1) { ++n_at; lo2 = fminf(lo2, ar[k]); hi2 = fmaxf(hi2, ar[k]); }
+        if (v && code[k] > b1) above += szr[k];
+      }
+      n_at = __reduce_add_sync(0xffffffffu, n_at);
+      above = __reduce_add_sync(0xffffffffu, above);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo2 = fminf(lo2, __shfl_xor_sync(0xffffffffu, lo2, o));
+        hi2 = fmaxf(hi2, __shfl_xor_sync(0xffffffffu, hi2, o));
+      }
+      cut = b1;
+      if (n_at > 8u && hi2 > lo2) {  // pass 2 inside the boundary bin
+        const float inv2 = 64.f / (hi2 - lo2);
+#pragma unroll
+        for (int k = 0; k < SW_KPL; ++k) {
+          const bool v = lane + 32 * k < C;
+          code[k] = !v ? 0u : code[k] > b1 ? 128u
+                  : code[k] == b1 ? 64u + min(63u, uint32_t((ar[k] - lo2) * inv2)) : 0u;
+        }
+        cut = pick(64u, above);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < SW_KPL; ++k) code[k] = 0u;
+    }
+    dbg_stamp(h, 6);
     if (fast) {
-      // L = min over U = {key >= tau} of (a - E)
+      // L = min over U of (a - E)
       float lower = INFINITY;
 #pragma unroll
       for (int k = 0; k < SW_KPL; ++k) {
         const uint32_t c = lane + 32 * k;
-        if (c < C && uint32_t(kr[k] >> 32) >= tau) lower = fminf(lower, av[c] - er[k]);
+        if (c < C && code[k] >= cut) lower = fminf(lower, ar[k] - er[k]);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) lower = fminf(lower, __shfl_xor_sync(0xffffffffu, lower, o));
@@ -268,7 +342,7 @@ __device__ __forceinline__ void select_head(
       for (int k = 0; k < SW_KPL; ++k) {
         const uint32_t c = lane + 32 * k;
         bool in = false;
-        if (c < C) in = av[c] + er[k] >= lower;
+        if (c < C) in = ar[k] + er[k] >= lower;
         const unsigned bal = __ballot_sync(0xffffffffu, in);
         const uint32_t pos = nc + __popc(bal & ((1u << lane) - 1u));
         if (in && pos < uint32_t(SW_MAXCAND)) ws.cand[pos] = c;
@@ -315,7 +389,7 @@ __device__ __forceinline__ void select_head(
         taken = nc;
         for (uint32_t b = 0; b < nc; b += 32) {
           const uint32_t i = b + lane;
-          uint32_t x = i < nc ? __ldg(sz + ids[i]) : 0u;
+          uint32_t x = i < nc ? meta_ld<SM_META>(sz + ids[i]) : 0u;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -374,7 +448,7 @@ __device__ __forceinline__ void select_head(
     taken = C;
     for (uint32_t b = 0; b < C; b += 32) {
       const uint32_t i = b + lane;
-      uint32_t x = i < C ? __ldg(sz + ids[i]) : 0u;
+      uint32_t x = i < C ? meta_ld<SM_META>(sz + ids[i]) : 0u;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -402,12 +476,33 @@ __device__ __forceinline__ void select_head(
   const uint32_t nrec = desc.rec_end > desc.rec_begin ? desc.rec_end - desc.rec_begin : 0;
   const uint32_t n = cum + sinks + nrec;
   // runs: one per taken cluster, then sinks, then recency (selection.hpp:91-109)
+  // the start row of cluster c from this warp's registers (lane c % 32 holds
+  // str[c / 32]); every lane calls it (shuffles), c ignored when !valid
+  auto start_of = [&](uint32_t c, bool valid) -> uint32_t {
+    uint32_t v = 0u;
+    const uint32_t src = c & 31u, kk = c >> 5;
+#pragma unroll
+    for (int k = 0; k < SW_KPL; ++k) {
+      const uint32_t t2 = __shfl_sync(0xffffffffu, str[k], src);
+      if (valid && uint32_t(k) == kk) v = t2;
+    }
+    return v;
+  };
   if (runs.row) {
     uint32_t* rr = runs.row + size_t(h) * runs.run_cap;
     uint32_t* ro = runs.off + size_t(h) * (runs.run_cap + 1);
-    for (uint32_t i = lane; i < taken; i += 32) {
-      rr[i] = row_base + __ldg(stt + ids[i]);
-      ro[i] = i ? incl[i - 1] : 0u;
+    if (have_str) {
+      for (uint32_t i0 = 0; i0 < taken; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const bool v = i < taken;
+        const uint32_t st0 = start_of(v ? ids[i] : 0u, v);
+        if (v) { rr[i] = row_base + st0; ro[i] = i ? incl[i - 1] : 0u; }
+      }
+    } else {
+      for (uint32_t i = lane; i < taken; i += 32) {
+        rr[i] = row_base + meta_ld<SM_META>(stt + ids[i]);
+        ro[i] = i ? incl[i - 1] : 0u;
+      }
     }
     if (lane == 0) {
       uint32_t nr = taken;
@@ -433,7 +528,7 @@ __device__ __forceinline__ void select_head(
           if (incl[mid] > e) hi = mid; else lo = mid + 1;
         }
         const uint32_t before = lo ? incl[lo - 1] : 0;
-        src[k] = (e < cum && lo < taken) ? __ldg(stt + ids[lo]) + (e - before) : 0u;
+        src[k] = (e < cum && lo < taken) ? meta_ld<SM_META>(stt + ids[lo]) + (e - before) : 0u;
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -464,37 +559,61 @@ __device__ __forceinline__ void select_head(
     trimmed_out[h] = trimmed;
   }
   // ---- cache (cache.hpp:38-57) -------------------------------------------------
+  // lookup of the taken clusters in the R retained bitmaps, then the taken
+  // set replaces the oldest slot (the ring was prefetched with the bitmaps)
   if (cache.bits) {
     const uint32_t W = cache.words, R = cache.retention;
     uint32_t* bits = cache.bits + size_t(h) * R * W;
-    uint32_t* ring = cache.ring + size_t(h) * 2;
-    uint32_t rhead = ring[0], rlen = ring[1];
     uint32_t hits = 0;
     unsigned long long miss_tokens = 0;
-    for (uint32_t i = lane; i < taken; i += 32) {
-      const uint32_t c = ids[i];
-      bool res = false;
-      for (uint32_t k = 0; k < R; ++k) res |= (bits[size_t(k) * W + (c >> 5)] >> (c & 31)) & 1u;
-      if (res) ++hits; else miss_tokens += sz[c];
-    }
-    hits = __reduce_add_sync(0xffffffffu, hits);
-    miss_tokens = warp_sum(miss_tokens);
     uint32_t slot;
     if (rlen < R) { slot = (rhead + rlen) % R; rlen++; }
     else { slot = rhead; rhead = (rhead + 1) % R; }
-    __syncwarp();
-    uint32_t* sb = bits + size_t(slot) * W;
-    for (uint32_t i = lane; i < W; i += 32) sb[i] = 0u;
-    __syncwarp();
-    for (uint32_t i = lane; i < taken; i += 32) atomicOr(&sb[ids[i] >> 5], 1u << (ids[i] & 31));
+    if (creg) {
+      uint32_t nw = 0u;  // lane w < W: the new bitmap's word w
+      for (uint32_t i0 = 0; i0 < taken; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const bool v = i < taken;
+        const uint32_t c = v ? ids[i] : 0u;
+        bool res = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t wk = __shfl_sync(0xffffffffu, cpre.cbits[k], (c >> 5) & 31u);
+          res |= uint32_t(k) < R && ((wk >> (c & 31u)) & 1u);
+        }
+        if (v) { if (res) ++hits; else miss_tokens += meta_ld<SM_META>(sz + c); }
+        for (uint32_t w = 0; w < W; ++w) {
+          const uint32_t mw = __reduce_or_sync(0xffffffffu, (v && (c >> 5) == w) ? 1u << (c & 31u) : 0u);
+          if (uint32_t(lane) == w) nw |= mw;
+        }
+      }
+      if (uint32_t(lane) < W) bits[size_t(slot) * W + lane] = nw;
+    } else {
+      for (uint32_t i = lane; i < taken; i += 32) {
+        const uint32_t c = ids[i];
+        bool res = false;
+        for (uint32_t k = 0; k < R; ++k) res |= (bits[size_t(k) * W + (c >> 5)] >> (c & 31)) & 1u;
+        if (res) ++hits; else miss_tokens += sz[c];
+      }
+      __syncwarp();
+      uint32_t* sb = bits + size_t(slot) * W;
+      for (uint32_t i = lane; i < W; i += 32) sb[i] = 0u;
+      __syncwarp();
+      for (uint32_t i = lane; i < taken; i += 32) atomicOr(&sb[ids[i] >> 5], 1u << (ids[i] & 31));
+    }
+    hits = __reduce_add_sync(0xffffffffu, hits);
+    miss_tokens = warp_sum(miss_tokens);
+    // lane j < 4 holds counter j (prefetched): taken, hits, miss tokens, bytes
+    unsigned long long cv = cpre.ctr;
+    if (lane == 0) cv += taken;
+    if (lane == 1) cv += hits;
+    if (lane == 2) cv += miss_tokens;
+    const unsigned long long c2 = __shfl_sync(0xffffffffu, cv, 2);
+    if (lane == 3) cv = c2 * 2ull * cache.d * 4ull;
+    if (lane < 4) cache.counters[size_t(h) * 4 + lane] = cv;
     if (lane == 0) {
-      ring[0] = rhead;
-      ring[1] = rlen;
-      unsigned long long* ctr = cache.counters + size_t(h) * 4;
-      ctr[0] += taken;
-      ctr[1] += hits;
-      ctr[2] += miss_tokens;
-      ctr[3] = ctr[2] * 2ull * cache.d * 4ull;
+      cache.ring[size_t(h) * 2] = rhead;
+      cache.ring[size_t(h) * 2 + 1] = rlen;
     }
   }
   dbg_stamp(h, 3);
@@ -515,10 +634,14 @@ k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_ba
   if (h >= desc.n_q) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ WarpSel wsa[SW_WARPS];
-  select_head(h, desc, p2, row_base, q, cents, aval + size_t(h) * c_pad,
-              aerr + size_t(h) * c_pad, n_clusters, sizes, starts, sorted_ids, token_ids,
-              rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, scores_out, cache,
-              smraw + size_t(wid) * warp_bytes, wsa[wid]);
+  // the cache state is not written by K1: fetched before waiting for it
+  const SelCachePre cpre = cache_prefetch(h, cache);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  select_head<false>(h, desc, p2, row_base, q, cents, aval + size_t(h) * c_pad,
+                     aerr + size_t(h) * c_pad, n_clusters, sizes, starts, sorted_ids, token_ids,
+                     rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, scores_out,
+                     cache, cpre, smraw + size_t(wid) * warp_bytes, wsa[wid]);
 }
 
 // ---------------------------------------------------------------------------
@@ -532,7 +655,7 @@ k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_ba
 constexpr int SF_WARPS = 8;
 
 template <int G>
-__global__ void __launch_bounds__(SF_WARPS * 32)
+__global__ void __launch_bounds__(SF_WARPS * 32, 2)  // two units per SM: one wave at config B
 k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_base,
                const float* __restrict__ q, const float* __restrict__ cents,
                const uint32_t* __restrict__ n_clusters, const uint32_t* __restrict__ sizes,
@@ -553,7 +676,24 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   asm volatile("griddepcontrol.wait;" ::: "memory");
   float* av_s = reinterpret_cast<float*>(smraw + size_t(G) * warp_bytes);  // [G][c_pad]
   float* ae_s = av_s + size_t(G) * c_pad;                                  // [G][c_pad]
+  uint32_t* sz_s = reinterpret_cast<uint32_t*>(ae_s + size_t(G) * c_pad);  // [c_pad]
+  uint32_t* st_s = sz_s + c_pad;                                           // [c_pad]
   const uint32_t C = n_clusters[unit];
+  // the unit's sizes / starts land in shared memory while the warps score
+  // (4-byte cp.async: the per-unit arrays are not 16-byte aligned)
+  {
+    const uint32_t* szg = sizes + size_t(unit) * desc.c_cap;
+    const uint32_t* stg = starts + size_t(unit) * (desc.c_cap + 1);
+    for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(sz_s + c))), "l"(szg + c));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(st_s + c))), "l"(stg + c));
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  SelCachePre cpre{{0u, 0u, 0u, 0u}, 0u, 0u, 0ull, false};
+  if (wid < G && mode != 1) cpre = cache_prefetch(unit * G + wid, cache);
   const float* qu = q + size_t(unit) * G * D;
   // 8 lanes per centroid row (lane sub holds float4 columns sub, sub+8, +16,
   // +24: 128 contiguous bytes per row per load), 4 rows per warp step
@@ -621,13 +761,14 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
       }
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   if (wid >= G || mode == 1) return;
   const uint32_t h = unit * G + wid;
-  select_head(h, desc, p2, row_base, q, cents, av_s + size_t(wid) * c_pad,
-              ae_s + size_t(wid) * c_pad, n_clusters, sizes, starts, sorted_ids, token_ids,
-              rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, nullptr, cache,
-              smraw + size_t(wid) * warp_bytes, wsa[wid]);
+  select_head<true>(h, desc, p2, row_base, q, cents, av_s + size_t(wid) * c_pad,
+                    ae_s + size_t(wid) * c_pad, n_clusters, sz_s, st_s, sorted_ids, token_ids,
+                    rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, nullptr, cache,
+                    cpre, smraw + size_t(wid) * warp_bytes, wsa[wid]);
 }
 
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap) {
@@ -645,8 +786,18 @@ static void dbg_report(uint32_t n, const unsigned long long* dbuf, float k1_ms, 
     if (x[1]) { ph[0] += double(x[1] - x[0]); ph[1] += double(x[2] - x[1]); ++nfast; }
     ph[2] += double(x[3] - x[2]);
   }
-  fprintf(stderr, "[k_select dbg] K1 %.1f us K2 %.1f us | K2 per-warp us: pop %.2f exact %.2f "
-          "out %.2f | fast %u/%u\n", k1_ms * 1e3, k2_ms * 1e3, nfast ? ph[0] / nfast * 1e-3 : 0,
+  double q[3] = {0, 0, 0};  // loads, pass 1, pass 2 (fast heads)
+  for (uint32_t b = 0; b < n; ++b) {
+    const unsigned long long* x = &hb[size_t(b) * 8];
+    if (x[1] && x[4] && x[6]) {
+      q[0] += double(x[4] - x[0]);
+      if (x[5]) { q[1] += double(x[5] - x[4]); q[2] += double(x[6] - x[5]); }
+    }
+  }
+  fprintf(stderr, "[k_select dbg] K1 %.1f us K2 %.1f us | K2 per-warp us: pop %.2f (loads %.2f "
+          "pass1 %.2f pass2 %.2f) exact %.2f out %.2f | fast %u/%u\n", k1_ms * 1e3, k2_ms * 1e3,
+          nfast ? ph[0] / nfast * 1e-3 : 0, nfast ? q[0] / nfast * 1e-3 : 0,
+          nfast ? q[1] / nfast * 1e-3 : 0, nfast ? q[2] / nfast * 1e-3 : 0,
           nfast ? ph[1] / nfast * 1e-3 : 0, ph[2] / n * 1e-3, nfast, n);
 }
 
@@ -697,7 +848,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   static const bool unfused = getenv("CKV_SELECT_UNFUSED") != nullptr;
   const bool few_units = units * 2 < uint32_t(num_sms());
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused && !few_units) {
-    const size_t smem_f = size_t(G) * warp_bytes + size_t(G) * c_pad * 8;
+    const size_t smem_f = size_t(G) * warp_bytes + size_t(G) * c_pad * 8 + size_t(c_pad) * 8;
     if (smem_f <= 200 * 1024) {
       for (const void* fn : {(const void*)k_select_fused<1>, (const void*)k_select_fused<2>,
                              (const void*)k_select_fused<4>, (const void*)k_select_fused<8>})
@@ -755,11 +906,21 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   }
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES))) {
     const dim3 g1(units, (c_pad + SC_WARPS * SC_ROWS - 1) / (SC_WARPS * SC_ROWS));
+    cudaLaunchConfig_t c1 = {};
+    c1.gridDim = g1;
+    c1.blockDim = dim3(SC_WARPS * 32);
+    c1.stream = st;
+    cudaLaunchAttribute a1[1];
+    a1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a1[0].val.programmaticStreamSerializationAllowed = 1;
+    c1.attrs = a1;
+    c1.numAttrs = 1;
+    const uint32_t cc = desc.c_cap;
     switch (G) {
-      case 1: k_score_approx<1><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, aval, aerr); break;
-      case 2: k_score_approx<2><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, aval, aerr); break;
-      case 4: k_score_approx<4><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, aval, aerr); break;
-      default: k_score_approx<8><<<g1, SC_WARPS * 32, 0, st>>>(q, cents, n_clusters, desc.c_cap, c_pad, aval, aerr); break;
+      case 1: CKV_CUDA_TRY(cudaLaunchKernelEx(&c1, k_score_approx<1>, q, cents, n_clusters, cc, c_pad, aval, aerr)); break;
+      case 2: CKV_CUDA_TRY(cudaLaunchKernelEx(&c1, k_score_approx<2>, q, cents, n_clusters, cc, c_pad, aval, aerr)); break;
+      case 4: CKV_CUDA_TRY(cudaLaunchKernelEx(&c1, k_score_approx<4>, q, cents, n_clusters, cc, c_pad, aval, aerr)); break;
+      default: CKV_CUDA_TRY(cudaLaunchKernelEx(&c1, k_score_approx<8>, q, cents, n_clusters, cc, c_pad, aval, aerr)); break;
     }
     CKV_LAUNCH_CHECK("k_score_approx");
   }
@@ -776,9 +937,22 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
     cudaMemset(dbuf, 0, size_t(desc.n_q) * 64);
     cudaMemcpyToSymbol(g_sel_dbg, &dbuf, sizeof(dbuf));
   }
-  k_select_warp<<<(desc.n_q + SW_WARPS - 1) / SW_WARPS, SW_WARPS * 32, smem, st>>>(
-      desc, p2, c_pad, row_base, q, cents, aval, aerr, n_clusters, sizes, starts, sorted_ids,
-      token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, scores, cache, warp_bytes);
+  {
+    cudaLaunchConfig_t c2 = {};
+    c2.gridDim = dim3((desc.n_q + SW_WARPS - 1) / SW_WARPS);
+    c2.blockDim = dim3(SW_WARPS * 32);
+    c2.dynamicSmemBytes = smem;
+    c2.stream = st;
+    cudaLaunchAttribute a2[1];
+    a2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a2[0].val.programmaticStreamSerializationAllowed = 1;
+    c2.attrs = a2;
+    c2.numAttrs = 1;
+    CKV_CUDA_TRY(cudaLaunchKernelEx(&c2, k_select_warp, desc, p2, c_pad, row_base, q, cents,
+                                    static_cast<const float*>(aval), static_cast<const float*>(aerr),
+                                    n_clusters, sizes, starts, sorted_ids, token_ids, rows, runs,
+                                    n_tokens, n_taken, trimmed, ranked, scores, cache, warp_bytes));
+  }
   CKV_LAUNCH_CHECK("k_select_warp");
   if (dbg) {
     cudaEventRecord(ev[2], st);
