@@ -102,6 +102,16 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def soak_for(torch, fn, seconds: float) -> None:
+    """Keeps the GPU busy for `seconds` (untimed) so the clock sampler sees
+    loaded clocks before a short timed region starts."""
+    t_end = time.time() + seconds
+    while time.time() < t_end:
+        for _ in range(10):
+            fn()
+        torch.cuda.synchronize()
+
+
 # --------------------------------------------------------------------------
 # synthetic inputs on device (distributions of trace.hpp:134-198)
 # --------------------------------------------------------------------------
@@ -534,6 +544,8 @@ def run_config_C(args, rank, world, torch, dev, ctx, hbm):
         import torch.distributed as dist
         dist.barrier()
     with ClockSampler(int(str(dev).split(":")[-1])) as clk:
+        soak_out = torch.empty_like(out)
+        soak_for(torch, lambda: sess.attend_only(q_all[0], soak_out), 0.4)
         e[0].record()
         for _ in range(args.steps):
             sess.step(q_all[t], kn_all[t], vn_all[t], out)
@@ -620,14 +632,29 @@ def run_config_E(args, rank, world, torch, dev, ctx, hbm):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+    # the sharded k-means through the native C++ driver (ckv_kmeans_sharded,
+    # NCCL collectives; rank 0's NCCL id reaches the others over the process
+    # group) — CKV_E_PY=1 runs sharded.py's torch.distributed host instead
+    native = os.environ.get("CKV_E_PY") is None
+    if native:
+        from paper_2412_03213_b200.sharded import NativeComm, kmeans_cosine_native
+        nid = [NativeComm.nccl_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(nid, src=0)
+        ncomm = NativeComm(ctx, world, rank, nccl_id=nid[0])
     e = _events(torch, 2)
     e[0].record()
-    shard = DeviceShard(K[:, sink_rows:], C0, ctx=ctx)
-    km = kmeans_cosine_sharded(shard, N, lo, seeds=seeds, comm=comm)
+    if native:
+        km = kmeans_cosine_native(K[:, sink_rows:], C0, N, lo, ncomm, seeds=seeds)
+    else:
+        shard = DeviceShard(K[:, sink_rows:], C0, ctx=ctx)
+        km = kmeans_cosine_sharded(shard, N, lo, seeds=seeds, comm=comm)
+        del shard
     e[1].record()
     torch.cuda.synchronize()
     prefill_ms = e[0].elapsed_time(e[1])
-    del shard
+    if native:
+        ncomm.close()
     dec = ShardedDecoder(km, K, V, G, B, comm, sink_rows=sink_rows, ctx=ctx)
     T = args.warmup + args.steps
     ar = torch.arange(U, device=dev)
@@ -644,6 +671,9 @@ def run_config_E(args, rank, world, torch, dev, ctx, hbm):
     if world > 1:
         dist.barrier()
     with ClockSampler(int(str(dev).split(":")[-1])) as clk:
+        soak_for(torch, lambda: dec.step(qs[0]), 0.4)
+        if world > 1:
+            dist.barrier()
         e[0].record()
         for t in range(args.warmup, T):
             dec.step(qs[t])
@@ -679,7 +709,9 @@ def run_config_E(args, rank, world, torch, dev, ctx, hbm):
                                     "bytes_per_step_no_dedupe": step_bytes_nodd},
             "prefill": {"ms": prefill_ms, "units": U, "C0": C0, "iters_min": int(min(iters)),
                         "iters_max": int(max(iters)), "passes": passes,
-                        "assign_tflops_rank0": flops / (prefill_ms * 1e-3) / 1e12},
+                        "assign_tflops_rank0": flops / (prefill_ms * 1e-3) / 1e12,
+                        "host": "ckv_kmeans_sharded (C++ driver, NCCL)" if native
+                                else "sharded.py (torch.distributed)"},
             "clocks": clk.summary()}
 
 
@@ -723,11 +755,15 @@ def run_config_A(args, torch, dev, ctx):
         sess.step(q_all[t], kn_all[t], vn_all[t], out)
     e = _events(torch, 2)
     torch.cuda.synchronize()
-    e[0].record()
-    for t in range(steps):
-        sess.step(q_all[args.warmup + t], kn_all[args.warmup + t], vn_all[args.warmup + t], out)
-    e[1].record()
-    torch.cuda.synchronize()
+    with ClockSampler(int(str(dev).split(":")[-1])) as clk:
+        soak_out = torch.empty_like(out)
+        soak_for(torch, lambda: sess.attend_only(q_all[0], soak_out), 0.4)
+        e[0].record()
+        for t in range(steps):
+            sess.step(q_all[args.warmup + t], kn_all[args.warmup + t], vn_all[args.warmup + t],
+                      out)
+        e[1].record()
+        torch.cuda.synchronize()
     gpu_step = e[0].elapsed_time(e[1]) / steps
     gp = float(np.median(gpu_prefill))
     # ---- CPU reference (the cpu_baseline leg) -----------------------------------
@@ -769,7 +805,8 @@ def run_config_A(args, torch, dev, ctx):
                              "sample": "the whole config-A step: select_tokens + "
                                        "approx_attention of all 32 q heads (median of 5), and "
                                        "cluster_prefill of all 8 heads (median of 3), on the "
-                                       "same bf16 heads copied to the host"}}
+                                       "same bf16 heads copied to the host"},
+            "clocks": clk.summary()}
 
 
 def run_page_baseline(torch, dev, ctx, sess, U, G, L, B, q, hbm, ps=16, kv_heads=8):

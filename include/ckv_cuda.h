@@ -215,6 +215,51 @@ int ckv_kmshard_partial_sums(ckv_kmshard* sh);
 int ckv_kmshard_result(ckv_kmshard* sh, const uint32_t* iters_host, float* centroids,
                        int32_t* labels);
 
+/* Communicators of the sequence-sharded paths (ckv_comm.cu).
+ *   NCCL:  one rank per GPU (process or thread); rank 0 makes an id with
+ *          ckv_comm_nccl_id and the caller hands it to every rank, which
+ *          calls ckv_comm_create_nccl (ncclCommInitRank).  The collectives
+ *          run in place on device buffers on the context's stream.  libnccl
+ *          is loaded at run time; CKV_ENCCL when it is missing or fails.
+ *   LOCAL: the ranks are threads of one process sharing a ckv_local_group
+ *          (collectives staged through host memory): several ranks on one
+ *          GPU, e.g. tests (NCCL refuses duplicate devices).
+ * Every rank of a communicator must make the same sequence of calls. */
+typedef struct ckv_comm ckv_comm;
+typedef struct ckv_local_group ckv_local_group;
+#define CKV_NCCL_ID_BYTES 128
+#define CKV_DT_I32 0
+#define CKV_DT_F64 1
+#define CKV_OP_SUM 0
+#define CKV_OP_MAX 1
+int ckv_comm_nccl_id(unsigned char* id_out /* CKV_NCCL_ID_BYTES */);
+int ckv_comm_create_nccl(ckv_ctx* ctx, int world, int rank, const unsigned char* id,
+                         ckv_comm** out);
+int ckv_local_group_create(int world, ckv_local_group** out);
+int ckv_local_group_destroy(ckv_local_group* g);
+int ckv_comm_create_local(ckv_ctx* ctx, ckv_local_group* g, int rank, ckv_comm** out);
+int ckv_comm_destroy(ckv_comm* c);
+int ckv_comm_world(const ckv_comm* c, int* world, int* rank);
+/* in place, device buffer of `count` CKV_DT_* elements, CKV_OP_SUM / MAX */
+int ckv_comm_allreduce(ckv_comm* c, void* dev, size_t count, int dtype, int op);
+/* recv [world][bytes] <- every rank's send [bytes]; device buffers */
+int ckv_comm_allgather(ckv_comm* c, const void* send, void* recv, size_t bytes);
+
+/* kmeans_cosine (clustering.hpp:160-263) of n_units heads whose n_total keys
+ * are position-sharded over the communicator's ranks: this rank holds rows
+ * [row_lo, row_lo + desc->n_local) of every unit at `keys` (device bf16,
+ * unit stride desc->key_stride).  The whole reference loop runs here, the
+ * per-shard steps above with the collectives between them (sharded.py is
+ * the same protocol over torch.distributed).  seeds_host [n_units] (the
+ * reference's init_rows draw) or init_rows_host [n_units*C] (global rows).
+ * Outputs on the device: centroids [n_units][C][128], identical on every
+ * rank; labels [n_units][n_local] of this shard.  Bit-identical to the
+ * single-process kmeans_cosine for any shard count. */
+int ckv_kmeans_sharded(ckv_comm* comm, const ckv_kmshard_desc* desc, const uint16_t* keys,
+                       uint64_t n_total, uint64_t row_lo, const uint64_t* seeds_host,
+                       const uint32_t* init_rows_host, uint32_t max_iters, float* centroids,
+                       int32_t* labels, ckv_kmeans_info* info_host);
+
 /* ------------------------------------------------------------------ */
 /* index (selection.hpp:16-48)                                         */
 /* ------------------------------------------------------------------ */

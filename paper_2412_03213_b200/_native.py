@@ -131,6 +131,17 @@ SIGNATURES = {
     "ckv_kmshard_finish": (C.c_int, [vp, u32, C.c_int]),
     "ckv_kmshard_partial_sums": (C.c_int, [vp]),
     "ckv_kmshard_result": (C.c_int, [vp, vp, vp, vp]),
+    "ckv_comm_nccl_id": (C.c_int, [vp]),
+    "ckv_comm_create_nccl": (C.c_int, [vp, C.c_int, C.c_int, vp, C.POINTER(vp)]),
+    "ckv_local_group_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "ckv_local_group_destroy": (C.c_int, [vp]),
+    "ckv_comm_create_local": (C.c_int, [vp, vp, C.c_int, C.POINTER(vp)]),
+    "ckv_comm_destroy": (C.c_int, [vp]),
+    "ckv_comm_world": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ckv_comm_allreduce": (C.c_int, [vp, vp, C.c_size_t, C.c_int, C.c_int]),
+    "ckv_comm_allgather": (C.c_int, [vp, vp, vp, C.c_size_t]),
+    "ckv_kmeans_sharded": (C.c_int, [vp, C.POINTER(KmShardDesc), vp, u64, u64, vp, vp, u32, vp,
+                                     vp, vp]),
     "ckv_relayout_kv": (C.c_int, [vp, u32, u32, vp, vp, vp, vp, vp, u32, u32, u32]),
     "ckv_score_range": (C.c_int, [vp, u32, u32, vp, vp, u32, u32, u32, u32, vp]),
     "ckv_select_scored": (C.c_int, [vp, C.POINTER(ShardSelectDesc), vp, vp, vp, vp, vp, vp,

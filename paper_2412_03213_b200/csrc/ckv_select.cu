@@ -846,7 +846,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   // fused (one CTA per unit: score + select) when the units fill the GPU;
   // a layer-sized launch (few units) scores with many CTAs per unit instead
   static const bool unfused = getenv("CKV_SELECT_UNFUSED") != nullptr;
-  const bool few_units = units * 2 < uint32_t(num_sms());
+  static const int few_env = getenv("CKV_SEL_FEW") ? atoi(getenv("CKV_SEL_FEW")) : -1;
+  const bool few_units = few_env >= 0 ? few_env != 0 : units * 2 < uint32_t(num_sms());
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused && !few_units) {
     const size_t smem_f = size_t(G) * warp_bytes + size_t(G) * c_pad * 8 + size_t(c_pad) * 8;
     if (smem_f <= 200 * 1024) {

@@ -477,3 +477,85 @@ class ShardedDecoder:
         return dict(out=out, token_ids=ids, weights=w, n_tokens=self.n_tokens,
                     n_taken=self.n_taken, trimmed=self.trimmed, ranked=self.ranked,
                     run_off=self.run_off, run_cnt=self.run_cnt)
+
+
+# --------------------------------------------------------------------------
+# the native driver (ckv_comm.cu): the same protocol in C++ over NCCL, no
+# torch.distributed — what a C/C++ host of the drop-in calls
+# --------------------------------------------------------------------------
+class NativeComm:
+    """A ckv_comm: NCCL (one rank per GPU; rank 0 makes the id with
+    `nccl_id()` and the caller distributes it) or LOCAL (the ranks are
+    threads of this process sharing `local_group(world)`: several ranks on
+    one GPU)."""
+
+    def __init__(self, ctx=None, world: int = 1, rank: int = 0, nccl_id: bytes | None = None,
+                 group=None):
+        from .api import Context
+        self.ctx = ctx or Context.default()
+        self.world, self.rank = world, rank
+        h = C.c_void_p()
+        if group is not None:
+            check(lib().ckv_comm_create_local(self.ctx.h, group, rank, C.byref(h)))
+        else:
+            if nccl_id is None:
+                if world != 1:
+                    raise ValueError("NativeComm: world > 1 over NCCL needs rank 0's nccl_id")
+                nccl_id = NativeComm.nccl_id()
+            buf = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+            check(lib().ckv_comm_create_nccl(self.ctx.h, world, rank, buf, C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def nccl_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        check(lib().ckv_comm_nccl_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def local_group(world: int):
+        g = C.c_void_p()
+        check(lib().ckv_local_group_create(world, C.byref(g)))
+        return g
+
+    def close(self):
+        if self.h:
+            lib().ckv_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def kmeans_cosine_native(keys: torch.Tensor, C_: int, n_total: int, row_lo: int,
+                         comm: NativeComm, seeds=None, init_rows=None, max_iters: int = 50,
+                         exact_only: bool = False) -> ShardedKMeansResult:
+    """kmeans_cosine_sharded through ckv_kmeans_sharded: this rank's keys
+    [U][n_local][128] (device bf16 bits), rows [row_lo, row_lo + n_local) of
+    every unit's n_total.  The whole loop runs in C++ (NCCL or LOCAL
+    collectives); repair_iterations holds only the number of repair passes
+    per unit (the C-ABI's ckv_kmeans_info.n_repair)."""
+    if not keys.is_cuda:
+        raise ValueError("kmeans_cosine_native: keys must be a CUDA tensor (no CPU fallback)")
+    if keys.stride(2) != 1 or keys.stride(1) != D:
+        keys = keys.contiguous()
+    U, n_local, _ = keys.shape
+    desc = N.KmShardDesc(U, n_local, C_, N.CKV_KM_EXACT_ONLY if exact_only else 0,
+                         keys.stride(0))
+    sd = None if seeds is None else np.ascontiguousarray(seeds, np.uint64)
+    ir = None if init_rows is None else np.ascontiguousarray(init_rows, np.uint32).reshape(U, -1)
+    cents = torch.empty((U, C_, D), dtype=torch.float32, device=keys.device)
+    labels = torch.empty((U, n_local), dtype=torch.int32, device=keys.device)
+    info = (N.KMeansInfo * U)()
+    check(lib().ckv_kmeans_sharded(comm.h, C.byref(desc), keys.data_ptr(), n_total, row_lo,
+                                   None if sd is None else sd.ctypes.data_as(C.c_void_p),
+                                   None if ir is None else ir.ctypes.data_as(C.c_void_p),
+                                   max_iters, cents.data_ptr(), labels.data_ptr(),
+                                   C.cast(info, C.c_void_p)))
+    iters = np.array([i.iterations_used for i in info], np.uint32)
+    conv = np.array([bool(i.converged) for i in info])
+    reps = [int(i.n_repair) for i in info]
+    return ShardedKMeansResult(C_, cents, labels, row_lo, iters, conv, reps, [])
