@@ -58,6 +58,7 @@ constexpr int TC_THREADS = (2 + 4 * TC_EGROUPS) * 32;
 constexpr uint32_t TC_FULL = 0xffffffffu;
 constexpr int TC_NCAND = 8;            // candidates an epilogue row keeps
 constexpr int TC_MERGE_SLOT = 1023;    // fix_count slot of the merged (C > 512) list
+constexpr int TC_FULL_SLOT = 1022;     // fix_count slot of the FULL fix-up queue length
 
 // dynamic smem (1024-B aligned base): A stages [stages][2 k-halves][128 x 128 B],
 // then B [2 k-halves][c_pad x 128 B], then the barriers.  B is the resident
@@ -652,6 +653,9 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
 // is the label.  Padding columns (>= C) score exactly 0 (zero operand rows);
 // a surviving one makes the row FULL (exact fix-up over all C).
 // ===========================================================================
+#ifndef CKV_T2_ENTRIES
+#define CKV_T2_ENTRIES 4  // in-band entries per row: 2 scored + 2 bounded by e1, or 2
+#endif
 constexpr int T2_CW = 256;                       // columns per TMEM chunk buffer
 constexpr int T2_NBUF = 512 / T2_CW;             // chunk buffers (512 TMEM columns)
 constexpr int T2_CG = T2_NBUF;                   // epilogue warps per lane quarter: one per buffer
@@ -894,7 +898,7 @@ k_assign_tc2(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ C
       // two best entries {score, first column, in-band mask} and the largest
       // score displaced from them
       float e0s = -INFINITY, e1s = -INFINITY, dmax = -INFINITY;
-      uint32_t e0c = 0u, e0m = 0u, e1c = 0u, e1m = 0u;
+      uint32_t e0c = 0u, e0m = 0u, e1c = 0u, e1m = 0u, e2c = 0u, e2m = 0u, e3c = 0u, e3m = 0u;
 #pragma unroll 1
       for (uint32_t ch = 0; ch < nch; ++ch) {
         const uint32_t cc = ch * T2_CW;
@@ -950,8 +954,19 @@ k_assign_tc2(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ C
           for (int q = 0; q < T2_GB; ++q) {
             const float bm = bmq[q];
             const uint32_t in = inq[q], col = cbeg + cc + (b0 + q) * 32;
+            // e2, e3 keep no score: e1s bounds them (they were <= e1 when
+            // they arrived or were pushed down, and e1s only grows); the
+            // entry leaving e3 records that bound in dmax
             const bool p = in != 0u, gt1 = p && bm > e1s, gt0 = p && bm > e0s;
+#if CKV_T2_ENTRIES == 4
+            dmax = (p && e3m) ? fmaxf(dmax, e1s) : dmax;
+            e3c = p ? e2c : e3c;
+            e3m = p ? e2m : e3m;
+            e2c = p ? (gt1 ? e1c : col) : e2c;
+            e2m = p ? (gt1 ? e1m : in) : e2m;
+#else
             dmax = p ? fmaxf(dmax, gt1 ? e1s : bm) : dmax;
+#endif
             e1s = gt0 ? e0s : (gt1 ? bm : e1s);
             e1c = gt0 ? e0c : (gt1 ? col : e1c);
             e1m = gt0 ? e0m : (gt1 ? in : e1m);
@@ -959,22 +974,29 @@ k_assign_tc2(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ C
             e0c = gt0 ? col : e0c;
             e0m = gt0 ? in : e0m;
           }
+          // entries that fell below the running max - band can never be
+          // candidates (lo <= M - band): e1 and what it bounds are dropped
+          if (e1s < lo) { e1s = -INFINITY; e1m = 0u; e2m = 0u; e3m = 0u; }
         }
       }
       // the row's decision: M = e0s; candidates = entries with score >= M - band
       if (row < a.n && a.mode == 0) {
         const float M = e0s, lo = M - band;
+        // e1, e2, e3 survive with e1 (their common bound)
         const bool u1 = e1s >= lo;
         bool full = !(M > -INFINITY) || dmax >= lo;
-        const uint32_t nin = __popc(e0m) + (u1 ? __popc(e1m) : 0u);
+        const uint32_t nin =
+            __popc(e0m) + (u1 ? __popc(e1m) + __popc(e2m) + __popc(e3m) : 0u);
         if (e0c + 32 - __ffs(e0m) >= a.C) full = true;  // a padding column survived
         if (u1 && e1c + 32 - __ffs(e1m) >= a.C) full = true;
+        if (u1 && e2m && e2c + 32 - __ffs(e2m) >= a.C) full = true;
+        if (u1 && e3m && e3c + 32 - __ffs(e3m) >= a.C) full = true;
         auto emit = [&](auto&& put) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            if (e == 1 && !u1) break;
-            uint32_t m = e ? e1m : e0m;
-            const uint32_t c = e ? e1c : e0c;
+          for (int e = 0; e < 4; ++e) {
+            if (e >= 1 && !u1) break;
+            uint32_t m = e == 0 ? e0m : e == 1 ? e1m : e == 2 ? e2m : e3m;
+            const uint32_t c = e == 0 ? e0c : e == 1 ? e1c : e == 2 ? e2c : e3c;
             while (m) {
               const uint32_t jj = __clz(m);
               m &= ~(0x80000000u >> jj);
@@ -1072,7 +1094,8 @@ k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
         uint32_t tiles_per_unit, const uint16_t* __restrict__ keys,
         uint64_t key_stride, const float* __restrict__ dirs, uint32_t C, uint32_t c_pad,
         const float* __restrict__ knorm, uint32_t n, int32_t* __restrict__ labels,
-        uint32_t label_stride) {
+        uint32_t label_stride, uint32_t* __restrict__ full_q = nullptr,
+        uint32_t* __restrict__ full_n = nullptr) {
   // region r = blockIdx.y holds count[r] entries from index r * per * 128
   // (k_assign_tc's CTA r processed tiles [r * per, (r + 1) * per)).
   // A half-warp per key (lane hl holds dims 8hl..8hl+7): two keys per warp,
@@ -1091,6 +1114,10 @@ k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
     const uint4 it = list[e];
     const uint32_t u = it.x, row = it.y;
     const bool full = it.z == TC_FULL;
+    if (full && full_q) {  // all C columns: a whole CTA per key, k_fixup_full
+      if (hl == 0) full_q[atomicAdd(full_n, 1u)] = e;
+      continue;
+    }
     const uint32_t nc = full ? C : it.z;
     const uint16_t* kr = keys + u * key_stride + size_t(row) * D;
     const uint4 kv = __ldg(reinterpret_cast<const uint4*>(kr) + hl);
@@ -1149,6 +1176,115 @@ k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
     }
     if (hl == 0)
       labels[size_t(u) * label_stride + row] = int32_t(bid == 0xffffffffu ? 0 : bid);
+  }
+}
+
+// FULL fix-ups (more in-band columns than the epilogue kept: near-ties among
+// many centroids): the argmax over all C columns of one key by a whole CTA.
+// Warp w takes columns w, w + 8, ...; lane L holds dims 4L..4L+3, the score
+// is a lane-tree f64 sum (products exact in f64; within 2^-46 |k| of the
+// sequential chain), kept in smem.  When the best two are closer than
+// 2^-40 |k|, every column within that of the best is re-scored with the
+// sequential dot_f64 chain (the reference's rounding) and the first maximum
+// wins (clustering.hpp:104-115).  One launch over the queue k_fixup filled.
+constexpr int FF_WARPS = 8;
+constexpr uint32_t FF_MAXC = TC_MAXC_ALL;
+__global__ void __launch_bounds__(FF_WARPS * 32)
+k_fixup_full(const uint4* __restrict__ list, const uint32_t* __restrict__ full_q,
+             const uint32_t* __restrict__ full_n, const uint16_t* __restrict__ keys,
+             uint64_t key_stride, const float* __restrict__ dirs, uint32_t C, uint32_t c_pad,
+             const float* __restrict__ knorm, uint32_t n, int32_t* __restrict__ labels,
+             uint32_t label_stride) {
+  __shared__ double sc[FF_MAXC];
+  __shared__ double wb[FF_WARPS], ws[FF_WARPS];
+  __shared__ uint32_t wi[FF_WARPS];
+  __shared__ double s_thr;
+  __shared__ uint32_t s_bid, s_tie;
+  const int lane = lane_id(), w = warp_id();
+  const uint32_t nf = *full_n;
+  for (uint32_t qi = blockIdx.x; qi < nf; qi += gridDim.x) {
+    const uint4 it = list[full_q[qi]];
+    const uint32_t u = it.x, row = it.y;
+    const uint16_t* kr = keys + u * key_stride + size_t(row) * D;
+    const uint2 kv = __ldg(reinterpret_cast<const uint2*>(kr) + lane);
+    const double k0 = double(__uint_as_float(kv.x << 16)), k1 = double(__uint_as_float(kv.x & 0xffff0000u));
+    const double k2 = double(__uint_as_float(kv.y << 16)), k3 = double(__uint_as_float(kv.y & 0xffff0000u));
+    const float* du = dirs + size_t(u) * c_pad * D;
+    double best = -INFINITY, second = -INFINITY;
+    uint32_t bid = 0xffffffffu;
+    for (uint32_t c0 = w; c0 < C; c0 += FF_WARPS * 4) {
+      double p[4];
+      uint32_t cc[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {  // 4 rows in flight per warp
+        cc[j] = c0 + FF_WARPS * j;
+        const float4 x = cc[j] < C ? __ldg(reinterpret_cast<const float4*>(du + size_t(cc[j]) * D) + lane)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        p[j] = __fma_rn(k3, double(x.w), __fma_rn(k2, double(x.z), __fma_rn(k1, double(x.y), k0 * double(x.x))));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) p[j] += __shfl_xor_sync(0xffffffffu, p[j], o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (cc[j] >= C) break;
+        const double sj = isnan(p[j]) ? -INFINITY : p[j];
+        if (lane == 0) sc[cc[j]] = sj;
+        if (sj > best) { second = best; best = sj; bid = cc[j]; }  // ids ascend per warp
+        else if (sj > second) second = sj;
+      }
+    }
+    if (lane == 0) { wb[w] = best; ws[w] = second; wi[w] = bid; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -INFINITY, s2 = -INFINITY;
+      uint32_t bi = 0xffffffffu;
+      for (int x = 0; x < FF_WARPS; ++x) {
+        if (wb[x] > b || (wb[x] == b && wi[x] < bi)) { s2 = fmax(s2, b); b = wb[x]; bi = wi[x]; }
+        else s2 = fmax(s2, wb[x]);
+        s2 = fmax(s2, ws[x]);
+      }
+      const double tie = double(knorm[size_t(u) * n + row]) * 0x1p-40;
+      s_bid = bi;
+      s_tie = (b > -INFINITY && !(b - s2 > tie)) ? 1u : 0u;
+      s_thr = b - tie;  // the near-tie re-score threshold
+    }
+    __syncthreads();
+    uint32_t label = s_bid;
+    if (s_tie) {
+      // near-tie: the sequential chain decides among the columns within
+      // the tie margin of the best, first maximum (lowest id on equality)
+      const double thr = s_thr;
+      double b2 = -INFINITY;
+      uint32_t i2 = 0xffffffffu;
+      for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+        if (!(sc[c] >= thr)) continue;
+        const double sj = exact_dot(kr, du + size_t(c) * D);
+        if (sj > b2) { b2 = sj; i2 = c; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, b2, o);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, i2, o);
+        if (os > b2 || (os == b2 && oi < i2)) { b2 = os; i2 = oi; }
+      }
+      __syncthreads();
+      if (lane == 0) { wb[w] = b2; wi[w] = i2; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double b = -INFINITY;
+        uint32_t bi = 0xffffffffu;
+        for (int x = 0; x < FF_WARPS; ++x)
+          if (wb[x] > b || (wb[x] == b && wi[x] < bi)) { b = wb[x]; bi = wi[x]; }
+        s_bid = bi;
+      }
+      __syncthreads();
+      label = s_bid;
+    }
+    if (threadIdx.x == 0)
+      labels[size_t(u) * label_stride + row] = int32_t(label == 0xffffffffu ? 0 : label);
+    __syncthreads();  // smem reused by the next key
   }
 }
 
@@ -1224,6 +1360,7 @@ __global__ void k_compact_active(const int32_t* __restrict__ active, uint32_t n_
     *count = n;
     *fix_count = 0;
     fix_count[TC_MERGE_SLOT] = 0;  // k_assign_merge's single region
+    fix_count[TC_FULL_SLOT] = 0;   // k_fixup_full's queue length
   }
 }
 
@@ -1242,6 +1379,7 @@ struct TcScratch {
   uint32_t* fix_count;
   uint4* fix_list;
   uint32_t* fix_ids;
+  uint32_t* full_q;  // FULL fix-up entries, k_fixup -> k_fixup_full
   float* knorm;
   float* eps_u;
   float* kerr;     // [unit] max_k |k - h(k)| (float bits, atomicMax'd as u32)
@@ -1271,6 +1409,8 @@ TcScratch carve(void* base, uint32_t n_units, uint32_t n) {
   p += align256(size_t(s.fix_cap) * 16);
   s.fix_ids = reinterpret_cast<uint32_t*>(p);
   p += align256(size_t(s.fix_cap) * 32);
+  s.full_q = reinterpret_cast<uint32_t*>(p);
+  p += align256(size_t(s.fix_cap) * 4);
   s.knorm = reinterpret_cast<float*>(p);
   p += align256(size_t(n_units) * n * 4);
   s.eps_u = reinterpret_cast<float*>(p);
@@ -1333,7 +1473,8 @@ size_t assign_tc_scratch_bytes(uint32_t n_units, uint32_t n, uint32_t C) {
   uint32_t nr = 1, rc = 0;
   tc_ranges((C + 31) / 32 * 32, &nr, &rc);
   const size_t summ = nr > 1 ? size_t(n_units) * n * nr * 16 : 0;
-  return align256(size_t(n_units) * 4) + 256 + 4096 + align256(cap * 16) + align256(cap * 32) + align256(size_t(n_units) * n * 4) +
+  return align256(size_t(n_units) * 4) + 256 + 4096 + align256(cap * 16) + align256(cap * 32) +
+         align256(cap * 4) + align256(size_t(n_units) * n * 4) +
          align256(size_t(n_units) * 4) + 256 + align256(size_t(n_units) * 4) +
          align256(cap * D * 2) + summ;
 }
@@ -1442,8 +1583,15 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   if (ta.n_ranges == 1) {
     k_fixup<<<dim3(8, num_sms()), 256, 0, st>>>(s.fix_list, s.fix_ids, s.fix_count, s.count,
                                                  ta.tiles_per_unit, keys, key_stride, dirs, C,
-                                                 c_pad, s.knorm, n, labels, label_stride);
+                                                 c_pad, s.knorm, n, labels, label_stride, s.full_q,
+                                                 s.fix_count + TC_FULL_SLOT);
     CKV_LAUNCH_CHECK("k_fixup");
+    k_fixup_full<<<2 * num_sms(), FF_WARPS * 32, 0, st>>>(s.fix_list, s.full_q,
+                                                           s.fix_count + TC_FULL_SLOT, keys,
+                                                           key_stride, dirs, C, c_pad, s.knorm, n,
+                                                           labels, label_stride);
+    CKV_LAUNCH_CHECK("k_fixup_full");
+    ++*launches;
   } else {
     k_assign_merge<<<dim3((n + 255) / 256, n_units), 256, 0, st>>>(
         s.summ, ta.n_ranges, n, s.list, s.count, s.knorm, s.eps_u, s.kerr, labels, label_stride,
@@ -1453,8 +1601,15 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
     k_fixup<<<dim3(8 * num_sms(), 1), 256, 0, st>>>(s.fix_list, s.fix_ids,
                                                      s.fix_count + TC_MERGE_SLOT, s.count,
                                                      ta.tiles_per_unit, keys, key_stride, dirs,
-                                                     C, c_pad, s.knorm, n, labels, label_stride);
+                                                     C, c_pad, s.knorm, n, labels, label_stride,
+                                                     s.full_q, s.fix_count + TC_FULL_SLOT);
     CKV_LAUNCH_CHECK("k_fixup");
+    k_fixup_full<<<2 * num_sms(), FF_WARPS * 32, 0, st>>>(s.fix_list, s.full_q,
+                                                           s.fix_count + TC_FULL_SLOT, keys,
+                                                           key_stride, dirs, C, c_pad, s.knorm, n,
+                                                           labels, label_stride);
+    CKV_LAUNCH_CHECK("k_fixup_full");
+    ++*launches;
     ++*launches;
   }
   *launches += 4;
