@@ -216,7 +216,8 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
          const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
          float* __restrict__ cents, float* __restrict__ dirs, uint16_t* __restrict__ dirs16,
          double* __restrict__ cnorm, float* __restrict__ deps, const int32_t* __restrict__ active,
-         const uint8_t* __restrict__ dirty) {
+         const uint8_t* __restrict__ dirty, double* __restrict__ sums_out,
+         const double* __restrict__ sums_in) {
   const uint32_t u = blockIdx.y;
   if (active && !active[u]) return;
   const uint32_t c = blockIdx.x * (blockDim.x >> 5) + warp_id();
@@ -233,10 +234,17 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
     return;
   }
   const uint32_t cnt = sizes[size_t(u) * c_stride + c];
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  if (sums_in) {  // incremental pass: the member sums were updated by k_update_delta
+    const double2* sp = reinterpret_cast<const double2*>(sums_in + (size_t(u) * c_stride + c) * D) + 2 * lane;
+    const double2 x = sp[0], y = sp[1];
+    finish_centroid(x.x, x.y, y.x, y.y, double(cnt), cents + (size_t(u) * c_stride + c) * D, dr, db,
+                    cnorm + size_t(u) * c_pad + c, deps + size_t(u) * c_pad + c);
+    return;
+  }
   const uint32_t beg = starts[size_t(u) * (c_stride + 1) + c];
   const uint32_t* ids = sorted_ids + size_t(u) * label_stride + beg;
   const uint2* kb = reinterpret_cast<const uint2*>(keys + u * key_stride) + lane;
-  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
   // member ids 32 at a time (one coalesced load), rows 16 in flight; the
   // f64 adds stay in member (= position) order, as update_centroids sums.
   for (uint32_t m0 = 0; m0 < cnt; m0 += 32) {
@@ -260,8 +268,57 @@ k_update(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t C, uin
       }
     }
   }
+  if (sums_out) {
+    double2* sp = reinterpret_cast<double2*>(sums_out + (size_t(u) * c_stride + c) * D) + 2 * lane;
+    sp[0] = make_double2(a0, a1);
+    sp[1] = make_double2(a2, a3);
+  }
   finish_centroid(a0, a1, a2, a3, double(cnt), cents + (size_t(u) * c_stride + c) * D, dr, db,
                   cnorm + size_t(u) * c_pad + c, deps + size_t(u) * c_pad + c);
+}
+
+// ---------------------------------------------------------------------------
+// incremental update (passes >= 2): only the keys whose label changed since
+// the last update move their bf16 values between the persisted f64 member
+// sums (subtract from the old cluster, add to the new).  Sums of bf16 values
+// in f64 are exact in any order, and so are these differences,
+// so the sums -- hence the centroids k_update finishes from them -- equal the
+// position-ordered recomputation bit for bit, at a cost proportional to the
+// moved keys instead of every member of every dirty cluster.
+// One warp per 32 consecutive keys; lane L adds dims 4L..4L+3 of each moved key.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_update_delta(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t n,
+               uint32_t c_stride, uint32_t label_stride, const int32_t* __restrict__ now,
+               const int32_t* __restrict__ before, const int32_t* __restrict__ active,
+               double* __restrict__ sums) {
+  const uint32_t u = blockIdx.y;
+  if (active && !active[u]) return;
+  const int lane = lane_id();
+  const uint32_t i0 = (blockIdx.x * (blockDim.x >> 5) + warp_id()) * 32;
+  if (i0 >= n) return;
+  const uint32_t i = i0 + lane;
+  const int32_t ln = i < n ? now[size_t(u) * label_stride + i] : -1;
+  const int32_t lb = i < n ? before[size_t(u) * label_stride + i] : -1;
+  unsigned moved = __ballot_sync(0xffffffffu, ln != lb);
+  const uint2* kb = reinterpret_cast<const uint2*>(keys + u * key_stride) + lane;
+  double* su = sums + size_t(u) * c_stride * D + 4 * lane;
+  while (moved) {
+    const int src = __ffs(moved) - 1;
+    moved &= moved - 1;
+    const int32_t cn = __shfl_sync(0xffffffffu, ln, src), cb = __shfl_sync(0xffffffffu, lb, src);
+    const uint2 v = __ldg(kb + size_t(i0 + src) * (D / 4));
+    const double x0 = double(__uint_as_float(v.x << 16)), x1 = double(__uint_as_float(v.x & 0xffff0000u));
+    const double x2 = double(__uint_as_float(v.y << 16)), x3 = double(__uint_as_float(v.y & 0xffff0000u));
+    if (cn >= 0) {
+      double* d = su + size_t(cn) * D;
+      atomicAdd(d, x0); atomicAdd(d + 1, x1); atomicAdd(d + 2, x2); atomicAdd(d + 3, x3);
+    }
+    if (cb >= 0) {
+      double* d = su + size_t(cb) * D;
+      atomicAdd(d, -x0); atomicAdd(d + 1, -x1); atomicAdd(d + 2, -x2); atomicAdd(d + 3, -x3);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -511,6 +568,9 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
   CKV_TRY(dalloc(ctx, 18, b_objlog, sizeof(double) * size_t(U) * (MI + 1)));
   CKV_TRY(dalloc(ctx, 19, b_nact, sizeof(int32_t)));
   CKV_TRY(dalloc(ctx, 21, b_dirty, size_t(U) * CS));
+  // persisted f64 member sums of the last update (incremental passes)
+  DevBuf b_sums;
+  CKV_TRY(dalloc(ctx, 38, b_sums, sizeof(double) * size_t(U) * CS * D));
 
   const bool use_tc = !(a.flags & CKV_KM_EXACT_ONLY) && assign_tc_supported(n, C);
   size_t tc_bytes = use_tc ? assign_tc_scratch_bytes(U, n, C) : 0;
@@ -660,10 +720,27 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     int32_t* cur = lab[t & 1];
     if (dbg) cudaEventRecord(dev_[0], st);
     // update from the previous labels (sizes/starts/sorted hold its sort)
+    // the first passes (most keys move) recompute the dirty clusters from
+    // their members and keep the f64 sums; from pass KM_INCR_FROM on (a few
+    // percent of the keys move) only the moved keys update the sums and the
+    // dirty clusters are finished from them (measured at config B: the
+    // atomic delta costs 2.7 / 1.1 / 0.6 ms in passes 2-4 against ~0.6 ms of
+    // recomputation, and 0.4 -> 0.03 ms afterwards).  CKV_KM_INCR_FROM=N
+    // overrides (a large N: always the full recomputation).
+    static const uint32_t incr_from = getenv("CKV_KM_INCR_FROM")
+                                          ? uint32_t(atoi(getenv("CKV_KM_INCR_FROM"))) : 5u;
+    const bool incr = t >= std::max(2u, incr_from);
+    if (incr) {
+      k_update_delta<<<dim3((n + 255) / 256, U), 256, 0, st>>>(
+          a.keys, a.key_stride, n, CS, LS, prev, cur, active, b_sums.as<double>());
+      CKV_LAUNCH_CHECK("k_update_delta");
+      ctx->launches++;
+    }
     k_update<<<dim3((c_pad + 7) / 8, U), 256, 0, st>>>(
         a.keys, a.key_stride, C, CS, c_pad, LS, b_sizes.as<uint32_t>(), b_starts.as<uint32_t>(),
         b_sorted.as<uint32_t>(), a.centroids, dirs, dirs16, cnorm, deps, active,
-        t == 1 ? nullptr : b_dirty.as<uint8_t>());
+        t == 1 ? nullptr : b_dirty.as<uint8_t>(), incr ? nullptr : b_sums.as<double>(),
+        incr ? b_sums.as<double>() : nullptr);
     CKV_LAUNCH_CHECK("k_update");
     ctx->launches++;
     if (dbg) cudaEventRecord(dev_[1], st);
