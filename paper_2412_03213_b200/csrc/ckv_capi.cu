@@ -917,6 +917,9 @@ struct ckv_session {
   // side stream and is committed async_delay steps later
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_done = nullptr;
+  // the batched step's second selection stream (session_select_attend)
+  cudaStream_t sel_stream = nullptr;
+  cudaEvent_t ev_sel_fork = nullptr, ev_sel_join = nullptr;
   uint32_t* stage_ncl = nullptr;  // n_clusters as the side stream's k-means leaves it
   struct Queued { uint32_t ready, pos0, rows, C; };
   std::deque<Queued> queue;
@@ -1039,6 +1042,10 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   rc |= salloc(&s->stage_ncl, s->U);
   if (!rc && cudaMallocHost(&s->h_stat, 8 * size_t(s->U)) != cudaSuccess) rc = 1;
   if (!rc && cudaEventCreateWithFlags(&s->ev_stat, cudaEventDisableTiming) != cudaSuccess) rc = 1;
+  if (!rc && (cudaStreamCreateWithFlags(&s->sel_stream, cudaStreamNonBlocking) != cudaSuccess ||
+              cudaEventCreateWithFlags(&s->ev_sel_fork, cudaEventDisableTiming) != cudaSuccess ||
+              cudaEventCreateWithFlags(&s->ev_sel_join, cudaEventDisableTiming) != cudaSuccess))
+    rc = 1;
   if (!rc && d->async_delay) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -1131,6 +1138,9 @@ int ckv_session_destroy(ckv_session* s) {
   cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
   cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
   if (s->side) { cudaStreamSynchronize(s->side); cudaStreamDestroy(s->side); }
+  if (s->sel_stream) { cudaStreamSynchronize(s->sel_stream); cudaStreamDestroy(s->sel_stream); }
+  if (s->ev_sel_fork) cudaEventDestroy(s->ev_sel_fork);
+  if (s->ev_sel_join) cudaEventDestroy(s->ev_sel_join);
   if (s->ev_fork) cudaEventDestroy(s->ev_fork);
   if (s->ev_done) cudaEventDestroy(s->ev_done);
   if (s->ev_stat) cudaEventDestroy(s->ev_stat);
@@ -1218,9 +1228,10 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
 // select + attend of units [u0, u0 + nu) (all offsets are per unit / per q
 // head, so a slice is a sub-session).  q_copy: when q is mapped host memory,
 // the selection leaves a device copy of it there and the attention reads that
-// (its bulk copies stay on HBM)
-static int session_select_attend_slice(ckv_session* s, uint32_t u0, uint32_t nu,
-                                       const float* q_dev, float* out_dev, float* q_copy) {
+// (its bulk copies stay on HBM).  The two halves take a stream each so the
+// batched step can overlap one slice's selection with another's attention.
+static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, uint32_t nu,
+                                const float* q_dev, float* q_copy, bool force_fused) {
   const uint32_t G = s->d.group, h0 = u0 * G;
   ckv_select_desc sd{};
   sd.n_q = nu * G;
@@ -1233,6 +1244,7 @@ static int session_select_attend_slice(ckv_session* s, uint32_t u0, uint32_t nu,
   sd.rec_begin = s->labeled_end;
   sd.rec_end = s->n_ctx;
   sd.flags = (s->d.flags & CKV_SESSION_L2_PERSIST) ? CKV_SEL_L2_PERSIST : 0u;
+  if (force_fused) sd.flags |= CKV_SEL_FORCE_FUSED;
   sd.row_base = sd.sink_count;
   const bool want_ids = (s->d.flags & CKV_SESSION_TOKEN_IDS) != 0;
   ckv_runs runs = s->runs;
@@ -1248,44 +1260,84 @@ static int session_select_attend_slice(ckv_session* s, uint32_t u0, uint32_t nu,
   }
   const float* qs = q_dev + size_t(h0) * D;
   float* qc = q_copy ? q_copy + size_t(h0) * D : nullptr;
-  CKV_TRY(launch_select(s->ctx->stream, sd, qs, s->cents + size_t(u0) * s->c_cap * D,
+  CKV_TRY(launch_select(st, sd, qs, s->cents + size_t(u0) * s->c_cap * D,
                         s->n_clusters + u0, s->sizes + size_t(u0) * s->c_cap,
                         s->starts + size_t(u0) * (s->c_cap + 1), s->sorted + size_t(u0) * s->p_cap,
                         want_ids ? s->token_ids + size_t(h0) * s->sel_cap : nullptr, nullptr, runs,
                         sd.row_base, s->n_tokens + h0, s->n_taken + h0, s->trimmed + h0,
                         s->ranked + size_t(h0) * s->c_cap, nullptr, cache, s->sel_scratch, qc));
+  s->ctx->launches += 2;
+  return CKV_OK;
+}
+
+static int session_attend_slice(ckv_session* s, cudaStream_t st, uint32_t u0, uint32_t nu,
+                                const float* q_dev, float* out_dev, float* q_copy) {
+  const uint32_t G = s->d.group, h0 = u0 * G;
+  const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
+  ckv_runs runs = s->runs;
+  runs.row += size_t(h0) * runs.run_cap;
+  runs.off += size_t(h0) * (runs.run_cap + 1);
+  runs.count += h0;
+  const float* qs = q_dev + size_t(h0) * D;
+  float* qc = q_copy ? q_copy + size_t(h0) * D : nullptr;
   ckv_attend_desc ad{};
-  ad.n_q = sd.n_q;
+  ad.n_q = nu * G;
   ad.group = G;
   ad.p_cap = s->p_cap;
   ad.sel_cap = s->sel_cap;
-  ad.max_tokens = std::min(s->d.budget, s->labeled_end) + sd.sink_count + (s->n_ctx - s->labeled_end);
+  ad.max_tokens = std::min(s->d.budget, s->labeled_end) + sink + (s->n_ctx - s->labeled_end);
   if (s->tiered) {  // misses backing -> page pool; the attention reads page runs
     ckv_runs tr = s->truns;
     tr.row += size_t(h0) * tr.run_cap;
     tr.off += size_t(h0) * (tr.run_cap + 1);
     tr.count += h0;
-    CKV_TRY(launch_tier_fetch(s->ctx->stream, s->tier, u0, nu, s->steps, runs, tr,
+    CKV_TRY(launch_tier_fetch(st, s->tier, u0, nu, s->steps, runs, tr,
                               s->ranked + size_t(h0) * s->c_cap, s->n_taken + h0, s->K, s->V));
     s->ctx->launches++;
     runs = tr;
   }
-  CKV_TRY(launch_attend(s->ctx->stream, ad, qc ? qc : qs, s->K + size_t(u0) * s->p_cap * D,
+  CKV_TRY(launch_attend(st, ad, qc ? qc : qs, s->K + size_t(u0) * s->p_cap * D,
                         s->V + size_t(u0) * s->p_cap * D, nullptr, runs, s->n_tokens + h0,
                         out_dev + size_t(h0) * D, nullptr, nullptr, s->part, s->tickets));
-  s->ctx->launches += 3;
+  s->ctx->launches++;
   return CKV_OK;
 }
 
 // one step's select + attend: every unit in one launch pair, or (layer mode,
 // ckv_session_set_layer_units) one pair per layer slice in layer order — the
-// dependency order of a model, where layer l+1's queries need layer l's output
+// dependency order of a model, where layer l+1's queries need layer l's output.
+// CKV_SESSION_SPLIT=1 (experiment, off): batched mode splits the units in
+// two (the first 1/8 and the rest) and runs the large slice's selection on a
+// second stream beside the small slice's attention, to overlap the
+// selection's latency tail with HBM work.  Measured slower at config B (144
+// vs 120 us/step: the concurrent kernels contend and the small attention
+// lands on the critical path).  Every attention follows its own selection;
+// the two attentions share the split-K scratch, so they run in order.
 static int session_select_attend(ckv_session* s, const float* q_dev, float* out_dev,
                                  float* q_copy = nullptr) {
+  cudaStream_t st = s->ctx->stream;
   const uint32_t lu = s->layer_units;
-  if (lu == 0 || lu >= s->U) return session_select_attend_slice(s, 0, s->U, q_dev, out_dev, q_copy);
-  for (uint32_t u0 = 0; u0 < s->U; u0 += lu)
-    CKV_TRY(session_select_attend_slice(s, u0, std::min(lu, s->U - u0), q_dev, out_dev, q_copy));
+  if (lu == 0 || lu >= s->U) {
+    static const bool split = getenv("CKV_SESSION_SPLIT") != nullptr;
+    const uint32_t u1 = s->U / 8;
+    if (!split || s->tiered || !s->sel_stream || u1 < 8) {
+      CKV_TRY(session_select_slice(s, st, 0, s->U, q_dev, q_copy, false));
+      return session_attend_slice(s, st, 0, s->U, q_dev, out_dev, q_copy);
+    }
+    CKV_CUDA_TRY(cudaEventRecord(s->ev_sel_fork, st));
+    CKV_CUDA_TRY(cudaStreamWaitEvent(s->sel_stream, s->ev_sel_fork, 0));
+    CKV_TRY(session_select_slice(s, s->sel_stream, u1, s->U - u1, q_dev, q_copy, true));
+    CKV_CUDA_TRY(cudaEventRecord(s->ev_sel_join, s->sel_stream));
+    CKV_TRY(session_select_slice(s, st, 0, u1, q_dev, q_copy, true));
+    CKV_TRY(session_attend_slice(s, st, 0, u1, q_dev, out_dev, q_copy));
+    CKV_CUDA_TRY(cudaStreamWaitEvent(st, s->ev_sel_join, 0));
+    return session_attend_slice(s, st, u1, s->U - u1, q_dev, out_dev, q_copy);
+  }
+  for (uint32_t u0 = 0; u0 < s->U; u0 += lu) {
+    const uint32_t nu = std::min(lu, s->U - u0);
+    CKV_TRY(session_select_slice(s, st, u0, nu, q_dev, q_copy, false));
+    CKV_TRY(session_attend_slice(s, st, u0, nu, q_dev, out_dev, q_copy));
+  }
   return CKV_OK;
 }
 

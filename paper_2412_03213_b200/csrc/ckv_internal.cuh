@@ -92,6 +92,10 @@ int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t
 }  // namespace ckvb
 
 namespace ckvb {
+// internal ckv_select_desc flag: take the fused (smem-only) selection kernel
+// whatever the unit count (the session's concurrent slices: the unfused path
+// shares one scratch buffer)
+constexpr uint32_t CKV_SEL_FORCE_FUSED = 0x80000000u;
 struct CacheDev {
   uint32_t n_slots, c_cap, retention, d, words;
   uint32_t* bits;                // [n_slots][retention][words]

@@ -847,7 +847,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   // a layer-sized launch (few units) scores with many CTAs per unit instead
   static const bool unfused = getenv("CKV_SELECT_UNFUSED") != nullptr;
   static const int few_env = getenv("CKV_SEL_FEW") ? atoi(getenv("CKV_SEL_FEW")) : -1;
-  const bool few_units = few_env >= 0 ? few_env != 0 : units * 2 < uint32_t(num_sms());
+  const bool few_units = (desc.flags & CKV_SEL_FORCE_FUSED) ? false
+                         : few_env >= 0 ? few_env != 0 : units * 2 < uint32_t(num_sms());
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused && !few_units) {
     const size_t smem_f = size_t(G) * warp_bytes + size_t(G) * c_pad * 8 + size_t(c_pad) * 8;
     if (smem_f <= 200 * 1024) {
