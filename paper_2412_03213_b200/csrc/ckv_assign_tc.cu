@@ -241,6 +241,9 @@ struct TcArgs {
   uint4* fix_list;             // {unit, row, n_cand | FULL, 0}
   uint32_t fix_cap;
   uint32_t* fix_ids;           // [fix_cap][8] candidate ids
+  // k16 rows in cluster-major order (k_permute_keys): row r of the A operand
+  // is key position perm[unit][r]; nullptr = position order
+  const uint32_t* perm;
   uint32_t mode;               // experiment knob (CKV_TC_MODE): 1 = no epilogue math,
                                // 2 = no TMEM reads either (producer + MMA only)
 };
@@ -890,7 +893,9 @@ k_assign_tc2(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ C
         eps = a.eps_u[unit];
         kerr = a.kerr_u[unit];
       }
-      const uint32_t row = k.tile * TC_M + lane_row, cbeg = k.range * a.rc, range = k.range;
+      const uint32_t prow = k.tile * TC_M + lane_row, cbeg = k.range * a.rc, range = k.range;
+      // the key position of this A row (cluster-major operand after k_permute_keys)
+      const uint32_t row = a.perm ? __ldg(a.perm + size_t(unit) * a.key_rows_per_unit + prow) : prow;
       // issued now, first used after the accumulator wait (which hides it);
       // rows past n: a negative band admits no candidate (lo > block max)
       const float kn = row < a.n ? __ldg(a.knorm + size_t(unit) * a.n + row) : -1.f;
@@ -946,7 +951,10 @@ k_assign_tc2(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ C
           uint32_t inq[T2_GB];
 #pragma unroll
           for (int q = 0; q < T2_GB; ++q) {
-            inq[q] = ~below_mask32(v[q], lo);  // bit 31-x <=> v[x] >= lo
+            // a block no row of the warp has in band needs no mask (warp-
+            // uniform: pays off when the warp's rows share their clusters)
+            inq[q] = 0u;
+            if (__any_sync(0xffffffffu, bmq[q] >= lo)) inq[q] = ~below_mask32(v[q], lo);
             if (b0 + q >= nbk) inq[q] = 0u;
           }
           // branch-free pair update per block: entry {bm, first column, mask}
@@ -1350,6 +1358,36 @@ k_assign_merge(const float4* __restrict__ summ, uint32_t n_ranges, uint32_t n,
   }
 }
 
+// cluster-major fp16 operand: dst row r of a unit = src row sorted[r] (the
+// index of the latest labels, so a 128-key tile holds a few clusters and the
+// epilogue's warp-uniform block skip applies); rows >= n stay zero and map to
+// themselves.  perm[r] = the key position (ckv_kmeans.cu, once per k-means run)
+__global__ void __launch_bounds__(256)
+k_permute_keys(const uint16_t* __restrict__ k16, uint32_t n, uint32_t n_pad,
+               const uint32_t* __restrict__ sorted, uint32_t label_stride,
+               const int32_t* __restrict__ active, uint16_t* __restrict__ k16p,
+               uint32_t* __restrict__ perm) {
+  const uint32_t u = blockIdx.y;
+  if (active && !active[u]) return;
+  const uint32_t r = blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4);
+  if (r >= n_pad) return;
+  const uint32_t src = r < n ? sorted[size_t(u) * label_stride + r] : r;
+  const uint4* s4 = reinterpret_cast<const uint4*>(k16 + (size_t(u) * n_pad + src) * D);
+  uint4* d4 = reinterpret_cast<uint4*>(k16p + (size_t(u) * n_pad + r) * D);
+  const int j = threadIdx.x & 15;
+  d4[j] = r < n ? s4[j] : make_uint4(0u, 0u, 0u, 0u);
+  if (j == 0) perm[size_t(u) * n_pad + r] = src;
+}
+
+int launch_permute_keys(cudaStream_t st, const uint16_t* k16, uint32_t n, uint32_t n_pad,
+                        const uint32_t* sorted, uint32_t label_stride, uint32_t n_units,
+                        const int32_t* active, uint16_t* k16p, uint32_t* perm) {
+  k_permute_keys<<<dim3((n_pad + 15) / 16, n_units), 256, 0, st>>>(k16, n, n_pad, sorted,
+                                                                    label_stride, active, k16p, perm);
+  CKV_LAUNCH_CHECK("k_permute_keys");
+  return CKV_OK;
+}
+
 __global__ void k_compact_active(const int32_t* __restrict__ active, uint32_t n_units,
                                   int32_t* __restrict__ list, int32_t* __restrict__ count,
                                   uint32_t* __restrict__ fix_count) {
@@ -1540,7 +1578,8 @@ static int launch_tc(cudaStream_t st, const CUtensorMap& kmap, const CUtensorMap
 int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32_t n,
               uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs16,
               const float* deps, const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
-              void* scratch, size_t scratch_bytes, uint64_t* launches) {
+              void* scratch, size_t scratch_bytes, uint64_t* launches, const uint16_t* k16p,
+              const uint32_t* perm) {
   (void)scratch_bytes;
   if (key_stride % D) {
     set_error("assign_tc: key stride must be a whole number of rows");
@@ -1555,9 +1594,10 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
   // fix-up keeps scoring the original bf16 keys
   CUtensorMap kmap, dmap;
   const uint32_t rows_per_unit = s.n_pad;
-  CKV_TRY(encode_2d(&kmap, s.k16, uint64_t(n_units) * rows_per_unit, TC_M));
+  CKV_TRY(encode_2d(&kmap, k16p ? k16p : s.k16, uint64_t(n_units) * rows_per_unit, TC_M));
   CKV_TRY(encode_2d(&dmap, dirs16, uint64_t(n_units) * c_pad, TC_BOXR));
   TcArgs ta;
+  ta.perm = k16p ? perm : nullptr;
   ta.unit_list = s.list;
   ta.n_list = s.count;
   ta.n = n;
@@ -1994,6 +2034,7 @@ int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t
   CKV_TRY(encode_2d(&kmap, kperm, uint64_t(U) * npad, TC_M));
   CKV_TRY(encode_2d(&dmap, bperm, uint64_t(U) * c_pad, TC_BOXR));
   TcArgs ta;
+  ta.perm = nullptr;
   ta.unit_list = mode;  // unused with a work list
   ta.n_list = n_one;
   ta.n = n;
@@ -2029,7 +2070,7 @@ int assign_mcr(ckv_ctx* ctx, const uint16_t* keys, uint64_t key_stride, uint32_t
   ctx->launches += 3;
   // the DENSE units through the ordinary path
   CKV_TRY(assign_tc(st, keys, key_stride, n, C, c_pad, U, dirs16, deps, dirs, cur, label_stride,
-                    dense, tc_scratch, tc_bytes, &ctx->launches));
+                    dense, tc_scratch, tc_bytes, &ctx->launches, nullptr, nullptr));
   static const bool dbg = getenv("CKV_DEBUG_KMEANS") != nullptr;
   if (dbg) {
     std::vector<int32_t> md(U);

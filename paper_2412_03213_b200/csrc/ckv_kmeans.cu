@@ -463,7 +463,11 @@ int assign_tc(cudaStream_t st, const uint16_t* keys, uint64_t key_stride, uint32
               uint32_t C, uint32_t c_pad, uint32_t n_units, const uint16_t* dirs16,
               const float* deps,
               const float* dirs, int32_t* labels, uint32_t label_stride, const int32_t* active,
-              void* scratch, size_t scratch_bytes, uint64_t* launches);
+              void* scratch, size_t scratch_bytes, uint64_t* launches,
+              const uint16_t* k16p = nullptr, const uint32_t* perm = nullptr);
+int launch_permute_keys(cudaStream_t st, const uint16_t* k16, uint32_t n, uint32_t n_pad,
+                        const uint32_t* sorted, uint32_t label_stride, uint32_t n_units,
+                        const int32_t* active, uint16_t* k16p, uint32_t* perm);
 
 // ---------------------------------------------------------------------------
 // host driver
@@ -653,10 +657,22 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
   CKV_LAUNCH_CHECK("k_dirs");
   ctx->launches += 2;
 
+  // CKV_KM_PERM_AT=t (experiment, off by default): from pass t on the fp16
+  // operand is cluster-major (k_permute_keys, built once from that pass's
+  // index) so the rows of a tile share their clusters and the epilogue's
+  // warp-uniform block skip could apply; labels keep their positions.
+  // Measured at config B: 15% fewer epilogue instructions but 8% slower
+  // (the per-row perm / knorm gathers and scattered label writes; on these
+  // keys the ~50 centroids of a key's true centre are near-ties spread over
+  // many blocks, so few blocks are skipped).
+  const uint16_t* k16p = nullptr;
+  const uint32_t* perm = nullptr;
+  static const uint32_t perm_at = getenv("CKV_KM_PERM_AT")
+                                      ? uint32_t(atoi(getenv("CKV_KM_PERM_AT"))) : 0u;
   auto assign = [&](int32_t* out) -> int {
     if (use_tc)
       return assign_tc(st, a.keys, a.key_stride, n, C, c_pad, U, dirs16, deps, dirs, out, LS, active,
-                       b_tc.p, tc_bytes, &ctx->launches);
+                       b_tc.p, tc_bytes, &ctx->launches, k16p, perm);
     k_assign_exact<<<dim3((n + 127) / 128, U), 128, 0, st>>>(a.keys, a.key_stride, n, C, c_pad,
                                                             dirs, out, LS, active);
     CKV_LAUNCH_CHECK("k_assign_exact");
@@ -765,6 +781,20 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     // instead of draining on a host round trip per pass
     constexpr uint32_t KM_SYNC = 4;
     CKV_TRY(control(t, &hf[U], dbg || t % KM_SYNC == 0 || t == MI));
+    if (use_tc && perm_at && t == perm_at && !mcr_enabled() && !k16p) {
+      // b_sorted holds the index of this pass's labels (count_repair)
+      DevBuf b_k16p, b_perm;
+      if (dalloc(ctx, 39, b_k16p, size_t(U) * prep.n_pad * D * 2) == CKV_OK &&
+          dalloc(ctx, 40, b_perm, size_t(U) * prep.n_pad * 4) == CKV_OK) {
+        CKV_TRY(launch_permute_keys(st, prep.k16, n, prep.n_pad, b_sorted.as<uint32_t>(), LS, U,
+                                    active, b_k16p.as<uint16_t>(), b_perm.as<uint32_t>()));
+        ctx->launches++;
+        k16p = b_k16p.as<uint16_t>();
+        perm = b_perm.as<uint32_t>();
+      } else {
+        cudaGetLastError();  // no room for the copy: stay in position order
+      }
+    }
     if (dbg) {
       cudaEventRecord(dev_[4], st);
       cudaEventSynchronize(dev_[4]);
