@@ -1236,6 +1236,29 @@ def main():
                              f"B={B}) select_tokens+approx_attention x5, median {layer_ms:.2f} ms, "
                              f"scaled x{args.layers} layers; model = the GPU-built clusters "
                              "(bit-identical to the reference's)"}
+            # SURVEY §8(d) prefill baseline: the reference's cluster_prefill of
+            # the same layer's heads, capped at 2 iterations (3 passes per head),
+            # one head per thread: cost per head-pass at 32k
+            try:
+                kh = [np.ascontiguousarray(k, np.float32) for k in sample[3]]
+                nh = len(kh)
+                kptr = (C.c_void_p * nh)(*[k.ctypes.data for k in kh])
+                seeds_np = np.array([N.lib().ckv_mix_seed(0, 0, h) for h in range(nh)], np.uint64)
+                npass = np.zeros(1, np.uint64)
+                cms = float(Rr.lib.ref_prefill_cpu(kptr, nh, L, D, seeds_np, 2, cores, npass))
+                thr = min(cores, nh)
+                gpu_hps = passes / (prefill_ms * 1e-3)
+                cpu_hps = int(npass[0]) / (cms * 1e-3)
+                cpu["prefill"] = {
+                    "head_passes_per_s": cpu_hps, "threads": thr,
+                    "ms_per_head_pass_per_thread": cms * thr / max(1, int(npass[0])),
+                    "gpu_head_passes_per_s": gpu_hps, "speedup": gpu_hps / cpu_hps,
+                    "sample": f"cluster_prefill of {nh} heads (32k, C0={C0}) capped at 2 "
+                              f"iterations ({int(npass[0])} head-passes) in {cms:.0f} ms on {thr} "
+                              f"threads; GPU: {passes} unit-passes in the {prefill_ms:.1f} ms "
+                              "prefill"}
+            except Exception as ex:  # the decode baseline above stands
+                cpu["prefill"] = {"sample": f"failed: {ex!r}"}
         except Exception as ex:  # reported, never silently replaced
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {ex!r}"}

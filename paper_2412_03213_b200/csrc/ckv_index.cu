@@ -120,10 +120,11 @@ k_index(const int32_t* __restrict__ labels, uint32_t n_pos, uint32_t p_cap, uint
   }
   __syncthreads();
 
-  // stable scatter: warp w walks its segment in order
-  uint32_t* out = sorted_ids + size_t(u) * p_cap;
+  // stable scatter: warp w walks its segment in order (sorted_ids NULL:
+  // the caller needs only the sizes / starts / flags)
+  uint32_t* out = sorted_ids ? sorted_ids + size_t(u) * p_cap : nullptr;
   uint32_t* cur = hist + w * C;
-  for (uint32_t b0 = p0; b0 < p1; b0 += 32 * IX_BATCH) {
+  for (uint32_t b0 = p0; out && b0 < p1; b0 += 32 * IX_BATCH) {
     int32_t lb[IX_BATCH];
 #pragma unroll
     for (int k = 0; k < IX_BATCH; ++k) {

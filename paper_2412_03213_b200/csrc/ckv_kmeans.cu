@@ -680,9 +680,15 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     return CKV_OK;
   };
 
-  auto count_repair = [&](int32_t* cur, const int32_t* prev) -> int {
+  // the member lists (sorted ids) feed only a full k_update (and the opt-in
+  // MCR / permutation): once the next update is incremental the index pass
+  // skips its stable scatter, the costliest part of k_index
+  static const uint32_t incr_from_ = getenv("CKV_KM_INCR_FROM")
+                                         ? uint32_t(atoi(getenv("CKV_KM_INCR_FROM"))) : 5u;
+  auto count_repair = [&](int32_t* cur, const int32_t* prev, bool need_sorted) -> int {
+    uint32_t* srt = need_sorted ? b_sorted.as<uint32_t>() : nullptr;
     CKV_TRY(launch_index(st, U, cur, n, LS, CS, nullptr, C, b_sizes.as<uint32_t>(),
-                         b_starts.as<uint32_t>(), b_sorted.as<uint32_t>(), prev,
+                         b_starts.as<uint32_t>(), srt, prev,
                          b_changed.as<int32_t>(), active, b_empty.as<int32_t>(),
                          prev ? b_dirty.as<uint8_t>() : nullptr));
     k_repair<<<U, 256, 0, st>>>(a.keys, a.key_stride, n, C, CS, c_pad, cur, LS,
@@ -691,7 +697,7 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     CKV_LAUNCH_CHECK("k_repair");
     // re-sort (and re-compare) the units that were repaired
     CKV_TRY(launch_index(st, U, cur, n, LS, CS, nullptr, C, b_sizes.as<uint32_t>(),
-                         b_starts.as<uint32_t>(), b_sorted.as<uint32_t>(), prev,
+                         b_starts.as<uint32_t>(), srt, prev,
                          b_changed.as<int32_t>(), b_empty.as<int32_t>(), nullptr,
                          prev ? b_dirty.as<uint8_t>() : nullptr));
     ctx->launches += 3;
@@ -724,7 +730,7 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
 
   // pass 0: initial assignment, count, repair, objective
   CKV_TRY(assign(lab[0]));
-  CKV_TRY(count_repair(lab[0], nullptr));
+  CKV_TRY(count_repair(lab[0], nullptr, true));
   CKV_TRY(control(0, &hf[U], true));
 
   // CKV_DEBUG_KMEANS=1: per-phase device times of each pass on stderr
@@ -772,7 +778,8 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     else
       CKV_TRY(assign(cur));
     if (dbg) cudaEventRecord(dev_[2], st);
-    CKV_TRY(count_repair(cur, prev));
+    CKV_TRY(count_repair(cur, prev, t + 1 < std::max(2u, incr_from_) || mcr_enabled() ||
+                                        (perm_at && t == perm_at)));
     if (dbg) cudaEventRecord(dev_[3], st);
     const int32_t active_before = hf[U];
     // the host reads the active count back only every KM_SYNC passes: the
