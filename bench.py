@@ -997,7 +997,7 @@ def main():
     T = 2 * (args.warmup + args.steps) + args.e2e_steps + 2
     ctx = Context(local)
     sess_flags = (N.CKV_KM_EXACT_ONLY if args.exact_kmeans else 0) | \
-        (N.CKV_SESSION_L2_PERSIST if os.environ.get("CKV_L2_PERSIST") else 0)
+        (0 if os.environ.get("CKV_NO_L2_PERSIST") else N.CKV_SESSION_L2_PERSIST)
     sess = Session(U, G, L, T, B, retention=1, cfg=ClusterConfig(max_iters=args.max_iters),
                    kv_heads=args.kv_heads, flags=sess_flags, ctx=ctx)
     if args.trace:  # a CKVT file's heads instead of the synthetic draw
@@ -1280,7 +1280,9 @@ def main():
                                f"{args.kv_heads} kv x {G} q heads, {L} ctx, B={B}, batch 1/GPU, "
                                "R=1 cache; all layers of a step in one select + one attend launch",
                    "global_batch": world, "seq_len": L, "parallelism": f"batch-sharded x{world}",
-                   "l2": "per-step working set ~0.6 GB >> 126 MB L2 (no flush needed)"},
+                   "l2": "per-step working set ~0.6 GB >> 126 MB L2 (no flush needed); "
+                         "the 54 MB of centroids sit in a persisting L2 window "
+                         "(CKV_SESSION_L2_PERSIST; CKV_NO_L2_PERSIST=1 disables)"},
         "select_attend_us_per_step": step_ms * 1e3,
         "roofline": {"bound": "hbm", "kernel": "k_attend", "achieved": att_gbs, "peak": hbm,
                      "unit": "GB/s", "frac": att_gbs / hbm, "traffic": ncu_traffic("k_attend"),
