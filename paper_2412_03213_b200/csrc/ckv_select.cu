@@ -216,7 +216,10 @@ __device__ __forceinline__ void select_head(
   const float* cu = cents + size_t(unit) * desc.c_cap * D;
   const uint32_t* sz = SM_META ? sizes : sizes + size_t(unit) * desc.c_cap;
   const uint32_t* stt = SM_META ? starts : starts + size_t(unit) * (desc.c_cap + 1);
-  const float4* qh4 = reinterpret_cast<const float4*>(q + size_t(h) * D);
+  // SM_META: q points at the head's row in shared memory (the fused kernel
+  // staged it), else at the q array in global memory
+  const float4* qh4 = reinterpret_cast<const float4*>(SM_META ? q : q + size_t(h) * D);
+  auto qld = [&](int j4) -> float4 { if constexpr (SM_META) return qh4[j4]; else return __ldg(qh4 + j4); };
   const bool exhaustive_req = (desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) != 0;
   // budget 0 takes no cluster (selection.hpp:91: the loop breaks at once);
   // the exhaustive path still ranks every cluster for CKV_SEL_FULL_RANK
@@ -365,7 +368,7 @@ __device__ __forceinline__ void select_head(
             const float4* row = reinterpret_cast<const float4*>(&stage[lane][0]);
 #pragma unroll 8
             for (int j4 = 0; j4 < D / 4; ++j4) {
-              const float4 m = row[j4], qq = __ldg(qh4 + j4);
+              const float4 m = row[j4], qq = qld(j4);
               acc = __fma_rn(double(qq.x), double(m.x), acc);
               acc = __fma_rn(double(qq.y), double(m.y), acc);
               acc = __fma_rn(double(qq.z), double(m.z), acc);
@@ -414,7 +417,7 @@ __device__ __forceinline__ void select_head(
         double acc = 0.0;
 #pragma unroll 4
         for (int j4 = 0; j4 < D / 4; ++j4) {
-          const float4 m = __ldg(row + j4), qq = __ldg(qh4 + j4);
+          const float4 m = __ldg(row + j4), qq = qld(j4);
           acc = __fma_rn(double(qq.x), double(m.x), acc);
           acc = __fma_rn(double(qq.y), double(m.y), acc);
           acc = __fma_rn(double(qq.z), double(m.z), acc);
@@ -696,16 +699,15 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   if (wid < G && mode != 1) cpre = cache_prefetch(unit * G + wid, cache);
   const float* qu = q + size_t(unit) * G * D;
   // 8 lanes per centroid row (lane sub holds float4 columns sub, sub+8, +16,
-  // +24: 128 contiguous bytes per row per load), 4 rows per warp step
+  // +24: 128 contiguous bytes per row per load), 4 rows per warp step.
+  // The unit's G q rows are read ONCE (warp g reads row g: over PCIe in the
+  // session's zero-copy step, where 8 warps each re-reading them cost ~8x
+  // the bytes) into shared memory, then every warp takes its operand there.
+  __shared__ __align__(16) float q_s[G][D];
   const int sub = lane & 7, rsel = lane >> 3;
-  float4 qv[G][4];
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      qv[g][k] = __ldg(reinterpret_cast<const float4*>(qu + size_t(g) * D) + sub + 8 * k);
   if (wid < G) {
     const float4 qw = __ldg(reinterpret_cast<const float4*>(qu + size_t(wid) * D) + lane);
+    reinterpret_cast<float4*>(q_s[wid])[lane] = qw;
     const float s2 = warp_sum(qw.x * qw.x + qw.y * qw.y + qw.z * qw.z + qw.w * qw.w);
     if (lane == 0) qn2[wid] = s2;
     // q read from mapped host memory (the session's zero-copy step): leave a
@@ -713,6 +715,11 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     if (q_copy) reinterpret_cast<float4*>(q_copy + (size_t(unit) * G + wid) * D)[lane] = qw;
   }
   __syncthreads();
+  float4 qv[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qv[g][k] = reinterpret_cast<const float4*>(q_s[g])[sub + 8 * k];
   float qnrm[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) qnrm[g] = SEL_ERR * sqrtf(qn2[g]);
@@ -765,7 +772,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   __syncthreads();
   if (wid >= G || mode == 1) return;
   const uint32_t h = unit * G + wid;
-  select_head<true>(h, desc, p2, row_base, q, cents, av_s + size_t(wid) * c_pad,
+  select_head<true>(h, desc, p2, row_base, q_s[wid], cents, av_s + size_t(wid) * c_pad,
                     ae_s + size_t(wid) * c_pad, n_clusters, sz_s, st_s, sorted_ids, token_ids,
                     rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, nullptr, cache,
                     cpre, smraw + size_t(wid) * warp_bytes, wsa[wid]);
