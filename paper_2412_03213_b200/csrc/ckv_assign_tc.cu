@@ -662,7 +662,10 @@ k_assign_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CU
 constexpr int T2_CW = 256;                       // columns per TMEM chunk buffer
 constexpr int T2_NBUF = 512 / T2_CW;             // chunk buffers (512 TMEM columns)
 constexpr int T2_CG = T2_NBUF;                   // epilogue warps per lane quarter: one per buffer
-constexpr int T2_GB = 4;                         // blocks a warp holds in registers at once
+#ifndef CKV_T2_GB
+#define CKV_T2_GB 2
+#endif
+constexpr int T2_GB = CKV_T2_GB;                 // blocks a warp holds in registers at once
 constexpr int T2_THREADS = (2 + 4 * T2_CG) * 32;
 struct T2Bars {
   uint64_t a_full[4], a_empty[4];
@@ -947,7 +950,10 @@ k_assign_tc2(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ C
             const float t2c = max3f(t1[6], t1[7], t1[8]), t2d = fmaxf(t1[9], t1[10]);
             bmq[q] = fmaxf(max3f(t2a, t2b, t2c), t2d);
           }
-          const float lo = fmaxf(max3f(e0s, bmq[0], bmq[1]), max3f(bmq[2], bmq[3], -INFINITY)) - band;
+          float mall = e0s;
+#pragma unroll
+          for (int q = 0; q < T2_GB; ++q) mall = fmaxf(mall, bmq[q]);
+          const float lo = mall - band;
           uint32_t inq[T2_GB];
 #pragma unroll
           for (int q = 0; q < T2_GB; ++q) {
