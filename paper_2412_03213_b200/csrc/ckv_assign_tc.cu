@@ -92,14 +92,41 @@ __device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mb_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
+// Watchdog for the pipelines' barrier waits: a wait still unsatisfied after
+// ~4 s of device time reports the barrier and traps, so a pipeline bug ends
+// the launch with an error instead of hanging the device.
+__device__ __noinline__ void mb_wait_timeout(const uint64_t* b, uint32_t parity) {
+  printf("[ckv] mbarrier wait timed out: block %d thread %d barrier smem+%u parity %u\n",
+         int(blockIdx.x), int(threadIdx.x), su32(b), parity);
+  __trap();
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct MbWatch {
+  uint32_t n = 0;
+  uint64_t t0 = 0;
+  __device__ __forceinline__ void tick(const uint64_t* b, uint32_t parity) {
+    if ((++n & 4095u) == 0u) {
+      const uint64_t t = global_ns();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) mb_wait_timeout(b, parity);
+    }
+  }
+};
 __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
   uint32_t done;
-  do {
+  MbWatch wd;
+  for (;;) {
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
         "selp.u32 %0, 1, 0, p; }"
         : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
-  } while (!done);
+    if (done) break;
+    wd.tick(b, parity);
+  }
 }
 // bit 31-j of the result set <=> x[j] < lo (the sign of the rounded x[j] - lo;
 // x[j] >= lo gives a difference >= +0).  FADD2 + four interleaved SHF chains.
@@ -694,8 +721,10 @@ __device__ __forceinline__ void mb_wait_sleep(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
       : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
+  MbWatch wd;
   while (!done) {
     __nanosleep(NS);
+    wd.tick(b, parity);
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");

@@ -136,12 +136,37 @@ struct __align__(128) AttSmem {
 struct ItemInfo {
   uint32_t h, s, e0, e1;
 };
+// StepSync (ckv_internal.cuh): wait until the selection has published q head
+// h for this step.  The acquire makes its run / count stores visible; they
+// are then read through L2 (__ldcg), never a possibly stale L1 line.
+__device__ __noinline__ void ready_timeout(uint32_t h, uint32_t want) {
+  printf("[ckv] k_attend: q head %u never published (want %u)\n", h, want);
+  __trap();
+}
+__device__ __forceinline__ void wait_ready(const uint32_t* ready, uint32_t h, uint32_t want) {
+  uint32_t v, n = 0;
+  uint64_t t0 = 0;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + h) : "memory");
+    if (v == want) return;
+    __nanosleep(64);
+    if ((++n & 1023u) == 0u) {  // watchdog: ~4 s
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) ready_timeout(h, want);
+    }
+  }
+}
 __device__ __forceinline__ ItemInfo item_info(uint32_t i, uint32_t splits,
-                                              const uint32_t* n_tokens) {
+                                              const uint32_t* n_tokens,
+                                              const uint32_t* ready = nullptr,
+                                              uint32_t want = 0u) {
   ItemInfo it;
   it.h = i / splits;
   it.s = i % splits;
-  const uint32_t nt = n_tokens[it.h];
+  if (ready) wait_ready(ready, it.h, want);
+  const uint32_t nt = __ldcg(n_tokens + it.h);
   it.e0 = uint32_t((uint64_t(nt) * it.s) / splits);
   it.e1 = uint32_t((uint64_t(nt) * (it.s + 1)) / splits);
   return it;
@@ -153,7 +178,8 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
          const uint16_t* __restrict__ K, const uint16_t* __restrict__ V,
          const uint32_t* __restrict__ rows, ckv_runs runs, const uint32_t* __restrict__ n_tokens,
          float* __restrict__ out, float* __restrict__ logits_ws, float* __restrict__ part,
-         uint32_t* __restrict__ tickets, float* __restrict__ weights, float* __restrict__ lse) {
+         uint32_t* __restrict__ tickets, float* __restrict__ weights, float* __restrict__ lse,
+         const uint32_t* __restrict__ ready, const uint32_t* __restrict__ epoch) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   AttSmem& sm = *reinterpret_cast<AttSmem*>(sm_raw);
   const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
@@ -174,14 +200,23 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
   // up their barriers) while the selection kernel drains; its run lists and
   // token counts are read only after this wait (a no-op otherwise).  The next
   // kernel may launch now: it waits for this grid before its dependent reads.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // StepSync: no grid-wide wait; each item waits for its q head instead (the
+  // selection is still running).  Everything else read here was written by
+  // kernels that completed before the selection passed its own wait.
+  uint32_t want = 0u;
+  if (ready) {
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(want) : "l"(epoch) : "memory");
+    ++want;
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (wid == AT_CWARPS) {
     // ======================= producer warp =====================================
     uint32_t st = 0, ph = 0, qk = 0;  // ring stage / parity, query-ring counter
     for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x, ++qk) {
-      const ItemInfo it = item_info(i, splits, n_tokens);
+      const ItemInfo it = item_info(i, splits, n_tokens, ready, want);
       const uint32_t unit = it.h / desc.group;
       const uint16_t* Ku = K + size_t(unit) * desc.p_cap * D;
       const uint16_t* Vu = V + size_t(unit) * desc.p_cap * D;
@@ -191,14 +226,14 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       const uint32_t* gro = nullptr;
       const uint32_t* grr = nullptr;
       if (!rows) {
-        nrun = runs.count[it.h];
+        nrun = __ldcg(runs.count + it.h);
         gro = runs.off + size_t(it.h) * (runs.run_cap + 1);
         grr = runs.row + size_t(it.h) * runs.run_cap;
         staged = nrun <= uint32_t(AT_RUNS);
         __syncwarp();  // the previous item's runs are no longer read
         if (staged) {
-          for (uint32_t r = lane; r <= nrun; r += 32) sm.roff[r] = __ldg(gro + r);
-          for (uint32_t r = lane; r < nrun; r += 32) sm.rrow[r] = __ldg(grr + r);
+          for (uint32_t r = lane; r <= nrun; r += 32) sm.roff[r] = __ldcg(gro + r);
+          for (uint32_t r = lane; r < nrun; r += 32) sm.rrow[r] = __ldcg(grr + r);
         }
         __syncwarp();
       }
@@ -206,6 +241,9 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
         const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
         mbar_wait(&sm.qempty[qs], qp ^ 1);
         mbar_expect_tx(&sm.qfull[qs], D * 4);
+        // the selection may have just written q's device copy (zero-copy
+        // step): order those generic-proxy stores before this bulk copy
+        if (ready) asm volatile("fence.proxy.async.global;" ::: "memory");
         bulk_g2s(sm.q[qs], q + size_t(it.h) * D, D * 4, &sm.qfull[qs]);
         const uint32_t* rowlist = rows ? rows + size_t(it.h) * desc.sel_cap : nullptr;
         uint32_t r = 0;
@@ -213,7 +251,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
           uint32_t lo = 0, hi = nrun;
           while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if ((staged ? sm.roff[mid] : __ldg(gro + mid)) <= it.e0) lo = mid; else hi = mid;
+            if ((staged ? sm.roff[mid] : __ldcg(gro + mid)) <= it.e0) lo = mid; else hi = mid;
           }
           r = lo;
         }
@@ -227,10 +265,10 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
               row = __ldg(rowlist + x);
               n = 1;
             } else {
-              while ((staged ? sm.roff[r + 1] : __ldg(gro + r + 1)) <= x) ++r;
-              const uint32_t ro = staged ? sm.roff[r] : __ldg(gro + r);
-              const uint32_t rend = staged ? sm.roff[r + 1] : __ldg(gro + r + 1);
-              row = (staged ? sm.rrow[r] : __ldg(grr + r)) + (x - ro);
+              while ((staged ? sm.roff[r + 1] : __ldcg(gro + r + 1)) <= x) ++r;
+              const uint32_t ro = staged ? sm.roff[r] : __ldcg(gro + r);
+              const uint32_t rend = staged ? sm.roff[r + 1] : __ldcg(gro + r + 1);
+              row = (staged ? sm.rrow[r] : __ldcg(grr + r)) + (x - ro);
               n = min(te, rend) - x;
             }
             bulk_g2s(&sm.k[st][x - e][0], Ku + size_t(row) * D, n * D * 2, &sm.full[st]);
@@ -243,6 +281,8 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       st = __shfl_sync(0xffffffffu, st, 0);
       ph = __shfl_sync(0xffffffffu, ph, 0);
     }
+    // StepSync: this grid never completes before the selection grid
+    if (ready) asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
 
@@ -252,7 +292,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
   const float qscale = 1.4426950408889634f * rsqrtf(float(D));  // exp -> exp2
   uint32_t st = 0, ph = 0, qk = 0;
   for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x, ++qk) {
-    const ItemInfo it = item_info(i, splits, n_tokens);
+    const ItemInfo it = item_info(i, splits, n_tokens, ready, want);
     const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
     mbar_wait(&sm.qfull[qs], qp);
     float qv[8];
@@ -391,7 +431,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       out[size_t(it.h) * D + t] = lse && !(L > 0.f) ? 0.f : o * (lse ? invL : 1.f / L);
       if (lse && t == 0) lse[it.h] = L > 0.f ? MM + __log2f(L) : -INFINITY;
       if (WEIGHTS) {
-        const uint32_t nt = n_tokens[it.h];
+        const uint32_t nt = __ldcg(n_tokens + it.h);
         const float* lg = logits_ws + size_t(it.h) * desc.sel_cap;
         float* wo = weights + size_t(it.h) * desc.sel_cap;
         for (uint32_t j = t; j < nt; j += AT_CWARPS * 32)
@@ -400,6 +440,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       if (t == 0) tickets[it.h] = 0;  // re-arm for the next launch
     }
   }
+  if (ready) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // work items that fill the GPU twice over at 3 resident CTAs per SM
@@ -439,7 +480,8 @@ uint32_t attend_splits(const ckv_attend_desc& d) {
 int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
                   const uint16_t* K, const uint16_t* V, const uint32_t* rows,
                   const ckv_runs& runs, const uint32_t* n_tokens, float* out, float* weights,
-                  float* logits_ws, float* part, uint32_t* tickets, float* lse) {
+                  float* logits_ws, float* part, uint32_t* tickets, float* lse,
+                  const StepSync* sync) {
   if (!rows && !runs.row) { set_error("attend: need rows or runs"); return CKV_EINVAL; }
   if (desc.n_q == 0 || desc.max_tokens == 0) return CKV_OK;
   const uint32_t splits = attend_splits(desc);
@@ -468,13 +510,18 @@ int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // StepSync only for run lists (the selection publishes per q head)
+  const bool use_sync = sync && sync->published && !rows;
+  const uint32_t* rdy = use_sync ? sync->ready : nullptr;
+  const uint32_t* ep = use_sync ? sync->epoch : nullptr;
   if (weights)
     CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_attend<true>, desc, splits, q, K, V, rows, runs,
-                                    n_tokens, out, logits_ws, part, tickets, weights, lse));
+                                    n_tokens, out, logits_ws, part, tickets, weights, lse, rdy,
+                                    ep));
   else
     CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_attend<false>, desc, splits, q, K, V, rows, runs,
                                     n_tokens, out, static_cast<float*>(nullptr), part, tickets,
-                                    static_cast<float*>(nullptr), lse));
+                                    static_cast<float*>(nullptr), lse, rdy, ep));
   CKV_LAUNCH_CHECK("k_attend");
   return CKV_OK;
 }

@@ -206,15 +206,19 @@ __global__ void k_append_clusters(const float* __restrict__ tmp_c, const int32_t
 }
 
 // append one token's K/V row per unit at position pos
+// (and advance the StepSync epoch: the step's selection / attention are done)
 __global__ void k_append_kv(const uint16_t* __restrict__ kn, const uint16_t* __restrict__ vn,
                             uint16_t* __restrict__ K, uint16_t* __restrict__ V, uint32_t pos,
-                            uint32_t p_cap) {
+                            uint32_t p_cap, uint32_t* __restrict__ epoch) {
   const uint32_t u = blockIdx.x, j = threadIdx.x;  // 16 threads x 16 B
+  if (epoch && u == 0 && j == 0) ++*epoch;
   const uint4* ks = reinterpret_cast<const uint4*>(kn + size_t(u) * D);
   const uint4* vs = reinterpret_cast<const uint4*>(vn + size_t(u) * D);
   reinterpret_cast<uint4*>(K + (size_t(u) * p_cap + pos) * D)[j] = ks[j];
   reinterpret_cast<uint4*>(V + (size_t(u) * p_cap + pos) * D)[j] = vs[j];
 }
+
+__global__ void k_epoch_advance(uint32_t* epoch) { ++*epoch; }
 
 // cluster-major relayout of the prompt KV (after the prefill index):
 // dst row r = src position  r              for r < sink or r >= labeled_end
@@ -896,6 +900,10 @@ struct ckv_session {
   uint16_t *tmpK = nullptr, *tmpV = nullptr;  // decode-batch relayout staging
   float* part = nullptr;
   uint32_t* tickets = nullptr;
+  // StepSync (ckv_internal.cuh): per-q-head selection -> attention flags
+  // and their epoch; off with CKV_SESSION_NO_STEPSYNC=1
+  uint32_t *step_ready = nullptr, *step_epoch = nullptr;
+  StepSync sync{};
   float *q_dev = nullptr, *out_dev = nullptr;
   uint16_t *kn_dev = nullptr, *vn_dev = nullptr;
   ckv_cache* cache = nullptr;
@@ -1032,6 +1040,8 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   rc |= salloc(&s->ranked, size_t(s->n_q) * s->c_cap);
   rc |= salloc(&s->part, attend_part_floats(s->n_q, s->sel_cap));
   rc |= salloc(&s->tickets, s->n_q);
+  rc |= salloc(&s->step_ready, s->n_q);
+  rc |= salloc(&s->step_epoch, 1);
   rc |= salloc(&s->q_dev, size_t(s->n_q) * D);
   rc |= salloc(&s->out_dev, size_t(s->n_q) * D);
   rc |= salloc(&s->kn_dev, size_t(s->U) * D);
@@ -1097,6 +1107,8 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   }
   if (rc) { ckv_session_destroy(s); return CKV_ENOMEM; }
   cudaMemsetAsync(s->tickets, 0, size_t(s->n_q) * 4, ctx->stream);
+  cudaMemsetAsync(s->step_ready, 0, size_t(s->n_q) * 4, ctx->stream);
+  cudaMemsetAsync(s->step_epoch, 0, 4, ctx->stream);
   cudaMemsetAsync(s->n_clusters, 0, size_t(s->U) * 4, ctx->stream);
   if (d->flags & CKV_SESSION_L2_PERSIST) {  // device-wide; restored by the last user
     int maxp = 0;
@@ -1136,6 +1148,7 @@ int ckv_session_destroy(ckv_session* s) {
   cudaFree(s->runs.row); cudaFree(s->runs.off); cudaFree(s->runs.count);
   cudaFree(s->tmpV); cudaFree(s->n_tokens); cudaFree(s->n_taken); cudaFree(s->trimmed);
   cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
+  cudaFree(s->step_ready); cudaFree(s->step_epoch);
   cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
   if (s->side) { cudaStreamSynchronize(s->side); cudaStreamDestroy(s->side); }
   if (s->sel_stream) { cudaStreamSynchronize(s->sel_stream); cudaStreamDestroy(s->sel_stream); }
@@ -1231,7 +1244,8 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
 // (its bulk copies stay on HBM).  The two halves take a stream each so the
 // batched step can overlap one slice's selection with another's attention.
 static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, uint32_t nu,
-                                const float* q_dev, float* q_copy, bool force_fused) {
+                                const float* q_dev, float* q_copy, bool force_fused,
+                                StepSync* sync = nullptr) {
   const uint32_t G = s->d.group, h0 = u0 * G;
   ckv_select_desc sd{};
   sd.n_q = nu * G;
@@ -1265,13 +1279,15 @@ static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
                         s->starts + size_t(u0) * (s->c_cap + 1), s->sorted + size_t(u0) * s->p_cap,
                         want_ids ? s->token_ids + size_t(h0) * s->sel_cap : nullptr, nullptr, runs,
                         sd.row_base, s->n_tokens + h0, s->n_taken + h0, s->trimmed + h0,
-                        s->ranked + size_t(h0) * s->c_cap, nullptr, cache, s->sel_scratch, qc));
+                        s->ranked + size_t(h0) * s->c_cap, nullptr, cache, s->sel_scratch, qc,
+                        sync));
   s->ctx->launches += 2;
   return CKV_OK;
 }
 
 static int session_attend_slice(ckv_session* s, cudaStream_t st, uint32_t u0, uint32_t nu,
-                                const float* q_dev, float* out_dev, float* q_copy) {
+                                const float* q_dev, float* out_dev, float* q_copy,
+                                const StepSync* sync = nullptr) {
   const uint32_t G = s->d.group, h0 = u0 * G;
   const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);
   ckv_runs runs = s->runs;
@@ -1298,7 +1314,8 @@ static int session_attend_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
   }
   CKV_TRY(launch_attend(st, ad, qc ? qc : qs, s->K + size_t(u0) * s->p_cap * D,
                         s->V + size_t(u0) * s->p_cap * D, nullptr, runs, s->n_tokens + h0,
-                        out_dev + size_t(h0) * D, nullptr, nullptr, s->part, s->tickets));
+                        out_dev + size_t(h0) * D, nullptr, nullptr, s->part, s->tickets,
+                        nullptr, sync));
   s->ctx->launches++;
   return CKV_OK;
 }
@@ -1321,8 +1338,18 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
     static const bool split = getenv("CKV_SESSION_SPLIT") != nullptr;
     const uint32_t u1 = s->U / 8;
     if (!split || s->tiered || !s->sel_stream || u1 < 8) {
-      CKV_TRY(session_select_slice(s, st, 0, s->U, q_dev, q_copy, false));
-      return session_attend_slice(s, st, 0, s->U, q_dev, out_dev, q_copy);
+      // StepSync: the attention starts on each q head as soon as its
+      // selection is published, overlapping the selection's tail (not with
+      // the tier fetch between them)
+      static const bool no_sync = getenv("CKV_SESSION_NO_STEPSYNC") != nullptr;
+      StepSync* sy = nullptr;
+      if (!no_sync && !s->tiered) {
+        s->sync.ready = s->step_ready;
+        s->sync.epoch = s->step_epoch;
+        sy = &s->sync;
+      }
+      CKV_TRY(session_select_slice(s, st, 0, s->U, q_dev, q_copy, false, sy));
+      return session_attend_slice(s, st, 0, s->U, q_dev, out_dev, q_copy, sy);
     }
     CKV_CUDA_TRY(cudaEventRecord(s->ev_sel_fork, st));
     CKV_CUDA_TRY(cudaStreamWaitEvent(s->sel_stream, s->ev_sel_fork, 0));
@@ -1352,7 +1379,12 @@ int ckv_session_set_layer_units(ckv_session* s, uint32_t layer_units) {
 
 int ckv_session_attend_only(ckv_session* s, const float* q_dev, float* out_dev) {
   if (!s->prefilled) { set_error("session: prefill first"); return CKV_EINVAL; }
-  return session_select_attend(s, q_dev, out_dev);
+  CKV_TRY(session_select_attend(s, q_dev, out_dev));
+  // no append follows: advance the StepSync epoch here
+  k_epoch_advance<<<1, 1, 0, s->ctx->stream>>>(s->step_epoch);
+  CKV_LAUNCH_CHECK("k_epoch_advance");
+  s->ctx->launches++;
+  return CKV_OK;
 }
 
 // The decode-batch k-means reports kmeans_cosine's input errors
@@ -1474,7 +1506,7 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
   }
   CKV_TRY(session_select_attend(s, qd, od, q_copy));
   // append this step's token (harness.hpp:318-320)
-  k_append_kv<<<s->U, 16, 0, st>>>(kd, vd, s->K, s->V, s->n_ctx, s->p_cap);
+  k_append_kv<<<s->U, 16, 0, st>>>(kd, vd, s->K, s->V, s->n_ctx, s->p_cap, s->step_epoch);
   CKV_LAUNCH_CHECK("k_append_kv");
   s->ctx->launches++;
   s->n_ctx++;

@@ -102,12 +102,26 @@ struct CacheDev {
   uint32_t* ring;                // [n_slots][2] = head, len
   unsigned long long* counters;  // [n_slots][4]
 };
+// Per-q-head hand-off from the selection to the attention of one step, so
+// the attention need not wait for the whole selection grid: the selection
+// publishes ready[h] = *epoch + 1 (release) once head h's runs and token
+// count are stored, the attention polls it (acquire) per work item.  epoch
+// is a device counter the step's last kernel (k_append_kv) advances, so the
+// protocol holds under graph replay.  published: set by launch_select when
+// the path it took publishes (the fused kernel); the attention uses the flags
+// only then.
+struct StepSync {
+  uint32_t* ready = nullptr;         // [n_q]
+  uint32_t* epoch = nullptr;         // [1]
+  bool published = false;
+};
 int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const float* cents, const uint32_t* n_clusters, const uint32_t* sizes,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
                   uint32_t* rows, const ckv_runs& runs, uint32_t row_base, uint32_t* n_tokens,
                   uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
-                  const CacheDev& cache, void* scratch, float* q_copy = nullptr);
+                  const CacheDev& cache, void* scratch, float* q_copy = nullptr,
+                  StepSync* sync = nullptr);
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap);
 int launch_score_approx(cudaStream_t st, uint32_t G, uint32_t n_units, const float* q,
                         const float* cents, const uint32_t* counts, uint32_t c_cap,
@@ -120,7 +134,8 @@ int launch_cache_invalidate(cudaStream_t st, const CacheDev& cache, uint32_t slo
 int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
                   const uint16_t* K, const uint16_t* V, const uint32_t* rows,
                   const ckv_runs& runs, const uint32_t* n_tokens, float* out, float* weights,
-                  float* logits_ws, float* part, uint32_t* tickets, float* lse = nullptr);
+                  float* logits_ws, float* part, uint32_t* tickets, float* lse = nullptr,
+                  const StepSync* sync = nullptr);
 size_t attend_part_floats(uint32_t n_q, uint32_t max_tokens);
 int ctx_scratch(ckv_ctx* ctx, int slot, size_t bytes, bool zero_new, void** out);
 int attend_scratch(ckv_ctx* ctx, const ckv_attend_desc& d, bool weights, float** part,

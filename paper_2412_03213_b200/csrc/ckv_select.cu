@@ -202,7 +202,7 @@ __device__ __forceinline__ void select_head(
     uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
     uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
     double* __restrict__ scores_out, const CacheDev& cache, const SelCachePre& cpre,
-    unsigned char* wbase, WarpSel& ws) {
+    unsigned char* wbase, WarpSel& ws, uint32_t* ready = nullptr, uint32_t ready_val = 0u) {
   const int lane = lane_id();
   dbg_stamp(h, 0);
   const uint32_t unit = h / desc.group;
@@ -561,6 +561,15 @@ __device__ __forceinline__ void select_head(
     n_taken_out[h] = taken;
     trimmed_out[h] = trimmed;
   }
+  // hand head h to the attention (StepSync): every lane's run / count stores
+  // are fenced before lane 0's release of the flag
+  if (ready) {
+    __threadfence();
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + h), "r"(ready_val)
+                   : "memory");
+  }
   // ---- cache (cache.hpp:38-57) -------------------------------------------------
   // lookup of the taken clusters in the R retained bitmaps, then the taken
   // set replaces the oldest slot (the ring was prefetched with the bitmaps)
@@ -666,7 +675,8 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
                uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
                uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
                uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
-               CacheDev cache, uint32_t warp_bytes, uint32_t mode, float* __restrict__ q_copy) {
+               CacheDev cache, uint32_t warp_bytes, uint32_t mode, float* __restrict__ q_copy,
+               uint32_t* __restrict__ ready, const uint32_t* __restrict__ epoch) {
   static_assert(G <= SF_WARPS, "one select warp per head");
   const uint32_t unit = blockIdx.x;
   const int lane = lane_id(), wid = warp_id();
@@ -677,6 +687,13 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   // (the last step's append / clustering) drains; nothing is read before it
   // completes (a no-op for a normal launch)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // StepSync: the attention may launch now (every CTA of this grid is
+  // resident once all have passed here); it waits per q head on ready[]
+  uint32_t ready_val = 0u;
+  if (ready) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    ready_val = *epoch + 1u;
+  }
   float* av_s = reinterpret_cast<float*>(smraw + size_t(G) * warp_bytes);  // [G][c_pad]
   float* ae_s = av_s + size_t(G) * c_pad;                                  // [G][c_pad]
   uint32_t* sz_s = reinterpret_cast<uint32_t*>(ae_s + size_t(G) * c_pad);  // [c_pad]
@@ -775,7 +792,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   select_head<true>(h, desc, p2, row_base, q_s[wid], cents, av_s + size_t(wid) * c_pad,
                     ae_s + size_t(wid) * c_pad, n_clusters, sz_s, st_s, sorted_ids, token_ids,
                     rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, nullptr, cache,
-                    cpre, smraw + size_t(wid) * warp_bytes, wsa[wid]);
+                    cpre, smraw + size_t(wid) * warp_bytes, wsa[wid], ready, ready_val);
 }
 
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap) {
@@ -832,8 +849,9 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
                   uint32_t* rows, const ckv_runs& runs, uint32_t row_base, uint32_t* n_tokens,
                   uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
-                  const CacheDev& cache, void* scratch, float* q_copy) {
+                  const CacheDev& cache, void* scratch, float* q_copy, StepSync* sync) {
   const uint32_t G = desc.group;
+  if (sync) sync->published = false;
   if (G < 1 || desc.n_q % G || !(G == 1 || G == 2 || G == 4 || G == 8)) {
     set_error("select: group must be 1, 2, 4 or 8 and divide n_q");
     return CKV_EINVAL;
@@ -863,8 +881,13 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                              (const void*)k_select_fused<4>, (const void*)k_select_fused<8>})
         CKV_CUDA_TRY(smem_optin(fn, 200 * 1024));
 #define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
-    token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode, q_copy
+    token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode, q_copy, \
+    rdy, ep
       static const uint32_t sel_mode = getenv("CKV_SEL_MODE") ? uint32_t(atoi(getenv("CKV_SEL_MODE"))) : 0u;
+      // mode 1 (experiment: scoring only) publishes nothing
+      const bool pub = sync && sync->ready && sync->epoch && sel_mode != 1;
+      uint32_t* rdy = pub ? sync->ready : nullptr;
+      const uint32_t* ep = pub ? sync->epoch : nullptr;
       // CKV_SEL_L2_PERSIST: the centroids (read by every step, ~60 MB at
       // config B) are accessed through a persisting L2 window, so the KV
       // stream of the attention between two steps does not evict them and the
@@ -906,6 +929,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       }
 #undef CKV_SF_ARGS
       CKV_LAUNCH_CHECK("k_select_fused");
+      if (pub) sync->published = true;
       return CKV_OK;
     }
   }
