@@ -303,7 +303,9 @@ def score_clusters(q: np.ndarray, model: ClusterModel, ctx: Context | None = Non
     return _select(ctx, q, model, index, 1, (), want_scores=True)[1]
 
 
-def _select(ctx, q, model, index, budget, recency, want_scores=False):
+def _select(ctx, q, model, index, budget, recency, want_scores=False, full_rank=True):
+    """full_rank=False: the decode path's selection (no full ranking: only
+    the taken clusters' ranks are written)."""
     dm = _DeviceModel(ctx, model, index)
     dev = ctx.device
     q = np.ascontiguousarray(q, np.float32).reshape(1, D)
@@ -317,7 +319,8 @@ def _select(ctx, q, model, index, budget, recency, want_scores=False):
     rnk = torch.zeros(dm.c_cap, dtype=torch.int32, device=dev)
     sc = torch.zeros(dm.c_cap, dtype=torch.float64, device=dev) if want_scores else None
     desc = N.SelectDesc(1, 1, budget, model.sink_count, dm.p_cap, dm.c_cap, sel_cap, 0, 0,
-                        N.CKV_SEL_FULL_RANK | (N.CKV_SEL_SCORES if want_scores else 0), 0)
+                        (N.CKV_SEL_FULL_RANK if full_rank else 0) |
+                        (N.CKV_SEL_SCORES if want_scores else 0), 0)
     check(lib().ckv_select(ctx.h, C.byref(desc), qd.data_ptr(), dm.cents.data_ptr(),
                            dm.ncl.data_ptr(), dm.sizes.data_ptr(), dm.starts.data_ptr(),
                            dm.sorted.data_ptr(), tok.data_ptr(), None, None, ntok.data_ptr(),

@@ -83,6 +83,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// the KV rows are read once per step: evict_first, so the stream does not
+// push the selection's centroids (evict_last) out of L2
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes,
+                                                uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ float ex2(float x) {  // 2^x, ex2.approx (-inf -> +0)
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -215,6 +225,8 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
   if (wid == AT_CWARPS) {
     // ======================= producer warp =====================================
     uint32_t st = 0, ph = 0, qk = 0;  // ring stage / parity, query-ring counter
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x, ++qk) {
       const ItemInfo it = item_info(i, splits, n_tokens, ready, want);
       const uint32_t unit = it.h / desc.group;
@@ -271,8 +283,8 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
               row = (staged ? sm.rrow[r] : __ldcg(grr + r)) + (x - ro);
               n = min(te, rend) - x;
             }
-            bulk_g2s(&sm.k[st][x - e][0], Ku + size_t(row) * D, n * D * 2, &sm.full[st]);
-            bulk_g2s(&sm.v[st][x - e][0], Vu + size_t(row) * D, n * D * 2, &sm.full[st]);
+            bulk_g2s_stream(&sm.k[st][x - e][0], Ku + size_t(row) * D, n * D * 2, &sm.full[st], pol);
+            bulk_g2s_stream(&sm.v[st][x - e][0], Vu + size_t(row) * D, n * D * 2, &sm.full[st], pol);
             x += n;
           }
           if (++st == AT_STAGES) { st = 0; ph ^= 1; }

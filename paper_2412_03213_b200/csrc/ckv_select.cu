@@ -138,6 +138,7 @@ k_score_approx(const float* __restrict__ q, const float* __restrict__ cents,
 struct WarpSel {  // per-warp static bookkeeping
   uint32_t cand[SW_MAXCAND];
   unsigned long long ckey[SW_MAXCAND];
+  float ca[SW_MAXCAND], ce[SW_MAXCAND];  // the candidates' approximate scores / bounds
   uint32_t hist[256];
 };
 
@@ -348,15 +349,46 @@ __device__ __forceinline__ void select_head(
         if (c < C) in = ar[k] + er[k] >= lower;
         const unsigned bal = __ballot_sync(0xffffffffu, in);
         const uint32_t pos = nc + __popc(bal & ((1u << lane) - 1u));
-        if (in && pos < uint32_t(SW_MAXCAND)) ws.cand[pos] = c;
+        if (in && pos < uint32_t(SW_MAXCAND)) {
+          ws.cand[pos] = c;
+          ws.ca[pos] = ar[k];
+          ws.ce[pos] = er[k];
+        }
         nc += __popc(bal);
       }
       fast = nc <= uint32_t(SW_MAXCAND);
       __syncwarp();
+      // ---- 3a. disjoint bounds: the approximate order IS the exact order ------
+      // s_c lies in [a_c - E_c, a_c + E_c]; when no two candidates' intervals
+      // meet, s orders S exactly as a does (and no two s tie), so the f64
+      // re-score is skipped.  Rank by a (index breaks ties), then test
+      // adjacent intervals in that order: if any two intervals meet, some
+      // adjacent pair does (an interval meeting a non-neighbour also meets an
+      // interval between them).  The test runs in f64, where a_i - a_j and
+      // E_i + E_j of fp32 values are exact.
+      bool approx_order = false;
+      if (fast) {
+        float* sa = reinterpret_cast<float*>(ws.ckey);  // [nc] a in rank order
+        float* se = sa + SW_MAXCAND;                     // [nc] E in rank order
+        for (uint32_t i = lane; i < nc; i += 32) {
+          const float ai = ws.ca[i];
+          uint32_t r = 0;
+          for (uint32_t j = 0; j < nc; ++j) r += ws.ca[j] > ai || (ws.ca[j] == ai && j < i);
+          ids[r] = ws.cand[i];
+          sa[r] = ai;
+          se[r] = ws.ce[i];
+        }
+        __syncwarp();
+        bool meet = false;
+        for (uint32_t r = lane; r + 1 < nc; r += 32)
+          meet |= double(sa[r]) - double(se[r]) <= double(sa[r + 1]) + double(se[r + 1]);
+        approx_order = !__any_sync(0xffffffffu, meet);
+        __syncwarp();
+      }
       if (fast) {
         dbg_stamp(h, 1);
         // ---- 3. exact f64 re-score of S (rows staged through smem) ---------------
-        for (uint32_t b = 0; b < nc; b += SW_STAGE) {
+        for (uint32_t b = 0; !approx_order && b < nc; b += SW_STAGE) {
           const uint32_t nb = min(uint32_t(SW_STAGE), nc - b);
           for (uint32_t r = 0; r < nb; ++r)
             cp_async16_sel(&stage[r][4 * lane], cu + size_t(ws.cand[b + r]) * D + 4 * lane, true);
@@ -379,7 +411,7 @@ __device__ __forceinline__ void select_head(
           __syncwarp();
         }
         // exact rank of every candidate within S -> ids[rank]
-        for (uint32_t i = lane; i < nc; i += 32) {
+        for (uint32_t i = lane; !approx_order && i < nc; i += 32) {
           const unsigned long long ki = ws.ckey[i];
           const uint32_t ci = ws.cand[i];
           uint32_t r = 0;
@@ -665,6 +697,48 @@ k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_ba
 // centroids instead of 1 per head.
 // ---------------------------------------------------------------------------
 constexpr int SF_WARPS = 8;
+// the unit's centroid block streams through a ring of SF_NS bulk-copied
+// stages of SF_ROWS rows (TMA bulk copies: many bytes in flight per CTA
+// without registers; the ring aliases the selection warps' buffers, which
+// are free while scoring)
+constexpr int SF_ROWS = 32;                          // rows per stage (16 KB)
+constexpr int SF_NS = 5;                             // stages
+constexpr size_t SF_RING = size_t(SF_NS) * SF_ROWS * D * 4;
+__device__ __forceinline__ uint32_t sel_su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void sel_mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sel_su32(b)), "r"(n));
+}
+__device__ __forceinline__ void sel_mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sel_su32(b)) : "memory");
+}
+__device__ __forceinline__ void sel_mb_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(sel_su32(b)), "r"(parity) : "memory");
+  } while (!done);
+}
+// rows [r0, r0 + n) of the unit's centroid block into a ring stage.  The
+// centroids are re-read every step: the copy marks them evict_last in L2 (the
+// attention's one-pass KV stream is marked evict_first), so they stay
+// resident between steps.
+__device__ __forceinline__ void sel_stage_rows(float* dst, const float* cu, uint32_t r0,
+                                               uint32_t n, uint64_t* bar) {
+  const uint32_t bytes = n * D * 4;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sel_su32(bar)),
+               "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(sel_su32(dst)), "l"(cu + size_t(r0) * D), "r"(bytes),
+      "r"(sel_su32(bar)), "l"(pol)
+      : "memory");
+}
 
 template <int G>
 __global__ void __launch_bounds__(SF_WARPS * 32, 2)  // two units per SM: one wave at config B
@@ -694,11 +768,24 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     ready_val = *epoch + 1u;
   }
-  float* av_s = reinterpret_cast<float*>(smraw + size_t(G) * warp_bytes);  // [G][c_pad]
+  if (wid < G) dbg_stamp(unit * G + wid, 7);
+  const size_t ring_bytes = max(size_t(G) * warp_bytes, SF_RING);
+  float* ring = reinterpret_cast<float*>(smraw);                          // [SF_NS][SF_ROWS][D]
+  float* av_s = reinterpret_cast<float*>(smraw + ring_bytes);              // [G][c_pad]
   float* ae_s = av_s + size_t(G) * c_pad;                                  // [G][c_pad]
   uint32_t* sz_s = reinterpret_cast<uint32_t*>(ae_s + size_t(G) * c_pad);  // [c_pad]
   uint32_t* st_s = sz_s + c_pad;                                           // [c_pad]
   const uint32_t C = n_clusters[unit];
+  const float* cu = cents + size_t(unit) * desc.c_cap * D;
+  __shared__ uint64_t full[SF_NS], empty[SF_NS];
+  const uint32_t nch = (C + SF_ROWS - 1) / SF_ROWS;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < SF_NS; ++k) { sel_mb_init(&full[k], 1); sel_mb_init(&empty[k], SF_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint32_t k = 0; k < nch && k < uint32_t(SF_NS); ++k)
+      sel_stage_rows(ring + size_t(k) * SF_ROWS * D, cu, k * SF_ROWS,
+                     min(uint32_t(SF_ROWS), C - k * SF_ROWS), &full[k]);
+  }
   // the unit's sizes / starts land in shared memory while the warps score
   // (4-byte cp.async: the per-unit arrays are not 16-byte aligned)
   {
@@ -740,19 +827,33 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   float qnrm[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) qnrm[g] = SEL_ERR * sqrtf(qn2[g]);
-  const float* cu = cents + size_t(unit) * desc.c_cap * D;
-  for (uint32_t c0 = uint32_t(wid) * 8; c0 < C; c0 += SF_WARPS * 8) {  // 2 steps of 4 rows
-    float4 m[2][4];
+  // stage k: rows [32k, 32k + 32); warp w takes rows 4w..4w+3 of it (8
+  // lanes per row, lane sub holds float4 columns sub, sub+8, +16, +24)
+  for (uint32_t k = 0; k < nch; ++k) {
+    const uint32_t stg = k % SF_NS, ph = (k / SF_NS) & 1u;
+    const float* rs = ring + size_t(stg) * SF_ROWS * D;
+    const uint32_t c0 = k * SF_ROWS + uint32_t(wid) * 4;
+    float4 m[1][4];
+    sel_mb_wait(&full[stg], ph);
+    {
+      const uint32_t rr = uint32_t(wid) * 4 + rsel;
 #pragma unroll
-    for (int st2 = 0; st2 < 2; ++st2) {
-      const uint32_t c = c0 + 4 * st2 + rsel;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        m[st2][k] = c < C ? __ldg(reinterpret_cast<const float4*>(cu + size_t(c) * D) + sub + 8 * k)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q4 = 0; q4 < 4; ++q4)
+        m[0][q4] = c0 + rsel < C ? reinterpret_cast<const float4*>(rs + size_t(rr) * D)[sub + 8 * q4]
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // the stage is in registers: release it; thread 0 refills it with
+    // stage k + SF_NS once every warp has released it
+    __syncwarp();
+    if (lane == 0) sel_mb_arrive(&empty[stg]);
+    if (threadIdx.x == 0 && k + SF_NS < nch) {
+      sel_mb_wait(&empty[stg], ph);
+      const uint32_t kn = k + SF_NS;
+      sel_stage_rows(ring + size_t(stg) * SF_ROWS * D, cu, kn * SF_ROWS,
+                     min(uint32_t(SF_ROWS), C - kn * SF_ROWS), &full[stg]);
     }
 #pragma unroll
-    for (int st2 = 0; st2 < 2; ++st2) {
+    for (int st2 = 0; st2 < 1; ++st2) {
       float acc[G], mn = 0.f;
 #pragma unroll
       for (int g = 0; g < G; ++g) acc[g] = 0.f;
@@ -772,7 +873,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
       }
-      const uint32_t c = c0 + 4 * st2 + rsel;
+      const uint32_t c = c0 + rsel;
       if (c < C && sub < G) {  // lane sub writes head sub (G <= 8)
         float a = acc[0];
 #pragma unroll
@@ -798,6 +899,27 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap) {
   const uint32_t c_pad = (c_cap + 31) / 32 * 32;
   return size_t(n_q) * c_pad * 8 + 64;  // aval + aerr
+}
+
+// the fused kernel's per-head stamps: 7 = CTA start, 0 = scores ready,
+// 1 = order known, 3 = head done
+static void dbg_report_fused(uint32_t n, const unsigned long long* dbuf, float ms) {
+  std::vector<unsigned long long> hb(size_t(n) * 8);
+  cudaMemcpy(hb.data(), dbuf, hb.size() * 8, cudaMemcpyDeviceToHost);
+  double sc = 0, pop = 0, rest = 0;
+  unsigned long long t_lo = ~0ull, t_hi = 0, s_hi = 0;
+  for (uint32_t h = 0; h < n; ++h) {
+    const unsigned long long* x = &hb[size_t(h) * 8];
+    sc += double(x[0] - x[7]);
+    pop += double(x[1] - x[0]);
+    rest += double(x[3] - x[1]);
+    t_lo = std::min(t_lo, x[7]);
+    t_hi = std::max(t_hi, x[3]);
+    s_hi = std::max(s_hi, x[7]);
+  }
+  fprintf(stderr, "[k_select_fused dbg] %.1f us | per head us: score %.2f pop %.2f rest %.2f | "
+          "span %.2f us, last CTA start +%.2f us\n", ms * 1e3, sc / n * 1e-3, pop / n * 1e-3,
+          rest / n * 1e-3, double(t_hi - t_lo) * 1e-3, double(s_hi - t_lo) * 1e-3);
 }
 
 static void dbg_report(uint32_t n, const unsigned long long* dbuf, float k1_ms, float k2_ms) {
@@ -875,7 +997,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   const bool few_units = (desc.flags & CKV_SEL_FORCE_FUSED) ? false
                          : few_env >= 0 ? few_env != 0 : units * 2 < uint32_t(num_sms());
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused && !few_units) {
-    const size_t smem_f = size_t(G) * warp_bytes + size_t(G) * c_pad * 8 + size_t(c_pad) * 8;
+    const size_t smem_f = std::max(size_t(G) * warp_bytes, SF_RING) + size_t(G) * c_pad * 8 +
+                          size_t(c_pad) * 8;
     if (smem_f <= 200 * 1024) {
       for (const void* fn : {(const void*)k_select_fused<1>, (const void*)k_select_fused<2>,
                              (const void*)k_select_fused<4>, (const void*)k_select_fused<8>})
@@ -921,6 +1044,12 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         cfg.numAttrs = persist && bytes ? 2 : 1;
         if (cfg.numAttrs == 1) cfg.attrs = attr + 1;
       }
+      unsigned long long* fbuf = nullptr;
+      if (dbg) {
+        cudaMalloc(&fbuf, size_t(desc.n_q) * 64);
+        cudaMemset(fbuf, 0, size_t(desc.n_q) * 64);
+        cudaMemcpyToSymbol(g_sel_dbg, &fbuf, sizeof(fbuf));
+      }
       switch (G) {
         case 1: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<1>, CKV_SF_ARGS)); break;
         case 2: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<2>, CKV_SF_ARGS)); break;
@@ -929,6 +1058,17 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       }
 #undef CKV_SF_ARGS
       CKV_LAUNCH_CHECK("k_select_fused");
+      if (dbg) {
+        cudaEventRecord(ev[1], st);
+        cudaEventSynchronize(ev[1]);
+        float a = 0;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        dbg_report_fused(desc.n_q, fbuf, a);
+        unsigned long long z = 0;
+        cudaMemcpyToSymbol(g_sel_dbg, &z, sizeof(z));
+        cudaFree(fbuf);
+        for (auto& e : ev) cudaEventDestroy(e);
+      }
       if (pub) sync->published = true;
       return CKV_OK;
     }

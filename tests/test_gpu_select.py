@@ -73,6 +73,41 @@ def test_select_ties_lowest_id(gpu_ctx):
     assert list(r.token_ids) == [4, 5]
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_select_near_ties_vs_oracle(gpu_ctx, seed):
+    """Clusters in near-tied triples (copies a few ulps apart): their score
+    bounds overlap, so the selection must take the exact f64 path for those
+    and still match the oracle's ranking bit for bit; budgets land inside
+    the triples.  Random clusters elsewhere take the disjoint-bounds path."""
+    from paper_2412_03213_b200 import api
+    rng = np.random.default_rng(40 + seed)
+    base = rng.standard_normal((60, 128)).astype(np.float32)
+    cents = np.repeat(base, 3, axis=0)
+    for r in range(1, cents.shape[0], 3):
+        j = rng.integers(0, 128, 3)
+        cents[r, j] = np.nextafter(cents[r, j], np.float32(np.inf))
+        cents[r + 1, j] = np.nextafter(cents[r + 1, j], np.float32(-np.inf))
+    C = cents.shape[0]
+    n = 6000
+    lab = rng.integers(0, C, n).astype(np.int32)
+    m = _model(lab, cents)
+    ix = api.build_index(m)
+    for t in range(6):
+        q = base[rng.integers(0, 60)] + 0.05 * rng.standard_normal(128).astype(np.float32)
+        for budget in (17, 100, 333):
+            r = port().select_tokens(q, cents, lab, 0, budget, np.zeros(0, np.uint32))
+            g = api.select_tokens(q, m, ix, budget)  # exhaustive (full ranking)
+            assert np.array_equal(g.ranked_clusters, r.ranked_clusters)
+            # the decode path's fast selection (candidate set + bounds)
+            f = api._select(gpu_ctx, q, m, ix, budget, (), full_rank=False)[0]
+            for x in (g, f):
+                k = x.n_clusters_taken
+                assert k == r.n_clusters_taken
+                assert np.array_equal(x.ranked_clusters[:k], r.ranked_clusters[:k])
+                assert x.trimmed_from_last == r.trimmed_from_last
+                assert np.array_equal(x.token_ids, r.token_ids)
+
+
 @pytest.mark.parametrize("budget", [1, 64, 1024, 5000])
 def test_select_vs_oracle_config_a(gpu_ctx, budget):
     from paper_2412_03213_b200 import api
