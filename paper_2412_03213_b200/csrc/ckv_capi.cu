@@ -1243,6 +1243,11 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
 // the selection leaves a device copy of it there and the attention reads that
 // (its bulk copies stay on HBM).  The two halves take a stream each so the
 // batched step can overlap one slice's selection with another's attention.
+static bool session_no_stepsync() {
+  static const bool off = getenv("CKV_SESSION_NO_STEPSYNC") != nullptr;
+  return off;
+}
+
 static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, uint32_t nu,
                                 const float* q_dev, float* q_copy, bool force_fused,
                                 StepSync* sync = nullptr) {
@@ -1274,13 +1279,19 @@ static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
   }
   const float* qs = q_dev + size_t(h0) * D;
   float* qc = q_copy ? q_copy + size_t(h0) * D : nullptr;
+  StepSync ls;  // the slice's flags (q heads from h0)
+  if (sync) {
+    ls = *sync;
+    ls.ready += h0;
+  }
   CKV_TRY(launch_select(st, sd, qs, s->cents + size_t(u0) * s->c_cap * D,
                         s->n_clusters + u0, s->sizes + size_t(u0) * s->c_cap,
                         s->starts + size_t(u0) * (s->c_cap + 1), s->sorted + size_t(u0) * s->p_cap,
                         want_ids ? s->token_ids + size_t(h0) * s->sel_cap : nullptr, nullptr, runs,
                         sd.row_base, s->n_tokens + h0, s->n_taken + h0, s->trimmed + h0,
                         s->ranked + size_t(h0) * s->c_cap, nullptr, cache, s->sel_scratch, qc,
-                        sync));
+                        sync ? &ls : nullptr));
+  if (sync) sync->published = ls.published;
   s->ctx->launches += 2;
   return CKV_OK;
 }
@@ -1312,10 +1323,15 @@ static int session_attend_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
     s->ctx->launches++;
     runs = tr;
   }
+  StepSync ls;
+  if (sync) {
+    ls = *sync;
+    ls.ready += h0;
+  }
   CKV_TRY(launch_attend(st, ad, qc ? qc : qs, s->K + size_t(u0) * s->p_cap * D,
                         s->V + size_t(u0) * s->p_cap * D, nullptr, runs, s->n_tokens + h0,
                         out_dev + size_t(h0) * D, nullptr, nullptr, s->part, s->tickets,
-                        nullptr, sync));
+                        nullptr, sync ? &ls : nullptr));
   s->ctx->launches++;
   return CKV_OK;
 }
@@ -1341,9 +1357,8 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
       // StepSync: the attention starts on each q head as soon as its
       // selection is published, overlapping the selection's tail (not with
       // the tier fetch between them)
-      static const bool no_sync = getenv("CKV_SESSION_NO_STEPSYNC") != nullptr;
       StepSync* sy = nullptr;
-      if (!no_sync && !s->tiered) {
+      if (!session_no_stepsync() && !s->tiered) {
         s->sync.ready = s->step_ready;
         s->sync.epoch = s->step_epoch;
         sy = &s->sync;
@@ -1360,10 +1375,17 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
     CKV_CUDA_TRY(cudaStreamWaitEvent(st, s->ev_sel_join, 0));
     return session_attend_slice(s, st, u1, s->U - u1, q_dev, out_dev, q_copy);
   }
+  // layer slices: disjoint q heads, so one epoch per step serves them all
+  StepSync* sy = nullptr;
+  if (!session_no_stepsync() && !s->tiered) {
+    s->sync.ready = s->step_ready;
+    s->sync.epoch = s->step_epoch;
+    sy = &s->sync;
+  }
   for (uint32_t u0 = 0; u0 < s->U; u0 += lu) {
     const uint32_t nu = std::min(lu, s->U - u0);
-    CKV_TRY(session_select_slice(s, st, u0, nu, q_dev, q_copy, false));
-    CKV_TRY(session_attend_slice(s, st, u0, nu, q_dev, out_dev, q_copy));
+    CKV_TRY(session_select_slice(s, st, u0, nu, q_dev, q_copy, false, sy));
+    CKV_TRY(session_attend_slice(s, st, u0, nu, q_dev, out_dev, q_copy, sy));
   }
   return CKV_OK;
 }

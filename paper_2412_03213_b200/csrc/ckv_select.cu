@@ -672,7 +672,8 @@ k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_ba
               uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
               uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
               uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
-              double* __restrict__ scores_out, CacheDev cache, uint32_t warp_bytes) {
+              double* __restrict__ scores_out, CacheDev cache, uint32_t warp_bytes,
+              uint32_t* __restrict__ ready, const uint32_t* __restrict__ epoch) {
   const int wid = warp_id();
   const uint32_t h = blockIdx.x * SW_WARPS + wid;
   if (h >= desc.n_q) return;
@@ -682,10 +683,11 @@ k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_ba
   const SelCachePre cpre = cache_prefetch(h, cache);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t ready_val = ready ? *epoch + 1u : 0u;  // StepSync (see k_select_fused)
   select_head<false>(h, desc, p2, row_base, q, cents, aval + size_t(h) * c_pad,
                      aerr + size_t(h) * c_pad, n_clusters, sizes, starts, sorted_ids, token_ids,
                      rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, scores_out,
-                     cache, cpre, smraw + size_t(wid) * warp_bytes, wsa[wid]);
+                     cache, cpre, smraw + size_t(wid) * warp_bytes, wsa[wid], ready, ready_val);
 }
 
 // ---------------------------------------------------------------------------
@@ -867,13 +869,43 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
           acc[g] = fmaf(x.x, y.x, fmaf(x.y, y.y, fmaf(x.z, y.z, fmaf(x.w, y.w, acc[g]))));
         }
       }
+      const uint32_t c = c0 + rsel;
+      if constexpr (G <= 4) {
+        // reduce-scatter over the row's 8 lanes: {acc[0..G), mn, 0...} -> lane
+        // sub holds the sum of value sub (7 shuffles instead of 3 (G + 1)),
+        // then mn is broadcast from lane 4 of the group
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = i < G ? acc[i] : (i == 4 ? mn : 0.f);
+        float w[4], x2[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool hi = sub & 4;
+          w[i] = (hi ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, hi ? v[i] : v[i + 4], 4);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const bool hi = sub & 2;
+          x2[i] = (hi ? w[i + 2] : w[i]) + __shfl_xor_sync(0xffffffffu, hi ? w[i] : w[i + 2], 2);
+        }
+        const bool hi = sub & 1;
+        const float y = (hi ? x2[1] : x2[0]) + __shfl_xor_sync(0xffffffffu, hi ? x2[0] : x2[1], 1);
+        const float mnf = __shfl_sync(0xffffffffu, y, (lane & ~7) | 4);
+        if (c < C && sub < G) {
+          float qn = qnrm[0];
+#pragma unroll
+          for (int g = 1; g < G; ++g) if (sub == g) qn = qnrm[g];
+          av_s[size_t(sub) * c_pad + c] = y;
+          ae_s[size_t(sub) * c_pad + c] = fmaf(qn, sqrtf(mnf), 1e-30f);
+        }
+        continue;
+      }
 #pragma unroll
       for (int o = 4; o > 0; o >>= 1) {
         mn += __shfl_xor_sync(0xffffffffu, mn, o);
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
       }
-      const uint32_t c = c0 + rsel;
       if (c < C && sub < G) {  // lane sub writes head sub (G <= 8)
         float a = acc[0];
 #pragma unroll
@@ -1121,10 +1153,17 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
     a2[0].val.programmaticStreamSerializationAllowed = 1;
     c2.attrs = a2;
     c2.numAttrs = 1;
+    // StepSync as in the fused kernel (not for the parity API's full ranking)
+    const bool pub = sync && sync->ready && sync->epoch &&
+                     !(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES));
+    uint32_t* rdy = pub ? sync->ready : nullptr;
+    const uint32_t* ep = pub ? sync->epoch : nullptr;
     CKV_CUDA_TRY(cudaLaunchKernelEx(&c2, k_select_warp, desc, p2, c_pad, row_base, q, cents,
                                     static_cast<const float*>(aval), static_cast<const float*>(aerr),
                                     n_clusters, sizes, starts, sorted_ids, token_ids, rows, runs,
-                                    n_tokens, n_taken, trimmed, ranked, scores, cache, warp_bytes));
+                                    n_tokens, n_taken, trimmed, ranked, scores, cache, warp_bytes,
+                                    rdy, ep));
+    if (pub) sync->published = true;
   }
   CKV_LAUNCH_CHECK("k_select_warp");
   if (dbg) {
