@@ -742,7 +742,11 @@ __device__ __forceinline__ void sel_stage_rows(float* dst, const float* cu, uint
       : "memory");
 }
 
-template <int G>
+// NC > 1 (few units, e.g. one layer's launch): a cluster of NC CTAs per
+// unit; CTA r scores the ring chunks r, r + NC, ... and stores its scores
+// straight into the leader CTA's shared memory (DSMEM), then the leader's
+// G warps select after one cluster barrier.
+template <int G, int NC>
 __global__ void __launch_bounds__(SF_WARPS * 32, 2)  // two units per SM: one wave at config B
 k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_base,
                const float* __restrict__ q, const float* __restrict__ cents,
@@ -754,7 +758,10 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
                CacheDev cache, uint32_t warp_bytes, uint32_t mode, float* __restrict__ q_copy,
                uint32_t* __restrict__ ready, const uint32_t* __restrict__ epoch) {
   static_assert(G <= SF_WARPS, "one select warp per head");
-  const uint32_t unit = blockIdx.x;
+  const uint32_t unit = blockIdx.x / NC;
+  uint32_t crank = 0;
+  if constexpr (NC > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const bool leader = crank == 0;
   const int lane = lane_id(), wid = warp_id();
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ WarpSel wsa[G];
@@ -770,7 +777,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     ready_val = *epoch + 1u;
   }
-  if (wid < G) dbg_stamp(unit * G + wid, 7);
+  if (leader && wid < G) dbg_stamp(unit * G + wid, 7);
   const size_t ring_bytes = max(size_t(G) * warp_bytes, SF_RING);
   float* ring = reinterpret_cast<float*>(smraw);                          // [SF_NS][SF_ROWS][D]
   float* av_s = reinterpret_cast<float*>(smraw + ring_bytes);              // [G][c_pad]
@@ -780,17 +787,31 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   const uint32_t C = n_clusters[unit];
   const float* cu = cents + size_t(unit) * desc.c_cap * D;
   __shared__ uint64_t full[SF_NS], empty[SF_NS];
+  // this CTA's ring chunks: global chunk crank + NC j for j < nloc
   const uint32_t nch = (C + SF_ROWS - 1) / SF_ROWS;
+  const uint32_t nloc = nch > crank ? (nch - crank + NC - 1) / NC : 0u;
   if (threadIdx.x == 0) {
     for (int k = 0; k < SF_NS; ++k) { sel_mb_init(&full[k], 1); sel_mb_init(&empty[k], SF_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (uint32_t k = 0; k < nch && k < uint32_t(SF_NS); ++k)
-      sel_stage_rows(ring + size_t(k) * SF_ROWS * D, cu, k * SF_ROWS,
-                     min(uint32_t(SF_ROWS), C - k * SF_ROWS), &full[k]);
+    for (uint32_t j = 0; j < nloc && j < uint32_t(SF_NS); ++j) {
+      const uint32_t k = crank + j * NC;
+      sel_stage_rows(ring + size_t(j) * SF_ROWS * D, cu, k * SF_ROWS,
+                     min(uint32_t(SF_ROWS), C - k * SF_ROWS), &full[j]);
+    }
   }
+  // the scores go to the leader's copy of av_s / ae_s (its own for NC = 1)
+  auto put_score = [&](float* p, float v) {
+    if constexpr (NC > 1) {
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(sel_su32(p)));
+      asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
+    } else {
+      *p = v;
+    }
+  };
   // the unit's sizes / starts land in shared memory while the warps score
   // (4-byte cp.async: the per-unit arrays are not 16-byte aligned)
-  {
+  if (leader) {
     const uint32_t* szg = sizes + size_t(unit) * desc.c_cap;
     const uint32_t* stg = starts + size_t(unit) * (desc.c_cap + 1);
     for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
@@ -802,7 +823,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
   SelCachePre cpre{{0u, 0u, 0u, 0u}, 0u, 0u, 0ull, false};
-  if (wid < G && mode != 1) cpre = cache_prefetch(unit * G + wid, cache);
+  if (leader && wid < G && mode != 1) cpre = cache_prefetch(unit * G + wid, cache);
   const float* qu = q + size_t(unit) * G * D;
   // 8 lanes per centroid row (lane sub holds float4 columns sub, sub+8, +16,
   // +24: 128 contiguous bytes per row per load), 4 rows per warp step.
@@ -818,7 +839,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     if (lane == 0) qn2[wid] = s2;
     // q read from mapped host memory (the session's zero-copy step): leave a
     // device copy for the attention kernel
-    if (q_copy) reinterpret_cast<float4*>(q_copy + (size_t(unit) * G + wid) * D)[lane] = qw;
+    if (q_copy && leader) reinterpret_cast<float4*>(q_copy + (size_t(unit) * G + wid) * D)[lane] = qw;
   }
   __syncthreads();
   float4 qv[G][4];
@@ -831,8 +852,9 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   for (int g = 0; g < G; ++g) qnrm[g] = SEL_ERR * sqrtf(qn2[g]);
   // stage k: rows [32k, 32k + 32); warp w takes rows 4w..4w+3 of it (8
   // lanes per row, lane sub holds float4 columns sub, sub+8, +16, +24)
-  for (uint32_t k = 0; k < nch; ++k) {
-    const uint32_t stg = k % SF_NS, ph = (k / SF_NS) & 1u;
+  for (uint32_t j = 0; j < nloc; ++j) {
+    const uint32_t k = crank + j * NC;
+    const uint32_t stg = j % SF_NS, ph = (j / SF_NS) & 1u;
     const float* rs = ring + size_t(stg) * SF_ROWS * D;
     const uint32_t c0 = k * SF_ROWS + uint32_t(wid) * 4;
     float4 m[1][4];
@@ -848,9 +870,9 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     // stage k + SF_NS once every warp has released it
     __syncwarp();
     if (lane == 0) sel_mb_arrive(&empty[stg]);
-    if (threadIdx.x == 0 && k + SF_NS < nch) {
+    if (threadIdx.x == 0 && j + SF_NS < nloc) {
       sel_mb_wait(&empty[stg], ph);
-      const uint32_t kn = k + SF_NS;
+      const uint32_t kn = k + SF_NS * NC;
       sel_stage_rows(ring + size_t(stg) * SF_ROWS * D, cu, kn * SF_ROWS,
                      min(uint32_t(SF_ROWS), C - kn * SF_ROWS), &full[stg]);
     }
@@ -895,8 +917,8 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
           float qn = qnrm[0];
 #pragma unroll
           for (int g = 1; g < G; ++g) if (sub == g) qn = qnrm[g];
-          av_s[size_t(sub) * c_pad + c] = y;
-          ae_s[size_t(sub) * c_pad + c] = fmaf(qn, sqrtf(mnf), 1e-30f);
+          put_score(av_s + size_t(sub) * c_pad + c, y);
+          put_score(ae_s + size_t(sub) * c_pad + c, fmaf(qn, sqrtf(mnf), 1e-30f));
         }
         continue;
       }
@@ -913,13 +935,20 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
         float qn = qnrm[0];
 #pragma unroll
         for (int g = 1; g < G; ++g) if (sub == g) qn = qnrm[g];
-        av_s[size_t(sub) * c_pad + c] = a;
-        ae_s[size_t(sub) * c_pad + c] = fmaf(qn, sqrtf(mn), 1e-30f);
+        put_score(av_s + size_t(sub) * c_pad + c, a);
+        put_score(ae_s + size_t(sub) * c_pad + c, fmaf(qn, sqrtf(mn), 1e-30f));
       }
     }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
+  if constexpr (NC > 1) {
+    // every CTA's remote score stores are visible to the leader after this
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+    if (!leader) return;
+  } else {
+    __syncthreads();
+  }
   if (wid >= G || mode == 1) return;
   const uint32_t h = unit * G + wid;
   select_head<true>(h, desc, p2, row_base, q_s[wid], cents, av_s + size_t(wid) * c_pad,
@@ -1026,15 +1055,23 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   // a layer-sized launch (few units) scores with many CTAs per unit instead
   static const bool unfused = getenv("CKV_SELECT_UNFUSED") != nullptr;
   static const int few_env = getenv("CKV_SEL_FEW") ? atoi(getenv("CKV_SEL_FEW")) : -1;
+  // few units: a cluster of nc CTAs per unit (k_select_fused<G, NC>)
+  uint32_t nc = 1;
+  while (nc < 8 && units * nc * 2 <= uint32_t(num_sms())) nc *= 2;
+  static const int nc_env = getenv("CKV_SEL_NC") ? atoi(getenv("CKV_SEL_NC")) : 0;
+  if (nc_env == 1 || nc_env == 2 || nc_env == 4 || nc_env == 8) nc = uint32_t(nc_env);
+  if (desc.flags & CKV_SEL_FORCE_FUSED) nc = 1;
   const bool few_units = (desc.flags & CKV_SEL_FORCE_FUSED) ? false
-                         : few_env >= 0 ? few_env != 0 : units * 2 < uint32_t(num_sms());
+                         : few_env >= 0 ? few_env != 0 : (units * 2 < uint32_t(num_sms()) && nc == 1);
   if (!(desc.flags & (CKV_SEL_FULL_RANK | CKV_SEL_SCORES)) && !unfused && !few_units) {
     const size_t smem_f = std::max(size_t(G) * warp_bytes, SF_RING) + size_t(G) * c_pad * 8 +
                           size_t(c_pad) * 8;
     if (smem_f <= 200 * 1024) {
-      for (const void* fn : {(const void*)k_select_fused<1>, (const void*)k_select_fused<2>,
-                             (const void*)k_select_fused<4>, (const void*)k_select_fused<8>})
+#define CKV_SF_FNS(NC_) (const void*)k_select_fused<1, NC_>, (const void*)k_select_fused<2, NC_>, \
+    (const void*)k_select_fused<4, NC_>, (const void*)k_select_fused<8, NC_>
+      for (const void* fn : {CKV_SF_FNS(1), CKV_SF_FNS(2), CKV_SF_FNS(4), CKV_SF_FNS(8)})
         CKV_CUDA_TRY(smem_optin(fn, 200 * 1024));
+#undef CKV_SF_FNS
 #define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
     token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode, q_copy, \
     rdy, ep
@@ -1048,15 +1085,20 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       // stream of the attention between two steps does not evict them and the
       // next select reads them from L2 instead of HBM.
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(units);
+      cfg.gridDim = dim3(units * nc);
       cfg.blockDim = dim3(SF_WARPS * 32);
       cfg.dynamicSmemBytes = smem_f;
       cfg.stream = st;
-      cudaLaunchAttribute attr[2];
+      // attr[0] the optional L2 window, [1] PDL, [2] the cluster shape
+      cudaLaunchAttribute attr[3];
       attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[1].val.programmaticStreamSerializationAllowed = 1;
+      attr[2].id = cudaLaunchAttributeClusterDimension;
+      attr[2].val.clusterDim.x = nc;
+      attr[2].val.clusterDim.y = 1;
+      attr[2].val.clusterDim.z = 1;
       cfg.attrs = attr + 1;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = 2;
       if (desc.flags & CKV_SEL_L2_PERSIST) {
         int dev_w = 0, v = 0;
         cudaGetDevice(&dev_w);
@@ -1073,8 +1115,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.attrs = attr;
-        cfg.numAttrs = persist && bytes ? 2 : 1;
-        if (cfg.numAttrs == 1) cfg.attrs = attr + 1;
+        cfg.numAttrs = persist && bytes ? 3 : 2;
+        if (cfg.numAttrs == 2) cfg.attrs = attr + 1;
       }
       unsigned long long* fbuf = nullptr;
       if (dbg) {
@@ -1082,12 +1124,20 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         cudaMemset(fbuf, 0, size_t(desc.n_q) * 64);
         cudaMemcpyToSymbol(g_sel_dbg, &fbuf, sizeof(fbuf));
       }
-      switch (G) {
-        case 1: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<1>, CKV_SF_ARGS)); break;
-        case 2: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<2>, CKV_SF_ARGS)); break;
-        case 4: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<4>, CKV_SF_ARGS)); break;
-        default: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<8>, CKV_SF_ARGS)); break;
+#define CKV_SF_CASE(NC_)                                                                     \
+  switch (G) {                                                                               \
+    case 1: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<1, NC_>, CKV_SF_ARGS)); break; \
+    case 2: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<2, NC_>, CKV_SF_ARGS)); break; \
+    case 4: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<4, NC_>, CKV_SF_ARGS)); break; \
+    default: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<8, NC_>, CKV_SF_ARGS)); break; \
+  }
+      switch (nc) {
+        case 1: CKV_SF_CASE(1) break;
+        case 2: CKV_SF_CASE(2) break;
+        case 4: CKV_SF_CASE(4) break;
+        default: CKV_SF_CASE(8) break;
       }
+#undef CKV_SF_CASE
 #undef CKV_SF_ARGS
       CKV_LAUNCH_CHECK("k_select_fused");
       if (dbg) {
