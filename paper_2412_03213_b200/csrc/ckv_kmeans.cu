@@ -1157,6 +1157,8 @@ k_kmeans_small(const uint16_t* __restrict__ keys, uint64_t key_stride, uint32_t 
       const int ch = __syncthreads_or(tid < int(rows) && my != prev[tid]);
       if (!ch) { converged = 1; it = t; break; }
       if (t == max_iters) { it = t; break; }
+    } else {
+      __syncthreads();  // every repair-loop read of cnt[] before it is rewritten below
     }
     // ---- update_centroids (clustering.hpp:205-218) --------------------------
     // members of each cluster in position order: per-warp counts, their
