@@ -501,8 +501,9 @@ int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
   static int per_sm_dev[64];  // resident CTAs per SM, per device (0 = not queried yet)
   int dev = 0;
   CKV_CUDA_TRY(cudaGetDevice(&dev));
-  for (const void* fn : {(const void*)k_attend<false>, (const void*)k_attend<true>})
-    CKV_CUDA_TRY(smem_optin(fn, int(smem), true));
+  // k_attend<false> always (the occupancy query below uses it)
+  CKV_CUDA_TRY(smem_optin((const void*)k_attend<false>, int(smem), true));
+  if (weights) CKV_CUDA_TRY(smem_optin((const void*)k_attend<true>, int(smem), true));
   int per_sm = per_sm_dev[dev & 63];
   if (per_sm == 0) {
     CKV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attend<false>,

@@ -1067,11 +1067,21 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
     const size_t smem_f = std::max(size_t(G) * warp_bytes, SF_RING) + size_t(G) * c_pad * 8 +
                           size_t(c_pad) * 8;
     if (smem_f <= 200 * 1024) {
-#define CKV_SF_FNS(NC_) (const void*)k_select_fused<1, NC_>, (const void*)k_select_fused<2, NC_>, \
-    (const void*)k_select_fused<4, NC_>, (const void*)k_select_fused<8, NC_>
-      for (const void* fn : {CKV_SF_FNS(1), CKV_SF_FNS(2), CKV_SF_FNS(4), CKV_SF_FNS(8)})
-        CKV_CUDA_TRY(smem_optin(fn, 200 * 1024));
-#undef CKV_SF_FNS
+      // the opt-in for the one instantiation launched (a per-call host cost)
+      {
+        const void* fns[4][4] = {
+            {(const void*)k_select_fused<1, 1>, (const void*)k_select_fused<2, 1>,
+             (const void*)k_select_fused<4, 1>, (const void*)k_select_fused<8, 1>},
+            {(const void*)k_select_fused<1, 2>, (const void*)k_select_fused<2, 2>,
+             (const void*)k_select_fused<4, 2>, (const void*)k_select_fused<8, 2>},
+            {(const void*)k_select_fused<1, 4>, (const void*)k_select_fused<2, 4>,
+             (const void*)k_select_fused<4, 4>, (const void*)k_select_fused<8, 4>},
+            {(const void*)k_select_fused<1, 8>, (const void*)k_select_fused<2, 8>,
+             (const void*)k_select_fused<4, 8>, (const void*)k_select_fused<8, 8>}};
+        const int ni = nc == 1 ? 0 : nc == 2 ? 1 : nc == 4 ? 2 : 3;
+        const int gi = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : 3;
+        CKV_CUDA_TRY(smem_optin(fns[ni][gi], 200 * 1024));
+      }
 #define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
     token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode, q_copy, \
     rdy, ep
@@ -1100,9 +1110,12 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       cfg.attrs = attr + 1;
       cfg.numAttrs = 2;
       if (desc.flags & CKV_SEL_L2_PERSIST) {
-        int dev_w = 0, v = 0;
+        // the device's window limit is fixed: queried once per device
+        static int win_dev[64];
+        int dev_w = 0;
         cudaGetDevice(&dev_w);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev_w);
+        int& v = win_dev[dev_w & 63];
+        if (v == 0) cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev_w);
         const size_t max_win = size_t(v);
         size_t persist = 0;
         cudaDeviceGetLimit(&persist, cudaLimitPersistingL2CacheSize);
