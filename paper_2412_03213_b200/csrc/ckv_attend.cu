@@ -138,6 +138,7 @@ struct __align__(128) AttSmem {
   float q[2][D];                    // query ring
   uint64_t full[AT_STAGES], empty[AT_STAGES], qfull[2], qempty[2];
   uint32_t roff[AT_RUNS + 1], rrow[AT_RUNS];  // producer: runs of the current item
+  uint32_t item[2];                 // dynamic schedule: the q slot's work item (~0 = done)
   float hm[8], hl[8];
   float hacc[8][D];
   uint32_t last;
@@ -189,7 +190,8 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
          const uint32_t* __restrict__ rows, ckv_runs runs, const uint32_t* __restrict__ n_tokens,
          float* __restrict__ out, float* __restrict__ logits_ws, float* __restrict__ part,
          uint32_t* __restrict__ tickets, float* __restrict__ weights, float* __restrict__ lse,
-         const uint32_t* __restrict__ ready, const uint32_t* __restrict__ epoch) {
+         const uint32_t* __restrict__ ready, const uint32_t* __restrict__ epoch,
+         uint32_t* __restrict__ work) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   AttSmem& sm = *reinterpret_cast<AttSmem*>(sm_raw);
   const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
@@ -227,7 +229,23 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
     uint32_t st = 0, ph = 0, qk = 0;  // ring stage / parity, query-ring counter
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x, ++qk) {
+    for (;; ++qk) {
+      // the next item: a fixed stride, or (StepSync) the shared counter, so
+      // items are taken in q-head order as the selection publishes them
+      uint32_t i = blockIdx.x + qk * gridDim.x;
+      if (work) {
+        if (lane == 0) i = atomicAdd(work, 1u);
+        i = __shfl_sync(0xffffffffu, i, 0);
+      }
+      if (i >= n_items) {
+        if (work && lane == 0) {  // tell the consumers through the q slot
+          const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
+          mbar_wait(&sm.qempty[qs], qp ^ 1);
+          sm.item[qs] = ~0u;
+          mbar_arrive(&sm.qfull[qs]);
+        }
+        break;
+      }
       const ItemInfo it = item_info(i, splits, n_tokens, ready, want);
       const uint32_t unit = it.h / desc.group;
       const uint16_t* Ku = K + size_t(unit) * desc.p_cap * D;
@@ -252,6 +270,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       if (lane == 0) {
         const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
         mbar_wait(&sm.qempty[qs], qp ^ 1);
+        sm.item[qs] = i;  // released to the consumers by the arrive below
         mbar_expect_tx(&sm.qfull[qs], D * 4);
         // the selection may have just written q's device copy (zero-copy
         // step): order those generic-proxy stores before this bulk copy
@@ -303,10 +322,18 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
   const int hl = t & 15;  // dims [8*hl, 8*hl+8)
   const float qscale = 1.4426950408889634f * rsqrtf(float(D));  // exp -> exp2
   uint32_t st = 0, ph = 0, qk = 0;
-  for (uint32_t i = blockIdx.x; i < n_items; i += gridDim.x, ++qk) {
-    const ItemInfo it = item_info(i, splits, n_tokens, ready, want);
+  for (;; ++qk) {
     const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
-    mbar_wait(&sm.qfull[qs], qp);
+    uint32_t i = blockIdx.x + qk * gridDim.x;
+    if (work) {
+      mbar_wait(&sm.qfull[qs], qp);
+      i = sm.item[qs];
+      if (i == ~0u) break;
+    } else {
+      if (i >= n_items) break;
+      mbar_wait(&sm.qfull[qs], qp);
+    }
+    const ItemInfo it = item_info(i, splits, n_tokens, ready, want);
     float qv[8];
     {
       const float4 a = *reinterpret_cast<const float4*>(&sm.q[qs][8 * hl]);
@@ -527,14 +554,15 @@ int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
   const bool use_sync = sync && sync->published && !rows;
   const uint32_t* rdy = use_sync ? sync->ready : nullptr;
   const uint32_t* ep = use_sync ? sync->epoch : nullptr;
+  uint32_t* wk = use_sync ? sync->work : nullptr;
   if (weights)
     CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_attend<true>, desc, splits, q, K, V, rows, runs,
                                     n_tokens, out, logits_ws, part, tickets, weights, lse, rdy,
-                                    ep));
+                                    ep, wk));
   else
     CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_attend<false>, desc, splits, q, K, V, rows, runs,
                                     n_tokens, out, static_cast<float*>(nullptr), part, tickets,
-                                    static_cast<float*>(nullptr), lse, rdy, ep));
+                                    static_cast<float*>(nullptr), lse, rdy, ep, wk));
   CKV_LAUNCH_CHECK("k_attend");
   return CKV_OK;
 }

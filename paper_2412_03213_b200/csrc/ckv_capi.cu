@@ -209,16 +209,21 @@ __global__ void k_append_clusters(const float* __restrict__ tmp_c, const int32_t
 // (and advance the StepSync epoch: the step's selection / attention are done)
 __global__ void k_append_kv(const uint16_t* __restrict__ kn, const uint16_t* __restrict__ vn,
                             uint16_t* __restrict__ K, uint16_t* __restrict__ V, uint32_t pos,
-                            uint32_t p_cap, uint32_t* __restrict__ epoch) {
+                            uint32_t p_cap, uint32_t* __restrict__ epoch,
+                            uint32_t* __restrict__ work) {
   const uint32_t u = blockIdx.x, j = threadIdx.x;  // 16 threads x 16 B
   if (epoch && u == 0 && j == 0) ++*epoch;
+  if (work && j == 0) work[u] = 0u;  // the attention work counters (per slice start unit)
   const uint4* ks = reinterpret_cast<const uint4*>(kn + size_t(u) * D);
   const uint4* vs = reinterpret_cast<const uint4*>(vn + size_t(u) * D);
   reinterpret_cast<uint4*>(K + (size_t(u) * p_cap + pos) * D)[j] = ks[j];
   reinterpret_cast<uint4*>(V + (size_t(u) * p_cap + pos) * D)[j] = vs[j];
 }
 
-__global__ void k_epoch_advance(uint32_t* epoch) { ++*epoch; }
+__global__ void k_epoch_advance(uint32_t* epoch, uint32_t* work, uint32_t n) {
+  for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) work[u] = 0u;
+  if (threadIdx.x == 0) ++*epoch;
+}
 
 // cluster-major relayout of the prompt KV (after the prefill index):
 // dst row r = src position  r              for r < sink or r >= labeled_end
@@ -902,7 +907,7 @@ struct ckv_session {
   uint32_t* tickets = nullptr;
   // StepSync (ckv_internal.cuh): per-q-head selection -> attention flags
   // and their epoch; off with CKV_SESSION_NO_STEPSYNC=1
-  uint32_t *step_ready = nullptr, *step_epoch = nullptr;
+  uint32_t *step_ready = nullptr, *step_epoch = nullptr, *step_work = nullptr;
   StepSync sync{};
   float *q_dev = nullptr, *out_dev = nullptr;
   uint16_t *kn_dev = nullptr, *vn_dev = nullptr;
@@ -1042,6 +1047,7 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   rc |= salloc(&s->tickets, s->n_q);
   rc |= salloc(&s->step_ready, s->n_q);
   rc |= salloc(&s->step_epoch, 1);
+  rc |= salloc(&s->step_work, s->U);
   rc |= salloc(&s->q_dev, size_t(s->n_q) * D);
   rc |= salloc(&s->out_dev, size_t(s->n_q) * D);
   rc |= salloc(&s->kn_dev, size_t(s->U) * D);
@@ -1109,6 +1115,7 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   cudaMemsetAsync(s->tickets, 0, size_t(s->n_q) * 4, ctx->stream);
   cudaMemsetAsync(s->step_ready, 0, size_t(s->n_q) * 4, ctx->stream);
   cudaMemsetAsync(s->step_epoch, 0, 4, ctx->stream);
+  cudaMemsetAsync(s->step_work, 0, size_t(s->U) * 4, ctx->stream);
   cudaMemsetAsync(s->n_clusters, 0, size_t(s->U) * 4, ctx->stream);
   if (d->flags & CKV_SESSION_L2_PERSIST) {  // device-wide; restored by the last user
     int maxp = 0;
@@ -1148,7 +1155,7 @@ int ckv_session_destroy(ckv_session* s) {
   cudaFree(s->runs.row); cudaFree(s->runs.off); cudaFree(s->runs.count);
   cudaFree(s->tmpV); cudaFree(s->n_tokens); cudaFree(s->n_taken); cudaFree(s->trimmed);
   cudaFree(s->ranked); cudaFree(s->part); cudaFree(s->tickets); cudaFree(s->q_dev);
-  cudaFree(s->step_ready); cudaFree(s->step_epoch);
+  cudaFree(s->step_ready); cudaFree(s->step_epoch); cudaFree(s->step_work);
   cudaFree(s->out_dev); cudaFree(s->kn_dev); cudaFree(s->vn_dev);
   if (s->side) { cudaStreamSynchronize(s->side); cudaStreamDestroy(s->side); }
   if (s->sel_stream) { cudaStreamSynchronize(s->sel_stream); cudaStreamDestroy(s->sel_stream); }
@@ -1327,6 +1334,7 @@ static int session_attend_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
   if (sync) {
     ls = *sync;
     ls.ready += h0;
+    if (ls.work) ls.work += u0;  // one counter per slice (first unit)
   }
   CKV_TRY(launch_attend(st, ad, qc ? qc : qs, s->K + size_t(u0) * s->p_cap * D,
                         s->V + size_t(u0) * s->p_cap * D, nullptr, runs, s->n_tokens + h0,
@@ -1361,6 +1369,7 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
       if (!session_no_stepsync() && !s->tiered) {
         s->sync.ready = s->step_ready;
         s->sync.epoch = s->step_epoch;
+        s->sync.work = s->step_work;
         sy = &s->sync;
       }
       CKV_TRY(session_select_slice(s, st, 0, s->U, q_dev, q_copy, false, sy));
@@ -1380,6 +1389,7 @@ static int session_select_attend(ckv_session* s, const float* q_dev, float* out_
   if (!session_no_stepsync() && !s->tiered) {
     s->sync.ready = s->step_ready;
     s->sync.epoch = s->step_epoch;
+    s->sync.work = nullptr;  // layer slices: the fixed item stride (measured faster here)
     sy = &s->sync;
   }
   for (uint32_t u0 = 0; u0 < s->U; u0 += lu) {
@@ -1403,7 +1413,7 @@ int ckv_session_attend_only(ckv_session* s, const float* q_dev, float* out_dev) 
   if (!s->prefilled) { set_error("session: prefill first"); return CKV_EINVAL; }
   CKV_TRY(session_select_attend(s, q_dev, out_dev));
   // no append follows: advance the StepSync epoch here
-  k_epoch_advance<<<1, 1, 0, s->ctx->stream>>>(s->step_epoch);
+  k_epoch_advance<<<1, 256, 0, s->ctx->stream>>>(s->step_epoch, s->step_work, s->U);
   CKV_LAUNCH_CHECK("k_epoch_advance");
   s->ctx->launches++;
   return CKV_OK;
@@ -1528,7 +1538,8 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
   }
   CKV_TRY(session_select_attend(s, qd, od, q_copy));
   // append this step's token (harness.hpp:318-320)
-  k_append_kv<<<s->U, 16, 0, st>>>(kd, vd, s->K, s->V, s->n_ctx, s->p_cap, s->step_epoch);
+  k_append_kv<<<s->U, 16, 0, st>>>(kd, vd, s->K, s->V, s->n_ctx, s->p_cap, s->step_epoch,
+                                   s->step_work);
   CKV_LAUNCH_CHECK("k_append_kv");
   s->ctx->launches++;
   s->n_ctx++;

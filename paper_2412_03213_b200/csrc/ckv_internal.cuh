@@ -113,6 +113,10 @@ struct CacheDev {
 struct StepSync {
   uint32_t* ready = nullptr;         // [n_q]
   uint32_t* epoch = nullptr;         // [1]
+  // the attention's work counter for this launch (items handed out in
+  // selection order, so no CTA holds an item whose head is still being
+  // selected while published heads wait); zeroed by the step's last kernel
+  uint32_t* work = nullptr;
   bool published = false;
 };
 int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,

@@ -1,0 +1,18 @@
+#!/bin/bash
+# dynamic attention scheduling under StepSync; selection padded to one CTA per SM
+mkdir -p gpurun_out
+timeout -k 10 500 python -m pytest tests/test_gpu_session.py tests/test_gpu_headline.py tests/test_gpu_attend.py -m gpu -x -q 2>&1 | tail -2
+run() {
+  timeout -k 10 300 python bench.py --steps 50 --warmup 10 --e2e-steps 20 --no-cpu --no-extra --max-iters 8 > gpurun_out/dyn.json 2>/dev/null
+  python -c "
+import json
+for l in open('gpurun_out/dyn.json'):
+    if l.startswith('{'):
+        d=json.loads(l); print('$1', 'us/step', round(d.get('ms_per_step')*1000,1), 'e2e us', round(1e6/d['e2e']['value'],1), 'layer us', round(d['per_layer']['ms_per_step']*1000,1))"
+}
+for r in 1 2; do
+  unset CKV_SEL_SMEM_KB CKV_SESSION_NO_STEPSYNC
+  run dyn
+  CKV_SEL_SMEM_KB=120 run dyn_pad120
+  CKV_SESSION_NO_STEPSYNC=1 run nosync
+done
