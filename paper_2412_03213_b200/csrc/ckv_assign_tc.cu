@@ -1426,11 +1426,20 @@ int launch_permute_keys(cudaStream_t st, const uint16_t* k16, uint32_t n, uint32
 __global__ void k_compact_active(const int32_t* __restrict__ active, uint32_t n_units,
                                   int32_t* __restrict__ list, int32_t* __restrict__ count,
                                   uint32_t* __restrict__ fix_count) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int32_t n = 0;
-    for (uint32_t u = 0; u < n_units; ++u)
-      if (!active || active[u]) list[n++] = int32_t(u);
-    *count = n;
+  // one warp: ballots keep the list in ascending unit order
+  if (blockIdx.x != 0) return;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (threadIdx.x >= 32) return;
+  uint32_t n = 0;
+  for (uint32_t u0 = 0; u0 < n_units; u0 += 32) {
+    const uint32_t u = u0 + lane;
+    const bool on = u < n_units && (!active || active[u]);
+    const unsigned m = __ballot_sync(0xffffffffu, on);
+    if (on) list[n + __popc(m & ((1u << lane) - 1u))] = int32_t(u);
+    n += __popc(m);
+  }
+  if (lane == 0) {
+    *count = int32_t(n);
     *fix_count = 0;
     fix_count[TC_MERGE_SLOT] = 0;  // k_assign_merge's single region
     fix_count[TC_FULL_SLOT] = 0;   // k_fixup_full's queue length
