@@ -261,6 +261,39 @@ def test_session_layer_mode_matches_batched(gpu_ctx):
         ss[0].set_layer_units(4)  # does not divide 6
 
 
+@pytest.mark.parametrize("layer_mode", [False, True])
+def test_session_attend_only_interleaved_with_steps(gpu_ctx, layer_mode):
+    """ckv_session_attend_only between steps (no append: it advances the
+    selection -> attention hand-off epoch itself): its output equals the next
+    step's for the same q, bit for bit, in both launch modes."""
+    import torch
+    from paper_2412_03213_b200 import api
+    from paper_2412_03213_b200.session import Session
+
+    layers, kvh, G, L, T, B = 2, 2, 2, 600, 16, 90
+    U = layers * kvh
+    heads = [head(33, u // kvh, u % kvh, L, T) for u in range(U)]
+    s = Session(U, G, L, T, B, retention=1,
+                cfg=api.ClusterConfig(decode_batch=7, c0_divisor=40), kv_heads=kvh)
+    s.load_prompt_host(np.stack([bf16_bits(h["K"]) for h in heads]),
+                       np.stack([bf16_bits(h["V"]) for h in heads]))
+    s.prefill()
+    if layer_mode:
+        s.set_layer_units(kvh)
+    dev = gpu_ctx.device
+    for t in range(T):
+        q = np.stack([heads[u]["Q"][(t + r) % T] for u in range(U) for r in range(G)])
+        qd = torch.from_numpy(q).to(dev)
+        kn = torch.from_numpy(np.stack([bf16_bits(heads[u]["dK"][t]) for u in range(U)]).view(np.int16)).to(dev)
+        vn = torch.from_numpy(np.stack([bf16_bits(heads[u]["dV"][t]) for u in range(U)]).view(np.int16)).to(dev)
+        a = torch.empty((U * G, 128), dtype=torch.float32, device=dev)
+        s.attend_only(qd, a)
+        if t % 3 == 0:  # two attend-only calls in a row
+            s.attend_only(qd, a)
+        b = s.step(qd, kn, vn)
+        assert torch.equal(a, b), t
+
+
 def test_session_fused_and_split_select_paths(gpu_ctx):
     """A session of 80 units selects with the fused kernel (one CTA per unit:
     scoring + selection, k_select_fused); its layer mode (8-unit slices)
