@@ -138,7 +138,7 @@ struct __align__(128) AttSmem {
   float q[2][D];                    // query ring
   uint64_t full[AT_STAGES], empty[AT_STAGES], qfull[2], qempty[2];
   uint32_t roff[AT_RUNS + 1], rrow[AT_RUNS];  // producer: runs of the current item
-  uint32_t item[2];                 // dynamic schedule: the q slot's work item (~0 = done)
+  uint4 item[2];                    // the q slot's work item {i, h, e0, e1} (i = ~0: done)
   float hm[8], hl[8];
   float hacc[8][D];
   uint32_t last;
@@ -169,22 +169,8 @@ __device__ __forceinline__ void wait_ready(const uint32_t* ready, uint32_t h, ui
     }
   }
 }
-__device__ __forceinline__ ItemInfo item_info(uint32_t i, uint32_t splits,
-                                              const uint32_t* n_tokens,
-                                              const uint32_t* ready = nullptr,
-                                              uint32_t want = 0u) {
-  ItemInfo it;
-  it.h = i / splits;
-  it.s = i % splits;
-  if (ready) wait_ready(ready, it.h, want);
-  const uint32_t nt = __ldcg(n_tokens + it.h);
-  it.e0 = uint32_t((uint64_t(nt) * it.s) / splits);
-  it.e1 = uint32_t((uint64_t(nt) * (it.s + 1)) / splits);
-  return it;
-}
-
 template <bool WEIGHTS>
-__global__ void __launch_bounds__(AT_THREADS, 1)
+__global__ void __launch_bounds__(AT_THREADS, 3)
 k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
          const uint16_t* __restrict__ K, const uint16_t* __restrict__ V,
          const uint32_t* __restrict__ rows, ckv_runs runs, const uint32_t* __restrict__ n_tokens,
@@ -229,48 +215,104 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
     uint32_t st = 0, ph = 0, qk = 0;  // ring stage / parity, query-ring counter
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    for (;; ++qk) {
-      // the next item: a fixed stride, or (StepSync) the shared counter, so
-      // items are taken in q-head order as the selection publishes them
-      uint32_t i = blockIdx.x + qk * gridDim.x;
+    // the CTA's next item: a fixed stride, or (StepSync) the shared counter,
+    // so items are taken in q-head order as the selection publishes them
+    uint32_t kf = 0;
+    auto fetch = [&]() -> uint32_t {
+      uint32_t i = blockIdx.x + (kf++) * gridDim.x;
       if (work) {
         if (lane == 0) i = atomicAdd(work, 1u);
         i = __shfl_sync(0xffffffffu, i, 0);
       }
-      if (i >= n_items) {
-        if (work && lane == 0) {  // tell the consumers through the q slot
+      return i;
+    };
+    // An item's metadata (token count, run count, up to AT_RUNS runs) is
+    // loaded into registers one item AHEAD, while the current item's tiles
+    // stream, so an item start costs no dependent global round trips.  Every
+    // lane acquires the head's flag itself before its loads (StepSync).
+    constexpr int MO = (AT_RUNS + 1 + 31) / 32, MR = (AT_RUNS + 31) / 32;
+    const uint32_t n_off = min(runs.run_cap + 1, uint32_t(AT_RUNS + 1));
+    const uint32_t n_row = min(runs.run_cap, uint32_t(AT_RUNS));
+    uint32_t m_nt = 0, m_nrun = 0, m_off[MO], m_row[MR];
+    auto meta_load = [&](uint32_t i) {
+      const uint32_t h = i / splits;
+      m_nt = __ldcg(n_tokens + h);
+      if (!rows) {
+        m_nrun = __ldcg(runs.count + h);
+        const uint32_t* gro = runs.off + size_t(h) * (runs.run_cap + 1);
+        const uint32_t* grr = runs.row + size_t(h) * runs.run_cap;
+#pragma unroll
+        for (int k = 0; k < MO; ++k) {
+          const uint32_t r = lane + 32 * k;
+          m_off[k] = r < n_off ? __ldcg(gro + r) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          const uint32_t r = lane + 32 * k;
+          m_row[k] = r < n_row ? __ldcg(grr + r) : 0u;
+        }
+      }
+    };
+    auto published = [&](uint32_t i) -> bool {  // non-blocking, per lane
+      if (!ready) return true;
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + i / splits)
+                   : "memory");
+      return __all_sync(0xffffffffu, v == want);
+    };
+    uint32_t i = fetch();
+    bool have = false;
+    if (i < n_items && published(i)) { meta_load(i); have = true; }
+    for (;; ++qk) {
+      if (i >= n_items) {  // tell the consumers through the q slot
+        if (lane == 0) {
           const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
           mbar_wait(&sm.qempty[qs], qp ^ 1);
-          sm.item[qs] = ~0u;
+          sm.item[qs] = make_uint4(~0u, 0u, 0u, 0u);
           mbar_arrive(&sm.qfull[qs]);
         }
         break;
       }
-      const ItemInfo it = item_info(i, splits, n_tokens, ready, want);
+      if (!have) {
+        if (ready) wait_ready(ready, i / splits, want);
+        meta_load(i);
+      }
+      ItemInfo it;
+      it.h = i / splits;
+      it.s = i % splits;
+      it.e0 = uint32_t((uint64_t(m_nt) * it.s) / splits);
+      it.e1 = uint32_t((uint64_t(m_nt) * (it.s + 1)) / splits);
       const uint32_t unit = it.h / desc.group;
       const uint16_t* Ku = K + size_t(unit) * desc.p_cap * D;
       const uint16_t* Vu = V + size_t(unit) * desc.p_cap * D;
-      // stage this q head's runs (rows mode: one entry per row, read in place)
-      uint32_t nrun = 0;
-      bool staged = false;
-      const uint32_t* gro = nullptr;
-      const uint32_t* grr = nullptr;
-      if (!rows) {
-        nrun = __ldcg(runs.count + it.h);
-        gro = runs.off + size_t(it.h) * (runs.run_cap + 1);
-        grr = runs.row + size_t(it.h) * runs.run_cap;
-        staged = nrun <= uint32_t(AT_RUNS);
-        __syncwarp();  // the previous item's runs are no longer read
-        if (staged) {
-          for (uint32_t r = lane; r <= nrun; r += 32) sm.roff[r] = __ldcg(gro + r);
-          for (uint32_t r = lane; r < nrun; r += 32) sm.rrow[r] = __ldcg(grr + r);
+      // this item's runs into shared memory (the previous item's issue loop,
+      // lane 0 below, is done with them: the warp has reconverged)
+      const uint32_t nrun = m_nrun;
+      const bool staged = !rows && nrun <= uint32_t(AT_RUNS);
+      const uint32_t* gro = rows ? nullptr : runs.off + size_t(it.h) * (runs.run_cap + 1);
+      const uint32_t* grr = rows ? nullptr : runs.row + size_t(it.h) * runs.run_cap;
+      __syncwarp();
+      if (staged) {
+#pragma unroll
+        for (int k = 0; k < MO; ++k) {
+          const uint32_t r = lane + 32 * k;
+          if (r <= nrun && r < n_off) sm.roff[r] = m_off[k];
         }
-        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          const uint32_t r = lane + 32 * k;
+          if (r < nrun && r < n_row) sm.rrow[r] = m_row[k];
+        }
       }
+      __syncwarp();
+      // look ahead: the next item and, if its head is published, its metadata
+      const uint32_t i_next = fetch();
+      have = false;
+      if (i_next < n_items && published(i_next)) { meta_load(i_next); have = true; }
       if (lane == 0) {
         const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
         mbar_wait(&sm.qempty[qs], qp ^ 1);
-        sm.item[qs] = i;  // released to the consumers by the arrive below
+        sm.item[qs] = make_uint4(i, it.h, it.e0, it.e1);  // released by the arrive below
         mbar_expect_tx(&sm.qfull[qs], D * 4);
         // the selection may have just written q's device copy (zero-copy
         // step): order those generic-proxy stores before this bulk copy
@@ -289,7 +331,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
         for (uint32_t e = it.e0; e < it.e1; e += AT_TILE) {
           const uint32_t te = min(e + AT_TILE, it.e1);
           mbar_wait(&sm.empty[st], ph ^ 1);
-            mbar_expect_tx(&sm.full[st], (te - e) * D * 2 * 2);
+          mbar_expect_tx(&sm.full[st], (te - e) * D * 2 * 2);
           for (uint32_t x = e; x < te;) {
             uint32_t row, n;
             if (rows) {
@@ -311,6 +353,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
       }
       st = __shfl_sync(0xffffffffu, st, 0);
       ph = __shfl_sync(0xffffffffu, ph, 0);
+      i = i_next;
     }
     // StepSync: this grid never completes before the selection grid
     if (ready) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -324,16 +367,15 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
   uint32_t st = 0, ph = 0, qk = 0;
   for (;; ++qk) {
     const uint32_t qs = qk & 1, qp = (qk >> 1) & 1;
-    uint32_t i = blockIdx.x + qk * gridDim.x;
-    if (work) {
-      mbar_wait(&sm.qfull[qs], qp);
-      i = sm.item[qs];
-      if (i == ~0u) break;
-    } else {
-      if (i >= n_items) break;
-      mbar_wait(&sm.qfull[qs], qp);
-    }
-    const ItemInfo it = item_info(i, splits, n_tokens, ready, want);
+    mbar_wait(&sm.qfull[qs], qp);  // the producer's item descriptor and q
+    const uint4 d4 = sm.item[qs];
+    if (d4.x == ~0u) break;
+    const uint32_t i = d4.x;
+    ItemInfo it;
+    it.h = d4.y;
+    it.s = i % splits;
+    it.e0 = d4.z;
+    it.e1 = d4.w;
     float qv[8];
     {
       const float4 a = *reinterpret_cast<const float4*>(&sm.q[qs][8 * hl]);
