@@ -85,8 +85,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 // the KV rows are read once per step: evict_first, so the stream does not
 // push the selection's centroids (evict_last) out of L2
+#ifndef CKV_AT_L2HINT
+#define CKV_AT_L2HINT 1
+#endif
 __device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes,
                                                 uint64_t* bar, uint64_t pol) {
+  if (!CKV_AT_L2HINT) { bulk_g2s(dst, src, bytes, bar); return; }
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
       "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
