@@ -212,6 +212,8 @@ __global__ void k_append_kv(const uint16_t* __restrict__ kn, const uint16_t* __r
                             uint32_t p_cap, uint32_t* __restrict__ epoch,
                             uint32_t* __restrict__ work) {
   const uint32_t u = blockIdx.x, j = threadIdx.x;  // 16 threads x 16 B
+  // the next step's selection (PDL) may start streaming its centroids now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (epoch && u == 0 && j == 0) ++*epoch;
   if (work && j == 0) work[u] = 0u;  // the attention work counters (per slice start unit)
   const uint4* ks = reinterpret_cast<const uint4*>(kn + size_t(u) * D);
@@ -937,6 +939,11 @@ struct ckv_session {
   struct Queued { uint32_t ready, pos0, rows, C; };
   std::deque<Queued> queue;
   uint32_t layer_units = 0;  // 0: one select + attend for all units; else per slice
+  // no kernel has written the centroids / sizes / starts / n_clusters since
+  // the previous selection, and the stream's last kernel is the append
+  // (CKV_SEL_EARLY for the next step's selections)
+  bool sel_early = false;
+  bool step_early = false;  // this step's selections may start early
   // physical two-tier cache (CKV_SESSION_TIERED / _TIER_HOST, ckv_tier.cu)
   bool tiered = false;
   TierArgs tier{};
@@ -1196,6 +1203,7 @@ int ckv_session_load_prompt(ckv_session* s, const uint16_t* Kh, const uint16_t* 
 }
 
 int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
+  s->sel_early = false;  // the prefill writes the centroids and the index
   ckv_prefill_desc pd{};
   pd.n_units = s->U;
   pd.L = s->d.prompt_len;
@@ -1250,6 +1258,11 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
 // the selection leaves a device copy of it there and the attention reads that
 // (its bulk copies stay on HBM).  The two halves take a stream each so the
 // batched step can overlap one slice's selection with another's attention.
+static bool session_no_early() {
+  static const bool off = getenv("CKV_SESSION_NO_EARLY") != nullptr;
+  return off;
+}
+
 static bool session_no_stepsync() {
   static const bool off = getenv("CKV_SESSION_NO_STEPSYNC") != nullptr;
   return off;
@@ -1271,6 +1284,7 @@ static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
   sd.rec_end = s->n_ctx;
   sd.flags = (s->d.flags & CKV_SESSION_L2_PERSIST) ? CKV_SEL_L2_PERSIST : 0u;
   if (force_fused) sd.flags |= CKV_SEL_FORCE_FUSED;
+  if (s->step_early) sd.flags |= CKV_SEL_EARLY;
   sd.row_base = sd.sink_count;
   const bool want_ids = (s->d.flags & CKV_SESSION_TOKEN_IDS) != 0;
   ckv_runs runs = s->runs;
@@ -1413,6 +1427,7 @@ int ckv_session_attend_only(ckv_session* s, const float* q_dev, float* out_dev) 
   if (!s->prefilled) { set_error("session: prefill first"); return CKV_EINVAL; }
   CKV_TRY(session_select_attend(s, q_dev, out_dev));
   // no append follows: advance the StepSync epoch here
+  s->sel_early = false;
   k_epoch_advance<<<1, 256, 0, s->ctx->stream>>>(s->step_epoch, s->step_work, s->U);
   CKV_LAUNCH_CHECK("k_epoch_advance");
   s->ctx->launches++;
@@ -1500,11 +1515,14 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
   cudaStream_t st = s->ctx->stream;
   // async mode: batches whose delay has run out join before this step's
   // selection (harness.hpp:237-243)
+  bool early = s->sel_early && !session_no_early();
+  s->sel_early = false;
   while (!s->queue.empty() && s->queue.front().ready <= s->steps) {
     const auto b = s->queue.front();
     CKV_CUDA_TRY(cudaStreamWaitEvent(st, s->ev_done, 0));
     CKV_TRY(session_commit_batch(s, b.pos0, b.rows, b.C, s->stage_ncl));
     s->queue.pop_front();
+    early = false;  // the commit wrote the centroids and the index
   }
   const float* qd = q;
   const uint16_t *kd = kn, *vd = vn;
@@ -1536,7 +1554,10 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
       od = s->out_dev;
     }
   }
-  CKV_TRY(session_select_attend(s, qd, od, q_copy));
+  s->step_early = early;
+  const int rc_sa = session_select_attend(s, qd, od, q_copy);
+  s->step_early = false;
+  CKV_TRY(rc_sa);
   // append this step's token (harness.hpp:318-320)
   k_append_kv<<<s->U, 16, 0, st>>>(kd, vd, s->K, s->V, s->n_ctx, s->p_cap, s->step_epoch,
                                    s->step_work);
@@ -1545,6 +1566,7 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
   s->n_ctx++;
   s->pending++;
   s->steps++;
+  s->sel_early = true;  // cleared below if a synchronous decode batch follows
   if (s->pending == s->d.decode_batch) {  // harness.hpp:321-336
     const uint32_t m = s->pending, pos0 = s->pend_pos0;
     const uint32_t C = std::min(s->d.c_plus, m);
@@ -1561,9 +1583,11 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
       CKV_CUDA_TRY(cudaEventRecord(s->ev_done, s->side));
       s->queue.push_back({s->steps - 1 + s->d.async_delay, pos0, m, C});
     } else if (kmeans_small_supported(m, C) && m <= uint32_t(BC_THREADS)) {
+      s->sel_early = false;
       CKV_TRY(session_cluster_batch(s, st, pos0, m, s->n_clusters));
       CKV_TRY(session_commit_batch(s, pos0, m, C, s->n_clusters));
     } else {  // large batches: the generic driver, full index, staged relayout
+      s->sel_early = false;
       ckv_decode_cluster_desc dd{};
       dd.n_units = s->U;
       dd.pos0 = pos0;

@@ -96,6 +96,10 @@ namespace ckvb {
 // whatever the unit count (the session's concurrent slices: the unfused path
 // shares one scratch buffer)
 constexpr uint32_t CKV_SEL_FORCE_FUSED = 0x80000000u;
+// the session's selection may stream the centroids / sizes / starts before
+// its grid dependency wait: no kernel since the previous selection wrote them
+// (the step's previous kernel is the append or an attention)
+constexpr uint32_t CKV_SEL_EARLY = 0x40000000u;
 struct CacheDev {
   uint32_t n_slots, c_cap, retention, d, words;
   uint32_t* bits;                // [n_slots][retention][words]

@@ -767,17 +767,12 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   __shared__ WarpSel wsa[G];
   __shared__ float qn2[G];
   // programmatic stream serialization: launched while the previous kernel
-  // (the last step's append / clustering) drains; nothing is read before it
-  // completes (a no-op for a normal launch)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  // StepSync: the attention may launch now (every CTA of this grid is
-  // resident once all have passed here); it waits per q head on ready[]
-  uint32_t ready_val = 0u;
-  if (ready) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    ready_val = *epoch + 1u;
-  }
-  if (leader && wid < G) dbg_stamp(unit * G + wid, 7);
+  // (the last step's append / clustering) drains; nothing it writes is read
+  // before it completes (a no-op for a normal launch).  CKV_SEL_EARLY: the
+  // centroid ring and the sizes / starts are issued before the wait (nothing
+  // since the previous selection wrote them).
+  const bool early = (desc.flags & CKV_SEL_EARLY) != 0;
+  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
   const size_t ring_bytes = max(size_t(G) * warp_bytes, SF_RING);
   float* ring = reinterpret_cast<float*>(smraw);                          // [SF_NS][SF_ROWS][D]
   float* av_s = reinterpret_cast<float*>(smraw + ring_bytes);              // [G][c_pad]
@@ -822,6 +817,15 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
+  if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // StepSync: the attention may launch now (every CTA of this grid is
+  // resident once all have passed here); it waits per q head on ready[]
+  uint32_t ready_val = 0u;
+  if (ready) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    ready_val = *epoch + 1u;
+  }
+  if (leader && wid < G) dbg_stamp(unit * G + wid, 7);
   SelCachePre cpre{{0u, 0u, 0u, 0u}, 0u, 0u, 0ull, false};
   if (leader && wid < G && mode != 1) cpre = cache_prefetch(unit * G + wid, cache);
   const float* qu = q + size_t(unit) * G * D;
