@@ -1232,6 +1232,10 @@ k_fixup(const uint4* __restrict__ list, const uint32_t* __restrict__ ids,
 // wins (clustering.hpp:104-115).  One launch over the queue k_fixup filled.
 constexpr int FF_WARPS = 8;
 constexpr uint32_t FF_MAXC = TC_MAXC_ALL;
+#ifndef CKV_FF_ROWS
+#define CKV_FF_ROWS 16
+#endif
+constexpr int FF_ROWS = CKV_FF_ROWS;  // centroid rows in flight per warp (k_fixup_full)
 __global__ void __launch_bounds__(FF_WARPS * 32)
 k_fixup_full(const uint4* __restrict__ list, const uint32_t* __restrict__ full_q,
              const uint32_t* __restrict__ full_n, const uint16_t* __restrict__ keys,
@@ -1255,11 +1259,11 @@ k_fixup_full(const uint4* __restrict__ list, const uint32_t* __restrict__ full_q
     const float* du = dirs + size_t(u) * c_pad * D;
     double best = -INFINITY, second = -INFINITY;
     uint32_t bid = 0xffffffffu;
-    for (uint32_t c0 = w; c0 < C; c0 += FF_WARPS * 4) {
-      double p[4];
-      uint32_t cc[4];
+    for (uint32_t c0 = w; c0 < C; c0 += FF_WARPS * FF_ROWS) {
+      double p[FF_ROWS];
+      uint32_t cc[FF_ROWS];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {  // 4 rows in flight per warp
+      for (int j = 0; j < FF_ROWS; ++j) {  // FF_ROWS rows in flight per warp
         cc[j] = c0 + FF_WARPS * j;
         const float4 x = cc[j] < C ? __ldg(reinterpret_cast<const float4*>(du + size_t(cc[j]) * D) + lane)
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1268,9 +1272,9 @@ k_fixup_full(const uint4* __restrict__ list, const uint32_t* __restrict__ full_q
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) p[j] += __shfl_xor_sync(0xffffffffu, p[j], o);
+        for (int j = 0; j < FF_ROWS; ++j) p[j] += __shfl_xor_sync(0xffffffffu, p[j], o);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < FF_ROWS; ++j) {
         if (cc[j] >= C) break;
         const double sj = isnan(p[j]) ? -INFINITY : p[j];
         if (lane == 0) sc[cc[j]] = sj;
