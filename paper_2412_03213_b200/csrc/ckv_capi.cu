@@ -898,6 +898,16 @@ struct ckv_session {
   uint32_t U = 0, n_q = 0, p_cap = 0, c_cap = 0, sel_cap = 0;
   uint16_t *K = nullptr, *V = nullptr;
   float* cents = nullptr;
+  // CKV_SESSION_F16_SCORES=1: the fused selection's approximate scores from an
+  // fp16 centroid copy (SelC16), refreshed before the first selection after
+  // anything rewrote the centroids.  Opt-in: measured no faster at config B
+  // (114.0 vs 113.9 us/step) and slower in layer mode (0.79 vs 0.75 ms/step)
+  // -- the scoring phase is not bound by the centroid bytes.
+  bool use_c16 = false;
+  uint16_t* c16 = nullptr;
+  float* cerr = nullptr;
+  bool c16_dirty = true;  // all rows
+  uint32_t c16_tail = 0;  // or only each unit's last c16_tail rows (committed decode batches)
   int32_t* labels = nullptr;
   uint32_t *n_clusters = nullptr, *sizes = nullptr, *starts = nullptr, *sorted = nullptr;
   uint32_t *token_ids = nullptr, *rows = nullptr, *n_tokens = nullptr, *n_taken = nullptr,
@@ -1031,6 +1041,11 @@ int ckv_session_create(ckv_ctx* ctx, const ckv_session_desc* d, ckv_session** ou
   rc |= salloc(&s->K, kv);
   rc |= salloc(&s->V, kv);
   rc |= salloc(&s->cents, size_t(s->U) * s->c_cap * D);
+  s->use_c16 = getenv("CKV_SESSION_F16_SCORES") != nullptr;
+  if (s->use_c16) {
+    rc |= salloc(&s->c16, size_t(s->U) * s->c_cap * D);
+    rc |= salloc(&s->cerr, size_t(s->U) * s->c_cap);
+  }
   rc |= salloc(&s->labels, size_t(s->U) * s->p_cap);
   rc |= salloc(&s->n_clusters, s->U);
   rc |= salloc(&s->sizes, size_t(s->U) * s->c_cap);
@@ -1157,6 +1172,7 @@ int ckv_session_destroy(ckv_session* s) {
   if (!s) return CKV_OK;
   cudaStreamSynchronize(s->ctx->stream);
   cudaFree(s->K); cudaFree(s->V); cudaFree(s->cents); cudaFree(s->labels);
+  cudaFree(s->c16); cudaFree(s->cerr);
   cudaFree(s->n_clusters); cudaFree(s->sizes); cudaFree(s->starts); cudaFree(s->sorted);
   cudaFree(s->token_ids); cudaFree(s->rows); cudaFree(s->sel_scratch); cudaFree(s->tmpK);
   cudaFree(s->runs.row); cudaFree(s->runs.off); cudaFree(s->runs.count);
@@ -1243,6 +1259,7 @@ int ckv_session_prefill(ckv_session* s, ckv_kmeans_info* info) {
     }
   }
   s->prefilled = true;
+  s->c16_dirty = true;
   const int rc = ckv_ctx_sync(s->ctx);
   if (dbg) {
     const auto t3 = std::chrono::steady_clock::now();
@@ -1305,13 +1322,15 @@ static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
     ls = *sync;
     ls.ready += h0;
   }
+  const SelC16 hc{s->use_c16 ? s->c16 + size_t(u0) * s->c_cap * D : nullptr,
+                  s->use_c16 ? s->cerr + size_t(u0) * s->c_cap : nullptr};
   CKV_TRY(launch_select(st, sd, qs, s->cents + size_t(u0) * s->c_cap * D,
                         s->n_clusters + u0, s->sizes + size_t(u0) * s->c_cap,
                         s->starts + size_t(u0) * (s->c_cap + 1), s->sorted + size_t(u0) * s->p_cap,
                         want_ids ? s->token_ids + size_t(h0) * s->sel_cap : nullptr, nullptr, runs,
                         sd.row_base, s->n_tokens + h0, s->n_taken + h0, s->trimmed + h0,
                         s->ranked + size_t(h0) * s->c_cap, nullptr, cache, s->sel_scratch, qc,
-                        sync ? &ls : nullptr));
+                        sync ? &ls : nullptr, s->use_c16 ? &hc : nullptr));
   if (sync) sync->published = ls.published;
   s->ctx->launches += 2;
   return CKV_OK;
@@ -1371,6 +1390,14 @@ static int session_attend_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
 static int session_select_attend(ckv_session* s, const float* q_dev, float* out_dev,
                                  float* q_copy = nullptr) {
   cudaStream_t st = s->ctx->stream;
+  if (s->use_c16 && (s->c16_dirty || s->c16_tail)) {  // centroids changed since the last selection
+    CKV_TRY(launch_cents_f16(st, s->cents, s->n_clusters, s->U, s->c_cap, s->c16, s->cerr,
+                             s->c16_dirty ? 0u : s->c16_tail));
+    s->ctx->launches++;
+    s->c16_dirty = false;
+    s->c16_tail = 0;
+    s->step_early = false;  // the selection reads what this kernel writes
+  }
   const uint32_t lu = s->layer_units;
   if (lu == 0 || lu >= s->U) {
     static const bool split = getenv("CKV_SESSION_SPLIT") != nullptr;
@@ -1504,6 +1531,7 @@ static int session_commit_batch(ckv_session* s, uint32_t pos0, uint32_t m, uint3
   }
   s->labeled_end += m;
   s->C_cur += C;
+  s->c16_tail += C;  // the batch's centroids are each unit's last C rows
   return CKV_OK;
 }
 
@@ -1600,6 +1628,7 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
                                        s->n_clusters, nullptr));
       s->labeled_end += m;
       s->C_cur += C;
+      s->c16_dirty = true;
       CKV_TRY(ckv_build_index(s->ctx, s->U, s->labeled_end, s->p_cap, s->c_cap, s->labels,
                               s->n_clusters, s->sizes, s->starts, s->sorted));
       const uint32_t sink = std::min(s->d.sink_tokens, s->d.prompt_len);

@@ -123,13 +123,25 @@ struct StepSync {
   uint32_t* work = nullptr;
   bool published = false;
 };
+// fp16 copy of a centroid block for the fused selection's approximate
+// scores: c16[u][c] = RN_fp16(mu_c) and cerr[u][c] >= |mu_c - c16[u][c]|_2
+// (components saturate at +-65504 and the bound grows with them; +inf when
+// it is not finite)
+struct SelC16 {
+  const uint16_t* c16;
+  const float* cerr;
+};
+// rows [0, n_clusters[u]) of every unit, or (tail > 0) only the last tail of them
+int launch_cents_f16(cudaStream_t st, const float* cents, const uint32_t* n_clusters,
+                     uint32_t n_units, uint32_t c_cap, uint16_t* c16, float* cerr,
+                     uint32_t tail = 0);
 int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const float* cents, const uint32_t* n_clusters, const uint32_t* sizes,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
                   uint32_t* rows, const ckv_runs& runs, uint32_t row_base, uint32_t* n_tokens,
                   uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
                   const CacheDev& cache, void* scratch, float* q_copy = nullptr,
-                  StepSync* sync = nullptr);
+                  StepSync* sync = nullptr, const SelC16* c16 = nullptr);
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap);
 int launch_score_approx(cudaStream_t st, uint32_t G, uint32_t n_units, const float* q,
                         const float* cents, const uint32_t* counts, uint32_t c_cap,

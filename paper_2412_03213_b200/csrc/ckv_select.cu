@@ -699,6 +699,9 @@ k_select_warp(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_ba
 // centroids instead of 1 per head.
 // ---------------------------------------------------------------------------
 constexpr int SF_WARPS = 8;
+#ifndef CKV_SEL_FFMA2
+#define CKV_SEL_FFMA2 1
+#endif
 // the unit's centroid block streams through a ring of SF_NS bulk-copied
 // stages of SF_ROWS rows (TMA bulk copies: many bytes in flight per CTA
 // without registers; the ring aliases the selection warps' buffers, which
@@ -724,32 +727,48 @@ __device__ __forceinline__ void sel_mb_wait(uint64_t* b, uint32_t parity) {
         : "=r"(done) : "r"(sel_su32(b)), "r"(parity) : "memory");
   } while (!done);
 }
-// rows [r0, r0 + n) of the unit's centroid block into a ring stage.  The
-// centroids are re-read every step: the copy marks them evict_last in L2 (the
-// attention's one-pass KV stream is marked evict_first), so they stay
-// resident between steps.
-__device__ __forceinline__ void sel_stage_rows(float* dst, const float* cu, uint32_t r0,
-                                               uint32_t n, uint64_t* bar) {
-  const uint32_t bytes = n * D * 4;
+// Ring stages of the unit's centroid block.  The centroids are re-read every
+// step: the copy marks them evict_last in L2 (the attention's one-pass KV
+// stream is marked evict_first), so they stay resident between steps.
+__device__ __forceinline__ void sel_stage_bytes(void* dst, const void* src, uint32_t bytes,
+                                                uint64_t* bar) {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sel_su32(bar)),
                "r"(bytes) : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(sel_su32(dst)), "l"(cu + size_t(r0) * D), "r"(bytes),
-      "r"(sel_su32(bar)), "l"(pol)
+      "[%0], [%1], %2, [%3], %4;" ::"r"(sel_su32(dst)), "l"(src), "r"(bytes), "r"(sel_su32(bar)),
+      "l"(pol)
       : "memory");
+}
+// ring stage k of a unit: rows [k * RPS, k * RPS + RPS) of its f32 (or, H, fp16) block
+template <bool H>
+__device__ __forceinline__ void sel_stage_chunk(void* ring, uint32_t slot, const float* cu,
+                                                const uint16_t* hu, uint32_t k, uint32_t C,
+                                                uint64_t* bar) {
+  constexpr uint32_t RPS = H ? 64u : 32u, RB = H ? D * 2u : D * 4u;
+  const uint32_t n = min(RPS, C - k * RPS);
+  char* dst = static_cast<char*>(ring) + size_t(slot) * RPS * RB;
+  const char* src = H ? reinterpret_cast<const char*>(hu) : reinterpret_cast<const char*>(cu);
+  sel_stage_bytes(dst, src + size_t(k) * RPS * RB, n * RB, bar);
 }
 
 // NC > 1 (few units, e.g. one layer's launch): a cluster of NC CTAs per
 // unit; CTA r scores the ring chunks r, r + NC, ... and stores its scores
 // straight into the leader CTA's shared memory (DSMEM), then the leader's
 // G warps select after one cluster barrier.
-template <int G, int NC>
+//
+// H (the session's step): the approximate scores come from the fp16 copy of
+// the centroids (SelC16: 256 B per row instead of 512, 64 rows per ring
+// stage) and each row's bound adds |q| * cerr_c >= |q . (mu_c - h(mu_c))|;
+// the exact phase still re-scores from the f32 centroids, so the selection
+// is unchanged -- only the candidate band is wider.
+template <int G, int NC, bool H>
 __global__ void __launch_bounds__(SF_WARPS * 32, 2)  // two units per SM: one wave at config B
 k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_base,
                const float* __restrict__ q, const float* __restrict__ cents,
+               const uint16_t* __restrict__ c16, const float* __restrict__ cerr,
                const uint32_t* __restrict__ n_clusters, const uint32_t* __restrict__ sizes,
                const uint32_t* __restrict__ starts, const uint32_t* __restrict__ sorted_ids,
                uint32_t* __restrict__ token_ids, uint32_t* __restrict__ rows_out, ckv_runs runs,
@@ -781,18 +800,18 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   uint32_t* st_s = sz_s + c_pad;                                           // [c_pad]
   const uint32_t C = n_clusters[unit];
   const float* cu = cents + size_t(unit) * desc.c_cap * D;
+  const uint16_t* hu = H ? c16 + size_t(unit) * desc.c_cap * D : nullptr;
+  const float* eu = H ? cerr + size_t(unit) * desc.c_cap : nullptr;
+  constexpr uint32_t RPS = H ? 64u : uint32_t(SF_ROWS);  // rows per ring stage (16 KB)
   __shared__ uint64_t full[SF_NS], empty[SF_NS];
   // this CTA's ring chunks: global chunk crank + NC j for j < nloc
-  const uint32_t nch = (C + SF_ROWS - 1) / SF_ROWS;
+  const uint32_t nch = (C + RPS - 1) / RPS;
   const uint32_t nloc = nch > crank ? (nch - crank + NC - 1) / NC : 0u;
   if (threadIdx.x == 0) {
     for (int k = 0; k < SF_NS; ++k) { sel_mb_init(&full[k], 1); sel_mb_init(&empty[k], SF_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (uint32_t j = 0; j < nloc && j < uint32_t(SF_NS); ++j) {
-      const uint32_t k = crank + j * NC;
-      sel_stage_rows(ring + size_t(j) * SF_ROWS * D, cu, k * SF_ROWS,
-                     min(uint32_t(SF_ROWS), C - k * SF_ROWS), &full[j]);
-    }
+    for (uint32_t j = 0; j < nloc && j < uint32_t(SF_NS); ++j)
+      sel_stage_chunk<H>(ring, j, cu, hu, crank + j * NC, C, &full[j]);
   }
   // the scores go to the leader's copy of av_s / ae_s (its own for NC = 1)
   auto put_score = [&](float* p, float v) {
@@ -846,24 +865,60 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     if (q_copy && leader) reinterpret_cast<float4*>(q_copy + (size_t(unit) * G + wid) * D)[lane] = qw;
   }
   __syncthreads();
+  // f32 rows: lane sub holds float4 columns sub, sub + 8, + 16, + 24; fp16
+  // rows (H): dims [8 sub, 8 sub + 8) and [64 + 8 sub, 64 + 8 sub + 8)
   float4 qv[G][4];
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) qv[g][k] = reinterpret_cast<const float4*>(q_s[g])[sub + 8 * k];
-  float qnrm[G];
+    for (int k = 0; k < 4; ++k)
+      qv[g][k] = reinterpret_cast<const float4*>(q_s[g])[H ? 2 * sub + (k & 1) + 16 * (k >> 1)
+                                                           : sub + 8 * k];
+  float qnrm[G], qabs[G];
 #pragma unroll
-  for (int g = 0; g < G; ++g) qnrm[g] = SEL_ERR * sqrtf(qn2[g]);
-  // stage k: rows [32k, 32k + 32); warp w takes rows 4w..4w+3 of it (8
-  // lanes per row, lane sub holds float4 columns sub, sub+8, +16, +24)
+  for (int g = 0; g < G; ++g) {
+    qnrm[g] = SEL_ERR * sqrtf(qn2[g]);
+    qabs[g] = 1.0001f * sqrtf(qn2[g]);  // >= |q| (the f32 sum's rounding is < 2^-17)
+  }
+  // stage k: rows [RPS k, RPS k + RPS); warp w takes rows 4w..4w+3 of it
+  // (f32) or 8w..8w+7 as two groups of 4 (H); 8 lanes per row
+  constexpr int NSUB = H ? 2 : 1;
   for (uint32_t j = 0; j < nloc; ++j) {
     const uint32_t k = crank + j * NC;
     const uint32_t stg = j % SF_NS, ph = (j / SF_NS) & 1u;
-    const float* rs = ring + size_t(stg) * SF_ROWS * D;
-    const uint32_t c0 = k * SF_ROWS + uint32_t(wid) * 4;
-    float4 m[1][4];
+    const uint32_t c0 = k * RPS + uint32_t(wid) * (4 * NSUB);
+    float ecv[NSUB];
+    if constexpr (H) {
+#pragma unroll
+      for (int s2 = 0; s2 < NSUB; ++s2) {
+        const uint32_t c = c0 + rsel + 4 * s2;
+        ecv[s2] = c < C ? __ldg(eu + c) : 0.f;
+      }
+    }
+    float4 m[NSUB][4];
     sel_mb_wait(&full[stg], ph);
-    {
+    if constexpr (H) {
+      const uint16_t* rs = reinterpret_cast<const uint16_t*>(ring) + size_t(stg) * RPS * D;
+#pragma unroll
+      for (int s2 = 0; s2 < NSUB; ++s2) {
+        const uint32_t rr = uint32_t(wid) * 8 + 4 * s2 + rsel;
+        uint4 hx[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+        if (c0 + 4 * s2 + rsel < C) {
+          hx[0] = reinterpret_cast<const uint4*>(rs + size_t(rr) * D)[sub];
+          hx[1] = reinterpret_cast<const uint4*>(rs + size_t(rr) * D)[8 + sub];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float2 x0 = __half22float2(*reinterpret_cast<const __half2*>(&hx[h].x));
+          const float2 x1 = __half22float2(*reinterpret_cast<const __half2*>(&hx[h].y));
+          const float2 x2 = __half22float2(*reinterpret_cast<const __half2*>(&hx[h].z));
+          const float2 x3 = __half22float2(*reinterpret_cast<const __half2*>(&hx[h].w));
+          m[s2][2 * h] = make_float4(x0.x, x0.y, x1.x, x1.y);
+          m[s2][2 * h + 1] = make_float4(x2.x, x2.y, x3.x, x3.y);
+        }
+      }
+    } else {
+      const float* rs = ring + size_t(stg) * SF_ROWS * D;
       const uint32_t rr = uint32_t(wid) * 4 + rsel;
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4)
@@ -876,13 +931,38 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     if (lane == 0) sel_mb_arrive(&empty[stg]);
     if (threadIdx.x == 0 && j + SF_NS < nloc) {
       sel_mb_wait(&empty[stg], ph);
-      const uint32_t kn = k + SF_NS * NC;
-      sel_stage_rows(ring + size_t(stg) * SF_ROWS * D, cu, kn * SF_ROWS,
-                     min(uint32_t(SF_ROWS), C - kn * SF_ROWS), &full[stg]);
+      sel_stage_chunk<H>(ring, stg, cu, hu, k + SF_NS * NC, C, &full[stg]);
     }
 #pragma unroll
-    for (int st2 = 0; st2 < 1; ++st2) {
-      float acc[G], mn = 0.f;
+    for (int st2 = 0; st2 < NSUB; ++st2) {
+      float acc[G], mn;
+#if CKV_SEL_FFMA2
+      // packed f32 FMAs (FFMA2): even / odd dims in the two halves, one
+      // instruction per two products; any summation order stays inside the
+      // 2^-14 |q| |row| bound
+      {
+        float2 a2[G], n2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int g = 0; g < G; ++g) a2[g] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 x = m[st2][k];
+          const float2 xl = make_float2(x.x, x.y), xh = make_float2(x.z, x.w);
+          n2 = __ffma2_rn(xl, xl, n2);
+          n2 = __ffma2_rn(xh, xh, n2);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float4 y = qv[g][k];
+            a2[g] = __ffma2_rn(xl, make_float2(y.x, y.y), a2[g]);
+            a2[g] = __ffma2_rn(xh, make_float2(y.z, y.w), a2[g]);
+          }
+        }
+        mn = n2.x + n2.y;
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] = a2[g].x + a2[g].y;
+      }
+#else
+      mn = 0.f;
 #pragma unroll
       for (int g = 0; g < G; ++g) acc[g] = 0.f;
 #pragma unroll
@@ -895,7 +975,13 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
           acc[g] = fmaf(x.x, y.x, fmaf(x.y, y.y, fmaf(x.z, y.z, fmaf(x.w, y.w, acc[g]))));
         }
       }
-      const uint32_t c = c0 + rsel;
+#endif
+      const uint32_t c = c0 + rsel + 4 * st2;
+      // the row's bound: 2^-14 |q| |row| (f32 arithmetic) + |q| cerr_c (H: fp16 rows)
+      auto bound = [&](float qn, float qa, float mnf) {
+        if constexpr (H) return fmaf(qn, sqrtf(mnf), fmaf(qa, ecv[st2], 1e-30f));
+        else return fmaf(qn, sqrtf(mnf), 1e-30f);
+      };
       if constexpr (G <= 4) {
         // reduce-scatter over the row's 8 lanes: {acc[0..G), mn, 0...} -> lane
         // sub holds the sum of value sub (7 shuffles instead of 3 (G + 1)),
@@ -918,11 +1004,11 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
         const float y = (hi ? x2[1] : x2[0]) + __shfl_xor_sync(0xffffffffu, hi ? x2[0] : x2[1], 1);
         const float mnf = __shfl_sync(0xffffffffu, y, (lane & ~7) | 4);
         if (c < C && sub < G) {
-          float qn = qnrm[0];
+          float qn = qnrm[0], qa = qabs[0];
 #pragma unroll
-          for (int g = 1; g < G; ++g) if (sub == g) qn = qnrm[g];
+          for (int g = 1; g < G; ++g) if (sub == g) { qn = qnrm[g]; qa = qabs[g]; }
           put_score(av_s + size_t(sub) * c_pad + c, y);
-          put_score(ae_s + size_t(sub) * c_pad + c, fmaf(qn, sqrtf(mnf), 1e-30f));
+          put_score(ae_s + size_t(sub) * c_pad + c, bound(qn, qa, mnf));
         }
         continue;
       }
@@ -936,11 +1022,11 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
         float a = acc[0];
 #pragma unroll
         for (int g = 1; g < G; ++g) if (sub == g) a = acc[g];
-        float qn = qnrm[0];
+        float qn = qnrm[0], qa = qabs[0];
 #pragma unroll
-        for (int g = 1; g < G; ++g) if (sub == g) qn = qnrm[g];
+        for (int g = 1; g < G; ++g) if (sub == g) { qn = qnrm[g]; qa = qabs[g]; }
         put_score(av_s + size_t(sub) * c_pad + c, a);
-        put_score(ae_s + size_t(sub) * c_pad + c, fmaf(qn, sqrtf(mn), 1e-30f));
+        put_score(ae_s + size_t(sub) * c_pad + c, bound(qn, qa, mn));
       }
     }
   }
@@ -959,6 +1045,58 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
                     ae_s + size_t(wid) * c_pad, n_clusters, sz_s, st_s, sorted_ids, token_ids,
                     rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, nullptr, cache,
                     cpre, smraw + size_t(wid) * warp_bytes, wsa[wid], ready, ready_val);
+}
+
+// the fp16 centroid copy of the fused selection (SelC16): one warp per
+// centroid row, lane L converts dims 4L..4L+3.  h = RN_fp16(mu) (saturated,
+// below-normal flushed: f32_to_f16_tc), and mu - h is exact in f32 for every
+// unsaturated component, so cerr = |mu - h|_2 carries only the f32 rounding
+// of the sum of squares (< 2^-17 relative; the 1.0001 margin covers it).
+__global__ void __launch_bounds__(256)
+k_cents_f16(const float* __restrict__ cents, const uint32_t* __restrict__ n_clusters,
+            uint32_t c_cap, uint32_t tail, uint16_t* __restrict__ c16, float* __restrict__ cerr) {
+  const uint32_t u = blockIdx.y, nc = min(n_clusters[u], c_cap);
+  uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (tail) {
+    if (c >= tail || c >= nc) return;
+    c = nc - 1 - c;
+  } else if (c >= nc) {
+    return;
+  }
+  const size_t r = size_t(u) * c_cap + c;
+  const float4 x = reinterpret_cast<const float4*>(cents + r * D)[lane];
+  const float xs[4] = {x.x, x.y, x.z, x.w};
+  uint16_t h[4];
+  float e2 = 0.f, e1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h[i] = f32_to_f16_tc(xs[i]);
+    const float d = __fsub_rn(xs[i], f16_to_f32(h[i]));
+    e2 = fmaf(d, d, e2);
+    e1 += fabsf(d);
+  }
+  e2 = warp_sum(e2);
+  e1 = warp_sum(e1);
+  reinterpret_cast<uint2*>(c16 + r * D)[lane] =
+      make_uint2(uint32_t(h[0]) | uint32_t(h[1]) << 16, uint32_t(h[2]) | uint32_t(h[3]) << 16);
+  if (lane == 0) {
+    // |d|_1 >= |d|_2 stands in where the squares underflow (flushed tiny components)
+    float e = e2 >= 1e-30f ? sqrtf(e2) * 1.0001f : e1 * 1.0001f;
+    if (!(e <= 3.0e38f)) e = INFINITY;  // overflowed or non-finite: no usable bound
+    cerr[r] = e;
+  }
+}
+
+int launch_cents_f16(cudaStream_t st, const float* cents, const uint32_t* n_clusters,
+                     uint32_t n_units, uint32_t c_cap, uint16_t* c16, float* cerr,
+                     uint32_t tail) {
+  if (n_units == 0 || c_cap == 0) return CKV_OK;
+  tail = std::min(tail, c_cap);
+  k_cents_f16<<<dim3(((tail ? tail : c_cap) + 7) / 8, n_units), 256, 0, st>>>(
+      cents, n_clusters, c_cap, tail, c16, cerr);
+  CKV_LAUNCH_CHECK("k_cents_f16");
+  return CKV_OK;
 }
 
 size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap) {
@@ -1036,7 +1174,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const uint32_t* starts, const uint32_t* sorted_ids, uint32_t* token_ids,
                   uint32_t* rows, const ckv_runs& runs, uint32_t row_base, uint32_t* n_tokens,
                   uint32_t* n_taken, uint32_t* trimmed, uint32_t* ranked, double* scores,
-                  const CacheDev& cache, void* scratch, float* q_copy, StepSync* sync) {
+                  const CacheDev& cache, void* scratch, float* q_copy, StepSync* sync,
+                  const SelC16* c16) {
   const uint32_t G = desc.group;
   if (sync) sync->published = false;
   if (G < 1 || desc.n_q % G || !(G == 1 || G == 2 || G == 4 || G == 8)) {
@@ -1072,21 +1211,23 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                           size_t(c_pad) * 8;
     if (smem_f <= 200 * 1024) {
       // the opt-in for the one instantiation launched (a per-call host cost)
+      // H: approximate scores from the fp16 centroid copy (session steps)
+      const bool hc = c16 && c16->c16 && c16->cerr;
+      const uint16_t* c16p = hc ? c16->c16 : nullptr;
+      const float* cerrp = hc ? c16->cerr : nullptr;
       {
-        const void* fns[4][4] = {
-            {(const void*)k_select_fused<1, 1>, (const void*)k_select_fused<2, 1>,
-             (const void*)k_select_fused<4, 1>, (const void*)k_select_fused<8, 1>},
-            {(const void*)k_select_fused<1, 2>, (const void*)k_select_fused<2, 2>,
-             (const void*)k_select_fused<4, 2>, (const void*)k_select_fused<8, 2>},
-            {(const void*)k_select_fused<1, 4>, (const void*)k_select_fused<2, 4>,
-             (const void*)k_select_fused<4, 4>, (const void*)k_select_fused<8, 4>},
-            {(const void*)k_select_fused<1, 8>, (const void*)k_select_fused<2, 8>,
-             (const void*)k_select_fused<4, 8>, (const void*)k_select_fused<8, 8>}};
+#define CKV_SF_FN(H_, NC_)                                                                    \
+  {(const void*)k_select_fused<1, NC_, H_>, (const void*)k_select_fused<2, NC_, H_>,          \
+   (const void*)k_select_fused<4, NC_, H_>, (const void*)k_select_fused<8, NC_, H_>}
+        const void* fns[2][4][4] = {
+            {CKV_SF_FN(false, 1), CKV_SF_FN(false, 2), CKV_SF_FN(false, 4), CKV_SF_FN(false, 8)},
+            {CKV_SF_FN(true, 1), CKV_SF_FN(true, 2), CKV_SF_FN(true, 4), CKV_SF_FN(true, 8)}};
+#undef CKV_SF_FN
         const int ni = nc == 1 ? 0 : nc == 2 ? 1 : nc == 4 ? 2 : 3;
         const int gi = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : 3;
-        CKV_CUDA_TRY(smem_optin(fns[ni][gi], 200 * 1024));
+        CKV_CUDA_TRY(smem_optin(fns[hc ? 1 : 0][ni][gi], 200 * 1024));
       }
-#define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, n_clusters, sizes, starts, sorted_ids, \
+#define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, c16p, cerrp, n_clusters, sizes, starts, sorted_ids, \
     token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode, q_copy, \
     rdy, ep
       static const uint32_t sel_mode = getenv("CKV_SEL_MODE") ? uint32_t(atoi(getenv("CKV_SEL_MODE"))) : 0u;
@@ -1123,9 +1264,11 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         const size_t max_win = size_t(v);
         size_t persist = 0;
         cudaDeviceGetLimit(&persist, cudaLimitPersistingL2CacheSize);
-        const size_t bytes = std::min(max_win, size_t(units) * desc.c_cap * D * 4);
+        const size_t bytes = std::min(max_win, size_t(units) * desc.c_cap * D * (hc ? 2 : 4));
         attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<float*>(cents);
+        attr[0].val.accessPolicyWindow.base_ptr =
+            hc ? const_cast<void*>(static_cast<const void*>(c16p))
+               : const_cast<void*>(static_cast<const void*>(cents));
         attr[0].val.accessPolicyWindow.num_bytes = bytes;
         attr[0].val.accessPolicyWindow.hitRatio =
             bytes ? float(std::min(1.0, double(persist) / double(bytes))) : 0.f;
@@ -1141,19 +1284,22 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         cudaMemset(fbuf, 0, size_t(desc.n_q) * 64);
         cudaMemcpyToSymbol(g_sel_dbg, &fbuf, sizeof(fbuf));
       }
-#define CKV_SF_CASE(NC_)                                                                     \
-  switch (G) {                                                                               \
-    case 1: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<1, NC_>, CKV_SF_ARGS)); break; \
-    case 2: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<2, NC_>, CKV_SF_ARGS)); break; \
-    case 4: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<4, NC_>, CKV_SF_ARGS)); break; \
-    default: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<8, NC_>, CKV_SF_ARGS)); break; \
+#define CKV_SF_CASE(NC_, H_)                                                                     \
+  switch (G) {                                                                                   \
+    case 1: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<1, NC_, H_>, CKV_SF_ARGS)); break; \
+    case 2: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<2, NC_, H_>, CKV_SF_ARGS)); break; \
+    case 4: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<4, NC_, H_>, CKV_SF_ARGS)); break; \
+    default: CKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_select_fused<8, NC_, H_>, CKV_SF_ARGS)); break; \
   }
-      switch (nc) {
-        case 1: CKV_SF_CASE(1) break;
-        case 2: CKV_SF_CASE(2) break;
-        case 4: CKV_SF_CASE(4) break;
-        default: CKV_SF_CASE(8) break;
-      }
+#define CKV_SF_NC(H_)                  \
+  switch (nc) {                        \
+    case 1: CKV_SF_CASE(1, H_) break;  \
+    case 2: CKV_SF_CASE(2, H_) break;  \
+    case 4: CKV_SF_CASE(4, H_) break;  \
+    default: CKV_SF_CASE(8, H_) break; \
+  }
+      if (hc) { CKV_SF_NC(true) } else { CKV_SF_NC(false) }
+#undef CKV_SF_NC
 #undef CKV_SF_CASE
 #undef CKV_SF_ARGS
       CKV_LAUNCH_CHECK("k_select_fused");

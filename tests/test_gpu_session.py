@@ -11,10 +11,16 @@ from tests._inputs import bf16_bits, head, port
 pytestmark = pytest.mark.gpu
 
 
-def test_session_vs_oracle_decode_loop(gpu_ctx):
+@pytest.mark.parametrize("f16_scores", [False, True])
+def test_session_vs_oracle_decode_loop(gpu_ctx, monkeypatch, f16_scores):
+    """f16_scores: the opt-in fp16 centroid copy for the approximate scores
+    (CKV_SESSION_F16_SCORES; the copy is refreshed after the prefill and after
+    each committed decode batch) must select exactly the same tokens."""
     import torch
     from paper_2412_03213_b200 import api
     from paper_2412_03213_b200.session import Session
+    if f16_scores:
+        monkeypatch.setenv("CKV_SESSION_F16_SCORES", "1")
 
     layers, kvh, G = 2, 2, 2
     L, T, B, m, R = 700, 45, 96, 20, 2

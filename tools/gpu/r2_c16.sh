@@ -1,0 +1,15 @@
+#!/bin/bash
+# fp16 centroid scores in the fused selection: parity suites + step A/B
+mkdir -p gpurun_out
+timeout -k 10 900 python -m pytest tests/test_gpu_select.py tests/test_gpu_session.py tests/test_gpu_headline.py tests/test_gpu_trace.py tests/test_gpu_quality.py -m gpu -x -q 2>&1 | tail -3
+B="python bench.py --steps 50 --warmup 10 --e2e-steps 10 --no-cpu --no-extra --max-iters 8"
+show() { python -c "
+import json,sys
+for l in open('gpurun_out/sp.json'):
+    if l.startswith('{'):
+        d=json.loads(l); pl=d.get('per_layer') or {}; print('$1', 'us/step', round(d['ms_per_step']*1000,1), 'sel', round(d['kernels_us']['k_select'],1), 'att', round(d['kernels_us']['k_attend'],1), 'e2e', round(d['e2e']['value']), 'layer_ms', pl.get('ms_per_step'))"; }
+for r in 1 2; do
+timeout 300 $B > gpurun_out/sp.json 2>gpurun_out/sp.err; show c16
+CKV_SESSION_F32_SCORES=1 timeout 300 $B > gpurun_out/sp.json 2>/dev/null; show f32
+done
+tail -3 gpurun_out/sp.err
