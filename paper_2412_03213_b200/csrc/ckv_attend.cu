@@ -112,7 +112,22 @@ __device__ __forceinline__ void consumer_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(AT_CWARPS * 32) : "memory");
 }
 
+#ifndef CKV_AT_FFMA2
+#define CKV_AT_FFMA2 1  // packed f32 FMAs (FFMA2) for the logits and the value update
+#endif
 __device__ __forceinline__ float dot8(const uint4 k, const float* qv) {
+#if CKV_AT_FFMA2
+  float2 s = make_float2(0.f, 0.f);
+  s = __ffma2_rn(make_float2(__uint_as_float(k.x << 16), __uint_as_float(k.x & 0xffff0000u)),
+                 make_float2(qv[0], qv[1]), s);
+  s = __ffma2_rn(make_float2(__uint_as_float(k.y << 16), __uint_as_float(k.y & 0xffff0000u)),
+                 make_float2(qv[2], qv[3]), s);
+  s = __ffma2_rn(make_float2(__uint_as_float(k.z << 16), __uint_as_float(k.z & 0xffff0000u)),
+                 make_float2(qv[4], qv[5]), s);
+  s = __ffma2_rn(make_float2(__uint_as_float(k.w << 16), __uint_as_float(k.w & 0xffff0000u)),
+                 make_float2(qv[6], qv[7]), s);
+  return s.x + s.y;
+#else
   float s = 0.f;
   s = fmaf(__uint_as_float(k.x << 16), qv[0], s);
   s = fmaf(__uint_as_float(k.x & 0xffff0000u), qv[1], s);
@@ -123,9 +138,37 @@ __device__ __forceinline__ float dot8(const uint4 k, const float* qv) {
   s = fmaf(__uint_as_float(k.w << 16), qv[6], s);
   s = fmaf(__uint_as_float(k.w & 0xffff0000u), qv[7], s);
   return s;
+#endif
+}
+
+// acc *= sc in packed pairs
+__device__ __forceinline__ void scale8(float sc, float* acc) {
+#if CKV_AT_FFMA2
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 r = __fmul2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), make_float2(sc, sc));
+    acc[2 * i] = r.x;
+    acc[2 * i + 1] = r.y;
+  }
+#else
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] *= sc;
+#endif
 }
 
 __device__ __forceinline__ void axpy8(float p, const uint4 v, float* acc) {
+#if CKV_AT_FFMA2
+  const float2 pp = make_float2(p, p);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 r = __ffma2_rn(
+        pp, make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u)),
+        make_float2(acc[2 * i], acc[2 * i + 1]));
+    acc[2 * i] = r.x;
+    acc[2 * i + 1] = r.y;
+  }
+#else
   acc[0] = fmaf(p, __uint_as_float(v.x << 16), acc[0]);
   acc[1] = fmaf(p, __uint_as_float(v.x & 0xffff0000u), acc[1]);
   acc[2] = fmaf(p, __uint_as_float(v.y << 16), acc[2]);
@@ -134,6 +177,7 @@ __device__ __forceinline__ void axpy8(float p, const uint4 v, float* acc) {
   acc[5] = fmaf(p, __uint_as_float(v.z & 0xffff0000u), acc[5]);
   acc[6] = fmaf(p, __uint_as_float(v.w << 16), acc[6]);
   acc[7] = fmaf(p, __uint_as_float(v.w & 0xffff0000u), acc[7]);
+#endif
 }
 
 struct __align__(128) AttSmem {
@@ -429,8 +473,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
         for (int kk = 0; kk < AT_RPH; ++kk) mn = fmaxf(mn, s[kk]);
         const float sc = ex2(m - mn);  // m = -inf -> 0
         l *= sc;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] *= sc;
+        scale8(sc, acc);
 #pragma unroll
         for (int kk = 0; kk < AT_RPH; ++kk) {
           const float p = ex2(s[kk] - mn);
@@ -451,8 +494,7 @@ k_attend(ckv_attend_desc desc, uint32_t splits, const float* __restrict__ q,
         if (mn != -INFINITY) {
           const float sc = ex2(m - mn);
           l *= sc;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] *= sc;
+          scale8(sc, acc);
 #pragma unroll
           for (int kk = 0; kk < AT_RPH; ++kk) {
             if (s[kk] != -INFINITY) {

@@ -135,36 +135,52 @@ __global__ void k_init_centroids(const uint16_t* __restrict__ keys, uint64_t key
 
 // normalize() (common.hpp:141-147) of every centroid -> f32 dirs (exact),
 // fp16 dirs (tensor-core B operand), f64 norms (for cosine_distance).
-// One thread per centroid: the norm is a sequential f64 chain by contract.
-__global__ void k_dirs(const float* __restrict__ cents, uint32_t C, uint32_t c_stride,
-                       uint32_t c_pad, float* __restrict__ dirs, uint16_t* __restrict__ dirs16,
-                       double* __restrict__ cnorm, float* __restrict__ deps,
-                       const int32_t* __restrict__ active) {
+// One warp per centroid: the row is loaded coalesced (lane L holds dims
+// 4L..4L+3) and staged in shared memory, where lane 0 runs the norm's
+// sequential f64 chain (the contract's order); every lane then divides and
+// stores its four dims (coalesced 16-B / 8-B stores).
+__global__ void __launch_bounds__(256)
+k_dirs(const float* __restrict__ cents, uint32_t C, uint32_t c_stride, uint32_t c_pad,
+       float* __restrict__ dirs, uint16_t* __restrict__ dirs16, double* __restrict__ cnorm,
+       float* __restrict__ deps, const int32_t* __restrict__ active) {
   const uint32_t u = blockIdx.y;
   if (active && !active[u]) return;
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t c = blockIdx.x * 8 + uint32_t(w);
   if (c >= c_pad) return;
-  float* dr = dirs + (size_t(u) * c_pad + c) * D;
-  uint16_t* db = dirs16 + (size_t(u) * c_pad + c) * D;
+  float4* dr = reinterpret_cast<float4*>(dirs + (size_t(u) * c_pad + c) * D) + lane;
+  uint2* db = reinterpret_cast<uint2*>(dirs16 + (size_t(u) * c_pad + c) * D) + lane;
   if (c >= C) {  // padding columns of the MMA operand
-    for (int j = 0; j < D; ++j) { dr[j] = 0.f; db[j] = 0; }
-    deps[size_t(u) * c_pad + c] = 0.f;
+    *dr = make_float4(0.f, 0.f, 0.f, 0.f);
+    *db = make_uint2(0u, 0u);
+    if (lane == 0) deps[size_t(u) * c_pad + c] = 0.f;
     return;
   }
-  const float* src = cents + (size_t(u) * c_stride + c) * D;
-  double nrm = sqrt(dot_seq_ff(src, src));
-  cnorm[size_t(u) * c_pad + c] = nrm;
+  __shared__ float row[8][D];
+  const float4 x = reinterpret_cast<const float4*>(cents + (size_t(u) * c_stride + c) * D)[lane];
+  reinterpret_cast<float4*>(row[w])[lane] = x;
+  __syncwarp();
+  double nrm = 0.0;
+  if (lane == 0) {
+    nrm = sqrt(dot_seq_ff(row[w], row[w]));
+    cnorm[size_t(u) * c_pad + c] = nrm;
+  }
+  nrm = __shfl_sync(0xffffffffu, nrm, 0);
+  const float xs[4] = {x.x, x.y, x.z, x.w};
+  float y[4];
+  uint16_t h[4];
   double e2 = 0.0;
-  for (int j = 0; j < D; ++j) {
-    float x = src[j];
-    float y = nrm > 0.0 ? float(double(x) / nrm) : x;
-    dr[j] = y;
-    const uint16_t b = f32_to_f16_tc(y);
-    db[j] = b;
-    const double e = double(y) - double(f16_to_f32(b));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    y[i] = nrm > 0.0 ? float(double(xs[i]) / nrm) : xs[i];
+    h[i] = f32_to_f16_tc(y[i]);
+    const double e = double(y[i]) - double(f16_to_f32(h[i]));
     e2 += e * e;
   }
-  deps[size_t(u) * c_pad + c] = float(sqrt(e2)) * 1.0001f;
+  *dr = make_float4(y[0], y[1], y[2], y[3]);
+  *db = make_uint2(uint32_t(h[0]) | uint32_t(h[1]) << 16, uint32_t(h[2]) | uint32_t(h[3]) << 16);
+  e2 = warp_sum(e2);  // any order: the 1.0001 margin covers the rounding of the sum
+  if (lane == 0) deps[size_t(u) * c_pad + c] = float(sqrt(e2)) * 1.0001f;
 }
 
 // ---------------------------------------------------------------------------
@@ -652,8 +668,8 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
   k_init_centroids<<<dim3(C, U), 128, 0, st>>>(a.keys, a.key_stride, a.init_rows, C, CS,
                                                 a.centroids);
   CKV_LAUNCH_CHECK("k_init_centroids");
-  k_dirs<<<dim3((c_pad + 127) / 128, U), 128, 0, st>>>(a.centroids, C, CS, c_pad, dirs, dirs16,
-                                                       cnorm, deps, active);
+  k_dirs<<<dim3((c_pad + 7) / 8, U), 256, 0, st>>>(a.centroids, C, CS, c_pad, dirs, dirs16,
+                                                    cnorm, deps, active);
   CKV_LAUNCH_CHECK("k_dirs");
   ctx->launches += 2;
 
