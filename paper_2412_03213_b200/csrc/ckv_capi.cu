@@ -216,6 +216,7 @@ __global__ void k_append_kv(const uint16_t* __restrict__ kn, const uint16_t* __r
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (epoch && u == 0 && j == 0) ++*epoch;
   if (work && j == 0) work[u] = 0u;  // the attention work counters (per slice start unit)
+  if (!kn) return;  // the fused selection appended the row
   const uint4* ks = reinterpret_cast<const uint4*>(kn + size_t(u) * D);
   const uint4* vs = reinterpret_cast<const uint4*>(vn + size_t(u) * D);
   reinterpret_cast<uint4*>(K + (size_t(u) * p_cap + pos) * D)[j] = ks[j];
@@ -953,6 +954,11 @@ struct ckv_session {
   // the previous selection, and the stream's last kernel is the append
   // (CKV_SEL_EARLY for the next step's selections)
   bool sel_early = false;
+  // this step's new K/V rows while its selection is launched (the fused
+  // selection appends them; app_done: every slice's launch did)
+  const uint16_t* app_k = nullptr;
+  const uint16_t* app_v = nullptr;
+  bool app_done = false;
   bool step_early = false;  // this step's selections may start early
   // physical two-tier cache (CKV_SESSION_TIERED / _TIER_HOST, ckv_tier.cu)
   bool tiered = false;
@@ -1280,6 +1286,12 @@ static bool session_no_early() {
   return off;
 }
 
+// CKV_SESSION_NO_FOLD_APPEND=1: the append kernel copies the new K/V rows
+// (instead of the fused selection)
+static bool session_no_fold_append() {
+  static const bool v = getenv("CKV_SESSION_NO_FOLD_APPEND") != nullptr;
+  return v;
+}
 static bool session_no_stepsync() {
   static const bool off = getenv("CKV_SESSION_NO_STEPSYNC") != nullptr;
   return off;
@@ -1321,6 +1333,14 @@ static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
   if (sync) {
     ls = *sync;
     ls.ready += h0;
+    if (s->app_k) {  // this slice's units append their new rows
+      ls.app_k = s->app_k + size_t(u0) * D;
+      ls.app_v = s->app_v + size_t(u0) * D;
+      ls.K = s->K + size_t(u0) * s->p_cap * D;
+      ls.V = s->V + size_t(u0) * s->p_cap * D;
+      ls.app_pos = s->n_ctx;
+      ls.p_cap = s->p_cap;
+    }
   }
   const SelC16 hc{s->use_c16 ? s->c16 + size_t(u0) * s->c_cap * D : nullptr,
                   s->use_c16 ? s->cerr + size_t(u0) * s->c_cap : nullptr};
@@ -1331,7 +1351,12 @@ static int session_select_slice(ckv_session* s, cudaStream_t st, uint32_t u0, ui
                         sd.row_base, s->n_tokens + h0, s->n_taken + h0, s->trimmed + h0,
                         s->ranked + size_t(h0) * s->c_cap, nullptr, cache, s->sel_scratch, qc,
                         sync ? &ls : nullptr, s->use_c16 ? &hc : nullptr));
-  if (sync) sync->published = ls.published;
+  if (sync) {
+    sync->published = ls.published;
+    s->app_done = s->app_done && ls.appended;
+  } else {
+    s->app_done = false;
+  }
   s->ctx->launches += 2;
   return CKV_OK;
 }
@@ -1583,12 +1608,19 @@ int ckv_session_step(ckv_session* s, const float* q, const uint16_t* kn, const u
     }
   }
   s->step_early = early;
+  // the fused selection copies the new K/V rows when every slice takes them
+  s->app_k = session_no_fold_append() ? nullptr : kd;
+  s->app_v = vd;
+  s->app_done = s->app_k != nullptr;
   const int rc_sa = session_select_attend(s, qd, od, q_copy);
   s->step_early = false;
+  s->app_k = s->app_v = nullptr;
   CKV_TRY(rc_sa);
-  // append this step's token (harness.hpp:318-320)
-  k_append_kv<<<s->U, 16, 0, st>>>(kd, vd, s->K, s->V, s->n_ctx, s->p_cap, s->step_epoch,
-                                   s->step_work);
+  const bool appended = s->app_done;
+  // append this step's token (harness.hpp:318-320), unless the selection did;
+  // the kernel still advances the StepSync epoch and zeroes the work counters
+  k_append_kv<<<s->U, 16, 0, st>>>(appended ? nullptr : kd, vd, s->K, s->V, s->n_ctx, s->p_cap,
+                                   s->step_epoch, s->step_work);
   CKV_LAUNCH_CHECK("k_append_kv");
   s->ctx->launches++;
   s->n_ctx++;

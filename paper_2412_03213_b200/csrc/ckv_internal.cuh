@@ -122,6 +122,25 @@ struct StepSync {
   // selected while published heads wait); zeroed by the step's last kernel
   uint32_t* work = nullptr;
   bool published = false;
+  // the step's K/V append (harness.hpp:318-320), folded into the fused
+  // selection: each unit's leader CTA copies its new row (k, v: this slice's
+  // first unit; possibly mapped host memory) to K/V row pos, which no kernel
+  // of this step reads (the recency range ends at pos).  Set `appended` when
+  // the launch took it; otherwise k_append_kv copies the row.
+  const uint16_t* app_k = nullptr;
+  const uint16_t* app_v = nullptr;
+  uint16_t* K = nullptr;
+  uint16_t* V = nullptr;
+  uint32_t app_pos = 0, p_cap = 0;
+  bool appended = false;
+};
+// the fused selection's append operand (a null k skips it)
+struct SelAppend {
+  const uint16_t* k;
+  const uint16_t* v;
+  uint16_t* K;
+  uint16_t* V;
+  uint32_t pos, p_cap;
 };
 // fp16 copy of a centroid block for the fused selection's approximate
 // scores: c16[u][c] = RN_fp16(mu_c) and cerr[u][c] >= |mu_c - c16[u][c]|_2

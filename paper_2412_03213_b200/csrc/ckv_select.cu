@@ -775,7 +775,8 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
                uint32_t* __restrict__ n_tokens, uint32_t* __restrict__ n_taken_out,
                uint32_t* __restrict__ trimmed_out, uint32_t* __restrict__ ranked_out,
                CacheDev cache, uint32_t warp_bytes, uint32_t mode, float* __restrict__ q_copy,
-               uint32_t* __restrict__ ready, const uint32_t* __restrict__ epoch) {
+               uint32_t* __restrict__ ready, const uint32_t* __restrict__ epoch,
+               SelAppend app) {
   static_assert(G <= SF_WARPS, "one select warp per head");
   const uint32_t unit = blockIdx.x / NC;
   uint32_t crank = 0;
@@ -837,6 +838,15 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
   if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the step's append (after the wait: the previous step's kernels are done
+  // with row pos's neighbours): the last warp copies the unit's new k / v row
+  // (16 lanes x 16 B each), in flight beside the q reads below
+  if (app.k && leader && wid == SF_WARPS - 1) {
+    const uint32_t j = uint32_t(lane) & 15u;
+    const uint16_t* src = (lane < 16 ? app.k : app.v) + size_t(unit) * D;
+    uint16_t* dst = (lane < 16 ? app.K : app.V) + (size_t(unit) * app.p_cap + app.pos) * D;
+    reinterpret_cast<uint4*>(dst)[j] = __ldg(reinterpret_cast<const uint4*>(src) + j);
+  }
   // StepSync: the attention may launch now (every CTA of this grid is
   // resident once all have passed here); it waits per q head on ready[]
   uint32_t ready_val = 0u;
@@ -1177,7 +1187,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
                   const CacheDev& cache, void* scratch, float* q_copy, StepSync* sync,
                   const SelC16* c16) {
   const uint32_t G = desc.group;
-  if (sync) sync->published = false;
+  if (sync) sync->published = sync->appended = false;
   if (G < 1 || desc.n_q % G || !(G == 1 || G == 2 || G == 4 || G == 8)) {
     set_error("select: group must be 1, 2, 4 or 8 and divide n_q");
     return CKV_EINVAL;
@@ -1229,12 +1239,18 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       }
 #define CKV_SF_ARGS desc, p2, c_pad, row_base, q, cents, c16p, cerrp, n_clusters, sizes, starts, sorted_ids, \
     token_ids, rows, runs, n_tokens, n_taken, trimmed, ranked, cache, warp_bytes, sel_mode, q_copy, \
-    rdy, ep
+    rdy, ep, sa
       static const uint32_t sel_mode = getenv("CKV_SEL_MODE") ? uint32_t(atoi(getenv("CKV_SEL_MODE"))) : 0u;
       // mode 1 (experiment: scoring only) publishes nothing
       const bool pub = sync && sync->ready && sync->epoch && sel_mode != 1;
       uint32_t* rdy = pub ? sync->ready : nullptr;
       const uint32_t* ep = pub ? sync->epoch : nullptr;
+      // the step's append rides along (StepSync sessions only)
+      SelAppend sa{nullptr, nullptr, nullptr, nullptr, 0u, 0u};
+      if (sync && sync->app_k) {
+        sa = SelAppend{sync->app_k, sync->app_v, sync->K, sync->V, sync->app_pos, sync->p_cap};
+        sync->appended = true;
+      }
       // CKV_SEL_L2_PERSIST: the centroids (read by every step, ~60 MB at
       // config B) are accessed through a persisting L2 window, so the KV
       // stream of the attention between two steps does not evict them and the
