@@ -444,6 +444,8 @@ int ckv_ctx_create(int device, void* stream, ckv_ctx** out) {
 int ckv_ctx_destroy(ckv_ctx* ctx) {
   if (!ctx) return CKV_OK;
   cudaSetDevice(ctx->device);
+  if (ctx->aux) ckv_ctx_destroy(ctx->aux);
+  cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);

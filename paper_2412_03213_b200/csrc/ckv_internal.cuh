@@ -19,6 +19,11 @@ struct ckv_ctx {
   static constexpr int kScratchSlots = 48;
   void* scratch[kScratchSlots];  // zeroed in ckv_ctx_create
   size_t scratch_cap[kScratchSlots];
+  // a second context on the same device (own non-blocking stream and
+  // scratch), created on first use: kmeans_run runs half of the units there
+  // from a second host thread, so one half's latency-bound update / fix-up /
+  // index kernels overlap the other half's tensor-core assignment
+  ckv_ctx* aux = nullptr;
 };
 
 namespace ckvb {

@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "ckv_internal.cuh"
@@ -519,6 +521,14 @@ int dalloc(ckv_ctx* ctx, int slot, DevBuf& b, size_t bytes) {
 static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
                             double* objective_host, uint32_t* repair_host);
 
+// the two-stream overlap (kmeans_run) for calls of at least this many units;
+// CKV_KM_OVERLAP=0 turns it off
+constexpr uint32_t kOverlapMinUnits = 16;
+static bool overlap_on() {
+  static const bool v = !(getenv("CKV_KM_OVERLAP") && atoi(getenv("CKV_KM_OVERLAP")) == 0);
+  return v;
+}
+
 // Units are independent, so a call whose scratch (dominated by the fp16 key
 // copy of the tensor-core path, ~n * 256 B per unit) would not fit next to
 // the caller's data runs its units in batches, each a complete k-means run.
@@ -538,8 +548,57 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
   }
   const size_t budget = std::max<size_t>(floor_b, free_b / 10 * 6);
   const uint32_t ub = uint32_t(std::max<size_t>(1, std::min<size_t>(U, budget / per_unit)));
-  if (ub >= U) return kmeans_run_units(ctx, a, info_host, objective_host, repair_host);
   const size_t MI1 = size_t(a.max_iters) + 1;
+  if (ub >= U && U >= kOverlapMinUnits && overlap_on()) {
+    // two halves, each a complete k-means run on its own context / stream
+    // from its own host thread; the GPU interleaves them (units are
+    // independent, so every result is the one-stream result)
+    if (!ctx->aux) {
+      ckv_ctx* x = nullptr;
+      CKV_TRY(ckv_ctx_create(ctx->device, nullptr, &x));
+      if (cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        ckv_ctx_destroy(x);
+        set_error("kmeans: aux stream creation failed");
+        return CKV_ECUDA;
+      }
+      x->own_stream = true;
+      ctx->aux = x;
+    }
+    ckv_ctx* x = ctx->aux;
+    cudaEvent_t ev_in, ev_out;
+    CKV_CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    CKV_CUDA_TRY(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    CKV_CUDA_TRY(cudaEventRecord(ev_in, ctx->stream));  // the caller's inputs are ready
+    CKV_CUDA_TRY(cudaStreamWaitEvent(x->stream, ev_in, 0));
+    const uint32_t u0 = U / 2;
+    KMeansArgs b = a;
+    b.n_units = U - u0;
+    b.keys = a.keys + size_t(u0) * a.key_stride;
+    b.init_rows = a.init_rows + size_t(u0) * a.C;
+    b.centroids = a.centroids + size_t(u0) * a.c_stride * D;
+    b.labels = a.labels + size_t(u0) * a.label_stride;
+    KMeansArgs f = a;
+    f.n_units = u0;
+    int rc2 = CKV_OK;
+    std::string err2;
+    std::thread th([&] {
+      cudaSetDevice(x->device);
+      rc2 = kmeans_run_units(x, b, info_host ? info_host + u0 : nullptr,
+                             objective_host ? objective_host + u0 * MI1 : nullptr,
+                             repair_host ? repair_host + u0 * MI1 : nullptr);
+      if (rc2 != CKV_OK) err2 = ckv_last_error();
+    });
+    const int rc1 = kmeans_run_units(ctx, f, info_host, objective_host, repair_host);
+    th.join();
+    cudaEventRecord(ev_out, x->stream);
+    cudaStreamWaitEvent(ctx->stream, ev_out, 0);  // the caller's stream sees both halves
+    cudaEventDestroy(ev_in);
+    cudaEventDestroy(ev_out);
+    if (rc1 != CKV_OK) return rc1;
+    if (rc2 != CKV_OK) { set_error(err2); return rc2; }
+    return CKV_OK;
+  }
+  if (ub >= U) return kmeans_run_units(ctx, a, info_host, objective_host, repair_host);
   for (uint32_t u0 = 0; u0 < U; u0 += ub) {
     KMeansArgs b = a;
     b.n_units = std::min(ub, U - u0);
@@ -604,10 +663,12 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
   }
   float* knorm = prep.knorm;
 
-  if (!ctx->h_flags || ctx->h_flags_cap < U + 1) {
+  // [0, U) validation flags, [U] the active-unit count the loop tests,
+  // [U + 1 + s] the lagged read-back slots
+  if (!ctx->h_flags || ctx->h_flags_cap < U + 3) {
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
-    CKV_CUDA_TRY(cudaMallocHost(&ctx->h_flags, sizeof(int32_t) * (U + 1)));
-    ctx->h_flags_cap = U + 1;
+    CKV_CUDA_TRY(cudaMallocHost(&ctx->h_flags, sizeof(int32_t) * (U + 3)));
+    ctx->h_flags_cap = U + 3;
   }
   int32_t* hf = ctx->h_flags;
 
@@ -727,6 +788,35 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     return CKV_OK;
   };
 
+  // lagged read-back (CKV_KM_LAG=0 turns it off): the active count of a
+  // read-back pass is copied behind an event and only waited for at the next
+  // read-back pass, so the launch queue never drains on the host round trip;
+  // the passes queued past the last convergence are no-ops, as above
+  static const bool lag = !(getenv("CKV_KM_LAG") && atoi(getenv("CKV_KM_LAG")) == 0);
+  cudaEvent_t ev_rb[2] = {nullptr, nullptr};
+  int pend = -1, rb_next = 0;
+  auto control_lagged = [&](uint32_t t) -> int {
+    CKV_CUDA_TRY(cudaMemsetAsync(b_nact.p, 0, sizeof(int32_t), st));
+    k_control<<<(U + 127) / 128, 128, 0, st>>>(
+        U, t, MI, active, b_changed.as<int32_t>(), b_conv.as<int32_t>(), b_iters.as<uint32_t>(),
+        b_empty.as<int32_t>(), b_rep.as<uint32_t>(), b_replog.as<uint32_t>(), b_obj.as<double>(),
+        b_objlog.as<double>(), b_nact.as<int32_t>());
+    CKV_LAUNCH_CHECK("k_control");
+    ctx->launches++;
+    const int sl = rb_next;
+    rb_next ^= 1;
+    if (!ev_rb[sl]) CKV_CUDA_TRY(cudaEventCreateWithFlags(&ev_rb[sl], cudaEventDisableTiming));
+    CKV_CUDA_TRY(cudaMemcpyAsync(&hf[U + 1 + sl], b_nact.p, sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, st));
+    CKV_CUDA_TRY(cudaEventRecord(ev_rb[sl], st));
+    if (pend >= 0) {  // the previous read-back decides whether to go on
+      CKV_CUDA_TRY(cudaEventSynchronize(ev_rb[pend]));
+      hf[U] = hf[U + 1 + pend];
+      trace_mark("lagged control, active units", long(hf[U]));
+    }
+    pend = sl;
+    return CKV_OK;
+  };
   auto control = [&](uint32_t t, int32_t* n_active_host, bool read_back) -> int {
     CKV_CUDA_TRY(cudaMemsetAsync(b_nact.p, 0, sizeof(int32_t), st));
     k_control<<<(U + 127) / 128, 128, 0, st>>>(
@@ -803,7 +893,10 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     // skips inactive units), and the launch queue stays ahead of the GPU
     // instead of draining on a host round trip per pass
     constexpr uint32_t KM_SYNC = 4;
-    CKV_TRY(control(t, &hf[U], dbg || t % KM_SYNC == 0 || t == MI));
+    if (lag && !dbg && t % KM_SYNC == 0 && t < MI)
+      CKV_TRY(control_lagged(t));
+    else
+      CKV_TRY(control(t, &hf[U], dbg || t % KM_SYNC == 0 || t == MI));
     if (use_tc && perm_at && t == perm_at && !mcr_enabled() && !k16p) {
       // b_sorted holds the index of this pass's labels (count_repair)
       DevBuf b_k16p, b_perm;
@@ -828,6 +921,8 @@ static int kmeans_run_units(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* 
     }
   }
   if (dbg) for (auto& e : dev_) cudaEventDestroy(e);
+  for (auto& e : ev_rb)
+    if (e) cudaEventDestroy(e);
 
   // final labels live in lab[iterations_used & 1]; lab[0] is the output
   k_copy_labels<<<dim3(32, U), 256, 0, st>>>(lab[1], lab[0], n, LS, b_iters.as<uint32_t>(), 1);
