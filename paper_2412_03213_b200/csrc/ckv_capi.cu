@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <atomic>
 #include <mutex>
 #include <random>
 #include <set>
@@ -62,10 +63,15 @@ int attend_scratch(ckv_ctx* ctx, const ckv_attend_desc& d, bool weights, float**
   return CKV_OK;
 }
 
-int num_sms() {
-  int dev = 0, n = 0;
+int num_sms() {  // per device, queried once (called several times per launch)
+  static std::atomic<int> sms[64];
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  int n = sms[dev & 63].load(std::memory_order_relaxed);
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev & 63].store(n, std::memory_order_relaxed);
+  }
   return n;
 }
 
@@ -988,6 +994,28 @@ static std::mutex g_l2_mu;
 static int g_l2_refs[64];
 static size_t g_l2_saved[64];
 
+// the device's persisting-L2 limit as this library last read or set it (the
+// selection's access-policy window sizes its hit ratio from it every launch;
+// SIZE_MAX: not read yet)
+static std::atomic<size_t> g_l2_limit[64];
+static bool g_l2_limit_init = [] {
+  for (auto& x : g_l2_limit) x.store(SIZE_MAX);
+  return true;
+}();
+
+extern "C++" {
+size_t ckvb::l2_persist_limit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  size_t v = g_l2_limit[dev & 63].load(std::memory_order_relaxed);
+  if (v == SIZE_MAX) {
+    if (cudaDeviceGetLimit(&v, cudaLimitPersistingL2CacheSize) != cudaSuccess) return 0;
+    g_l2_limit[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+}  // extern "C++"
+
 static bool l2_persist_acquire(int dev, size_t want) {
   std::lock_guard<std::mutex> lock(g_l2_mu);
   const int i = dev & 63;
@@ -996,6 +1024,9 @@ static bool l2_persist_acquire(int dev, size_t want) {
   if (g_l2_refs[i] == 0) g_l2_saved[i] = cur;
   if (want > cur && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess)
     return false;
+  size_t now = cur;
+  if (cudaDeviceGetLimit(&now, cudaLimitPersistingL2CacheSize) == cudaSuccess)
+    g_l2_limit[i].store(now, std::memory_order_relaxed);
   ++g_l2_refs[i];
   return true;
 }
@@ -1006,6 +1037,7 @@ static void l2_persist_release(int dev) {
   if (g_l2_refs[i] > 0 && --g_l2_refs[i] == 0) {
     cudaCtxResetPersistingL2Cache();
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_saved[i]);
+    g_l2_limit[i].store(SIZE_MAX, std::memory_order_relaxed);  // re-read on next use
   }
 }
 

@@ -181,6 +181,8 @@ int launch_attend(cudaStream_t st, const ckv_attend_desc& desc, const float* q,
                   float* logits_ws, float* part, uint32_t* tickets, float* lse = nullptr,
                   const StepSync* sync = nullptr);
 size_t attend_part_floats(uint32_t n_q, uint32_t max_tokens);
+// the current device's persisting-L2 limit (cached; ckv_capi.cu)
+size_t l2_persist_limit();
 int ctx_scratch(ckv_ctx* ctx, int slot, size_t bytes, bool zero_new, void** out);
 int attend_scratch(ckv_ctx* ctx, const ckv_attend_desc& d, bool weights, float** part,
                    uint32_t** tickets, float** lw);

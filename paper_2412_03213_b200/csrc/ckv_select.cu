@@ -1278,8 +1278,7 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
         int& v = win_dev[dev_w & 63];
         if (v == 0) cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev_w);
         const size_t max_win = size_t(v);
-        size_t persist = 0;
-        cudaDeviceGetLimit(&persist, cudaLimitPersistingL2CacheSize);
+        const size_t persist = l2_persist_limit();
         const size_t bytes = std::min(max_win, size_t(units) * desc.c_cap * D * (hc ? 2 : 4));
         attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
         attr[0].val.accessPolicyWindow.base_ptr =
