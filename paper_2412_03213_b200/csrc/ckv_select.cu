@@ -1133,6 +1133,27 @@ static void dbg_report_fused(uint32_t n, const unsigned long long* dbuf, float m
   fprintf(stderr, "[k_select_fused dbg] %.1f us | per head us: score %.2f pop %.2f rest %.2f | "
           "span %.2f us, last CTA start +%.2f us\n", ms * 1e3, sc / n * 1e-3, pop / n * 1e-3,
           rest / n * 1e-3, double(t_hi - t_lo) * 1e-3, double(s_hi - t_lo) * 1e-3);
+  // select_head phases (stamps 0 start, 4 loads, 6 histogram, 1 candidates,
+  // 2 exact re-score + prefix, 3 outputs): means, and the heads whose
+  // exact phase took > 0.5 us (the f64 re-score ran)
+  double ph[5] = {0, 0, 0, 0, 0};
+  uint32_t nf = 0, slow = 0;
+  for (uint32_t h = 0; h < n; ++h) {
+    const unsigned long long* x = &hb[size_t(h) * 8];
+    if (!x[1] || !x[4] || !x[6]) continue;
+    ++nf;
+    ph[0] += double(x[4] - x[0]);
+    ph[1] += double(x[6] - x[4]);
+    ph[2] += double(x[1] - x[6]);
+    ph[3] += double(x[2] - x[1]);
+    ph[4] += double(x[3] - x[2]);
+    slow += (x[2] - x[1]) > 500ull;
+  }
+  if (nf)
+    fprintf(stderr, "[k_select_fused dbg] fast heads %u/%u: loads %.2f hist %.2f cand %.2f "
+            "exact+prefix %.2f outputs %.2f us; exact re-score ran in %u\n", nf, n,
+            ph[0] / nf * 1e-3, ph[1] / nf * 1e-3, ph[2] / nf * 1e-3, ph[3] / nf * 1e-3,
+            ph[4] / nf * 1e-3, slow);
 }
 
 static void dbg_report(uint32_t n, const unsigned long long* dbuf, float k1_ms, float k2_ms) {
