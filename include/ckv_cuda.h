@@ -104,7 +104,13 @@ typedef struct {
  * ckv_kmeans_init_rows or the caller's init_rows); outputs on device.
  * info_host: host array [n_units]; objective_host: host f64
  * [n_units*(max_iters+1)] or NULL; repair_host: host u32
- * [n_units*(max_iters+1)] or NULL.  Replaces kmeans_cosine. */
+ * [n_units*(max_iters+1)] or NULL.  Replaces kmeans_cosine.
+ * A call of >= 16 units (here and in ckv_cluster_prefill) runs its two
+ * halves concurrently: the second on an internal context of ctx's device
+ * (own stream and scratch, created on first use, freed by ckv_ctx_destroy)
+ * from an internal host thread; the call returns after both, with ctx's
+ * stream ordered after the second half's work.  Results are those of the
+ * one-stream run (units are independent).  CKV_KM_OVERLAP=0 disables it. */
 int ckv_kmeans(ckv_ctx* ctx, const ckv_kmeans_desc* desc, const uint16_t* keys,
                const uint32_t* init_rows, float* centroids, int32_t* labels,
                ckv_kmeans_info* info_host, double* objective_host, uint32_t* repair_host);
