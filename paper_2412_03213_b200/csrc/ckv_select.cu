@@ -150,7 +150,7 @@ __device__ __forceinline__ void dbg_stamp(uint32_t h, int slot) {
   if (g_sel_dbg && lane_id() == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_sel_dbg[size_t(h) * 8 + slot] = t;
+    g_sel_dbg[size_t(h) * 16 + slot] = t;
   }
 #else
   (void)h;
@@ -890,6 +890,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
     qnrm[g] = SEL_ERR * sqrtf(qn2[g]);
     qabs[g] = 1.0001f * sqrtf(qn2[g]);  // >= |q| (the f32 sum's rounding is < 2^-17)
   }
+  if (leader && wid < G) dbg_stamp(unit * G + wid, 8);
   // stage k: rows [RPS k, RPS k + RPS); warp w takes rows 4w..4w+3 of it
   // (f32) or 8w..8w+7 as two groups of 4 (H); 8 lanes per row
   constexpr int NSUB = H ? 2 : 1;
@@ -1040,6 +1041,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
       }
     }
   }
+  if (leader && wid < G) dbg_stamp(unit * G + wid, 9);
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   if constexpr (NC > 1) {
     // every CTA's remote score stores are visible to the leader after this
@@ -1051,6 +1053,7 @@ k_select_fused(ckv_select_desc desc, uint32_t p2, uint32_t c_pad, uint32_t row_b
   }
   if (wid >= G || mode == 1) return;
   const uint32_t h = unit * G + wid;
+  dbg_stamp(h, 10);
   select_head<true>(h, desc, p2, row_base, q_s[wid], cents, av_s + size_t(wid) * c_pad,
                     ae_s + size_t(wid) * c_pad, n_clusters, sz_s, st_s, sorted_ids, token_ids,
                     rows_out, runs, n_tokens, n_taken_out, trimmed_out, ranked_out, nullptr, cache,
@@ -1117,12 +1120,12 @@ size_t select_scratch_bytes(uint32_t n_q, uint32_t c_cap) {
 // the fused kernel's per-head stamps: 7 = CTA start, 0 = scores ready,
 // 1 = order known, 3 = head done
 static void dbg_report_fused(uint32_t n, const unsigned long long* dbuf, float ms) {
-  std::vector<unsigned long long> hb(size_t(n) * 8);
+  std::vector<unsigned long long> hb(size_t(n) * 16);
   cudaMemcpy(hb.data(), dbuf, hb.size() * 8, cudaMemcpyDeviceToHost);
   double sc = 0, pop = 0, rest = 0;
   unsigned long long t_lo = ~0ull, t_hi = 0, s_hi = 0;
   for (uint32_t h = 0; h < n; ++h) {
-    const unsigned long long* x = &hb[size_t(h) * 8];
+    const unsigned long long* x = &hb[size_t(h) * 16];
     sc += double(x[0] - x[7]);
     pop += double(x[1] - x[0]);
     rest += double(x[3] - x[1]);
@@ -1139,7 +1142,7 @@ static void dbg_report_fused(uint32_t n, const unsigned long long* dbuf, float m
   double ph[5] = {0, 0, 0, 0, 0};
   uint32_t nf = 0, slow = 0;
   for (uint32_t h = 0; h < n; ++h) {
-    const unsigned long long* x = &hb[size_t(h) * 8];
+    const unsigned long long* x = &hb[size_t(h) * 16];
     if (!x[1] || !x[4] || !x[6]) continue;
     ++nf;
     ph[0] += double(x[4] - x[0]);
@@ -1149,6 +1152,16 @@ static void dbg_report_fused(uint32_t n, const unsigned long long* dbuf, float m
     ph[4] += double(x[3] - x[2]);
     slow += (x[2] - x[1]) > 500ull;
   }
+  double pre = 0, loop = 0, bar = 0;
+  for (uint32_t h = 0; h < n; ++h) {
+    const unsigned long long* x = &hb[size_t(h) * 16];
+    pre += double(x[8] - x[7]);
+    loop += double(x[9] - x[8]);
+    bar += double(x[10] - x[9]);
+  }
+  fprintf(stderr, "[k_select_fused dbg] scoring phase per head: q / cache prefetch %.2f, "
+          "ring loop %.2f, cp.async wait + CTA barrier %.2f us\n", pre / n * 1e-3,
+          loop / n * 1e-3, bar / n * 1e-3);
   if (nf)
     fprintf(stderr, "[k_select_fused dbg] fast heads %u/%u: loads %.2f hist %.2f cand %.2f "
             "exact+prefix %.2f outputs %.2f us; exact re-score ran in %u\n", nf, n,
@@ -1157,18 +1170,18 @@ static void dbg_report_fused(uint32_t n, const unsigned long long* dbuf, float m
 }
 
 static void dbg_report(uint32_t n, const unsigned long long* dbuf, float k1_ms, float k2_ms) {
-  std::vector<unsigned long long> hb(size_t(n) * 8);
+  std::vector<unsigned long long> hb(size_t(n) * 16);
   cudaMemcpy(hb.data(), dbuf, hb.size() * 8, cudaMemcpyDeviceToHost);
   double ph[3] = {0, 0, 0};
   uint32_t nfast = 0;
   for (uint32_t b = 0; b < n; ++b) {
-    const unsigned long long* x = &hb[size_t(b) * 8];
+    const unsigned long long* x = &hb[size_t(b) * 16];
     if (x[1]) { ph[0] += double(x[1] - x[0]); ph[1] += double(x[2] - x[1]); ++nfast; }
     ph[2] += double(x[3] - x[2]);
   }
   double q[3] = {0, 0, 0};  // loads, pass 1, pass 2 (fast heads)
   for (uint32_t b = 0; b < n; ++b) {
-    const unsigned long long* x = &hb[size_t(b) * 8];
+    const unsigned long long* x = &hb[size_t(b) * 16];
     if (x[1] && x[4] && x[6]) {
       q[0] += double(x[4] - x[0]);
       if (x[5]) { q[1] += double(x[5] - x[4]); q[2] += double(x[6] - x[5]); }
@@ -1316,8 +1329,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
       }
       unsigned long long* fbuf = nullptr;
       if (dbg) {
-        cudaMalloc(&fbuf, size_t(desc.n_q) * 64);
-        cudaMemset(fbuf, 0, size_t(desc.n_q) * 64);
+        cudaMalloc(&fbuf, size_t(desc.n_q) * 128);
+        cudaMemset(fbuf, 0, size_t(desc.n_q) * 128);
         cudaMemcpyToSymbol(g_sel_dbg, &fbuf, sizeof(fbuf));
       }
 #define CKV_SF_CASE(NC_, H_)                                                                     \
@@ -1387,8 +1400,8 @@ int launch_select(cudaStream_t st, const ckv_select_desc& desc, const float* q,
   CKV_CUDA_TRY(smem_optin((const void*)k_select_warp, 200 * 1024));
   unsigned long long* dbuf = nullptr;
   if (dbg) {
-    cudaMalloc(&dbuf, size_t(desc.n_q) * 64);
-    cudaMemset(dbuf, 0, size_t(desc.n_q) * 64);
+    cudaMalloc(&dbuf, size_t(desc.n_q) * 128);
+    cudaMemset(dbuf, 0, size_t(desc.n_q) * 128);
     cudaMemcpyToSymbol(g_sel_dbg, &dbuf, sizeof(dbuf));
   }
   {
