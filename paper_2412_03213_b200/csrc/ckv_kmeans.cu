@@ -565,11 +565,18 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
       ctx->aux = x;
     }
     ckv_ctx* x = ctx->aux;
-    cudaEvent_t ev_in, ev_out;
-    CKV_CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-    CKV_CUDA_TRY(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-    CKV_CUDA_TRY(cudaEventRecord(ev_in, ctx->stream));  // the caller's inputs are ready
-    CKV_CUDA_TRY(cudaStreamWaitEvent(x->stream, ev_in, 0));
+    // the two fork / join events, destroyed on every path out
+    struct Events {
+      cudaEvent_t in = nullptr, out = nullptr;
+      ~Events() {
+        if (in) cudaEventDestroy(in);
+        if (out) cudaEventDestroy(out);
+      }
+    } ev;
+    CKV_CUDA_TRY(cudaEventCreateWithFlags(&ev.in, cudaEventDisableTiming));
+    CKV_CUDA_TRY(cudaEventCreateWithFlags(&ev.out, cudaEventDisableTiming));
+    CKV_CUDA_TRY(cudaEventRecord(ev.in, ctx->stream));  // the caller's inputs are ready
+    CKV_CUDA_TRY(cudaStreamWaitEvent(x->stream, ev.in, 0));
     const uint32_t u0 = U / 2;
     KMeansArgs b = a;
     b.n_units = U - u0;
@@ -581,19 +588,22 @@ int kmeans_run(ckv_ctx* ctx, const KMeansArgs& a, ckv_kmeans_info* info_host,
     f.n_units = u0;
     int rc2 = CKV_OK;
     std::string err2;
-    std::thread th([&] {
+    auto second = [&] {
       cudaSetDevice(x->device);
       rc2 = kmeans_run_units(x, b, info_host ? info_host + u0 : nullptr,
                              objective_host ? objective_host + u0 * MI1 : nullptr,
                              repair_host ? repair_host + u0 * MI1 : nullptr);
       if (rc2 != CKV_OK) err2 = ckv_last_error();
-    });
+    };
+    std::thread th;
+    try {
+      th = std::thread(second);
+    } catch (...) {  // no thread to be had: the halves run one after the other
+    }
     const int rc1 = kmeans_run_units(ctx, f, info_host, objective_host, repair_host);
-    th.join();
-    cudaEventRecord(ev_out, x->stream);
-    cudaStreamWaitEvent(ctx->stream, ev_out, 0);  // the caller's stream sees both halves
-    cudaEventDestroy(ev_in);
-    cudaEventDestroy(ev_out);
+    if (th.joinable()) th.join(); else second();
+    cudaEventRecord(ev.out, x->stream);
+    cudaStreamWaitEvent(ctx->stream, ev.out, 0);  // the caller's stream sees both halves
     if (rc1 != CKV_OK) return rc1;
     if (rc2 != CKV_OK) { set_error(err2); return rc2; }
     return CKV_OK;
